@@ -1,0 +1,9 @@
+"""CPU oracle for balanced butterfly counting (arXiv 2308.07932).
+
+TEST INFRASTRUCTURE ONLY: tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+--impl reference legs are the only callers.  The product path (paper_2308_07932_b200)
+never imports this package, and this package never imports the product path.
+"""
+from .oracle import (  # noqa: F401
+    OracleError, build, brute, route_g, route_s, pairs, topk_pairs, priority_order,
+)
