@@ -1,0 +1,137 @@
+/*
+ * bbf.h — C ABI of libbbf.so: exact balanced / unbalanced butterfly counting in a signed
+ * bipartite graph on NVIDIA B200 (sm_100a).  Hot path of arXiv 2308.07932
+ * (/root/reference/PAPER.md), re-designed for the GPU; see DESIGN.md.
+ *
+ * Definitions the library computes (all exact, integer):
+ *   - signed bipartite graph G = (U, V, E), E ⊆ U x V, one sign per edge (PAPER.md:571,
+ *     §Problem Definition); the ABI sign byte is 1 = positive, 0 = negative (PAPER.md:1031,
+ *     "weight 1 ... positive");
+ *   - butterfly: 4-cycle u_i - v_i - u_j - v_j (Def. Butterfly);
+ *   - balanced butterfly: an even number of negative edges (Def. Balanced
+ *     butterfly); unbalanced otherwise;
+ *   - per same-side pair (z, y): a = #common neighbours c with sigma(z,c) = sigma(y,c)
+ *     ("symmetric wedges"), d = #with opposite signs ("asymmetric wedges",
+ *     PAPER.md:660-664); balanced(z,y) = C(a,2) + C(d,2) (Lemma 2) and
+ *     unbalanced(z,y) = a*d (Theorem proof);
+ *   - global counts: every butterfly once (Alg. 2 BB-Bucket);
+ *   - per-vertex counts: butterflies containing the vertex (vBBFC);
+ *   - top-k pairs: the k same-side pairs with the largest balanced(z,y) > 0 (case study,
+ *     PAPER.md:26-27), ordered by balanced desc, then smaller id asc, then larger id asc
+ *     (reading R11).
+ *
+ * Conventions
+ *   Ownership: input arrays are borrowed for the duration of the call and copied; a
+ *     bbf_graph owns its device memory until bbf_graph_free.  Outputs are caller-allocated,
+ *     host memory unless BBF_PTR_DEVICE is passed (then device pointers on the graph's
+ *     device, written stream-ordered on the graph's stream).
+ *   Synchronisation: calls return after host outputs are written.
+ *   Threading: calls on one handle must be serialised; distinct handles are independent.
+ *   Collectives: with a bbf_comm, every rank calls the same functions in the same order with
+ *     the same graph; each rank counts its shard of the work and the library all-reduces
+ *     (NCCL, u64 sum) so every rank receives the full results.
+ *   Errors: every function returns a bbf_status; on failure outputs are unspecified, the
+ *     message is available from bbf_last_error() (thread-local), and the handle stays valid
+ *     except after BBF_ECUDA.  No C++ exception crosses the ABI.
+ *   Empty graphs are valid and count zero.  There is no CPU fallback: without a usable
+ *     sm_100 device every counting call returns BBF_ECUDA.
+ */
+#ifndef BBF_H_
+#define BBF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BBF_ABI_VERSION 1
+
+typedef struct bbf_graph bbf_graph; /* opaque; one graph resident on one GPU (one rank)   */
+typedef struct bbf_comm bbf_comm;   /* opaque NCCL communicator                          */
+
+typedef enum {
+  BBF_OK = 0,
+  BBF_EINVAL = 1,    /* null pointer, sign byte not in {0,1}, k == 0, bad flags/side      */
+  BBF_ERANGE = 2,    /* col >= n_v, row_ptr[0] != 0 or not monotone, n or nnz >= 2^31    */
+  BBF_EDUP = 3,      /* duplicate (u,v) edge (SPEC.md:56 DuplicateEdge)                   */
+  BBF_ENOMEM = 4,    /* device or host allocation failed                                  */
+  BBF_ECUDA = 5,     /* CUDA error / no sm_100 device                                     */
+  BBF_ENCCL = 6,     /* NCCL error or library built without NCCL                          */
+  BBF_EOVERFLOW = 7  /* a count could exceed 2^64-1 ("report, do not wrap")  */
+} bbf_status;
+
+enum { BBF_SIDE_U = 0, BBF_SIDE_V = 1 };
+
+enum {
+  BBF_PTR_DEVICE = 1u << 0,   /* input (load) / output (count) pointers are device pointers */
+  BBF_FORCE_SPARSE = 1u << 2, /* count: use the sparse wedge-aggregation kernels            */
+  BBF_FORCE_DENSE = 1u << 3   /* count: use the dense int8 tensor-core path (tcgen05)       */
+};
+
+/* Results of one count.  wedges_G is the paper's wedge count for Alg. 2 on this graph
+ * (priority-eligible wedges) — the "wedges" of the wedges/s metric,
+ * independent of which kernels ran.  ms_count is the device time of the count call. */
+typedef struct {
+  uint64_t balanced, unbalanced, total, wedges_G;
+  float ms_count;
+} bbf_counts;
+
+/* One same-side pair (input ids, a < b) and its Lemma-2 counts. */
+typedef struct {
+  uint32_t a, b;
+  uint64_t balanced, unbalanced;
+} bbf_pair;
+
+int bbf_abi_version(void);
+
+/* Thread-local message of the last failure on this thread ("" if none). */
+const char *bbf_last_error(void);
+
+/* NCCL bootstrap: rank 0 creates the 128-byte id, the caller broadcasts it (e.g. over a
+ * torch.distributed process group), every rank calls bbf_comm_init with it. */
+bbf_status bbf_nccl_unique_id(uint8_t id[128]);
+bbf_status bbf_comm_init(const uint8_t id[128], int nranks, int rank, int device, bbf_comm **out);
+bbf_status bbf_comm_free(bbf_comm *comm);
+
+/* Load a signed bipartite graph given as a U-side CSR and build the device representation
+ * (degree priority ranks per Def. Vertex Priority PAPER.md:601-609, both-direction adjacency
+ * sorted by priority per Alg. 2 line 3 PAPER.md:747, sign bit packed into each column word,
+ * and the work plan).
+ *   n_u, n_v  : |U|, |V|; n_u + n_v < 2^31.
+ *   row_ptr   : n_u+1 entries, row_ptr[0] == 0, non-decreasing, row_ptr[n_u] = nnz < 2^31.
+ *   col       : nnz V-side indices (< n_v), any order within a row, no duplicate (u,v).
+ *   sign      : nnz bytes, 1 = positive, 0 = negative.
+ *   flags     : BBF_PTR_DEVICE if the three arrays are device pointers on `device`.
+ *   device    : CUDA device ordinal.  cuda_stream: cudaStream_t to order work on (NULL =
+ *               the library creates its own stream).  comm: NULL for a single GPU.
+ * Errors: BBF_EINVAL, BBF_ERANGE, BBF_EDUP, BBF_ENOMEM, BBF_ECUDA. */
+bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t *row_ptr,
+                              const uint32_t *col, const uint8_t *sign, uint32_t flags,
+                              int device, void *cuda_stream, bbf_comm *comm, bbf_graph **out);
+bbf_status bbf_graph_free(bbf_graph *g);
+
+/* Global balanced / unbalanced counts (each butterfly once; Alg. 2).  out: host. */
+bbf_status bbf_count_global(bbf_graph *g, bbf_counts *out);
+
+/* Per-vertex counts (butterflies containing each vertex; vBBFC semantics),
+ * indexed by input ids.  Any of the four arrays may be NULL.  Host arrays unless
+ * BBF_PTR_DEVICE.  totals (nullable, host) receives the global counts as well. */
+bbf_status bbf_count_per_vertex(bbf_graph *g, uint64_t *bal_u, uint64_t *unb_u, uint64_t *bal_v,
+                                uint64_t *unb_v, uint32_t flags, bbf_counts *totals);
+
+/* Top-k same-side pairs by balanced count on `side` (BBF_SIDE_U / BBF_SIDE_V).  out: host
+ * array of k slots; *n_out receives min(k, #pairs with balanced > 0).  k >= 1. */
+bbf_status bbf_count_pairs_topk(bbf_graph *g, int side, uint32_t k, bbf_pair *out,
+                                uint32_t *n_out, uint32_t flags);
+
+/* Introspection for tests and the bench (no effect on results).  Returns the number of
+ * GPU kernels the library launched on this handle since load, and the algorithmic byte
+ * count of the last count call's wedge-aggregation kernels. */
+bbf_status bbf_graph_stats(bbf_graph *g, uint64_t *kernel_launches, uint64_t *algo_bytes,
+                           float *ms_main_kernel);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BBF_H_ */

@@ -1,0 +1,227 @@
+"""Thin ctypes binding of libbbf.so (include/bbf.h) — argument marshalling only.
+
+Every step of the counting path runs in the library's CUDA kernels; this module converts
+numpy arrays / torch CUDA tensors to pointers and status codes to exceptions.  There is no
+CPU fallback: if libbbf.so is missing or no sm_100 device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbbf.so")
+
+BBF_OK, BBF_EINVAL, BBF_ERANGE, BBF_EDUP, BBF_ENOMEM, BBF_ECUDA, BBF_ENCCL, BBF_EOVERFLOW = range(8)
+STATUS_NAMES = {0: "BBF_OK", 1: "BBF_EINVAL", 2: "BBF_ERANGE", 3: "BBF_EDUP", 4: "BBF_ENOMEM",
+                5: "BBF_ECUDA", 6: "BBF_ENCCL", 7: "BBF_EOVERFLOW"}
+BBF_SIDE_U, BBF_SIDE_V = 0, 1
+BBF_PTR_DEVICE = 1 << 0
+BBF_FORCE_SPARSE = 1 << 2
+BBF_FORCE_DENSE = 1 << 3
+
+
+class BBFError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS_NAMES.get(status, str(status))
+
+
+class bbf_counts(C.Structure):
+    _fields_ = [("balanced", C.c_uint64), ("unbalanced", C.c_uint64), ("total", C.c_uint64),
+                ("wedges_G", C.c_uint64), ("ms_count", C.c_float)]
+
+
+class bbf_pair(C.Structure):
+    _fields_ = [("a", C.c_uint32), ("b", C.c_uint32), ("balanced", C.c_uint64),
+                ("unbalanced", C.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libbbf.so (raises ImportError if it was not built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run python -m paper_2308_07932_b200.build")
+        L = C.CDLL(LIB_PATH)
+        P, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
+        L.bbf_abi_version.restype = i32
+        L.bbf_last_error.restype = C.c_char_p
+        L.bbf_nccl_unique_id.argtypes = [P]
+        L.bbf_comm_init.argtypes = [P, i32, i32, i32, P]
+        L.bbf_comm_free.argtypes = [P]
+        L.bbf_graph_load_csr.argtypes = [u32, u32, P, P, P, u32, i32, P, P, P]
+        L.bbf_graph_free.argtypes = [P]
+        L.bbf_count_global.argtypes = [P, P]
+        L.bbf_count_per_vertex.argtypes = [P, P, P, P, P, u32, P]
+        L.bbf_count_pairs_topk.argtypes = [P, i32, u32, P, P, u32]
+        L.bbf_graph_stats.argtypes = [P, P, P, P]
+        for f in ("bbf_nccl_unique_id", "bbf_comm_init", "bbf_comm_free", "bbf_graph_load_csr",
+                  "bbf_graph_free", "bbf_count_global", "bbf_count_per_vertex",
+                  "bbf_count_pairs_topk", "bbf_graph_stats"):
+            getattr(L, f).restype = i32
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != BBF_OK:
+        raise BBFError(st, lib().bbf_last_error().decode(errors="replace"))
+
+
+def abi_version() -> int:
+    return lib().bbf_abi_version()
+
+
+def last_error() -> str:
+    return lib().bbf_last_error().decode(errors="replace")
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().bbf_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class Comm:
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        self.h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().bbf_comm_init(buf, nranks, rank, device, C.byref(self.h)))
+        self.nranks, self.rank, self.device = nranks, rank, device
+
+    def free(self):
+        if self.h:
+            lib().bbf_comm_free(self.h)
+            self.h = C.c_void_p()
+
+
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if _is_torch(x):
+        return C.c_void_p(x.data_ptr())
+    return x.ctypes.data_as(C.c_void_p)
+
+
+class Graph:
+    """A signed bipartite graph resident on one GPU (bbf_graph_load_csr).
+
+    row_ptr (uint64, n_u+1), col (uint32), sign (uint8, 1 = positive): numpy arrays (host) or
+    torch CUDA tensors (then BBF_PTR_DEVICE is passed)."""
+
+    def __init__(self, n_u, n_v, row_ptr, col, sign, device: int = 0, stream=None,
+                 comm: Comm | None = None, flags: int = 0):
+        dev = _is_torch(row_ptr) and row_ptr.is_cuda
+        if dev:
+            flags |= BBF_PTR_DEVICE
+            keep = (row_ptr, col, sign)
+        else:
+            keep = (np.ascontiguousarray(row_ptr, dtype=np.uint64),
+                    np.ascontiguousarray(col, dtype=np.uint32),
+                    np.ascontiguousarray(sign, dtype=np.uint8))
+        self._keep = keep
+        self.h = C.c_void_p()
+        self.n_u, self.n_v = int(n_u), int(n_v)
+        st = C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else (stream or 0))
+        _check(lib().bbf_graph_load_csr(self.n_u, self.n_v, _ptr(keep[0]), _ptr(keep[1]),
+                                        _ptr(keep[2]), flags, device, st,
+                                        comm.h if comm else None, C.byref(self.h)))
+        self._keep = None
+
+    @classmethod
+    def from_synth(cls, g, **kw):
+        return cls(g.n_u, g.n_v, g.row_ptr, g.col, g.sign, **kw)
+
+    def free(self):
+        if self.h:
+            lib().bbf_graph_free(self.h)
+            self.h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.free()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def count_global(self) -> dict:
+        c = bbf_counts()
+        _check(lib().bbf_count_global(self.h, C.byref(c)))
+        return dict(balanced=c.balanced, unbalanced=c.unbalanced, total=c.total,
+                    wedges_G=c.wedges_G, ms_count=c.ms_count)
+
+    def count_per_vertex(self, out=None, flags: int = 0):
+        """Returns (totals dict, bal_u, unb_u, bal_v, unb_v).  `out` may be a tuple of four
+        torch CUDA uint64/int64 tensors (device outputs, BBF_PTR_DEVICE)."""
+        c = bbf_counts()
+        if out is not None:
+            bu, nu, bv, nv = out
+            flags |= BBF_PTR_DEVICE
+        else:
+            bu, nu = np.zeros(self.n_u, np.uint64), np.zeros(self.n_u, np.uint64)
+            bv, nv = np.zeros(self.n_v, np.uint64), np.zeros(self.n_v, np.uint64)
+        _check(lib().bbf_count_per_vertex(self.h, _ptr(bu), _ptr(nu), _ptr(bv), _ptr(nv), flags,
+                                          C.byref(c)))
+        tot = dict(balanced=c.balanced, unbalanced=c.unbalanced, total=c.total,
+                   wedges_G=c.wedges_G, ms_count=c.ms_count)
+        return tot, bu, nu, bv, nv
+
+    def count_pairs_topk(self, k: int, side: int = BBF_SIDE_U, flags: int = 0):
+        buf = (bbf_pair * max(int(k), 1))()
+        n = C.c_uint32()
+        _check(lib().bbf_count_pairs_topk(self.h, side, int(k), buf, C.byref(n), flags))
+        return [(buf[i].a, buf[i].b, buf[i].balanced, buf[i].unbalanced) for i in range(n.value)]
+
+    def stats(self) -> dict:
+        L, B = C.c_uint64(), C.c_uint64()
+        ms = C.c_float()
+        _check(lib().bbf_graph_stats(self.h, C.byref(L), C.byref(B), C.byref(ms)))
+        return dict(kernel_launches=L.value, algo_bytes=B.value, ms_main_kernel=ms.value)
+
+
+# ABI-named aliases (same names as include/bbf.h)
+bbf_abi_version = abi_version
+bbf_last_error = last_error
+bbf_nccl_unique_id = nccl_unique_id
+bbf_comm_init = Comm
+bbf_graph_load_csr = Graph
+
+
+def bbf_graph_free(g: Graph):
+    g.free()
+
+
+def bbf_comm_free(c: Comm):
+    c.free()
+
+
+def bbf_count_global(g: Graph):
+    return g.count_global()
+
+
+def bbf_count_per_vertex(g: Graph, out=None, flags: int = 0):
+    return g.count_per_vertex(out, flags)
+
+
+def bbf_count_pairs_topk(g: Graph, side: int, k: int, flags: int = 0):
+    return g.count_pairs_topk(k, side, flags)
+
+
+def bbf_graph_stats(g: Graph):
+    return g.stats()

@@ -1,0 +1,333 @@
+// api.cu — the C ABI of libbbf.so (include/bbf.h): handle lifetime, status codes, the count
+// entry points, per-vertex output mapping (S9) and the multi-GPU reduction (S12, NCCL u64 sum).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "bbf_internal.cuh"
+
+namespace bbf {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+bbf_status cuda_status(cudaError_t e, const char* what) {
+  g_last_error = std::string("CUDA error: ") + cudaGetErrorString(e) + " in " + what;
+  if (e == cudaErrorMemoryAllocation) return BBF_ENOMEM;
+  return BBF_ECUDA;
+}
+
+// ---------------------------------------------------------------------------- NCCL (dlopen)
+namespace {
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce;
+  });
+  return api;
+}
+
+bbf_status nccl_status(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return BBF_OK;
+  const char* s = nccl().GetErrorString ? nccl().GetErrorString(r) : "?";
+  set_error(std::string("NCCL error: ") + s + " in " + what);
+  return BBF_ENCCL;
+}
+
+bool device_ok(int device, int* num_sms) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return false;
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, device) != cudaSuccess) return false;
+  if (p.major < 10) return false;
+  if (num_sms) *num_sms = p.multiProcessorCount;
+  return true;
+}
+
+// rank space -> input ids (S9)
+__global__ void k_scatter_pv(const unsigned long long* __restrict__ pv, const uint32_t* __restrict__ inv,
+                             uint32_t row0, uint32_t cnt, uint32_t n, unsigned long long* __restrict__ ob,
+                             unsigned long long* __restrict__ on) {
+  uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= cnt) return;
+  uint32_t id = inv[row0 + r];
+  if (ob) ob[id] = pv[row0 + r];
+  if (on) on[id] = pv[n + row0 + r];
+}
+
+bbf_status allreduce_u64(bbf_graph* g, unsigned long long* dbuf, size_t count) {
+  if (!g->comm || g->comm->nranks <= 1 || !count) return BBF_OK;
+  return nccl_status(nccl().AllReduce(dbuf, dbuf, count, ncclUint64, ncclSum,
+                                      (ncclComm_t)g->comm->nccl, g->stream),
+                     "ncclAllReduce");
+}
+
+bbf_status check_overflow(bbf_graph* g) {
+  if (g->ws_bound >= 18446744073709551615.0L) {
+    set_error("counts could exceed 2^64-1 (bound (maxdeg-1)/2 * W_S)");
+    return BBF_EOVERFLOW;
+  }
+  return BBF_OK;
+}
+
+bbf_status ensure_plan_g(bbf_graph* g) {
+  if (!g->plan_g.valid) BBF_TRY(make_plan(g, 0, &g->plan_g));
+  return BBF_OK;
+}
+
+// dense (tcgen05) vs sparse dispatch
+bool use_dense(bbf_graph* g, uint32_t flags) {
+  if (flags & BBF_FORCE_SPARSE) return false;
+  if (flags & BBF_FORCE_DENSE) return true;
+  return dense_supported(g);
+}
+
+bbf_status do_count(bbf_graph* g, bool per_vertex, uint32_t flags, unsigned long long* BN,
+                    float* ms) {
+  BBF_TRY(check_overflow(g));
+  int rank = g->comm ? g->comm->rank : 0, nranks = g->comm ? g->comm->nranks : 1;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, g->stream);
+  if (per_vertex) BBF_CUDA(cudaMemsetAsync(g->pv, 0, 16ull * g->n, g->stream));
+  bbf_status s;
+  if (use_dense(g, flags)) {
+    if (!dense_supported(g)) {
+      set_error("BBF_FORCE_DENSE: graph not supported by the dense int8 path");
+      return BBF_EINVAL;
+    }
+    s = run_dense(g, per_vertex, rank, nranks, BN);
+  } else {
+    s = ensure_plan_g(g);
+    if (s == BBF_OK) s = run_sparse(g, &g->plan_g, per_vertex, rank, nranks, BN);
+  }
+  if (s != BBF_OK) { cudaEventDestroy(a); cudaEventDestroy(b); return s; }
+  if (g->comm && g->comm->nranks > 1) {
+    BBF_CUDA(cudaMemcpyAsync(g->d_acc + 12, BN, 16, cudaMemcpyHostToDevice, g->stream));
+    BBF_TRY(allreduce_u64(g, g->d_acc + 12, 2));
+    if (per_vertex) BBF_TRY(allreduce_u64(g, (unsigned long long*)g->pv, 2ull * g->n));
+    BBF_CUDA(cudaMemcpyAsync(BN, g->d_acc + 12, 16, cudaMemcpyDeviceToHost, g->stream));
+  }
+  cudaEventRecord(b, g->stream);
+  BBF_CUDA(cudaStreamSynchronize(g->stream));
+  cudaEventElapsedTime(ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return BBF_OK;
+}
+
+}  // namespace
+}  // namespace bbf
+
+using namespace bbf;
+
+extern "C" {
+
+int bbf_abi_version(void) { return BBF_ABI_VERSION; }
+
+const char* bbf_last_error(void) { return g_last_error.c_str(); }
+
+bbf_status bbf_nccl_unique_id(uint8_t id[128]) {
+  if (!id) { set_error("null id"); return BBF_EINVAL; }
+  if (!nccl().ok) { set_error("libnccl.so.2 not loadable"); return BBF_ENCCL; }
+  ncclUniqueId u;
+  BBF_TRY(nccl_status(nccl().GetUniqueId(&u), "ncclGetUniqueId"));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(id, &u, 128);
+  return BBF_OK;
+}
+
+bbf_status bbf_comm_init(const uint8_t id[128], int nranks, int rank, int device, bbf_comm** out) {
+  if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) { set_error("bad comm args"); return BBF_EINVAL; }
+  if (!device_ok(device, nullptr)) { set_error("no sm_100 device"); return BBF_ECUDA; }
+  if (!nccl().ok) { set_error("libnccl.so.2 not loadable"); return BBF_ENCCL; }
+  BBF_CUDA(cudaSetDevice(device));
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  ncclComm_t c;
+  BBF_TRY(nccl_status(nccl().CommInitRank(&c, nranks, u, rank), "ncclCommInitRank"));
+  bbf_comm* cm = new bbf_comm{(void*)c, nranks, rank, device};
+  *out = cm;
+  return BBF_OK;
+}
+
+bbf_status bbf_comm_free(bbf_comm* comm) {
+  if (!comm) return BBF_OK;
+  if (comm->nccl && nccl().ok) nccl().CommDestroy((ncclComm_t)comm->nccl);
+  delete comm;
+  return BBF_OK;
+}
+
+bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_ptr, const uint32_t* col,
+                              const uint8_t* sign, uint32_t flags, int device, void* cuda_stream,
+                              bbf_comm* comm, bbf_graph** out) {
+  if (!out || !row_ptr) { set_error("null pointer"); return BBF_EINVAL; }
+  *out = nullptr;
+  if (flags & ~(uint32_t)(BBF_PTR_DEVICE | BBF_FORCE_SPARSE | BBF_FORCE_DENSE)) {
+    set_error("unknown flags");
+    return BBF_EINVAL;
+  }
+  if ((uint64_t)n_u + n_v >= (1ull << 31)) { set_error("n_u + n_v >= 2^31"); return BBF_ERANGE; }
+  int num_sms = 0;
+  if (!device_ok(device, &num_sms)) { set_error("no usable sm_100 CUDA device"); return BBF_ECUDA; }
+  BBF_CUDA(cudaSetDevice(device));
+  const bool dptr = flags & BBF_PTR_DEVICE;
+  uint64_t nnz = 0;
+  if (dptr) {
+    BBF_CUDA(cudaMemcpy(&nnz, row_ptr + n_u, 8, cudaMemcpyDeviceToHost));
+  } else {
+    nnz = row_ptr[n_u];
+  }
+  if (nnz >= (1ull << 31)) { set_error("nnz >= 2^31"); return BBF_ERANGE; }
+  if (nnz && (!col || !sign)) { set_error("null col/sign"); return BBF_EINVAL; }
+  bbf_graph* g = new bbf_graph();
+  std::memset(g, 0, sizeof(*g));
+  g->device = device;
+  g->num_sms = num_sms;
+  g->comm = comm;
+  g->n_u = n_u; g->n_v = n_v; g->n = n_u + n_v; g->nnz = nnz;
+  if (cuda_stream) {
+    g->stream = (cudaStream_t)cuda_stream;
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete g; return cuda_status(e, "cudaStreamCreate"); }
+    g->own_stream = true;
+  }
+  bbf_status s = BBF_OK;
+  cudaError_t e = cudaMalloc(&g->d_acc, 16 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&g->pv, 16ull * (g->n + 1));
+  if (e != cudaSuccess) s = cuda_status(e, "cudaMalloc");
+  if (s == BBF_OK) s = build_graph(g, row_ptr, col, sign, dptr);
+  if (s == BBF_OK) {
+    e = cudaStreamSynchronize(g->stream);
+    if (e != cudaSuccess) s = cuda_status(e, "graph build");
+  }
+  if (s != BBF_OK) {
+    std::string msg = g_last_error;
+    bbf_graph_free(g);
+    g_last_error = msg;
+    return s;
+  }
+  *out = g;
+  return BBF_OK;
+}
+
+bbf_status bbf_graph_free(bbf_graph* g) {
+  if (!g) return BBF_OK;
+  cudaSetDevice(g->device);
+  cudaStreamSynchronize(g->stream);
+  free_plan(&g->plan_g);
+  free_plan(&g->plan_s[0]);
+  free_plan(&g->plan_s[1]);
+  void* ptrs[] = {g->off, g->adj, g->mid, g->end1, g->inv, g->degs, g->degpre, g->scratch, g->d_acc, g->pv};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (g->own_stream) cudaStreamDestroy(g->stream);
+  delete g;
+  return BBF_OK;
+}
+
+bbf_status bbf_count_global(bbf_graph* g, bbf_counts* out) {
+  if (!g || !out) { set_error("null pointer"); return BBF_EINVAL; }
+  BBF_CUDA(cudaSetDevice(g->device));
+  unsigned long long BN[2] = {0, 0};
+  float ms = 0;
+  BBF_TRY(do_count(g, false, 0, BN, &ms));
+  BBF_TRY(ensure_plan_g(g));
+  out->balanced = BN[0];
+  out->unbalanced = BN[1];
+  out->total = BN[0] + BN[1];
+  out->wedges_G = g->plan_g.W_full;
+  out->ms_count = ms;
+  return BBF_OK;
+}
+
+bbf_status bbf_count_per_vertex(bbf_graph* g, uint64_t* bal_u, uint64_t* unb_u, uint64_t* bal_v,
+                                uint64_t* unb_v, uint32_t flags, bbf_counts* totals) {
+  if (!g) { set_error("null graph"); return BBF_EINVAL; }
+  if (flags & ~(uint32_t)(BBF_PTR_DEVICE | BBF_FORCE_SPARSE | BBF_FORCE_DENSE)) {
+    set_error("unknown flags");
+    return BBF_EINVAL;
+  }
+  BBF_CUDA(cudaSetDevice(g->device));
+  unsigned long long BN[2] = {0, 0};
+  float ms = 0;
+  BBF_TRY(do_count(g, true, flags, BN, &ms));
+  cudaStream_t st = g->stream;
+  const bool dptr = flags & BBF_PTR_DEVICE;
+  // S9: rank space -> input ids, straight into device outputs or via one staging buffer
+  unsigned long long* stage = nullptr;
+  uint64_t* outs[4] = {bal_u, unb_u, bal_v, unb_v};
+  if (!dptr && (bal_u || unb_u || bal_v || unb_v)) BBF_CUDA(cudaMallocAsync(&stage, 16ull * (g->n + 1), st));
+  for (int side = 0; side < 2; ++side) {
+    uint32_t cnt = side ? g->n_v : g->n_u, row0 = side ? g->n_u : 0;
+    uint64_t* ob = outs[2 * side];
+    uint64_t* on = outs[2 * side + 1];
+    if (!cnt || (!ob && !on)) continue;
+    unsigned long long* db = dptr ? (unsigned long long*)ob : (ob ? stage + 2ull * row0 : nullptr);
+    unsigned long long* dn = dptr ? (unsigned long long*)on : (on ? stage + 2ull * row0 + cnt : nullptr);
+    k_scatter_pv<<<(cnt + 255) / 256, 256, 0, st>>>((const unsigned long long*)g->pv, g->inv, row0, cnt,
+                                                   g->n, db, dn);
+    g->launches++;
+    if (!dptr) {
+      if (ob) BBF_CUDA(cudaMemcpyAsync(ob, db, 8ull * cnt, cudaMemcpyDeviceToHost, st));
+      if (on) BBF_CUDA(cudaMemcpyAsync(on, dn, 8ull * cnt, cudaMemcpyDeviceToHost, st));
+    }
+  }
+  if (stage) cudaFreeAsync(stage, st);
+  BBF_CUDA(cudaStreamSynchronize(st));
+  if (totals) {
+    BBF_TRY(ensure_plan_g(g));
+    totals->balanced = BN[0];
+    totals->unbalanced = BN[1];
+    totals->total = BN[0] + BN[1];
+    totals->wedges_G = g->plan_g.W_full;
+    totals->ms_count = ms;
+  }
+  return BBF_OK;
+}
+
+bbf_status bbf_count_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uint32_t* n_out,
+                                uint32_t flags) {
+  if (!g || !out || !n_out) { set_error("null pointer"); return BBF_EINVAL; }
+  if (k == 0) { set_error("k == 0"); return BBF_EINVAL; }
+  if (side != BBF_SIDE_U && side != BBF_SIDE_V) { set_error("bad side"); return BBF_EINVAL; }
+  if (flags & ~(uint32_t)(BBF_FORCE_SPARSE)) { set_error("unsupported flags for topk"); return BBF_EINVAL; }
+  BBF_CUDA(cudaSetDevice(g->device));
+  BBF_TRY(check_overflow(g));
+  return run_pairs_topk(g, side, k, out, n_out);
+}
+
+bbf_status bbf_graph_stats(bbf_graph* g, uint64_t* kernel_launches, uint64_t* algo_bytes,
+                           float* ms_main_kernel) {
+  if (!g) { set_error("null graph"); return BBF_EINVAL; }
+  if (kernel_launches) *kernel_launches = g->launches;
+  if (algo_bytes) *algo_bytes = g->algo_bytes;
+  if (ms_main_kernel) *ms_main_kernel = g->ms_main;
+  return BBF_OK;
+}
+
+}  // extern "C"

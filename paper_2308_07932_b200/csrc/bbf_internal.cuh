@@ -1,0 +1,227 @@
+// bbf_internal.cuh — device representation and shared helpers of libbbf.so (sm_100a).
+//
+// Rank space (DESIGN.md §"Data layout in HBM"):
+//   * every vertex gets a local rank l on its own side: position in descending priority order
+//     (degree desc, then global id desc) — Def. Vertex Priority.  Same-side
+//     priority comparisons are comparisons of l; cross-side comparisons happen once per edge
+//     at build time (mid_start).
+//   * rows: U rows 0..n_u-1 (row = l), V rows n_u..n-1 (row = n_u + l).
+//   * adj[2*nnz]: column word = l(y) | neg << 31, rows sorted ascending by l(y), i.e. by
+//     descending priority (Alg. 2 line 3, "Rearrange Γ(u) ... in ascending order", PAPER.md:747,
+//     with our rank running opposite to p).  Every compare masks bit 31.
+//   * mid_start[x]: first entry whose neighbour has lower priority than x (p(v) < p(u),
+//     PAPER.md:753): the eligible middles are the suffix [mid_start[x], end1[x]).
+//   * end1[x]: first entry whose neighbour has degree <= 1.  Such a vertex lies on no 4-cycle,
+//     so wedges ending (or centred) there contribute to no count (DESIGN.md §"Pruning").
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/bbf.h"
+
+namespace bbf {
+
+constexpr uint32_t kMask = 0x7fffffffu;
+constexpr uint32_t kNegBit = 0x80000000u;
+
+// ---------------------------------------------------------------------------- counter zones
+// Per end side, the end-vertex rank space [0, L4) is cut into zones by degree; a same-side
+// pair (x, w) has a + d <= deg(w) (each wedge x-v-w uses a distinct middle v in N(w)), so the
+// packed (a, d) field of w needs only bits for deg(w):
+//   zone 0: deg > 65535    64-bit field (a word, d word)
+//   zone 1: 256..65535     32-bit field (a:16 | d:16)
+//   zone 2: 16..255        16-bit field (a:8  | d:8 )
+//   zone 3: 4..15           8-bit field (a:4  | d:4 )
+//   zone 4: 2..3            4-bit field (a:2  | d:2 )
+//   deg <= 1: no counter (never on a butterfly).
+struct Zones {
+  uint32_t L[5];   // L[z] = first rank past zone z (cumulative): L[0]=#deg>65535 ... L[4]=#deg>=2
+  uint32_t WB[6];  // word base of each zone; WB[5] = total words
+};
+
+__host__ __device__ inline uint32_t zone_of_l(const Zones& z, uint32_t l) {
+  return (l < z.L[0]) ? 0 : (l < z.L[1]) ? 1 : (l < z.L[2]) ? 2 : (l < z.L[3]) ? 3 : 4;
+}
+
+// global word of field l (base word for zone 0), shift within word, and increment for class
+__device__ __forceinline__ void field_of(const Zones& z, uint32_t l, uint32_t cls, uint32_t& base,
+                                         uint32_t& word, uint32_t& inc) {
+  if (l < z.L[0]) {
+    base = 2u * l;
+    word = base + cls;
+    inc = 1u;
+  } else if (l < z.L[1]) {
+    base = word = z.WB[1] + (l - z.L[0]);
+    inc = 1u << (16u * cls);
+  } else if (l < z.L[2]) {
+    uint32_t i = l - z.L[1];
+    base = word = z.WB[2] + (i >> 1);
+    inc = 1u << (((i & 1u) << 4) + 8u * cls);
+  } else if (l < z.L[3]) {
+    uint32_t i = l - z.L[2];
+    base = word = z.WB[3] + (i >> 2);
+    inc = 1u << (((i & 3u) << 3) + 4u * cls);
+  } else {
+    uint32_t i = l - z.L[3];
+    base = word = z.WB[4] + (i >> 3);
+    inc = 1u << (((i & 7u) << 2) + 2u * cls);
+  }
+}
+
+// read (a, d) of field l from a window whose first global word is word0
+__device__ __forceinline__ void field_read(const Zones& z, const uint32_t* ctr, uint32_t word0,
+                                           uint32_t l, uint32_t& a, uint32_t& d) {
+  if (l < z.L[0]) {
+    uint32_t w = 2u * l - word0;
+    a = ctr[w];
+    d = ctr[w + 1];
+  } else if (l < z.L[1]) {
+    uint32_t v = ctr[z.WB[1] + (l - z.L[0]) - word0];
+    a = v & 0xffffu;
+    d = v >> 16;
+  } else if (l < z.L[2]) {
+    uint32_t i = l - z.L[1];
+    uint32_t v = (ctr[z.WB[2] + (i >> 1) - word0] >> ((i & 1u) << 4)) & 0xffffu;
+    a = v & 0xffu;
+    d = v >> 8;
+  } else if (l < z.L[3]) {
+    uint32_t i = l - z.L[2];
+    uint32_t v = (ctr[z.WB[3] + (i >> 2) - word0] >> ((i & 3u) << 3)) & 0xffu;
+    a = v & 0xfu;
+    d = v >> 4;
+  } else {
+    uint32_t i = l - z.L[3];
+    uint32_t v = (ctr[z.WB[4] + (i >> 3) - word0] >> ((i & 7u) << 2)) & 0xfu;
+    a = v & 3u;
+    d = v >> 2;
+  }
+}
+
+// first l whose field's last word is >= g (so every l below it fits in words < g)
+__host__ __device__ inline uint32_t l_first_last_word_ge(const Zones& z, uint64_t g) {
+  if (g >= z.WB[5]) return z.L[4];
+  if (g < z.WB[1]) {  // zone 0: last word 2l+1 >= g
+    uint64_t l = (g == 0) ? 0 : (g) / 2;  // smallest l with 2l+1 >= g
+    return (uint32_t)l;
+  }
+  if (g < z.WB[2]) return z.L[0] + (uint32_t)(g - z.WB[1]);
+  if (g < z.WB[3]) return z.L[1] + (uint32_t)(2ull * (g - z.WB[2]));
+  if (g < z.WB[4]) return z.L[2] + (uint32_t)(4ull * (g - z.WB[3]));
+  return z.L[3] + (uint32_t)(8ull * (g - z.WB[4]));
+}
+
+__host__ __device__ inline uint32_t word_of_l(const Zones& z, uint32_t l) {
+  if (l < z.L[0]) return 2u * l;
+  if (l < z.L[1]) return z.WB[1] + (l - z.L[0]);
+  if (l < z.L[2]) return z.WB[2] + ((l - z.L[1]) >> 1);
+  if (l < z.L[3]) return z.WB[3] + ((l - z.L[2]) >> 2);
+  return z.WB[4] + ((l - z.L[3]) >> 3);
+}
+
+__host__ __device__ inline unsigned long long comb2(unsigned long long x) {
+  return x ? x * (x - 1ull) / 2ull : 0ull;
+}
+
+// ---------------------------------------------------------------------------- plan
+// A "route" is one wedge enumeration the engine runs:
+//   route G: Alg. 2, starts = all rows, middles = [mid_start, end1),
+//            ends = N(v) ∩ {l(w) > l(x)} ∩ {deg(w) >= 2}.
+//   route S(side): same-side pairs with full common neighbourhoods (vBBFC semantics,
+//            PAPER.md:875 "we drop the rank comparison"), starts = rows of `side`, middles =
+//            [off, end1), ends = l(w) > l(x) (each unordered pair once).
+struct Unit {  // one T3 work unit: start row x, end-rank range [lo, hi)
+  uint32_t x, lo, hi, pad;
+};
+
+struct Plan {
+  int route;           // 0 = G, 1 = S(U), 2 = S(V)
+  uint32_t* ub;        // per middle entry: first eligible end (absolute adj index)
+  uint64_t* work;      // per row: pruned wedge count
+  uint32_t* t1;        // rows with 0 < work <= kT1Max
+  Unit* units;         // T3 units
+  uint32_t n_t1, n_units;
+  uint32_t max_mid;    // max middles of a T3 start
+  unsigned long long W_full;    // un-pruned wedge count (route G: W_G of the paper)
+  unsigned long long W_pruned;  // wedges the kernels actually visit
+  unsigned long long W_t1, W_t3;
+  bool valid;
+};
+
+}  // namespace bbf
+
+// ---------------------------------------------------------------------------- graph handle
+struct bbf_comm {
+  void* nccl;  // ncclComm_t
+  int nranks, rank, device;
+};
+
+struct bbf_graph {
+  int device;
+  cudaStream_t stream;
+  bool own_stream;
+  bbf_comm* comm;
+  uint32_t n_u, n_v, n;
+  uint64_t nnz;
+  // rank-space CSR
+  uint32_t* off;      // n+1
+  uint32_t* adj;      // 2*nnz
+  uint32_t* mid;      // n   (mid_start)
+  uint32_t* end1;     // n
+  uint32_t* inv;      // n   : row -> input id on its side
+  uint32_t* degs;     // n   : degree by row (rank order, per side non-increasing)
+  uint64_t* degpre;   // n+2 : per side inclusive prefix of degrees over rows (side-local, see plan)
+  bbf::Zones zones[2];
+  uint32_t L4[2];     // #vertices with degree >= 2 per side
+  uint32_t maxdeg[2];
+  long double ws_bound;  // overflow bound on B + N
+  bbf::Plan plan_g;
+  bbf::Plan plan_s[2];
+  // scratch for the engine
+  uint32_t* scratch;  // per-CTA middle arrays
+  size_t scratch_words;
+  unsigned long long* d_acc;  // [0]=B [1]=N [2..] misc counters, [8]=unit cursor, [9]=t1 cursor
+  uint64_t* pv;              // 2*n per-vertex (B, N interleaved by array: pv[0..n), pv[n..2n))
+  // stats
+  uint64_t launches;
+  uint64_t algo_bytes;
+  float ms_main;
+  int num_sms;
+};
+
+// error helpers (api.cu)
+namespace bbf {
+void set_error(const std::string& msg);
+bbf_status cuda_status(cudaError_t e, const char* what);
+}  // namespace bbf
+
+#define BBF_CUDA(call)                                             \
+  do {                                                             \
+    cudaError_t e_ = (call);                                       \
+    if (e_ != cudaSuccess) return bbf::cuda_status(e_, #call);     \
+  } while (0)
+
+#define BBF_TRY(call)                          \
+  do {                                         \
+    bbf_status s_ = (call);                    \
+    if (s_ != BBF_OK) return s_;               \
+  } while (0)
+
+// internal entry points across translation units
+namespace bbf {
+bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* col,
+                       const uint8_t* sign, bool device_ptrs);
+bbf_status make_plan(bbf_graph* g, int route, Plan* p);
+void free_plan(Plan* p);
+// run the sparse engine for a route; per_vertex -> accumulate into g->pv (rank space)
+bbf_status run_sparse(bbf_graph* g, Plan* p, bool per_vertex, int rank, int nranks,
+                      unsigned long long* host_BN);
+bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, int rank, int nranks,
+                           unsigned long long* host_BN, unsigned long long* cb, unsigned long long* cn,
+                           unsigned long long* cid, unsigned long long cap, unsigned long long* n_cand);
+bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uint32_t* n_out);
+bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks,
+                     unsigned long long* host_BN);
+bool dense_supported(bbf_graph* g);
+}  // namespace bbf

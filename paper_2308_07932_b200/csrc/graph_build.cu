@@ -1,0 +1,365 @@
+// graph_build.cu — S1-S4 of the hot path: validate the input CSR, degrees,
+// vertex priority ranks (Def. Vertex Priority), both-direction adjacency in
+// rank space sorted by priority (Alg. 2 line 3) with the sign packed into bit 31,
+// duplicate detection, and the per-row cut points mid_start / end1.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "bbf_internal.cuh"
+
+namespace bbf {
+namespace {
+
+enum : uint32_t { kErrRowPtr = 1, kErrCol = 2, kErrSign = 4, kErrDup = 8 };
+
+__global__ void k_validate_rows(const uint64_t* __restrict__ rp, uint32_t n_u, uint32_t* err) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i == 0 && rp[0] != 0) atomicOr(err, kErrRowPtr);
+  if (i < n_u && rp[i + 1] < rp[i]) atomicOr(err, kErrRowPtr);
+}
+
+__global__ void k_validate_edges(const uint32_t* __restrict__ col, const uint8_t* __restrict__ sg,
+                                 uint64_t nnz, uint32_t n_v, uint32_t* err) {
+  uint32_t bad = 0;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    if (col[e] >= n_v) bad |= kErrCol;
+    if (sg[e] > 1) bad |= kErrSign;
+  }
+  if (bad) atomicOr(err, bad);
+}
+
+// degree keys: key = deg << 32 | gid  (gid: U -> u, V -> n_u + v)
+__global__ void k_keys_u(const uint64_t* __restrict__ rp, uint32_t n_u, uint64_t* __restrict__ key) {
+  uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < n_u) key[u] = ((rp[u + 1] - rp[u]) << 32) | u;
+}
+
+__global__ void k_hist_v(const uint32_t* __restrict__ col, uint64_t nnz, uint32_t* __restrict__ dv) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&dv[col[e]], 1u);
+}
+
+__global__ void k_keys_v(const uint32_t* __restrict__ dv, uint32_t n_u, uint32_t n_v,
+                         uint64_t* __restrict__ key) {
+  uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < n_v) key[v] = ((uint64_t)dv[v] << 32) | (uint64_t)(n_u + v);
+}
+
+// sorted (descending) keys -> row tables: inv (row -> input id), degs, lr (input id -> local rank)
+__global__ void k_rank_tables(const uint64_t* __restrict__ skey, uint32_t cnt, uint32_t id_base,
+                              uint32_t row_base, uint32_t* __restrict__ inv,
+                              uint32_t* __restrict__ degs, uint32_t* __restrict__ lr) {
+  uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= cnt) return;
+  uint64_t k = skey[l];
+  uint32_t id = (uint32_t)(k & 0xffffffffu) - id_base;
+  inv[row_base + l] = id;
+  degs[row_base + l] = (uint32_t)(k >> 32);
+  lr[id] = l;
+}
+
+__device__ __forceinline__ uint32_t row_of_edge(const uint64_t* __restrict__ rp, uint32_t n_u,
+                                                uint64_t e) {
+  // largest u with rp[u] <= e  (rows may be empty)
+  uint32_t lo = 0, hi = n_u;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    uint32_t mid = lo + (hi - lo) / 2;
+    if (rp[mid] <= e) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// directed entries in rank space: U row lr_u[u] gets (lr_v[v], neg); V row n_u + lr_v[v] gets
+// (lr_u[u], neg).  Key = row << 32 | l << 1 | neg, so one radix sort orders rows and columns.
+__global__ void k_entries(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                          const uint8_t* __restrict__ sg, uint64_t nnz, uint32_t n_u,
+                          const uint32_t* __restrict__ lr_u, const uint32_t* __restrict__ lr_v,
+                          uint64_t* __restrict__ keys) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t u = row_of_edge(rp, n_u, e);
+    uint32_t v = col[e];
+    uint64_t neg = sg[e] ? 0u : 1u;  // weight 0 = negative
+    uint64_t a = lr_u[u], b = lr_v[v];
+    keys[e] = (a << 32) | (b << 1) | neg;
+    keys[nnz + e] = ((uint64_t)(n_u + b) << 32) | (a << 1) | neg;
+  }
+}
+
+__global__ void k_decode(const uint64_t* __restrict__ keys, uint64_t m, uint32_t* __restrict__ adj,
+                         uint32_t* err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[i];
+    uint32_t lo = (uint32_t)k;
+    adj[i] = (lo >> 1) | ((lo & 1u) << 31);
+    if (i > 0 && (keys[i - 1] >> 1) == (k >> 1)) atomicOr(err, kErrDup);  // same row, same col
+  }
+}
+
+// number of entries of the descending array a[0..cnt) that are > key
+__device__ __forceinline__ uint32_t count_greater(const uint64_t* __restrict__ a, uint32_t cnt,
+                                                  uint64_t key) {
+  uint32_t lo = 0, hi = cnt;
+  while (lo < hi) {
+    uint32_t mid = lo + (hi - lo) / 2;
+    if (a[mid] > key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// first index in adj[b, e) whose masked column >= t
+__device__ __forceinline__ uint32_t lower_bound_col(const uint32_t* __restrict__ adj, uint32_t b,
+                                                    uint32_t e, uint32_t t) {
+  while (b < e) {
+    uint32_t mid = b + (e - b) / 2;
+    if ((adj[mid] & kMask) < t) b = mid + 1; else e = mid;
+  }
+  return b;
+}
+
+// mid_start[x]: first neighbour with lower priority than x; end1[x]: first neighbour of degree<=1
+__global__ void k_cuts(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                       const uint64_t* __restrict__ skey_u, const uint64_t* __restrict__ skey_v,
+                       uint32_t n_u, uint32_t n_v, uint32_t L4u, uint32_t L4v,
+                       uint32_t* __restrict__ mid, uint32_t* __restrict__ end1) {
+  uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n_u + n_v) return;
+  bool is_u = x < n_u;
+  uint64_t kx = is_u ? skey_u[x] : skey_v[x - n_u];
+  uint32_t higher = is_u ? count_greater(skey_v, n_v, kx) : count_greater(skey_u, n_u, kx);
+  uint32_t b = off[x], e = off[x + 1];
+  mid[x] = lower_bound_col(adj, b, e, higher);
+  end1[x] = lower_bound_col(adj, b, e, is_u ? L4v : L4u);
+}
+
+// number of entries of the non-increasing degs[base, base+cnt) that are >= t
+__global__ void k_count_ge(const uint32_t* __restrict__ degs, uint32_t base, uint32_t cnt,
+                           unsigned long long* out) {
+  const uint32_t th[5] = {65536u, 256u, 16u, 4u, 2u};
+  int t = threadIdx.x;
+  if (t >= 5) return;
+  uint32_t lo = 0, hi = cnt;
+  while (lo < hi) {
+    uint32_t mid = lo + (hi - lo) / 2;
+    if (degs[base + mid] >= th[t]) lo = mid + 1; else hi = mid;
+  }
+  out[t] = lo;
+}
+
+// sum over vertices of C(deg, 2) per side (overflow pre-check)
+__global__ void k_ws(const uint32_t* __restrict__ degs, uint32_t n_u, uint32_t n,
+                     unsigned long long* out) {
+  unsigned long long su = 0, sv = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    unsigned long long d = degs[i];
+    if (i < n_u) su += comb2(d); else sv += comb2(d);
+  }
+  for (int o = 16; o; o >>= 1) {
+    su += __shfl_xor_sync(0xffffffffu, su, o);
+    sv += __shfl_xor_sync(0xffffffffu, sv, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&out[0], su);
+    atomicAdd(&out[1], sv);
+  }
+}
+
+__global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint32_t n, uint64_t* __restrict__ b) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = a[i];
+}
+
+inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {
+  uint64_t g = (n + block - 1) / block;
+  if (g == 0) g = 1;
+  return (unsigned)std::min<uint64_t>(g, cap);
+}
+
+inline int bits_for(uint64_t x) {
+  int b = 0;
+  while ((1ull << b) <= x) ++b;
+  return b;
+}
+
+}  // namespace
+
+bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* col,
+                       const uint8_t* sign, bool device_ptrs) {
+  cudaStream_t st = g->stream;
+  const uint32_t n_u = g->n_u, n_v = g->n_v, n = g->n;
+  const uint64_t nnz = g->nnz;
+  const uint64_t m = 2 * nnz;
+  // device copies of the input (S1)
+  const uint64_t* d_rp = row_ptr;
+  const uint32_t* d_col = col;
+  const uint8_t* d_sg = sign;
+  uint64_t* own_rp = nullptr;
+  uint32_t* own_col = nullptr;
+  uint8_t* own_sg = nullptr;
+  if (!device_ptrs) {
+    BBF_CUDA(cudaMallocAsync(&own_rp, sizeof(uint64_t) * (n_u + 1), st));
+    BBF_CUDA(cudaMemcpyAsync(own_rp, row_ptr, sizeof(uint64_t) * (n_u + 1), cudaMemcpyHostToDevice, st));
+    if (nnz) {
+      BBF_CUDA(cudaMallocAsync(&own_col, sizeof(uint32_t) * nnz, st));
+      BBF_CUDA(cudaMallocAsync(&own_sg, nnz, st));
+      BBF_CUDA(cudaMemcpyAsync(own_col, col, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice, st));
+      BBF_CUDA(cudaMemcpyAsync(own_sg, sign, nnz, cudaMemcpyHostToDevice, st));
+    }
+    d_rp = own_rp; d_col = own_col; d_sg = own_sg;
+  }
+  uint32_t* d_err;
+  BBF_CUDA(cudaMallocAsync(&d_err, 4 * sizeof(uint32_t), st));
+  BBF_CUDA(cudaMemsetAsync(d_err, 0, 4 * sizeof(uint32_t), st));
+  k_validate_rows<<<grid_for(n_u + 1, 256, 1u << 30), 256, 0, st>>>(d_rp, n_u, d_err);
+  if (nnz) k_validate_edges<<<grid_for(nnz, 256), 256, 0, st>>>(d_col, d_sg, nnz, n_v, d_err);
+  g->launches += 2;
+  uint32_t h_err = 0;
+  BBF_CUDA(cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaStreamSynchronize(st));
+  auto cleanup_input = [&]() {
+    if (own_rp) cudaFreeAsync(own_rp, st);
+    if (own_col) cudaFreeAsync(own_col, st);
+    if (own_sg) cudaFreeAsync(own_sg, st);
+  };
+  if (h_err) {
+    cudaFreeAsync(d_err, st);
+    cleanup_input();
+    cudaStreamSynchronize(st);
+    if (h_err & kErrRowPtr) { set_error("row_ptr[0] != 0 or row_ptr not non-decreasing"); return BBF_ERANGE; }
+    if (h_err & kErrCol) { set_error("col index >= n_v"); return BBF_ERANGE; }
+    set_error("sign byte not in {0,1}");
+    return BBF_EINVAL;
+  }
+
+  // S2-S3: degrees and per-side priority ranks
+  uint64_t *key_u, *key_v, *skey_u, *skey_v;
+  uint32_t *dv, *lr_u, *lr_v;
+  BBF_CUDA(cudaMallocAsync(&key_u, 8ull * (n_u + 1), st));
+  BBF_CUDA(cudaMallocAsync(&key_v, 8ull * (n_v + 1), st));
+  BBF_CUDA(cudaMallocAsync(&skey_u, 8ull * (n_u + 1), st));
+  BBF_CUDA(cudaMallocAsync(&skey_v, 8ull * (n_v + 1), st));
+  BBF_CUDA(cudaMallocAsync(&dv, 4ull * (n_v + 1), st));
+  BBF_CUDA(cudaMallocAsync(&lr_u, 4ull * (n_u + 1), st));
+  BBF_CUDA(cudaMallocAsync(&lr_v, 4ull * (n_v + 1), st));
+  BBF_CUDA(cudaMemsetAsync(dv, 0, 4ull * (n_v + 1), st));
+  if (n_u) k_keys_u<<<grid_for(n_u, 256, 1u << 30), 256, 0, st>>>(d_rp, n_u, key_u);
+  if (nnz) k_hist_v<<<grid_for(nnz, 256), 256, 0, st>>>(d_col, nnz, dv);
+  if (n_v) k_keys_v<<<grid_for(n_v, 256, 1u << 30), 256, 0, st>>>(dv, n_u, n_v, key_v);
+  g->launches += 3;
+
+  size_t tmp_bytes = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+  int kbits = std::min(64, 32 + bits_for(std::max<uint64_t>(nnz, 1)));  // deg < 2^31
+  cub::DeviceRadixSort::SortKeysDescending(nullptr, t1, key_u, skey_u, (int)n_u, 0, kbits, st);
+  cub::DeviceRadixSort::SortKeysDescending(nullptr, t2, key_v, skey_v, (int)n_v, 0, kbits, st);
+  int ebits = 32 + bits_for(std::max<uint32_t>(n, 1));
+  cub::DeviceRadixSort::SortKeys(nullptr, t3, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)m, 0,
+                                 ebits, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, t4, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)(n + 1), st);
+  tmp_bytes = std::max(std::max(t1, t2), std::max(t3, t4));
+  size_t t5 = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, t5, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n, st);
+  tmp_bytes = std::max(tmp_bytes, t5);
+  void* tmp;
+  BBF_CUDA(cudaMallocAsync(&tmp, tmp_bytes + 16, st));
+  if (n_u) BBF_CUDA(cub::DeviceRadixSort::SortKeysDescending(tmp, t1, key_u, skey_u, (int)n_u, 0, kbits, st));
+  if (n_v) BBF_CUDA(cub::DeviceRadixSort::SortKeysDescending(tmp, t2, key_v, skey_v, (int)n_v, 0, kbits, st));
+  g->launches += 8;
+
+  BBF_CUDA(cudaMallocAsync(&g->inv, 4ull * (n + 1), st));
+  BBF_CUDA(cudaMallocAsync(&g->degs, 4ull * (n + 1), st));
+  BBF_CUDA(cudaMallocAsync(&g->off, 4ull * (n + 1), st));
+  BBF_CUDA(cudaMallocAsync(&g->mid, 4ull * (n + 1), st));
+  BBF_CUDA(cudaMallocAsync(&g->end1, 4ull * (n + 1), st));
+  BBF_CUDA(cudaMallocAsync(&g->adj, 4ull * (m + 1), st));
+  BBF_CUDA(cudaMallocAsync(&g->degpre, 8ull * (n + 1), st));
+  if (n_u) k_rank_tables<<<grid_for(n_u, 256, 1u << 30), 256, 0, st>>>(skey_u, n_u, 0, 0, g->inv, g->degs, lr_u);
+  if (n_v) k_rank_tables<<<grid_for(n_v, 256, 1u << 30), 256, 0, st>>>(skey_v, n_v, n_u, n_u, g->inv, g->degs, lr_v);
+  g->launches += 2;
+
+  // S4: rank-space adjacency, one radix sort of the 2*nnz directed entries
+  if (m) {
+    uint64_t *ek, *eks;
+    BBF_CUDA(cudaMallocAsync(&ek, 8ull * m, st));
+    BBF_CUDA(cudaMallocAsync(&eks, 8ull * m, st));
+    k_entries<<<grid_for(nnz, 256), 256, 0, st>>>(d_rp, d_col, d_sg, nnz, n_u, lr_u, lr_v, ek);
+    BBF_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t3, ek, eks, (int64_t)m, 0, ebits, st));
+    k_decode<<<grid_for(m, 256), 256, 0, st>>>(eks, m, g->adj, d_err);
+    g->launches += 6;
+    cudaFreeAsync(ek, st);
+    cudaFreeAsync(eks, st);
+  }
+  // row offsets: exclusive scan of degrees in row order (rows U by rank, then V by rank)
+  BBF_CUDA(cudaMemsetAsync(g->degs + n, 0, 4, st));
+  BBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t4, g->degs, g->off, (int)(n + 1), st));
+  g->launches += 1;
+
+  // zone boundaries per side (rank counts of degree thresholds)
+  unsigned long long* d_cnt;
+  BBF_CUDA(cudaMallocAsync(&d_cnt, 16 * sizeof(unsigned long long), st));
+  BBF_CUDA(cudaMemsetAsync(d_cnt, 0, 16 * sizeof(unsigned long long), st));
+  k_count_ge<<<1, 32, 0, st>>>(g->degs, 0, n_u, d_cnt);
+  k_count_ge<<<1, 32, 0, st>>>(g->degs, n_u, n_v, d_cnt + 5);
+  k_ws<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(g->degs, n_u, n, d_cnt + 10);
+  g->launches += 3;
+  unsigned long long h_cnt[16];
+  BBF_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, st));
+  uint32_t h_maxdeg[2] = {0, 0};
+  if (n_u) BBF_CUDA(cudaMemcpyAsync(&h_maxdeg[0], g->degs, 4, cudaMemcpyDeviceToHost, st));
+  if (n_v) BBF_CUDA(cudaMemcpyAsync(&h_maxdeg[1], g->degs + n_u, 4, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaStreamSynchronize(st));
+  g->maxdeg[0] = h_maxdeg[0];
+  g->maxdeg[1] = h_maxdeg[1];
+  for (int s = 0; s < 2; ++s) {
+    Zones& z = g->zones[s];
+    for (int i = 0; i < 5; ++i) z.L[i] = (uint32_t)h_cnt[5 * s + i];
+    z.WB[0] = 0;
+    z.WB[1] = 2u * z.L[0];
+    z.WB[2] = z.WB[1] + (z.L[1] - z.L[0]);
+    z.WB[3] = z.WB[2] + (z.L[2] - z.L[1] + 1) / 2;
+    z.WB[4] = z.WB[3] + (z.L[3] - z.L[2] + 3) / 4;
+    z.WB[5] = z.WB[4] + (z.L[4] - z.L[3] + 7) / 8;
+    g->L4[s] = z.L[4];
+  }
+  // B + N = sum_{u<w} C(T_uw, 2) <= (maxT - 1)/2 * sum_{u<w} T_uw = (maxdeg_U - 1)/2 * W_S(U)
+  {
+    long double bu = (long double)(g->maxdeg[0] ? g->maxdeg[0] - 1 : 0) / 2.0L * (long double)h_cnt[11];
+    long double bv = (long double)(g->maxdeg[1] ? g->maxdeg[1] - 1 : 0) / 2.0L * (long double)h_cnt[10];
+    g->ws_bound = std::min(bu, bv);
+  }
+  if (h_err & kErrDup) {
+    cudaFreeAsync(tmp, st);
+    cleanup_input();
+    cudaFreeAsync(key_u, st); cudaFreeAsync(key_v, st); cudaFreeAsync(skey_u, st);
+    cudaFreeAsync(skey_v, st); cudaFreeAsync(dv, st); cudaFreeAsync(lr_u, st); cudaFreeAsync(lr_v, st);
+    cudaFreeAsync(d_cnt, st); cudaFreeAsync(d_err, st);
+    cudaStreamSynchronize(st);
+    set_error("duplicate (u,v) edge");
+    return BBF_EDUP;
+  }
+  if (n) {
+    k_cuts<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(g->off, g->adj, skey_u, skey_v, n_u, n_v,
+                                                      g->L4[0], g->L4[1], g->mid, g->end1);
+    // inclusive prefix of degrees over rows (u64), used to split hub end-ranges by expected work
+    uint64_t* d64;
+    BBF_CUDA(cudaMallocAsync(&d64, 8ull * n, st));
+    k_u32_to_u64<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(g->degs, n, d64);
+    BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp, t5, d64, g->degpre, (int)n, st));
+    g->launches += 3;
+    cudaFreeAsync(d64, st);
+  }
+  cudaFreeAsync(tmp, st);
+  cleanup_input();
+  cudaFreeAsync(key_u, st); cudaFreeAsync(key_v, st); cudaFreeAsync(skey_u, st);
+  cudaFreeAsync(skey_v, st); cudaFreeAsync(dv, st); cudaFreeAsync(lr_u, st); cudaFreeAsync(lr_v, st);
+  cudaFreeAsync(d_cnt, st); cudaFreeAsync(d_err, st);
+  BBF_CUDA(cudaGetLastError());
+  return BBF_OK;
+}
+
+}  // namespace bbf

@@ -1,0 +1,297 @@
+// plan.cu — S5 of the hot path: per eligible middle entry (x -> v) the first eligible end
+// ub = upper_bound(N(v), l(x)) (Alg. 2 line 10 "w in Γ(v) | p(w) < p(u)", as a
+// suffix of the priority-sorted list), the per-start work, the wedge count W of the route,
+// tiering of starts by work, and the split of hub starts into end-range units.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "bbf_internal.cuh"
+
+namespace bbf {
+
+constexpr uint32_t kT1Max = 512;  // starts with at most this many (pruned) wedges -> warp hash
+
+namespace {
+
+struct RouteRows {
+  int route;  // 0 G, 1 S(U), 2 S(V)
+  uint32_t n_u, n;
+  __device__ __forceinline__ bool in_route(uint32_t x) const {
+    return route == 0 || (route == 1 ? x < n_u : x >= n_u);
+  }
+};
+
+__device__ __forceinline__ uint32_t upper_bound_col(const uint32_t* __restrict__ adj, uint32_t b,
+                                                    uint32_t e, uint32_t t) {
+  while (b < e) {
+    uint32_t mid = b + (e - b) / 2;
+    if ((adj[mid] & kMask) <= t) b = mid + 1; else e = mid;
+  }
+  return b;
+}
+
+__device__ __forceinline__ uint32_t row_of_entry(const uint32_t* __restrict__ off, uint32_t n,
+                                                 uint32_t e) {
+  uint32_t lo = 0, hi = n;  // largest x with off[x] <= e
+  while (hi - lo > 1) {
+    uint32_t mid = lo + (hi - lo) / 2;
+    if (off[mid] <= e) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// one thread per adjacency entry: if the entry is a middle of its row for this route, compute
+// ub, the pruned segment length (ends of degree >= 2) and the full count (all ends; W_G)
+__global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
+                               const uint32_t* __restrict__ adj, const uint32_t* __restrict__ mid,
+                               const uint32_t* __restrict__ end1, uint64_t m,
+                               uint32_t* __restrict__ ub, uint64_t* __restrict__ len,
+                               unsigned long long* __restrict__ w_full) {
+  unsigned long long full = 0;
+  for (uint64_t e64 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e64 < m;
+       e64 += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t e = (uint32_t)e64;
+    uint32_t x = row_of_entry(off, rr.n, e);
+    uint32_t lo = rr.route == 0 ? mid[x] : off[x];
+    uint64_t l_seg = 0;
+    if (rr.in_route(x) && e >= lo && e < end1[x]) {
+      uint32_t sb = x < rr.n_u ? 0 : rr.n_u, ob = x < rr.n_u ? rr.n_u : 0;
+      uint32_t lx = x - sb;
+      uint32_t rv = ob + (adj[e] & kMask);
+      uint32_t b = off[rv], f = off[rv + 1];
+      uint32_t u = upper_bound_col(adj, b, f, lx);
+      uint32_t en = end1[rv];
+      ub[e] = u;
+      full += f - u;
+      l_seg = en > u ? en - u : 0;
+    }
+    len[e] = l_seg;
+  }
+  for (int o = 16; o; o >>= 1) full += __shfl_xor_sync(0xffffffffu, full, o);
+  if ((threadIdx.x & 31) == 0 && full) atomicAdd(w_full, full);
+}
+
+__global__ void k_seg_bounds(RouteRows rr, const uint32_t* __restrict__ off,
+                             const uint32_t* __restrict__ mid, const uint32_t* __restrict__ end1,
+                             uint32_t* __restrict__ b, uint32_t* __restrict__ e) {
+  uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= rr.n) return;
+  if (!rr.in_route(x)) { b[x] = e[x] = 0; return; }
+  uint32_t lo = rr.route == 0 ? mid[x] : off[x];
+  uint32_t hi = end1[x];
+  b[x] = lo;
+  e[x] = hi > lo ? hi : lo;
+}
+
+// count T1 / T3 rows, W per tier, units per T3 row
+__global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, uint64_t w_target,
+                       uint32_t* __restrict__ nunits, unsigned long long* __restrict__ acc) {
+  uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long w1 = 0, w3 = 0;
+  uint32_t u = 0;
+  if (x < n) {
+    uint64_t w = work[x];
+    if (w > 0 && w <= kT1Max) w1 = w;
+    if (w > kT1Max) {
+      w3 = w;
+      u = (uint32_t)std::min<uint64_t>((w + w_target - 1) / w_target, 4096);
+    }
+    nunits[x] = u;
+  }
+  for (int o = 16; o; o >>= 1) {
+    w1 += __shfl_xor_sync(0xffffffffu, w1, o);
+    w3 += __shfl_xor_sync(0xffffffffu, w3, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (w1) atomicAdd(&acc[0], w1);
+    if (w3) atomicAdd(&acc[1], w3);
+  }
+}
+
+struct IsT1 {
+  const uint64_t* work;
+  __device__ __forceinline__ bool operator()(uint32_t x) const {
+    uint64_t w = work[x];
+    return w > 0 && w <= kT1Max;
+  }
+};
+
+// fill the units of every T3 row: split [l(x)+1, L4) into nunits pieces of ~equal sum of end
+// degrees (expected wedges per end rank are proportional to the end's degree)
+__global__ void k_units(uint32_t n, uint32_t n_u, const uint32_t* __restrict__ nunits,
+                        const uint32_t* __restrict__ ustart, const uint64_t* __restrict__ degpre,
+                        uint32_t L4u, uint32_t L4v, const uint32_t* __restrict__ mid_lo,
+                        const uint32_t* __restrict__ end1, Unit* __restrict__ units,
+                        unsigned int* __restrict__ max_mid) {
+  uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  uint32_t k = nunits[x];
+  if (!k) return;
+  uint32_t sb = x < n_u ? 0 : n_u;
+  uint32_t L4 = x < n_u ? L4u : L4v;
+  uint32_t lx = x - sb;
+  uint32_t lo = lx + 1, hi = L4 > lo ? L4 : lo;
+  atomicMax(max_mid, end1[x] - mid_lo[x]);
+  uint32_t base = ustart[x];
+  // prefix over rows: P(r) = sum degs[0..r]; sum over side-local [a, b) = P(sb+b-1) - P(sb+a-1)
+  auto pre = [&](uint32_t l) -> uint64_t {  // sum of degs of side-local ranks [0, l)
+    uint32_t r = sb + l;
+    uint64_t at = r ? degpre[r - 1] : 0;
+    uint64_t base0 = sb ? degpre[sb - 1] : 0;
+    return at - base0;
+  };
+  uint64_t s0 = pre(lo), s1 = pre(hi);
+  uint32_t prev = lo;
+  for (uint32_t j = 0; j < k; ++j) {
+    uint32_t cut;
+    if (j + 1 == k) {
+      cut = hi;
+    } else {
+      uint64_t t = s0 + (s1 - s0) * (uint64_t)(j + 1) / k;
+      uint32_t a = prev, b = hi;  // smallest l in [prev, hi] with pre(l) >= t
+      while (a < b) {
+        uint32_t m = a + (b - a) / 2;
+        if (pre(m) < t) a = m + 1; else b = m;
+      }
+      cut = a;
+    }
+    units[base + j] = Unit{x, prev, cut, 0};
+    prev = cut;
+  }
+}
+
+inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {
+  uint64_t g = (n + block - 1) / block;
+  if (g == 0) g = 1;
+  return (unsigned)std::min<uint64_t>(g, cap);
+}
+
+}  // namespace
+
+void free_plan(Plan* p) {
+  if (p->ub) cudaFree(p->ub);
+  if (p->work) cudaFree(p->work);
+  if (p->t1) cudaFree(p->t1);
+  if (p->units) cudaFree(p->units);
+  *p = Plan{};
+}
+
+bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
+  cudaStream_t st = g->stream;
+  const uint32_t n = g->n;
+  const uint64_t m = 2 * g->nnz;
+  free_plan(p);
+  p->route = route;
+  RouteRows rr{route, g->n_u, n};
+  BBF_CUDA(cudaMallocAsync(&p->ub, 4ull * (m + 1), st));
+  BBF_CUDA(cudaMallocAsync(&p->work, 8ull * (n + 1), st));
+  uint64_t* len;
+  uint32_t *sb, *se, *nunits, *ustart;
+  unsigned long long* acc;
+  BBF_CUDA(cudaMallocAsync(&len, 8ull * (m + 1), st));
+  BBF_CUDA(cudaMallocAsync(&sb, 4ull * (n + 1), st));
+  BBF_CUDA(cudaMallocAsync(&se, 4ull * (n + 1), st));
+  BBF_CUDA(cudaMallocAsync(&nunits, 4ull * (n + 1), st));
+  BBF_CUDA(cudaMallocAsync(&ustart, 4ull * (n + 1), st));
+  BBF_CUDA(cudaMallocAsync(&acc, 8 * sizeof(unsigned long long), st));
+  BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
+  BBF_CUDA(cudaMemsetAsync(p->work, 0, 8ull * (n + 1), st));
+  if (m) {
+    k_plan_entries<<<grid_for(m, 256), 256, 0, st>>>(rr, g->off, g->adj, g->mid, g->end1, m, p->ub,
+                                                   len, &acc[0]);
+    g->launches += 1;
+  }
+  if (n) {
+    k_seg_bounds<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(rr, g->off, g->mid, g->end1, sb, se);
+    size_t tb = 0;
+    cub::DeviceSegmentedReduce::Sum(nullptr, tb, len, p->work, (int)n, sb, se, st);
+    void* tmp;
+    BBF_CUDA(cudaMallocAsync(&tmp, tb + 16, st));
+    BBF_CUDA(cub::DeviceSegmentedReduce::Sum(tmp, tb, len, p->work, (int)n, sb, se, st));
+    g->launches += 2;
+    cudaFreeAsync(tmp, st);
+  }
+  // pruned total, to size units
+  unsigned long long* d_wp;
+  BBF_CUDA(cudaMallocAsync(&d_wp, 8, st));
+  {
+    size_t tb = 0;
+    cub::DeviceReduce::Sum(nullptr, tb, p->work, d_wp, (int)n, st);
+    void* tmp;
+    BBF_CUDA(cudaMallocAsync(&tmp, tb + 16, st));
+    BBF_CUDA(cub::DeviceReduce::Sum(tmp, tb, p->work, d_wp, (int)n, st));
+    g->launches += 1;
+    cudaFreeAsync(tmp, st);
+  }
+  unsigned long long h_wp = 0, h_wf = 0;
+  BBF_CUDA(cudaMemcpyAsync(&h_wp, d_wp, 8, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaMemcpyAsync(&h_wf, &acc[0], 8, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaStreamSynchronize(st));
+  p->W_pruned = h_wp;
+  p->W_full = h_wf;
+  uint64_t w_target = std::max<uint64_t>(h_wp / ((uint64_t)g->num_sms * 6ull + 1), 1ull << 16);
+
+  // tiers and units
+  BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
+  if (n) {
+    k_tier<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, p->work, w_target, nunits, acc);
+    g->launches += 1;
+  }
+  BBF_CUDA(cudaMallocAsync(&p->t1, 4ull * (n + 1), st));
+  uint32_t* d_nsel;
+  BBF_CUDA(cudaMallocAsync(&d_nsel, 8, st));
+  {
+    cub::CountingInputIterator<uint32_t> it(0);
+    size_t tb = 0;
+    cub::DeviceSelect::If(nullptr, tb, it, p->t1, d_nsel, (int)n, IsT1{p->work}, st);
+    size_t tb2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb2, nunits, ustart, (int)(n + 1), st);
+    tb = std::max(tb, tb2);
+    void* tmp;
+    BBF_CUDA(cudaMallocAsync(&tmp, tb + 16, st));
+    BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t1, d_nsel, (int)n, IsT1{p->work}, st));
+    BBF_CUDA(cudaMemsetAsync(nunits + n, 0, 4, st));
+    BBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nunits, ustart, (int)(n + 1), st));
+    g->launches += 3;
+    cudaFreeAsync(tmp, st);
+  }
+  uint32_t h_nsel = 0, h_nunits = 0;
+  unsigned long long h_acc[2];
+  BBF_CUDA(cudaMemcpyAsync(&h_nsel, d_nsel, 4, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaMemcpyAsync(&h_nunits, ustart + n, 4, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaMemcpyAsync(h_acc, acc, 16, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaStreamSynchronize(st));
+  p->n_t1 = h_nsel;
+  p->n_units = h_nunits;
+  p->W_t1 = h_acc[0];
+  p->W_t3 = h_acc[1];
+  BBF_CUDA(cudaMallocAsync(&p->units, sizeof(Unit) * (h_nunits + 1), st));
+  unsigned int* d_maxmid;
+  BBF_CUDA(cudaMallocAsync(&d_maxmid, 4, st));
+  BBF_CUDA(cudaMemsetAsync(d_maxmid, 0, 4, st));
+  if (n && h_nunits) {
+    k_units<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, g->n_u, nunits, ustart, g->degpre,
+                                                      g->L4[0], g->L4[1], sb, g->end1, p->units,
+                                                      d_maxmid);
+    g->launches += 1;
+  }
+  unsigned int h_maxmid = 0;
+  BBF_CUDA(cudaMemcpyAsync(&h_maxmid, d_maxmid, 4, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaStreamSynchronize(st));
+  p->max_mid = h_maxmid;
+  cudaFreeAsync(len, st);
+  cudaFreeAsync(sb, st);
+  cudaFreeAsync(se, st);
+  cudaFreeAsync(nunits, st);
+  cudaFreeAsync(ustart, st);
+  cudaFreeAsync(acc, st);
+  cudaFreeAsync(d_wp, st);
+  cudaFreeAsync(d_nsel, st);
+  cudaFreeAsync(d_maxmid, st);
+  BBF_CUDA(cudaGetLastError());
+  p->valid = true;
+  return BBF_OK;
+}
+
+}  // namespace bbf

@@ -1,0 +1,190 @@
+"""GPU parity: libbbf.so (through the C ABI) vs the CPU oracle, element by element, on the same
+seeded inputs.  Integer results must be bit-exact."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from synth import graphs as G
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 8
+
+
+@pytest.fixture(scope="module")
+def bbf():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2308_07932_b200 import build
+    build.build()
+    from paper_2308_07932_b200 import bbf as B
+    return B
+
+
+def gpu_all(B, g, flags=0):
+    with B.Graph.from_synth(g) as h:
+        glob = h.count_global()
+        tot, bu, nu, bv, nv = h.count_per_vertex(flags=flags)
+    return glob, tot, bu, nu, bv, nv
+
+
+def check_full(B, g, flags=0):
+    glob, tot, bu, nu, bv, nv = gpu_all(B, g, flags)
+    rg = O.route_g(g, threads=THREADS)
+    assert (glob["balanced"], glob["unbalanced"]) == (rg["B"], rg["N"]), g.name
+    assert glob["wedges_G"] == rg["W_G"], g.name
+    assert (tot["balanced"], tot["unbalanced"]) == (rg["B"], rg["N"])
+    bal, unb = O.route_s(g, threads=THREADS)
+    assert np.array_equal(bu, bal[:g.n_u]), g.name
+    assert np.array_equal(nu, unb[:g.n_u]), g.name
+    assert np.array_equal(bv, bal[g.n_u:]), g.name
+    assert np.array_equal(nv, unb[g.n_u:]), g.name
+
+
+def test_config1_global_and_per_vertex(bbf):
+    g = G.config1()
+    check_full(bbf, g)
+    br = O.brute(g)
+    with bbf.Graph.from_synth(g) as h:
+        c = h.count_global()
+    assert (c["balanced"], c["unbalanced"]) == (br["B"], br["N"])
+
+
+def test_config2_per_vertex_and_topk(bbf):
+    g = G.config2()
+    check_full(bbf, g)
+    with bbf.Graph.from_synth(g) as h:
+        for side in (0, 1):
+            got = h.count_pairs_topk(100, side=side)
+            want = O.topk_pairs(g, 100, side=side, threads=THREADS)
+            assert got == want, side
+        assert h.count_per_vertex()[0]["unbalanced"] == 0  # signs per movie: N = 0
+
+
+def test_spec_corpus_subset(bbf):
+    rng = np.random.default_rng(600)
+    pe = [0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9]
+    pp = [0.0, 0.25, 0.5, 0.75, 1.0]
+    for i in range(300):
+        n_u, n_v = int(rng.integers(1, 13)), int(rng.integers(1, 13))
+        g = G.random_bipartite(n_u, n_v, pe[i % 9], pp[(i // 9) % 5], seed=i)
+        check_full(bbf, g)
+
+
+@pytest.mark.parametrize("m,n", [(2, 2), (3, 3), (40, 30), (300, 200), (700, 600)])
+def test_complete_bipartite_closed_form(bbf, m, n):
+    g = G.complete(m, n)
+    c = lambda k: k * (k - 1) // 2
+    glob, tot, bu, nu, bv, nv = gpu_all(bbf, g)
+    assert glob["balanced"] == c(m) * c(n) and glob["unbalanced"] == 0
+    assert np.all(bu == (m - 1) * c(n)) and np.all(bv == (n - 1) * c(m))
+    assert not nu.any() and not nv.any()
+
+
+def test_edge_cases(bbf):
+    # empty graph, isolated vertices, a single butterfly, a star
+    for g, want in [
+        (G.from_edges(1, 1, [], [], []), (0, 0)),
+        (G.from_edges(5, 4, [0, 0, 1, 1], [0, 1, 0, 1], [1, 1, 1, 0]), (0, 1)),
+        (G.from_edges(1, 6, [0] * 6, list(range(6)), [1, 0, 1, 1, 0, 1]), (0, 0)),
+        (G.from_edges(3, 3, [0, 0, 1, 1], [0, 1, 0, 1], [0, 0, 0, 0]), (1, 0)),
+    ]:
+        check_full(bbf, g)
+        with bbf.Graph.from_synth(g) as h:
+            c = h.count_global()
+        assert (c["balanced"], c["unbalanced"]) == want
+
+
+def test_errors(bbf):
+    dup = G.SignedBipartite(2, 2, np.array([0, 2, 2], np.uint64), np.array([0, 0], np.uint32),
+                            np.array([1, 0], np.uint8))
+    with pytest.raises(bbf.BBFError) as e:
+        bbf.Graph.from_synth(dup)
+    assert e.value.name == "BBF_EDUP"
+    rng_bad = G.SignedBipartite(2, 2, np.array([0, 1, 2], np.uint64), np.array([0, 2], np.uint32),
+                                np.array([1, 1], np.uint8))
+    with pytest.raises(bbf.BBFError) as e:
+        bbf.Graph.from_synth(rng_bad)
+    assert e.value.name == "BBF_ERANGE"
+    sgn_bad = G.SignedBipartite(2, 2, np.array([0, 1, 2], np.uint64), np.array([0, 1], np.uint32),
+                                np.array([1, 3], np.uint8))
+    with pytest.raises(bbf.BBFError) as e:
+        bbf.Graph.from_synth(sgn_bad)
+    assert e.value.name == "BBF_EINVAL"
+    mono_bad = G.SignedBipartite(2, 2, np.array([0, 2, 1], np.uint64), np.array([0, 1], np.uint32),
+                                 np.array([1, 1], np.uint8))
+    with pytest.raises(bbf.BBFError) as e:
+        bbf.Graph.from_synth(mono_bad)
+    assert e.value.name == "BBF_ERANGE"
+    with bbf.Graph.from_synth(G.config1()) as h:
+        with pytest.raises(bbf.BBFError):
+            h.count_pairs_topk(0)
+
+
+def zoned_graph(seed=11):
+    """Degrees spanning every counter zone (deg > 65535 down to 2) on the U side, enough
+    degree-2/3 ends to need several 48K-word windows, and hub starts split into units."""
+    rng = np.random.default_rng(seed)
+    n_v = 80_000
+    degs = [70_000] * 2 + [300] * 40 + [40] * 1500 + [6] * 20_000 + [2] * 450_000 + [3] * 60_000 + [1] * 5000
+    n_u = len(degs)
+    w = 1.0 / np.arange(1, n_v + 1) ** 0.6
+    cdf = np.cumsum(w) / w.sum()
+    degs = np.array(degs)
+    big = np.nonzero(degs >= 1000)[0]
+    us = [np.full(degs[b], b) for b in big]
+    vs = [rng.choice(n_v, size=degs[b], replace=False) for b in big]
+    small = np.nonzero(degs < 1000)[0]
+    su = np.repeat(small, degs[small])
+    sv = np.searchsorted(cdf, rng.random(su.size), side="right").clip(0, n_v - 1)
+    key = np.unique(su.astype(np.int64) * n_v + sv)  # duplicates dropped: degrees <= target
+    us.append(key // n_v)
+    vs.append(key % n_v)
+    u = np.concatenate(us)
+    v = np.concatenate(vs)
+    s = (rng.random(u.size) < 0.6).astype(np.uint8)
+    return G.from_edges(n_u, n_v, u, v, s, name="zoned")
+
+
+def test_zoned_windows_global_and_sampled_vertices(bbf):
+    g = zoned_graph()
+    rg = O.route_g(g, threads=THREADS)
+    with bbf.Graph.from_synth(g) as h:
+        c = h.count_global()
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+    assert (c["balanced"], c["unbalanced"], c["wedges_G"]) == (rg["B"], rg["N"], rg["W_G"])
+    assert (tot["balanced"], tot["unbalanced"]) == (rg["B"], rg["N"])
+    # per-vertex: sum identities at any size + sampled vBBFC vertices
+    assert int(bu.sum()) == 2 * rg["B"] and int(bv.sum()) == 2 * rg["B"]
+    assert int(nu.sum()) == 2 * rg["N"] and int(nv.sum()) == 2 * rg["N"]
+    rng = np.random.default_rng(0)
+    su = np.unique(np.concatenate([np.arange(0, 50), rng.integers(0, g.n_u, 400)]))
+    sv = np.unique(rng.integers(0, g.n_v, 60))
+    bal, unb = O.route_s(g, verts=np.concatenate([su, g.n_u + sv]), threads=THREADS)
+    assert np.array_equal(bu[su], bal[:su.size]) and np.array_equal(nu[su], unb[:su.size])
+    assert np.array_equal(bv[sv], bal[su.size:]) and np.array_equal(nv[sv], unb[su.size:])
+
+
+def test_config3_full_size(bbf):
+    g = G.config3()
+    rg = O.route_g(g, threads=THREADS)
+    with bbf.Graph.from_synth(g) as h:
+        c = h.count_global()
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+        c2 = h.count_global()
+    assert (c["balanced"], c["unbalanced"], c["wedges_G"]) == (rg["B"], rg["N"], rg["W_G"])
+    assert c2["balanced"] == c["balanced"] and c2["unbalanced"] == c["unbalanced"]  # deterministic
+    assert (tot["balanced"], tot["unbalanced"]) == (rg["B"], rg["N"])
+    assert int(bu.sum()) == 2 * rg["B"] and int(bv.sum()) == 2 * rg["B"]
+    assert int(nu.sum()) == 2 * rg["N"] and int(nv.sum()) == 2 * rg["N"]
+    rng = np.random.default_rng(3)
+    deg_u = np.diff(g.row_ptr.astype(np.int64))
+    top = np.argsort(-deg_u)[:20]
+    su = np.unique(np.concatenate([top, rng.integers(0, g.n_u, 300)]))
+    sv = np.unique(rng.integers(0, g.n_v, 200))
+    bal, unb = O.route_s(g, verts=np.concatenate([su, g.n_u + sv]), threads=THREADS)
+    assert np.array_equal(bu[su], bal[:su.size]) and np.array_equal(nu[su], unb[:su.size])
+    assert np.array_equal(bv[sv], bal[su.size:]) and np.array_equal(nv[sv], unb[su.size:])
