@@ -94,12 +94,12 @@ def route_g(g, starts=None, threads=None):
     lib = _load()
     keep, a = _graph_args(g)
     st = None if starts is None else np.ascontiguousarray(starts, dtype=np.uint32)
-    out = np.zeros(3, np.uint64)
+    out = np.zeros(4, np.uint64)
     rc = lib.oracle_route_g(*a, _ptr(st), C.c_uint64(0 if st is None else st.size),
                             _threads(threads), _ptr(out))
     if rc:
         raise OracleError(rc)
-    return dict(B=int(out[0]), N=int(out[1]), W_G=int(out[2]))
+    return dict(B=int(out[0]), N=int(out[1]), W_G=int(out[2]), count_s=float(out[3]) * 1e-9)
 
 
 def route_s(g, verts=None, threads=None):

@@ -146,6 +146,7 @@ struct Plan {
   unsigned long long W_full;    // un-pruned wedge count (route G: W_G of the paper)
   unsigned long long W_pruned;  // wedges the kernels actually visit
   unsigned long long W_t1, W_t3;
+  unsigned long long M_t3;     // eligible middles of T3 starts
   bool valid;
 };
 

@@ -551,10 +551,10 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   host_BN[0] = h[0];
   host_BN[1] = h[1];
   if (n_cand) *n_cand = h[4];
-  // algorithmic bytes of the engine: 4 B per visited wedge per pass,
-  // 16 B per eligible middle (column word, ub, end1, cursor), 16 B per vertex output
-  unsigned long long wedges = p->W_pruned;
-  g->algo_bytes = 4ull * wedges * (per_vertex ? 2 : 1) + 16ull * g->nnz + (per_vertex ? 16ull * g->n : 0);
+  // algorithmic bytes of the hub kernel k_t3: 4 B column word per
+  // visited wedge per pass (pass 2 re-reads it for per-vertex counts) + 16 B per eligible
+  // middle of its starts (column word, ub, end1 of the middle's row, 4 B id-side output)
+  g->algo_bytes = 4ull * p->W_t3 * (per_vertex ? 2 : 1) + 16ull * p->M_t3;
   return BBF_OK;
 }
 

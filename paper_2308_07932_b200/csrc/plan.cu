@@ -86,15 +86,17 @@ __global__ void k_seg_bounds(RouteRows rr, const uint32_t* __restrict__ off,
 
 // count T1 / T3 rows, W per tier, units per T3 row
 __global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, uint64_t w_target,
+                       const uint32_t* __restrict__ mlo, const uint32_t* __restrict__ mhi,
                        uint32_t* __restrict__ nunits, unsigned long long* __restrict__ acc) {
   uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long w1 = 0, w3 = 0;
+  unsigned long long w1 = 0, w3 = 0, m3 = 0;
   uint32_t u = 0;
   if (x < n) {
     uint64_t w = work[x];
     if (w > 0 && w <= kT1Max) w1 = w;
     if (w > kT1Max) {
       w3 = w;
+      m3 = mhi[x] - mlo[x];
       u = (uint32_t)std::min<uint64_t>((w + w_target - 1) / w_target, 4096);
     }
     nunits[x] = u;
@@ -102,10 +104,12 @@ __global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, uint64_t w
   for (int o = 16; o; o >>= 1) {
     w1 += __shfl_xor_sync(0xffffffffu, w1, o);
     w3 += __shfl_xor_sync(0xffffffffu, w3, o);
+    m3 += __shfl_xor_sync(0xffffffffu, m3, o);
   }
   if ((threadIdx.x & 31) == 0) {
     if (w1) atomicAdd(&acc[0], w1);
     if (w3) atomicAdd(&acc[1], w3);
+    if (m3) atomicAdd(&acc[2], m3);
   }
 }
 
@@ -235,7 +239,7 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   // tiers and units
   BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
   if (n) {
-    k_tier<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, p->work, w_target, nunits, acc);
+    k_tier<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, p->work, w_target, sb, se, nunits, acc);
     g->launches += 1;
   }
   BBF_CUDA(cudaMallocAsync(&p->t1, 4ull * (n + 1), st));
@@ -257,15 +261,16 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     cudaFreeAsync(tmp, st);
   }
   uint32_t h_nsel = 0, h_nunits = 0;
-  unsigned long long h_acc[2];
+  unsigned long long h_acc[3];
   BBF_CUDA(cudaMemcpyAsync(&h_nsel, d_nsel, 4, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaMemcpyAsync(&h_nunits, ustart + n, 4, cudaMemcpyDeviceToHost, st));
-  BBF_CUDA(cudaMemcpyAsync(h_acc, acc, 16, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaMemcpyAsync(h_acc, acc, 24, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaStreamSynchronize(st));
   p->n_t1 = h_nsel;
   p->n_units = h_nunits;
   p->W_t1 = h_acc[0];
   p->W_t3 = h_acc[1];
+  p->M_t3 = h_acc[2];
   BBF_CUDA(cudaMallocAsync(&p->units, sizeof(Unit) * (h_nunits + 1), st));
   unsigned int* d_maxmid;
   BBF_CUDA(cudaMallocAsync(&d_maxmid, 4, st));

@@ -171,6 +171,39 @@ def chung_lu_weights(n: int, mean: float, wmax: float, gamma: float) -> np.ndarr
     return wmax * (i0 / (idx + i0)) ** alpha
 
 
+def _accel():
+    """torch CUDA device for the exact, order-free primitives below (searchsorted of float64
+    keys, sort-based unique) when a GPU is present; results are identical to numpy's."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch
+    except Exception:
+        pass
+    return None
+
+
+def _searchsorted_right(cdf: np.ndarray, r: np.ndarray) -> np.ndarray:
+    t = _accel()
+    if t is None:
+        return np.searchsorted(cdf, r, side="right")
+    out = t.searchsorted(t.from_numpy(cdf).cuda(), t.from_numpy(r).cuda(), right=True)
+    return out.cpu().numpy()
+
+
+def _unique_first(keys: np.ndarray):
+    """np.unique(keys, return_index=True): sorted distinct keys and first occurrence index."""
+    t = _accel()
+    if t is None:
+        return np.unique(keys, return_index=True)
+    k = t.from_numpy(keys).cuda()
+    uniq, inv = t.unique(k, sorted=True, return_inverse=True)
+    pos = t.arange(k.numel(), device=k.device)
+    first = t.full((uniq.numel(),), k.numel(), dtype=t.int64, device=k.device)
+    first.scatter_reduce_(0, inv, pos, reduce="amin")
+    return uniq.cpu().numpy(), first.cpu().numpy()
+
+
 def chung_lu(n_u: int, n_v: int, m: int, gamma: float, wmax_u: float, wmax_v: float, seed: int):
     """Distinct (u, v) pairs, endpoints drawn independently prop. to Chung-Lu weights.
     Draw order: batch 0 of ceil(1.2 m) draws, then batches of ceil(0.1 m) draws, each batch
@@ -185,11 +218,11 @@ def chung_lu(n_u: int, n_v: int, m: int, gamma: float, wmax_u: float, wmax_v: fl
     chunks = []
     batch = int(np.ceil(1.2 * m))
     while True:
-        bu = np.searchsorted(cu, rng.random(batch), side="right").clip(0, n_u - 1)
-        bv = np.searchsorted(cv, rng.random(batch), side="right").clip(0, n_v - 1)
+        bu = _searchsorted_right(cu, rng.random(batch)).clip(0, n_u - 1)
+        bv = _searchsorted_right(cv, rng.random(batch)).clip(0, n_v - 1)
         chunks.append(bu.astype(np.int64) * n_v + bv)
         keys = np.concatenate(chunks) if len(chunks) > 1 else chunks[0]
-        uniq, first = np.unique(keys, return_index=True)
+        uniq, first = _unique_first(keys)
         if uniq.size >= m:
             break
         batch = int(np.ceil(0.1 * m))

@@ -1,0 +1,38 @@
+"""One hot-path step (device CSR -> build/plan -> per-vertex count -> free) for profiling.
+python tools/step_once.py --config 3 [--steps 1] [--global-only]"""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--global-only", action="store_true")
+    a = ap.parse_args()
+    import torch
+    from paper_2308_07932_b200 import bbf
+    from synth import graphs as G
+    g = G.make_config(a.config)
+    dev = torch.device("cuda", 0)
+    rp = torch.from_numpy(g.row_ptr.view(np.int64)).to(dev)
+    col = torch.from_numpy(g.col.view(np.int32)).to(dev)
+    sg = torch.from_numpy(g.sign).to(dev)
+    outs = tuple(torch.zeros(k, dtype=torch.int64, device=dev) for k in (g.n_u, g.n_u, g.n_v, g.n_v))
+    s = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(s)
+    for _ in range(a.steps):
+        h = bbf.Graph(g.n_u, g.n_v, rp, col, sg, stream=s)
+        r = h.count_global() if a.global_only else h.count_per_vertex(out=outs)[0]
+        print(r, h.stats(), flush=True)
+        h.free()
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()
