@@ -66,6 +66,21 @@ bool device_ok(int device, int* num_sms) {
   return true;
 }
 
+// Keep freed stream-ordered memory in the device's default pool: a graph's buffers are
+// re-allocated on every load, and returning them to the driver at each synchronisation costs
+// more than the count itself on large graphs.
+void keep_pool(int device) {
+  static std::once_flag flags[64];
+  if (device < 0 || device >= 64) return;
+  std::call_once(flags[device], [device] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
 // rank space -> input ids (S9)
 __global__ void k_scatter_pv(const unsigned long long* __restrict__ pv, const uint32_t* __restrict__ inv,
                              uint32_t row0, uint32_t cnt, uint32_t n, unsigned long long* __restrict__ ob,
@@ -217,8 +232,9 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_pt
     g->own_stream = true;
   }
   bbf_status s = BBF_OK;
-  cudaError_t e = cudaMalloc(&g->d_acc, 16 * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMalloc(&g->pv, 16ull * (g->n + 1));
+  keep_pool(device);
+  cudaError_t e = cudaMallocAsync(&g->d_acc, 16 * sizeof(unsigned long long), g->stream);
+  if (e == cudaSuccess) e = cudaMallocAsync(&g->pv, 16ull * (g->n + 1), g->stream);
   if (e != cudaSuccess) s = cuda_status(e, "cudaMalloc");
   if (s == BBF_OK) s = build_graph(g, row_ptr, col, sign, dptr);
   if (s == BBF_OK) {
@@ -238,13 +254,13 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_pt
 bbf_status bbf_graph_free(bbf_graph* g) {
   if (!g) return BBF_OK;
   cudaSetDevice(g->device);
-  cudaStreamSynchronize(g->stream);
-  free_plan(&g->plan_g);
-  free_plan(&g->plan_s[0]);
-  free_plan(&g->plan_s[1]);
+  free_plan(&g->plan_g, g->stream);
+  free_plan(&g->plan_s[0], g->stream);
+  free_plan(&g->plan_s[1], g->stream);
   void* ptrs[] = {g->off, g->adj, g->mid, g->end1, g->inv, g->degs, g->degpre, g->scratch, g->d_acc, g->pv};
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, g->stream);
+  cudaStreamSynchronize(g->stream);
   if (g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
   return BBF_OK;

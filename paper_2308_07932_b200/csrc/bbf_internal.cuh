@@ -143,6 +143,7 @@ struct Plan {
   Unit* units;         // T3 units
   uint32_t n_t1, n_units;
   uint32_t max_mid;    // max middles of a T3 start
+  unsigned long long max_work;  // max wedges of a T3 start
   unsigned long long W_full;    // un-pruned wedge count (route G: W_G of the paper)
   unsigned long long W_pruned;  // wedges the kernels actually visit
   unsigned long long W_t1, W_t3;
@@ -175,6 +176,7 @@ struct bbf_graph {
   uint64_t* degpre;   // n+2 : per side inclusive prefix of degrees over rows (side-local, see plan)
   bbf::Zones zones[2];
   uint32_t L4[2];     // #vertices with degree >= 2 per side
+  uint32_t Llong[2];  // #vertices with degree > 32 per side ("long" middles of the hub kernel)
   uint32_t maxdeg[2];
   long double ws_bound;  // overflow bound on B + N
   bbf::Plan plan_g;
@@ -214,7 +216,7 @@ namespace bbf {
 bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* col,
                        const uint8_t* sign, bool device_ptrs);
 bbf_status make_plan(bbf_graph* g, int route, Plan* p);
-void free_plan(Plan* p);
+void free_plan(Plan* p, cudaStream_t st);
 // run the sparse engine for a route; per_vertex -> accumulate into g->pv (rank space)
 bbf_status run_sparse(bbf_graph* g, Plan* p, bool per_vertex, int rank, int nranks,
                       unsigned long long* host_BN);

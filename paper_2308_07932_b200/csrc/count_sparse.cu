@@ -20,6 +20,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "bbf_internal.cuh"
@@ -30,7 +32,6 @@ namespace {
 constexpr int kT3Threads = 1024;
 constexpr uint32_t kWin = 48 * 1024;  // counter words per CTA window (192 KB)
 constexpr uint32_t kBm = kWin / 32;   // bitmap words
-constexpr uint32_t kLong = 64;        // middles with longer remaining segments go warp-wide
 constexpr int kT1Warps = 12;
 constexpr uint32_t kT1Slots = 1024;
 
@@ -52,6 +53,8 @@ struct EngineArgs {
   unsigned long long* pv;   // [0, n) balanced per row, [n, 2n) unbalanced per row
   uint32_t* scratch;
   uint32_t max_mid;
+  uint32_t kwin_cap;  // max windows per side
+  uint32_t rec_stride;  // record slots per window: max middles + max unit work / kRecMax
   // pair candidates (top-k): balanced, unbalanced, (min id << 32 | max id)
   unsigned long long* cb;
   unsigned long long* cn;
@@ -77,20 +80,59 @@ __device__ __forceinline__ void emit_pair(const EngineArgs& a, uint32_t x, uint3
 }
 
 // ===================================================================================== T3
+// One CTA per unit (start x, end-rank range).  The end ranks of x's side are cut into a fixed
+// grid of windows of kWin counter words (degree-zoned fields, bbf_internal.cuh).
+//   pre-scan : warps walk each middle's segment once (coalesced) and record every maximal run
+//              of entries that falls into one window ("segment record": middle, start, length),
+//              bucketed by window;
+//   per window (only windows that received records):
+//     scan   : block-wide prefix of the window's record lengths;
+//     pass 1 : 256-entry chunks of the flattened window pulled by warps; each lane finds its
+//              record with a ballot/popc load-balanced search; one shared atomic per wedge;
+//     pass 2 : (per-vertex) the same chunks read the final (a, d) of each end: middle shares;
+//     epilogue: Lemma 2 per touched word (bitmap), clear.
+constexpr uint32_t kRecMax = 1024;
+constexpr uint32_t kMaxWin = 256;
+
+__device__ __forceinline__ void t3_inc(const Zones& Z, uint32_t* ctr, uint32_t* bm, uint32_t word0,
+                                       uint32_t l, uint32_t cls) {
+  uint32_t base, word, inc;
+  field_of(Z, l, cls, base, word, inc);
+  uint32_t prev = atomicAdd(&ctr[word - word0], inc);
+  if (prev == 0) atomicOr(&bm[(base - word0) >> 5], 1u << ((base - word0) & 31));
+}
+
+__device__ __forceinline__ void mid_share(const Zones& Z, const uint32_t* ctr, uint32_t word0,
+                                          uint32_t ev, uint32_t wv, unsigned long long& b,
+                                          unsigned long long& nn) {
+  uint32_t ad, dd;
+  field_read(Z, ctr, word0, ev & kMask, ad, dd);
+  if (((ev ^ wv) >> 31) == 0) { b += ad - 1; nn += dd; }   // symmetric: (a-1, d)
+  else { b += dd - 1; nn += ad; }                            // asymmetric: (d-1, a)
+}
+
 template <bool PV, bool PAIRS>
 __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
+  using BlockScan = cub::BlockScan<uint32_t, kT3Threads>;
   extern __shared__ uint32_t smem[];
-  uint32_t* ctr = smem;         // kWin
-  uint32_t* bm = smem + kWin;   // kBm
-  __shared__ uint32_t sh_unit, sh_next, sh_nlong, sh_next2;
+  uint32_t* ctr = smem;                   // kWin
+  uint32_t* bm = smem + kWin;             // kBm
+  uint32_t* flag = bm + kBm;              // 32 warps x 32
+  uint32_t* sh_cnt = flag + 32 * 32;      // kMaxWin record counts
+  __shared__ typename BlockScan::TempStorage scan_tmp;
+  __shared__ uint32_t sh_unit, sh_run, sh_c[4];
   __shared__ unsigned long long sh_red[2][32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kT3Threads / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* wflag = flag + warp * 32;
 
-  for (uint32_t i = tid; i < kWin + kBm; i += kT3Threads) smem[i] = 0;
-  uint32_t* Sw = a.scratch + (size_t)blockIdx.x * 4 * a.max_mid;
-  uint32_t* Scur = Sw + a.max_mid;
-  uint32_t* Sold = Scur + a.max_mid;
-  uint32_t* Send = Sold + a.max_mid;
+  for (uint32_t i = tid; i < kWin + kBm + 32 * 32 + kMaxWin; i += kT3Threads) smem[i] = 0;
+  const size_t M = a.max_mid, RS = a.rec_stride, RC = RS * a.kwin_cap;
+  uint32_t* Sw = a.scratch + (size_t)blockIdx.x * (3 * M + 3 * RC);
+  uint32_t* Scur = Sw + M;
+  uint32_t* Send = Scur + M;
+  uint32_t* Ri = Send + M;       // [window][slot] middle index
+  uint32_t* Rp = Ri + RC;        // start position in adj
+  uint32_t* Rl = Rp + RC;        // length
   unsigned long long totB = 0, totN = 0;
   __syncthreads();
 
@@ -104,18 +146,17 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
     const bool xu = x < a.n_u;
     const uint32_t sb = xu ? 0 : a.n_u, ob = xu ? a.n_u : 0, lx = x - sb;
     const Zones& Z = a.z[xu ? 0 : 1];
+    const uint32_t K = (Z.WB[5] + kWin - 1) / kWin;
     const uint32_t m_lo = a.mid ? a.mid[x] : a.off[x];
     const uint32_t m = a.end1[x] - m_lo;
-    if (tid == 0) { sh_next = 0xffffffffu; sh_nlong = 0; sh_next2 = 0xffffffffu; }
-    __syncthreads();
-    // ---- unit setup: middle words, cursors (first end >= u.lo), segment ends, long list
-    uint32_t my_min = 0xffffffffu;
+    if (tid < 4) sh_c[tid] = 0;
+    // ---- unit setup: middle words and segments [first end >= u.lo, first end >= u.hi)
     for (uint32_t i = tid; i < m; i += kT3Threads) {
       uint32_t e = m_lo + i;
       uint32_t wv = a.adj[e];
       uint32_t rv = ob + (wv & kMask);
       uint32_t s = a.ub[e], en = a.end1[rv];
-      if (u.lo > lx + 1 && s < en) {  // binary search for the unit's first end rank
+      if (u.lo > lx + 1 && s < en) {
         uint32_t b = s, f = en;
         while (b < f) {
           uint32_t md = b + (f - b) / 2;
@@ -123,132 +164,107 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
         }
         s = b;
       }
+      if (u.hi < Z.L[4] && s < en) {
+        uint32_t b = s, f = en;
+        while (b < f) {
+          uint32_t md = b + (f - b) / 2;
+          if ((a.adj[md] & kMask) < u.hi) b = md + 1; else f = md;
+        }
+        en = b;
+      }
       Sw[i] = wv;
       Scur[i] = s;
       Send[i] = en;
-      if (s < en) {
-        uint32_t l0 = a.adj[s] & kMask;
-        if (l0 < my_min) my_min = l0;
-      }
     }
-    for (int o = 16; o; o >>= 1) my_min = min(my_min, __shfl_xor_sync(0xffffffffu, my_min, o));
-    if (lane == 0 && my_min != 0xffffffffu) atomicMin(&sh_next, my_min);
     __syncthreads();
-    uint32_t wl_lo = sh_next;
+    // ---- pre-scan: per-window segment records (warp per middle, middles pulled dynamically)
+    while (true) {
+      uint32_t i = 0;
+      if (lane == 0) i = atomicAdd(&sh_c[0], 1u);
+      i = __shfl_sync(0xffffffffu, i, 0);
+      if (i >= m) break;
+      const uint32_t s = Scur[i], e = Send[i];
+      if (s >= e) continue;
+      uint32_t open_k = 0xffffffffu, open_slot = 0, open_p = 0, carry_k = 0xfffffffeu;
+      for (uint32_t pos = s; pos < e; pos += 32) {
+        const uint32_t p = pos + lane;
+        const bool valid = p < e;
+        const uint32_t k = valid ? word_of_l(Z, a.adj[p] & kMask) / kWin : 0xffffffffu;
+        uint32_t kprev = __shfl_up_sync(0xffffffffu, k, 1);
+        if (lane == 0) kprev = carry_k;
+        // a record also restarts every kRecMax entries (p - s is a multiple of kRecMax), so no
+        // record is longer than kRecMax and warps stay balanced inside a window
+        const bool is_start = valid && (k != kprev || ((p - s) % kRecMax) == 0);
+        const uint32_t smask = __ballot_sync(0xffffffffu, is_start);
+        if (smask && open_k != 0xffffffffu && lane == 0)
+          Rl[(size_t)open_k * RS + open_slot] = pos + (__ffs(smask) - 1) - open_p;
+        uint32_t slot = 0;
+        if (is_start) {
+          slot = atomicAdd(&sh_cnt[k], 1u);
+          Ri[(size_t)k * RS + slot] = i;
+          Rp[(size_t)k * RS + slot] = p;
+          const uint32_t later = smask & ~((2u << lane) - 1u);
+          if (later) Rl[(size_t)k * RS + slot] = (__ffs(later) - 1) - lane;
+        }
+        if (smask) {  // the last start of this step stays open
+          const int last = 31 - __clz(smask);
+          open_k = __shfl_sync(0xffffffffu, k, last);
+          open_slot = __shfl_sync(0xffffffffu, slot, last);
+          open_p = pos + last;
+        }
+        carry_k = __shfl_sync(0xffffffffu, k, 31);
+      }
+      if (lane == 0 && open_k != 0xffffffffu) Rl[(size_t)open_k * RS + open_slot] = e - open_p;
+    }
+    __syncthreads();
     unsigned long long xB = 0, xN = 0;
 
-    while (wl_lo < u.hi) {
-      const uint32_t word0 = word_of_l(Z, wl_lo);
-      uint32_t wl_hi = l_first_last_word_ge(Z, (uint64_t)word0 + kWin);
-      if (wl_hi > u.hi) wl_hi = u.hi;
-      // ---------------- pass 1: count symmetric / asymmetric wedges per end (Alg. 2 l. 9-14)
-      // a warp owns a chunk of 32 middles in both passes; short remaining segments are walked
-      // one lane per middle, long ones by the whole warp (coalesced 128-B reads)
-      uint32_t nmin = 0xffffffffu;
-      for (uint32_t c = warp; c * 32 < m; c += nw) {
-        const uint32_t i = c * 32 + lane;
-        uint32_t cur = 0, en = 0, wv = 0;
-        bool has = false, lng = false;
-        if (i < m) {
-          cur = Scur[i]; en = Send[i]; wv = Sw[i];
-          has = cur < en;
-          lng = has && (en - cur > kLong);
-        }
-        const uint32_t old = cur;
-        if (has && !lng) {
-          uint32_t l = 0xffffffffu;
-          while (cur < en) {
-            uint32_t ev = a.adj[cur];
-            l = ev & kMask;
-            if (l >= wl_hi) break;
-            uint32_t base, word, inc;
-            field_of(Z, l, (ev ^ wv) >> 31, base, word, inc);
-            uint32_t prev = atomicAdd(&ctr[word - word0], inc);
-            if (prev == 0) atomicOr(&bm[(base - word0) >> 5], 1u << ((base - word0) & 31));
-            ++cur;
-          }
-          if (cur < en) nmin = min(nmin, l);
-        }
-        uint32_t lmask = __ballot_sync(0xffffffffu, lng);
-        while (lmask) {
-          const int j = __ffs(lmask) - 1;
-          lmask &= lmask - 1;
-          uint32_t jc = __shfl_sync(0xffffffffu, cur, j);
-          const uint32_t je = __shfl_sync(0xffffffffu, en, j);
-          const uint32_t jw = __shfl_sync(0xffffffffu, wv, j);
-          while (true) {
-            uint32_t idx = jc + lane;
-            uint32_t ev = idx < je ? a.adj[idx] : 0xffffffffu;
-            uint32_t l = ev & kMask;
-            bool in = idx < je && l < wl_hi;
-            if (in) {
-              uint32_t base, word, inc;
-              field_of(Z, l, (ev ^ jw) >> 31, base, word, inc);
-              uint32_t prev = atomicAdd(&ctr[word - word0], inc);
-              if (prev == 0) atomicOr(&bm[(base - word0) >> 5], 1u << ((base - word0) & 31));
-            }
-            uint32_t cnt = __popc(__ballot_sync(0xffffffffu, in));
-            uint32_t lnext = __shfl_sync(0xffffffffu, l, cnt & 31);
-            jc += cnt;
-            if (cnt < 32) {
-              if (jc < je) nmin = min(nmin, lnext);
-              break;
-            }
-          }
-          if (lane == j) cur = jc;
-        }
-        if (i < m) { Sold[i] = old; Scur[i] = cur; }
-      }
-      for (int o = 16; o; o >>= 1) nmin = min(nmin, __shfl_xor_sync(0xffffffffu, nmin, o));
-      if (lane == 0 && nmin != 0xffffffffu) atomicMin(&sh_next2, nmin);
+    for (uint32_t k = 0; k < K; ++k) {
+      const uint32_t nrec = sh_cnt[k];
+      if (nrec == 0) continue;
+      const uint32_t word0 = k * kWin;
+      const uint32_t* ri = Ri + (size_t)k * RS;
+      const uint32_t* rp = Rp + (size_t)k * RS;
+      const uint32_t* rl = Rl + (size_t)k * RS;
+      if (tid < 4) sh_c[tid] = 0;
+      if (tid == 0) { atomicAdd(&a.acc[6], (unsigned long long)nrec); atomicAdd(&a.acc[7], 1ull); }
       __syncthreads();
-      const uint32_t next_lo = sh_next2;
-      __syncthreads();
-      if (tid == 0) sh_next2 = 0xffffffffu;
-
-      // ---------------- pass 2: middles' per-vertex shares from the final (a, d) of each end
-      if (PV) {
-        for (uint32_t c = warp; c * 32 < m; c += nw) {
-          const uint32_t i = c * 32 + lane;
-          uint32_t old = 0, cur = 0, wv = 0;
-          if (i < m) { old = Sold[i]; cur = Scur[i]; wv = Sw[i]; }
-          const bool lng = cur - old > kLong;
-          if (!lng && cur > old) {
+      // ---------------- pass 1 (Alg. 2 lines 9-14) and pass 2 (per-vertex shares):
+      // one warp per segment record (records are <= kRecMax entries), pulled dynamically
+#pragma unroll 1
+      for (int pass = 0; pass < (PV ? 2 : 1); ++pass) {
+        while (true) {
+          uint32_t r = 0;
+          if (lane == 0) r = atomicAdd(&sh_c[pass], 1u);
+          r = __shfl_sync(0xffffffffu, r, 0);
+          if (r >= nrec) break;
+          const uint32_t i = ri[r], p0 = rp[r], len = rl[r];
+          const uint32_t wv = Sw[i];
+          if (pass == 0) {
+            for (uint32_t o = lane; o < len; o += 128) {
+              uint32_t ev[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) ev[q] = (o + 32 * q < len) ? a.adj[p0 + o + 32 * q] : 0u;
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (o + 32 * q < len) t3_inc(Z, ctr, bm, word0, ev[q] & kMask, (ev[q] ^ wv) >> 31);
+            }
+          } else {
             unsigned long long cb = 0, cn = 0;
-            for (uint32_t p = old; p < cur; ++p) {
-              uint32_t ev = a.adj[p];
-              uint32_t ad, dd;
-              field_read(Z, ctr, word0, ev & kMask, ad, dd);
-              if (((ev ^ wv) >> 31) == 0) { cb += ad - 1; cn += dd; }
-              else { cb += dd - 1; cn += ad; }
+            for (uint32_t o = lane; o < len; o += 128) {
+              uint32_t ev[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) ev[q] = (o + 32 * q < len) ? a.adj[p0 + o + 32 * q] : 0u;
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (o + 32 * q < len) mid_share(Z, ctr, word0, ev[q], wv, cb, cn);
             }
-            if (cb | cn) {
-              uint32_t vr = ob + (wv & kMask);
+            cb = warp_sum(cb);
+            cn = warp_sum(cn);
+            if (lane == 0 && (cb | cn)) {
+              const uint32_t vr = ob + (wv & kMask);
               atomicAdd(&a.pv[vr], cb);
               atomicAdd(&a.pv[a.n + vr], cn);
-            }
-          }
-          uint32_t lmask = __ballot_sync(0xffffffffu, lng);
-          while (lmask) {
-            const int j = __ffs(lmask) - 1;
-            lmask &= lmask - 1;
-            const uint32_t jo = __shfl_sync(0xffffffffu, old, j);
-            const uint32_t jc = __shfl_sync(0xffffffffu, cur, j);
-            const uint32_t jw = __shfl_sync(0xffffffffu, wv, j);
-            unsigned long long b2 = 0, n2 = 0;
-            for (uint32_t p = jo + lane; p < jc; p += 32) {
-              uint32_t ev = a.adj[p];
-              uint32_t ad, dd;
-              field_read(Z, ctr, word0, ev & kMask, ad, dd);
-              if (((ev ^ jw) >> 31) == 0) { b2 += ad - 1; n2 += dd; }
-              else { b2 += dd - 1; n2 += ad; }
-            }
-            b2 = warp_sum(b2);
-            n2 = warp_sum(n2);
-            if (lane == 0 && (b2 | n2)) {
-              uint32_t vr = ob + (jw & kMask);
-              atomicAdd(&a.pv[vr], b2);
-              atomicAdd(&a.pv[a.n + vr], n2);
             }
           }
         }
@@ -267,29 +283,27 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
           uint32_t gw = word0 + wi;
           uint32_t v = ctr[wi];
           ctr[wi] = 0;
-          uint32_t nf, fbits, lbase;
+          uint32_t nf, lbase;
           uint32_t av[8], dv[8];
-          if (gw < Z.WB[1]) {  // zone 0: (a word, d word)
+          if (gw < Z.WB[1]) {  // zone 0: (a word, d word); bits are set on the a word only
             av[0] = v;
             dv[0] = ctr[wi + 1];
             ctr[wi + 1] = 0;
-            nf = 1; fbits = 64; lbase = gw >> 1;
+            nf = 1; lbase = gw >> 1;
           } else if (gw < Z.WB[2]) {
-            av[0] = v & 0xffffu; dv[0] = v >> 16; nf = 1; fbits = 32; lbase = Z.L[0] + (gw - Z.WB[1]);
+            av[0] = v & 0xffffu; dv[0] = v >> 16; nf = 1; lbase = Z.L[0] + (gw - Z.WB[1]);
           } else if (gw < Z.WB[3]) {
-            nf = 2; fbits = 16; lbase = Z.L[1] + 2 * (gw - Z.WB[2]);
+            nf = 2; lbase = Z.L[1] + 2 * (gw - Z.WB[2]);
             for (int f = 0; f < 2; ++f) { uint32_t q = (v >> (16 * f)) & 0xffffu; av[f] = q & 0xffu; dv[f] = q >> 8; }
           } else if (gw < Z.WB[4]) {
-            nf = 4; fbits = 8; lbase = Z.L[2] + 4 * (gw - Z.WB[3]);
+            nf = 4; lbase = Z.L[2] + 4 * (gw - Z.WB[3]);
             for (int f = 0; f < 4; ++f) { uint32_t q = (v >> (8 * f)) & 0xffu; av[f] = q & 0xfu; dv[f] = q >> 4; }
           } else {
-            nf = 8; fbits = 4; lbase = Z.L[3] + 8 * (gw - Z.WB[4]);
+            nf = 8; lbase = Z.L[3] + 8 * (gw - Z.WB[4]);
             for (int f = 0; f < 8; ++f) { uint32_t q = (v >> (4 * f)) & 0xfu; av[f] = q & 3u; dv[f] = q >> 2; }
           }
-          (void)fbits;
           for (uint32_t f = 0; f < nf; ++f) {
             unsigned long long A = av[f], D = dv[f];
-            if (!(A | D)) continue;
             unsigned long long fb = comb2(A) + comb2(D), fn = A * D;
             if (!(fb | fn)) continue;
             xB += fb;
@@ -304,8 +318,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
         }
       }
       __syncthreads();
-      wl_lo = next_lo;
     }
+    for (uint32_t k = tid; k < K; k += kT3Threads) sh_cnt[k] = 0;
     // unit totals -> start vertex
     totB += xB;
     totN += xN;
@@ -314,10 +328,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
       if (lane == 0) { sh_red[0][warp] = b; sh_red[1][warp] = nn; }
       __syncthreads();
       if (warp == 0) {
-        b = sh_red[0][lane];
-        nn = sh_red[1][lane];
-        b = warp_sum(b);
-        nn = warp_sum(nn);
+        b = warp_sum(sh_red[0][lane]);
+        nn = warp_sum(sh_red[1][lane]);
         if (lane == 0 && (b | nn)) {
           atomicAdd(&a.pv[x], b);
           atomicAdd(&a.pv[a.n + x], nn);
@@ -484,7 +496,7 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
 template <bool PV, bool PAIRS>
 cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, Plan* p,
                           cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2) {
-  const size_t smem3 = sizeof(uint32_t) * (kWin + kBm);
+  const size_t smem3 = sizeof(uint32_t) * (kWin + kBm + 32 * 32 + kMaxWin);
   const size_t smem1 = sizeof(uint32_t) * kT1Warps * (2 * kT1Slots + 3 * 32 + 64);
   cudaError_t err;
   err = cudaFuncSetAttribute(k_t3<PV, PAIRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
@@ -512,12 +524,21 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
                            unsigned long long* cn, unsigned long long* cid,
                            unsigned long long cap, unsigned long long* n_cand) {
   cudaStream_t st = g->stream;
-  // scratch for the hub kernel's middle arrays
-  size_t need = (size_t)g->num_sms * 4 * std::max<uint32_t>(p->max_mid, 1);
+  // scratch for the hub kernel: per CTA 3 middle arrays + 4 record arrays [window][middle]
+  uint32_t kwin_cap = 1;
+  for (int s2 = 0; s2 < 2; ++s2)
+    kwin_cap = std::max<uint32_t>(kwin_cap, (g->zones[s2].WB[5] + kWin - 1) / kWin);
+  if (kwin_cap > kMaxWin) {
+    set_error("end side too large for the hub kernel's window table");
+    return BBF_ERANGE;
+  }
+  size_t mm = std::max<uint32_t>(p->max_mid, 1);
+  size_t rs = mm + p->max_work / kRecMax + 1;
+  size_t need = (size_t)g->num_sms * (3 * mm + 3 * rs * kwin_cap);
   if (need > g->scratch_words) {
-    if (g->scratch) cudaFree(g->scratch);
+    if (g->scratch) cudaFreeAsync(g->scratch, st);
     g->scratch = nullptr;
-    BBF_CUDA(cudaMalloc(&g->scratch, need * sizeof(uint32_t)));
+    BBF_CUDA(cudaMallocAsync(&g->scratch, need * sizeof(uint32_t), st));
     g->scratch_words = need;
   }
   BBF_CUDA(cudaMemsetAsync(g->d_acc, 0, 16 * sizeof(unsigned long long), st));
@@ -529,6 +550,8 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   ea.rank = rank; ea.nranks = nranks;
   ea.acc = g->d_acc; ea.pv = (unsigned long long*)g->pv; ea.scratch = g->scratch;
   ea.max_mid = std::max<uint32_t>(p->max_mid, 1);
+  ea.kwin_cap = kwin_cap;
+  ea.rec_stride = (uint32_t)(std::max<uint32_t>(p->max_mid, 1) + p->max_work / kRecMax + 1);
   ea.cb = cb; ea.cn = cn; ea.cid = cid; ea.cap = cap;
   cudaEvent_t e0, e1, e2;
   cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
@@ -551,6 +574,9 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   host_BN[0] = h[0];
   host_BN[1] = h[1];
   if (n_cand) *n_cand = h[4];
+  if (getenv("BBF_DEBUG"))
+    fprintf(stderr, "[bbf] engine: t3 %.3f ms, t1 %.3f ms, t3 entries pass1 %llu, records %llu, windows %llu\n",
+            ms1, ms2, h[5], h[6], h[7]);
   // algorithmic bytes of the hub kernel k_t3: 4 B column word per
   // visited wedge per pass (pass 2 re-reads it for per-vertex counts) + 16 B per eligible
   // middle of its starts (column word, ub, end1 of the middle's row, 4 B id-side output)

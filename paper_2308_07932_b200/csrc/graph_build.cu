@@ -140,9 +140,9 @@ __global__ void k_cuts(const uint32_t* __restrict__ off, const uint32_t* __restr
 // number of entries of the non-increasing degs[base, base+cnt) that are >= t
 __global__ void k_count_ge(const uint32_t* __restrict__ degs, uint32_t base, uint32_t cnt,
                            unsigned long long* out) {
-  const uint32_t th[5] = {65536u, 256u, 16u, 4u, 2u};
+  const uint32_t th[6] = {65536u, 256u, 16u, 4u, 2u, 33u};  // zones; 33: "long" middles (deg > 32)
   int t = threadIdx.x;
-  if (t >= 5) return;
+  if (t >= 6) return;
   uint32_t lo = 0, hi = cnt;
   while (lo < hi) {
     uint32_t mid = lo + (hi - lo) / 2;
@@ -303,8 +303,8 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   BBF_CUDA(cudaMallocAsync(&d_cnt, 16 * sizeof(unsigned long long), st));
   BBF_CUDA(cudaMemsetAsync(d_cnt, 0, 16 * sizeof(unsigned long long), st));
   k_count_ge<<<1, 32, 0, st>>>(g->degs, 0, n_u, d_cnt);
-  k_count_ge<<<1, 32, 0, st>>>(g->degs, n_u, n_v, d_cnt + 5);
-  k_ws<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(g->degs, n_u, n, d_cnt + 10);
+  k_count_ge<<<1, 32, 0, st>>>(g->degs, n_u, n_v, d_cnt + 6);
+  k_ws<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(g->degs, n_u, n, d_cnt + 12);
   g->launches += 3;
   unsigned long long h_cnt[16];
   BBF_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
@@ -317,7 +317,8 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   g->maxdeg[1] = h_maxdeg[1];
   for (int s = 0; s < 2; ++s) {
     Zones& z = g->zones[s];
-    for (int i = 0; i < 5; ++i) z.L[i] = (uint32_t)h_cnt[5 * s + i];
+    for (int i = 0; i < 5; ++i) z.L[i] = (uint32_t)h_cnt[6 * s + i];
+    g->Llong[s] = (uint32_t)h_cnt[6 * s + 5];
     z.WB[0] = 0;
     z.WB[1] = 2u * z.L[0];
     z.WB[2] = z.WB[1] + (z.L[1] - z.L[0]);
@@ -328,8 +329,8 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   }
   // B + N = sum_{u<w} C(T_uw, 2) <= (maxT - 1)/2 * sum_{u<w} T_uw = (maxdeg_U - 1)/2 * W_S(U)
   {
-    long double bu = (long double)(g->maxdeg[0] ? g->maxdeg[0] - 1 : 0) / 2.0L * (long double)h_cnt[11];
-    long double bv = (long double)(g->maxdeg[1] ? g->maxdeg[1] - 1 : 0) / 2.0L * (long double)h_cnt[10];
+    long double bu = (long double)(g->maxdeg[0] ? g->maxdeg[0] - 1 : 0) / 2.0L * (long double)h_cnt[13];
+    long double bv = (long double)(g->maxdeg[1] ? g->maxdeg[1] - 1 : 0) / 2.0L * (long double)h_cnt[12];
     g->ws_bound = std::min(bu, bv);
   }
   if (h_err & kErrDup) {

@@ -5,6 +5,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "bbf_internal.cuh"
 
@@ -126,8 +128,9 @@ struct IsT1 {
 __global__ void k_units(uint32_t n, uint32_t n_u, const uint32_t* __restrict__ nunits,
                         const uint32_t* __restrict__ ustart, const uint64_t* __restrict__ degpre,
                         uint32_t L4u, uint32_t L4v, const uint32_t* __restrict__ mid_lo,
-                        const uint32_t* __restrict__ end1, Unit* __restrict__ units,
-                        unsigned int* __restrict__ max_mid) {
+                        const uint32_t* __restrict__ end1, const uint64_t* __restrict__ work,
+                        Unit* __restrict__ units, unsigned int* __restrict__ max_mid,
+                        unsigned long long* __restrict__ max_work) {
   uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
   uint32_t k = nunits[x];
@@ -137,6 +140,7 @@ __global__ void k_units(uint32_t n, uint32_t n_u, const uint32_t* __restrict__ n
   uint32_t lx = x - sb;
   uint32_t lo = lx + 1, hi = L4 > lo ? L4 : lo;
   atomicMax(max_mid, end1[x] - mid_lo[x]);
+  atomicMax(max_work, (unsigned long long)work[x]);
   uint32_t base = ustart[x];
   // prefix over rows: P(r) = sum degs[0..r]; sum over side-local [a, b) = P(sb+b-1) - P(sb+a-1)
   auto pre = [&](uint32_t l) -> uint64_t {  // sum of degs of side-local ranks [0, l)
@@ -173,11 +177,11 @@ inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) 
 
 }  // namespace
 
-void free_plan(Plan* p) {
-  if (p->ub) cudaFree(p->ub);
-  if (p->work) cudaFree(p->work);
-  if (p->t1) cudaFree(p->t1);
-  if (p->units) cudaFree(p->units);
+void free_plan(Plan* p, cudaStream_t st) {
+  if (p->ub) cudaFreeAsync(p->ub, st);
+  if (p->work) cudaFreeAsync(p->work, st);
+  if (p->t1) cudaFreeAsync(p->t1, st);
+  if (p->units) cudaFreeAsync(p->units, st);
   *p = Plan{};
 }
 
@@ -185,7 +189,7 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   cudaStream_t st = g->stream;
   const uint32_t n = g->n;
   const uint64_t m = 2 * g->nnz;
-  free_plan(p);
+  free_plan(p, st);
   p->route = route;
   RouteRows rr{route, g->n_u, n};
   BBF_CUDA(cudaMallocAsync(&p->ub, 4ull * (m + 1), st));
@@ -272,19 +276,28 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   p->W_t3 = h_acc[1];
   p->M_t3 = h_acc[2];
   BBF_CUDA(cudaMallocAsync(&p->units, sizeof(Unit) * (h_nunits + 1), st));
-  unsigned int* d_maxmid;
-  BBF_CUDA(cudaMallocAsync(&d_maxmid, 4, st));
-  BBF_CUDA(cudaMemsetAsync(d_maxmid, 0, 4, st));
+  unsigned int* d_maxmid;  // [0] max middles, [2..3] max work (u64)
+  BBF_CUDA(cudaMallocAsync(&d_maxmid, 16, st));
+  BBF_CUDA(cudaMemsetAsync(d_maxmid, 0, 16, st));
   if (n && h_nunits) {
     k_units<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, g->n_u, nunits, ustart, g->degpre,
-                                                      g->L4[0], g->L4[1], sb, g->end1, p->units,
-                                                      d_maxmid);
+                                                      g->L4[0], g->L4[1], sb, g->end1, p->work,
+                                                      p->units, d_maxmid, (unsigned long long*)(d_maxmid + 2));
     g->launches += 1;
   }
-  unsigned int h_maxmid = 0;
-  BBF_CUDA(cudaMemcpyAsync(&h_maxmid, d_maxmid, 4, cudaMemcpyDeviceToHost, st));
+  unsigned int h_maxmid[4] = {0, 0, 0, 0};
+  BBF_CUDA(cudaMemcpyAsync(h_maxmid, d_maxmid, 16, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaStreamSynchronize(st));
-  p->max_mid = h_maxmid;
+  p->max_mid = h_maxmid[0];
+  p->max_work = *(unsigned long long*)(h_maxmid + 2);
+  if (getenv("BBF_DEBUG"))
+    fprintf(stderr,
+            "[bbf] plan route=%d W_full=%llu W_pruned=%llu W_t1=%llu (%u starts) W_t3=%llu (%u units) "
+            "M_t3=%llu max_mid=%u w_target=%llu words U=%u V=%u\n",
+            route, (unsigned long long)p->W_full, (unsigned long long)p->W_pruned,
+            (unsigned long long)p->W_t1, p->n_t1, (unsigned long long)p->W_t3, p->n_units,
+            (unsigned long long)p->M_t3, p->max_mid, (unsigned long long)w_target, g->zones[0].WB[5],
+            g->zones[1].WB[5]);
   cudaFreeAsync(len, st);
   cudaFreeAsync(sb, st);
   cudaFreeAsync(se, st);

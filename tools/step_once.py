@@ -3,6 +3,7 @@ python tools/step_once.py --config 3 [--steps 1] [--global-only]"""
 import argparse
 import os
 import sys
+import time
 
 import numpy as np
 
@@ -26,12 +27,20 @@ def main():
     outs = tuple(torch.zeros(k, dtype=torch.int64, device=dev) for k in (g.n_u, g.n_u, g.n_v, g.n_v))
     s = torch.cuda.Stream(dev)
     torch.cuda.set_stream(s)
-    for _ in range(a.steps):
-        h = bbf.Graph(g.n_u, g.n_v, rp, col, sg, stream=s)
-        r = h.count_global() if a.global_only else h.count_per_vertex(out=outs)[0]
-        print(r, h.stats(), flush=True)
-        h.free()
     torch.cuda.synchronize()
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        h = bbf.Graph(g.n_u, g.n_v, rp, col, sg, stream=s)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        r = h.count_global() if a.global_only else h.count_per_vertex(out=outs)[0]
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        st = h.stats()
+        h.free()
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
+        print(f"load {1e3*(t1-t0):.1f} ms  count {1e3*(t2-t1):.1f} ms (device {r['ms_count']:.1f}, main {st['ms_main_kernel']:.1f})  free {1e3*(t3-t2):.1f} ms", r, flush=True)
 
 
 if __name__ == "__main__":
