@@ -46,7 +46,7 @@ def test_config_shapes_and_simplicity():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg", [3, 5])
+@pytest.mark.parametrize("cfg", [3])
 def test_large_configs_match_recorded_hash(cfg):
     g = G.make_config(cfg)
     sha, n_u, n_v, nnz = golden()[cfg]
