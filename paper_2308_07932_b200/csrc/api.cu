@@ -257,7 +257,8 @@ bbf_status bbf_graph_free(bbf_graph* g) {
   free_plan(&g->plan_g, g->stream);
   free_plan(&g->plan_s[0], g->stream);
   free_plan(&g->plan_s[1], g->stream);
-  void* ptrs[] = {g->off, g->adj, g->mid, g->end1, g->inv, g->degs, g->degpre, g->scratch, g->d_acc, g->pv};
+  void* ptrs[] = {g->off, g->adj, g->mid, g->end1, g->inv, g->degs, g->degpre, g->scratch, g->d_acc, g->pv,
+                  g->adjc, g->runid, g->runs};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, g->stream);
   cudaStreamSynchronize(g->stream);

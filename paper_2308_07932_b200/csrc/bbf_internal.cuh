@@ -120,6 +120,26 @@ __host__ __device__ inline uint32_t word_of_l(const Zones& z, uint32_t l) {
   return z.WB[4] + ((l - z.L[3]) >> 3);
 }
 
+// ---------------------------------------------------------------------------- counter address
+// adjc[e] encodes, for the end vertex y of adjacency entry e, where its (a, d) field lives in
+// the zoned counter layout of y's side, so the hub kernel never evaluates the zone chain per
+// wedge:  bits 0-22 base word g, 23-27 bit shift, 28-29 width code (field 4/8/16/32 bits),
+// 30 wide (zone 0: a in word g, d in word g+1), 31 negative sign (as in adj).
+constexpr uint32_t kCWordBits = 23;
+constexpr uint32_t kCWordMask = (1u << kCWordBits) - 1u;
+constexpr uint32_t kWin = 48 * 1024;  // counter words per hub-kernel window (192 KB of smem)
+
+__host__ __device__ inline uint32_t encode_caddr(const Zones& z, uint32_t l) {
+  uint32_t g, sh = 0, wc = 0, wide = 0;
+  if (l < z.L[0]) { g = 2u * l; wide = 1; }
+  else if (l < z.L[1]) { g = z.WB[1] + (l - z.L[0]); wc = 3; }
+  else if (l < z.L[2]) { uint32_t i = l - z.L[1]; g = z.WB[2] + (i >> 1); sh = (i & 1u) << 4; wc = 2; }
+  else if (l < z.L[3]) { uint32_t i = l - z.L[2]; g = z.WB[3] + (i >> 2); sh = (i & 3u) << 3; wc = 1; }
+  else if (l < z.L[4]) { uint32_t i = l - z.L[3]; g = z.WB[4] + (i >> 3); sh = (i & 7u) << 2; wc = 0; }
+  else { g = 0; }  // degree <= 1: never counted
+  return (g & kCWordMask) | (sh << 23) | (wc << 28) | (wide << 30);
+}
+
 __host__ __device__ inline unsigned long long comb2(unsigned long long x) {
   return x ? x * (x - 1ull) / 2ull : 0ull;
 }
@@ -175,6 +195,10 @@ struct bbf_graph {
   uint32_t* degs;     // n   : degree by row (rank order, per side non-increasing)
   uint64_t* degpre;   // n+2 : per side inclusive prefix of degrees over rows (side-local, see plan)
   bbf::Zones zones[2];
+  uint32_t* adjc;     // 2*nnz counter addresses of the end vertex (+ sign bit), see encode_caddr
+  uint32_t* runid;    // 2*nnz: index of the window run containing the entry
+  uint2* runs;        // nruns: {first entry, window id} of every maximal same-window run of a row
+  uint32_t nruns;
   uint32_t L4[2];     // #vertices with degree >= 2 per side
   uint32_t Llong[2];  // #vertices with degree > 32 per side ("long" middles of the hub kernel)
   uint32_t maxdeg[2];

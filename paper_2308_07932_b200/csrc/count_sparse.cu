@@ -30,7 +30,6 @@ namespace bbf {
 namespace {
 
 constexpr int kT3Threads = 1024;
-constexpr uint32_t kWin = 48 * 1024;  // counter words per CTA window (192 KB)
 constexpr uint32_t kBm = kWin / 32;   // bitmap words
 constexpr int kT1Warps = 12;
 constexpr uint32_t kT1Slots = 1024;
@@ -38,6 +37,10 @@ constexpr uint32_t kT1Slots = 1024;
 struct EngineArgs {
   const uint32_t* off;
   const uint32_t* adj;
+  const uint32_t* adjc;
+  const uint32_t* runid;
+  const uint2* runs;
+  uint32_t nruns;
   const uint32_t* mid;   // route G middle start; nullptr for route S (off used)
   const uint32_t* end1;
   const uint32_t* ub;
@@ -82,16 +85,19 @@ __device__ __forceinline__ void emit_pair(const EngineArgs& a, uint32_t x, uint3
 // ===================================================================================== T3
 // One CTA per unit (start x, end-rank range).  The end ranks of x's side are cut into a fixed
 // grid of windows of kWin counter words (degree-zoned fields, bbf_internal.cuh).
-//   pre-scan : warps walk each middle's segment once (coalesced) and record every maximal run
-//              of entries that falls into one window ("segment record": middle, start, length),
-//              bucketed by window;
+//   pre-scan : warps take batches of 32 middles (one coalesced header load), walk every
+//              middle's segment once and emit a "segment record" {adj position, length,
+//              middle word} for every maximal run of entries inside one window (runs are split
+//              every kRecMax entries), bucketed by window;
 //   per window (only windows that received records):
-//     scan   : block-wide prefix of the window's record lengths;
-//     pass 1 : 256-entry chunks of the flattened window pulled by warps; each lane finds its
-//              record with a ballot/popc load-balanced search; one shared atomic per wedge;
-//     pass 2 : (per-vertex) the same chunks read the final (a, d) of each end: middle shares;
-//     epilogue: Lemma 2 per touched word (bitmap), clear.
+//     pass 1 : batches of 32 records per warp; one shared atomic per wedge;
+//     pass 2 : (per-vertex) the same batches read the final (a, d) of each end: middle shares;
+//     epilogue: Lemma 2 per touched counter word (bitmap), clear.
+// Inside a batch, items longer than kFlatMax entries are walked by the whole warp (128 entries
+// in flight); shorter ones are flattened across the lanes (ballot / __fns load balancing), so
+// short middles and records keep every lane busy.
 constexpr uint32_t kRecMax = 1024;
+constexpr uint32_t kFlatMax = 64;
 constexpr uint32_t kMaxWin = 256;
 
 __device__ __forceinline__ void t3_inc(const Zones& Z, uint32_t* ctr, uint32_t* bm, uint32_t word0,
@@ -103,41 +109,87 @@ __device__ __forceinline__ void t3_inc(const Zones& Z, uint32_t* ctr, uint32_t* 
 }
 
 __device__ __forceinline__ void mid_share(const Zones& Z, const uint32_t* ctr, uint32_t word0,
-                                          uint32_t ev, uint32_t wv, unsigned long long& b,
-                                          unsigned long long& nn) {
+                                          uint32_t ev, uint32_t wv, uint32_t& b, uint32_t& nn) {
   uint32_t ad, dd;
   field_read(Z, ctr, word0, ev & kMask, ad, dd);
   if (((ev ^ wv) >> 31) == 0) { b += ad - 1; nn += dd; }   // symmetric: (a-1, d)
   else { b += dd - 1; nn += ad; }                            // asymmetric: (d-1, a)
 }
 
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// Flattened-step owner lookup: lanes hold items (len, excl = exclusive prefix); for flattened
+// index f = base + lane returns the lane that owns f.  nz = ballot(len > 0).
+__device__ __forceinline__ int flat_owner(uint32_t len, uint32_t excl, uint32_t nz, uint32_t base,
+                                          int lane) {
+  const uint32_t bit = (len > 0 && excl >= base && excl < base + 32) ? (1u << (excl - base)) : 0u;
+  const uint32_t smask = __reduce_or_sync(0xffffffffu, bit);
+  const uint32_t before = __popc(__ballot_sync(0xffffffffu, len > 0 && excl < base));
+  const int rank = (int)(before + __popc(smask & ((2u << lane) - 1u))) - 1;
+  return rank >= 0 ? (int)__fns(nz, 0, rank + 1) : 0;
+}
+
+// one wedge: ev = adjc entry of the end (counter address + sign), wv = middle's adj word
+__device__ __forceinline__ void t3_inc_c(uint32_t* ctr, uint32_t* bm, uint32_t word0, uint32_t ev,
+                                         uint32_t wv) {
+  const uint32_t g = (ev & kCWordMask) - word0;
+  const uint32_t cls = (ev ^ wv) >> 31;        // 0 symmetric (a), 1 asymmetric (d)
+  const uint32_t sh = (ev >> 23) & 31u, wc = (ev >> 28) & 3u, wide = (ev >> 30) & 1u;
+  const uint32_t word = g + (wide & cls);
+  const uint32_t inc = 1u << (sh + ((cls & (wide ^ 1u)) << (wc + 1u)));
+  const uint32_t prev = atomicAdd(&ctr[word], inc);
+  if (prev == 0) atomicOr(&bm[g >> 5], 1u << (g & 31));
+}
+
+__device__ __forceinline__ void t3_share_c(const uint32_t* ctr, uint32_t word0, uint32_t ev,
+                                           uint32_t wv, uint32_t& b, uint32_t& nn) {
+  const uint32_t g = (ev & kCWordMask) - word0;
+  uint32_t ad, dd;
+  if ((ev >> 30) & 1u) {
+    ad = ctr[g];
+    dd = ctr[g + 1];
+  } else {
+    const uint32_t sh = (ev >> 23) & 31u, half = 2u << ((ev >> 28) & 3u);
+    const uint32_t v = ctr[g] >> sh;
+    const uint32_t msk = (half == 16u) ? 0xffffu : ((1u << half) - 1u);
+    ad = v & msk;
+    dd = (v >> half) & msk;
+  }
+  if (((ev ^ wv) >> 31) == 0) { b += ad - 1; nn += dd; }   // symmetric: (a-1, d)
+  else { b += dd - 1; nn += ad; }                            // asymmetric: (d-1, a)
+}
+
+struct Rec {  // 16 B segment record
+  uint32_t p, len, wv, pad;
+};
+
 template <bool PV, bool PAIRS>
 __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
-  using BlockScan = cub::BlockScan<uint32_t, kT3Threads>;
   extern __shared__ uint32_t smem[];
   uint32_t* ctr = smem;                   // kWin
   uint32_t* bm = smem + kWin;             // kBm
-  uint32_t* flag = bm + kBm;              // 32 warps x 32
-  uint32_t* sh_cnt = flag + 32 * 32;      // kMaxWin record counts
-  __shared__ typename BlockScan::TempStorage scan_tmp;
-  __shared__ uint32_t sh_unit, sh_run, sh_c[4];
+  uint32_t* sh_cnt = bm + kBm;            // kMaxWin record counts
+  __shared__ uint32_t sh_unit, sh_c[4];
+  __shared__ uint32_t sh_acc[32][2][32];  // per-warp pass-2 accumulators of a batch
   __shared__ unsigned long long sh_red[2][32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t* wflag = flag + warp * 32;
 
-  for (uint32_t i = tid; i < kWin + kBm + 32 * 32 + kMaxWin; i += kT3Threads) smem[i] = 0;
-  const size_t M = a.max_mid, RS = a.rec_stride, RC = RS * a.kwin_cap;
-  uint32_t* Sw = a.scratch + (size_t)blockIdx.x * (3 * M + 3 * RC);
-  uint32_t* Scur = Sw + M;
-  uint32_t* Send = Scur + M;
-  uint32_t* Ri = Send + M;       // [window][slot] middle index
-  uint32_t* Rp = Ri + RC;        // start position in adj
-  uint32_t* Rl = Rp + RC;        // length
+  for (uint32_t i = tid; i < kWin + kBm + kMaxWin; i += kT3Threads) smem[i] = 0;
+  const size_t RS = a.rec_stride;
+  Rec* R = reinterpret_cast<Rec*>(a.scratch) + (size_t)blockIdx.x * RS * a.kwin_cap;
   unsigned long long totB = 0, totN = 0;
   __syncthreads();
 
   while (true) {
     if (tid == 0) sh_unit = (uint32_t)atomicAdd(&a.acc[2], 1ull);
+    if (tid < 4) sh_c[tid] = 0;
     __syncthreads();
     const uint64_t ui = (uint64_t)sh_unit * a.nranks + a.rank;
     if (ui >= a.n_units) break;
@@ -149,72 +201,63 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
     const uint32_t K = (Z.WB[5] + kWin - 1) / kWin;
     const uint32_t m_lo = a.mid ? a.mid[x] : a.off[x];
     const uint32_t m = a.end1[x] - m_lo;
-    if (tid < 4) sh_c[tid] = 0;
-    // ---- unit setup: middle words and segments [first end >= u.lo, first end >= u.hi)
-    for (uint32_t i = tid; i < m; i += kT3Threads) {
-      uint32_t e = m_lo + i;
-      uint32_t wv = a.adj[e];
-      uint32_t rv = ob + (wv & kMask);
-      uint32_t s = a.ub[e], en = a.end1[rv];
-      if (u.lo > lx + 1 && s < en) {
-        uint32_t b = s, f = en;
-        while (b < f) {
-          uint32_t md = b + (f - b) / 2;
-          if ((a.adj[md] & kMask) < u.lo) b = md + 1; else f = md;
-        }
-        s = b;
-      }
-      if (u.hi < Z.L[4] && s < en) {
-        uint32_t b = s, f = en;
-        while (b < f) {
-          uint32_t md = b + (f - b) / 2;
-          if ((a.adj[md] & kMask) < u.hi) b = md + 1; else f = md;
-        }
-        en = b;
-      }
-      Sw[i] = wv;
-      Scur[i] = s;
-      Send[i] = en;
-    }
-    __syncthreads();
-    // ---- pre-scan: per-window segment records (warp per middle, middles pulled dynamically)
+    const bool split_lo = u.lo > lx + 1, split_hi = u.hi < Z.L[4];
+
+    // ---------------- pre-scan: segment records per window
     while (true) {
-      uint32_t i = 0;
-      if (lane == 0) i = atomicAdd(&sh_c[0], 1u);
-      i = __shfl_sync(0xffffffffu, i, 0);
-      if (i >= m) break;
-      const uint32_t s = Scur[i], e = Send[i];
-      if (s >= e) continue;
-      uint32_t open_k = 0xffffffffu, open_slot = 0, open_p = 0, carry_k = 0xfffffffeu;
-      for (uint32_t pos = s; pos < e; pos += 32) {
-        const uint32_t p = pos + lane;
-        const bool valid = p < e;
-        const uint32_t k = valid ? word_of_l(Z, a.adj[p] & kMask) / kWin : 0xffffffffu;
-        uint32_t kprev = __shfl_up_sync(0xffffffffu, k, 1);
-        if (lane == 0) kprev = carry_k;
-        // a record also restarts every kRecMax entries (p - s is a multiple of kRecMax), so no
-        // record is longer than kRecMax and warps stay balanced inside a window
-        const bool is_start = valid && (k != kprev || ((p - s) % kRecMax) == 0);
-        const uint32_t smask = __ballot_sync(0xffffffffu, is_start);
-        if (smask && open_k != 0xffffffffu && lane == 0)
-          Rl[(size_t)open_k * RS + open_slot] = pos + (__ffs(smask) - 1) - open_p;
-        uint32_t slot = 0;
-        if (is_start) {
-          slot = atomicAdd(&sh_cnt[k], 1u);
-          Ri[(size_t)k * RS + slot] = i;
-          Rp[(size_t)k * RS + slot] = p;
-          const uint32_t later = smask & ~((2u << lane) - 1u);
-          if (later) Rl[(size_t)k * RS + slot] = (__ffs(later) - 1) - lane;
+      uint32_t bt = 0;
+      if (lane == 0) bt = atomicAdd(&sh_c[0], 1u);
+      bt = __shfl_sync(0xffffffffu, bt, 0);
+      if (bt * 32 >= m) break;
+      const uint32_t i = bt * 32 + lane;
+      uint32_t wv = 0, s = 0, en = 0;
+      if (i < m) {
+        const uint32_t e = m_lo + i;
+        wv = a.adj[e];
+        s = a.ub[e];
+        en = a.end1[ob + (wv & kMask)];
+        if (split_lo && s < en) {
+          uint32_t b = s, f = en;
+          while (b < f) {
+            uint32_t md = b + (f - b) / 2;
+            if ((a.adj[md] & kMask) < u.lo) b = md + 1; else f = md;
+          }
+          s = b;
         }
-        if (smask) {  // the last start of this step stays open
-          const int last = 31 - __clz(smask);
-          open_k = __shfl_sync(0xffffffffu, k, last);
-          open_slot = __shfl_sync(0xffffffffu, slot, last);
-          open_p = pos + last;
+        if (split_hi && s < en) {
+          uint32_t b = s, f = en;
+          while (b < f) {
+            uint32_t md = b + (f - b) / 2;
+            if ((a.adj[md] & kMask) < u.hi) b = md + 1; else f = md;
+          }
+          en = b;
         }
-        carry_k = __shfl_sync(0xffffffffu, k, 31);
       }
-      if (lane == 0 && open_k != 0xffffffffu) Rl[(size_t)open_k * RS + open_slot] = e - open_p;
+      // records of this middle = the graph's window runs of row v clipped to [s, en)
+      const uint32_t r0 = s < en ? a.runid[s] : 0;
+      const uint32_t nr = s < en ? a.runid[en - 1] - r0 + 1 : 0;
+      const uint32_t incl = warp_incl_scan(nr, lane), excl = incl - nr;
+      const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t nz = __ballot_sync(0xffffffffu, nr > 0);
+      for (uint32_t base = 0; base < T; base += 32) {
+        const int ow = flat_owner(nr, excl, nz, base, lane);
+        const uint32_t f = base + lane;
+        const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, ow);
+        const uint32_t o_r0 = __shfl_sync(0xffffffffu, r0, ow);
+        const uint32_t o_s = __shfl_sync(0xffffffffu, s, ow);
+        const uint32_t o_en = __shfl_sync(0xffffffffu, en, ow);
+        const uint32_t o_wv = __shfl_sync(0xffffffffu, wv, ow);
+        if (f < T) {
+          const uint32_t r = o_r0 + (f - o_excl);
+          const uint2 run = a.runs[r];
+          const uint32_t rs = max(run.x, o_s);
+          const uint32_t re = (r + 1 < a.nruns) ? min(a.runs[r + 1].x, o_en) : o_en;
+          for (uint32_t p = rs; p < re; p += kRecMax) {
+            const uint32_t slot = atomicAdd(&sh_cnt[run.y], 1u);
+            R[(size_t)run.y * RS + slot] = Rec{p, min(kRecMax, re - p), o_wv, 0u};
+          }
+        }
+      }
     }
     __syncthreads();
     unsigned long long xB = 0, xN = 0;
@@ -223,49 +266,82 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
       const uint32_t nrec = sh_cnt[k];
       if (nrec == 0) continue;
       const uint32_t word0 = k * kWin;
-      const uint32_t* ri = Ri + (size_t)k * RS;
-      const uint32_t* rp = Rp + (size_t)k * RS;
-      const uint32_t* rl = Rl + (size_t)k * RS;
+      const Rec* rw = R + (size_t)k * RS;
       if (tid < 4) sh_c[tid] = 0;
       if (tid == 0) { atomicAdd(&a.acc[6], (unsigned long long)nrec); atomicAdd(&a.acc[7], 1ull); }
       __syncthreads();
-      // ---------------- pass 1 (Alg. 2 lines 9-14) and pass 2 (per-vertex shares):
-      // one warp per segment record (records are <= kRecMax entries), pulled dynamically
+      // ---------------- pass 1 (Alg. 2 lines 9-14) and pass 2 (per-vertex shares)
 #pragma unroll 1
       for (int pass = 0; pass < (PV ? 2 : 1); ++pass) {
         while (true) {
-          uint32_t r = 0;
-          if (lane == 0) r = atomicAdd(&sh_c[pass], 1u);
-          r = __shfl_sync(0xffffffffu, r, 0);
-          if (r >= nrec) break;
-          const uint32_t i = ri[r], p0 = rp[r], len = rl[r];
-          const uint32_t wv = Sw[i];
-          if (pass == 0) {
-            for (uint32_t o = lane; o < len; o += 128) {
+          uint32_t bt = 0;
+          if (lane == 0) bt = atomicAdd(&sh_c[pass], 1u);
+          bt = __shfl_sync(0xffffffffu, bt, 0);
+          if (bt * 32 >= nrec) break;
+          const uint32_t r = bt * 32 + lane;
+          Rec rc{0, 0, 0, 0};
+          if (r < nrec) rc = rw[r];
+          const bool lng = rc.len > kFlatMax;
+          if (pass == 1) { sh_acc[warp][0][lane] = 0; sh_acc[warp][1][lane] = 0; __syncwarp(); }
+          // -- short records flattened over the lanes
+          {
+            const uint32_t fl = lng ? 0 : rc.len;
+            const uint32_t incl = warp_incl_scan(fl, lane), excl = incl - fl;
+            const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
+            const uint32_t nz = __ballot_sync(0xffffffffu, fl > 0);
+            for (uint32_t base = 0; base < T; base += 32) {
+              const int ow = flat_owner(fl, excl, nz, base, lane);
+              const uint32_t f = base + lane;
+              const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, ow);
+              const uint32_t o_p = __shfl_sync(0xffffffffu, rc.p, ow);
+              const uint32_t o_wv = __shfl_sync(0xffffffffu, rc.wv, ow);
+              if (f < T) {
+                const uint32_t ev = a.adjc[o_p + (f - o_excl)];
+                if (pass == 0) {
+                  t3_inc_c(ctr, bm, word0, ev, o_wv);
+                } else {
+                  uint32_t cb = 0, cn = 0;
+                  t3_share_c(ctr, word0, ev, o_wv, cb, cn);
+                  if (cb) atomicAdd(&sh_acc[warp][0][ow], cb);
+                  if (cn) atomicAdd(&sh_acc[warp][1][ow], cn);
+                }
+              }
+            }
+          }
+          // -- long records over the whole warp, 128 entries in flight
+          uint32_t lmask = __ballot_sync(0xffffffffu, lng);
+          while (lmask) {
+            const int j = __ffs(lmask) - 1;
+            lmask &= lmask - 1;
+            const uint32_t jp = __shfl_sync(0xffffffffu, rc.p, j), jl = __shfl_sync(0xffffffffu, rc.len, j);
+            const uint32_t jw = __shfl_sync(0xffffffffu, rc.wv, j);
+            uint32_t cb = 0, cn = 0;
+            for (uint32_t o = lane; o < jl; o += 128) {
               uint32_t ev[4];
 #pragma unroll
-              for (int q = 0; q < 4; ++q) ev[q] = (o + 32 * q < len) ? a.adj[p0 + o + 32 * q] : 0u;
+              for (int q = 0; q < 4; ++q) ev[q] = (o + 32 * q < jl) ? a.adjc[jp + o + 32 * q] : 0u;
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
-                if (o + 32 * q < len) t3_inc(Z, ctr, bm, word0, ev[q] & kMask, (ev[q] ^ wv) >> 31);
+              for (int q = 0; q < 4; ++q) {
+                if (o + 32 * q < jl) {
+                  if (pass == 0) t3_inc_c(ctr, bm, word0, ev[q], jw);
+                  else t3_share_c(ctr, word0, ev[q], jw, cb, cn);
+                }
+              }
             }
-          } else {
-            unsigned long long cb = 0, cn = 0;
-            for (uint32_t o = lane; o < len; o += 128) {
-              uint32_t ev[4];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) ev[q] = (o + 32 * q < len) ? a.adj[p0 + o + 32 * q] : 0u;
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                if (o + 32 * q < len) mid_share(Z, ctr, word0, ev[q], wv, cb, cn);
+            if (pass == 1) {
+              if (cb) atomicAdd(&sh_acc[warp][0][j], cb);
+              if (cn) atomicAdd(&sh_acc[warp][1][j], cn);
             }
-            cb = warp_sum(cb);
-            cn = warp_sum(cn);
-            if (lane == 0 && (cb | cn)) {
-              const uint32_t vr = ob + (wv & kMask);
-              atomicAdd(&a.pv[vr], cb);
-              atomicAdd(&a.pv[a.n + vr], cn);
+          }
+          if (pass == 1) {
+            __syncwarp();
+            const uint32_t cb = sh_acc[warp][0][lane], cn = sh_acc[warp][1][lane];
+            if (cb | cn) {
+              const uint32_t vr = ob + (rc.wv & kMask);
+              atomicAdd(&a.pv[vr], (unsigned long long)cb);
+              atomicAdd(&a.pv[a.n + vr], (unsigned long long)cn);
             }
+            __syncwarp();
           }
         }
         __syncthreads();
@@ -496,7 +572,7 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
 template <bool PV, bool PAIRS>
 cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, Plan* p,
                           cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2) {
-  const size_t smem3 = sizeof(uint32_t) * (kWin + kBm + 32 * 32 + kMaxWin);
+  const size_t smem3 = sizeof(uint32_t) * (kWin + kBm + kMaxWin);
   const size_t smem1 = sizeof(uint32_t) * kT1Warps * (2 * kT1Slots + 3 * 32 + 64);
   cudaError_t err;
   err = cudaFuncSetAttribute(k_t3<PV, PAIRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
@@ -534,7 +610,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   }
   size_t mm = std::max<uint32_t>(p->max_mid, 1);
   size_t rs = mm + p->max_work / kRecMax + 1;
-  size_t need = (size_t)g->num_sms * (3 * mm + 3 * rs * kwin_cap);
+  size_t need = (size_t)g->num_sms * 4 * rs * kwin_cap;  // 16-B records [window][slot]
   if (need > g->scratch_words) {
     if (g->scratch) cudaFreeAsync(g->scratch, st);
     g->scratch = nullptr;
@@ -543,7 +619,8 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   }
   BBF_CUDA(cudaMemsetAsync(g->d_acc, 0, 16 * sizeof(unsigned long long), st));
   EngineArgs ea{};
-  ea.off = g->off; ea.adj = g->adj; ea.mid = p->route == 0 ? g->mid : nullptr; ea.end1 = g->end1;
+  ea.off = g->off; ea.adj = g->adj; ea.adjc = g->adjc; ea.runid = g->runid; ea.runs = g->runs;
+  ea.nruns = g->nruns; ea.mid = p->route == 0 ? g->mid : nullptr; ea.end1 = g->end1;
   ea.ub = p->ub; ea.work = p->work; ea.inv = g->inv; ea.t1 = p->t1; ea.units = p->units;
   ea.n_t1 = p->n_t1; ea.n_units = p->n_units; ea.n_u = g->n_u; ea.n = g->n;
   ea.z[0] = g->zones[0]; ea.z[1] = g->zones[1];

@@ -174,6 +174,42 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint32_t n, uint64_
   if (i < n) b[i] = a[i];
 }
 
+// counter address of each entry's end vertex (entries [0, nnz) are U rows -> V ends)
+__global__ void k_caddr(const uint32_t* __restrict__ adj, uint64_t m, uint64_t nnz, Zones zu, Zones zv,
+                        uint32_t* __restrict__ adjc) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t w = adj[e];
+    const Zones& z = e < nnz ? zv : zu;
+    adjc[e] = encode_caddr(z, w & kMask) | (w & kNegBit);
+  }
+}
+
+__global__ void k_row_starts(const uint32_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ flag) {
+  uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < n && off[x + 1] > off[x]) flag[off[x]] = 1u;
+}
+
+// entry e starts a run if it starts its row (flag preset) or its window differs from e-1's
+__global__ void k_run_flags(const uint32_t* __restrict__ adjc, uint64_t m, uint32_t* __restrict__ flag) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    if (flag[e]) continue;
+    uint32_t k = (adjc[e] & kCWordMask) / kWin, kp = (adjc[e - 1] & kCWordMask) / kWin;
+    flag[e] = k != kp ? 1u : 0u;
+  }
+}
+
+__global__ void k_runs(const uint32_t* __restrict__ adjc, const uint32_t* __restrict__ flag,
+                       uint64_t m, uint32_t* __restrict__ runid, uint2* __restrict__ runs) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t r = runid[e] - 1u;  // inclusive scan -> 0-based run index
+    runid[e] = r;
+    if (flag[e]) runs[r] = make_uint2((uint32_t)e, (adjc[e] & kCWordMask) / kWin);
+  }
+}
+
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {
   uint64_t g = (n + block - 1) / block;
   if (g == 0) g = 1;
@@ -353,6 +389,37 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp, t5, d64, g->degpre, (int)n, st));
     g->launches += 3;
     cudaFreeAsync(d64, st);
+  }
+  // hub-kernel counter addresses and window runs (DESIGN.md §"Counter windows")
+  for (int s2 = 0; s2 < 2; ++s2)
+    if (g->zones[s2].WB[5] > kCWordMask) {
+      set_error("too many counter words on one side for the hub kernel's 23-bit address");
+      return BBF_ERANGE;
+    }
+  BBF_CUDA(cudaMallocAsync(&g->adjc, 4ull * (m + 1), st));
+  BBF_CUDA(cudaMallocAsync(&g->runid, 4ull * (m + 1), st));
+  g->nruns = 0;
+  if (m) {
+    uint32_t* flag;
+    BBF_CUDA(cudaMallocAsync(&flag, 4ull * (m + 1), st));
+    BBF_CUDA(cudaMemsetAsync(flag, 0, 4ull * (m + 1), st));
+    k_caddr<<<grid_for(m, 256), 256, 0, st>>>(g->adj, m, nnz, g->zones[0], g->zones[1], g->adjc);
+    k_row_starts<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(g->off, n, flag);
+    k_run_flags<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, m, flag);
+    size_t ts = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, ts, flag, g->runid, (int64_t)m, st);
+    void* tmp2;
+    BBF_CUDA(cudaMallocAsync(&tmp2, ts + 16, st));
+    BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp2, ts, flag, g->runid, (int64_t)m, st));
+    BBF_CUDA(cudaMemcpyAsync(&g->nruns, g->runid + (m - 1), 4, cudaMemcpyDeviceToHost, st));
+    BBF_CUDA(cudaStreamSynchronize(st));
+    BBF_CUDA(cudaMallocAsync(&g->runs, sizeof(uint2) * (g->nruns + 1), st));
+    k_runs<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, flag, m, g->runid, g->runs);
+    g->launches += 6;
+    cudaFreeAsync(tmp2, st);
+    cudaFreeAsync(flag, st);
+  } else {
+    BBF_CUDA(cudaMallocAsync(&g->runs, sizeof(uint2), st));
   }
   cudaFreeAsync(tmp, st);
   cleanup_input();
