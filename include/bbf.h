@@ -102,7 +102,10 @@ bbf_status bbf_comm_free(bbf_comm *comm);
  *   row_ptr   : n_u+1 entries, row_ptr[0] == 0, non-decreasing, row_ptr[n_u] = nnz < 2^31.
  *   col       : nnz V-side indices (< n_v), any order within a row, no duplicate (u,v).
  *   sign      : nnz bytes, 1 = positive, 0 = negative.
- *   flags     : BBF_PTR_DEVICE if the three arrays are device pointers on `device`.
+ *   flags     : BBF_PTR_DEVICE if the three arrays are device pointers on `device`;
+ *               BBF_FORCE_SPARSE or BBF_FORCE_DENSE (exclusive) fix the path every count on this
+ *               handle uses unless the count call passes its own (default: the dispatch rule
+ *               of DESIGN.md §6 picks the faster path; both give bit-identical results).
  *   device    : CUDA device ordinal.  cuda_stream: cudaStream_t to order work on (NULL =
  *               the library creates its own stream).  comm: NULL for a single GPU.
  * Errors: BBF_EINVAL, BBF_ERANGE, BBF_EDUP, BBF_ENOMEM, BBF_ECUDA. */
@@ -111,7 +114,9 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t *row_pt
                               int device, void *cuda_stream, bbf_comm *comm, bbf_graph **out);
 bbf_status bbf_graph_free(bbf_graph *g);
 
-/* Global balanced / unbalanced counts (each butterfly once; Alg. 2).  out: host. */
+/* Global balanced / unbalanced counts (each butterfly once; Alg. 2).  out: host.  Path: the
+ * load flags' BBF_FORCE_* if any, else the dispatch rule.  BBF_EINVAL if BBF_FORCE_DENSE was
+ * given for a graph the dense path does not support (other side > 65,536 vertices). */
 bbf_status bbf_count_global(bbf_graph *g, bbf_counts *out);
 
 /* Per-vertex counts (butterflies containing each vertex; vBBFC semantics),
@@ -125,11 +130,14 @@ bbf_status bbf_count_per_vertex(bbf_graph *g, uint64_t *bal_u, uint64_t *unb_u, 
 bbf_status bbf_count_pairs_topk(bbf_graph *g, int side, uint32_t k, bbf_pair *out,
                                 uint32_t *n_out, uint32_t flags);
 
-/* Introspection for tests and the bench (no effect on results).  Returns the number of
- * GPU kernels the library launched on this handle since load, and the algorithmic byte
- * count of the last count call's wedge-aggregation kernels. */
+/* Introspection for tests and the bench (no effect on results).  kernel_launches: GPU kernels the
+ * library launched on this handle since load.  For the last count call's main kernel (the hub
+ * wedge-aggregation kernel k_t3 on the sparse path, k_dense_tiles on the dense path):
+ * algo_bytes = algorithmic bytes (sparse path; 0 on the dense path), algo_ops = algorithmic
+ * int8 tensor ops (dense path; 0 on the sparse path), ms_main_kernel = its device time
+ * (DESIGN.md §5).  Any pointer may be NULL. */
 bbf_status bbf_graph_stats(bbf_graph *g, uint64_t *kernel_launches, uint64_t *algo_bytes,
-                           float *ms_main_kernel);
+                           double *algo_ops, float *ms_main_kernel);
 
 #ifdef __cplusplus
 }

@@ -61,7 +61,7 @@ def lib():
         L.bbf_count_global.argtypes = [P, P]
         L.bbf_count_per_vertex.argtypes = [P, P, P, P, P, u32, P]
         L.bbf_count_pairs_topk.argtypes = [P, i32, u32, P, P, u32]
-        L.bbf_graph_stats.argtypes = [P, P, P, P]
+        L.bbf_graph_stats.argtypes = [P, P, P, P, P]
         for f in ("bbf_nccl_unique_id", "bbf_comm_init", "bbf_comm_free", "bbf_graph_load_csr",
                   "bbf_graph_free", "bbf_count_global", "bbf_count_per_vertex",
                   "bbf_count_pairs_topk", "bbf_graph_stats"):
@@ -190,9 +190,11 @@ class Graph:
 
     def stats(self) -> dict:
         L, B = C.c_uint64(), C.c_uint64()
+        ops = C.c_double()
         ms = C.c_float()
-        _check(lib().bbf_graph_stats(self.h, C.byref(L), C.byref(B), C.byref(ms)))
-        return dict(kernel_launches=L.value, algo_bytes=B.value, ms_main_kernel=ms.value)
+        _check(lib().bbf_graph_stats(self.h, C.byref(L), C.byref(B), C.byref(ops), C.byref(ms)))
+        return dict(kernel_launches=L.value, algo_bytes=B.value, algo_ops=ops.value,
+                    ms_main_kernel=ms.value)
 
 
 # ABI-named aliases (same names as include/bbf.h)

@@ -113,10 +113,10 @@ bbf_status ensure_plan_g(bbf_graph* g) {
 }
 
 // dense (tcgen05) vs sparse dispatch
-bool use_dense(bbf_graph* g, uint32_t flags) {
+bool use_dense(bbf_graph* g, uint32_t flags, bool per_vertex) {
   if (flags & BBF_FORCE_SPARSE) return false;
   if (flags & BBF_FORCE_DENSE) return true;
-  return dense_supported(g);
+  return dense_preferred(g, per_vertex);
 }
 
 bbf_status do_count(bbf_graph* g, bool per_vertex, uint32_t flags, unsigned long long* BN,
@@ -128,16 +128,16 @@ bbf_status do_count(bbf_graph* g, bool per_vertex, uint32_t flags, unsigned long
   cudaEventCreate(&b);
   cudaEventRecord(a, g->stream);
   if (per_vertex) BBF_CUDA(cudaMemsetAsync(g->pv, 0, 16ull * g->n, g->stream));
-  bbf_status s;
-  if (use_dense(g, flags)) {
+  bbf_status s = ensure_plan_g(g);  // W_G of the graph (and the sparse plan) either way
+  if (s != BBF_OK) { cudaEventDestroy(a); cudaEventDestroy(b); return s; }
+  if (use_dense(g, flags, per_vertex)) {
     if (!dense_supported(g)) {
       set_error("BBF_FORCE_DENSE: graph not supported by the dense int8 path");
       return BBF_EINVAL;
     }
     s = run_dense(g, per_vertex, rank, nranks, BN);
   } else {
-    s = ensure_plan_g(g);
-    if (s == BBF_OK) s = run_sparse(g, &g->plan_g, per_vertex, rank, nranks, BN);
+    s = run_sparse(g, &g->plan_g, per_vertex, rank, nranks, BN);
   }
   if (s != BBF_OK) { cudaEventDestroy(a); cudaEventDestroy(b); return s; }
   if (g->comm && g->comm->nranks > 1) {
@@ -205,6 +205,10 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_pt
     set_error("unknown flags");
     return BBF_EINVAL;
   }
+  if ((flags & BBF_FORCE_SPARSE) && (flags & BBF_FORCE_DENSE)) {
+    set_error("BBF_FORCE_SPARSE and BBF_FORCE_DENSE are exclusive");
+    return BBF_EINVAL;
+  }
   if ((uint64_t)n_u + n_v >= (1ull << 31)) { set_error("n_u + n_v >= 2^31"); return BBF_ERANGE; }
   int num_sms = 0;
   if (!device_ok(device, &num_sms)) { set_error("no usable sm_100 CUDA device"); return BBF_ECUDA; }
@@ -222,6 +226,7 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_pt
   std::memset(g, 0, sizeof(*g));
   g->device = device;
   g->num_sms = num_sms;
+  g->load_flags = flags & (uint32_t)(BBF_FORCE_SPARSE | BBF_FORCE_DENSE);
   g->comm = comm;
   g->n_u = n_u; g->n_v = n_v; g->n = n_u + n_v; g->nnz = nnz;
   if (cuda_stream) {
@@ -272,8 +277,7 @@ bbf_status bbf_count_global(bbf_graph* g, bbf_counts* out) {
   BBF_CUDA(cudaSetDevice(g->device));
   unsigned long long BN[2] = {0, 0};
   float ms = 0;
-  BBF_TRY(do_count(g, false, 0, BN, &ms));
-  BBF_TRY(ensure_plan_g(g));
+  BBF_TRY(do_count(g, false, g->load_flags, BN, &ms));
   out->balanced = BN[0];
   out->unbalanced = BN[1];
   out->total = BN[0] + BN[1];
@@ -292,6 +296,7 @@ bbf_status bbf_count_per_vertex(bbf_graph* g, uint64_t* bal_u, uint64_t* unb_u, 
   BBF_CUDA(cudaSetDevice(g->device));
   unsigned long long BN[2] = {0, 0};
   float ms = 0;
+  if ((flags & (BBF_FORCE_SPARSE | BBF_FORCE_DENSE)) == 0) flags |= g->load_flags;
   BBF_TRY(do_count(g, true, flags, BN, &ms));
   cudaStream_t st = g->stream;
   const bool dptr = flags & BBF_PTR_DEVICE;
@@ -339,10 +344,11 @@ bbf_status bbf_count_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* ou
 }
 
 bbf_status bbf_graph_stats(bbf_graph* g, uint64_t* kernel_launches, uint64_t* algo_bytes,
-                           float* ms_main_kernel) {
+                           double* algo_ops, float* ms_main_kernel) {
   if (!g) { set_error("null graph"); return BBF_EINVAL; }
   if (kernel_launches) *kernel_launches = g->launches;
   if (algo_bytes) *algo_bytes = g->algo_bytes;
+  if (algo_ops) *algo_ops = g->algo_ops;
   if (ms_main_kernel) *ms_main_kernel = g->ms_main;
   return BBF_OK;
 }

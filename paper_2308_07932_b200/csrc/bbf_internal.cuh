@@ -184,6 +184,7 @@ struct bbf_graph {
   cudaStream_t stream;
   bool own_stream;
   bbf_comm* comm;
+  uint32_t load_flags;  // BBF_FORCE_SPARSE / BBF_FORCE_DENSE given at load: default dispatch
   uint32_t n_u, n_v, n;
   uint64_t nnz;
   // rank-space CSR
@@ -212,7 +213,8 @@ struct bbf_graph {
   uint64_t* pv;              // 2*n per-vertex (B, N interleaved by array: pv[0..n), pv[n..2n))
   // stats
   uint64_t launches;
-  uint64_t algo_bytes;
+  uint64_t algo_bytes;  // algorithmic bytes of the last count's main kernel (sparse path)
+  double algo_ops;      // algorithmic int8 ops of the last count's main kernel (dense path)
   float ms_main;
   int num_sms;
 };
@@ -251,4 +253,5 @@ bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uin
 bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks,
                      unsigned long long* host_BN);
 bool dense_supported(bbf_graph* g);
+bool dense_preferred(bbf_graph* g, bool per_vertex);
 }  // namespace bbf

@@ -658,6 +658,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   // visited wedge per pass (pass 2 re-reads it for per-vertex counts) + 16 B per eligible
   // middle of its starts (column word, ub, end1 of the middle's row, 4 B id-side output)
   g->algo_bytes = 4ull * p->W_t3 * (per_vertex ? 2 : 1) + 16ull * p->M_t3;
+  g->algo_ops = 0;
   return BBF_OK;
 }
 

@@ -1,11 +1,526 @@
-// dense_i8.cu — S10 (dense int8 tensor-core path).  Placeholder until the tcgen05 kernel lands:
-// the dispatcher never selects it, and BBF_FORCE_DENSE reports BBF_EINVAL.
+// dense_i8.cu — S10 of the hot path: the dense int8 tensor-core path (tcgen05, sm_100a).
+//
+// For one side s (rows = the side's vertices in rank order, K = the other side's vertices) let
+// A in {0,1} be the adjacency and S in {-1,0,+1} the signed adjacency.  For a same-side pair
+// (i, j): T_ij = (A A^T)_ij = #common neighbours and P_ij = (S S^T)_ij = #agreeing - #disagreeing
+// common neighbours, so the agree / disagree wedge counts of Def. Symmetric / Asymmetric Wedge
+// are a = (T+P)/2, d = (T-P)/2, and Lemma 2 gives the
+// pair's balanced count C(a,2) + C(d,2), unbalanced a*d.  Summing over i < j
+// counts every butterfly once (Alg. 2's global count); the row + column sums of the upper
+// triangle are the per-vertex counts of the side (vBBFC semantics).
+//
+// Kernel k_dense_tiles: persistent, one CTA per SM, 6 warps:
+//   warp 0     TMA producer: per K block of 128 B, A_i, S_i (128 rows) and A_j, S_j (256 rows)
+//              into a 2-stage 128B-swizzled shared-memory ring (96 KB per stage);
+//   warp 1     TMEM allocator + MMA issuer: tcgen05.mma.cta_group::1.kind::i8, M=128, N=256,
+//              K=32 per instruction; T accumulates in TMEM columns [0,256) (u8 x u8), P in
+//              [256,512) (s8 x s8), both exact s32;
+//   warps 2-5  epilogue: tcgen05.ld 32 columns at a time, Lemma 2 per element, row sums in
+//              registers, column sums by a lane-transposing butterfly + shared atomics, u64
+//              atomics to the per-vertex array once per tile.
+// Tiles (I, J) of 128 x 256 cover the upper triangle only (j > i masked on diagonal tiles).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "bbf_internal.cuh"
 
 namespace bbf {
-bool dense_supported(bbf_graph*) { return false; }
-bbf_status run_dense(bbf_graph*, bool, int, int, unsigned long long*) {
-  set_error("dense path not built");
-  return BBF_EINVAL;
+namespace {
+
+constexpr uint32_t kBM = 128;       // rows i per tile (MMA M, TMEM lanes)
+constexpr uint32_t kBN = 256;       // rows j per tile (MMA N)
+constexpr uint32_t kBK = 128;       // K bytes per stage (one 128-B swizzle row)
+constexpr uint32_t kStages = 2;
+constexpr uint32_t kTileI = kBM * kBK;           // 16 KB
+constexpr uint32_t kTileJ = kBN * kBK;           // 32 KB
+constexpr uint32_t kStageBytes = 2 * kTileI + 2 * kTileJ;  // A_i, S_i, A_j, S_j = 96 KB
+constexpr int kThreads = 192;
+constexpr int kEpiWarp0 = 2;
+constexpr size_t kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 2 * kBN * 8 /*col acc*/ + 256;
+
+// ------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// K-major operand tile, 128-B swizzle, rows of 128 B, 8-row atoms 1024 B apart
+// (SBO = 1024 B, LBO = 16 B (unused for swizzled K-major), version 1, layout SWIZZLE_128B = 2)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)64u << 32) |
+         ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// instruction descriptors: D s32 (bits 4-5 = 2), A/B format bits 7-9 / 10-12 (0 u8, 1 s8),
+// K-major A and B, N >> 3 at bit 17, M >> 4 at bit 24
+constexpr uint32_t kIdescT = (2u << 4) | (0u << 7) | (0u << 10) | ((kBN >> 3) << 17) | ((kBM >> 4) << 24);
+constexpr uint32_t kIdescP = (2u << 4) | (1u << 7) | (1u << 10) | ((kBN >> 3) << 17) | ((kBM >> 4) << 24);
+
+struct DenseArgs {
+  const uint2* tiles;  // (I, J)
+  uint32_t n_tiles;
+  uint32_t n_rows;     // rows of this side
+  uint32_t n_kb;       // K blocks of 128 B
+  uint32_t pv_row0;    // pv index of row 0 (0 for U, n_u for V)
+  uint32_t n;          // pv stride (N counts at pv[n + ...])
+  int rank, nranks;
+  unsigned long long* pv;  // nullptr: global only
+  unsigned long long* acc; // [0] B, [1] N
+};
+
+// Column sums of a warp's 32 x 32 block: lane L ends holding the sum over the 32 lanes (rows)
+// of column L.  Recursive halving: each step exchanges half of the remaining columns.
+template <int H>
+__device__ __forceinline__ void xpose_step(unsigned long long (&v)[32], int lane) {
+  const bool up = lane & H;
+#pragma unroll
+  for (int c = 0; c < H; ++c) {
+    unsigned long long send = up ? v[c] : v[c + H];
+    unsigned long long keep = up ? v[c + H] : v[c];
+    v[c] = keep + __shfl_xor_sync(0xffffffffu, send, H);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_dense_tiles(const __grid_constant__ CUtensorMap mA_i, const __grid_constant__ CUtensorMap mS_i,
+                  const __grid_constant__ CUtensorMap mA_j, const __grid_constant__ CUtensorMap mS_j,
+                  const DenseArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-B aligned operand ring (128-B swizzle atoms)
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned long long* colB = reinterpret_cast<unsigned long long*>(smem + kStages * kStageBytes);
+  unsigned long long* colN = colB + kBN;
+  __shared__ __align__(8) uint64_t bar_full[kStages], bar_empty[kStages], bar_tfull, bar_tempty;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (uint32_t i = threadIdx.x; i < 2 * kBN; i += kThreads) colB[i] = 0;
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < kStages; ++s) {
+      mbar_init(smem_u32(&bar_full[s]), 1);
+      mbar_init(smem_u32(&bar_empty[s]), 1);
+    }
+    mbar_init(smem_u32(&bar_tfull), 1);
+    mbar_init(smem_u32(&bar_tempty), 4 * 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tmem_base_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    // ================================================================ TMA producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mA_i)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mS_i)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mA_j)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mS_j)) : "memory");
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t t = blockIdx.x * a.nranks + a.rank; t < a.n_tiles; t += gridDim.x * a.nranks) {
+        const uint2 tile = a.tiles[t];
+        const int32_t ri = (int32_t)(tile.x * kBM), rj = (int32_t)(tile.y * kBN);
+        for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
+          mbar_wait(smem_u32(&bar_empty[stage]), phase ^ 1u);
+          const uint32_t fb = smem_u32(&bar_full[stage]);
+          mbar_arrive_expect_tx(fb, kStageBytes);
+          const uint32_t base = smem_u32(smem + stage * kStageBytes);
+          const int32_t k0 = (int32_t)(kb * kBK);
+          tma_load_2d(base, &mA_i, fb, k0, ri);
+          tma_load_2d(base + kTileI, &mS_i, fb, k0, ri);
+          tma_load_2d(base + 2 * kTileI, &mA_j, fb, k0, rj);
+          tma_load_2d(base + 2 * kTileI + kTileJ, &mS_j, fb, k0, rj);
+          if (++stage == kStages) { stage = 0; phase ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================================ MMA issuer
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, lt = 0;
+      for (uint32_t t = blockIdx.x * a.nranks + a.rank; t < a.n_tiles; t += gridDim.x * a.nranks, ++lt) {
+        if (lt > 0) {
+          mbar_wait(smem_u32(&bar_tempty), (lt - 1) & 1u);
+          tc_fence_after();
+        }
+        for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
+          mbar_wait(smem_u32(&bar_full[stage]), phase);
+          tc_fence_after();
+          const uint32_t base = smem_u32(smem + stage * kStageBytes);
+#pragma unroll
+          for (uint32_t kk = 0; kk < kBK / 32; ++kk) {
+            const uint32_t acc = (kb | kk) ? 1u : 0u;
+            const uint32_t off = kk * 32;
+            mma_i8(tmem, smem_desc(base + off), smem_desc(base + 2 * kTileI + off), kIdescT, acc);
+            mma_i8(tmem + kBN, smem_desc(base + kTileI + off),
+                   smem_desc(base + 2 * kTileI + kTileJ + off), kIdescP, acc);
+          }
+          mma_commit(smem_u32(&bar_empty[stage]));  // frees the stage when these MMAs finish
+          if (++stage == kStages) { stage = 0; phase ^= 1u; }
+        }
+        mma_commit(smem_u32(&bar_tfull));
+      }
+    }
+  } else {
+    // ================================================================ epilogue (warps 2..5)
+    const uint32_t q = (uint32_t)(warp & 3);  // TMEM lane quarter this warp may access
+    const uint32_t etid = threadIdx.x - kEpiWarp0 * 32;  // 0..127
+    unsigned long long totB = 0, totN = 0;
+    uint32_t lt = 0;
+    for (uint32_t t = blockIdx.x * a.nranks + a.rank; t < a.n_tiles; t += gridDim.x * a.nranks, ++lt) {
+      const uint2 tile = a.tiles[t];
+      const uint32_t i = tile.x * kBM + q * 32 + lane;  // this thread's row
+      const uint32_t j0 = tile.y * kBN;
+      const bool diag = j0 < tile.x * kBM + kBM;        // some j <= i in the tile
+      mbar_wait(smem_u32(&bar_tfull), lt & 1u);
+      tc_fence_after();
+      unsigned long long rB = 0, rN = 0;
+#pragma unroll 1
+      for (uint32_t c = 0; c < kBN / 32; ++c) {
+        uint32_t tv[32], pv[32];
+        const uint32_t ta = tmem + ((q * 32) << 16) + c * 32;
+        tmem_ld32(ta, tv);
+        tmem_ld32(ta + kBN, pv);
+        tmem_wait_ld();
+        unsigned long long vb[32], vn[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const uint32_t tt = tv[e], pp = pv[e];
+          const uint32_t ad = (tt + pp) >> 1, dd = (tt - pp) >> 1;  // a, d (t >= |p|)
+          uint32_t fb = ((ad * (ad - 1u)) >> 1) + ((dd * (dd - 1u)) >> 1);
+          uint32_t fn = ad * dd;
+          if (diag && j0 + c * 32 + (uint32_t)e <= i) { fb = 0; fn = 0; }
+          rB += fb;
+          rN += fn;
+          vb[e] = fb;
+          vn[e] = fn;
+        }
+        if (a.pv) {
+          xpose_step<16>(vb, lane); xpose_step<16>(vn, lane);
+          xpose_step<8>(vb, lane);  xpose_step<8>(vn, lane);
+          xpose_step<4>(vb, lane);  xpose_step<4>(vn, lane);
+          xpose_step<2>(vb, lane);  xpose_step<2>(vn, lane);
+          xpose_step<1>(vb, lane);  xpose_step<1>(vn, lane);
+          if (vb[0]) atomicAdd(&colB[c * 32 + lane], vb[0]);
+          if (vn[0]) atomicAdd(&colN[c * 32 + lane], vn[0]);
+        }
+      }
+      // TMEM may be overwritten by the next tile's MMAs from here on
+      tc_fence_before();
+      mbar_arrive(smem_u32(&bar_tempty));
+      totB += rB;
+      totN += rN;
+      if (a.pv) {
+        if ((rB | rN) && i < a.n_rows) {
+          atomicAdd(&a.pv[a.pv_row0 + i], rB);
+          atomicAdd(&a.pv[a.n + a.pv_row0 + i], rN);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (uint32_t jj = etid; jj < kBN; jj += 128) {
+          const unsigned long long b = colB[jj], nn = colN[jj];
+          colB[jj] = 0;
+          colN[jj] = 0;
+          const uint32_t j = j0 + jj;
+          if ((b | nn) && j < a.n_rows) {
+            atomicAdd(&a.pv[a.pv_row0 + j], b);
+            atomicAdd(&a.pv[a.n + a.pv_row0 + j], nn);
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      totB += __shfl_xor_sync(0xffffffffu, totB, o);
+      totN += __shfl_xor_sync(0xffffffffu, totN, o);
+    }
+    if (lane == 0 && (totB | totN)) {
+      atomicAdd(&a.acc[0], totB);
+      atomicAdd(&a.acc[1], totN);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// A (0/1, u8) and S (+1/-1, s8) rows of both sides from the rank-space CSR: entry e of row x
+// sets column l(y) of row x's side matrix
+__global__ void k_dense_fill(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                             uint32_t n, uint32_t n_u, uint64_t m, uint8_t* __restrict__ Au,
+                             uint8_t* __restrict__ Su, uint64_t ku, uint8_t* __restrict__ Av,
+                             uint8_t* __restrict__ Sv, uint64_t kv) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = n;  // row: largest x with off[x] <= e
+    while (hi - lo > 1) {
+      uint32_t md = lo + (hi - lo) / 2;
+      if (off[md] <= e) lo = md; else hi = md;
+    }
+    const uint32_t x = lo, w = adj[e];
+    const uint8_t s = (w & kNegBit) ? (uint8_t)0xFF : (uint8_t)1;  // -1 / +1
+    const uint64_t c = w & kMask;
+    if (x < n_u) {
+      if (Au) { Au[x * ku + c] = 1; Su[x * ku + c] = s; }
+    } else {
+      if (Av) { Av[(x - n_u) * kv + c] = 1; Sv[(x - n_u) * kv + c] = s; }
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, void* base, uint64_t rows, uint64_t k, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {k, rows};
+  cuuint64_t strides[1] = {k};
+  cuuint32_t box[2] = {kBK, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+inline uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
+
+// upper-triangle tile list of one side (I over 128-row blocks, J over 256-row blocks), J outer
+std::vector<uint2> tile_list(uint32_t rows_pad) {
+  std::vector<uint2> t;
+  const uint32_t nI = rows_pad / kBM, nJ = rows_pad / kBN;
+  for (uint32_t J = 0; J < nJ; ++J)
+    for (uint32_t I = 0; I < nI; ++I)
+      if (J * kBN + kBN > I * kBM + 1) t.push_back(make_uint2(I, J));
+  return t;
+}
+
+}  // namespace
+
+// The dense path holds both sides' A and S (n_u_pad x n_v_pad bytes each, twice) and needs
+// K = the other side padded to 128 to stay below 65,536 so every per-element count fits 32 bits.
+bool dense_supported(bbf_graph* g) {
+  const uint64_t ru = round_up(std::max<uint32_t>(g->n_u, 1), kBN), rv = round_up(std::max<uint32_t>(g->n_v, 1), kBN);
+  const uint64_t ku = round_up(std::max<uint32_t>(g->n_v, 1), kBK), kv = round_up(std::max<uint32_t>(g->n_u, 1), kBK);
+  if (ku > 65536 || kv > 65536) return false;
+  const uint64_t bytes = 2 * (ru * ku + rv * kv);
+  return bytes <= (16ull << 30);
+}
+
+// dense-vs-sparse choice: estimated int8 tensor time of both sides vs the
+// sparse engine's measured wedge rate on W_pruned wedges
+bool dense_preferred(bbf_graph* g, bool per_vertex) {
+  if (!dense_supported(g) || !g->plan_g.valid) return false;
+  const double nu = g->n_u, nv = g->n_v;
+  const double cu = nu * nu * round_up(g->n_v, kBK), cv = nv * nv * round_up(g->n_u, kBK);
+  const double ops = 2.0 * (per_vertex ? cu + cv : std::min(cu, cv));
+  const double t_dense = ops / 2.5e15 + 1e-4;
+  const double t_sparse = (double)g->plan_g.W_pruned / 2.0e11 + 1e-4;
+  return t_dense < t_sparse;
+}
+
+bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsigned long long* host_BN) {
+  cudaStream_t st = g->stream;
+  if (!dense_supported(g)) {
+    set_error("graph not supported by the dense int8 path");
+    return BBF_EINVAL;
+  }
+  if (!encode_fn()) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return BBF_ECUDA;
+  }
+  // global only: the cheaper side (cost ~ rows^2 * K); per-vertex: both sides
+  const bool do_u = per_vertex || (uint64_t)g->n_u * g->n_u * g->n_v <= (uint64_t)g->n_v * g->n_v * g->n_u;
+  const bool do_v = per_vertex || !do_u;
+  const uint64_t ru = round_up(std::max<uint32_t>(g->n_u, 1), kBN), rv = round_up(std::max<uint32_t>(g->n_v, 1), kBN);
+  const uint64_t ku = round_up(std::max<uint32_t>(g->n_v, 1), kBK), kv = round_up(std::max<uint32_t>(g->n_u, 1), kBK);
+  uint8_t *Au = nullptr, *Su = nullptr, *Av = nullptr, *Sv = nullptr;
+  if (do_u) {
+    BBF_CUDA(cudaMallocAsync(&Au, ru * ku, st));
+    BBF_CUDA(cudaMallocAsync(&Su, ru * ku, st));
+    BBF_CUDA(cudaMemsetAsync(Au, 0, ru * ku, st));
+    BBF_CUDA(cudaMemsetAsync(Su, 0, ru * ku, st));
+  }
+  if (do_v) {
+    BBF_CUDA(cudaMallocAsync(&Av, rv * kv, st));
+    BBF_CUDA(cudaMallocAsync(&Sv, rv * kv, st));
+    BBF_CUDA(cudaMemsetAsync(Av, 0, rv * kv, st));
+    BBF_CUDA(cudaMemsetAsync(Sv, 0, rv * kv, st));
+  }
+  const uint64_t m = 2 * g->nnz;
+  if (m) {
+    unsigned grid = (unsigned)std::min<uint64_t>((m + 255) / 256, 148u * 64u);
+    k_dense_fill<<<grid, 256, 0, st>>>(g->off, g->adj, g->n, g->n_u, m, Au, Su, ku, Av, Sv, kv);
+    g->launches++;
+  }
+  BBF_CUDA(cudaMemsetAsync(g->d_acc, 0, 16 * sizeof(unsigned long long), st));
+  BBF_CUDA(cudaFuncSetAttribute(k_dense_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  unsigned long long BN_side[2][2] = {{0, 0}, {0, 0}};
+  uint2* dtiles[2] = {nullptr, nullptr};
+  bbf_status status = BBF_OK;
+  double ops = 0;
+  for (int side = 0; side < 2 && status == BBF_OK; ++side) {
+    if (side == 0 ? !do_u : !do_v) continue;
+    const uint64_t rows_pad = side ? rv : ru, k = side ? kv : ku;
+    uint8_t* A = side ? Av : Au;
+    uint8_t* S = side ? Sv : Su;
+    CUtensorMap mAi, mSi, mAj, mSj;
+    if (!make_map(&mAi, A, rows_pad, k, kBM) || !make_map(&mSi, S, rows_pad, k, kBM) ||
+        !make_map(&mAj, A, rows_pad, k, kBN) || !make_map(&mSj, S, rows_pad, k, kBN)) {
+      set_error("cuTensorMapEncodeTiled failed");
+      status = BBF_ECUDA;
+      break;
+    }
+    std::vector<uint2> tl = tile_list((uint32_t)rows_pad);
+    cudaError_t err = cudaMallocAsync(&dtiles[side], sizeof(uint2) * (tl.size() + 1), st);
+    if (err == cudaSuccess)
+      err = cudaMemcpyAsync(dtiles[side], tl.data(), sizeof(uint2) * tl.size(), cudaMemcpyHostToDevice, st);
+    if (err != cudaSuccess) { status = cuda_status(err, "dense tiles"); break; }
+    DenseArgs da{};
+    da.tiles = dtiles[side];
+    da.n_tiles = (uint32_t)tl.size();
+    da.n_rows = side ? g->n_v : g->n_u;
+    da.n_kb = (uint32_t)(k / kBK);
+    da.pv_row0 = side ? g->n_u : 0;
+    da.n = g->n;
+    da.rank = rank;
+    da.nranks = nranks;
+    da.pv = per_vertex ? (unsigned long long*)g->pv : nullptr;
+    da.acc = g->d_acc + 2 * side;
+    const unsigned grid = (unsigned)std::min<uint64_t>(g->num_sms, tl.size());
+    k_dense_tiles<<<grid, kThreads, kSmemBytes, st>>>(mAi, mSi, mAj, mSj, da);
+    g->launches++;
+    ops += 2.0 * 2.0 * (double)tl.size() * kBM * kBN * (double)k;
+    err = cudaGetLastError();
+    if (err != cudaSuccess) { status = cuda_status(err, "k_dense_tiles launch"); break; }
+  }
+  cudaEventRecord(e1, st);
+  unsigned long long h[4] = {0, 0, 0, 0};
+  if (status == BBF_OK) {
+    cudaError_t err = cudaMemcpyAsync(h, g->d_acc, sizeof(h), cudaMemcpyDeviceToHost, st);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    if (err != cudaSuccess) status = cuda_status(err, "dense path");
+  }
+  float ms = 0;
+  if (status == BBF_OK) cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  for (void* p : {(void*)Au, (void*)Su, (void*)Av, (void*)Sv, (void*)dtiles[0], (void*)dtiles[1]})
+    if (p) cudaFreeAsync(p, st);
+  if (status != BBF_OK) return status;
+  BN_side[0][0] = h[0]; BN_side[0][1] = h[1];
+  BN_side[1][0] = h[2]; BN_side[1][1] = h[3];
+  const int s0 = do_u ? 0 : 1;
+  host_BN[0] = BN_side[s0][0];
+  host_BN[1] = BN_side[s0][1];
+  g->ms_main = ms;
+  g->algo_bytes = 0;
+  g->algo_ops = ops;
+  if (getenv("BBF_DEBUG"))
+    fprintf(stderr, "[bbf] dense: %.3f ms, %.3e int8 ops (%.1f TOPS), sides U=%d V=%d, B U/V %llu/%llu\n",
+            ms, ops, ops / (ms * 1e-3) / 1e12, (int)do_u, (int)do_v, BN_side[0][0], BN_side[1][0]);
+  return BBF_OK;
+}
+
 }  // namespace bbf

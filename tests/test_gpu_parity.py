@@ -188,3 +188,80 @@ def test_config3_full_size(bbf):
     bal, unb = O.route_s(g, verts=np.concatenate([su, g.n_u + sv]), threads=THREADS)
     assert np.array_equal(bu[su], bal[:su.size]) and np.array_equal(nu[su], unb[:su.size])
     assert np.array_equal(bv[sv], bal[su.size:]) and np.array_equal(nv[sv], unb[su.size:])
+
+
+# ----------------------------------------------------------------------------- dense int8 path
+def dense_all(B, g):
+    with B.Graph.from_synth(g, flags=B.BBF_FORCE_DENSE) as h:
+        glob = h.count_global()
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+        st = h.stats()
+    assert st["algo_ops"] > 0  # the tcgen05 kernel ran (not the sparse engine)
+    return glob, tot, bu, nu, bv, nv
+
+
+def check_dense(B, g):
+    glob, tot, bu, nu, bv, nv = dense_all(B, g)
+    rg = O.route_g(g, threads=THREADS)
+    assert (glob["balanced"], glob["unbalanced"]) == (rg["B"], rg["N"]), g.name
+    assert glob["wedges_G"] == rg["W_G"]
+    assert (tot["balanced"], tot["unbalanced"]) == (rg["B"], rg["N"]), g.name
+    bal, unb = O.route_s(g, threads=THREADS)
+    assert np.array_equal(bu, bal[:g.n_u]) and np.array_equal(nu, unb[:g.n_u]), g.name
+    assert np.array_equal(bv, bal[g.n_u:]) and np.array_equal(nv, unb[g.n_u:]), g.name
+
+
+def test_dense_config1_and_edge_cases(bbf):
+    check_dense(bbf, G.config1())
+    for g in [G.from_edges(1, 1, [], [], []),
+              G.from_edges(5, 4, [0, 0, 1, 1], [0, 1, 0, 1], [1, 1, 1, 0]),
+              G.from_edges(3, 3, [0, 0, 1, 1], [0, 1, 0, 1], [0, 0, 0, 0]),
+              G.from_edges(1, 6, [0] * 6, list(range(6)), [1, 0, 1, 1, 0, 1])]:
+        check_dense(bbf, g)
+
+
+@pytest.mark.parametrize("n_u,n_v,pe,pp,seed", [
+    (300, 700, 0.3, 0.5, 1),     # several 128/256 tiles on both sides, ragged tails
+    (517, 263, 0.5, 0.7, 2),
+    (1000, 129, 0.2, 0.9, 3),    # K just above one 128-byte block
+    (257, 1500, 0.1, 0.3, 4),
+])
+def test_dense_random_multi_tile(bbf, n_u, n_v, pe, pp, seed):
+    check_dense(bbf, G.random_bipartite(n_u, n_v, pe, pp, seed=seed))
+
+
+@pytest.mark.parametrize("m,n", [(2, 2), (130, 70), (700, 600)])
+def test_dense_complete_bipartite_closed_form(bbf, m, n):
+    c = lambda k: k * (k - 1) // 2
+    glob, tot, bu, nu, bv, nv = dense_all(bbf, G.complete(m, n))
+    assert glob["balanced"] == c(m) * c(n) and glob["unbalanced"] == 0
+    assert np.all(bu == (m - 1) * c(n)) and np.all(bv == (n - 1) * c(m))
+    assert not nu.any() and not nv.any()
+
+
+def test_dense_config2_per_vertex(bbf):
+    check_dense(bbf, G.config2())
+
+
+def test_dense_equals_sparse_config4_full_size(bbf):
+    """configs[3] at full size: dense (tcgen05) and sparse engines agree element by element on
+    both sides' per-vertex arrays; global B/N/W_G equal the oracle's Alg. 2 count; sampled
+    vertices equal vBBFC computed one by one."""
+    g = G.config4()
+    rg = O.route_g(g, threads=THREADS)
+    res = {}
+    for name, fl in (("dense", bbf.BBF_FORCE_DENSE), ("sparse", bbf.BBF_FORCE_SPARSE)):
+        with bbf.Graph.from_synth(g, flags=fl) as h:
+            c = h.count_global()
+            res[name] = (c,) + tuple(h.count_per_vertex()[1:])
+            assert (c["balanced"], c["unbalanced"], c["wedges_G"]) == (rg["B"], rg["N"], rg["W_G"]), name
+    for a, b in zip(res["dense"][1:], res["sparse"][1:]):
+        assert np.array_equal(a, b)
+    _, bu, nu, bv, nv = res["dense"]
+    assert int(bu.sum()) == 2 * rg["B"] and int(nv.sum()) == 2 * rg["N"]
+    rng = np.random.default_rng(4)
+    su = np.unique(rng.integers(0, g.n_u, 40))
+    sv = np.unique(rng.integers(0, g.n_v, 40))
+    bal, unb = O.route_s(g, verts=np.concatenate([su, g.n_u + sv]), threads=THREADS)
+    assert np.array_equal(bu[su], bal[:su.size]) and np.array_equal(nu[su], unb[:su.size])
+    assert np.array_equal(bv[sv], bal[su.size:]) and np.array_equal(nv[sv], unb[su.size:])

@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--global-only", action="store_true")
+    ap.add_argument("--path", choices=["auto", "dense", "sparse"], default="auto")
     a = ap.parse_args()
     import torch
     from paper_2308_07932_b200 import bbf
@@ -30,7 +31,8 @@ def main():
     torch.cuda.synchronize()
     for _ in range(a.steps):
         t0 = time.perf_counter()
-        h = bbf.Graph(g.n_u, g.n_v, rp, col, sg, stream=s)
+        fl = {"auto": 0, "dense": bbf.BBF_FORCE_DENSE, "sparse": bbf.BBF_FORCE_SPARSE}[a.path]
+        h = bbf.Graph(g.n_u, g.n_v, rp, col, sg, stream=s, flags=fl)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         r = h.count_global() if a.global_only else h.count_per_vertex(out=outs)[0]
