@@ -178,6 +178,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
   uint32_t* sh_cnt = bm + kBm;            // kMaxWin record counts
   __shared__ uint32_t sh_unit, sh_c[4];
   __shared__ uint32_t sh_acc[32][2][32];  // per-warp pass-2 accumulators of a batch
+  __shared__ uint8_t sh_own[32][32];      // per-warp owner table of a flattened step
+  const uint32_t* __restrict__ adjc = a.adjc;
   __shared__ unsigned long long sh_red[2][32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -283,29 +285,47 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
           if (r < nrec) rc = rw[r];
           const bool lng = rc.len > kFlatMax;
           if (pass == 1) { sh_acc[warp][0][lane] = 0; sh_acc[warp][1][lane] = 0; __syncwarp(); }
-          // -- short records flattened over the lanes
+          // -- short records flattened over the lanes: step `base` gives lane L the flattened
+          //    entry base + L; its owner (the record holding it) is the last record starting at or
+          //    before it in this step (start positions -> bitmask + owner table), else the owner
+          //    carried over from the previous step
           {
             const uint32_t fl = lng ? 0 : rc.len;
             const uint32_t incl = warp_incl_scan(fl, lane), excl = incl - fl;
             const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
-            const uint32_t nz = __ballot_sync(0xffffffffu, fl > 0);
+            int carry = 0;
             for (uint32_t base = 0; base < T; base += 32) {
-              const int ow = flat_owner(fl, excl, nz, base, lane);
+              const bool st = fl > 0 && excl >= base && excl < base + 32;
+              if (st) sh_own[warp][excl - base] = (uint8_t)lane;
+              const uint32_t smask = __reduce_or_sync(0xffffffffu, st ? 1u << (excl - base) : 0u);
+              __syncwarp();
+              const uint32_t m = smask & (0xffffffffu >> (31 - lane));
+              const int gs = m ? 31 - __clz(m) : 0;  // first lane of my owner's group in this step
+              const int ow = m ? (int)sh_own[warp][gs] : carry;
+              carry = __shfl_sync(0xffffffffu, ow, 31);
               const uint32_t f = base + lane;
               const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, ow);
               const uint32_t o_p = __shfl_sync(0xffffffffu, rc.p, ow);
               const uint32_t o_wv = __shfl_sync(0xffffffffu, rc.wv, ow);
+              uint32_t cb = 0, cn = 0;
               if (f < T) {
-                const uint32_t ev = a.adjc[o_p + (f - o_excl)];
-                if (pass == 0) {
-                  t3_inc_c(ctr, bm, word0, ev, o_wv);
-                } else {
-                  uint32_t cb = 0, cn = 0;
-                  t3_share_c(ctr, word0, ev, o_wv, cb, cn);
-                  if (cb) atomicAdd(&sh_acc[warp][0][ow], cb);
-                  if (cn) atomicAdd(&sh_acc[warp][1][ow], cn);
+                const uint32_t ev = adjc[o_p + (f - o_excl)];
+                if (pass == 0) t3_inc_c(ctr, bm, word0, ev, o_wv);
+                else t3_share_c(ctr, word0, ev, o_wv, cb, cn);
+              }
+              if (pass == 1) {
+                // segmented sum over each owner's lane group; its last lane adds it (one writer
+                // per owner per step, so no atomics)
+                const uint32_t ib = warp_incl_scan(cb, lane), in = warp_incl_scan(cn, lane);
+                const int src = gs > 0 ? gs - 1 : 0;
+                const uint32_t pb = __shfl_sync(0xffffffffu, ib, src), pn = __shfl_sync(0xffffffffu, in, src);
+                const bool last = f < T && (f + 1 == T || lane == 31 || ((smask >> (lane + 1)) & 1u));
+                if (last) {
+                  sh_acc[warp][0][ow] += ib - (gs > 0 ? pb : 0u);
+                  sh_acc[warp][1][ow] += in - (gs > 0 ? pn : 0u);
                 }
               }
+              __syncwarp();
             }
           }
           // -- long records over the whole warp, 128 entries in flight
@@ -315,11 +335,12 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
             lmask &= lmask - 1;
             const uint32_t jp = __shfl_sync(0xffffffffu, rc.p, j), jl = __shfl_sync(0xffffffffu, rc.len, j);
             const uint32_t jw = __shfl_sync(0xffffffffu, rc.wv, j);
+            const uint32_t* __restrict__ src = adjc + jp;
             uint32_t cb = 0, cn = 0;
             for (uint32_t o = lane; o < jl; o += 128) {
               uint32_t ev[4];
 #pragma unroll
-              for (int q = 0; q < 4; ++q) ev[q] = (o + 32 * q < jl) ? a.adjc[jp + o + 32 * q] : 0u;
+              for (int q = 0; q < 4; ++q) ev[q] = (o + 32 * q < jl) ? src[o + 32 * q] : 0u;
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 if (o + 32 * q < jl) {
@@ -329,8 +350,9 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
               }
             }
             if (pass == 1) {
-              if (cb) atomicAdd(&sh_acc[warp][0][j], cb);
-              if (cn) atomicAdd(&sh_acc[warp][1][j], cn);
+              cb = __reduce_add_sync(0xffffffffu, cb);
+              cn = __reduce_add_sync(0xffffffffu, cn);
+              if (lane == 0) { sh_acc[warp][0][j] += cb; sh_acc[warp][1][j] += cn; }
             }
           }
           if (pass == 1) {
@@ -347,47 +369,55 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
         __syncthreads();
       }
 
-      // ---------------- epilogue: Lemma 2 per touched end, clear the window
+      // ---------------- epilogue: Lemma 2 per touched end, clear the window.  A packed word is
+      // skipped unless some field has a + d >= 2 (SWAR test: a or d >= 2, or a and d both odd);
+      // fields narrower than 32 bits hold a, d < 2^16, so C(a,2) + C(d,2) and a*d fit 32 bits.
       for (uint32_t bw = tid; bw < kBm; bw += kT3Threads) {
         uint32_t bits = bm[bw];
         if (!bits) continue;
         bm[bw] = 0;
         while (bits) {
-          uint32_t j = __ffs(bits) - 1;
+          const uint32_t j = __ffs(bits) - 1;
           bits &= bits - 1;
-          uint32_t wi = bw * 32 + j;
-          uint32_t gw = word0 + wi;
-          uint32_t v = ctr[wi];
+          const uint32_t wi = bw * 32 + j;
+          const uint32_t gw = word0 + wi;
+          const uint32_t v = ctr[wi];
           ctr[wi] = 0;
-          uint32_t nf, lbase;
-          uint32_t av[8], dv[8];
           if (gw < Z.WB[1]) {  // zone 0: (a word, d word); bits are set on the a word only
-            av[0] = v;
-            dv[0] = ctr[wi + 1];
+            const unsigned long long A = v, D = ctr[wi + 1];
             ctr[wi + 1] = 0;
-            nf = 1; lbase = gw >> 1;
-          } else if (gw < Z.WB[2]) {
-            av[0] = v & 0xffffu; dv[0] = v >> 16; nf = 1; lbase = Z.L[0] + (gw - Z.WB[1]);
-          } else if (gw < Z.WB[3]) {
-            nf = 2; lbase = Z.L[1] + 2 * (gw - Z.WB[2]);
-            for (int f = 0; f < 2; ++f) { uint32_t q = (v >> (16 * f)) & 0xffffu; av[f] = q & 0xffu; dv[f] = q >> 8; }
-          } else if (gw < Z.WB[4]) {
-            nf = 4; lbase = Z.L[2] + 4 * (gw - Z.WB[3]);
-            for (int f = 0; f < 4; ++f) { uint32_t q = (v >> (8 * f)) & 0xffu; av[f] = q & 0xfu; dv[f] = q >> 4; }
-          } else {
-            nf = 8; lbase = Z.L[3] + 8 * (gw - Z.WB[4]);
-            for (int f = 0; f < 8; ++f) { uint32_t q = (v >> (4 * f)) & 0xfu; av[f] = q & 3u; dv[f] = q >> 2; }
+            const unsigned long long fb = comb2(A) + comb2(D), fn = A * D;
+            if (fb | fn) {
+              xB += fb;
+              xN += fn;
+              const uint32_t wrow = sb + (gw >> 1);
+              if (PV) {
+                atomicAdd(&a.pv[wrow], fb);
+                atomicAdd(&a.pv[a.n + wrow], fn);
+              }
+              if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
+            }
+            continue;
           }
-          for (uint32_t f = 0; f < nf; ++f) {
-            unsigned long long A = av[f], D = dv[f];
-            unsigned long long fb = comb2(A) + comb2(D), fn = A * D;
-            if (!(fb | fn)) continue;
+          uint32_t h, lbase, hi, lo;  // half-field width, first rank, SWAR masks
+          if (gw < Z.WB[2]) { h = 16; lbase = Z.L[0] + (gw - Z.WB[1]); hi = 0xfffefffeu; lo = 0x00000001u; }
+          else if (gw < Z.WB[3]) { h = 8; lbase = Z.L[1] + 2 * (gw - Z.WB[2]); hi = 0xfefefefeu; lo = 0x00010001u; }
+          else if (gw < Z.WB[4]) { h = 4; lbase = Z.L[2] + 4 * (gw - Z.WB[3]); hi = 0xeeeeeeeeu; lo = 0x01010101u; }
+          else { h = 2; lbase = Z.L[3] + 8 * (gw - Z.WB[4]); hi = 0xaaaaaaaau; lo = 0x11111111u; }
+          uint32_t cm = (v & hi) | (v & (v >> h) & lo);  // non-zero bits only in contributing fields
+          const uint32_t fw = 2 * h, fmask = (h == 16) ? 0xffffu : ((1u << h) - 1u);
+          while (cm) {
+            const uint32_t f = (uint32_t)(__ffs(cm) - 1) / fw;  // field index
+            cm &= ~(((fw == 32) ? 0xffffffffu : ((1u << fw) - 1u)) << (f * fw));
+            const uint32_t q = v >> (f * fw);
+            const uint32_t A = q & fmask, D = (q >> h) & fmask;
+            const uint32_t fb = ((A * (A - 1u)) >> 1) + ((D * (D - 1u)) >> 1), fn = A * D;
             xB += fb;
             xN += fn;
-            uint32_t wrow = sb + lbase + f;
+            const uint32_t wrow = sb + lbase + f;
             if (PV) {
-              atomicAdd(&a.pv[wrow], fb);
-              atomicAdd(&a.pv[a.n + wrow], fn);
+              atomicAdd(&a.pv[wrow], (unsigned long long)fb);
+              atomicAdd(&a.pv[a.n + wrow], (unsigned long long)fn);
             }
             if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
           }

@@ -86,6 +86,15 @@ __global__ void k_seg_bounds(RouteRows rr, const uint32_t* __restrict__ off,
   e[x] = hi > lo ? hi : lo;
 }
 
+// work[x] = sum of the segment lengths of x's middle entries [b, e) from their inclusive prefix
+__global__ void k_row_work(uint32_t n, const uint64_t* __restrict__ pre, const uint32_t* __restrict__ b,
+                           const uint32_t* __restrict__ e, uint64_t* __restrict__ work) {
+  uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const uint32_t lo = b[x], hi = e[x];
+  work[x] = hi > lo ? pre[hi - 1] - (lo ? pre[lo - 1] : 0ull) : 0ull;
+}
+
 // count T1 / T3 rows, W per tier, units per T3 row
 __global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, uint64_t w_target,
                        const uint32_t* __restrict__ mlo, const uint32_t* __restrict__ mhi,
@@ -211,14 +220,19 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     g->launches += 1;
   }
   if (n) {
+    // per-row work = difference of the inclusive prefix of the per-entry segment lengths
     k_seg_bounds<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(rr, g->off, g->mid, g->end1, sb, se);
-    size_t tb = 0;
-    cub::DeviceSegmentedReduce::Sum(nullptr, tb, len, p->work, (int)n, sb, se, st);
-    void* tmp;
-    BBF_CUDA(cudaMallocAsync(&tmp, tb + 16, st));
-    BBF_CUDA(cub::DeviceSegmentedReduce::Sum(tmp, tb, len, p->work, (int)n, sb, se, st));
+    if (m) {
+      size_t tb = 0;
+      cub::DeviceScan::InclusiveSum(nullptr, tb, len, len, (int64_t)m, st);
+      void* tmp;
+      BBF_CUDA(cudaMallocAsync(&tmp, tb + 16, st));
+      BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, len, len, (int64_t)m, st));
+      cudaFreeAsync(tmp, st);
+      g->launches += 2;
+    }
+    k_row_work<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, len, sb, se, p->work);
     g->launches += 2;
-    cudaFreeAsync(tmp, st);
   }
   // pruned total, to size units
   unsigned long long* d_wp;
