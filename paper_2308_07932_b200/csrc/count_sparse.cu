@@ -100,22 +100,6 @@ constexpr uint32_t kRecMax = 1024;
 constexpr uint32_t kFlatMax = 64;
 constexpr uint32_t kMaxWin = 256;
 
-__device__ __forceinline__ void t3_inc(const Zones& Z, uint32_t* ctr, uint32_t* bm, uint32_t word0,
-                                       uint32_t l, uint32_t cls) {
-  uint32_t base, word, inc;
-  field_of(Z, l, cls, base, word, inc);
-  uint32_t prev = atomicAdd(&ctr[word - word0], inc);
-  if (prev == 0) atomicOr(&bm[(base - word0) >> 5], 1u << ((base - word0) & 31));
-}
-
-__device__ __forceinline__ void mid_share(const Zones& Z, const uint32_t* ctr, uint32_t word0,
-                                          uint32_t ev, uint32_t wv, uint32_t& b, uint32_t& nn) {
-  uint32_t ad, dd;
-  field_read(Z, ctr, word0, ev & kMask, ad, dd);
-  if (((ev ^ wv) >> 31) == 0) { b += ad - 1; nn += dd; }   // symmetric: (a-1, d)
-  else { b += dd - 1; nn += ad; }                            // asymmetric: (d-1, a)
-}
-
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -136,46 +120,110 @@ __device__ __forceinline__ int flat_owner(uint32_t len, uint32_t excl, uint32_t 
   return rank >= 0 ? (int)__fns(nz, 0, rank + 1) : 0;
 }
 
-// one wedge: ev = adjc entry of the end (counter address + sign), wv = middle's adj word
+// one wedge: ev = adjc entry of the end (counter address + sign), wv = middle's adj word.
+// WIDE: the graph has 64-bit (zone 0) fields; BM: maintain the touched-word bitmap.
+template <bool WIDE, bool BM>
 __device__ __forceinline__ void t3_inc_c(uint32_t* ctr, uint32_t* bm, uint32_t word0, uint32_t ev,
                                          uint32_t wv) {
   const uint32_t g = (ev & kCWordMask) - word0;
   const uint32_t cls = (ev ^ wv) >> 31;        // 0 symmetric (a), 1 asymmetric (d)
-  const uint32_t sh = (ev >> 23) & 31u, wc = (ev >> 28) & 3u, wide = (ev >> 30) & 1u;
-  const uint32_t word = g + (wide & cls);
-  const uint32_t inc = 1u << (sh + ((cls & (wide ^ 1u)) << (wc + 1u)));
-  const uint32_t prev = atomicAdd(&ctr[word], inc);
-  if (prev == 0) atomicOr(&bm[g >> 5], 1u << (g & 31));
+  const uint32_t sh = (ev >> 23) & 31u, wc = (ev >> 28) & 3u;
+  uint32_t word = g, inc;
+  if (WIDE) {
+    const uint32_t wide = (ev >> 30) & 1u;
+    word = g + (wide & cls);
+    inc = 1u << (sh + ((cls & (wide ^ 1u)) << (wc + 1u)));
+  } else {
+    inc = 1u << (sh + (cls << (wc + 1u)));
+  }
+  if (BM) {
+    const uint32_t prev = atomicAdd(&ctr[word], inc);
+    if (prev == 0) atomicOr(&bm[g >> 5], 1u << (g & 31));
+  } else {
+    atomicAdd(&ctr[word], inc);
+  }
 }
 
+template <bool WIDE>
 __device__ __forceinline__ void t3_share_c(const uint32_t* ctr, uint32_t word0, uint32_t ev,
                                            uint32_t wv, uint32_t& b, uint32_t& nn) {
   const uint32_t g = (ev & kCWordMask) - word0;
   uint32_t ad, dd;
-  if ((ev >> 30) & 1u) {
+  if (WIDE && ((ev >> 30) & 1u)) {
     ad = ctr[g];
     dd = ctr[g + 1];
   } else {
-    const uint32_t sh = (ev >> 23) & 31u, half = 2u << ((ev >> 28) & 3u);
-    const uint32_t v = ctr[g] >> sh;
-    const uint32_t msk = (half == 16u) ? 0xffffu : ((1u << half) - 1u);
+    const uint32_t h = 2u << ((ev >> 28) & 3u);  // half-field width 2..16
+    const uint32_t v = ctr[g] >> ((ev >> 23) & 31u);
+    const uint32_t msk = (1u << h) - 1u;
     ad = v & msk;
-    dd = (v >> half) & msk;
+    dd = (v >> h) & msk;
   }
   if (((ev ^ wv) >> 31) == 0) { b += ad - 1; nn += dd; }   // symmetric: (a-1, d)
   else { b += dd - 1; nn += ad; }                            // asymmetric: (d-1, a)
+}
+
+// Lemma 2 on one packed counter word (global word gw >= WB[1]); skipped unless some field has
+// a + d >= 2 (SWAR test: a or d >= 2, or a and d both odd).  Fields narrower than 32 bits hold
+// a, d < 2^16, so C(a,2) + C(d,2) and a*d fit 32 bits.
+template <bool PV, bool PAIRS>
+__device__ __forceinline__ void epi_packed(const EngineArgs& a, const Zones& Z, uint32_t sb, uint32_t x,
+                                           uint32_t gw, uint32_t v, unsigned long long& xB,
+                                           unsigned long long& xN) {
+  uint32_t h, lbase, hi, lo;  // half-field width, first rank of the word, SWAR masks
+  if (gw < Z.WB[2]) { h = 16; lbase = Z.L[0] + (gw - Z.WB[1]); hi = 0xfffefffeu; lo = 0x00000001u; }
+  else if (gw < Z.WB[3]) { h = 8; lbase = Z.L[1] + 2 * (gw - Z.WB[2]); hi = 0xfefefefeu; lo = 0x00010001u; }
+  else if (gw < Z.WB[4]) { h = 4; lbase = Z.L[2] + 4 * (gw - Z.WB[3]); hi = 0xeeeeeeeeu; lo = 0x01010101u; }
+  else { h = 2; lbase = Z.L[3] + 8 * (gw - Z.WB[4]); hi = 0xaaaaaaaau; lo = 0x11111111u; }
+  uint32_t cm = (v & hi) | (v & (v >> h) & lo);  // non-zero bits only in contributing fields
+  const uint32_t fw = 2 * h, fmask = (1u << h) - 1u;
+  const uint32_t fclr = (fw == 32) ? 0xffffffffu : ((1u << fw) - 1u);
+  while (cm) {
+    const uint32_t f = (uint32_t)(__ffs(cm) - 1) / fw;  // field index
+    cm &= ~(fclr << (f * fw));
+    const uint32_t q = v >> (f * fw);
+    const uint32_t A = q & fmask, D = (q >> h) & fmask;
+    const uint32_t fb = ((A * (A - 1u)) >> 1) + ((D * (D - 1u)) >> 1), fn = A * D;
+    xB += fb;
+    xN += fn;
+    const uint32_t wrow = sb + lbase + f;
+    if (PV) {
+      atomicAdd(&a.pv[wrow], (unsigned long long)fb);
+      atomicAdd(&a.pv[a.n + wrow], (unsigned long long)fn);
+    }
+    if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
+  }
+}
+
+// Lemma 2 on one 64-bit field (zone 0: a word, d word at global words gw, gw + 1)
+template <bool PV, bool PAIRS>
+__device__ __forceinline__ void epi_wide(const EngineArgs& a, uint32_t sb, uint32_t x, uint32_t gw,
+                                         uint32_t va, uint32_t vd, unsigned long long& xB,
+                                         unsigned long long& xN) {
+  const unsigned long long A = va, D = vd;
+  const unsigned long long fb = comb2(A) + comb2(D), fn = A * D;
+  if (!(fb | fn)) return;
+  xB += fb;
+  xN += fn;
+  const uint32_t wrow = sb + (gw >> 1);
+  if (PV) {
+    atomicAdd(&a.pv[wrow], fb);
+    atomicAdd(&a.pv[a.n + wrow], fn);
+  }
+  if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
 }
 
 struct Rec {  // 16 B segment record
   uint32_t p, len, wv, pad;
 };
 
-template <bool PV, bool PAIRS>
+template <bool PV, bool PAIRS, bool WIDE>
 __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
   extern __shared__ uint32_t smem[];
   uint32_t* ctr = smem;                   // kWin
   uint32_t* bm = smem + kWin;             // kBm
   uint32_t* sh_cnt = bm + kBm;            // kMaxWin record counts
+  uint32_t* sh_wc = sh_cnt + kMaxWin;     // kMaxWin wedge counts
   __shared__ uint32_t sh_unit, sh_c[4];
   __shared__ uint32_t sh_acc[32][2][32];  // per-warp pass-2 accumulators of a batch
   __shared__ uint8_t sh_own[32][32];      // per-warp owner table of a flattened step
@@ -183,7 +231,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
   __shared__ unsigned long long sh_red[2][32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  for (uint32_t i = tid; i < kWin + kBm + kMaxWin; i += kT3Threads) smem[i] = 0;
+  for (uint32_t i = tid; i < kWin + kBm + 2 * kMaxWin; i += kT3Threads) smem[i] = 0;
   const size_t RS = a.rec_stride;
   Rec* R = reinterpret_cast<Rec*>(a.scratch) + (size_t)blockIdx.x * RS * a.kwin_cap;
   unsigned long long totB = 0, totN = 0;
@@ -254,6 +302,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
           const uint2 run = a.runs[r];
           const uint32_t rs = max(run.x, o_s);
           const uint32_t re = (r + 1 < a.nruns) ? min(a.runs[r + 1].x, o_en) : o_en;
+          if (re > rs) atomicAdd(&sh_wc[run.y], re - rs);
           for (uint32_t p = rs; p < re; p += kRecMax) {
             const uint32_t slot = atomicAdd(&sh_cnt[run.y], 1u);
             R[(size_t)run.y * RS + slot] = Rec{p, min(kRecMax, re - p), o_wv, 0u};
@@ -269,6 +318,12 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
       if (nrec == 0) continue;
       const uint32_t word0 = k * kWin;
       const Rec* rw = R + (size_t)k * RS;
+      // records per warp batch: spread a window's records over all 32 warps (>= 2 batches each)
+      const uint32_t bsz = min(32u, max(2u, (nrec + 63u) / 64u));
+      // dense window: at least as many wedges as counter words -> no touched-word bitmap, the
+      // epilogue scans every word of the window
+      const uint32_t nwk = min(kWin, Z.WB[5] - word0);
+      const bool dense = sh_wc[k] >= nwk;
       if (tid < 4) sh_c[tid] = 0;
       if (tid == 0) { atomicAdd(&a.acc[6], (unsigned long long)nrec); atomicAdd(&a.acc[7], 1ull); }
       __syncthreads();
@@ -279,10 +334,10 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
           uint32_t bt = 0;
           if (lane == 0) bt = atomicAdd(&sh_c[pass], 1u);
           bt = __shfl_sync(0xffffffffu, bt, 0);
-          if (bt * 32 >= nrec) break;
-          const uint32_t r = bt * 32 + lane;
+          if (bt * bsz >= nrec) break;
+          const uint32_t r = bt * bsz + lane;
           Rec rc{0, 0, 0, 0};
-          if (r < nrec) rc = rw[r];
+          if ((uint32_t)lane < bsz && r < nrec) rc = rw[r];
           const bool lng = rc.len > kFlatMax;
           if (pass == 1) { sh_acc[warp][0][lane] = 0; sh_acc[warp][1][lane] = 0; __syncwarp(); }
           // -- short records flattened over the lanes: step `base` gives lane L the flattened
@@ -310,8 +365,9 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
               uint32_t cb = 0, cn = 0;
               if (f < T) {
                 const uint32_t ev = adjc[o_p + (f - o_excl)];
-                if (pass == 0) t3_inc_c(ctr, bm, word0, ev, o_wv);
-                else t3_share_c(ctr, word0, ev, o_wv, cb, cn);
+                if (pass == 1) t3_share_c<WIDE>(ctr, word0, ev, o_wv, cb, cn);
+                else if (dense) t3_inc_c<WIDE, false>(ctr, bm, word0, ev, o_wv);
+                else t3_inc_c<WIDE, true>(ctr, bm, word0, ev, o_wv);
               }
               if (pass == 1) {
                 // segmented sum over each owner's lane group; its last lane adds it (one writer
@@ -337,16 +393,18 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
             const uint32_t jw = __shfl_sync(0xffffffffu, rc.wv, j);
             const uint32_t* __restrict__ src = adjc + jp;
             uint32_t cb = 0, cn = 0;
-            for (uint32_t o = lane; o < jl; o += 128) {
-              uint32_t ev[4];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) ev[q] = (o + 32 * q < jl) ? src[o + 32 * q] : 0u;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                if (o + 32 * q < jl) {
-                  if (pass == 0) t3_inc_c(ctr, bm, word0, ev[q], jw);
-                  else t3_share_c(ctr, word0, ev[q], jw, cb, cn);
-                }
+            for (uint32_t o = lane; o < jl; o += 64) {
+              const bool h1 = o + 32 < jl;
+              const uint32_t e0 = src[o], e1 = h1 ? src[o + 32] : 0u;
+              if (pass == 1) {
+                t3_share_c<WIDE>(ctr, word0, e0, jw, cb, cn);
+                if (h1) t3_share_c<WIDE>(ctr, word0, e1, jw, cb, cn);
+              } else if (dense) {
+                t3_inc_c<WIDE, false>(ctr, bm, word0, e0, jw);
+                if (h1) t3_inc_c<WIDE, false>(ctr, bm, word0, e1, jw);
+              } else {
+                t3_inc_c<WIDE, true>(ctr, bm, word0, e0, jw);
+                if (h1) t3_inc_c<WIDE, true>(ctr, bm, word0, e1, jw);
               }
             }
             if (pass == 1) {
@@ -369,63 +427,53 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
         __syncthreads();
       }
 
-      // ---------------- epilogue: Lemma 2 per touched end, clear the window.  A packed word is
-      // skipped unless some field has a + d >= 2 (SWAR test: a or d >= 2, or a and d both odd);
-      // fields narrower than 32 bits hold a, d < 2^16, so C(a,2) + C(d,2) and a*d fit 32 bits.
-      for (uint32_t bw = tid; bw < kBm; bw += kT3Threads) {
-        uint32_t bits = bm[bw];
-        if (!bits) continue;
-        bm[bw] = 0;
-        while (bits) {
-          const uint32_t j = __ffs(bits) - 1;
-          bits &= bits - 1;
-          const uint32_t wi = bw * 32 + j;
-          const uint32_t gw = word0 + wi;
-          const uint32_t v = ctr[wi];
-          ctr[wi] = 0;
-          if (gw < Z.WB[1]) {  // zone 0: (a word, d word); bits are set on the a word only
-            const unsigned long long A = v, D = ctr[wi + 1];
-            ctr[wi + 1] = 0;
-            const unsigned long long fb = comb2(A) + comb2(D), fn = A * D;
-            if (fb | fn) {
-              xB += fb;
-              xN += fn;
-              const uint32_t wrow = sb + (gw >> 1);
-              if (PV) {
-                atomicAdd(&a.pv[wrow], fb);
-                atomicAdd(&a.pv[a.n + wrow], fn);
-              }
-              if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
+      // ---------------- epilogue: Lemma 2 per touched end (Alg. 2 lines 15-18), clear the window
+      if (dense) {
+        uint4* c4 = reinterpret_cast<uint4*>(ctr);
+        for (uint32_t i4 = tid; i4 < (nwk + 3) / 4; i4 += kT3Threads) {
+          const uint4 q = c4[i4];
+          if (!(q.x | q.y | q.z | q.w)) continue;
+          c4[i4] = make_uint4(0u, 0u, 0u, 0u);
+          const uint32_t gw = word0 + 4 * i4;
+          if (WIDE && gw < Z.WB[1]) {  // zone 0 pairs (a word, d word), word0 and WB[1] even
+            epi_wide<PV, PAIRS>(a, sb, x, gw, q.x, q.y, xB, xN);
+            if (gw + 2 < Z.WB[1]) epi_wide<PV, PAIRS>(a, sb, x, gw + 2, q.z, q.w, xB, xN);
+            else {
+              if (q.z) epi_packed<PV, PAIRS>(a, Z, sb, x, gw + 2, q.z, xB, xN);
+              if (q.w) epi_packed<PV, PAIRS>(a, Z, sb, x, gw + 3, q.w, xB, xN);
             }
             continue;
           }
-          uint32_t h, lbase, hi, lo;  // half-field width, first rank, SWAR masks
-          if (gw < Z.WB[2]) { h = 16; lbase = Z.L[0] + (gw - Z.WB[1]); hi = 0xfffefffeu; lo = 0x00000001u; }
-          else if (gw < Z.WB[3]) { h = 8; lbase = Z.L[1] + 2 * (gw - Z.WB[2]); hi = 0xfefefefeu; lo = 0x00010001u; }
-          else if (gw < Z.WB[4]) { h = 4; lbase = Z.L[2] + 4 * (gw - Z.WB[3]); hi = 0xeeeeeeeeu; lo = 0x01010101u; }
-          else { h = 2; lbase = Z.L[3] + 8 * (gw - Z.WB[4]); hi = 0xaaaaaaaau; lo = 0x11111111u; }
-          uint32_t cm = (v & hi) | (v & (v >> h) & lo);  // non-zero bits only in contributing fields
-          const uint32_t fw = 2 * h, fmask = (h == 16) ? 0xffffu : ((1u << h) - 1u);
-          while (cm) {
-            const uint32_t f = (uint32_t)(__ffs(cm) - 1) / fw;  // field index
-            cm &= ~(((fw == 32) ? 0xffffffffu : ((1u << fw) - 1u)) << (f * fw));
-            const uint32_t q = v >> (f * fw);
-            const uint32_t A = q & fmask, D = (q >> h) & fmask;
-            const uint32_t fb = ((A * (A - 1u)) >> 1) + ((D * (D - 1u)) >> 1), fn = A * D;
-            xB += fb;
-            xN += fn;
-            const uint32_t wrow = sb + lbase + f;
-            if (PV) {
-              atomicAdd(&a.pv[wrow], (unsigned long long)fb);
-              atomicAdd(&a.pv[a.n + wrow], (unsigned long long)fn);
+          if (q.x) epi_packed<PV, PAIRS>(a, Z, sb, x, gw, q.x, xB, xN);
+          if (q.y) epi_packed<PV, PAIRS>(a, Z, sb, x, gw + 1, q.y, xB, xN);
+          if (q.z) epi_packed<PV, PAIRS>(a, Z, sb, x, gw + 2, q.z, xB, xN);
+          if (q.w) epi_packed<PV, PAIRS>(a, Z, sb, x, gw + 3, q.w, xB, xN);
+        }
+      } else {
+        for (uint32_t bw = tid; bw < kBm; bw += kT3Threads) {
+          uint32_t bits = bm[bw];
+          if (!bits) continue;
+          bm[bw] = 0;
+          while (bits) {
+            const uint32_t j = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const uint32_t wi = bw * 32 + j;
+            const uint32_t gw = word0 + wi;
+            const uint32_t v = ctr[wi];
+            ctr[wi] = 0;
+            if (WIDE && gw < Z.WB[1]) {  // bits are set on the a word only
+              const uint32_t vd = ctr[wi + 1];
+              ctr[wi + 1] = 0;
+              epi_wide<PV, PAIRS>(a, sb, x, gw, v, vd, xB, xN);
+            } else {
+              epi_packed<PV, PAIRS>(a, Z, sb, x, gw, v, xB, xN);
             }
-            if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
           }
         }
       }
       __syncthreads();
     }
-    for (uint32_t k = tid; k < K; k += kT3Threads) sh_cnt[k] = 0;
+    for (uint32_t k = tid; k < K; k += kT3Threads) { sh_cnt[k] = 0; sh_wc[k] = 0; }
     // unit totals -> start vertex
     totB += xB;
     totN += xN;
@@ -599,19 +647,19 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
   }
 }
 
-template <bool PV, bool PAIRS>
+template <bool PV, bool PAIRS, bool WIDE>
 cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, Plan* p,
                           cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2) {
-  const size_t smem3 = sizeof(uint32_t) * (kWin + kBm + kMaxWin);
+  const size_t smem3 = sizeof(uint32_t) * (kWin + kBm + 2 * kMaxWin);
   const size_t smem1 = sizeof(uint32_t) * kT1Warps * (2 * kT1Slots + 3 * 32 + 64);
   cudaError_t err;
-  err = cudaFuncSetAttribute(k_t3<PV, PAIRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
+  err = cudaFuncSetAttribute(k_t3<PV, PAIRS, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
   if (err != cudaSuccess) return err;
   err = cudaFuncSetAttribute(k_t1<PV, PAIRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
   if (err != cudaSuccess) return err;
   cudaEventRecord(e0, st);
   if (p->n_units) {
-    k_t3<PV, PAIRS><<<g->num_sms, kT3Threads, smem3, st>>>(ea);
+    k_t3<PV, PAIRS, WIDE><<<g->num_sms, kT3Threads, smem3, st>>>(ea);
     g->launches++;
   }
   cudaEventRecord(e1, st);
@@ -663,9 +711,16 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   cudaEvent_t e0, e1, e2;
   cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
   cudaError_t err;
-  if (pairs) err = launch_engine<false, true>(g, ea, st, p, e0, e1, e2);
-  else if (per_vertex) err = launch_engine<true, false>(g, ea, st, p, e0, e1, e2);
-  else err = launch_engine<false, false>(g, ea, st, p, e0, e1, e2);
+  const bool wide = g->zones[0].L[0] > 0 || g->zones[1].L[0] > 0;  // some degree > 65535
+  if (wide) {
+    if (pairs) err = launch_engine<false, true, true>(g, ea, st, p, e0, e1, e2);
+    else if (per_vertex) err = launch_engine<true, false, true>(g, ea, st, p, e0, e1, e2);
+    else err = launch_engine<false, false, true>(g, ea, st, p, e0, e1, e2);
+  } else {
+    if (pairs) err = launch_engine<false, true, false>(g, ea, st, p, e0, e1, e2);
+    else if (per_vertex) err = launch_engine<true, false, false>(g, ea, st, p, e0, e1, e2);
+    else err = launch_engine<false, false, false>(g, ea, st, p, e0, e1, e2);
+  }
   if (err != cudaSuccess) {
     cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
     return cuda_status(err, "sparse engine launch");
