@@ -59,10 +59,11 @@ bbf_status nccl_status(ncclResult_t r, const char* what) {
 bool device_ok(int device, int* num_sms) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return false;
-  cudaDeviceProp p;
-  if (cudaGetDeviceProperties(&p, device) != cudaSuccess) return false;
-  if (p.major < 10) return false;
-  if (num_sms) *num_sms = p.multiProcessorCount;
+  int major = 0, sms = 0;  // attributes, not cudaGetDeviceProperties (milliseconds per call)
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess) return false;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return false;
+  if (major < 10) return false;
+  if (num_sms) *num_sms = sms;
   return true;
 }
 

@@ -127,7 +127,11 @@ __host__ __device__ inline uint32_t word_of_l(const Zones& z, uint32_t l) {
 // 30 wide (zone 0: a in word g, d in word g+1), 31 negative sign (as in adj).
 constexpr uint32_t kCWordBits = 23;
 constexpr uint32_t kCWordMask = (1u << kCWordBits) - 1u;
-constexpr uint32_t kWin = 48 * 1024;  // counter words per hub-kernel window (192 KB of smem)
+#ifndef BBF_T3_CTAS
+#define BBF_T3_CTAS 1
+#endif
+constexpr uint32_t kT3Ctas = BBF_T3_CTAS;           // hub-kernel CTAs per SM
+constexpr uint32_t kWin = 48 * 1024 / kT3Ctas;      // counter words per hub-kernel window
 
 __host__ __device__ inline uint32_t encode_caddr(const Zones& z, uint32_t l) {
   uint32_t g, sh = 0, wc = 0, wide = 0;
@@ -138,6 +142,25 @@ __host__ __device__ inline uint32_t encode_caddr(const Zones& z, uint32_t l) {
   else if (l < z.L[4]) { uint32_t i = l - z.L[3]; g = z.WB[4] + (i >> 3); sh = (i & 7u) << 2; wc = 0; }
   else { g = 0; }  // degree <= 1: never counted
   return (g & kCWordMask) | (sh << 23) | (wc << 28) | (wide << 30);
+}
+
+// Compact encoding (graphs without 64-bit fields and at most 2^20 counter words per side):
+// bits 0-19 word g, 20-21 width code wc (half-field h = 2 << wc), 22-26 P0, 27-31 P1, where P0 /
+// P1 is the bit of the field to increment when the start->middle edge is positive / negative:
+// the wedge is symmetric (a, at bit sh) iff both edges have the same sign, asymmetric (d, at
+// bit sh + h) otherwise, so the middle->end sign is folded into the two positions.
+constexpr uint32_t kCpWordBits = 20;
+constexpr uint32_t kCpWordMask = (1u << kCpWordBits) - 1u;
+
+__host__ __device__ inline uint32_t encode_caddr_compact(const Zones& z, uint32_t l, uint32_t neg) {
+  uint32_t g = 0, sh = 0, wc = 0;
+  if (l < z.L[1]) { g = z.WB[1] + (l - z.L[0]); wc = 3; }
+  else if (l < z.L[2]) { uint32_t i = l - z.L[1]; g = z.WB[2] + (i >> 1); sh = (i & 1u) << 4; wc = 2; }
+  else if (l < z.L[3]) { uint32_t i = l - z.L[2]; g = z.WB[3] + (i >> 2); sh = (i & 3u) << 3; wc = 1; }
+  else if (l < z.L[4]) { uint32_t i = l - z.L[3]; g = z.WB[4] + (i >> 3); sh = (i & 7u) << 2; wc = 0; }
+  const uint32_t pa = sh, pd = sh + (2u << wc);
+  const uint32_t p0 = neg ? pd : pa, p1 = neg ? pa : pd;
+  return (g & kCpWordMask) | (wc << 20) | (p0 << 22) | (p1 << 27);
 }
 
 __host__ __device__ inline unsigned long long comb2(unsigned long long x) {
@@ -200,6 +223,7 @@ struct bbf_graph {
   uint32_t* runid;    // 2*nnz: index of the window run containing the entry
   uint2* runs;        // nruns: {first entry, window id} of every maximal same-window run of a row
   uint32_t nruns;
+  bool compact;       // adjc uses encode_caddr_compact (else encode_caddr + sign bit)
   uint32_t L4[2];     // #vertices with degree >= 2 per side
   uint32_t Llong[2];  // #vertices with degree > 32 per side ("long" middles of the hub kernel)
   uint32_t maxdeg[2];

@@ -29,7 +29,8 @@
 namespace bbf {
 namespace {
 
-constexpr int kT3Threads = 1024;
+constexpr int kT3Threads = 1024 / kT3Ctas;
+constexpr int kT3Warps = kT3Threads / 32;
 constexpr uint32_t kBm = kWin / 32;   // bitmap words
 constexpr int kT1Warps = 12;
 constexpr uint32_t kT1Slots = 1024;
@@ -93,11 +94,11 @@ __device__ __forceinline__ void emit_pair(const EngineArgs& a, uint32_t x, uint3
 //     pass 1 : batches of 32 records per warp; one shared atomic per wedge;
 //     pass 2 : (per-vertex) the same batches read the final (a, d) of each end: middle shares;
 //     epilogue: Lemma 2 per touched counter word (bitmap), clear.
-// Inside a batch, items longer than kFlatMax entries are walked by the whole warp (128 entries
-// in flight); shorter ones are flattened across the lanes (ballot / __fns load balancing), so
-// short middles and records keep every lane busy.
+// Inside a batch, the records are flattened over the lanes in 16-B chunks of adjc (one LDG.128
+// per lane per step), so every lane is busy whatever the record lengths.
 constexpr uint32_t kRecMax = 1024;
-constexpr uint32_t kFlatMax = 64;
+constexpr int kU = 1;  // flattened steps per iteration of the hub kernel's record loop
+constexpr int kEncWide = 0, kEncNarrow = 1, kEncCompact = 2;  // adjc encodings
 constexpr uint32_t kMaxWin = 256;
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
@@ -163,6 +164,30 @@ __device__ __forceinline__ void t3_share_c(const uint32_t* ctr, uint32_t word0, 
   else { b += dd - 1; nn += ad; }                            // asymmetric: (d-1, a)
 }
 
+// Compact encoding (encode_caddr_compact): shamt = 22 + 5 * (start->middle edge negative)
+// selects the bit this wedge increments; oshamt = 49 - shamt the other half of the field.
+template <bool BM>
+__device__ __forceinline__ void t3_inc_cp(uint32_t* ctr, uint32_t* bm, uint32_t word0, uint32_t ev,
+                                          uint32_t shamt) {
+  const uint32_t g = (ev & kCpWordMask) - word0;
+  const uint32_t inc = 1u << ((ev >> shamt) & 31u);
+  if (BM) {
+    const uint32_t prev = atomicAdd(&ctr[g], inc);
+    if (prev == 0) atomicOr(&bm[g >> 5], 1u << (g & 31));
+  } else {
+    atomicAdd(&ctr[g], inc);
+  }
+}
+
+// middle share of one wedge: its own class count - 1 balanced, the other class unbalanced
+__device__ __forceinline__ void t3_share_cp(const uint32_t* ctr, uint32_t word0, uint32_t ev,
+                                            uint32_t shamt, uint32_t oshamt, uint32_t& b, uint32_t& nn) {
+  const uint32_t v = ctr[(ev & kCpWordMask) - word0];
+  const uint32_t msk = (1u << (2u << ((ev >> 20) & 3u))) - 1u;
+  b += ((v >> ((ev >> shamt) & 31u)) & msk) - 1u;
+  nn += (v >> ((ev >> oshamt) & 31u)) & msk;
+}
+
 // Lemma 2 on one packed counter word (global word gw >= WB[1]); skipped unless some field has
 // a + d >= 2 (SWAR test: a or d >= 2, or a and d both odd).  Fields narrower than 32 bits hold
 // a, d < 2^16, so C(a,2) + C(d,2) and a*d fit 32 bits.
@@ -217,18 +242,21 @@ struct Rec {  // 16 B segment record
   uint32_t p, len, wv, pad;
 };
 
-template <bool PV, bool PAIRS, bool WIDE>
-__global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
+template <bool PV, bool PAIRS, int ENC>
+__global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) {
+  constexpr bool WIDE = ENC == kEncWide, CP = ENC == kEncCompact;
   extern __shared__ uint32_t smem[];
   uint32_t* ctr = smem;                   // kWin
   uint32_t* bm = smem + kWin;             // kBm
   uint32_t* sh_cnt = bm + kBm;            // kMaxWin record counts
   uint32_t* sh_wc = sh_cnt + kMaxWin;     // kMaxWin wedge counts
   __shared__ uint32_t sh_unit, sh_c[4];
-  __shared__ uint32_t sh_acc[32][2][32];  // per-warp pass-2 accumulators of a batch
-  __shared__ uint8_t sh_own[32][32];      // per-warp owner table of a flattened step
+  __shared__ uint32_t sh_acc[kT3Warps][2][32];  // per-warp pass-2 accumulators of a batch
+  __shared__ uint8_t sh_own[kT3Warps][32];      // per-warp owner table of a flattened step
   const uint32_t* __restrict__ adjc = a.adjc;
-  __shared__ unsigned long long sh_red[2][32];
+  __shared__ unsigned long long sh_red[2][kT3Warps];
+  __shared__ unsigned long long sh_dbg[4];  // pass-1 steps, pass-1 chunks, small windows, dense windows
+  if (threadIdx.x < 4) sh_dbg[threadIdx.x] = 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   for (uint32_t i = tid; i < kWin + kBm + 2 * kMaxWin; i += kT3Threads) smem[i] = 0;
@@ -319,13 +347,18 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
       const uint32_t word0 = k * kWin;
       const Rec* rw = R + (size_t)k * RS;
       // records per warp batch: spread a window's records over all 32 warps (>= 2 batches each)
-      const uint32_t bsz = min(32u, max(2u, (nrec + 63u) / 64u));
+      const uint32_t bsz = min(32u, max(2u, (nrec + 2 * kT3Warps - 1) / (2 * kT3Warps)));
       // dense window: at least as many wedges as counter words -> no touched-word bitmap, the
       // epilogue scans every word of the window
       const uint32_t nwk = min(kWin, Z.WB[5] - word0);
       const bool dense = sh_wc[k] >= nwk;
       if (tid < 4) sh_c[tid] = 0;
-      if (tid == 0) { atomicAdd(&a.acc[6], (unsigned long long)nrec); atomicAdd(&a.acc[7], 1ull); }
+      if (tid == 0) {
+        atomicAdd(&a.acc[6], (unsigned long long)nrec);
+        atomicAdd(&a.acc[7], 1ull);
+        if (nrec < 64) sh_dbg[2]++;
+        if (dense) sh_dbg[3]++;
+      }
       __syncthreads();
       // ---------------- pass 1 (Alg. 2 lines 9-14) and pass 2 (per-vertex shares)
 #pragma unroll 1
@@ -338,79 +371,85 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
           const uint32_t r = bt * bsz + lane;
           Rec rc{0, 0, 0, 0};
           if ((uint32_t)lane < bsz && r < nrec) rc = rw[r];
-          const bool lng = rc.len > kFlatMax;
           if (pass == 1) { sh_acc[warp][0][lane] = 0; sh_acc[warp][1][lane] = 0; __syncwarp(); }
-          // -- short records flattened over the lanes: step `base` gives lane L the flattened
-          //    entry base + L; its owner (the record holding it) is the last record starting at or
-          //    before it in this step (start positions -> bitmask + owner table), else the owner
-          //    carried over from the previous step
-          {
-            const uint32_t fl = lng ? 0 : rc.len;
-            const uint32_t incl = warp_incl_scan(fl, lane), excl = incl - fl;
-            const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
-            int carry = 0;
-            for (uint32_t base = 0; base < T; base += 32) {
-              const bool st = fl > 0 && excl >= base && excl < base + 32;
+          // The batch's records are flattened over the lanes in 16-B chunks of the adjacency
+          // (4 entries, one LDG.128 per lane, consecutive lanes on consecutive chunks of a
+          // record; a record's first / last chunk is masked to [p, p + len)).  Step `base` gives
+          // lane L chunk base + L; its owner (the record holding it) is the last record starting
+          // at or before it in this step (start bitmask + owner table), else the owner carried
+          // over from the previous step.
+          const uint32_t nch = rc.len ? (rc.p + rc.len + 3) / 4 - rc.p / 4 : 0;
+          const uint32_t incl = warp_incl_scan(nch, lane), excl = incl - nch;
+          const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
+          int carry = 0;
+          if (pass == 0 && lane == 0) {
+            atomicAdd(&sh_dbg[0], (unsigned long long)((T + 31) / 32));
+            atomicAdd(&sh_dbg[1], (unsigned long long)T);
+          }
+          // kU steps per iteration: owner lookups first, then all chunk loads in flight, then
+          // the counter updates (hides the global-load latency behind the other steps' work)
+          for (uint32_t base0 = 0; base0 < T; base0 += 32 * kU) {
+            uint32_t smask[kU], ow[kU], gs[kU], ch[kU], o_p[kU], o_len[kU], o_wv[kU];
+            uint4 q[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const uint32_t base = base0 + 32 * u;
+              const bool st = nch > 0 && excl >= base && excl < base + 32;
               if (st) sh_own[warp][excl - base] = (uint8_t)lane;
-              const uint32_t smask = __reduce_or_sync(0xffffffffu, st ? 1u << (excl - base) : 0u);
+              smask[u] = __reduce_or_sync(0xffffffffu, st ? 1u << (excl - base) : 0u);
               __syncwarp();
-              const uint32_t m = smask & (0xffffffffu >> (31 - lane));
-              const int gs = m ? 31 - __clz(m) : 0;  // first lane of my owner's group in this step
-              const int ow = m ? (int)sh_own[warp][gs] : carry;
-              carry = __shfl_sync(0xffffffffu, ow, 31);
-              const uint32_t f = base + lane;
-              const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, ow);
-              const uint32_t o_p = __shfl_sync(0xffffffffu, rc.p, ow);
-              const uint32_t o_wv = __shfl_sync(0xffffffffu, rc.wv, ow);
+              const uint32_t m = smask[u] & (0xffffffffu >> (31 - lane));
+              gs[u] = m ? 31 - __clz(m) : 0;  // first lane of my owner's group in this step
+              ow[u] = m ? (uint32_t)sh_own[warp][gs[u]] : (uint32_t)carry;
+              __syncwarp();
+              carry = __shfl_sync(0xffffffffu, (int)ow[u], 31);
+              const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, ow[u]);
+              o_p[u] = __shfl_sync(0xffffffffu, rc.p, ow[u]);
+              o_len[u] = __shfl_sync(0xffffffffu, rc.len, ow[u]);
+              o_wv[u] = __shfl_sync(0xffffffffu, rc.wv, ow[u]);
+              ch[u] = o_p[u] / 4 + (base + lane - o_excl);  // absolute 16-B chunk of adjc
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+              q[u] = (base0 + 32 * u + lane < T) ? reinterpret_cast<const uint4*>(adjc)[ch[u]]
+                                                  : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const uint32_t c = base0 + 32 * u + lane;
+              const uint32_t shamt = 22u + 5u * (o_wv[u] >> 31), oshamt = 49u - shamt;
               uint32_t cb = 0, cn = 0;
-              if (f < T) {
-                const uint32_t ev = adjc[o_p + (f - o_excl)];
-                if (pass == 1) t3_share_c<WIDE>(ctr, word0, ev, o_wv, cb, cn);
-                else if (dense) t3_inc_c<WIDE, false>(ctr, bm, word0, ev, o_wv);
-                else t3_inc_c<WIDE, true>(ctr, bm, word0, ev, o_wv);
+              if (c < T) {
+                const uint32_t e0 = 4 * ch[u];
+                const uint32_t ev[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const uint32_t e = e0 + j;
+                  if (e >= o_p[u] && e < o_p[u] + o_len[u]) {
+                    if (CP) {
+                      if (pass == 1) t3_share_cp(ctr, word0, ev[j], shamt, oshamt, cb, cn);
+                      else if (dense) t3_inc_cp<false>(ctr, bm, word0, ev[j], shamt);
+                      else t3_inc_cp<true>(ctr, bm, word0, ev[j], shamt);
+                    } else {
+                      if (pass == 1) t3_share_c<WIDE>(ctr, word0, ev[j], o_wv[u], cb, cn);
+                      else if (dense) t3_inc_c<WIDE, false>(ctr, bm, word0, ev[j], o_wv[u]);
+                      else t3_inc_c<WIDE, true>(ctr, bm, word0, ev[j], o_wv[u]);
+                    }
+                  }
+                }
               }
-              if (pass == 1) {
+              if (pass == 1 && __any_sync(0xffffffffu, (cb | cn) != 0)) {
                 // segmented sum over each owner's lane group; its last lane adds it (one writer
                 // per owner per step, so no atomics)
                 const uint32_t ib = warp_incl_scan(cb, lane), in = warp_incl_scan(cn, lane);
-                const int src = gs > 0 ? gs - 1 : 0;
+                const int src = gs[u] > 0 ? (int)gs[u] - 1 : 0;
                 const uint32_t pb = __shfl_sync(0xffffffffu, ib, src), pn = __shfl_sync(0xffffffffu, in, src);
-                const bool last = f < T && (f + 1 == T || lane == 31 || ((smask >> (lane + 1)) & 1u));
+                const bool last = c < T && (c + 1 == T || lane == 31 || ((smask[u] >> (lane + 1)) & 1u));
                 if (last) {
-                  sh_acc[warp][0][ow] += ib - (gs > 0 ? pb : 0u);
-                  sh_acc[warp][1][ow] += in - (gs > 0 ? pn : 0u);
+                  sh_acc[warp][0][ow[u]] += ib - (gs[u] > 0 ? pb : 0u);
+                  sh_acc[warp][1][ow[u]] += in - (gs[u] > 0 ? pn : 0u);
                 }
+                __syncwarp();
               }
-              __syncwarp();
-            }
-          }
-          // -- long records over the whole warp, 128 entries in flight
-          uint32_t lmask = __ballot_sync(0xffffffffu, lng);
-          while (lmask) {
-            const int j = __ffs(lmask) - 1;
-            lmask &= lmask - 1;
-            const uint32_t jp = __shfl_sync(0xffffffffu, rc.p, j), jl = __shfl_sync(0xffffffffu, rc.len, j);
-            const uint32_t jw = __shfl_sync(0xffffffffu, rc.wv, j);
-            const uint32_t* __restrict__ src = adjc + jp;
-            uint32_t cb = 0, cn = 0;
-            for (uint32_t o = lane; o < jl; o += 64) {
-              const bool h1 = o + 32 < jl;
-              const uint32_t e0 = src[o], e1 = h1 ? src[o + 32] : 0u;
-              if (pass == 1) {
-                t3_share_c<WIDE>(ctr, word0, e0, jw, cb, cn);
-                if (h1) t3_share_c<WIDE>(ctr, word0, e1, jw, cb, cn);
-              } else if (dense) {
-                t3_inc_c<WIDE, false>(ctr, bm, word0, e0, jw);
-                if (h1) t3_inc_c<WIDE, false>(ctr, bm, word0, e1, jw);
-              } else {
-                t3_inc_c<WIDE, true>(ctr, bm, word0, e0, jw);
-                if (h1) t3_inc_c<WIDE, true>(ctr, bm, word0, e1, jw);
-              }
-            }
-            if (pass == 1) {
-              cb = __reduce_add_sync(0xffffffffu, cb);
-              cn = __reduce_add_sync(0xffffffffu, cn);
-              if (lane == 0) { sh_acc[warp][0][j] += cb; sh_acc[warp][1][j] += cn; }
             }
           }
           if (pass == 1) {
@@ -482,8 +521,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
       if (lane == 0) { sh_red[0][warp] = b; sh_red[1][warp] = nn; }
       __syncthreads();
       if (warp == 0) {
-        b = warp_sum(sh_red[0][lane]);
-        nn = warp_sum(sh_red[1][lane]);
+        b = warp_sum(lane < kT3Warps ? sh_red[0][lane] : 0ull);
+        nn = warp_sum(lane < kT3Warps ? sh_red[1][lane] : 0ull);
         if (lane == 0 && (b | nn)) {
           atomicAdd(&a.pv[x], b);
           atomicAdd(&a.pv[a.n + x], nn);
@@ -497,6 +536,12 @@ __global__ void __launch_bounds__(kT3Threads, 1) k_t3(const EngineArgs a) {
   if (lane == 0 && (totB | totN)) {
     atomicAdd(&a.acc[0], totB);
     atomicAdd(&a.acc[1], totN);
+  }
+  if (tid == 0) {
+    atomicAdd(&a.acc[5], sh_dbg[0]);
+    atomicAdd(&a.acc[8], sh_dbg[1]);
+    atomicAdd(&a.acc[9], sh_dbg[2]);
+    atomicAdd(&a.acc[10], sh_dbg[3]);
   }
 }
 
@@ -647,19 +692,19 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
   }
 }
 
-template <bool PV, bool PAIRS, bool WIDE>
+template <bool PV, bool PAIRS, int ENC>
 cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, Plan* p,
                           cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2) {
   const size_t smem3 = sizeof(uint32_t) * (kWin + kBm + 2 * kMaxWin);
   const size_t smem1 = sizeof(uint32_t) * kT1Warps * (2 * kT1Slots + 3 * 32 + 64);
   cudaError_t err;
-  err = cudaFuncSetAttribute(k_t3<PV, PAIRS, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
+  err = cudaFuncSetAttribute(k_t3<PV, PAIRS, ENC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
   if (err != cudaSuccess) return err;
   err = cudaFuncSetAttribute(k_t1<PV, PAIRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
   if (err != cudaSuccess) return err;
   cudaEventRecord(e0, st);
   if (p->n_units) {
-    k_t3<PV, PAIRS, WIDE><<<g->num_sms, kT3Threads, smem3, st>>>(ea);
+    k_t3<PV, PAIRS, ENC><<<g->num_sms * kT3Ctas, kT3Threads, smem3, st>>>(ea);
     g->launches++;
   }
   cudaEventRecord(e1, st);
@@ -688,7 +733,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   }
   size_t mm = std::max<uint32_t>(p->max_mid, 1);
   size_t rs = mm + p->max_work / kRecMax + 1;
-  size_t need = (size_t)g->num_sms * 4 * rs * kwin_cap;  // 16-B records [window][slot]
+  size_t need = (size_t)g->num_sms * kT3Ctas * 4 * rs * kwin_cap;  // 16-B records [window][slot]
   if (need > g->scratch_words) {
     if (g->scratch) cudaFreeAsync(g->scratch, st);
     g->scratch = nullptr;
@@ -712,20 +757,25 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
   cudaError_t err;
   const bool wide = g->zones[0].L[0] > 0 || g->zones[1].L[0] > 0;  // some degree > 65535
-  if (wide) {
-    if (pairs) err = launch_engine<false, true, true>(g, ea, st, p, e0, e1, e2);
-    else if (per_vertex) err = launch_engine<true, false, true>(g, ea, st, p, e0, e1, e2);
-    else err = launch_engine<false, false, true>(g, ea, st, p, e0, e1, e2);
+  const int enc = g->compact ? kEncCompact : wide ? kEncWide : kEncNarrow;
+  if (enc == kEncCompact) {
+    if (pairs) err = launch_engine<false, true, kEncCompact>(g, ea, st, p, e0, e1, e2);
+    else if (per_vertex) err = launch_engine<true, false, kEncCompact>(g, ea, st, p, e0, e1, e2);
+    else err = launch_engine<false, false, kEncCompact>(g, ea, st, p, e0, e1, e2);
+  } else if (enc == kEncWide) {
+    if (pairs) err = launch_engine<false, true, kEncWide>(g, ea, st, p, e0, e1, e2);
+    else if (per_vertex) err = launch_engine<true, false, kEncWide>(g, ea, st, p, e0, e1, e2);
+    else err = launch_engine<false, false, kEncWide>(g, ea, st, p, e0, e1, e2);
   } else {
-    if (pairs) err = launch_engine<false, true, false>(g, ea, st, p, e0, e1, e2);
-    else if (per_vertex) err = launch_engine<true, false, false>(g, ea, st, p, e0, e1, e2);
-    else err = launch_engine<false, false, false>(g, ea, st, p, e0, e1, e2);
+    if (pairs) err = launch_engine<false, true, kEncNarrow>(g, ea, st, p, e0, e1, e2);
+    else if (per_vertex) err = launch_engine<true, false, kEncNarrow>(g, ea, st, p, e0, e1, e2);
+    else err = launch_engine<false, false, kEncNarrow>(g, ea, st, p, e0, e1, e2);
   }
   if (err != cudaSuccess) {
     cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
     return cuda_status(err, "sparse engine launch");
   }
-  unsigned long long h[8];
+  unsigned long long h[12];
   BBF_CUDA(cudaMemcpyAsync(h, g->d_acc, sizeof(h), cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaStreamSynchronize(st));
   float ms1 = 0, ms2 = 0;
@@ -737,8 +787,10 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   host_BN[1] = h[1];
   if (n_cand) *n_cand = h[4];
   if (getenv("BBF_DEBUG"))
-    fprintf(stderr, "[bbf] engine: t3 %.3f ms, t1 %.3f ms, t3 entries pass1 %llu, records %llu, windows %llu\n",
-            ms1, ms2, h[5], h[6], h[7]);
+    fprintf(stderr,
+            "[bbf] engine: t3 %.3f ms, t1 %.3f ms, records %llu, windows %llu (small %llu, dense %llu), "
+            "pass-1 steps %llu chunks %llu (lane use %.1f%%)\n",
+            ms1, ms2, h[6], h[7], h[9], h[10], h[5], h[8], 100.0 * h[8] / (32.0 * (h[5] ? h[5] : 1)));
   // algorithmic bytes of the hub kernel k_t3: 4 B column word per
   // visited wedge per pass (pass 2 re-reads it for per-vertex counts) + 16 B per eligible
   // middle of its starts (column word, ub, end1 of the middle's row, 4 B id-side output)

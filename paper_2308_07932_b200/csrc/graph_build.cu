@@ -5,6 +5,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "bbf_internal.cuh"
@@ -176,12 +177,13 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint32_t n, uint64_
 
 // counter address of each entry's end vertex (entries [0, nnz) are U rows -> V ends)
 __global__ void k_caddr(const uint32_t* __restrict__ adj, uint64_t m, uint64_t nnz, Zones zu, Zones zv,
-                        uint32_t* __restrict__ adjc) {
+                        bool compact, uint32_t* __restrict__ adjc) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
        e += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t w = adj[e];
     const Zones& z = e < nnz ? zv : zu;
-    adjc[e] = encode_caddr(z, w & kMask) | (w & kNegBit);
+    adjc[e] = compact ? encode_caddr_compact(z, w & kMask, w >> 31)
+                      : encode_caddr(z, w & kMask) | (w & kNegBit);
   }
 }
 
@@ -191,22 +193,23 @@ __global__ void k_row_starts(const uint32_t* __restrict__ off, uint32_t n, uint3
 }
 
 // entry e starts a run if it starts its row (flag preset) or its window differs from e-1's
-__global__ void k_run_flags(const uint32_t* __restrict__ adjc, uint64_t m, uint32_t* __restrict__ flag) {
+__global__ void k_run_flags(const uint32_t* __restrict__ adjc, uint64_t m, uint32_t wmask,
+                            uint32_t* __restrict__ flag) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
        e += (uint64_t)gridDim.x * blockDim.x) {
     if (flag[e]) continue;
-    uint32_t k = (adjc[e] & kCWordMask) / kWin, kp = (adjc[e - 1] & kCWordMask) / kWin;
+    uint32_t k = (adjc[e] & wmask) / kWin, kp = (adjc[e - 1] & wmask) / kWin;
     flag[e] = k != kp ? 1u : 0u;
   }
 }
 
 __global__ void k_runs(const uint32_t* __restrict__ adjc, const uint32_t* __restrict__ flag,
-                       uint64_t m, uint32_t* __restrict__ runid, uint2* __restrict__ runs) {
+                       uint64_t m, uint32_t wmask, uint32_t* __restrict__ runid, uint2* __restrict__ runs) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
        e += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t r = runid[e] - 1u;  // inclusive scan -> 0-based run index
     runid[e] = r;
-    if (flag[e]) runs[r] = make_uint2((uint32_t)e, (adjc[e] & kCWordMask) / kWin);
+    if (flag[e]) runs[r] = make_uint2((uint32_t)e, (adjc[e] & wmask) / kWin);
   }
 }
 
@@ -396,16 +399,20 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
       set_error("too many counter words on one side for the hub kernel's 23-bit address");
       return BBF_ERANGE;
     }
-  BBF_CUDA(cudaMallocAsync(&g->adjc, 4ull * (m + 1), st));
+  g->compact = g->zones[0].L[0] == 0 && g->zones[1].L[0] == 0 && g->zones[0].WB[5] <= kCpWordMask &&
+               g->zones[1].WB[5] <= kCpWordMask && !getenv("BBF_NO_COMPACT");  // env: test hook
+  const uint32_t wmask = g->compact ? kCpWordMask : kCWordMask;
+  BBF_CUDA(cudaMallocAsync(&g->adjc, 4ull * (m + 8), st));  // padded: 16-B chunk loads
   BBF_CUDA(cudaMallocAsync(&g->runid, 4ull * (m + 1), st));
   g->nruns = 0;
   if (m) {
     uint32_t* flag;
     BBF_CUDA(cudaMallocAsync(&flag, 4ull * (m + 1), st));
     BBF_CUDA(cudaMemsetAsync(flag, 0, 4ull * (m + 1), st));
-    k_caddr<<<grid_for(m, 256), 256, 0, st>>>(g->adj, m, nnz, g->zones[0], g->zones[1], g->adjc);
+    k_caddr<<<grid_for(m, 256), 256, 0, st>>>(g->adj, m, nnz, g->zones[0], g->zones[1], g->compact,
+                                            g->adjc);
     k_row_starts<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(g->off, n, flag);
-    k_run_flags<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, m, flag);
+    k_run_flags<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, m, wmask, flag);
     size_t ts = 0;
     cub::DeviceScan::InclusiveSum(nullptr, ts, flag, g->runid, (int64_t)m, st);
     void* tmp2;
@@ -414,7 +421,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     BBF_CUDA(cudaMemcpyAsync(&g->nruns, g->runid + (m - 1), 4, cudaMemcpyDeviceToHost, st));
     BBF_CUDA(cudaStreamSynchronize(st));
     BBF_CUDA(cudaMallocAsync(&g->runs, sizeof(uint2) * (g->nruns + 1), st));
-    k_runs<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, flag, m, g->runid, g->runs);
+    k_runs<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, flag, m, wmask, g->runid, g->runs);
     g->launches += 6;
     cudaFreeAsync(tmp2, st);
     cudaFreeAsync(flag, st);

@@ -265,3 +265,17 @@ def test_dense_equals_sparse_config4_full_size(bbf):
     bal, unb = O.route_s(g, verts=np.concatenate([su, g.n_u + sv]), threads=THREADS)
     assert np.array_equal(bu[su], bal[:su.size]) and np.array_equal(nu[su], unb[:su.size])
     assert np.array_equal(bv[sv], bal[su.size:]) and np.array_equal(nv[sv], unb[su.size:])
+
+
+def test_counter_encodings_agree(bbf, monkeypatch):
+    """The hub kernel's two counter-address encodings (compact, and the general one used when
+    a side has more than 2^20 counter words) give identical per-vertex arrays."""
+    g = G.config3()
+    with bbf.Graph.from_synth(g) as h:
+        ref = h.count_per_vertex()
+    monkeypatch.setenv("BBF_NO_COMPACT", "1")
+    with bbf.Graph.from_synth(g) as h:
+        got = h.count_per_vertex()
+    assert got[0]["balanced"] == ref[0]["balanced"] and got[0]["unbalanced"] == ref[0]["unbalanced"]
+    for a, b in zip(got[1:], ref[1:]):
+        assert np.array_equal(a, b)
