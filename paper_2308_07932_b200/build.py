@@ -41,7 +41,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(job):
         s, o = job
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
+        extra = os.environ.get("BBF_NVCC_EXTRA", "").split()  # diagnostics, e.g. -DBBF_T3_PROF
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", s, "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log = os.path.join(BUILD, os.path.basename(o) + ".log")
         with open(log, "w") as f:

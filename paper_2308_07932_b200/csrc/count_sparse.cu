@@ -97,6 +97,20 @@ __device__ __forceinline__ void emit_pair(const EngineArgs& a, uint32_t x, uint3
 // Inside a batch, the records are flattened over the lanes in 16-B chunks of adjc (one LDG.128
 // per lane per step), so every lane is busy whatever the record lengths.
 constexpr uint32_t kRecMax = 1024;
+// BBF_T3_PROF: per-phase clock64 totals of the hub kernel (thread 0, after each CTA barrier),
+// flushed to acc[11..15]; diagnostics only (off in production builds)
+#ifdef BBF_T3_PROF
+#define T3_MARK(slot)                                             \
+  do {                                                            \
+    if (tid == 0) {                                               \
+      const long long now_ = clock64();                           \
+      sh_prof[slot] += (unsigned long long)(now_ - t_prof);       \
+      t_prof = now_;                                              \
+    }                                                             \
+  } while (0)
+#else
+#define T3_MARK(slot) do {} while (0)
+#endif
 constexpr int kU = 1;  // flattened steps per iteration of the hub kernel's record loop
 constexpr int kEncWide = 0, kEncNarrow = 1, kEncCompact = 2;  // adjc encodings
 constexpr uint32_t kMaxWin = 256;
@@ -166,23 +180,40 @@ __device__ __forceinline__ void t3_share_c(const uint32_t* ctr, uint32_t word0, 
 
 // Compact encoding (encode_caddr_compact): shamt = 22 + 5 * (start->middle edge negative)
 // selects the bit this wedge increments; oshamt = 49 - shamt the other half of the field.
+// Counters are addressed through 32-bit shared-window addresses (cbase = shared address of
+// the window's word 0 minus 4 * word0), so an update is LOP + LEA + shifts + one ATOMS/RED.
+__device__ __forceinline__ void sh_red_add(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t sh_atom_add(uint32_t addr, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(addr), "r"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ uint32_t sh_load(uint32_t addr) {
+  uint32_t r;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
+  return r;
+}
+
 template <bool BM>
-__device__ __forceinline__ void t3_inc_cp(uint32_t* ctr, uint32_t* bm, uint32_t word0, uint32_t ev,
+__device__ __forceinline__ void t3_inc_cp(uint32_t cbase, uint32_t* bm, uint32_t word0, uint32_t ev,
                                           uint32_t shamt) {
-  const uint32_t g = (ev & kCpWordMask) - word0;
+  const uint32_t gw = ev & kCpWordMask;
   const uint32_t inc = 1u << ((ev >> shamt) & 31u);
   if (BM) {
-    const uint32_t prev = atomicAdd(&ctr[g], inc);
+    const uint32_t prev = sh_atom_add(cbase + 4u * gw, inc);
+    const uint32_t g = gw - word0;
     if (prev == 0) atomicOr(&bm[g >> 5], 1u << (g & 31));
   } else {
-    atomicAdd(&ctr[g], inc);
+    sh_red_add(cbase + 4u * gw, inc);
   }
 }
 
 // middle share of one wedge: its own class count - 1 balanced, the other class unbalanced
-__device__ __forceinline__ void t3_share_cp(const uint32_t* ctr, uint32_t word0, uint32_t ev,
-                                            uint32_t shamt, uint32_t oshamt, uint32_t& b, uint32_t& nn) {
-  const uint32_t v = ctr[(ev & kCpWordMask) - word0];
+__device__ __forceinline__ void t3_share_cp(uint32_t cbase, uint32_t ev, uint32_t shamt, uint32_t oshamt,
+                                            uint32_t& b, uint32_t& nn) {
+  const uint32_t v = sh_load(cbase + 4u * (ev & kCpWordMask));
   const uint32_t msk = (1u << (2u << ((ev >> 20) & 3u))) - 1u;
   b += ((v >> ((ev >> shamt) & 31u)) & msk) - 1u;
   nn += (v >> ((ev >> oshamt) & 31u)) & msk;
@@ -256,6 +287,11 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
   const uint32_t* __restrict__ adjc = a.adjc;
   __shared__ unsigned long long sh_red[2][kT3Warps];
   __shared__ unsigned long long sh_dbg[4];  // pass-1 steps, pass-1 chunks, small windows, dense windows
+#ifdef BBF_T3_PROF
+  __shared__ unsigned long long sh_prof[8];  // pre-scan, window setup, pass 1, pass 2, epilogue, unit tail, small-window passes
+  long long t_prof = clock64();
+  if (threadIdx.x < 8) sh_prof[threadIdx.x] = 0;
+#endif
   if (threadIdx.x < 4) sh_dbg[threadIdx.x] = 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -280,6 +316,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
     const uint32_t m_lo = a.mid ? a.mid[x] : a.off[x];
     const uint32_t m = a.end1[x] - m_lo;
     const bool split_lo = u.lo > lx + 1, split_hi = u.hi < Z.L[4];
+    T3_MARK(5);
 
     // ---------------- pre-scan: segment records per window
     while (true) {
@@ -339,12 +376,14 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       }
     }
     __syncthreads();
+    T3_MARK(0);
     unsigned long long xB = 0, xN = 0;
 
     for (uint32_t k = 0; k < K; ++k) {
       const uint32_t nrec = sh_cnt[k];
       if (nrec == 0) continue;
       const uint32_t word0 = k * kWin;
+      const uint32_t cbase = (uint32_t)__cvta_generic_to_shared(ctr) - 4u * word0;
       const Rec* rw = R + (size_t)k * RS;
       // records per warp batch: spread a window's records over all 32 warps (>= 2 batches each)
       const uint32_t bsz = min(32u, max(2u, (nrec + 2 * kT3Warps - 1) / (2 * kT3Warps)));
@@ -360,6 +399,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
         if (dense) sh_dbg[3]++;
       }
       __syncthreads();
+      T3_MARK(1);
       // ---------------- pass 1 (Alg. 2 lines 9-14) and pass 2 (per-vertex shares)
 #pragma unroll 1
       for (int pass = 0; pass < (PV ? 2 : 1); ++pass) {
@@ -426,9 +466,9 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
                   const uint32_t e = e0 + j;
                   if (e >= o_p[u] && e < o_p[u] + o_len[u]) {
                     if (CP) {
-                      if (pass == 1) t3_share_cp(ctr, word0, ev[j], shamt, oshamt, cb, cn);
-                      else if (dense) t3_inc_cp<false>(ctr, bm, word0, ev[j], shamt);
-                      else t3_inc_cp<true>(ctr, bm, word0, ev[j], shamt);
+                      if (pass == 1) t3_share_cp(cbase, ev[j], shamt, oshamt, cb, cn);
+                      else if (dense) t3_inc_cp<false>(cbase, bm, word0, ev[j], shamt);
+                      else t3_inc_cp<true>(cbase, bm, word0, ev[j], shamt);
                     } else {
                       if (pass == 1) t3_share_c<WIDE>(ctr, word0, ev[j], o_wv[u], cb, cn);
                       else if (dense) t3_inc_c<WIDE, false>(ctr, bm, word0, ev[j], o_wv[u]);
@@ -464,6 +504,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           }
         }
         __syncthreads();
+        T3_MARK(2 + pass);
       }
 
       // ---------------- epilogue: Lemma 2 per touched end (Alg. 2 lines 15-18), clear the window
@@ -511,6 +552,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
         }
       }
       __syncthreads();
+      T3_MARK(4);
     }
     for (uint32_t k = tid; k < K; k += kT3Threads) { sh_cnt[k] = 0; sh_wc[k] = 0; }
     // unit totals -> start vertex
@@ -537,6 +579,11 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
     atomicAdd(&a.acc[0], totB);
     atomicAdd(&a.acc[1], totN);
   }
+#ifdef BBF_T3_PROF
+  if (tid == 0) {
+    for (int i = 0; i < 5; ++i) atomicAdd(&a.acc[11 + i], sh_prof[i]);
+  }
+#endif
   if (tid == 0) {
     atomicAdd(&a.acc[5], sh_dbg[0]);
     atomicAdd(&a.acc[8], sh_dbg[1]);
@@ -775,7 +822,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
     return cuda_status(err, "sparse engine launch");
   }
-  unsigned long long h[12];
+  unsigned long long h[16];
   BBF_CUDA(cudaMemcpyAsync(h, g->d_acc, sizeof(h), cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaStreamSynchronize(st));
   float ms1 = 0, ms2 = 0;
@@ -791,6 +838,13 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
             "[bbf] engine: t3 %.3f ms, t1 %.3f ms, records %llu, windows %llu (small %llu, dense %llu), "
             "pass-1 steps %llu chunks %llu (lane use %.1f%%)\n",
             ms1, ms2, h[6], h[7], h[9], h[10], h[5], h[8], 100.0 * h[8] / (32.0 * (h[5] ? h[5] : 1)));
+#ifdef BBF_T3_PROF
+  {
+    const double clk = 1.965e6 * g->num_sms * kT3Ctas;  // cycles per ms summed over CTAs
+    fprintf(stderr, "[bbf] t3 phases (ms of CTA time): prescan %.2f setup %.2f pass1 %.2f pass2 %.2f epi %.2f\n",
+            h[11] / clk, h[12] / clk, h[13] / clk, h[14] / clk, h[15] / clk);
+  }
+#endif
   // algorithmic bytes of the hub kernel k_t3: 4 B column word per
   // visited wedge per pass (pass 2 re-reads it for per-vertex counts) + 16 B per eligible
   // middle of its starts (column word, ub, end1 of the middle's row, 4 B id-side output)
