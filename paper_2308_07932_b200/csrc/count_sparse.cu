@@ -59,6 +59,7 @@ struct EngineArgs {
   uint32_t max_mid;
   uint32_t kwin_cap;  // max windows per side
   uint32_t rec_stride;  // record slots per window: max middles + max unit work / kRecMax
+  uint32_t dense_div;   // a window is scanned densely when wedges * dense_div >= its words
   // pair candidates (top-k): balanced, unbalanced, (min id << 32 | max id)
   unsigned long long* cb;
   unsigned long long* cn;
@@ -97,6 +98,12 @@ __device__ __forceinline__ void emit_pair(const EngineArgs& a, uint32_t x, uint3
 // Inside a batch, the records are flattened over the lanes in 16-B chunks of adjc (one LDG.128
 // per lane per step), so every lane is busy whatever the record lengths.
 constexpr uint32_t kRecMax = 1024;
+#ifdef BBF_T3_PROF
+__device__ unsigned long long g_prof_cnt[4];  // nonzero counter words, contributing fields
+#define T3_COUNT(i, v) atomicAdd(&g_prof_cnt[i], (unsigned long long)(v))
+#else
+#define T3_COUNT(i, v) do {} while (0)
+#endif
 // BBF_T3_PROF: per-phase clock64 totals of the hub kernel (thread 0, after each CTA barrier),
 // flushed to acc[11..15]; diagnostics only (off in production builds)
 #ifdef BBF_T3_PROF
@@ -244,8 +251,8 @@ __device__ __forceinline__ void epi_packed(const EngineArgs& a, const Zones& Z, 
     xN += fn;
     const uint32_t wrow = sb + lbase + f;
     if (PV) {
-      atomicAdd(&a.pv[wrow], (unsigned long long)fb);
-      atomicAdd(&a.pv[a.n + wrow], (unsigned long long)fn);
+      if (fb) atomicAdd(&a.pv[wrow], (unsigned long long)fb);  // skip zero REDs
+      if (fn) atomicAdd(&a.pv[a.n + wrow], (unsigned long long)fn);
     }
     if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
   }
@@ -263,8 +270,8 @@ __device__ __forceinline__ void epi_wide(const EngineArgs& a, uint32_t sb, uint3
   xN += fn;
   const uint32_t wrow = sb + (gw >> 1);
   if (PV) {
-    atomicAdd(&a.pv[wrow], fb);
-    atomicAdd(&a.pv[a.n + wrow], fn);
+    if (fb) atomicAdd(&a.pv[wrow], fb);
+    if (fn) atomicAdd(&a.pv[a.n + wrow], fn);
   }
   if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
 }
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       // dense window: at least as many wedges as counter words -> no touched-word bitmap, the
       // epilogue scans every word of the window
       const uint32_t nwk = min(kWin, Z.WB[5] - word0);
-      const bool dense = sh_wc[k] >= nwk;
+      const bool dense = sh_wc[k] * a.dense_div >= nwk;
       if (tid < 4) sh_c[tid] = 0;
       if (tid == 0) {
         atomicAdd(&a.acc[6], (unsigned long long)nrec);
@@ -497,8 +504,8 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             const uint32_t cb = sh_acc[warp][0][lane], cn = sh_acc[warp][1][lane];
             if (cb | cn) {
               const uint32_t vr = ob + (rc.wv & kMask);
-              atomicAdd(&a.pv[vr], (unsigned long long)cb);
-              atomicAdd(&a.pv[a.n + vr], (unsigned long long)cn);
+              if (cb) atomicAdd(&a.pv[vr], (unsigned long long)cb);
+              if (cn) atomicAdd(&a.pv[a.n + vr], (unsigned long long)cn);
             }
             __syncwarp();
           }
@@ -800,6 +807,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   ea.kwin_cap = kwin_cap;
   ea.rec_stride = (uint32_t)(std::max<uint32_t>(p->max_mid, 1) + p->max_work / kRecMax + 1);
   ea.cb = cb; ea.cn = cn; ea.cid = cid; ea.cap = cap;
+  ea.dense_div = getenv("BBF_DENSE_DIV") ? (uint32_t)atoi(getenv("BBF_DENSE_DIV")) : 2u;
   cudaEvent_t e0, e1, e2;
   cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
   cudaError_t err;
