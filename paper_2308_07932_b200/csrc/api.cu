@@ -239,8 +239,8 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_pt
   }
   bbf_status s = BBF_OK;
   keep_pool(device);
-  cudaError_t e = cudaMallocAsync(&g->d_acc, 16 * sizeof(unsigned long long), g->stream);
-  if (e == cudaSuccess) e = cudaMallocAsync(&g->pv, 16ull * (g->n + 1), g->stream);
+  cudaError_t e = dmalloc(&g->d_acc, 16 * sizeof(unsigned long long), g->stream);
+  if (e == cudaSuccess) e = dmalloc(&g->pv, 16ull * (g->n + 1), g->stream);
   if (e != cudaSuccess) s = cuda_status(e, "cudaMalloc");
   if (s == BBF_OK) s = build_graph(g, row_ptr, col, sign, dptr);
   if (s == BBF_OK) {
@@ -266,7 +266,7 @@ bbf_status bbf_graph_free(bbf_graph* g) {
   void* ptrs[] = {g->off, g->adj, g->mid, g->end1, g->inv, g->degs, g->degpre, g->scratch, g->d_acc, g->pv,
                   g->adjc, g->runid, g->runs};
   for (void* p : ptrs)
-    if (p) cudaFreeAsync(p, g->stream);
+    if (p) dfree(p, g->stream);
   cudaStreamSynchronize(g->stream);
   if (g->own_stream) cudaStreamDestroy(g->stream);
   delete g;
@@ -304,7 +304,7 @@ bbf_status bbf_count_per_vertex(bbf_graph* g, uint64_t* bal_u, uint64_t* unb_u, 
   // S9: rank space -> input ids, straight into device outputs or via one staging buffer
   unsigned long long* stage = nullptr;
   uint64_t* outs[4] = {bal_u, unb_u, bal_v, unb_v};
-  if (!dptr && (bal_u || unb_u || bal_v || unb_v)) BBF_CUDA(cudaMallocAsync(&stage, 16ull * (g->n + 1), st));
+  if (!dptr && (bal_u || unb_u || bal_v || unb_v)) BBF_CUDA(dmalloc(&stage, 16ull * (g->n + 1), st));
   for (int side = 0; side < 2; ++side) {
     uint32_t cnt = side ? g->n_v : g->n_u, row0 = side ? g->n_u : 0;
     uint64_t* ob = outs[2 * side];
@@ -320,7 +320,7 @@ bbf_status bbf_count_per_vertex(bbf_graph* g, uint64_t* bal_u, uint64_t* unb_u, 
       if (on) BBF_CUDA(cudaMemcpyAsync(on, dn, 8ull * cnt, cudaMemcpyDeviceToHost, st));
     }
   }
-  if (stage) cudaFreeAsync(stage, st);
+  if (stage) dfree(stage, st);
   BBF_CUDA(cudaStreamSynchronize(st));
   if (totals) {
     BBF_TRY(ensure_plan_g(g));

@@ -263,6 +263,13 @@ bbf_status cuda_status(cudaError_t e, const char* what);
 
 // internal entry points across translation units
 namespace bbf {
+// device-memory cache (mem.cu): stream-ordered like cudaMallocAsync / cudaFreeAsync
+cudaError_t dmalloc_raw(void** out, size_t bytes, cudaStream_t st);
+void dfree(void* p, cudaStream_t st);
+template <class T>
+inline cudaError_t dmalloc(T** out, size_t bytes, cudaStream_t st) {
+  return dmalloc_raw(reinterpret_cast<void**>(out), bytes, st);
+}
 bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* col,
                        const uint8_t* sign, bool device_ptrs);
 bbf_status make_plan(bbf_graph* g, int route, Plan* p);

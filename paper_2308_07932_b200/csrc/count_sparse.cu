@@ -789,9 +789,9 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   size_t rs = mm + p->max_work / kRecMax + 1;
   size_t need = (size_t)g->num_sms * kT3Ctas * 4 * rs * kwin_cap;  // 16-B records [window][slot]
   if (need > g->scratch_words) {
-    if (g->scratch) cudaFreeAsync(g->scratch, st);
+    if (g->scratch) dfree(g->scratch, st);
     g->scratch = nullptr;
-    BBF_CUDA(cudaMallocAsync(&g->scratch, need * sizeof(uint32_t), st));
+    BBF_CUDA(dmalloc(&g->scratch, need * sizeof(uint32_t), st));
     g->scratch_words = need;
   }
   BBF_CUDA(cudaMemsetAsync(g->d_acc, 0, 16 * sizeof(unsigned long long), st));
@@ -896,38 +896,38 @@ bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uin
   unsigned long long ncand = 0;
   unsigned long long *cb = nullptr, *cn = nullptr, *cid = nullptr;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    BBF_CUDA(cudaMallocAsync(&cb, 8 * cap, st));
-    BBF_CUDA(cudaMallocAsync(&cn, 8 * cap, st));
-    BBF_CUDA(cudaMallocAsync(&cid, 8 * cap, st));
+    BBF_CUDA(dmalloc(&cb, 8 * cap, st));
+    BBF_CUDA(dmalloc(&cn, 8 * cap, st));
+    BBF_CUDA(dmalloc(&cid, 8 * cap, st));
     unsigned long long BN[2];
     BBF_TRY(run_sparse_impl(g, p, false, true, 0, 1, BN, cb, cn, cid, cap, &ncand));
     if (ncand <= cap) break;
-    cudaFreeAsync(cb, st); cudaFreeAsync(cn, st); cudaFreeAsync(cid, st);
+    dfree(cb, st); dfree(cn, st); dfree(cid, st);
     cap = ncand + 1024;
     if (attempt == 1) { set_error("top-k candidate buffer overflow"); return BBF_ENOMEM; }
   }
   uint32_t take = (uint32_t)std::min<unsigned long long>(k, ncand);
   *n_out = take;
   if (take == 0) {
-    cudaFreeAsync(cb, st); cudaFreeAsync(cn, st); cudaFreeAsync(cid, st);
+    dfree(cb, st); dfree(cn, st); dfree(cid, st);
     BBF_CUDA(cudaStreamSynchronize(st));
     return BBF_OK;
   }
   const int nc = (int)ncand;
   uint32_t *idx0, *idx1, *idx2;
   unsigned long long *kid, *kb, *kb2;
-  BBF_CUDA(cudaMallocAsync(&idx0, 4ull * nc, st));
-  BBF_CUDA(cudaMallocAsync(&idx1, 4ull * nc, st));
-  BBF_CUDA(cudaMallocAsync(&idx2, 4ull * nc, st));
-  BBF_CUDA(cudaMallocAsync(&kid, 8ull * nc, st));
-  BBF_CUDA(cudaMallocAsync(&kb, 8ull * nc, st));
-  BBF_CUDA(cudaMallocAsync(&kb2, 8ull * nc, st));
+  BBF_CUDA(dmalloc(&idx0, 4ull * nc, st));
+  BBF_CUDA(dmalloc(&idx1, 4ull * nc, st));
+  BBF_CUDA(dmalloc(&idx2, 4ull * nc, st));
+  BBF_CUDA(dmalloc(&kid, 8ull * nc, st));
+  BBF_CUDA(dmalloc(&kb, 8ull * nc, st));
+  BBF_CUDA(dmalloc(&kb2, 8ull * nc, st));
   k_iota<<<256, 256, 0, st>>>(idx0, ncand);
   size_t t1 = 0, t2 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, t1, cid, kid, idx0, idx1, nc, 0, 64, st);
   cub::DeviceRadixSort::SortPairsDescending(nullptr, t2, kb, kb2, idx1, idx2, nc, 0, 64, st);
   void* tmp;
-  BBF_CUDA(cudaMallocAsync(&tmp, std::max(t1, t2) + 16, st));
+  BBF_CUDA(dmalloc(&tmp, std::max(t1, t2) + 16, st));
   BBF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t1, cid, kid, idx0, idx1, nc, 0, 64, st));
   k_gather_u64<<<256, 256, 0, st>>>(cb, idx1, ncand, kb);
   BBF_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, t2, kb, kb2, idx1, idx2, nc, 0, 64, st));
@@ -947,7 +947,7 @@ bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uin
     out[i].unbalanced = hn[i];
   }
   void* fr[] = {cb, cn, cid, idx0, idx1, idx2, kid, kb, kb2, tmp};
-  for (void* q : fr) cudaFreeAsync(q, st);
+  for (void* q : fr) dfree(q, st);
   BBF_CUDA(cudaStreamSynchronize(st));
   return BBF_OK;
 }

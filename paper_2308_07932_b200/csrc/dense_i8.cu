@@ -433,14 +433,14 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
   const uint64_t ku = round_up(std::max<uint32_t>(g->n_v, 1), kBK), kv = round_up(std::max<uint32_t>(g->n_u, 1), kBK);
   uint8_t *Au = nullptr, *Su = nullptr, *Av = nullptr, *Sv = nullptr;
   if (do_u) {
-    BBF_CUDA(cudaMallocAsync(&Au, ru * ku, st));
-    BBF_CUDA(cudaMallocAsync(&Su, ru * ku, st));
+    BBF_CUDA(dmalloc(&Au, ru * ku, st));
+    BBF_CUDA(dmalloc(&Su, ru * ku, st));
     BBF_CUDA(cudaMemsetAsync(Au, 0, ru * ku, st));
     BBF_CUDA(cudaMemsetAsync(Su, 0, ru * ku, st));
   }
   if (do_v) {
-    BBF_CUDA(cudaMallocAsync(&Av, rv * kv, st));
-    BBF_CUDA(cudaMallocAsync(&Sv, rv * kv, st));
+    BBF_CUDA(dmalloc(&Av, rv * kv, st));
+    BBF_CUDA(dmalloc(&Sv, rv * kv, st));
     BBF_CUDA(cudaMemsetAsync(Av, 0, rv * kv, st));
     BBF_CUDA(cudaMemsetAsync(Sv, 0, rv * kv, st));
   }
@@ -473,7 +473,7 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
       break;
     }
     std::vector<uint2> tl = tile_list((uint32_t)rows_pad);
-    cudaError_t err = cudaMallocAsync(&dtiles[side], sizeof(uint2) * (tl.size() + 1), st);
+    cudaError_t err = dmalloc(&dtiles[side], sizeof(uint2) * (tl.size() + 1), st);
     if (err == cudaSuccess)
       err = cudaMemcpyAsync(dtiles[side], tl.data(), sizeof(uint2) * tl.size(), cudaMemcpyHostToDevice, st);
     if (err != cudaSuccess) { status = cuda_status(err, "dense tiles"); break; }
@@ -507,7 +507,7 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   for (void* p : {(void*)Au, (void*)Su, (void*)Av, (void*)Sv, (void*)dtiles[0], (void*)dtiles[1]})
-    if (p) cudaFreeAsync(p, st);
+    if (p) dfree(p, st);
   if (status != BBF_OK) return status;
   BN_side[0][0] = h[0]; BN_side[0][1] = h[1];
   BN_side[1][0] = h[2]; BN_side[1][1] = h[3];

@@ -241,18 +241,18 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   uint32_t* own_col = nullptr;
   uint8_t* own_sg = nullptr;
   if (!device_ptrs) {
-    BBF_CUDA(cudaMallocAsync(&own_rp, sizeof(uint64_t) * (n_u + 1), st));
+    BBF_CUDA(dmalloc(&own_rp, sizeof(uint64_t) * (n_u + 1), st));
     BBF_CUDA(cudaMemcpyAsync(own_rp, row_ptr, sizeof(uint64_t) * (n_u + 1), cudaMemcpyHostToDevice, st));
     if (nnz) {
-      BBF_CUDA(cudaMallocAsync(&own_col, sizeof(uint32_t) * nnz, st));
-      BBF_CUDA(cudaMallocAsync(&own_sg, nnz, st));
+      BBF_CUDA(dmalloc(&own_col, sizeof(uint32_t) * nnz, st));
+      BBF_CUDA(dmalloc(&own_sg, nnz, st));
       BBF_CUDA(cudaMemcpyAsync(own_col, col, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice, st));
       BBF_CUDA(cudaMemcpyAsync(own_sg, sign, nnz, cudaMemcpyHostToDevice, st));
     }
     d_rp = own_rp; d_col = own_col; d_sg = own_sg;
   }
   uint32_t* d_err;
-  BBF_CUDA(cudaMallocAsync(&d_err, 4 * sizeof(uint32_t), st));
+  BBF_CUDA(dmalloc(&d_err, 4 * sizeof(uint32_t), st));
   BBF_CUDA(cudaMemsetAsync(d_err, 0, 4 * sizeof(uint32_t), st));
   k_validate_rows<<<grid_for(n_u + 1, 256, 1u << 30), 256, 0, st>>>(d_rp, n_u, d_err);
   if (nnz) k_validate_edges<<<grid_for(nnz, 256), 256, 0, st>>>(d_col, d_sg, nnz, n_v, d_err);
@@ -261,12 +261,12 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   BBF_CUDA(cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaStreamSynchronize(st));
   auto cleanup_input = [&]() {
-    if (own_rp) cudaFreeAsync(own_rp, st);
-    if (own_col) cudaFreeAsync(own_col, st);
-    if (own_sg) cudaFreeAsync(own_sg, st);
+    if (own_rp) dfree(own_rp, st);
+    if (own_col) dfree(own_col, st);
+    if (own_sg) dfree(own_sg, st);
   };
   if (h_err) {
-    cudaFreeAsync(d_err, st);
+    dfree(d_err, st);
     cleanup_input();
     cudaStreamSynchronize(st);
     if (h_err & kErrRowPtr) { set_error("row_ptr[0] != 0 or row_ptr not non-decreasing"); return BBF_ERANGE; }
@@ -278,13 +278,13 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   // S2-S3: degrees and per-side priority ranks
   uint64_t *key_u, *key_v, *skey_u, *skey_v;
   uint32_t *dv, *lr_u, *lr_v;
-  BBF_CUDA(cudaMallocAsync(&key_u, 8ull * (n_u + 1), st));
-  BBF_CUDA(cudaMallocAsync(&key_v, 8ull * (n_v + 1), st));
-  BBF_CUDA(cudaMallocAsync(&skey_u, 8ull * (n_u + 1), st));
-  BBF_CUDA(cudaMallocAsync(&skey_v, 8ull * (n_v + 1), st));
-  BBF_CUDA(cudaMallocAsync(&dv, 4ull * (n_v + 1), st));
-  BBF_CUDA(cudaMallocAsync(&lr_u, 4ull * (n_u + 1), st));
-  BBF_CUDA(cudaMallocAsync(&lr_v, 4ull * (n_v + 1), st));
+  BBF_CUDA(dmalloc(&key_u, 8ull * (n_u + 1), st));
+  BBF_CUDA(dmalloc(&key_v, 8ull * (n_v + 1), st));
+  BBF_CUDA(dmalloc(&skey_u, 8ull * (n_u + 1), st));
+  BBF_CUDA(dmalloc(&skey_v, 8ull * (n_v + 1), st));
+  BBF_CUDA(dmalloc(&dv, 4ull * (n_v + 1), st));
+  BBF_CUDA(dmalloc(&lr_u, 4ull * (n_u + 1), st));
+  BBF_CUDA(dmalloc(&lr_v, 4ull * (n_v + 1), st));
   BBF_CUDA(cudaMemsetAsync(dv, 0, 4ull * (n_v + 1), st));
   if (n_u) k_keys_u<<<grid_for(n_u, 256, 1u << 30), 256, 0, st>>>(d_rp, n_u, key_u);
   if (nnz) k_hist_v<<<grid_for(nnz, 256), 256, 0, st>>>(d_col, nnz, dv);
@@ -304,18 +304,18 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   cub::DeviceScan::InclusiveSum(nullptr, t5, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n, st);
   tmp_bytes = std::max(tmp_bytes, t5);
   void* tmp;
-  BBF_CUDA(cudaMallocAsync(&tmp, tmp_bytes + 16, st));
+  BBF_CUDA(dmalloc(&tmp, tmp_bytes + 16, st));
   if (n_u) BBF_CUDA(cub::DeviceRadixSort::SortKeysDescending(tmp, t1, key_u, skey_u, (int)n_u, 0, kbits, st));
   if (n_v) BBF_CUDA(cub::DeviceRadixSort::SortKeysDescending(tmp, t2, key_v, skey_v, (int)n_v, 0, kbits, st));
   g->launches += 8;
 
-  BBF_CUDA(cudaMallocAsync(&g->inv, 4ull * (n + 1), st));
-  BBF_CUDA(cudaMallocAsync(&g->degs, 4ull * (n + 1), st));
-  BBF_CUDA(cudaMallocAsync(&g->off, 4ull * (n + 1), st));
-  BBF_CUDA(cudaMallocAsync(&g->mid, 4ull * (n + 1), st));
-  BBF_CUDA(cudaMallocAsync(&g->end1, 4ull * (n + 1), st));
-  BBF_CUDA(cudaMallocAsync(&g->adj, 4ull * (m + 1), st));
-  BBF_CUDA(cudaMallocAsync(&g->degpre, 8ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&g->inv, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&g->degs, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&g->off, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&g->mid, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&g->end1, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&g->adj, 4ull * (m + 1), st));
+  BBF_CUDA(dmalloc(&g->degpre, 8ull * (n + 1), st));
   if (n_u) k_rank_tables<<<grid_for(n_u, 256, 1u << 30), 256, 0, st>>>(skey_u, n_u, 0, 0, g->inv, g->degs, lr_u);
   if (n_v) k_rank_tables<<<grid_for(n_v, 256, 1u << 30), 256, 0, st>>>(skey_v, n_v, n_u, n_u, g->inv, g->degs, lr_v);
   g->launches += 2;
@@ -323,14 +323,14 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   // S4: rank-space adjacency, one radix sort of the 2*nnz directed entries
   if (m) {
     uint64_t *ek, *eks;
-    BBF_CUDA(cudaMallocAsync(&ek, 8ull * m, st));
-    BBF_CUDA(cudaMallocAsync(&eks, 8ull * m, st));
+    BBF_CUDA(dmalloc(&ek, 8ull * m, st));
+    BBF_CUDA(dmalloc(&eks, 8ull * m, st));
     k_entries<<<grid_for(nnz, 256), 256, 0, st>>>(d_rp, d_col, d_sg, nnz, n_u, lr_u, lr_v, ek);
     BBF_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t3, ek, eks, (int64_t)m, 0, ebits, st));
     k_decode<<<grid_for(m, 256), 256, 0, st>>>(eks, m, g->adj, d_err);
     g->launches += 6;
-    cudaFreeAsync(ek, st);
-    cudaFreeAsync(eks, st);
+    dfree(ek, st);
+    dfree(eks, st);
   }
   // row offsets: exclusive scan of degrees in row order (rows U by rank, then V by rank)
   BBF_CUDA(cudaMemsetAsync(g->degs + n, 0, 4, st));
@@ -339,7 +339,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
 
   // zone boundaries per side (rank counts of degree thresholds)
   unsigned long long* d_cnt;
-  BBF_CUDA(cudaMallocAsync(&d_cnt, 16 * sizeof(unsigned long long), st));
+  BBF_CUDA(dmalloc(&d_cnt, 16 * sizeof(unsigned long long), st));
   BBF_CUDA(cudaMemsetAsync(d_cnt, 0, 16 * sizeof(unsigned long long), st));
   k_count_ge<<<1, 32, 0, st>>>(g->degs, 0, n_u, d_cnt);
   k_count_ge<<<1, 32, 0, st>>>(g->degs, n_u, n_v, d_cnt + 6);
@@ -373,11 +373,11 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     g->ws_bound = std::min(bu, bv);
   }
   if (h_err & kErrDup) {
-    cudaFreeAsync(tmp, st);
+    dfree(tmp, st);
     cleanup_input();
-    cudaFreeAsync(key_u, st); cudaFreeAsync(key_v, st); cudaFreeAsync(skey_u, st);
-    cudaFreeAsync(skey_v, st); cudaFreeAsync(dv, st); cudaFreeAsync(lr_u, st); cudaFreeAsync(lr_v, st);
-    cudaFreeAsync(d_cnt, st); cudaFreeAsync(d_err, st);
+    dfree(key_u, st); dfree(key_v, st); dfree(skey_u, st);
+    dfree(skey_v, st); dfree(dv, st); dfree(lr_u, st); dfree(lr_v, st);
+    dfree(d_cnt, st); dfree(d_err, st);
     cudaStreamSynchronize(st);
     set_error("duplicate (u,v) edge");
     return BBF_EDUP;
@@ -387,11 +387,11 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
                                                       g->L4[0], g->L4[1], g->mid, g->end1);
     // inclusive prefix of degrees over rows (u64), used to split hub end-ranges by expected work
     uint64_t* d64;
-    BBF_CUDA(cudaMallocAsync(&d64, 8ull * n, st));
+    BBF_CUDA(dmalloc(&d64, 8ull * n, st));
     k_u32_to_u64<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(g->degs, n, d64);
     BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp, t5, d64, g->degpre, (int)n, st));
     g->launches += 3;
-    cudaFreeAsync(d64, st);
+    dfree(d64, st);
   }
   // hub-kernel counter addresses and window runs (DESIGN.md §"Counter windows")
   for (int s2 = 0; s2 < 2; ++s2)
@@ -402,12 +402,12 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   g->compact = g->zones[0].L[0] == 0 && g->zones[1].L[0] == 0 && g->zones[0].WB[5] <= kCpWordMask &&
                g->zones[1].WB[5] <= kCpWordMask && !getenv("BBF_NO_COMPACT");  // env: test hook
   const uint32_t wmask = g->compact ? kCpWordMask : kCWordMask;
-  BBF_CUDA(cudaMallocAsync(&g->adjc, 4ull * (m + 8), st));  // padded: 16-B chunk loads
-  BBF_CUDA(cudaMallocAsync(&g->runid, 4ull * (m + 1), st));
+  BBF_CUDA(dmalloc(&g->adjc, 4ull * (m + 8), st));  // padded: 16-B chunk loads
+  BBF_CUDA(dmalloc(&g->runid, 4ull * (m + 1), st));
   g->nruns = 0;
   if (m) {
     uint32_t* flag;
-    BBF_CUDA(cudaMallocAsync(&flag, 4ull * (m + 1), st));
+    BBF_CUDA(dmalloc(&flag, 4ull * (m + 1), st));
     BBF_CUDA(cudaMemsetAsync(flag, 0, 4ull * (m + 1), st));
     k_caddr<<<grid_for(m, 256), 256, 0, st>>>(g->adj, m, nnz, g->zones[0], g->zones[1], g->compact,
                                             g->adjc);
@@ -416,23 +416,23 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     size_t ts = 0;
     cub::DeviceScan::InclusiveSum(nullptr, ts, flag, g->runid, (int64_t)m, st);
     void* tmp2;
-    BBF_CUDA(cudaMallocAsync(&tmp2, ts + 16, st));
+    BBF_CUDA(dmalloc(&tmp2, ts + 16, st));
     BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp2, ts, flag, g->runid, (int64_t)m, st));
     BBF_CUDA(cudaMemcpyAsync(&g->nruns, g->runid + (m - 1), 4, cudaMemcpyDeviceToHost, st));
     BBF_CUDA(cudaStreamSynchronize(st));
-    BBF_CUDA(cudaMallocAsync(&g->runs, sizeof(uint2) * (g->nruns + 1), st));
+    BBF_CUDA(dmalloc(&g->runs, sizeof(uint2) * (g->nruns + 1), st));
     k_runs<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, flag, m, wmask, g->runid, g->runs);
     g->launches += 6;
-    cudaFreeAsync(tmp2, st);
-    cudaFreeAsync(flag, st);
+    dfree(tmp2, st);
+    dfree(flag, st);
   } else {
-    BBF_CUDA(cudaMallocAsync(&g->runs, sizeof(uint2), st));
+    BBF_CUDA(dmalloc(&g->runs, sizeof(uint2), st));
   }
-  cudaFreeAsync(tmp, st);
+  dfree(tmp, st);
   cleanup_input();
-  cudaFreeAsync(key_u, st); cudaFreeAsync(key_v, st); cudaFreeAsync(skey_u, st);
-  cudaFreeAsync(skey_v, st); cudaFreeAsync(dv, st); cudaFreeAsync(lr_u, st); cudaFreeAsync(lr_v, st);
-  cudaFreeAsync(d_cnt, st); cudaFreeAsync(d_err, st);
+  dfree(key_u, st); dfree(key_v, st); dfree(skey_u, st);
+  dfree(skey_v, st); dfree(dv, st); dfree(lr_u, st); dfree(lr_v, st);
+  dfree(d_cnt, st); dfree(d_err, st);
   BBF_CUDA(cudaGetLastError());
   return BBF_OK;
 }

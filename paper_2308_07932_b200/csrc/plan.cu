@@ -187,10 +187,10 @@ inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) 
 }  // namespace
 
 void free_plan(Plan* p, cudaStream_t st) {
-  if (p->ub) cudaFreeAsync(p->ub, st);
-  if (p->work) cudaFreeAsync(p->work, st);
-  if (p->t1) cudaFreeAsync(p->t1, st);
-  if (p->units) cudaFreeAsync(p->units, st);
+  if (p->ub) dfree(p->ub, st);
+  if (p->work) dfree(p->work, st);
+  if (p->t1) dfree(p->t1, st);
+  if (p->units) dfree(p->units, st);
   *p = Plan{};
 }
 
@@ -201,17 +201,17 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   free_plan(p, st);
   p->route = route;
   RouteRows rr{route, g->n_u, n};
-  BBF_CUDA(cudaMallocAsync(&p->ub, 4ull * (m + 1), st));
-  BBF_CUDA(cudaMallocAsync(&p->work, 8ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&p->ub, 4ull * (m + 1), st));
+  BBF_CUDA(dmalloc(&p->work, 8ull * (n + 1), st));
   uint64_t* len;
   uint32_t *sb, *se, *nunits, *ustart;
   unsigned long long* acc;
-  BBF_CUDA(cudaMallocAsync(&len, 8ull * (m + 1), st));
-  BBF_CUDA(cudaMallocAsync(&sb, 4ull * (n + 1), st));
-  BBF_CUDA(cudaMallocAsync(&se, 4ull * (n + 1), st));
-  BBF_CUDA(cudaMallocAsync(&nunits, 4ull * (n + 1), st));
-  BBF_CUDA(cudaMallocAsync(&ustart, 4ull * (n + 1), st));
-  BBF_CUDA(cudaMallocAsync(&acc, 8 * sizeof(unsigned long long), st));
+  BBF_CUDA(dmalloc(&len, 8ull * (m + 1), st));
+  BBF_CUDA(dmalloc(&sb, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&se, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&nunits, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&ustart, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&acc, 8 * sizeof(unsigned long long), st));
   BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
   BBF_CUDA(cudaMemsetAsync(p->work, 0, 8ull * (n + 1), st));
   if (m) {
@@ -226,9 +226,9 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
       size_t tb = 0;
       cub::DeviceScan::InclusiveSum(nullptr, tb, len, len, (int64_t)m, st);
       void* tmp;
-      BBF_CUDA(cudaMallocAsync(&tmp, tb + 16, st));
+      BBF_CUDA(dmalloc(&tmp, tb + 16, st));
       BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, len, len, (int64_t)m, st));
-      cudaFreeAsync(tmp, st);
+      dfree(tmp, st);
       g->launches += 2;
     }
     k_row_work<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, len, sb, se, p->work);
@@ -236,15 +236,15 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   }
   // pruned total, to size units
   unsigned long long* d_wp;
-  BBF_CUDA(cudaMallocAsync(&d_wp, 8, st));
+  BBF_CUDA(dmalloc(&d_wp, 8, st));
   {
     size_t tb = 0;
     cub::DeviceReduce::Sum(nullptr, tb, p->work, d_wp, (int)n, st);
     void* tmp;
-    BBF_CUDA(cudaMallocAsync(&tmp, tb + 16, st));
+    BBF_CUDA(dmalloc(&tmp, tb + 16, st));
     BBF_CUDA(cub::DeviceReduce::Sum(tmp, tb, p->work, d_wp, (int)n, st));
     g->launches += 1;
-    cudaFreeAsync(tmp, st);
+    dfree(tmp, st);
   }
   unsigned long long h_wp = 0, h_wf = 0;
   BBF_CUDA(cudaMemcpyAsync(&h_wp, d_wp, 8, cudaMemcpyDeviceToHost, st));
@@ -260,9 +260,9 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     k_tier<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, p->work, w_target, sb, se, nunits, acc);
     g->launches += 1;
   }
-  BBF_CUDA(cudaMallocAsync(&p->t1, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&p->t1, 4ull * (n + 1), st));
   uint32_t* d_nsel;
-  BBF_CUDA(cudaMallocAsync(&d_nsel, 8, st));
+  BBF_CUDA(dmalloc(&d_nsel, 8, st));
   {
     cub::CountingInputIterator<uint32_t> it(0);
     size_t tb = 0;
@@ -271,12 +271,12 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     cub::DeviceScan::ExclusiveSum(nullptr, tb2, nunits, ustart, (int)(n + 1), st);
     tb = std::max(tb, tb2);
     void* tmp;
-    BBF_CUDA(cudaMallocAsync(&tmp, tb + 16, st));
+    BBF_CUDA(dmalloc(&tmp, tb + 16, st));
     BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t1, d_nsel, (int)n, IsT1{p->work}, st));
     BBF_CUDA(cudaMemsetAsync(nunits + n, 0, 4, st));
     BBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nunits, ustart, (int)(n + 1), st));
     g->launches += 3;
-    cudaFreeAsync(tmp, st);
+    dfree(tmp, st);
   }
   uint32_t h_nsel = 0, h_nunits = 0;
   unsigned long long h_acc[3];
@@ -289,9 +289,9 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   p->W_t1 = h_acc[0];
   p->W_t3 = h_acc[1];
   p->M_t3 = h_acc[2];
-  BBF_CUDA(cudaMallocAsync(&p->units, sizeof(Unit) * (h_nunits + 1), st));
+  BBF_CUDA(dmalloc(&p->units, sizeof(Unit) * (h_nunits + 1), st));
   unsigned int* d_maxmid;  // [0] max middles, [2..3] max work (u64)
-  BBF_CUDA(cudaMallocAsync(&d_maxmid, 16, st));
+  BBF_CUDA(dmalloc(&d_maxmid, 16, st));
   BBF_CUDA(cudaMemsetAsync(d_maxmid, 0, 16, st));
   if (n && h_nunits) {
     k_units<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, g->n_u, nunits, ustart, g->degpre,
@@ -312,15 +312,15 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
             (unsigned long long)p->W_t1, p->n_t1, (unsigned long long)p->W_t3, p->n_units,
             (unsigned long long)p->M_t3, p->max_mid, (unsigned long long)w_target, g->zones[0].WB[5],
             g->zones[1].WB[5]);
-  cudaFreeAsync(len, st);
-  cudaFreeAsync(sb, st);
-  cudaFreeAsync(se, st);
-  cudaFreeAsync(nunits, st);
-  cudaFreeAsync(ustart, st);
-  cudaFreeAsync(acc, st);
-  cudaFreeAsync(d_wp, st);
-  cudaFreeAsync(d_nsel, st);
-  cudaFreeAsync(d_maxmid, st);
+  dfree(len, st);
+  dfree(sb, st);
+  dfree(se, st);
+  dfree(nunits, st);
+  dfree(ustart, st);
+  dfree(acc, st);
+  dfree(d_wp, st);
+  dfree(d_nsel, st);
+  dfree(d_maxmid, st);
   BBF_CUDA(cudaGetLastError());
   p->valid = true;
   return BBF_OK;

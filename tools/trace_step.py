@@ -14,6 +14,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--out", default="gpurun_out/trace.json")
+    ap.add_argument("--steps", type=int, default=1)
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -37,7 +38,8 @@ def main():
         step()
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        step()
+        for _ in range(a.steps):
+            step()
         torch.cuda.synchronize()
     prof.export_chrome_trace(a.out)
     ev = json.load(open(a.out))["traceEvents"]
@@ -69,7 +71,7 @@ def main():
                  key=lambda e: -e.get("dur", 0))
     print("longest runtime API calls (ms):")
     for e in cpu[:15]:
-        print(f"  {1e-3*e.get('dur',0):8.3f}  {e['name']}")
+        print(f"  {1e-3*e.get('dur',0):8.3f}  {e['name']}  at +{1e-3*(e['ts']-t0):.1f} ms")
 
 
 if __name__ == "__main__":
