@@ -37,12 +37,30 @@ WORKLOADS = {
 
 
 def peaks():
+    """(HBM GB/s, source), (int8 dense TOP/s, source).  int8 is not in MEASURED_PEAKS.json: it is
+    the measured bf16 burst figure x 2, the guide's nominal int8 (4.5 POPS) / bf16 (2.25 PF) ratio."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        hbm = (float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)")
+        i8 = (2.0 * float(p["bf16_tflops"]),
+              "MEASURED_PEAKS.json bf16_tflops (burst) x 2 (nominal int8/bf16 ratio 4.5/2.25)")
     except Exception:
-        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+        hbm = (6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)")
+        i8 = (4500.0, "nominal B200 dense int8 4.5 POPS (no measured peak available)")
+    return hbm, i8
+
+
+def ncu_traffic(config: int, kernel: str):
+    """dram read+write bytes per launch of `kernel` on `config` from the committed ncu --set full
+    summary (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        e = t.get(f"{kernel}@{config}")
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
 
 
 class ClockSampler:
@@ -160,6 +178,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampler")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
@@ -208,17 +227,20 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     clk = ClockSampler(local)
-    clk.start()
+    if not args.no_clocks:
+        clk.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
     main_ms = []
     algo_bytes = 0
+    algo_ops = 0.0
     e0.record(stream)
     for _ in range(args.steps):
         tot, st = step()
         launches += st["kernel_launches"]
         main_ms.append(st["ms_main_kernel"])
         algo_bytes = st["algo_bytes"]
+        algo_ops = st["algo_ops"]
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -235,10 +257,18 @@ def main():
     value = W_G * args.steps / (ms * 1e-3)
     bfly = tot["balanced"] * args.steps / (ms * 1e-3)
 
-    # e2e: the same step through the public API with HOST buffers (H2D of the CSR and D2H of
-    # the per-vertex arrays inside the timed region)
+    # e2e: the same step through the public API with HOST buffers: the CSR in pinned host memory
+    # (H2D inside bbf_graph_load_csr) and the per-vertex arrays written back to pinned host
+    # memory (D2H inside bbf_count_per_vertex), every step inside the timed region
     e2e_ms = None
     if args.e2e_steps > 0:
+        h_rp = torch.from_numpy(g.row_ptr.view(np.int64)).pin_memory()
+        h_col = torch.from_numpy(g.col.view(np.int32)).pin_memory()
+        h_sg = torch.from_numpy(g.sign).pin_memory()
+        h_out = tuple(torch.zeros(k, dtype=torch.int64).pin_memory() for k in (n_u, n_u, n_v, n_v))
+        h = bbf.Graph(n_u, n_v, h_rp, h_col, h_sg, device=local, stream=stream, comm=comm)
+        h.count_per_vertex(out=h_out)  # warm-up of the host path
+        h.free()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -246,8 +276,8 @@ def main():
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(args.e2e_steps):
-            h = bbf.Graph(n_u, n_v, g.row_ptr, g.col, g.sign, device=local, stream=stream, comm=comm)
-            tot_e, bu, nu, bv, nv = h.count_per_vertex()
+            h = bbf.Graph(n_u, n_v, h_rp, h_col, h_sg, device=local, stream=stream, comm=comm)
+            tot_e = h.count_per_vertex(out=h_out)[0]
             h.free()
         t1.record(stream)
         torch.cuda.synchronize()
@@ -260,17 +290,21 @@ def main():
     h2d = g.row_ptr.nbytes + g.col.nbytes + g.sign.nbytes
     d2h = 8 * 2 * (n_u + n_v)
 
-    peak, peak_src = peaks()
+    (hbm_peak, hbm_src), (i8_peak, i8_src) = peaks()
     kms = float(np.mean(main_ms)) if main_ms else 0.0
-    achieved = algo_bytes / (kms * 1e-3) / 1e9 if kms > 0 else 0.0
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_k_t3_summary.json")) as f:
-            prof = json.load(f)
-        if prof.get("config") == args.config:
-            traffic = prof.get("dram_bytes_per_launch")
-    except Exception:
-        pass
+    if algo_ops > 0:  # dense int8 tensor-core path (k_dense_tiles)
+        achieved = algo_ops / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
+        roof = {"bound": "tensor", "kernel": "k_dense_tiles (tcgen05 kind::i8, T=AA^T and P=SS^T)",
+                "achieved": achieved, "peak": i8_peak, "peak_source": i8_src, "unit": "TOP/s (int8)",
+                "frac": achieved / i8_peak, "traffic": ncu_traffic(args.config, "k_dense_tiles"),
+                "algo_ops_per_launch": algo_ops}
+    else:  # sparse path, hub wedge-aggregation kernel
+        achieved = algo_bytes / (kms * 1e-3) / 1e9 if kms > 0 else 0.0
+        roof = {"bound": "hbm", "kernel": "k_t3 (hub wedge aggregation)",
+                "achieved": achieved, "peak": hbm_peak, "peak_source": hbm_src, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": ncu_traffic(args.config, "k_t3"),
+                "algo_bytes_per_launch": algo_bytes}
+    roof.update({"ms_per_launch": kms, "share_of_step": kms / ms_step if ms_step else None})
 
     line = {
         "metric": METRIC, "value": value, "unit": "wedges/s", "n_gpus": world,
@@ -287,11 +321,7 @@ def main():
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "k_t3 (hub wedge aggregation)",
-                     "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                     "frac": achieved / peak if peak else None, "traffic": traffic,
-                     "algo_bytes_per_launch": algo_bytes, "ms_per_launch": kms,
-                     "share_of_step": kms / ms_step if ms_step else None},
+        "roofline": roof,
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -126,6 +126,9 @@ class Graph:
         if dev:
             flags |= BBF_PTR_DEVICE
             keep = (row_ptr, col, sign)
+        elif _is_torch(row_ptr):  # host torch tensors (e.g. pinned): passed as they are
+            assert all(t.is_contiguous() for t in (row_ptr, col, sign))
+            keep = (row_ptr, col, sign)
         else:
             keep = (np.ascontiguousarray(row_ptr, dtype=np.uint64),
                     np.ascontiguousarray(col, dtype=np.uint32),
@@ -168,11 +171,13 @@ class Graph:
 
     def count_per_vertex(self, out=None, flags: int = 0):
         """Returns (totals dict, bal_u, unb_u, bal_v, unb_v).  `out` may be a tuple of four
-        torch CUDA uint64/int64 tensors (device outputs, BBF_PTR_DEVICE)."""
+        int64/uint64 torch tensors: CUDA tensors (device outputs, BBF_PTR_DEVICE) or host
+        tensors (e.g. pinned memory, written by the library's D2H copies)."""
         c = bbf_counts()
         if out is not None:
             bu, nu, bv, nv = out
-            flags |= BBF_PTR_DEVICE
+            if bu.is_cuda:
+                flags |= BBF_PTR_DEVICE
         else:
             bu, nu = np.zeros(self.n_u, np.uint64), np.zeros(self.n_u, np.uint64)
             bv, nv = np.zeros(self.n_v, np.uint64), np.zeros(self.n_v, np.uint64)

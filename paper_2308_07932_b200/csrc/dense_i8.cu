@@ -491,7 +491,9 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
     const unsigned grid = (unsigned)std::min<uint64_t>(g->num_sms, tl.size());
     k_dense_tiles<<<grid, kThreads, kSmemBytes, st>>>(mAi, mSi, mAj, mSj, da);
     g->launches++;
-    ops += 2.0 * 2.0 * (double)tl.size() * kBM * kBN * (double)k;
+    // algorithmic int8 ops: T and P over the n(n-1)/2 pairs, K MACs each, 2 ops/MAC
+    const double nr = side ? g->n_v : g->n_u, kk = side ? g->n_u : g->n_v;
+    ops += 2.0 * 2.0 * (nr * (nr - 1.0) / 2.0) * kk;
     err = cudaGetLastError();
     if (err != cudaSuccess) { status = cuda_status(err, "k_dense_tiles launch"); break; }
   }
