@@ -3,6 +3,8 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -89,8 +91,8 @@ __global__ void k_scatter_pv(const unsigned long long* __restrict__ pv, const ui
   uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= cnt) return;
   uint32_t id = inv[row0 + r];
-  if (ob) ob[id] = pv[row0 + r];
-  if (on) on[id] = pv[n + row0 + r];
+  if (ob) ob[id] = pv[2ull * (row0 + r)];       // (B, N) interleaved per row
+  if (on) on[id] = pv[2ull * (row0 + r) + 1];
 }
 
 bbf_status allreduce_u64(bbf_graph* g, unsigned long long* dbuf, size_t count) {
@@ -124,6 +126,15 @@ bbf_status do_count(bbf_graph* g, bool per_vertex, uint32_t flags, unsigned long
                     float* ms) {
   BBF_TRY(check_overflow(g));
   int rank = g->comm ? g->comm->rank : 0, nranks = g->comm ? g->comm->nranks : 1;
+  // test hook: BBF_FAKE_WORLD="r/N" counts only rank r's shard of an N-rank job on this single
+  // GPU (no collective), so tests can check that the shards of every rank sum to the full count
+  if (!g->comm && getenv("BBF_FAKE_WORLD")) {
+    int r = 0, N = 1;
+    if (sscanf(getenv("BBF_FAKE_WORLD"), "%d/%d", &r, &N) == 2 && N >= 1 && r >= 0 && r < N) {
+      rank = r;
+      nranks = N;
+    }
+  }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);

@@ -234,7 +234,7 @@ struct bbf_graph {
   uint32_t* scratch;  // per-CTA middle arrays
   size_t scratch_words;
   unsigned long long* d_acc;  // [0]=B [1]=N [2..] misc counters, [8]=unit cursor, [9]=t1 cursor
-  uint64_t* pv;              // 2*n per-vertex (B, N interleaved by array: pv[0..n), pv[n..2n))
+  uint64_t* pv;              // 2*n per-vertex counts, (B, N) interleaved per row: pv[2r], pv[2r+1]
   // stats
   uint64_t launches;
   uint64_t algo_bytes;  // algorithmic bytes of the last count's main kernel (sparse path)

@@ -251,8 +251,10 @@ __device__ __forceinline__ void epi_packed(const EngineArgs& a, const Zones& Z, 
     xN += fn;
     const uint32_t wrow = sb + lbase + f;
     if (PV) {
-      if (fb) atomicAdd(&a.pv[wrow], (unsigned long long)fb);  // skip zero REDs
-      if (fn) atomicAdd(&a.pv[a.n + wrow], (unsigned long long)fn);
+#ifndef BBF_T3_NO_END_RED
+      if (fb) atomicAdd(&a.pv[2ull * (wrow)], (unsigned long long)fb);  // skip zero REDs
+      if (fn) atomicAdd(&a.pv[2ull * (wrow) + 1], (unsigned long long)fn);
+#endif
     }
     if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
   }
@@ -270,8 +272,8 @@ __device__ __forceinline__ void epi_wide(const EngineArgs& a, uint32_t sb, uint3
   xN += fn;
   const uint32_t wrow = sb + (gw >> 1);
   if (PV) {
-    if (fb) atomicAdd(&a.pv[wrow], fb);
-    if (fn) atomicAdd(&a.pv[a.n + wrow], fn);
+    if (fb) atomicAdd(&a.pv[2ull * (wrow)], fb);
+    if (fn) atomicAdd(&a.pv[2ull * (wrow) + 1], fn);
   }
   if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
 }
@@ -504,8 +506,8 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             const uint32_t cb = sh_acc[warp][0][lane], cn = sh_acc[warp][1][lane];
             if (cb | cn) {
               const uint32_t vr = ob + (rc.wv & kMask);
-              if (cb) atomicAdd(&a.pv[vr], (unsigned long long)cb);
-              if (cn) atomicAdd(&a.pv[a.n + vr], (unsigned long long)cn);
+              if (cb) atomicAdd(&a.pv[2ull * (vr)], (unsigned long long)cb);
+              if (cn) atomicAdd(&a.pv[2ull * (vr) + 1], (unsigned long long)cn);
             }
             __syncwarp();
           }
@@ -573,8 +575,8 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
         b = warp_sum(lane < kT3Warps ? sh_red[0][lane] : 0ull);
         nn = warp_sum(lane < kT3Warps ? sh_red[1][lane] : 0ull);
         if (lane == 0 && (b | nn)) {
-          atomicAdd(&a.pv[x], b);
-          atomicAdd(&a.pv[a.n + x], nn);
+          atomicAdd(&a.pv[2ull * (x)], b);
+          atomicAdd(&a.pv[2ull * (x) + 1], nn);
         }
       }
     }
@@ -697,8 +699,8 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
           uint32_t b2 = sh_mb[lane], n2 = sh_mn[lane];
           if (b2 | n2) {
             uint32_t vr = ob + (wv & kMask);
-            atomicAdd(&a.pv[vr], (unsigned long long)b2);
-            atomicAdd(&a.pv[a.n + vr], (unsigned long long)n2);
+            atomicAdd(&a.pv[2ull * (vr)], (unsigned long long)b2);
+            atomicAdd(&a.pv[2ull * (vr) + 1], (unsigned long long)n2);
           }
           sh_mb[lane] = 0;
           sh_mn[lane] = 0;
@@ -721,8 +723,8 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
       xN += fn;
       uint32_t wrow = sb + key - 1;
       if (PV) {
-        atomicAdd(&a.pv[wrow], fb);
-        atomicAdd(&a.pv[a.n + wrow], fn);
+        atomicAdd(&a.pv[2ull * (wrow)], fb);
+        atomicAdd(&a.pv[2ull * (wrow) + 1], fn);
       }
       if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
     }
@@ -733,8 +735,8 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
       xB = warp_sum(xB);
       xN = warp_sum(xN);
       if (lane == 0 && (xB | xN)) {
-        atomicAdd(&a.pv[x], xB);
-        atomicAdd(&a.pv[a.n + x], xN);
+        atomicAdd(&a.pv[2ull * (x)], xB);
+        atomicAdd(&a.pv[2ull * (x) + 1], xN);
       }
     }
   }

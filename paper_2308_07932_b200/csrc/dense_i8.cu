@@ -297,8 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       totN += rN;
       if (a.pv) {
         if ((rB | rN) && i < a.n_rows) {
-          atomicAdd(&a.pv[a.pv_row0 + i], rB);
-          atomicAdd(&a.pv[a.n + a.pv_row0 + i], rN);
+          atomicAdd(&a.pv[2ull * (a.pv_row0 + i)], rB);
+          atomicAdd(&a.pv[2ull * (a.pv_row0 + i) + 1], rN);
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         for (uint32_t jj = etid; jj < kBN; jj += 128) {
@@ -307,8 +307,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           colN[jj] = 0;
           const uint32_t j = j0 + jj;
           if ((b | nn) && j < a.n_rows) {
-            atomicAdd(&a.pv[a.pv_row0 + j], b);
-            atomicAdd(&a.pv[a.n + a.pv_row0 + j], nn);
+            atomicAdd(&a.pv[2ull * (a.pv_row0 + j)], b);
+            atomicAdd(&a.pv[2ull * (a.pv_row0 + j) + 1], nn);
           }
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
