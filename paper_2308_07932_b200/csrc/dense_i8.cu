@@ -331,6 +331,245 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ============================================================================ CTA-pair kernel
+// k_dense_pair: the same computation on 256 x 256 tiles with tcgen05.mma.cta_group::2 (M = 256,
+// N = 256) by a cluster of 2 CTAs on one TPC.  CTA r of the pair loads rows [128r, 128r + 128)
+// of the i-block (A_i, S_i: the MMA's A operand halves) and of the j-block (A_j, S_j: the B
+// operand halves) into its own 3-stage ring (64 KB per stage), both completing on the leader's
+// full barrier; the leader issues the MMAs, which read both CTAs' shared memory and accumulate
+// rows [128r, 128r + 128) of T and P in CTA r's TMEM.  Each CTA's epilogue handles its 128 rows
+// exactly as in k_dense_tiles.  Operand traffic per MAC is 2/3 of the single-CTA kernel's.
+constexpr uint32_t kPB = 256;                     // pair tile (rows i and rows j)
+constexpr uint32_t kPStages = 3;
+constexpr uint32_t kPHalf = 128 * kBK;            // 16 KB: one operand half (128 rows x 128 B)
+constexpr uint32_t kPStageBytes = 4 * kPHalf;     // A_i, S_i, A_j, S_j halves = 64 KB
+constexpr size_t kPSmemBytes = kPStages * kPStageBytes + 1024 + 2 * kBN * 8 + 256;
+constexpr uint32_t kIdescT2 = (2u << 4) | (0u << 7) | (0u << 10) | ((kPB >> 3) << 17) | ((kPB >> 4) << 24);
+constexpr uint32_t kIdescP2 = (2u << 4) | (1u << 7) | (1u << 10) | ((kPB >> 3) << 17) | ((kPB >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA into this CTA's shared memory, completing on the leader's barrier (cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster,
+                                                 int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.cta_group::2"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// commit: arrive on the barrier at this offset in both CTAs of the pair when the MMAs finish
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_dense_pair(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mS,
+                 const DenseArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned long long* colB = reinterpret_cast<unsigned long long*>(smem + kPStages * kPStageBytes);
+  unsigned long long* colN = colB + kBN;
+  __shared__ __align__(8) uint64_t bar_full[kPStages], bar_empty[kPStages], bar_tfull, bar_tempty;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  for (uint32_t i = threadIdx.x; i < 2 * kBN; i += kThreads) colB[i] = 0;
+  if (threadIdx.x == 0) {
+    for (uint32_t st = 0; st < kPStages; ++st) {
+      mbar_init(smem_u32(&bar_full[st]), 1);
+      mbar_init(smem_u32(&bar_empty[st]), 1);
+    }
+    mbar_init(smem_u32(&bar_tfull), 1);
+    mbar_init(smem_u32(&bar_tempty), 2 * 4);  // one arrival per epilogue warp of both CTAs
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tmem_base_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    // ================================================================ TMA producer (both CTAs)
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mS)) : "memory");
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t t = pair * a.nranks + a.rank; t < a.n_tiles; t += npairs * a.nranks) {
+        const uint2 tile = a.tiles[t];
+        const int32_t ri = (int32_t)(tile.x * kPB + crank * 128), rj = (int32_t)(tile.y * kPB + crank * 128);
+        for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
+          mbar_wait(smem_u32(&bar_empty[stage]), phase ^ 1u);
+          const uint32_t fb = mapa_rank(smem_u32(&bar_full[stage]), 0);
+          if (leader) mbar_arrive_expect_tx(smem_u32(&bar_full[stage]), 2 * kPStageBytes);
+          const uint32_t base = smem_u32(smem + stage * kPStageBytes);
+          const int32_t k0 = (int32_t)(kb * kBK);
+          tma_load_2d_pair(base, &mA, fb, k0, ri);
+          tma_load_2d_pair(base + kPHalf, &mS, fb, k0, ri);
+          tma_load_2d_pair(base + 2 * kPHalf, &mA, fb, k0, rj);
+          tma_load_2d_pair(base + 3 * kPHalf, &mS, fb, k0, rj);
+          if (++stage == kPStages) { stage = 0; phase ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================================ MMA issuer (leader only)
+    if (leader && lane == 0) {
+      uint32_t stage = 0, phase = 0, lt = 0;
+      for (uint32_t t = pair * a.nranks + a.rank; t < a.n_tiles; t += npairs * a.nranks, ++lt) {
+        if (lt > 0) {
+          mbar_wait(smem_u32(&bar_tempty), (lt - 1) & 1u);
+          tc_fence_after();
+        }
+        for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
+          mbar_wait(smem_u32(&bar_full[stage]), phase);
+          tc_fence_after();
+          const uint32_t base = smem_u32(smem + stage * kPStageBytes);
+#pragma unroll
+          for (uint32_t kk = 0; kk < kBK / 32; ++kk) {
+            const uint32_t acc = (kb | kk) ? 1u : 0u;
+            const uint32_t off = kk * 32;
+            mma_i8_pair(tmem, smem_desc(base + off), smem_desc(base + 2 * kPHalf + off), kIdescT2, acc);
+            mma_i8_pair(tmem + kBN, smem_desc(base + kPHalf + off), smem_desc(base + 3 * kPHalf + off),
+                        kIdescP2, acc);
+          }
+          mma_commit_pair(smem_u32(&bar_empty[stage]));  // frees the stage in both CTAs
+          if (++stage == kPStages) { stage = 0; phase ^= 1u; }
+        }
+        mma_commit_pair(smem_u32(&bar_tfull));
+      }
+    }
+  } else {
+    // ================================================================ epilogue (warps 2..5)
+    const uint32_t q = (uint32_t)(warp & 3);
+    const uint32_t etid = threadIdx.x - kEpiWarp0 * 32;
+    const uint32_t tempty_leader = mapa_rank(smem_u32(&bar_tempty), 0);
+    unsigned long long totB = 0, totN = 0;
+    uint32_t lt = 0;
+    for (uint32_t t = pair * a.nranks + a.rank; t < a.n_tiles; t += npairs * a.nranks, ++lt) {
+      const uint2 tile = a.tiles[t];
+      const uint32_t i = tile.x * kPB + crank * 128 + q * 32 + lane;  // this thread's row
+      const uint32_t j0 = tile.y * kPB;
+      const bool diag = tile.x == tile.y;
+      mbar_wait(smem_u32(&bar_tfull), lt & 1u);
+      tc_fence_after();
+      unsigned long long rB = 0, rN = 0;
+#pragma unroll 1
+      for (uint32_t c = 0; c < kBN / 32; ++c) {
+        uint32_t tv[32], pv[32];
+        const uint32_t ta = tmem + ((q * 32) << 16) + c * 32;
+        tmem_ld32(ta, tv);
+        tmem_ld32(ta + kBN, pv);
+        tmem_wait_ld();
+        unsigned long long vb[32], vn[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const uint32_t tt = tv[e], pp = pv[e];
+          const uint32_t ad = (tt + pp) >> 1, dd = (tt - pp) >> 1;
+          uint32_t fb = ((ad * (ad - 1u)) >> 1) + ((dd * (dd - 1u)) >> 1);
+          uint32_t fn = ad * dd;
+          if (diag && j0 + c * 32 + (uint32_t)e <= i) { fb = 0; fn = 0; }
+          rB += fb;
+          rN += fn;
+          vb[e] = fb;
+          vn[e] = fn;
+        }
+        if (a.pv) {
+          xpose_step<16>(vb, lane); xpose_step<16>(vn, lane);
+          xpose_step<8>(vb, lane);  xpose_step<8>(vn, lane);
+          xpose_step<4>(vb, lane);  xpose_step<4>(vn, lane);
+          xpose_step<2>(vb, lane);  xpose_step<2>(vn, lane);
+          xpose_step<1>(vb, lane);  xpose_step<1>(vn, lane);
+          if (vb[0]) atomicAdd(&colB[c * 32 + lane], vb[0]);
+          if (vn[0]) atomicAdd(&colN[c * 32 + lane], vn[0]);
+        }
+      }
+      // this warp is done with TMEM: one arrival on the leader's tmem_empty barrier
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader)
+                     : "memory");
+      totB += rB;
+      totN += rN;
+      if (a.pv) {
+        if ((rB | rN) && i < a.n_rows) {
+          atomicAdd(&a.pv[2ull * (a.pv_row0 + i)], rB);
+          atomicAdd(&a.pv[2ull * (a.pv_row0 + i) + 1], rN);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (uint32_t jj = etid; jj < kBN; jj += 128) {
+          const unsigned long long b = colB[jj], nn = colN[jj];
+          colB[jj] = 0;
+          colN[jj] = 0;
+          const uint32_t j = j0 + jj;
+          if ((b | nn) && j < a.n_rows) {
+            atomicAdd(&a.pv[2ull * (a.pv_row0 + j)], b);
+            atomicAdd(&a.pv[2ull * (a.pv_row0 + j) + 1], nn);
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      totB += __shfl_xor_sync(0xffffffffu, totB, o);
+      totN += __shfl_xor_sync(0xffffffffu, totN, o);
+    }
+    if (lane == 0 && (totB | totN)) {
+      atomicAdd(&a.acc[0], totB);
+      atomicAdd(&a.acc[1], totN);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// upper-triangle pair tiles (I <= J over 256-row blocks), J outer
+std::vector<uint2> pair_tile_list(uint32_t rows_pad) {
+  std::vector<uint2> t;
+  const uint32_t nb = rows_pad / kPB;
+  for (uint32_t J = 0; J < nb; ++J)
+    for (uint32_t I = 0; I <= J; ++I) t.push_back(make_uint2(I, J));
+  return t;
+}
+
 // A (0/1, u8) and S (+1/-1, s8) rows of both sides from the rank-space CSR: entry e of row x
 // sets column l(y) of row x's side matrix
 __global__ void k_dense_fill(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
@@ -452,6 +691,7 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
   }
   BBF_CUDA(cudaMemsetAsync(g->d_acc, 0, 16 * sizeof(unsigned long long), st));
   BBF_CUDA(cudaFuncSetAttribute(k_dense_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+  BBF_CUDA(cudaFuncSetAttribute(k_dense_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmemBytes));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -465,14 +705,17 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
     const uint64_t rows_pad = side ? rv : ru, k = side ? kv : ku;
     uint8_t* A = side ? Av : Au;
     uint8_t* S = side ? Sv : Su;
+    const bool pair_kernel = !getenv("BBF_DENSE_1CTA");
     CUtensorMap mAi, mSi, mAj, mSj;
-    if (!make_map(&mAi, A, rows_pad, k, kBM) || !make_map(&mSi, S, rows_pad, k, kBM) ||
-        !make_map(&mAj, A, rows_pad, k, kBN) || !make_map(&mSj, S, rows_pad, k, kBN)) {
+    bool ok = pair_kernel ? (make_map(&mAi, A, rows_pad, k, 128) && make_map(&mSi, S, rows_pad, k, 128))
+                          : (make_map(&mAi, A, rows_pad, k, kBM) && make_map(&mSi, S, rows_pad, k, kBM) &&
+                             make_map(&mAj, A, rows_pad, k, kBN) && make_map(&mSj, S, rows_pad, k, kBN));
+    if (!ok) {
       set_error("cuTensorMapEncodeTiled failed");
       status = BBF_ECUDA;
       break;
     }
-    std::vector<uint2> tl = tile_list((uint32_t)rows_pad);
+    std::vector<uint2> tl = pair_kernel ? pair_tile_list((uint32_t)rows_pad) : tile_list((uint32_t)rows_pad);
     cudaError_t err = dmalloc(&dtiles[side], sizeof(uint2) * (tl.size() + 1), st);
     if (err == cudaSuccess)
       err = cudaMemcpyAsync(dtiles[side], tl.data(), sizeof(uint2) * tl.size(), cudaMemcpyHostToDevice, st);
@@ -488,8 +731,13 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
     da.nranks = nranks;
     da.pv = per_vertex ? (unsigned long long*)g->pv : nullptr;
     da.acc = g->d_acc + 2 * side;
-    const unsigned grid = (unsigned)std::min<uint64_t>(g->num_sms, tl.size());
-    k_dense_tiles<<<grid, kThreads, kSmemBytes, st>>>(mAi, mSi, mAj, mSj, da);
+    if (pair_kernel) {
+      const unsigned pairs = (unsigned)std::min<uint64_t>(g->num_sms / 2, tl.size());
+      k_dense_pair<<<2 * pairs, kThreads, kPSmemBytes, st>>>(mAi, mSi, da);
+    } else {
+      const unsigned grid = (unsigned)std::min<uint64_t>(g->num_sms, tl.size());
+      k_dense_tiles<<<grid, kThreads, kSmemBytes, st>>>(mAi, mSi, mAj, mSj, da);
+    }
     g->launches++;
     // algorithmic int8 ops: T and P over the n(n-1)/2 pairs, K MACs each, 2 ops/MAC
     const double nr = side ? g->n_v : g->n_u, kk = side ? g->n_u : g->n_v;
