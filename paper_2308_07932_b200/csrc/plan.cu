@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "bbf_internal.cuh"
 
@@ -304,6 +305,20 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   BBF_CUDA(cudaStreamSynchronize(st));
   p->max_mid = h_maxmid[0];
   p->max_work = *(unsigned long long*)(h_maxmid + 2);
+  if (getenv("BBF_DEBUG") && atoi(getenv("BBF_DEBUG")) >= 2) {  // work histogram by log2 bucket
+    std::vector<uint64_t> hw(n);
+    cudaMemcpy(hw.data(), p->work, 8ull * n, cudaMemcpyDeviceToHost);
+    unsigned long long cnt[40] = {0}, sum[40] = {0};
+    for (uint32_t x = 0; x < n; ++x) {
+      if (!hw[x]) continue;
+      int b = 0;
+      while ((2ull << b) <= hw[x]) ++b;
+      cnt[b]++;
+      sum[b] += hw[x];
+    }
+    for (int b = 0; b < 40; ++b)
+      if (cnt[b]) fprintf(stderr, "[bbf]   work [2^%d, 2^%d): %llu starts, %llu wedges\n", b, b + 1, cnt[b], sum[b]);
+  }
   if (getenv("BBF_DEBUG"))
     fprintf(stderr,
             "[bbf] plan route=%d W_full=%llu W_pruned=%llu W_t1=%llu (%u starts) W_t3=%llu (%u units) "
