@@ -119,6 +119,10 @@ __device__ unsigned long long g_prof_cnt[4];  // nonzero counter words, contribu
 #define T3_MARK(slot) do {} while (0)
 #endif
 constexpr int kU = 1;  // flattened steps per iteration of the hub kernel's record loop
+#ifndef BBF_T3_CE
+#define BBF_T3_CE 8
+#endif
+constexpr uint32_t kCE = BBF_T3_CE;  // adjacency entries per lane per step (16-B aligned chunks)
 constexpr int kEncWide = 0, kEncNarrow = 1, kEncCompact = 2;  // adjc encodings
 constexpr uint32_t kMaxWin = 256;
 
@@ -412,14 +416,24 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       // ---------------- pass 1 (Alg. 2 lines 9-14) and pass 2 (per-vertex shares)
 #pragma unroll 1
       for (int pass = 0; pass < (PV ? 2 : 1); ++pass) {
+        // batches of bsz records; the next batch's records are loaded while this one is
+        // processed (their global-load latency was the kernel's top stall)
+        auto fetch = [&](uint32_t& btx, Rec& rx) {
+          uint32_t b0 = 0;
+          if (lane == 0) b0 = atomicAdd(&sh_c[pass], 1u);
+          btx = __shfl_sync(0xffffffffu, b0, 0);
+          const uint32_t r = btx * bsz + lane;
+          rx = Rec{0, 0, 0, 0};
+          if (btx * bsz < nrec && (uint32_t)lane < bsz && r < nrec) rx = rw[r];
+        };
+        uint32_t bt_next;
+        Rec rc_next;
+        fetch(bt_next, rc_next);
         while (true) {
-          uint32_t bt = 0;
-          if (lane == 0) bt = atomicAdd(&sh_c[pass], 1u);
-          bt = __shfl_sync(0xffffffffu, bt, 0);
+          const uint32_t bt = bt_next;
+          const Rec rc = rc_next;
           if (bt * bsz >= nrec) break;
-          const uint32_t r = bt * bsz + lane;
-          Rec rc{0, 0, 0, 0};
-          if ((uint32_t)lane < bsz && r < nrec) rc = rw[r];
+          fetch(bt_next, rc_next);
           if (pass == 1) { sh_acc[warp][0][lane] = 0; sh_acc[warp][1][lane] = 0; __syncwarp(); }
           // The batch's records are flattened over the lanes in 16-B chunks of the adjacency
           // (4 entries, one LDG.128 per lane, consecutive lanes on consecutive chunks of a
@@ -427,7 +441,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           // lane L chunk base + L; its owner (the record holding it) is the last record starting
           // at or before it in this step (start bitmask + owner table), else the owner carried
           // over from the previous step.
-          const uint32_t nch = rc.len ? (rc.p + rc.len + 3) / 4 - rc.p / 4 : 0;
+          const uint32_t nch = rc.len ? (rc.p + rc.len + kCE - 1) / kCE - rc.p / kCE : 0;
           const uint32_t incl = warp_incl_scan(nch, lane), excl = incl - nch;
           const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
           int carry = 0;
@@ -439,7 +453,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           // the counter updates (hides the global-load latency behind the other steps' work)
           for (uint32_t base0 = 0; base0 < T; base0 += 32 * kU) {
             uint32_t smask[kU], ow[kU], gs[kU], ch[kU], o_p[kU], o_len[kU], o_wv[kU];
-            uint4 q[kU];
+            uint4 q[kU][kCE / 4];
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
               const uint32_t base = base0 + 32 * u;
@@ -456,22 +470,28 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
               o_p[u] = __shfl_sync(0xffffffffu, rc.p, ow[u]);
               o_len[u] = __shfl_sync(0xffffffffu, rc.len, ow[u]);
               o_wv[u] = __shfl_sync(0xffffffffu, rc.wv, ow[u]);
-              ch[u] = o_p[u] / 4 + (base + lane - o_excl);  // absolute 16-B chunk of adjc
+              ch[u] = o_p[u] / kCE + (base + lane - o_excl);  // absolute chunk of adjc (kCE entries)
             }
 #pragma unroll
             for (int u = 0; u < kU; ++u)
-              q[u] = (base0 + 32 * u + lane < T) ? reinterpret_cast<const uint4*>(adjc)[ch[u]]
-                                                  : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+              for (int h = 0; h < kCE / 4; ++h)
+                q[u][h] = (base0 + 32 * u + lane < T) ? reinterpret_cast<const uint4*>(adjc)[ch[u] * (kCE / 4) + h]
+                                                     : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
               const uint32_t c = base0 + 32 * u + lane;
               const uint32_t shamt = 22u + 5u * (o_wv[u] >> 31), oshamt = 49u - shamt;
               uint32_t cb = 0, cn = 0;
               if (c < T) {
-                const uint32_t e0 = 4 * ch[u];
-                const uint32_t ev[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+                const uint32_t e0 = kCE * ch[u];
+                uint32_t ev[kCE];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int h = 0; h < kCE / 4; ++h) {
+                  ev[4 * h] = q[u][h].x; ev[4 * h + 1] = q[u][h].y; ev[4 * h + 2] = q[u][h].z; ev[4 * h + 3] = q[u][h].w;
+                }
+#pragma unroll
+                for (int j = 0; j < kCE; ++j) {
                   const uint32_t e = e0 + j;
                   if (e >= o_p[u] && e < o_p[u] + o_len[u]) {
                     if (CP) {

@@ -402,7 +402,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   g->compact = g->zones[0].L[0] == 0 && g->zones[1].L[0] == 0 && g->zones[0].WB[5] <= kCpWordMask &&
                g->zones[1].WB[5] <= kCpWordMask && !getenv("BBF_NO_COMPACT");  // env: test hook
   const uint32_t wmask = g->compact ? kCpWordMask : kCWordMask;
-  BBF_CUDA(dmalloc(&g->adjc, 4ull * (m + 8), st));  // padded: 16-B chunk loads
+  BBF_CUDA(dmalloc(&g->adjc, 4ull * (m + 32), st));  // padded: 16-B chunk loads
   BBF_CUDA(dmalloc(&g->runid, 4ull * (m + 1), st));
   g->nruns = 0;
   if (m) {
