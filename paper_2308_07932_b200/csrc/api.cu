@@ -111,7 +111,16 @@ bbf_status check_overflow(bbf_graph* g) {
 }
 
 bbf_status ensure_plan_g(bbf_graph* g) {
+  BBF_TRY(ensure_adj(g));
   if (!g->plan_g.valid) BBF_TRY(make_plan(g, 0, &g->plan_g));
+  return BBF_OK;
+}
+
+// the paper's wedge count W_G of the graph (the "wedges" of wedges/s, reading R20)
+bbf_status wedges_g(bbf_graph* g, unsigned long long* w) {
+  if (g->wg_valid) { *w = g->W_G; return BBF_OK; }
+  BBF_TRY(ensure_plan_g(g));
+  *w = g->plan_g.W_full;
   return BBF_OK;
 }
 
@@ -140,7 +149,8 @@ bbf_status do_count(bbf_graph* g, bool per_vertex, uint32_t flags, unsigned long
   cudaEventCreate(&b);
   cudaEventRecord(a, g->stream);
   if (per_vertex) BBF_CUDA(cudaMemsetAsync(g->pv, 0, 16ull * g->n, g->stream));
-  bbf_status s = ensure_plan_g(g);  // W_G of the graph (and the sparse plan) either way
+  bbf_status s = BBF_OK;
+  if (!g->wg_valid) s = ensure_plan_g(g);  // W_G of the graph (and the sparse plan)
   if (s != BBF_OK) { cudaEventDestroy(a); cudaEventDestroy(b); return s; }
   if (use_dense(g, flags, per_vertex)) {
     if (!dense_supported(g)) {
@@ -149,7 +159,8 @@ bbf_status do_count(bbf_graph* g, bool per_vertex, uint32_t flags, unsigned long
     }
     s = run_dense(g, per_vertex, rank, nranks, BN);
   } else {
-    s = run_sparse(g, &g->plan_g, per_vertex, rank, nranks, BN);
+    s = ensure_plan_g(g);
+    if (s == BBF_OK) s = run_sparse(g, &g->plan_g, per_vertex, rank, nranks, BN);
   }
   if (s != BBF_OK) { cudaEventDestroy(a); cudaEventDestroy(b); return s; }
   if (g->comm && g->comm->nranks > 1) {
@@ -275,7 +286,8 @@ bbf_status bbf_graph_free(bbf_graph* g) {
   free_plan(&g->plan_s[0], g->stream);
   free_plan(&g->plan_s[1], g->stream);
   void* ptrs[] = {g->off, g->adj, g->mid, g->end1, g->inv, g->degs, g->degpre, g->scratch, g->d_acc, g->pv,
-                  g->adjc, g->runid, g->runs};
+                  g->adjc, g->runid, g->runs, g->skey, g->lr, g->in_rp, g->in_col, g->in_sg,
+                  g->dA[0], g->dA[1], g->dS[0], g->dS[1]};
   for (void* p : ptrs)
     if (p) dfree(p, g->stream);
   cudaStreamSynchronize(g->stream);
@@ -290,10 +302,12 @@ bbf_status bbf_count_global(bbf_graph* g, bbf_counts* out) {
   unsigned long long BN[2] = {0, 0};
   float ms = 0;
   BBF_TRY(do_count(g, false, g->load_flags, BN, &ms));
+  unsigned long long wg = 0;
+  BBF_TRY(wedges_g(g, &wg));
   out->balanced = BN[0];
   out->unbalanced = BN[1];
   out->total = BN[0] + BN[1];
-  out->wedges_G = g->plan_g.W_full;
+  out->wedges_G = wg;
   out->ms_count = ms;
   return BBF_OK;
 }
@@ -334,11 +348,12 @@ bbf_status bbf_count_per_vertex(bbf_graph* g, uint64_t* bal_u, uint64_t* unb_u, 
   if (stage) dfree(stage, st);
   BBF_CUDA(cudaStreamSynchronize(st));
   if (totals) {
-    BBF_TRY(ensure_plan_g(g));
+    unsigned long long wg = 0;
+    BBF_TRY(wedges_g(g, &wg));
     totals->balanced = BN[0];
     totals->unbalanced = BN[1];
     totals->total = BN[0] + BN[1];
-    totals->wedges_G = g->plan_g.W_full;
+    totals->wedges_G = wg;
     totals->ms_count = ms;
   }
   return BBF_OK;
@@ -352,6 +367,7 @@ bbf_status bbf_count_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* ou
   if (flags & ~(uint32_t)(BBF_FORCE_SPARSE)) { set_error("unsupported flags for topk"); return BBF_EINVAL; }
   BBF_CUDA(cudaSetDevice(g->device));
   BBF_TRY(check_overflow(g));
+  BBF_TRY(ensure_adj(g));
   return run_pairs_topk(g, side, k, out, n_out);
 }
 

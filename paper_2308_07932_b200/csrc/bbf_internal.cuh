@@ -224,6 +224,21 @@ struct bbf_graph {
   uint2* runs;        // nruns: {first entry, window id} of every maximal same-window run of a row
   uint32_t nruns;
   bool compact;       // adjc uses encode_caddr_compact (else encode_caddr + sign bit)
+  // build state: core arrays always; adjacency (adj, mid, end1, degpre, adjc, runid, runs) built
+  // at load for the sparse path, lazily (from the kept input CSR) after a dense load
+  uint64_t* skey;     // n   : priority keys deg << 32 | gid sorted descending, U then V
+  uint32_t* lr;       // n   : local rank by input id, U ids then V ids
+  uint64_t* in_rp;    // device copy of the input CSR, kept only after a dense load
+  uint32_t* in_col;
+  uint8_t* in_sg;
+  bool adj_built;
+  bool wg_valid;
+  unsigned long long W_G;  // paper wedge count (O(nnz) formula), valid if wg_valid
+  // dense operands (dense_i8.cu): per side A (u8 0/1) and S (s8 +-1/0), rows_pad x k_pad
+  uint8_t* dA[2];
+  uint8_t* dS[2];
+  uint64_t drows[2], dk[2];
+  bool dense_built;
   uint32_t L4[2];     // #vertices with degree >= 2 per side
   uint32_t Llong[2];  // #vertices with degree > 32 per side ("long" middles of the hub kernel)
   uint32_t maxdeg[2];
@@ -272,6 +287,10 @@ inline cudaError_t dmalloc(T** out, size_t bytes, cudaStream_t st) {
 }
 bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* col,
                        const uint8_t* sign, bool device_ptrs);
+bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, const uint8_t* d_sg);
+bbf_status ensure_adj(bbf_graph* g);
+bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col,
+                                const uint8_t* d_sg);
 bbf_status make_plan(bbf_graph* g, int route, Plan* p);
 void free_plan(Plan* p, cudaStream_t st);
 // run the sparse engine for a route; per_vertex -> accumulate into g->pv (rank space)

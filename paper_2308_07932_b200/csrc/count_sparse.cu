@@ -193,12 +193,14 @@ __device__ __forceinline__ void t3_share_c(const uint32_t* ctr, uint32_t word0, 
 // selects the bit this wedge increments; oshamt = 49 - shamt the other half of the field.
 // Counters are addressed through 32-bit shared-window addresses (cbase = shared address of
 // the window's word 0 minus 4 * word0), so an update is LOP + LEA + shifts + one ATOMS/RED.
+// volatile (ordered with each other and with barriers) but without a "memory" clobber, so the
+// compiler may still move the global chunk loads across them
 __device__ __forceinline__ void sh_red_add(uint32_t addr, uint32_t v) {
-  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));
 }
 __device__ __forceinline__ uint32_t sh_atom_add(uint32_t addr, uint32_t v) {
   uint32_t r;
-  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(addr), "r"(v) : "memory");
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(addr), "r"(v));
   return r;
 }
 __device__ __forceinline__ uint32_t sh_load(uint32_t addr) {

@@ -598,6 +598,44 @@ __global__ void k_dense_fill(const uint32_t* __restrict__ off, const uint32_t* _
   }
 }
 
+// A and S of both sides straight from the input U-side CSR (input ids -> local ranks)
+__global__ void k_dense_fill_input(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                                   const uint8_t* __restrict__ sg, uint64_t nnz, uint32_t n_u,
+                                   const uint32_t* __restrict__ lr, uint8_t* __restrict__ Au,
+                                   uint8_t* __restrict__ Su, uint64_t ku, uint8_t* __restrict__ Av,
+                                   uint8_t* __restrict__ Sv, uint64_t kv) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = n_u;  // row: largest u with rp[u] <= e
+    while (hi - lo > 1) {
+      const uint32_t md = lo + (hi - lo) / 2;
+      if (rp[md] <= e) lo = md; else hi = md;
+    }
+    const uint64_t ru = lr[lo], rv = lr[n_u + col[e]];
+    const uint8_t s = sg[e] ? (uint8_t)1 : (uint8_t)0xFF;  // weight 1 = +1, 0 = -1
+    Au[ru * ku + rv] = 1;
+    Su[ru * ku + rv] = s;
+    Av[rv * kv + ru] = 1;
+    Sv[rv * kv + ru] = s;
+  }
+}
+
+// number of nonzero bytes (duplicate check: a duplicate (u,v) writes one cell twice)
+__global__ void k_count_nz(const uint4* __restrict__ a, uint64_t n16, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 q = a[i];
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t x = w[k];  // bytes are 0 or 1
+      c += __popc(x);
+    }
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -650,13 +688,59 @@ bool dense_supported(bbf_graph* g) {
 // dense-vs-sparse choice: estimated int8 tensor time of both sides vs the
 // sparse engine's measured wedge rate on W_pruned wedges
 bool dense_preferred(bbf_graph* g, bool per_vertex) {
-  if (!dense_supported(g) || !g->plan_g.valid) return false;
+  if (!dense_supported(g) || (!g->wg_valid && !g->plan_g.valid)) return false;
   const double nu = g->n_u, nv = g->n_v;
   const double cu = nu * nu * round_up(g->n_v, kBK), cv = nv * nv * round_up(g->n_u, kBK);
   const double ops = 2.0 * (per_vertex ? cu + cv : std::min(cu, cv));
   const double t_dense = ops / 2.5e15 + 1e-4;
-  const double t_sparse = (double)g->plan_g.W_pruned / 2.0e11 + 1e-4;
+  const double w = g->wg_valid ? (double)g->W_G : (double)g->plan_g.W_pruned;
+  const double t_sparse = w / 2.0e11 + 1e-4;
   return t_dense < t_sparse;
+}
+
+bbf_status alloc_dense_operands(bbf_graph* g) {
+  cudaStream_t st = g->stream;
+  g->drows[0] = round_up(std::max<uint32_t>(g->n_u, 1), kBN);
+  g->drows[1] = round_up(std::max<uint32_t>(g->n_v, 1), kBN);
+  g->dk[0] = round_up(std::max<uint32_t>(g->n_v, 1), kBK);
+  g->dk[1] = round_up(std::max<uint32_t>(g->n_u, 1), kBK);
+  for (int s2 = 0; s2 < 2; ++s2) {
+    const uint64_t bytes = g->drows[s2] * g->dk[s2];
+    BBF_CUDA(dmalloc(&g->dA[s2], bytes, st));
+    BBF_CUDA(dmalloc(&g->dS[s2], bytes, st));
+    BBF_CUDA(cudaMemsetAsync(g->dA[s2], 0, bytes, st));
+    BBF_CUDA(cudaMemsetAsync(g->dS[s2], 0, bytes, st));
+  }
+  return BBF_OK;
+}
+
+// dense operands of both sides from the input CSR (device arrays), with the duplicate-edge check
+// (SPEC.md:56): every edge sets one cell of A_U, so a duplicate leaves fewer than nnz ones
+bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col,
+                                const uint8_t* d_sg) {
+  cudaStream_t st = g->stream;
+  BBF_TRY(alloc_dense_operands(g));
+  if (g->nnz) {
+    unsigned grid = (unsigned)std::min<uint64_t>((g->nnz + 255) / 256, 148u * 64u);
+    k_dense_fill_input<<<grid, 256, 0, st>>>(d_rp, d_col, d_sg, g->nnz, g->n_u, g->lr, g->dA[0], g->dS[0],
+                                             g->dk[0], g->dA[1], g->dS[1], g->dk[1]);
+    unsigned long long* d_nz;
+    BBF_CUDA(dmalloc(&d_nz, 8, st));
+    BBF_CUDA(cudaMemsetAsync(d_nz, 0, 8, st));
+    const uint64_t n16 = g->drows[0] * g->dk[0] / 16;  // k padded to 128: whole uint4s
+    k_count_nz<<<148 * 8, 256, 0, st>>>(reinterpret_cast<const uint4*>(g->dA[0]), n16, d_nz);
+    g->launches += 2;
+    unsigned long long nz = 0;
+    BBF_CUDA(cudaMemcpyAsync(&nz, d_nz, 8, cudaMemcpyDeviceToHost, st));
+    BBF_CUDA(cudaStreamSynchronize(st));
+    dfree(d_nz, st);
+    if (nz != g->nnz) {
+      set_error("duplicate (u,v) edge");
+      return BBF_EDUP;
+    }
+  }
+  g->dense_built = true;
+  return BBF_OK;
 }
 
 bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsigned long long* host_BN) {
@@ -669,30 +753,29 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
     set_error("cuTensorMapEncodeTiled unavailable");
     return BBF_ECUDA;
   }
+  // operands of both sides, built once per graph (at load for dense graphs, else here from the
+  // rank-space adjacency) and kept until bbf_graph_free
+  if (!g->dense_built) {
+    if (g->in_rp) {
+      BBF_TRY(build_dense_operands(g, g->in_rp, g->in_col, g->in_sg));
+    } else {
+      BBF_TRY(ensure_adj(g));
+      BBF_TRY(alloc_dense_operands(g));
+      const uint64_t m = 2 * g->nnz;
+      if (m) {
+        unsigned grid = (unsigned)std::min<uint64_t>((m + 255) / 256, 148u * 64u);
+        k_dense_fill<<<grid, 256, 0, st>>>(g->off, g->adj, g->n, g->n_u, m, g->dA[0], g->dS[0], g->dk[0],
+                                           g->dA[1], g->dS[1], g->dk[1]);
+        g->launches++;
+      }
+      g->dense_built = true;
+    }
+  }
   // global only: the cheaper side (cost ~ rows^2 * K); per-vertex: both sides
   const bool do_u = per_vertex || (uint64_t)g->n_u * g->n_u * g->n_v <= (uint64_t)g->n_v * g->n_v * g->n_u;
   const bool do_v = per_vertex || !do_u;
-  const uint64_t ru = round_up(std::max<uint32_t>(g->n_u, 1), kBN), rv = round_up(std::max<uint32_t>(g->n_v, 1), kBN);
-  const uint64_t ku = round_up(std::max<uint32_t>(g->n_v, 1), kBK), kv = round_up(std::max<uint32_t>(g->n_u, 1), kBK);
-  uint8_t *Au = nullptr, *Su = nullptr, *Av = nullptr, *Sv = nullptr;
-  if (do_u) {
-    BBF_CUDA(dmalloc(&Au, ru * ku, st));
-    BBF_CUDA(dmalloc(&Su, ru * ku, st));
-    BBF_CUDA(cudaMemsetAsync(Au, 0, ru * ku, st));
-    BBF_CUDA(cudaMemsetAsync(Su, 0, ru * ku, st));
-  }
-  if (do_v) {
-    BBF_CUDA(dmalloc(&Av, rv * kv, st));
-    BBF_CUDA(dmalloc(&Sv, rv * kv, st));
-    BBF_CUDA(cudaMemsetAsync(Av, 0, rv * kv, st));
-    BBF_CUDA(cudaMemsetAsync(Sv, 0, rv * kv, st));
-  }
-  const uint64_t m = 2 * g->nnz;
-  if (m) {
-    unsigned grid = (unsigned)std::min<uint64_t>((m + 255) / 256, 148u * 64u);
-    k_dense_fill<<<grid, 256, 0, st>>>(g->off, g->adj, g->n, g->n_u, m, Au, Su, ku, Av, Sv, kv);
-    g->launches++;
-  }
+  const uint64_t ru = g->drows[0], rv = g->drows[1], ku = g->dk[0], kv = g->dk[1];
+  uint8_t *Au = g->dA[0], *Su = g->dS[0], *Av = g->dA[1], *Sv = g->dS[1];
   BBF_CUDA(cudaMemsetAsync(g->d_acc, 0, 16 * sizeof(unsigned long long), st));
   BBF_CUDA(cudaFuncSetAttribute(k_dense_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
   BBF_CUDA(cudaFuncSetAttribute(k_dense_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmemBytes));
@@ -760,7 +843,7 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
   if (status == BBF_OK) cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  for (void* p : {(void*)Au, (void*)Su, (void*)Av, (void*)Sv, (void*)dtiles[0], (void*)dtiles[1]})
+  for (void* p : {(void*)dtiles[0], (void*)dtiles[1]})
     if (p) dfree(p, st);
   if (status != BBF_OK) return status;
   BN_side[0][0] = h[0]; BN_side[0][1] = h[1];

@@ -225,14 +225,44 @@ inline int bits_for(uint64_t x) {
   return b;
 }
 
+// Paper wedge count W_G of Alg. 2 in O(nnz), without the sorted adjacency: for a
+// middle v, the eligible starts are its m_v neighbours of higher priority, and the k-th of them
+// (k = 0.. in priority order) sees deg(v) - 1 - k eligible ends, so v contributes
+// m_v (deg v - 1) - m_v (m_v - 1) / 2.  (Cross-checked against the plan's per-entry count.)
+__global__ void k_wg_m(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ col, uint64_t nnz,
+                       uint32_t n_u, const uint64_t* __restrict__ key_u, const uint64_t* __restrict__ key_v,
+                       uint32_t* __restrict__ mcnt) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = row_of_edge(rp, n_u, e), v = col[e];
+    if (key_u[u] > key_v[v]) atomicAdd(&mcnt[n_u + v], 1u);  // u is an eligible start for middle v
+    else atomicAdd(&mcnt[u], 1u);
+  }
+}
+
+__global__ void k_wg_sum(const uint32_t* __restrict__ mcnt, const uint64_t* __restrict__ key_u,
+                         const uint64_t* __restrict__ key_v, uint32_t n_u, uint32_t n,
+                         unsigned long long* __restrict__ out) {
+  unsigned long long s = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned long long mv = mcnt[i];
+    const unsigned long long d = (i < n_u ? key_u[i] : key_v[i - n_u]) >> 32;
+    if (mv) s += mv * (d - 1ull) - mv * (mv - 1ull) / 2ull;
+  }
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
 }  // namespace
 
+// S1-S3 and the row offsets / zones; then either the rank-space adjacency (S4, sparse path) or,
+// for a graph the dispatch rule sends to the dense path, the dense operands (adjacency deferred
+// until a sparse call needs it; the input CSR is then kept on the device).
 bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* col,
                        const uint8_t* sign, bool device_ptrs) {
   cudaStream_t st = g->stream;
   const uint32_t n_u = g->n_u, n_v = g->n_v, n = g->n;
   const uint64_t nnz = g->nnz;
-  const uint64_t m = 2 * nnz;
   // device copies of the input (S1)
   const uint64_t* d_rp = row_ptr;
   const uint32_t* d_col = col;
@@ -243,14 +273,20 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   if (!device_ptrs) {
     BBF_CUDA(dmalloc(&own_rp, sizeof(uint64_t) * (n_u + 1), st));
     BBF_CUDA(cudaMemcpyAsync(own_rp, row_ptr, sizeof(uint64_t) * (n_u + 1), cudaMemcpyHostToDevice, st));
+    BBF_CUDA(dmalloc(&own_col, sizeof(uint32_t) * (nnz + 1), st));
+    BBF_CUDA(dmalloc(&own_sg, nnz + 1, st));
     if (nnz) {
-      BBF_CUDA(dmalloc(&own_col, sizeof(uint32_t) * nnz, st));
-      BBF_CUDA(dmalloc(&own_sg, nnz, st));
       BBF_CUDA(cudaMemcpyAsync(own_col, col, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice, st));
       BBF_CUDA(cudaMemcpyAsync(own_sg, sign, nnz, cudaMemcpyHostToDevice, st));
     }
     d_rp = own_rp; d_col = own_col; d_sg = own_sg;
   }
+  auto cleanup_input = [&]() {
+    if (own_rp) dfree(own_rp, st);
+    if (own_col) dfree(own_col, st);
+    if (own_sg) dfree(own_sg, st);
+    own_rp = nullptr; own_col = nullptr; own_sg = nullptr;
+  };
   uint32_t* d_err;
   BBF_CUDA(dmalloc(&d_err, 4 * sizeof(uint32_t), st));
   BBF_CUDA(cudaMemsetAsync(d_err, 0, 4 * sizeof(uint32_t), st));
@@ -260,11 +296,6 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   uint32_t h_err = 0;
   BBF_CUDA(cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaStreamSynchronize(st));
-  auto cleanup_input = [&]() {
-    if (own_rp) dfree(own_rp, st);
-    if (own_col) dfree(own_col, st);
-    if (own_sg) dfree(own_sg, st);
-  };
   if (h_err) {
     dfree(d_err, st);
     cleanup_input();
@@ -274,35 +305,32 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     set_error("sign byte not in {0,1}");
     return BBF_EINVAL;
   }
+  dfree(d_err, st);
 
   // S2-S3: degrees and per-side priority ranks
-  uint64_t *key_u, *key_v, *skey_u, *skey_v;
-  uint32_t *dv, *lr_u, *lr_v;
+  uint64_t *key_u, *key_v;
+  uint32_t* dv;
   BBF_CUDA(dmalloc(&key_u, 8ull * (n_u + 1), st));
   BBF_CUDA(dmalloc(&key_v, 8ull * (n_v + 1), st));
-  BBF_CUDA(dmalloc(&skey_u, 8ull * (n_u + 1), st));
-  BBF_CUDA(dmalloc(&skey_v, 8ull * (n_v + 1), st));
+  BBF_CUDA(dmalloc(&g->skey, 8ull * (n + 1), st));
   BBF_CUDA(dmalloc(&dv, 4ull * (n_v + 1), st));
-  BBF_CUDA(dmalloc(&lr_u, 4ull * (n_u + 1), st));
-  BBF_CUDA(dmalloc(&lr_v, 4ull * (n_v + 1), st));
+  BBF_CUDA(dmalloc(&g->lr, 4ull * (n + 1), st));
   BBF_CUDA(cudaMemsetAsync(dv, 0, 4ull * (n_v + 1), st));
   if (n_u) k_keys_u<<<grid_for(n_u, 256, 1u << 30), 256, 0, st>>>(d_rp, n_u, key_u);
   if (nnz) k_hist_v<<<grid_for(nnz, 256), 256, 0, st>>>(d_col, nnz, dv);
   if (n_v) k_keys_v<<<grid_for(n_v, 256, 1u << 30), 256, 0, st>>>(dv, n_u, n_v, key_v);
   g->launches += 3;
+  uint64_t* skey_u = g->skey;
+  uint64_t* skey_v = g->skey + n_u;
+  uint32_t* lr_u = g->lr;
+  uint32_t* lr_v = g->lr + n_u;
 
-  size_t tmp_bytes = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+  size_t tmp_bytes = 0, t1 = 0, t2 = 0, t4 = 0;
   int kbits = std::min(64, 32 + bits_for(std::max<uint64_t>(nnz, 1)));  // deg < 2^31
   cub::DeviceRadixSort::SortKeysDescending(nullptr, t1, key_u, skey_u, (int)n_u, 0, kbits, st);
   cub::DeviceRadixSort::SortKeysDescending(nullptr, t2, key_v, skey_v, (int)n_v, 0, kbits, st);
-  int ebits = 32 + bits_for(std::max<uint32_t>(n, 1));
-  cub::DeviceRadixSort::SortKeys(nullptr, t3, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)m, 0,
-                                 ebits, st);
   cub::DeviceScan::ExclusiveSum(nullptr, t4, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)(n + 1), st);
-  tmp_bytes = std::max(std::max(t1, t2), std::max(t3, t4));
-  size_t t5 = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, t5, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n, st);
-  tmp_bytes = std::max(tmp_bytes, t5);
+  tmp_bytes = std::max(std::max(t1, t2), t4);
   void* tmp;
   BBF_CUDA(dmalloc(&tmp, tmp_bytes + 16, st));
   if (n_u) BBF_CUDA(cub::DeviceRadixSort::SortKeysDescending(tmp, t1, key_u, skey_u, (int)n_u, 0, kbits, st));
@@ -312,15 +340,133 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   BBF_CUDA(dmalloc(&g->inv, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&g->degs, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&g->off, 4ull * (n + 1), st));
+  if (n_u) k_rank_tables<<<grid_for(n_u, 256, 1u << 30), 256, 0, st>>>(skey_u, n_u, 0, 0, g->inv, g->degs, lr_u);
+  if (n_v) k_rank_tables<<<grid_for(n_v, 256, 1u << 30), 256, 0, st>>>(skey_v, n_v, n_u, n_u, g->inv, g->degs, lr_v);
+  g->launches += 2;
+  // row offsets: exclusive scan of degrees in row order (rows U by rank, then V by rank)
+  BBF_CUDA(cudaMemsetAsync(g->degs + n, 0, 4, st));
+  BBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t4, g->degs, g->off, (int)(n + 1), st));
+  g->launches += 1;
+  dfree(tmp, st);
+
+  // zone boundaries per side (rank counts of degree thresholds), overflow bound
+  unsigned long long* d_cnt;
+  BBF_CUDA(dmalloc(&d_cnt, 16 * sizeof(unsigned long long), st));
+  BBF_CUDA(cudaMemsetAsync(d_cnt, 0, 16 * sizeof(unsigned long long), st));
+  k_count_ge<<<1, 32, 0, st>>>(g->degs, 0, n_u, d_cnt);
+  k_count_ge<<<1, 32, 0, st>>>(g->degs, n_u, n_v, d_cnt + 6);
+  k_ws<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(g->degs, n_u, n, d_cnt + 12);
+  g->launches += 3;
+  unsigned long long h_cnt[16];
+  BBF_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
+  uint32_t h_maxdeg[2] = {0, 0};
+  if (n_u) BBF_CUDA(cudaMemcpyAsync(&h_maxdeg[0], g->degs, 4, cudaMemcpyDeviceToHost, st));
+  if (n_v) BBF_CUDA(cudaMemcpyAsync(&h_maxdeg[1], g->degs + n_u, 4, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaStreamSynchronize(st));
+  dfree(d_cnt, st);
+  g->maxdeg[0] = h_maxdeg[0];
+  g->maxdeg[1] = h_maxdeg[1];
+  for (int s2 = 0; s2 < 2; ++s2) {
+    Zones& z = g->zones[s2];
+    for (int i = 0; i < 5; ++i) z.L[i] = (uint32_t)h_cnt[6 * s2 + i];
+    g->Llong[s2] = (uint32_t)h_cnt[6 * s2 + 5];
+    z.WB[0] = 0;
+    z.WB[1] = 2u * z.L[0];
+    z.WB[2] = z.WB[1] + (z.L[1] - z.L[0]);
+    z.WB[3] = z.WB[2] + (z.L[2] - z.L[1] + 1) / 2;
+    z.WB[4] = z.WB[3] + (z.L[3] - z.L[2] + 3) / 4;
+    z.WB[5] = z.WB[4] + (z.L[4] - z.L[3] + 7) / 8;
+    g->L4[s2] = z.L[4];
+  }
+  // B + N = sum_{u<w} C(T_uw, 2) <= (maxT - 1)/2 * sum_{u<w} T_uw = (maxdeg_U - 1)/2 * W_S(U)
+  {
+    long double bu = (long double)(g->maxdeg[0] ? g->maxdeg[0] - 1 : 0) / 2.0L * (long double)h_cnt[13];
+    long double bv = (long double)(g->maxdeg[1] ? g->maxdeg[1] - 1 : 0) / 2.0L * (long double)h_cnt[12];
+    g->ws_bound = std::min(bu, bv);
+  }
+
+  // dense candidates: W_G without the adjacency, then the dispatch rule decides the load path
+  bool dense_load = false;
+  if (dense_supported(g) && !(g->load_flags & BBF_FORCE_SPARSE)) {
+    uint32_t* mcnt;
+    unsigned long long* d_wg;
+    BBF_CUDA(dmalloc(&mcnt, 4ull * (n + 1), st));
+    BBF_CUDA(dmalloc(&d_wg, 8, st));
+    BBF_CUDA(cudaMemsetAsync(mcnt, 0, 4ull * (n + 1), st));
+    BBF_CUDA(cudaMemsetAsync(d_wg, 0, 8, st));
+    if (nnz) k_wg_m<<<grid_for(nnz, 256), 256, 0, st>>>(d_rp, d_col, nnz, n_u, key_u, key_v, mcnt);
+    if (n) k_wg_sum<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(mcnt, key_u, key_v, n_u, n, d_wg);
+    g->launches += 2;
+    unsigned long long wg = 0;
+    BBF_CUDA(cudaMemcpyAsync(&wg, d_wg, 8, cudaMemcpyDeviceToHost, st));
+    BBF_CUDA(cudaStreamSynchronize(st));
+    dfree(mcnt, st);
+    dfree(d_wg, st);
+    g->W_G = wg;
+    g->wg_valid = true;
+    dense_load = (g->load_flags & BBF_FORCE_DENSE) || dense_preferred(g, true);
+  }
+  dfree(key_u, st);
+  dfree(key_v, st);
+  dfree(dv, st);
+
+  if (dense_load) {
+    bbf_status s = build_dense_operands(g, d_rp, d_col, d_sg);
+    if (s != BBF_OK) { cleanup_input(); cudaStreamSynchronize(st); return s; }
+    // keep the input CSR for a later sparse call (build_adj); device inputs are only borrowed
+    if (own_rp) {
+      g->in_rp = own_rp; g->in_col = own_col; g->in_sg = own_sg;
+      own_rp = nullptr; own_col = nullptr; own_sg = nullptr;
+    } else {
+      BBF_CUDA(dmalloc(&g->in_rp, sizeof(uint64_t) * (n_u + 1), st));
+      BBF_CUDA(dmalloc(&g->in_col, sizeof(uint32_t) * (nnz + 1), st));
+      BBF_CUDA(dmalloc(&g->in_sg, nnz + 1, st));
+      BBF_CUDA(cudaMemcpyAsync(g->in_rp, d_rp, sizeof(uint64_t) * (n_u + 1), cudaMemcpyDeviceToDevice, st));
+      if (nnz) {
+        BBF_CUDA(cudaMemcpyAsync(g->in_col, d_col, 4ull * nnz, cudaMemcpyDeviceToDevice, st));
+        BBF_CUDA(cudaMemcpyAsync(g->in_sg, d_sg, nnz, cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    BBF_CUDA(cudaGetLastError());
+    return BBF_OK;
+  }
+  bbf_status s = build_adj(g, d_rp, d_col, d_sg);
+  cleanup_input();
+  return s;
+}
+
+bbf_status ensure_adj(bbf_graph* g) {
+  if (g->adj_built) return BBF_OK;
+  if (!g->in_rp) { set_error("internal: adjacency requested without the input CSR"); return BBF_ECUDA; }
+  BBF_TRY(build_adj(g, g->in_rp, g->in_col, g->in_sg));
+  return BBF_OK;
+}
+
+// S4: rank-space adjacency of both directions (one radix sort of the 2*nnz directed entries),
+// duplicate check, mid_start / end1 cuts, degree prefix, hub-kernel counter addresses and runs
+bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, const uint8_t* d_sg) {
+  cudaStream_t st = g->stream;
+  const uint32_t n_u = g->n_u, n_v = g->n_v, n = g->n;
+  const uint64_t nnz = g->nnz;
+  const uint64_t m = 2 * nnz;
+  const uint64_t* skey_u = g->skey;
+  const uint64_t* skey_v = g->skey + n_u;
+  const uint32_t* lr_u = g->lr;
+  const uint32_t* lr_v = g->lr + n_u;
+  uint32_t* d_err;
+  BBF_CUDA(dmalloc(&d_err, 4 * sizeof(uint32_t), st));
+  BBF_CUDA(cudaMemsetAsync(d_err, 0, 4 * sizeof(uint32_t), st));
+  size_t t3 = 0, t5 = 0;
+  int ebits = 32 + bits_for(std::max<uint32_t>(n, 1));
+  cub::DeviceRadixSort::SortKeys(nullptr, t3, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)m, 0,
+                                 ebits, st);
+  cub::DeviceScan::InclusiveSum(nullptr, t5, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n, st);
+  void* tmp;
+  BBF_CUDA(dmalloc(&tmp, std::max(t3, t5) + 16, st));
   BBF_CUDA(dmalloc(&g->mid, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&g->end1, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&g->adj, 4ull * (m + 1), st));
   BBF_CUDA(dmalloc(&g->degpre, 8ull * (n + 1), st));
-  if (n_u) k_rank_tables<<<grid_for(n_u, 256, 1u << 30), 256, 0, st>>>(skey_u, n_u, 0, 0, g->inv, g->degs, lr_u);
-  if (n_v) k_rank_tables<<<grid_for(n_v, 256, 1u << 30), 256, 0, st>>>(skey_v, n_v, n_u, n_u, g->inv, g->degs, lr_v);
-  g->launches += 2;
-
-  // S4: rank-space adjacency, one radix sort of the 2*nnz directed entries
   if (m) {
     uint64_t *ek, *eks;
     BBF_CUDA(dmalloc(&ek, 8ull * m, st));
@@ -332,52 +478,12 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     dfree(ek, st);
     dfree(eks, st);
   }
-  // row offsets: exclusive scan of degrees in row order (rows U by rank, then V by rank)
-  BBF_CUDA(cudaMemsetAsync(g->degs + n, 0, 4, st));
-  BBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t4, g->degs, g->off, (int)(n + 1), st));
-  g->launches += 1;
-
-  // zone boundaries per side (rank counts of degree thresholds)
-  unsigned long long* d_cnt;
-  BBF_CUDA(dmalloc(&d_cnt, 16 * sizeof(unsigned long long), st));
-  BBF_CUDA(cudaMemsetAsync(d_cnt, 0, 16 * sizeof(unsigned long long), st));
-  k_count_ge<<<1, 32, 0, st>>>(g->degs, 0, n_u, d_cnt);
-  k_count_ge<<<1, 32, 0, st>>>(g->degs, n_u, n_v, d_cnt + 6);
-  k_ws<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(g->degs, n_u, n, d_cnt + 12);
-  g->launches += 3;
-  unsigned long long h_cnt[16];
-  BBF_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
+  uint32_t h_err = 0;
   BBF_CUDA(cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, st));
-  uint32_t h_maxdeg[2] = {0, 0};
-  if (n_u) BBF_CUDA(cudaMemcpyAsync(&h_maxdeg[0], g->degs, 4, cudaMemcpyDeviceToHost, st));
-  if (n_v) BBF_CUDA(cudaMemcpyAsync(&h_maxdeg[1], g->degs + n_u, 4, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaStreamSynchronize(st));
-  g->maxdeg[0] = h_maxdeg[0];
-  g->maxdeg[1] = h_maxdeg[1];
-  for (int s = 0; s < 2; ++s) {
-    Zones& z = g->zones[s];
-    for (int i = 0; i < 5; ++i) z.L[i] = (uint32_t)h_cnt[6 * s + i];
-    g->Llong[s] = (uint32_t)h_cnt[6 * s + 5];
-    z.WB[0] = 0;
-    z.WB[1] = 2u * z.L[0];
-    z.WB[2] = z.WB[1] + (z.L[1] - z.L[0]);
-    z.WB[3] = z.WB[2] + (z.L[2] - z.L[1] + 1) / 2;
-    z.WB[4] = z.WB[3] + (z.L[3] - z.L[2] + 3) / 4;
-    z.WB[5] = z.WB[4] + (z.L[4] - z.L[3] + 7) / 8;
-    g->L4[s] = z.L[4];
-  }
-  // B + N = sum_{u<w} C(T_uw, 2) <= (maxT - 1)/2 * sum_{u<w} T_uw = (maxdeg_U - 1)/2 * W_S(U)
-  {
-    long double bu = (long double)(g->maxdeg[0] ? g->maxdeg[0] - 1 : 0) / 2.0L * (long double)h_cnt[13];
-    long double bv = (long double)(g->maxdeg[1] ? g->maxdeg[1] - 1 : 0) / 2.0L * (long double)h_cnt[12];
-    g->ws_bound = std::min(bu, bv);
-  }
+  dfree(d_err, st);
   if (h_err & kErrDup) {
     dfree(tmp, st);
-    cleanup_input();
-    dfree(key_u, st); dfree(key_v, st); dfree(skey_u, st);
-    dfree(skey_v, st); dfree(dv, st); dfree(lr_u, st); dfree(lr_v, st);
-    dfree(d_cnt, st); dfree(d_err, st);
     cudaStreamSynchronize(st);
     set_error("duplicate (u,v) edge");
     return BBF_EDUP;
@@ -393,6 +499,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     g->launches += 3;
     dfree(d64, st);
   }
+  dfree(tmp, st);
   // hub-kernel counter addresses and window runs (DESIGN.md §"Counter windows")
   for (int s2 = 0; s2 < 2; ++s2)
     if (g->zones[s2].WB[5] > kCWordMask) {
@@ -402,7 +509,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   g->compact = g->zones[0].L[0] == 0 && g->zones[1].L[0] == 0 && g->zones[0].WB[5] <= kCpWordMask &&
                g->zones[1].WB[5] <= kCpWordMask && !getenv("BBF_NO_COMPACT");  // env: test hook
   const uint32_t wmask = g->compact ? kCpWordMask : kCWordMask;
-  BBF_CUDA(dmalloc(&g->adjc, 4ull * (m + 32), st));  // padded: 16-B chunk loads
+  BBF_CUDA(dmalloc(&g->adjc, 4ull * (m + 32), st));  // padded: 32-B chunk loads
   BBF_CUDA(dmalloc(&g->runid, 4ull * (m + 1), st));
   g->nruns = 0;
   if (m) {
@@ -428,12 +535,8 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   } else {
     BBF_CUDA(dmalloc(&g->runs, sizeof(uint2), st));
   }
-  dfree(tmp, st);
-  cleanup_input();
-  dfree(key_u, st); dfree(key_v, st); dfree(skey_u, st);
-  dfree(skey_v, st); dfree(dv, st); dfree(lr_u, st); dfree(lr_v, st);
-  dfree(d_cnt, st); dfree(d_err, st);
   BBF_CUDA(cudaGetLastError());
+  g->adj_built = true;
   return BBF_OK;
 }
 
