@@ -130,6 +130,23 @@ bbf_status bbf_count_per_vertex(bbf_graph *g, uint64_t *bal_u, uint64_t *unb_u, 
 bbf_status bbf_count_pairs_topk(bbf_graph *g, int side, uint32_t k, bbf_pair *out,
                                 uint32_t *n_out, uint32_t flags);
 
+/* SBESPAR one-shot sparsification estimate of the global balanced count (PAPER.md:1402-1438,
+ * §Approximation by Sparsification): for trial t = 0..trials-1, keep each edge of the input CSR
+ * independently with probability rho, count the sampled graph exactly (the same path as
+ * bbf_count_global) and scale its balanced count by rho^-4 (reading R18: a butterfly survives iff
+ * its 4 edges do).  Edge e of the U-side CSR is kept iff rho >= 1 or
+ * sm64(sm64(seed + t) ^ e) < floor(rho * 2^64), sm64 = SplitMix64, so the draws are reproducible.
+ *   n_u, n_v, row_ptr, col, sign, flags (BBF_PTR_DEVICE, BBF_FORCE_*), device, cuda_stream, comm:
+ *     as bbf_graph_load_csr; rho in (0, 1]; trials >= 1.
+ *   sampled_balanced / sampled_unbalanced: host u64[trials] (nullable) — exact counts of each
+ *     sampled graph; estimates: host double[trials] — sampled balanced count * rho^-4.
+ * Errors: BBF_EINVAL (rho, trials, null estimates), those of bbf_graph_load_csr. */
+bbf_status bbf_estimate_global(uint32_t n_u, uint32_t n_v, const uint64_t *row_ptr, const uint32_t *col,
+                               const uint8_t *sign, uint32_t flags, double rho, uint32_t trials,
+                               uint64_t seed, int device, void *cuda_stream, bbf_comm *comm,
+                               uint64_t *sampled_balanced, uint64_t *sampled_unbalanced,
+                               double *estimates);
+
 /* Introspection for tests and the bench (no effect on results).  kernel_launches: GPU kernels the
  * library launched on this handle since load.  For the last count call's main kernel (the hub
  * wedge-aggregation kernel k_t3 on the sparse path, k_dense_tiles on the dense path):

@@ -428,3 +428,42 @@ int oracle_priority_order(uint32_t n_u, uint32_t n_v, const uint64_t *row_ptr,
   graph_free(&g);
   return 0;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * SBESPAR sparsification (§Approximation by Sparsification): "samples each
+ * edge in the network independently with a fixed probability rho and constructs a network with
+ * the sampled edges E' only".  The independent draws come from the counter-based generator the
+ * library documents (include/bbf.h, bbf_estimate_global), written out here on its own:
+ * SplitMix64 sm64(x) = mix(x + 0x9E3779B97F4A7C15); trial t uses key = sm64(seed + t); edge e of
+ * the U-side CSR is kept iff rho >= 1 or sm64(key ^ e) < floor(rho * 2^64).
+ * out_rp: n_u+1; out_col / out_sign: capacity nnz; *out_nnz receives the kept count.
+ * ---------------------------------------------------------------------------------------- */
+uint64_t oracle_sm64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+int oracle_sparsify(uint32_t n_u, const uint64_t *row_ptr, const uint32_t *col, const uint8_t *sign,
+                    double rho, uint64_t seed, uint32_t trial, uint64_t *out_rp, uint32_t *out_col,
+                    uint8_t *out_sign, uint64_t *out_nnz) {
+  if (!(rho > 0.0 && rho <= 1.0)) return 1;
+  const uint64_t key = oracle_sm64(seed + trial);
+  const int keep_all = rho >= 1.0;
+  const uint64_t thr = keep_all ? ~0ull : (uint64_t)(rho * 18446744073709551616.0);
+  uint64_t k = 0;
+  out_rp[0] = 0;
+  for (uint32_t u = 0; u < n_u; ++u) {
+    for (uint64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) {
+      if (keep_all || oracle_sm64(key ^ e) < thr) {
+        out_col[k] = col[e];
+        out_sign[k] = sign[e];
+        ++k;
+      }
+    }
+    out_rp[u + 1] = k;
+  }
+  *out_nnz = k;
+  return 0;
+}

@@ -47,6 +47,10 @@ def _load():
         lib.oracle_route_s.argtypes = [u32, u32, P, P, P, P, u64, i32, P, P]
         lib.oracle_pairs.argtypes = [u32, u32, P, P, P, i32, i32, P, P, P, P, u64, P]
         lib.oracle_priority_order.argtypes = [u32, u32, P, P, P, P]
+        lib.oracle_sm64.argtypes = [u64]
+        lib.oracle_sm64.restype = u64
+        lib.oracle_sparsify.argtypes = [u32, P, P, P, C.c_double, u64, u32, P, P, P, P]
+        lib.oracle_sparsify.restype = i32
         for f in (lib.oracle_brute, lib.oracle_route_g, lib.oracle_route_s, lib.oracle_pairs,
                   lib.oracle_priority_order):
             f.restype = i32
@@ -158,3 +162,38 @@ def priority_order(g):
     if rc:
         raise OracleError(rc)
     return pos
+
+
+def sm64(x: int) -> int:
+    """The generator of the sparsification draws (SplitMix64 output for state x)."""
+    return int(_load().oracle_sm64(C.c_uint64(x & (2**64 - 1))))
+
+
+def sparsify(g, rho: float, seed: int, trial: int = 0):
+    """SBESPAR sample: each edge kept independently w.p. rho (documented
+    counter-based draws, see bbf_oracle.c).  Returns a synth.graphs.SignedBipartite."""
+    from synth.graphs import SignedBipartite
+    lib = _load()
+    keep, a = _graph_args(g)
+    rp = np.zeros(g.n_u + 1, np.uint64)
+    col = np.zeros(max(g.nnz, 1), np.uint32)
+    sg = np.zeros(max(g.nnz, 1), np.uint8)
+    k = np.zeros(1, np.uint64)
+    rc = lib.oracle_sparsify(a[0], a[2], a[3], a[4], C.c_double(rho), C.c_uint64(seed),
+                             C.c_uint32(trial), _ptr(rp), _ptr(col), _ptr(sg), _ptr(k))
+    if rc:
+        raise OracleError(rc)
+    m = int(k[0])
+    return SignedBipartite(g.n_u, g.n_v, rp, col[:m].copy(), sg[:m].copy())
+
+
+def estimate(g, rho: float, trials: int, seed: int = 0, threads=None):
+    """SBESPAR estimate of the global balanced count: per trial, the exact Alg.-2 count of the
+    sample scaled by rho^-4 (reading R18).  Returns dict(sampled_B, sampled_N, estimates)."""
+    sb, sn, est = [], [], []
+    for t in range(trials):
+        r = route_g(sparsify(g, rho, seed, t), threads=threads)
+        sb.append(r["B"])
+        sn.append(r["N"])
+        est.append(r["B"] / rho ** 4)
+    return dict(sampled_B=sb, sampled_N=sn, estimates=est)

@@ -62,9 +62,11 @@ def lib():
         L.bbf_count_per_vertex.argtypes = [P, P, P, P, P, u32, P]
         L.bbf_count_pairs_topk.argtypes = [P, i32, u32, P, P, u32]
         L.bbf_graph_stats.argtypes = [P, P, P, P, P]
+        L.bbf_estimate_global.argtypes = [u32, u32, P, P, P, u32, C.c_double, u32, u64, i32, P, P,
+                                          P, P, P]
         for f in ("bbf_nccl_unique_id", "bbf_comm_init", "bbf_comm_free", "bbf_graph_load_csr",
                   "bbf_graph_free", "bbf_count_global", "bbf_count_per_vertex",
-                  "bbf_count_pairs_topk", "bbf_graph_stats"):
+                  "bbf_count_pairs_topk", "bbf_graph_stats", "bbf_estimate_global"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -202,6 +204,30 @@ class Graph:
                     ms_main_kernel=ms.value)
 
 
+def estimate_global(n_u, n_v, row_ptr, col, sign, rho: float, trials: int, seed: int = 0,
+                    device: int = 0, stream=None, comm: Comm | None = None, flags: int = 0) -> dict:
+    """SBESPAR sparsification estimate (bbf_estimate_global).  Returns dict(sampled_B, sampled_N
+    (uint64 arrays), estimates (float64 array), mean, stddev)."""
+    dev = _is_torch(row_ptr) and row_ptr.is_cuda
+    if dev:
+        flags |= BBF_PTR_DEVICE
+        keep = (row_ptr, col, sign)
+    elif _is_torch(row_ptr):
+        keep = (row_ptr, col, sign)
+    else:
+        keep = (np.ascontiguousarray(row_ptr, dtype=np.uint64),
+                np.ascontiguousarray(col, dtype=np.uint32),
+                np.ascontiguousarray(sign, dtype=np.uint8))
+    sb, sn = np.zeros(trials, np.uint64), np.zeros(trials, np.uint64)
+    est = np.zeros(trials, np.float64)
+    st = C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else (stream or 0))
+    _check(lib().bbf_estimate_global(int(n_u), int(n_v), _ptr(keep[0]), _ptr(keep[1]), _ptr(keep[2]),
+                                     flags, float(rho), int(trials), int(seed) & (2**64 - 1), device,
+                                     st, comm.h if comm else None, _ptr(sb), _ptr(sn), _ptr(est)))
+    return dict(sampled_B=sb, sampled_N=sn, estimates=est, mean=float(est.mean()),
+                stddev=float(est.std(ddof=1)) if trials > 1 else 0.0)
+
+
 # ABI-named aliases (same names as include/bbf.h)
 bbf_abi_version = abi_version
 bbf_last_error = last_error
@@ -232,3 +258,6 @@ def bbf_count_pairs_topk(g: Graph, side: int, k: int, flags: int = 0):
 
 def bbf_graph_stats(g: Graph):
     return g.stats()
+
+
+bbf_estimate_global = estimate_global

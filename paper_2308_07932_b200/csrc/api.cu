@@ -239,7 +239,15 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_pt
   const bool dptr = flags & BBF_PTR_DEVICE;
   uint64_t nnz = 0;
   if (dptr) {
-    BBF_CUDA(cudaMemcpy(&nnz, row_ptr + n_u, 8, cudaMemcpyDeviceToHost));
+    // ordered after the caller's work on its stream (a plain cudaMemcpy would run on the legacy
+    // default stream, which does not wait for non-blocking streams)
+    if (cuda_stream) {
+      BBF_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n_u, 8, cudaMemcpyDeviceToHost, (cudaStream_t)cuda_stream));
+      BBF_CUDA(cudaStreamSynchronize((cudaStream_t)cuda_stream));
+    } else {
+      BBF_CUDA(cudaDeviceSynchronize());
+      BBF_CUDA(cudaMemcpy(&nnz, row_ptr + n_u, 8, cudaMemcpyDeviceToHost));
+    }
   } else {
     nnz = row_ptr[n_u];
   }

@@ -306,3 +306,20 @@ def test_fake_world_shards_sum_to_full_count(bbf, monkeypatch, path, world):
     assert acc[0] == full[0]["balanced"] and acc[1] == full[0]["unbalanced"]
     for a, b in zip(acc[2:], full[1:]):
         assert np.array_equal(a.astype(np.uint64), b)
+
+
+# ----------------------------------------------------------------------------- NEXT-1 SBESPAR
+@pytest.mark.parametrize("name,rho,trials", [("config1", 0.5, 6), ("config2", 0.7, 3), ("config3", 0.6, 2),
+                                             ("corpus", 1.0, 2)])
+def test_estimator_samples_match_oracle(bbf, name, rho, trials):
+    """bbf_estimate_global draws the same edge samples as the oracle (same documented
+    counter-based generator) and counts each sample exactly: per-trial sampled B and N are
+    bit-exact and the estimates equal B * rho^-4."""
+    g = {"config1": G.config1, "config2": G.config2, "config3": G.config3,
+         "corpus": lambda: G.random_bipartite(12, 11, 0.5, 0.5, seed=4)}[name]()
+    got = bbf.estimate_global(g.n_u, g.n_v, g.row_ptr, g.col, g.sign, rho, trials, seed=123)
+    for t in range(trials):
+        r = O.route_g(O.sparsify(g, rho, 123, t), threads=THREADS)
+        assert (int(got["sampled_B"][t]), int(got["sampled_N"][t])) == (r["B"], r["N"]), (name, t)
+        # the estimate is the one floating-point step: equal up to rounding (a few ulps)
+        assert abs(got["estimates"][t] - r["B"] / rho ** 4) <= 1e-12 * max(1.0, r["B"] / rho ** 4)
