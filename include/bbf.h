@@ -62,9 +62,12 @@ typedef enum {
 } bbf_status;
 
 enum { BBF_SIDE_U = 0, BBF_SIDE_V = 1 };
+enum { BBF_METRIC_BALANCED = 0, BBF_METRIC_DEGREE = 1 };
 
 enum {
   BBF_PTR_DEVICE = 1u << 0,   /* input (load) / output (count) pointers are device pointers */
+  BBF_POSITIVE_ONLY = 1u << 1, /* load: keep only the positive edges (case-study analytics,   */
+                               /* PAPER.md:15-27 "only formed by the edges with sign 1")       */
   BBF_FORCE_SPARSE = 1u << 2, /* count: use the sparse wedge-aggregation kernels            */
   BBF_FORCE_DENSE = 1u << 3   /* count: use the dense int8 tensor-core path (tcgen05)       */
 };
@@ -103,6 +106,9 @@ bbf_status bbf_comm_free(bbf_comm *comm);
  *   col       : nnz V-side indices (< n_v), any order within a row, no duplicate (u,v).
  *   sign      : nnz bytes, 1 = positive, 0 = negative.
  *   flags     : BBF_PTR_DEVICE if the three arrays are device pointers on `device`;
+ *               BBF_POSITIVE_ONLY: the graph is restricted to its positive edges after
+ *               validation (every count then describes the positive subgraph, where every
+ *               butterfly is balanced; a duplicate pair with a negative copy is not detected);
  *               BBF_FORCE_SPARSE or BBF_FORCE_DENSE (exclusive) fix the path every count on this
  *               handle uses unless the count call passes its own (default: the dispatch rule
  *               of DESIGN.md §6 picks the faster path; both give bit-identical results).
@@ -129,6 +135,15 @@ bbf_status bbf_count_per_vertex(bbf_graph *g, uint64_t *bal_u, uint64_t *unb_u, 
  * array of k slots; *n_out receives min(k, #pairs with balanced > 0).  k >= 1. */
 bbf_status bbf_count_pairs_topk(bbf_graph *g, int side, uint32_t k, bbf_pair *out,
                                 uint32_t *n_out, uint32_t flags);
+
+/* Top-k vertices of one side (case study, "top-10 actors with most number of
+ * positive butterflies / positive edges"): metric BBF_METRIC_BALANCED ranks by
+ * the per-vertex balanced count (bbf_count_per_vertex), BBF_METRIC_DEGREE by degree in the loaded
+ * graph (with BBF_POSITIVE_ONLY at load: positive degree).  Order: score desc, then input id asc;
+ * every vertex of the side is ranked (zero scores included).  ids, scores: host arrays of k
+ * slots; *n_out = min(k, |side|).  Errors: BBF_EINVAL (side, metric, k == 0, null pointers). */
+bbf_status bbf_topk_vertices(bbf_graph *g, int side, int metric, uint32_t k, uint32_t *ids,
+                             uint64_t *scores, uint32_t *n_out);
 
 /* SBESPAR one-shot sparsification estimate of the global balanced count (PAPER.md:1402-1438,
  * §Approximation by Sparsification): for trial t = 0..trials-1, keep each edge of the input CSR

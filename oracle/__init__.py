@@ -6,5 +6,5 @@ never imports this package, and this package never imports the product path.
 """
 from .oracle import (  # noqa: F401
     OracleError, build, brute, route_g, route_s, pairs, topk_pairs, priority_order, sm64,
-    sparsify, estimate,
+    sparsify, estimate, positive_subgraph, topk_vertices,
 )

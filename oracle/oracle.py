@@ -197,3 +197,31 @@ def estimate(g, rho: float, trials: int, seed: int = 0, threads=None):
         sn.append(r["N"])
         est.append(r["B"] / rho ** 4)
     return dict(sampled_B=sb, sampled_N=sn, estimates=est)
+
+
+def positive_subgraph(g):
+    """Case-study restriction (PAPER.md:15-27, "only formed by the edges with sign/weight as 1";
+    SPEC.md:449): the graph with its positive edges only, vertex sets unchanged."""
+    from synth.graphs import SignedBipartite
+    keep = g.sign == 1
+    u = np.repeat(np.arange(g.n_u), np.diff(g.row_ptr.astype(np.int64)))[keep]
+    rp = np.zeros(g.n_u + 1, np.uint64)
+    np.add.at(rp, u + 1, 1)
+    return SignedBipartite(g.n_u, g.n_v, np.cumsum(rp).astype(np.uint64), g.col[keep].copy(),
+                           g.sign[keep].copy())
+
+
+def topk_vertices(g, k: int, side: int = 0, metric: str = "balanced", threads=None):
+    """Top-k vertices of a side: by per-vertex balanced count (vBBFC) or by
+    degree, score desc then id asc, all vertices ranked.  Returns [(id, score)]."""
+    cnt = g.n_u if side == 0 else g.n_v
+    if metric == "degree":
+        if side == 0:
+            score = np.diff(g.row_ptr.astype(np.int64))
+        else:
+            score = np.bincount(g.col.astype(np.int64), minlength=g.n_v)
+    else:
+        verts = np.arange(cnt, dtype=np.uint32) + (0 if side == 0 else g.n_u)
+        score = route_s(g, verts=verts, threads=threads)[0].astype(np.int64)
+    order = sorted(range(cnt), key=lambda i: (-int(score[i]), i))
+    return [(i, int(score[i])) for i in order[:k]]

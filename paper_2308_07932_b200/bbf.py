@@ -19,6 +19,8 @@ STATUS_NAMES = {0: "BBF_OK", 1: "BBF_EINVAL", 2: "BBF_ERANGE", 3: "BBF_EDUP", 4:
                 5: "BBF_ECUDA", 6: "BBF_ENCCL", 7: "BBF_EOVERFLOW"}
 BBF_SIDE_U, BBF_SIDE_V = 0, 1
 BBF_PTR_DEVICE = 1 << 0
+BBF_POSITIVE_ONLY = 1 << 1
+BBF_METRIC_BALANCED, BBF_METRIC_DEGREE = 0, 1
 BBF_FORCE_SPARSE = 1 << 2
 BBF_FORCE_DENSE = 1 << 3
 
@@ -62,11 +64,12 @@ def lib():
         L.bbf_count_per_vertex.argtypes = [P, P, P, P, P, u32, P]
         L.bbf_count_pairs_topk.argtypes = [P, i32, u32, P, P, u32]
         L.bbf_graph_stats.argtypes = [P, P, P, P, P]
+        L.bbf_topk_vertices.argtypes = [P, i32, i32, u32, P, P, P]
         L.bbf_estimate_global.argtypes = [u32, u32, P, P, P, u32, C.c_double, u32, u64, i32, P, P,
                                           P, P, P]
         for f in ("bbf_nccl_unique_id", "bbf_comm_init", "bbf_comm_free", "bbf_graph_load_csr",
                   "bbf_graph_free", "bbf_count_global", "bbf_count_per_vertex",
-                  "bbf_count_pairs_topk", "bbf_graph_stats", "bbf_estimate_global"):
+                  "bbf_count_pairs_topk", "bbf_graph_stats", "bbf_estimate_global", "bbf_topk_vertices"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -195,6 +198,14 @@ class Graph:
         _check(lib().bbf_count_pairs_topk(self.h, side, int(k), buf, C.byref(n), flags))
         return [(buf[i].a, buf[i].b, buf[i].balanced, buf[i].unbalanced) for i in range(n.value)]
 
+    def topk_vertices(self, k: int, side: int = BBF_SIDE_U, metric: int = BBF_METRIC_BALANCED):
+        """[(input id, score)] of the top-k vertices of `side` (bbf_topk_vertices)."""
+        ids = np.zeros(max(int(k), 1), np.uint32)
+        sc = np.zeros(max(int(k), 1), np.uint64)
+        n = C.c_uint32()
+        _check(lib().bbf_topk_vertices(self.h, side, metric, int(k), _ptr(ids), _ptr(sc), C.byref(n)))
+        return [(int(ids[i]), int(sc[i])) for i in range(n.value)]
+
     def stats(self) -> dict:
         L, B = C.c_uint64(), C.c_uint64()
         ops = C.c_double()
@@ -261,3 +272,7 @@ def bbf_graph_stats(g: Graph):
 
 
 bbf_estimate_global = estimate_global
+
+
+def bbf_topk_vertices(g: Graph, side: int, metric: int, k: int):
+    return g.topk_vertices(k, side, metric)

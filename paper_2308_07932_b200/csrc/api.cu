@@ -1,8 +1,10 @@
 // api.cu — the C ABI of libbbf.so (include/bbf.h): handle lifetime, status codes, the count
 // entry points, per-vertex output mapping (S9) and the multi-GPU reduction (S12, NCCL u64 sum).
+#include <cub/cub.cuh>
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -93,6 +95,17 @@ __global__ void k_scatter_pv(const unsigned long long* __restrict__ pv, const ui
   uint32_t id = inv[row0 + r];
   if (ob) ob[id] = pv[2ull * (row0 + r)];       // (B, N) interleaved per row
   if (on) on[id] = pv[2ull * (row0 + r) + 1];
+}
+
+// per-vertex score (balanced count or degree) of one side in input-id order, ids ascending
+__global__ void k_rank_scores(const unsigned long long* __restrict__ pv, const uint32_t* __restrict__ degs,
+                              const uint32_t* __restrict__ inv, uint32_t row0, uint32_t cnt, bool degree,
+                              unsigned long long* __restrict__ score, uint32_t* __restrict__ id) {
+  uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= cnt) return;
+  const uint32_t i = inv[row0 + r];
+  score[i] = degree ? (unsigned long long)degs[row0 + r] : pv[2ull * (row0 + r)];
+  id[i] = i;
 }
 
 bbf_status allreduce_u64(bbf_graph* g, unsigned long long* dbuf, size_t count) {
@@ -224,7 +237,7 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_pt
                               bbf_comm* comm, bbf_graph** out) {
   if (!out || !row_ptr) { set_error("null pointer"); return BBF_EINVAL; }
   *out = nullptr;
-  if (flags & ~(uint32_t)(BBF_PTR_DEVICE | BBF_FORCE_SPARSE | BBF_FORCE_DENSE)) {
+  if (flags & ~(uint32_t)(BBF_PTR_DEVICE | BBF_POSITIVE_ONLY | BBF_FORCE_SPARSE | BBF_FORCE_DENSE)) {
     set_error("unknown flags");
     return BBF_EINVAL;
   }
@@ -258,6 +271,7 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_pt
   g->device = device;
   g->num_sms = num_sms;
   g->load_flags = flags & (uint32_t)(BBF_FORCE_SPARSE | BBF_FORCE_DENSE);
+  g->positive_only = flags & BBF_POSITIVE_ONLY;
   g->comm = comm;
   g->n_u = n_u; g->n_v = n_v; g->n = n_u + n_v; g->nnz = nnz;
   if (cuda_stream) {
@@ -377,6 +391,47 @@ bbf_status bbf_count_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* ou
   BBF_TRY(check_overflow(g));
   BBF_TRY(ensure_adj(g));
   return run_pairs_topk(g, side, k, out, n_out);
+}
+
+bbf_status bbf_topk_vertices(bbf_graph* g, int side, int metric, uint32_t k, uint32_t* ids,
+                             uint64_t* scores, uint32_t* n_out) {
+  if (!g || !ids || !scores || !n_out) { set_error("null pointer"); return BBF_EINVAL; }
+  if (k == 0) { set_error("k == 0"); return BBF_EINVAL; }
+  if (side != BBF_SIDE_U && side != BBF_SIDE_V) { set_error("bad side"); return BBF_EINVAL; }
+  if (metric != BBF_METRIC_BALANCED && metric != BBF_METRIC_DEGREE) { set_error("bad metric"); return BBF_EINVAL; }
+  BBF_CUDA(cudaSetDevice(g->device));
+  cudaStream_t st = g->stream;
+  const uint32_t cnt = side ? g->n_v : g->n_u, row0 = side ? g->n_u : 0;
+  *n_out = 0;
+  if (cnt == 0) return BBF_OK;
+  if (metric == BBF_METRIC_BALANCED) {
+    unsigned long long BN[2];
+    float ms;
+    BBF_TRY(do_count(g, true, g->load_flags, BN, &ms));
+  }
+  unsigned long long *sc, *sc2;
+  uint32_t *id, *id2;
+  BBF_CUDA(dmalloc(&sc, 8ull * cnt, st));
+  BBF_CUDA(dmalloc(&sc2, 8ull * cnt, st));
+  BBF_CUDA(dmalloc(&id, 4ull * cnt, st));
+  BBF_CUDA(dmalloc(&id2, 4ull * cnt, st));
+  k_rank_scores<<<(cnt + 255) / 256, 256, 0, st>>>((const unsigned long long*)g->pv, g->degs, g->inv, row0, cnt,
+                                                   metric == BBF_METRIC_DEGREE, sc, id);
+  g->launches++;
+  // one stable radix sort by score descending over ids generated in ascending order
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, sc, sc2, id, id2, (int)cnt, 0, 64, st);
+  void* tmp;
+  BBF_CUDA(dmalloc(&tmp, tb + 16, st));
+  BBF_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, sc, sc2, id, id2, (int)cnt, 0, 64, st));
+  g->launches += 4;
+  const uint32_t take = std::min(k, cnt);
+  BBF_CUDA(cudaMemcpyAsync(ids, id2, 4ull * take, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaMemcpyAsync(scores, sc2, 8ull * take, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaStreamSynchronize(st));
+  for (void* p : {(void*)sc, (void*)sc2, (void*)id, (void*)id2, tmp}) dfree(p, st);
+  *n_out = take;
+  return BBF_OK;
 }
 
 bbf_status bbf_graph_stats(bbf_graph* g, uint64_t* kernel_launches, uint64_t* algo_bytes,

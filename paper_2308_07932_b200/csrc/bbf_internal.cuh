@@ -208,6 +208,7 @@ struct bbf_graph {
   bool own_stream;
   bbf_comm* comm;
   uint32_t load_flags;  // BBF_FORCE_SPARSE / BBF_FORCE_DENSE given at load: default dispatch
+  bool positive_only;   // BBF_POSITIVE_ONLY: negative edges dropped after validation
   uint32_t n_u, n_v, n;
   uint64_t nnz;
   // rank-space CSR

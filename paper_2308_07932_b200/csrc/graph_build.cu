@@ -225,6 +225,29 @@ inline int bits_for(uint64_t x) {
   return b;
 }
 
+// BBF_POSITIVE_ONLY compaction: keep[e] = edge e is positive; pos = exclusive prefix
+__global__ void k_keep_pos(const uint8_t* __restrict__ sg, uint64_t nnz, uint32_t* __restrict__ keep) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    keep[e] = sg[e] == 1 ? 1u : 0u;
+}
+__global__ void k_pos_rows(const uint64_t* __restrict__ rp, uint32_t n_u, const uint32_t* __restrict__ pos,
+                           uint64_t* __restrict__ nrp) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u <= n_u;
+       u += (uint64_t)gridDim.x * blockDim.x)
+    nrp[u] = pos[rp[u]];
+}
+__global__ void k_pos_compact(uint64_t nnz, const uint32_t* __restrict__ keep, const uint32_t* __restrict__ pos,
+                              const uint32_t* __restrict__ col, const uint8_t* __restrict__ sg,
+                              uint32_t* __restrict__ ncol, uint8_t* __restrict__ nsg) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    if (keep[e]) {
+      ncol[pos[e]] = col[e];
+      nsg[pos[e]] = sg[e];
+    }
+}
+
 // Paper wedge count W_G of Alg. 2 in O(nnz), without the sorted adjacency: for a
 // middle v, the eligible starts are its m_v neighbours of higher priority, and the k-th of them
 // (k = 0.. in priority order) sees deg(v) - 1 - k eligible ends, so v contributes
@@ -262,7 +285,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
                        const uint8_t* sign, bool device_ptrs) {
   cudaStream_t st = g->stream;
   const uint32_t n_u = g->n_u, n_v = g->n_v, n = g->n;
-  const uint64_t nnz = g->nnz;
+  uint64_t nnz = g->nnz;  // the positive-only filter may reduce it
   // device copies of the input (S1)
   const uint64_t* d_rp = row_ptr;
   const uint32_t* d_col = col;
@@ -306,6 +329,39 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     return BBF_EINVAL;
   }
   dfree(d_err, st);
+
+  // BBF_POSITIVE_ONLY: restrict to the positive edges (case-study analytics) before anything else
+  if (g->positive_only && nnz) {
+    uint32_t *keep, *pos, *pcol;
+    uint64_t* prp;
+    uint8_t* psg;
+    BBF_CUDA(dmalloc(&keep, 4ull * (nnz + 1), st));
+    BBF_CUDA(dmalloc(&pos, 4ull * (nnz + 1), st));
+    BBF_CUDA(dmalloc(&prp, 8ull * (n_u + 1), st));
+    BBF_CUDA(dmalloc(&pcol, 4ull * (nnz + 1), st));
+    BBF_CUDA(dmalloc(&psg, nnz + 1, st));
+    k_keep_pos<<<grid_for(nnz, 256), 256, 0, st>>>(d_sg, nnz, keep);
+    BBF_CUDA(cudaMemsetAsync(keep + nnz, 0, 4, st));
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, keep, pos, (int64_t)(nnz + 1), st);
+    void* tmp0;
+    BBF_CUDA(dmalloc(&tmp0, tb + 16, st));
+    BBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp0, tb, keep, pos, (int64_t)(nnz + 1), st));
+    k_pos_rows<<<grid_for(n_u + 1, 256, 1u << 30), 256, 0, st>>>(d_rp, n_u, pos, prp);
+    k_pos_compact<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, keep, pos, d_col, d_sg, pcol, psg);
+    g->launches += 5;
+    uint32_t kept = 0;
+    BBF_CUDA(cudaMemcpyAsync(&kept, pos + nnz, 4, cudaMemcpyDeviceToHost, st));
+    BBF_CUDA(cudaStreamSynchronize(st));
+    dfree(tmp0, st);
+    dfree(keep, st);
+    dfree(pos, st);
+    cleanup_input();
+    own_rp = prp; own_col = pcol; own_sg = psg;
+    d_rp = prp; d_col = pcol; d_sg = psg;
+    g->nnz = kept;
+    nnz = kept;
+  }
 
   // S2-S3: degrees and per-side priority ranks
   uint64_t *key_u, *key_v;

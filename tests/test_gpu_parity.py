@@ -323,3 +323,37 @@ def test_estimator_samples_match_oracle(bbf, name, rho, trials):
         assert (int(got["sampled_B"][t]), int(got["sampled_N"][t])) == (r["B"], r["N"]), (name, t)
         # the estimate is the one floating-point step: equal up to rounding (a few ulps)
         assert abs(got["estimates"][t] - r["B"] / rho ** 4) <= 1e-12 * max(1.0, r["B"] / rho ** 4)
+
+
+# ----------------------------------------------------------------------------- NEXT-2 analytics
+@pytest.mark.parametrize("name", ["config2", "random", "config1"])
+def test_positive_only_analytics(bbf, name):
+    """BBF_POSITIVE_ONLY at load: every count describes the positive subgraph (case study,
+    PAPER.md:15-27): per-vertex arrays = vBBFC on the oracle's positive subgraph, N = 0, top-k
+    pairs and top-k vertices (by balanced count and by positive degree) = the oracle rankings."""
+    g = {"config2": G.config2, "config1": G.config1,
+         "random": lambda: G.random_bipartite(300, 200, 0.1, 0.5, seed=8)}[name]()
+    p = O.positive_subgraph(g)
+    with bbf.Graph.from_synth(g, flags=bbf.BBF_POSITIVE_ONLY) as h:
+        c = h.count_global()
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+        pairs = h.count_pairs_topk(50, side=0)
+        tv_b = h.topk_vertices(20, side=0, metric=bbf.BBF_METRIC_BALANCED)
+        tv_d = h.topk_vertices(20, side=1, metric=bbf.BBF_METRIC_DEGREE)
+    rg = O.route_g(p, threads=THREADS)
+    assert (c["balanced"], c["unbalanced"], c["wedges_G"]) == (rg["B"], 0, rg["W_G"])
+    bal, unb = O.route_s(p, threads=THREADS)
+    assert np.array_equal(bu, bal[:g.n_u]) and np.array_equal(bv, bal[g.n_u:])
+    assert not nu.any() and not nv.any()
+    assert pairs == O.topk_pairs(p, 50, side=0, threads=THREADS)
+    assert tv_b == O.topk_vertices(p, 20, 0, "balanced", threads=THREADS)
+    assert tv_d == O.topk_vertices(p, 20, 1, "degree")
+
+
+def test_topk_vertices_signed_graph(bbf):
+    g = G.config2()
+    with bbf.Graph.from_synth(g) as h:
+        got = h.topk_vertices(100, side=1, metric=bbf.BBF_METRIC_BALANCED)
+        got_all = h.topk_vertices(10 ** 6, side=0, metric=bbf.BBF_METRIC_DEGREE)
+    assert got == O.topk_vertices(g, 100, 1, "balanced", threads=THREADS)
+    assert got_all == O.topk_vertices(g, 10 ** 6, 0, "degree")
