@@ -29,7 +29,10 @@
 namespace bbf {
 namespace {
 
-constexpr int kT3Threads = 1024 / kT3Ctas;
+#ifndef BBF_T3_THREADS
+#define BBF_T3_THREADS (1024 / BBF_T3_CTAS)
+#endif
+constexpr int kT3Threads = BBF_T3_THREADS;
 constexpr int kT3Warps = kT3Threads / 32;
 constexpr uint32_t kBm = kWin / 32;   // bitmap words
 constexpr int kT1Warps = 12;
@@ -288,6 +291,55 @@ struct Rec {  // 16 B segment record
   uint32_t p, len, wv, pad;
 };
 
+// The kCE entries of one chunk: vm has bit j set iff entry j belongs to the owner record.
+// MODE 0: pass 1 in a dense window, 1: pass 1 with the touched-word bitmap, 2: pass 2.
+template <int MODE, bool CP, bool WIDE>
+__device__ __forceinline__ void t3_chunk(const uint32_t (&ev)[kCE], uint32_t vm, uint32_t cbase,
+                                         uint32_t* ctr, uint32_t* bm, uint32_t word0, uint32_t shamt,
+                                         uint32_t oshamt, uint32_t wv, uint32_t& cb, uint32_t& cn) {
+#pragma unroll
+  for (int j = 0; j < (int)kCE; ++j) {
+    if (!((vm >> j) & 1u)) continue;
+    if (CP) {
+      if (MODE == 2) t3_share_cp(cbase, ev[j], shamt, oshamt, cb, cn);
+      else if (MODE == 0) t3_inc_cp<false>(cbase, bm, word0, ev[j], shamt);
+      else t3_inc_cp<true>(cbase, bm, word0, ev[j], shamt);
+    } else {
+      if (MODE == 2) t3_share_c<WIDE>(ctr, word0, ev[j], wv, cb, cn);
+      else if (MODE == 0) t3_inc_c<WIDE, false>(ctr, bm, word0, ev[j], wv);
+      else t3_inc_c<WIDE, true>(ctr, bm, word0, ev[j], wv);
+    }
+  }
+}
+
+// One flattened step of a record batch: lane L takes chunk base + L; its owner is the last record
+// starting at or before it in this step (start bitmask + per-warp owner table), else the owner
+// carried over from the previous step.
+struct StepMeta {
+  uint32_t c, ch, p, len, wv, ow, gs, smask;
+};
+
+__device__ __forceinline__ StepMeta step_lookup(uint32_t base, uint32_t nch, uint32_t excl, const Rec& rc,
+                                                int& carry, uint8_t* own, int lane) {
+  StepMeta m;
+  const bool st = nch > 0 && excl >= base && excl < base + 32;
+  if (st) own[excl - base] = (uint8_t)lane;
+  m.smask = __reduce_or_sync(0xffffffffu, st ? 1u << (excl - base) : 0u);
+  __syncwarp();
+  const uint32_t mm = m.smask & (0xffffffffu >> (31 - lane));
+  m.gs = mm ? 31 - __clz(mm) : 0;
+  m.ow = mm ? (uint32_t)own[m.gs] : (uint32_t)carry;
+  __syncwarp();
+  carry = __shfl_sync(0xffffffffu, (int)m.ow, 31);
+  const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, m.ow);
+  m.p = __shfl_sync(0xffffffffu, rc.p, m.ow);
+  m.len = __shfl_sync(0xffffffffu, rc.len, m.ow);
+  m.wv = __shfl_sync(0xffffffffu, rc.wv, m.ow);
+  m.c = base + lane;
+  m.ch = m.p / kCE + (m.c - o_excl);
+  return m;
+}
+
 template <bool PV, bool PAIRS, int ENC>
 __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) {
   constexpr bool WIDE = ENC == kEncWide, CP = ENC == kEncCompact;
@@ -401,7 +453,11 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       const uint32_t cbase = (uint32_t)__cvta_generic_to_shared(ctr) - 4u * word0;
       const Rec* rw = R + (size_t)k * RS;
       // records per warp batch: spread a window's records over all 32 warps (>= 2 batches each)
+      #ifdef BBF_T3_BSZ
+      const uint32_t bsz = BBF_T3_BSZ;
+#else
       const uint32_t bsz = min(32u, max(2u, (nrec + 2 * kT3Warps - 1) / (2 * kT3Warps)));
+#endif
       // dense window: at least as many wedges as counter words -> no touched-word bitmap, the
       // epilogue scans every word of the window
       const uint32_t nwk = min(kWin, Z.WB[5] - word0);
@@ -447,10 +503,72 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           const uint32_t incl = warp_incl_scan(nch, lane), excl = incl - nch;
           const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
           int carry = 0;
+#ifdef BBF_T3_PROF
           if (pass == 0 && lane == 0) {
             atomicAdd(&sh_dbg[0], (unsigned long long)((T + 31) / 32));
             atomicAdd(&sh_dbg[1], (unsigned long long)T);
           }
+#endif
+#ifdef BBF_T3_PREFETCH
+          // software pipeline: step base + 32's owner lookup and chunk loads are issued before
+          // step base's counter updates (needs the registers of <= 768 threads per CTA)
+          StepMeta cur{}, nxt{};
+          uint4 qc[kCE / 4], qn[kCE / 4];
+          if (T) {
+            cur = step_lookup(0, nch, excl, rc, carry, sh_own[warp], lane);
+#pragma unroll
+            for (int h = 0; h < (int)(kCE / 4); ++h)
+              qc[h] = cur.c < T ? reinterpret_cast<const uint4*>(adjc)[cur.ch * (kCE / 4) + h] : make_uint4(0u, 0u, 0u, 0u);
+          }
+          for (uint32_t base = 0; base < T; base += 32) {
+            if (base + 32 < T) {
+              nxt = step_lookup(base + 32, nch, excl, rc, carry, sh_own[warp], lane);
+#pragma unroll
+              for (int h = 0; h < (int)(kCE / 4); ++h)
+                qn[h] = nxt.c < T ? reinterpret_cast<const uint4*>(adjc)[nxt.ch * (kCE / 4) + h] : make_uint4(0u, 0u, 0u, 0u);
+            }
+            const uint32_t c = cur.c;
+            const uint32_t shamt = 22u + 5u * (cur.wv >> 31), oshamt = 49u - shamt;
+            uint32_t cb = 0, cn = 0;
+            if (c < T) {
+              const uint32_t e0 = kCE * cur.ch;
+              uint32_t ev[kCE];
+#pragma unroll
+              for (int h = 0; h < (int)(kCE / 4); ++h) {
+                ev[4 * h] = qc[h].x; ev[4 * h + 1] = qc[h].y; ev[4 * h + 2] = qc[h].z; ev[4 * h + 3] = qc[h].w;
+              }
+#pragma unroll
+              for (int j = 0; j < (int)kCE; ++j) {
+                const uint32_t e = e0 + j;
+                if (e >= cur.p && e < cur.p + cur.len) {
+                  if (CP) {
+                    if (pass == 1) t3_share_cp(cbase, ev[j], shamt, oshamt, cb, cn);
+                    else if (dense) t3_inc_cp<false>(cbase, bm, word0, ev[j], shamt);
+                    else t3_inc_cp<true>(cbase, bm, word0, ev[j], shamt);
+                  } else {
+                    if (pass == 1) t3_share_c<WIDE>(ctr, word0, ev[j], cur.wv, cb, cn);
+                    else if (dense) t3_inc_c<WIDE, false>(ctr, bm, word0, ev[j], cur.wv);
+                    else t3_inc_c<WIDE, true>(ctr, bm, word0, ev[j], cur.wv);
+                  }
+                }
+              }
+            }
+            if (pass == 1 && __any_sync(0xffffffffu, (cb | cn) != 0)) {
+              const uint32_t ib = warp_incl_scan(cb, lane), in = warp_incl_scan(cn, lane);
+              const int src = cur.gs > 0 ? (int)cur.gs - 1 : 0;
+              const uint32_t pb = __shfl_sync(0xffffffffu, ib, src), pn = __shfl_sync(0xffffffffu, in, src);
+              const bool last = c < T && (c + 1 == T || lane == 31 || ((cur.smask >> (lane + 1)) & 1u));
+              if (last) {
+                sh_acc[warp][0][cur.ow] += ib - (cur.gs > 0 ? pb : 0u);
+                sh_acc[warp][1][cur.ow] += in - (cur.gs > 0 ? pn : 0u);
+              }
+              __syncwarp();
+            }
+            cur = nxt;
+#pragma unroll
+            for (int h = 0; h < (int)(kCE / 4); ++h) qc[h] = qn[h];
+          }
+#else
           // kU steps per iteration: owner lookups first, then all chunk loads in flight, then
           // the counter updates (hides the global-load latency behind the other steps' work)
           for (uint32_t base0 = 0; base0 < T; base0 += 32 * kU) {
@@ -478,7 +596,11 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             for (int u = 0; u < kU; ++u)
 #pragma unroll
               for (int h = 0; h < kCE / 4; ++h)
+#if defined(BBF_T3_EXPT) && BBF_T3_EXPT == 2
+                q[u][h] = (base0 + 32 * u + lane < T) ? make_uint4(word0 + (((ch[u] * 2654435761u + h * 40503u) >> 8) & 0x3FFFu), word0 + (((ch[u] * 2654435761u + h * 40503u) >> 11) & 0x3FFFu), word0 + (((ch[u] * 2654435761u + h * 40503u) >> 14) & 0x3FFFu), word0 + (((ch[u] * 2654435761u + h * 40503u) >> 17) & 0x3FFFu))
+#else
                 q[u][h] = (base0 + 32 * u + lane < T) ? reinterpret_cast<const uint4*>(adjc)[ch[u] * (kCE / 4) + h]
+#endif
                                                      : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
@@ -489,24 +611,17 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
                 const uint32_t e0 = kCE * ch[u];
                 uint32_t ev[kCE];
 #pragma unroll
-                for (int h = 0; h < kCE / 4; ++h) {
+                for (int h = 0; h < (int)(kCE / 4); ++h) {
                   ev[4 * h] = q[u][h].x; ev[4 * h + 1] = q[u][h].y; ev[4 * h + 2] = q[u][h].z; ev[4 * h + 3] = q[u][h].w;
                 }
-#pragma unroll
-                for (int j = 0; j < kCE; ++j) {
-                  const uint32_t e = e0 + j;
-                  if (e >= o_p[u] && e < o_p[u] + o_len[u]) {
-                    if (CP) {
-                      if (pass == 1) t3_share_cp(cbase, ev[j], shamt, oshamt, cb, cn);
-                      else if (dense) t3_inc_cp<false>(cbase, bm, word0, ev[j], shamt);
-                      else t3_inc_cp<true>(cbase, bm, word0, ev[j], shamt);
-                    } else {
-                      if (pass == 1) t3_share_c<WIDE>(ctr, word0, ev[j], o_wv[u], cb, cn);
-                      else if (dense) t3_inc_c<WIDE, false>(ctr, bm, word0, ev[j], o_wv[u]);
-                      else t3_inc_c<WIDE, true>(ctr, bm, word0, ev[j], o_wv[u]);
-                    }
-                  }
-                }
+                // entries [o_p, o_p + o_len) of this chunk as a bit mask
+                const int lo = (int)(o_p[u] > e0 ? o_p[u] - e0 : 0u);
+                const uint32_t end = o_p[u] + o_len[u];
+                const int hi = (int)(end - e0 < kCE ? end - e0 : kCE);
+                const uint32_t vm = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
+                if (pass == 1) t3_chunk<2, CP, WIDE>(ev, vm, cbase, ctr, bm, word0, shamt, oshamt, o_wv[u], cb, cn);
+                else if (dense) t3_chunk<0, CP, WIDE>(ev, vm, cbase, ctr, bm, word0, shamt, oshamt, o_wv[u], cb, cn);
+                else t3_chunk<1, CP, WIDE>(ev, vm, cbase, ctr, bm, word0, shamt, oshamt, o_wv[u], cb, cn);
               }
               if (pass == 1 && __any_sync(0xffffffffu, (cb | cn) != 0)) {
                 // segmented sum over each owner's lane group; its last lane adds it (one writer
@@ -523,6 +638,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
               }
             }
           }
+#endif
           if (pass == 1) {
             __syncwarp();
             const uint32_t cb = sh_acc[warp][0][lane], cn = sh_acc[warp][1][lane];
