@@ -212,6 +212,20 @@ __device__ __forceinline__ uint32_t sh_load(uint32_t addr) {
   return r;
 }
 
+// predicated forms (no branch around each entry of a chunk): the update / load only happens if
+// `on` is non-zero; the predicated load returns 0 otherwise
+__device__ __forceinline__ void sh_red_add_if(uint32_t addr, uint32_t v, uint32_t on) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr),
+               "r"(v), "r"(on));
+}
+__device__ __forceinline__ uint32_t sh_load_if(uint32_t addr, uint32_t on) {
+  uint32_t r;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\tmov.u32 %0, 0;\n\t@p ld.shared.u32 %0, [%1];\n\t}"
+               : "=r"(r)
+               : "r"(addr), "r"(on));
+  return r;
+}
+
 template <bool BM>
 __device__ __forceinline__ void t3_inc_cp(uint32_t cbase, uint32_t* bm, uint32_t word0, uint32_t ev,
                                           uint32_t shamt) {
@@ -297,6 +311,25 @@ template <int MODE, bool CP, bool WIDE>
 __device__ __forceinline__ void t3_chunk(const uint32_t (&ev)[kCE], uint32_t vm, uint32_t cbase,
                                          uint32_t* ctr, uint32_t* bm, uint32_t word0, uint32_t shamt,
                                          uint32_t oshamt, uint32_t wv, uint32_t& cb, uint32_t& cn) {
+  if (CP && MODE == 0) {  // pass 1, dense window: branch-free predicated updates
+#pragma unroll
+    for (int j = 0; j < (int)kCE; ++j)
+      sh_red_add_if(cbase + 4u * (ev[j] & kCpWordMask), 1u << ((ev[j] >> shamt) & 31u), vm & (1u << j));
+    return;
+  }
+  if (CP && MODE == 2) {  // pass 2: predicated loads; sum of own-class counts minus #entries
+    uint32_t own = 0, oth = 0;
+#pragma unroll
+    for (int j = 0; j < (int)kCE; ++j) {
+      const uint32_t v = sh_load_if(cbase + 4u * (ev[j] & kCpWordMask), vm & (1u << j));
+      const uint32_t msk = (1u << (2u << ((ev[j] >> 20) & 3u))) - 1u;
+      own += (v >> ((ev[j] >> shamt) & 31u)) & msk;
+      oth += (v >> ((ev[j] >> oshamt) & 31u)) & msk;
+    }
+    cb += own - (uint32_t)__popc(vm);
+    cn += oth;
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < (int)kCE; ++j) {
     if (!((vm >> j) & 1u)) continue;
