@@ -63,6 +63,7 @@ struct EngineArgs {
   uint32_t kwin_cap;  // max windows per side
   uint32_t rec_stride;  // record slots per window: max middles + max unit work / kRecMax
   uint32_t dense_div;   // a window is scanned densely when wedges * dense_div >= its words
+  uint32_t bsz;         // records per warp batch (0 = adaptive)
   // pair candidates (top-k): balanced, unbalanced, (min id << 32 | max id)
   unsigned long long* cb;
   unsigned long long* cn;
@@ -486,11 +487,9 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       const uint32_t cbase = (uint32_t)__cvta_generic_to_shared(ctr) - 4u * word0;
       const Rec* rw = R + (size_t)k * RS;
       // records per warp batch: spread a window's records over all 32 warps (>= 2 batches each)
-      #ifdef BBF_T3_BSZ
-      const uint32_t bsz = BBF_T3_BSZ;
-#else
-      const uint32_t bsz = min(32u, max(2u, (nrec + 2 * kT3Warps - 1) / (2 * kT3Warps)));
-#endif
+            // records per warp batch: a fixed batch (a.bsz) amortises the batch set-up over more
+      // steps; 0 = spread the window's records over all warps (>= 2 batches each)
+      const uint32_t bsz = a.bsz ? a.bsz : min(32u, max(2u, (nrec + 2 * kT3Warps - 1) / (2 * kT3Warps)));
       // dense window: at least as many wedges as counter words -> no touched-word bitmap, the
       // epilogue scans every word of the window
       const uint32_t nwk = min(kWin, Z.WB[5] - word0);
@@ -981,6 +980,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   ea.rec_stride = (uint32_t)(std::max<uint32_t>(p->max_mid, 1) + p->max_work / kRecMax + 1);
   ea.cb = cb; ea.cn = cn; ea.cid = cid; ea.cap = cap;
   ea.dense_div = getenv("BBF_DENSE_DIV") ? (uint32_t)atoi(getenv("BBF_DENSE_DIV")) : 2u;
+  ea.bsz = getenv("BBF_T3_BSZ") ? (uint32_t)std::min(32, std::max(0, atoi(getenv("BBF_T3_BSZ")))) : 16u;
   cudaEvent_t e0, e1, e2;
   cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
   cudaError_t err;
