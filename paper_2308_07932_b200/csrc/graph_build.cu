@@ -79,24 +79,24 @@ __device__ __forceinline__ uint32_t row_of_edge(const uint64_t* __restrict__ rp,
 __global__ void k_entries(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ col,
                           const uint8_t* __restrict__ sg, uint64_t nnz, uint32_t n_u,
                           const uint32_t* __restrict__ lr_u, const uint32_t* __restrict__ lr_v,
-                          uint64_t* __restrict__ keys) {
+                          uint32_t lsh, uint64_t* __restrict__ keys) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t u = row_of_edge(rp, n_u, e);
     uint32_t v = col[e];
     uint64_t neg = sg[e] ? 0u : 1u;  // weight 0 = negative
     uint64_t a = lr_u[u], b = lr_v[v];
-    keys[e] = (a << 32) | (b << 1) | neg;
-    keys[nnz + e] = ((uint64_t)(n_u + b) << 32) | (a << 1) | neg;
+    keys[e] = (a << lsh) | (b << 1) | neg;
+    keys[nnz + e] = ((uint64_t)(n_u + b) << lsh) | (a << 1) | neg;
   }
 }
 
-__global__ void k_decode(const uint64_t* __restrict__ keys, uint64_t m, uint32_t* __restrict__ adj,
+__global__ void k_decode(const uint64_t* __restrict__ keys, uint64_t m, uint64_t lmask, uint32_t* __restrict__ adj,
                          uint32_t* err) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t k = keys[i];
-    uint32_t lo = (uint32_t)k;
+    const uint32_t lo = (uint32_t)(k & lmask);
     adj[i] = (lo >> 1) | ((lo & 1u) << 31);
     if (i > 0 && (keys[i - 1] >> 1) == (k >> 1)) atomicOr(err, kErrDup);  // same row, same col
   }
@@ -513,7 +513,11 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
   BBF_CUDA(dmalloc(&d_err, 4 * sizeof(uint32_t), st));
   BBF_CUDA(cudaMemsetAsync(d_err, 0, 4 * sizeof(uint32_t), st));
   size_t t3 = 0, t5 = 0;
-  int ebits = 32 + bits_for(std::max<uint32_t>(n, 1));
+  // key = row << lsh | l << 1 | neg, lsh = 1 + bits of the largest local rank: the radix sort
+  // covers bits(n) + lsh bits (48 on config 5 instead of 56)
+  const uint32_t lsh = 1 + bits_for(std::max<uint32_t>(std::max(n_u, n_v), 1));
+  const uint64_t lmask = (1ull << lsh) - 1ull;
+  int ebits = (int)lsh + bits_for(std::max<uint32_t>(n, 1));
   cub::DeviceRadixSort::SortKeys(nullptr, t3, (uint64_t*)nullptr, (uint64_t*)nullptr, (int64_t)m, 0,
                                  ebits, st);
   cub::DeviceScan::InclusiveSum(nullptr, t5, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n, st);
@@ -527,9 +531,9 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     uint64_t *ek, *eks;
     BBF_CUDA(dmalloc(&ek, 8ull * m, st));
     BBF_CUDA(dmalloc(&eks, 8ull * m, st));
-    k_entries<<<grid_for(nnz, 256), 256, 0, st>>>(d_rp, d_col, d_sg, nnz, n_u, lr_u, lr_v, ek);
+    k_entries<<<grid_for(nnz, 256), 256, 0, st>>>(d_rp, d_col, d_sg, nnz, n_u, lr_u, lr_v, lsh, ek);
     BBF_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t3, ek, eks, (int64_t)m, 0, ebits, st));
-    k_decode<<<grid_for(m, 256), 256, 0, st>>>(eks, m, g->adj, d_err);
+    k_decode<<<grid_for(m, 256), 256, 0, st>>>(eks, m, lmask, g->adj, d_err);
     g->launches += 6;
     dfree(ek, st);
     dfree(eks, st);

@@ -357,3 +357,20 @@ def test_topk_vertices_signed_graph(bbf):
         got_all = h.topk_vertices(10 ** 6, side=0, metric=bbf.BBF_METRIC_DEGREE)
     assert got == O.topk_vertices(g, 100, 1, "balanced", threads=THREADS)
     assert got_all == O.topk_vertices(g, 10 ** 6, 0, "degree")
+
+
+@pytest.mark.parametrize("env", [{"BBF_T3_BSZ": "2"}, {"BBF_T3_BSZ": "32"}, {"BBF_T3_BSZ": "0"},
+                                 {"BBF_DENSE_DIV": "1000000"}, {"BBF_DENSE_DIV": "1"}])
+def test_schedule_independence(bbf, monkeypatch, env):
+    """Counts do not depend on the hub kernel's schedule (record batch size, dense-window
+    threshold) — the GPU analogue of SPEC.md:359's determinism across worker counts."""
+    g = G.config2()
+    with bbf.Graph.from_synth(g, flags=bbf.BBF_FORCE_SPARSE) as h:
+        ref = h.count_per_vertex()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    with bbf.Graph.from_synth(g, flags=bbf.BBF_FORCE_SPARSE) as h:
+        got = h.count_per_vertex()
+    assert (got[0]["balanced"], got[0]["unbalanced"]) == (ref[0]["balanced"], ref[0]["unbalanced"])
+    for a, b in zip(got[1:], ref[1:]):
+        assert np.array_equal(a, b)
