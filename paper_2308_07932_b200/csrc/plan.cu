@@ -253,7 +253,10 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   BBF_CUDA(cudaStreamSynchronize(st));
   p->W_pruned = h_wp;
   p->W_full = h_wf;
-  uint64_t w_target = std::max<uint64_t>(h_wp / ((uint64_t)g->num_sms * 6ull + 1), 1ull << 16);
+  // hub units of ~1/6 of one SM's share of the whole job: with N ranks the share is W / (N * SMs),
+  // so a rank's largest unit stays well below its per-SM work at any N
+  const uint64_t nranks = g->comm ? (uint64_t)g->comm->nranks : 1ull;
+  uint64_t w_target = std::max<uint64_t>(h_wp / (nranks * (uint64_t)g->num_sms * 6ull + 1), 1ull << 16);
 
   // tiers and units
   BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
