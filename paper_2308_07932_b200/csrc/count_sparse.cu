@@ -385,6 +385,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
   __shared__ uint32_t sh_unit, sh_c[4];
   __shared__ uint32_t sh_acc[kT3Warps][2][32];  // per-warp pass-2 accumulators of a batch
   __shared__ uint8_t sh_own[kT3Warps][32];      // per-warp owner table of a flattened step
+  __shared__ Zones sh_z;                        // the current unit's end-side zone table
   const uint32_t* __restrict__ adjc = a.adjc;
   __shared__ unsigned long long sh_red[2][kT3Warps];
   __shared__ unsigned long long sh_dbg[4];  // pass-1 steps, pass-1 chunks, small windows, dense windows
@@ -412,7 +413,11 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
     const uint32_t x = u.x;
     const bool xu = x < a.n_u;
     const uint32_t sb = xu ? 0 : a.n_u, ob = xu ? a.n_u : 0, lx = x - sb;
-    const Zones& Z = a.z[xu ? 0 : 1];
+    // the end side's zone table in shared memory (an indexed kernel-parameter read is an LDC
+    // with a long-scoreboard dependency on every epilogue word)
+    if (tid < 11) reinterpret_cast<uint32_t*>(&sh_z)[tid] = reinterpret_cast<const uint32_t*>(&a.z[xu ? 0 : 1])[tid];
+    __syncthreads();
+    const Zones& Z = sh_z;
     const uint32_t K = (Z.WB[5] + kWin - 1) / kWin;
     const uint32_t m_lo = a.mid ? a.mid[x] : a.off[x];
     const uint32_t m = a.end1[x] - m_lo;
@@ -683,7 +688,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           }
         }
         __syncthreads();
-        T3_MARK(2 + pass);
+        T3_MARK(nrec < 64 ? 1 : 2 + pass);  // slot 1: set-up + passes of small windows
       }
 
       // ---------------- epilogue: Lemma 2 per touched end (Alg. 2 lines 15-18), clear the window
