@@ -513,22 +513,30 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       for (int pass = 0; pass < (PV ? 2 : 1); ++pass) {
         // batches of bsz records; the next batch's records are loaded while this one is
         // processed (their global-load latency was the kernel's top stall)
-        auto fetch = [&](uint32_t& btx, Rec& rx) {
-          uint32_t b0 = 0;
-          if (lane == 0) b0 = atomicAdd(&sh_c[pass], 1u);
-          btx = __shfl_sync(0xffffffffu, b0, 0);
-          const uint32_t r = btx * bsz + lane;
+        // guided batches: up to bsz records, shrinking near the end of the window so the warps
+        // reach the pass barrier together
+        auto fetch = [&](uint32_t& cntx, Rec& rx) {
+          uint32_t s0 = 0, c0 = 0;
+          if (lane == 0) {
+            const uint32_t seen = *reinterpret_cast<volatile uint32_t*>(&sh_c[pass]);
+            const uint32_t rem = seen < nrec ? nrec - seen : 0u;
+            const uint32_t sz = min(bsz, max(12u, rem / kT3Warps));
+            s0 = atomicAdd(&sh_c[pass], sz);
+            c0 = s0 < nrec ? min(sz, nrec - s0) : 0u;
+          }
+          const uint32_t r0x = __shfl_sync(0xffffffffu, s0, 0);
+          cntx = __shfl_sync(0xffffffffu, c0, 0);
           rx = Rec{0, 0, 0, 0};
-          if (btx * bsz < nrec && (uint32_t)lane < bsz && r < nrec) rx = rw[r];
+          if ((uint32_t)lane < cntx) rx = rw[r0x + lane];
         };
-        uint32_t bt_next;
+        uint32_t cnt_next;
         Rec rc_next;
-        fetch(bt_next, rc_next);
+        fetch(cnt_next, rc_next);
         while (true) {
-          const uint32_t bt = bt_next;
+          const uint32_t cnt = cnt_next;
           const Rec rc = rc_next;
-          if (bt * bsz >= nrec) break;
-          fetch(bt_next, rc_next);
+          if (cnt == 0) break;
+          fetch(cnt_next, rc_next);
           if (pass == 1) { sh_acc[warp][0][lane] = 0; sh_acc[warp][1][lane] = 0; __syncwarp(); }
           // The batch's records are flattened over the lanes in 16-B chunks of the adjacency
           // (4 entries, one LDG.128 per lane, consecutive lanes on consecutive chunks of a
