@@ -131,7 +131,7 @@ constexpr uint32_t kCWordMask = (1u << kCWordBits) - 1u;
 #define BBF_T3_CTAS 1
 #endif
 constexpr uint32_t kT3Ctas = BBF_T3_CTAS;           // hub-kernel CTAs per SM
-constexpr uint32_t kWin = 48 * 1024 / kT3Ctas;      // counter words per hub-kernel window
+constexpr uint32_t kWin = 51 * 1024 / kT3Ctas;      // counter words per hub-kernel window (204 KB)
 
 __host__ __device__ inline uint32_t encode_caddr(const Zones& z, uint32_t l) {
   uint32_t g, sh = 0, wc = 0, wide = 0;
