@@ -283,7 +283,7 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_pt
   }
   bbf_status s = BBF_OK;
   keep_pool(device);
-  cudaError_t e = dmalloc(&g->d_acc, 16 * sizeof(unsigned long long), g->stream);
+  cudaError_t e = dmalloc(&g->d_acc, 32 * sizeof(unsigned long long), g->stream);
   if (e == cudaSuccess) e = dmalloc(&g->pv, 16ull * (g->n + 1), g->stream);
   if (e != cudaSuccess) s = cuda_status(e, "cudaMalloc");
   if (s == BBF_OK) s = build_graph(g, row_ptr, col, sign, dptr);

@@ -51,8 +51,9 @@ struct EngineArgs {
   const uint64_t* work;
   const uint32_t* inv;
   const uint32_t* t1;
+  const uint32_t* t2;
   const Unit* units;
-  uint32_t n_t1, n_units;
+  uint32_t n_t1, n_t2, n_units;
   uint32_t n_u, n;
   Zones z[2];
   int rank, nranks;
@@ -931,6 +932,167 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
   }
 }
 
+// ===================================================================================== T2
+// Mid-size starts (kT1Max < work <= T2 max): one CTA per start, a shared open-addressing hash of
+// (end rank + 1 -> a | d << 16) with S = pow2 >= 2 * work slots, so a start is done in one sweep
+// of its wedges (no counter windows, no records).  Warps take chunks of 32 middles; inside a
+// chunk the wedges are spread over the lanes as in k_t1.  a + d <= #middles <= work < 2^16.
+constexpr int kT2Threads = 512;
+constexpr int kT2Warps = kT2Threads / 32;
+constexpr uint32_t kT2Per = 5 * 32;  // per-warp scratch words
+
+template <bool PV, bool PAIRS>
+__global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
+  extern __shared__ uint32_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  volatile uint32_t* keys = smem;
+  uint32_t* vals = smem + kT2Slots;
+  uint32_t* sh_incl = vals + kT2Slots + warp * kT2Per;
+  uint32_t* sh_s = sh_incl + 32;
+  uint32_t* sh_wv = sh_s + 32;
+  uint32_t* sh_mb = sh_wv + 32;
+  uint32_t* sh_mn = sh_mb + 32;
+  __shared__ uint32_t sh_item, sh_c[2];
+  __shared__ unsigned long long sh_red[2][kT2Warps];
+  for (uint32_t i = tid; i < 2 * kT2Slots; i += kT2Threads) ((uint32_t*)keys)[i] = 0;
+  sh_mb[lane] = 0;
+  sh_mn[lane] = 0;
+  unsigned long long totB = 0, totN = 0;
+  __syncthreads();
+  while (true) {
+    if (tid == 0) {
+      sh_item = (uint32_t)atomicAdd(&a.acc[16], 1ull);
+      sh_c[0] = 0;
+      sh_c[1] = 0;
+    }
+    __syncthreads();
+    const uint64_t ti = (uint64_t)sh_item * a.nranks + a.rank;
+    if (ti >= a.n_t2) break;
+    const uint32_t x = a.t2[ti];
+    const bool xu = x < a.n_u;
+    const uint32_t sb = xu ? 0 : a.n_u, ob = xu ? a.n_u : 0;
+    const uint32_t m_lo = a.mid ? a.mid[x] : a.off[x];
+    const uint32_t m = a.end1[x] - m_lo;
+    const uint32_t W = (uint32_t)a.work[x];
+    uint32_t S = 64;
+    while (S < 2 * W && S < kT2Slots) S <<= 1;
+    const uint32_t mask = S - 1;
+#pragma unroll 1
+    // middles spread over all warps: chunks of cs <= 32 middles, chunk ck to warp ck mod warps
+    const uint32_t cs = min(32u, max(1u, (m + kT2Warps - 1) / kT2Warps));
+    for (int pass = 0; pass < (PV ? 2 : 1); ++pass) {
+      for (uint32_t ck = warp; ck * cs < m; ck += kT2Warps) {
+        const uint32_t cb = ck * cs;
+        const uint32_t i = cb + lane;
+        uint32_t wv = 0, s = 0, len = 0;
+        if ((uint32_t)lane < cs && i < m) {
+          wv = a.adj[m_lo + i];
+          s = a.ub[m_lo + i];
+          const uint32_t en = a.end1[ob + (wv & kMask)];
+          len = en > s ? en - s : 0;
+        }
+        const uint32_t incl = warp_incl_scan(len, lane);
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (tot == 0) continue;
+        sh_incl[lane] = incl;
+        sh_s[lane] = s;
+        sh_wv[lane] = wv;
+        __syncwarp();
+        for (uint32_t t = lane; t < ((tot + 31) & ~31u); t += 32) {
+          if (t < tot) {
+            uint32_t lo = 0, hi = 31;  // first j with incl[j] > t
+            while (lo < hi) {
+              const uint32_t md = (lo + hi) >> 1;
+              if (sh_incl[md] > t) hi = md; else lo = md + 1;
+            }
+            const uint32_t j = lo;
+            const uint32_t excl = j ? sh_incl[j - 1] : 0;
+            const uint32_t ev = a.adj[sh_s[j] + (t - excl)];
+            const uint32_t l = ev & kMask;
+            const uint32_t cls = (ev ^ sh_wv[j]) >> 31;
+            const uint32_t key = l + 1;
+            uint32_t h = hslot(l, mask);
+            if (pass == 0) {
+              while (true) {
+                uint32_t k = keys[h];
+                if (k == key) break;
+                if (k == 0) {
+                  k = atomicCAS((uint32_t*)&keys[h], 0u, key);
+                  if (k == 0 || k == key) break;
+                }
+                h = (h + 1) & mask;
+              }
+              atomicAdd(&vals[h], cls ? 65536u : 1u);
+            } else {
+              while (keys[h] != key) h = (h + 1) & mask;
+              const uint32_t v = vals[h];
+              const uint32_t ad = v & 0xffffu, dd = v >> 16;
+              const uint32_t b2 = cls ? dd - 1 : ad - 1, n2 = cls ? ad : dd;
+              if (b2) atomicAdd(&sh_mb[j], b2);
+              if (n2) atomicAdd(&sh_mn[j], n2);
+            }
+          }
+        }
+        __syncwarp();
+        if (pass == 1) {
+          const uint32_t b2 = sh_mb[lane], n2 = sh_mn[lane];
+          if (b2 | n2) {
+            const uint32_t vr = ob + (wv & kMask);
+            if (b2) atomicAdd(&a.pv[2ull * vr], (unsigned long long)b2);
+            if (n2) atomicAdd(&a.pv[2ull * vr + 1], (unsigned long long)n2);
+          }
+          sh_mb[lane] = 0;
+          sh_mn[lane] = 0;
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+    }
+    // ---- epilogue: Lemma 2 per end (Alg. 2 lines 15-18), clear
+    unsigned long long xB = 0, xN = 0;
+    for (uint32_t k = tid; k < S; k += kT2Threads) {
+      const uint32_t key = keys[k];
+      if (!key) continue;
+      const uint32_t v = vals[k];
+      keys[k] = 0;
+      vals[k] = 0;
+      const uint32_t A = v & 0xffffu, D = v >> 16;
+      const uint32_t fb = ((A * (A - 1u)) >> 1) + ((D * (D - 1u)) >> 1), fn = A * D;
+      if (!(fb | fn)) continue;
+      xB += fb;
+      xN += fn;
+      const uint32_t wrow = sb + key - 1;
+      if (PV) {
+        if (fb) atomicAdd(&a.pv[2ull * wrow], (unsigned long long)fb);
+        if (fn) atomicAdd(&a.pv[2ull * wrow + 1], (unsigned long long)fn);
+      }
+      if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
+    }
+    totB += xB;
+    totN += xN;
+    if (PV) {
+      const unsigned long long b = warp_sum(xB), nn = warp_sum(xN);
+      if (lane == 0) { sh_red[0][warp] = b; sh_red[1][warp] = nn; }
+      __syncthreads();
+      if (warp == 0) {
+        const unsigned long long bb = warp_sum(lane < kT2Warps ? sh_red[0][lane] : 0ull);
+        const unsigned long long n2 = warp_sum(lane < kT2Warps ? sh_red[1][lane] : 0ull);
+        if (lane == 0 && (bb | n2)) {
+          atomicAdd(&a.pv[2ull * x], bb);
+          atomicAdd(&a.pv[2ull * x + 1], n2);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  totB = warp_sum(totB);
+  totN = warp_sum(totN);
+  if (lane == 0 && (totB | totN)) {
+    atomicAdd(&a.acc[0], totB);
+    atomicAdd(&a.acc[1], totN);
+  }
+}
+
 template <bool PV, bool PAIRS, int ENC>
 cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, Plan* p,
                           cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2) {
@@ -949,6 +1111,13 @@ cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, P
   cudaEventRecord(e1, st);
   if (p->n_t1) {
     k_t1<PV, PAIRS><<<g->num_sms * 2, kT1Warps * 32, smem1, st>>>(ea);
+    g->launches++;
+  }
+  if (p->n_t2) {
+    const size_t smem2 = sizeof(uint32_t) * (2 * kT2Slots + kT2Warps * kT2Per);
+    err = cudaFuncSetAttribute(k_t2<PV, PAIRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+    if (err != cudaSuccess) return err;
+    k_t2<PV, PAIRS><<<g->num_sms * 3, kT2Threads, smem2, st>>>(ea);
     g->launches++;
   }
   cudaEventRecord(e2, st);
@@ -979,12 +1148,12 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     BBF_CUDA(dmalloc(&g->scratch, need * sizeof(uint32_t), st));
     g->scratch_words = need;
   }
-  BBF_CUDA(cudaMemsetAsync(g->d_acc, 0, 16 * sizeof(unsigned long long), st));
+  BBF_CUDA(cudaMemsetAsync(g->d_acc, 0, 32 * sizeof(unsigned long long), st));
   EngineArgs ea{};
   ea.off = g->off; ea.adj = g->adj; ea.adjc = g->adjc; ea.runid = g->runid; ea.runs = g->runs;
   ea.nruns = g->nruns; ea.mid = p->route == 0 ? g->mid : nullptr; ea.end1 = g->end1;
-  ea.ub = p->ub; ea.work = p->work; ea.inv = g->inv; ea.t1 = p->t1; ea.units = p->units;
-  ea.n_t1 = p->n_t1; ea.n_units = p->n_units; ea.n_u = g->n_u; ea.n = g->n;
+  ea.ub = p->ub; ea.work = p->work; ea.inv = g->inv; ea.t1 = p->t1; ea.t2 = p->t2; ea.units = p->units;
+  ea.n_t1 = p->n_t1; ea.n_t2 = p->n_t2; ea.n_units = p->n_units; ea.n_u = g->n_u; ea.n = g->n;
   ea.z[0] = g->zones[0]; ea.z[1] = g->zones[1];
   ea.rank = rank; ea.nranks = nranks;
   ea.acc = g->d_acc; ea.pv = (unsigned long long*)g->pv; ea.scratch = g->scratch;

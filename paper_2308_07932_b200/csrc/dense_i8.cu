@@ -776,7 +776,7 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
   const bool do_v = per_vertex || !do_u;
   const uint64_t ru = g->drows[0], rv = g->drows[1], ku = g->dk[0], kv = g->dk[1];
   uint8_t *Au = g->dA[0], *Su = g->dS[0], *Av = g->dA[1], *Sv = g->dS[1];
-  BBF_CUDA(cudaMemsetAsync(g->d_acc, 0, 16 * sizeof(unsigned long long), st));
+  BBF_CUDA(cudaMemsetAsync(g->d_acc, 0, 32 * sizeof(unsigned long long), st));
   BBF_CUDA(cudaFuncSetAttribute(k_dense_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
   BBF_CUDA(cudaFuncSetAttribute(k_dense_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmemBytes));
   cudaEvent_t e0, e1;

@@ -14,6 +14,8 @@
 namespace bbf {
 
 constexpr uint32_t kT1Max = 512;  // starts with at most this many (pruned) wedges -> warp hash
+// starts with (kT1Max, kT2Max] wedges -> one CTA with a shared hash (k_t2); above -> hub units
+// (k_t3).  Env BBF_T2_MAX overrides (0 disables the T2 tier).
 
 namespace {
 
@@ -97,16 +99,17 @@ __global__ void k_row_work(uint32_t n, const uint64_t* __restrict__ pre, const u
 }
 
 // count T1 / T3 rows, W per tier, units per T3 row
-__global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, uint64_t w_target,
+__global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, uint64_t w_target, uint64_t t2max,
                        const uint32_t* __restrict__ mlo, const uint32_t* __restrict__ mhi,
                        uint32_t* __restrict__ nunits, unsigned long long* __restrict__ acc) {
   uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long w1 = 0, w3 = 0, m3 = 0;
+  unsigned long long w1 = 0, w3 = 0, m3 = 0, w2 = 0;
   uint32_t u = 0;
   if (x < n) {
     uint64_t w = work[x];
     if (w > 0 && w <= kT1Max) w1 = w;
-    if (w > kT1Max) {
+    if (w > kT1Max && w <= t2max) w2 = w;
+    if (w > kT1Max && w > t2max) {
       w3 = w;
       m3 = mhi[x] - mlo[x];
       u = (uint32_t)std::min<uint64_t>((w + w_target - 1) / w_target, 4096);
@@ -117,13 +120,24 @@ __global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, uint64_t w
     w1 += __shfl_xor_sync(0xffffffffu, w1, o);
     w3 += __shfl_xor_sync(0xffffffffu, w3, o);
     m3 += __shfl_xor_sync(0xffffffffu, m3, o);
+    w2 += __shfl_xor_sync(0xffffffffu, w2, o);
   }
   if ((threadIdx.x & 31) == 0) {
     if (w1) atomicAdd(&acc[0], w1);
     if (w3) atomicAdd(&acc[1], w3);
     if (m3) atomicAdd(&acc[2], m3);
+    if (w2) atomicAdd(&acc[3], w2);
   }
 }
+
+struct IsT2 {
+  const uint64_t* work;
+  uint64_t t2max;
+  __device__ __forceinline__ bool operator()(uint32_t x) const {
+    uint64_t w = work[x];
+    return w > kT1Max && w <= t2max;
+  }
+};
 
 struct IsT1 {
   const uint64_t* work;
@@ -191,6 +205,7 @@ void free_plan(Plan* p, cudaStream_t st) {
   if (p->ub) dfree(p->ub, st);
   if (p->work) dfree(p->work, st);
   if (p->t1) dfree(p->t1, st);
+  if (p->t2) dfree(p->t2, st);
   if (p->units) dfree(p->units, st);
   *p = Plan{};
 }
@@ -259,40 +274,48 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   uint64_t w_target = std::max<uint64_t>(h_wp / (nranks * (uint64_t)g->num_sms * 6ull + 1), 1ull << 16);
 
   // tiers and units
+  // a T2 start's distinct ends (<= its wedges) must fit the k_t2 hash at load <= 1/2
+  const uint64_t t2max = std::min<uint64_t>(
+      getenv("BBF_T2_MAX") ? (uint64_t)atoll(getenv("BBF_T2_MAX")) : kT2MaxDefault, kT2Slots / 2);
   BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
   if (n) {
-    k_tier<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, p->work, w_target, sb, se, nunits, acc);
+    k_tier<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, p->work, w_target, t2max, sb, se, nunits, acc);
     g->launches += 1;
   }
   BBF_CUDA(dmalloc(&p->t1, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&p->t2, 4ull * (n + 1), st));
   uint32_t* d_nsel;
   BBF_CUDA(dmalloc(&d_nsel, 8, st));
   {
     cub::CountingInputIterator<uint32_t> it(0);
-    size_t tb = 0;
+    size_t tb = 0, tb3 = 0;
     cub::DeviceSelect::If(nullptr, tb, it, p->t1, d_nsel, (int)n, IsT1{p->work}, st);
+    cub::DeviceSelect::If(nullptr, tb3, it, p->t2, d_nsel + 1, (int)n, IsT2{p->work, t2max}, st);
     size_t tb2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb2, nunits, ustart, (int)(n + 1), st);
-    tb = std::max(tb, tb2);
+    tb = std::max(std::max(tb, tb2), tb3);
     void* tmp;
     BBF_CUDA(dmalloc(&tmp, tb + 16, st));
     BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t1, d_nsel, (int)n, IsT1{p->work}, st));
+    BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t2, d_nsel + 1, (int)n, IsT2{p->work, t2max}, st));
     BBF_CUDA(cudaMemsetAsync(nunits + n, 0, 4, st));
     BBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nunits, ustart, (int)(n + 1), st));
-    g->launches += 3;
+    g->launches += 5;
     dfree(tmp, st);
   }
-  uint32_t h_nsel = 0, h_nunits = 0;
-  unsigned long long h_acc[3];
-  BBF_CUDA(cudaMemcpyAsync(&h_nsel, d_nsel, 4, cudaMemcpyDeviceToHost, st));
+  uint32_t h_nsel[2] = {0, 0}, h_nunits = 0;
+  unsigned long long h_acc[4];
+  BBF_CUDA(cudaMemcpyAsync(h_nsel, d_nsel, 8, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaMemcpyAsync(&h_nunits, ustart + n, 4, cudaMemcpyDeviceToHost, st));
-  BBF_CUDA(cudaMemcpyAsync(h_acc, acc, 24, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaMemcpyAsync(h_acc, acc, 32, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaStreamSynchronize(st));
-  p->n_t1 = h_nsel;
+  p->n_t1 = h_nsel[0];
+  p->n_t2 = h_nsel[1];
   p->n_units = h_nunits;
   p->W_t1 = h_acc[0];
   p->W_t3 = h_acc[1];
   p->M_t3 = h_acc[2];
+  p->W_t2 = h_acc[3];
   BBF_CUDA(dmalloc(&p->units, sizeof(Unit) * (h_nunits + 1), st));
   unsigned int* d_maxmid;  // [0] max middles, [2..3] max work (u64)
   BBF_CUDA(dmalloc(&d_maxmid, 16, st));
@@ -324,10 +347,11 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   }
   if (getenv("BBF_DEBUG"))
     fprintf(stderr,
-            "[bbf] plan route=%d W_full=%llu W_pruned=%llu W_t1=%llu (%u starts) W_t3=%llu (%u units) "
+            "[bbf] plan route=%d W_full=%llu W_pruned=%llu W_t1=%llu (%u starts) W_t2=%llu (%u starts) W_t3=%llu (%u units) "
             "M_t3=%llu max_mid=%u w_target=%llu words U=%u V=%u\n",
             route, (unsigned long long)p->W_full, (unsigned long long)p->W_pruned,
-            (unsigned long long)p->W_t1, p->n_t1, (unsigned long long)p->W_t3, p->n_units,
+            (unsigned long long)p->W_t1, p->n_t1, (unsigned long long)p->W_t2, p->n_t2,
+            (unsigned long long)p->W_t3, p->n_units,
             (unsigned long long)p->M_t3, p->max_mid, (unsigned long long)w_target, g->zones[0].WB[5],
             g->zones[1].WB[5]);
   dfree(len, st);
