@@ -258,16 +258,16 @@ template <bool PV, bool PAIRS>
 __device__ __forceinline__ void epi_packed(const EngineArgs& a, const Zones& Z, uint32_t sb, uint32_t x,
                                            uint32_t gw, uint32_t v, unsigned long long& xB,
                                            unsigned long long& xN) {
-  uint32_t h, lbase, hi, lo;  // half-field width, first rank of the word, SWAR masks
-  if (gw < Z.WB[2]) { h = 16; lbase = Z.L[0] + (gw - Z.WB[1]); hi = 0xfffefffeu; lo = 0x00000001u; }
-  else if (gw < Z.WB[3]) { h = 8; lbase = Z.L[1] + 2 * (gw - Z.WB[2]); hi = 0xfefefefeu; lo = 0x00010001u; }
-  else if (gw < Z.WB[4]) { h = 4; lbase = Z.L[2] + 4 * (gw - Z.WB[3]); hi = 0xeeeeeeeeu; lo = 0x01010101u; }
-  else { h = 2; lbase = Z.L[3] + 8 * (gw - Z.WB[4]); hi = 0xaaaaaaaau; lo = 0x11111111u; }
+  uint32_t h, lfw, lbase, hi, lo;  // half-field width, log2 field width, first rank, SWAR masks
+  if (gw < Z.WB[2]) { h = 16; lfw = 5; lbase = Z.L[0] + (gw - Z.WB[1]); hi = 0xfffefffeu; lo = 0x00000001u; }
+  else if (gw < Z.WB[3]) { h = 8; lfw = 4; lbase = Z.L[1] + 2 * (gw - Z.WB[2]); hi = 0xfefefefeu; lo = 0x00010001u; }
+  else if (gw < Z.WB[4]) { h = 4; lfw = 3; lbase = Z.L[2] + 4 * (gw - Z.WB[3]); hi = 0xeeeeeeeeu; lo = 0x01010101u; }
+  else { h = 2; lfw = 2; lbase = Z.L[3] + 8 * (gw - Z.WB[4]); hi = 0xaaaaaaaau; lo = 0x11111111u; }
   uint32_t cm = (v & hi) | (v & (v >> h) & lo);  // non-zero bits only in contributing fields
   const uint32_t fw = 2 * h, fmask = (1u << h) - 1u;
   const uint32_t fclr = (fw == 32) ? 0xffffffffu : ((1u << fw) - 1u);
   while (cm) {
-    const uint32_t f = (uint32_t)(__ffs(cm) - 1) / fw;  // field index
+    const uint32_t f = (uint32_t)(__ffs(cm) - 1) >> lfw;  // field index
     cm &= ~(fclr << (f * fw));
     const uint32_t q = v >> (f * fw);
     const uint32_t A = q & fmask, D = (q >> h) & fmask;
