@@ -954,6 +954,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
   uint32_t* sh_mn = sh_mb + 32;
   __shared__ uint32_t sh_item, sh_c[2];
   __shared__ unsigned long long sh_red[2][kT2Warps];
+  __shared__ uint8_t sh_own2[kT2Warps][32];
   for (uint32_t i = tid; i < 2 * kT2Slots; i += kT2Threads) ((uint32_t*)keys)[i] = 0;
   sh_mb[lane] = 0;
   sh_mn[lane] = 0;
@@ -977,9 +978,9 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
     uint32_t S = 64;
     while (S < 2 * W && S < kT2Slots) S <<= 1;
     const uint32_t mask = S - 1;
-#pragma unroll 1
     // middles spread over all warps: chunks of cs <= 32 middles, chunk ck to warp ck mod warps
     const uint32_t cs = min(32u, max(1u, (m + kT2Warps - 1) / kT2Warps));
+#pragma unroll 1
     for (int pass = 0; pass < (PV ? 2 : 1); ++pass) {
       for (uint32_t ck = warp; ck * cs < m; ck += kT2Warps) {
         const uint32_t cb = ck * cs;
@@ -991,25 +992,32 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
           const uint32_t en = a.end1[ob + (wv & kMask)];
           len = en > s ? en - s : 0;
         }
-        const uint32_t incl = warp_incl_scan(len, lane);
+        const uint32_t incl = warp_incl_scan(len, lane), excl = incl - len;
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         if (tot == 0) continue;
-        sh_incl[lane] = incl;
-        sh_s[lane] = s;
-        sh_wv[lane] = wv;
-        __syncwarp();
-        for (uint32_t t = lane; t < ((tot + 31) & ~31u); t += 32) {
+        // wedges flattened over the lanes; the owner middle of lane L's wedge is the last middle
+        // starting at or before it in this step (start bitmask + owner table), else the carried one
+        int carry = 0;
+        uint32_t accb = 0, accn = 0;  // pass 2: this lane's middle totals (lane = middle)
+        for (uint32_t base = 0; base < tot; base += 32) {
+          const bool st = len > 0 && excl >= base && excl < base + 32;
+          if (st) sh_own2[warp][excl - base] = (uint8_t)lane;
+          const uint32_t smask = __reduce_or_sync(0xffffffffu, st ? 1u << (excl - base) : 0u);
+          __syncwarp();
+          const uint32_t mm = smask & (0xffffffffu >> (31 - lane));
+          const int gs = mm ? 31 - __clz(mm) : 0;
+          const int ow = mm ? (int)sh_own2[warp][gs] : carry;
+          __syncwarp();
+          carry = __shfl_sync(0xffffffffu, ow, 31);
+          const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, ow);
+          const uint32_t o_s = __shfl_sync(0xffffffffu, s, ow);
+          const uint32_t o_wv = __shfl_sync(0xffffffffu, wv, ow);
+          const uint32_t t = base + lane;
+          uint32_t b2 = 0, n2 = 0;
           if (t < tot) {
-            uint32_t lo = 0, hi = 31;  // first j with incl[j] > t
-            while (lo < hi) {
-              const uint32_t md = (lo + hi) >> 1;
-              if (sh_incl[md] > t) hi = md; else lo = md + 1;
-            }
-            const uint32_t j = lo;
-            const uint32_t excl = j ? sh_incl[j - 1] : 0;
-            const uint32_t ev = a.adj[sh_s[j] + (t - excl)];
+            const uint32_t ev = a.adj[o_s + (t - o_excl)];
             const uint32_t l = ev & kMask;
-            const uint32_t cls = (ev ^ sh_wv[j]) >> 31;
+            const uint32_t cls = (ev ^ o_wv) >> 31;
             const uint32_t key = l + 1;
             uint32_t h = hslot(l, mask);
             if (pass == 0) {
@@ -1027,19 +1035,32 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
               while (keys[h] != key) h = (h + 1) & mask;
               const uint32_t v = vals[h];
               const uint32_t ad = v & 0xffffu, dd = v >> 16;
-              const uint32_t b2 = cls ? dd - 1 : ad - 1, n2 = cls ? ad : dd;
-              if (b2) atomicAdd(&sh_mb[j], b2);
-              if (n2) atomicAdd(&sh_mn[j], n2);
+              b2 = cls ? dd - 1 : ad - 1;
+              n2 = cls ? ad : dd;
             }
           }
+          if (pass == 1 && __any_sync(0xffffffffu, (b2 | n2) != 0)) {
+            // per-owner sums by a segmented scan; the owner's last lane in this step hands the
+            // sum to the owner lane through shared memory
+            const uint32_t ib = warp_incl_scan(b2, lane), in = warp_incl_scan(n2, lane);
+            const int src = gs > 0 ? gs - 1 : 0;
+            const uint32_t pb = __shfl_sync(0xffffffffu, ib, src), pn = __shfl_sync(0xffffffffu, in, src);
+            const bool last = t < tot && (t + 1 == tot || lane == 31 || ((smask >> (lane + 1)) & 1u));
+            if (last) {
+              sh_mb[ow] += ib - (gs > 0 ? pb : 0u);
+              sh_mn[ow] += in - (gs > 0 ? pn : 0u);
+            }
+            __syncwarp();
+          }
         }
-        __syncwarp();
         if (pass == 1) {
-          const uint32_t b2 = sh_mb[lane], n2 = sh_mn[lane];
-          if (b2 | n2) {
+          __syncwarp();
+          accb = sh_mb[lane];
+          accn = sh_mn[lane];
+          if (accb | accn) {
             const uint32_t vr = ob + (wv & kMask);
-            if (b2) atomicAdd(&a.pv[2ull * vr], (unsigned long long)b2);
-            if (n2) atomicAdd(&a.pv[2ull * vr + 1], (unsigned long long)n2);
+            if (accb) atomicAdd(&a.pv[2ull * vr], (unsigned long long)accb);
+            if (accn) atomicAdd(&a.pv[2ull * vr + 1], (unsigned long long)accn);
           }
           sh_mb[lane] = 0;
           sh_mn[lane] = 0;
