@@ -276,7 +276,7 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   // tiers and units
   // a T2 start's distinct ends (<= its wedges) must fit the k_t2 hash at load <= 1/2
   const uint64_t t2max = std::min<uint64_t>(
-      getenv("BBF_T2_MAX") ? (uint64_t)atoll(getenv("BBF_T2_MAX")) : kT2MaxDefault, kT2Slots / 2);
+      getenv("BBF_T2_MAX") ? (uint64_t)atoll(getenv("BBF_T2_MAX")) : kT2MaxDefault, kT2Slots * 3 / 4);
   BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
   if (n) {
     k_tier<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, p->work, w_target, t2max, sb, se, nunits, acc);
