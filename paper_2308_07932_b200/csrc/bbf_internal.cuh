@@ -302,7 +302,8 @@ bbf_status run_sparse(bbf_graph* g, Plan* p, bool per_vertex, int rank, int nran
                       unsigned long long* host_BN);
 bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, int rank, int nranks,
                            unsigned long long* host_BN, unsigned long long* cb, unsigned long long* cn,
-                           unsigned long long* cid, unsigned long long cap, unsigned long long* n_cand);
+                           unsigned long long* cid, unsigned long long cap, unsigned long long* n_cand,
+                           unsigned long long tau);
 bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uint32_t* n_out);
 bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks,
                      unsigned long long* host_BN);

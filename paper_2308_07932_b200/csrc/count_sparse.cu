@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
 #include <vector>
 
 #include "bbf_internal.cuh"
@@ -65,6 +66,7 @@ struct EngineArgs {
   uint32_t rec_stride;  // record slots per window: max middles + max unit work / kRecMax
   uint32_t dense_div;   // a window is scanned densely when wedges * dense_div >= its words
   uint32_t bsz;         // records per warp batch (0 = adaptive)
+  unsigned long long tau;  // top-k: only pairs with balanced >= tau are candidates
   // pair candidates (top-k): balanced, unbalanced, (min id << 32 | max id)
   unsigned long long* cb;
   unsigned long long* cn;
@@ -79,6 +81,7 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 
 __device__ __forceinline__ void emit_pair(const EngineArgs& a, uint32_t x, uint32_t wrow,
                                           unsigned long long fb, unsigned long long fn) {
+  if (fb < a.tau) return;  // below the current top-k threshold
   unsigned long long slot = atomicAdd(&a.acc[4], 1ull);
   if (slot < a.cap) {
     unsigned long long ix = a.inv[x], iw = a.inv[wrow];
@@ -1150,7 +1153,7 @@ cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, P
 bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, int rank,
                            int nranks, unsigned long long* host_BN, unsigned long long* cb,
                            unsigned long long* cn, unsigned long long* cid,
-                           unsigned long long cap, unsigned long long* n_cand) {
+                           unsigned long long cap, unsigned long long* n_cand, unsigned long long tau) {
   cudaStream_t st = g->stream;
   // scratch for the hub kernel: per CTA 3 middle arrays + 4 record arrays [window][middle]
   uint32_t kwin_cap = 1;
@@ -1181,7 +1184,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   ea.max_mid = std::max<uint32_t>(p->max_mid, 1);
   ea.kwin_cap = kwin_cap;
   ea.rec_stride = (uint32_t)(std::max<uint32_t>(p->max_mid, 1) + p->max_work / kRecMax + 1);
-  ea.cb = cb; ea.cn = cn; ea.cid = cid; ea.cap = cap;
+  ea.cb = cb; ea.cn = cn; ea.cid = cid; ea.cap = cap; ea.tau = tau;
   ea.dense_div = getenv("BBF_DENSE_DIV") ? (uint32_t)atoi(getenv("BBF_DENSE_DIV")) : 2u;
   ea.bsz = getenv("BBF_T3_BSZ") ? (uint32_t)std::min(32, std::max(0, atoi(getenv("BBF_T3_BSZ")))) : 16u;
   cudaEvent_t e0, e1, e2;
@@ -1240,7 +1243,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
 bbf_status run_sparse(bbf_graph* g, Plan* p, bool per_vertex, int rank, int nranks,
                       unsigned long long* host_BN) {
   return run_sparse_impl(g, p, per_vertex, false, rank, nranks, host_BN, nullptr, nullptr, nullptr,
-                         0, nullptr);
+                         0, nullptr, 1ull);
 }
 
 }  // namespace bbf
@@ -1268,19 +1271,52 @@ bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uin
   cudaStream_t st = g->stream;
   Plan* p = &g->plan_s[side];
   if (!p->valid) BBF_TRY(make_plan(g, 1 + side, p));
+  // Candidates are the pairs with balanced >= tau (reading R11 ranks by balanced count).  tau
+  // starts at 1 (every pair with a balanced butterfly); if the candidates overflow the buffer,
+  // tau is raised to the (4k)-th largest balanced count among the stored ones and the pass is
+  // repeated; if a raised tau leaves fewer than k candidates it is lowered 16x and repeated.
   unsigned long long cap = std::min<unsigned long long>(p->W_pruned + 1024, 1ull << 24);
-  unsigned long long ncand = 0;
+  if (getenv("BBF_TOPK_CAP")) cap = std::max<unsigned long long>(k, strtoull(getenv("BBF_TOPK_CAP"), nullptr, 10));  // test hook
+  unsigned long long ncand = 0, tau = 1;
+  unsigned long long lo = 0, lo_count = 0;  // largest tau seen to overflow the buffer (0: none)
+  unsigned long long hi = 0;                // smallest tau seen to leave fewer than k (0: none)
   unsigned long long *cb = nullptr, *cn = nullptr, *cid = nullptr;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    BBF_CUDA(dmalloc(&cb, 8 * cap, st));
-    BBF_CUDA(dmalloc(&cn, 8 * cap, st));
-    BBF_CUDA(dmalloc(&cid, 8 * cap, st));
+  BBF_CUDA(dmalloc(&cb, 8 * cap, st));
+  BBF_CUDA(dmalloc(&cn, 8 * cap, st));
+  BBF_CUDA(dmalloc(&cid, 8 * cap, st));
+  for (int it = 0;; ++it) {
     unsigned long long BN[2];
-    BBF_TRY(run_sparse_impl(g, p, false, true, 0, 1, BN, cb, cn, cid, cap, &ncand));
-    if (ncand <= cap) break;
-    dfree(cb, st); dfree(cn, st); dfree(cid, st);
-    cap = ncand + 1024;
-    if (attempt == 1) { set_error("top-k candidate buffer overflow"); return BBF_ENOMEM; }
+    BBF_TRY(run_sparse_impl(g, p, false, true, 0, 1, BN, cb, cn, cid, cap, &ncand, tau));
+    if (ncand <= cap && (ncand >= k || tau == 1)) break;  // complete candidate set
+    if (it >= 64) { set_error("top-k threshold search did not converge"); return BBF_ENOMEM; }
+    if (ncand > cap) {
+      lo = tau;
+      lo_count = ncand;
+      // the stored candidates are a subset: their (4k)-th largest balanced count bounds tau
+      std::vector<unsigned long long> hb(cap);
+      BBF_CUDA(cudaMemcpyAsync(hb.data(), cb, 8 * cap, cudaMemcpyDeviceToHost, st));
+      BBF_CUDA(cudaStreamSynchronize(st));
+      const size_t r = std::min<size_t>(cap - 1, 4ull * k);
+      std::nth_element(hb.begin(), hb.begin() + r, hb.end(), std::greater<unsigned long long>());
+      tau = std::max(tau + 1, hb[r]);
+    } else {
+      hi = tau;  // too few candidates at this threshold
+    }
+    if (hi && tau >= hi) tau = lo + (hi - lo) / 2;
+    if (tau <= lo) tau = lo + 1;
+    if (hi && tau >= hi) {
+      // ties: no integer threshold separates "too many" from "too few"; take every candidate at
+      // tau = lo in a buffer of the exact size
+      dfree(cb, st); dfree(cn, st); dfree(cid, st);
+      cap = lo_count;
+      if (cap >= (1ull << 31)) { set_error("top-k: too many tied candidates"); return BBF_ENOMEM; }
+      BBF_CUDA(dmalloc(&cb, 8 * cap, st));
+      BBF_CUDA(dmalloc(&cn, 8 * cap, st));
+      BBF_CUDA(dmalloc(&cid, 8 * cap, st));
+      tau = lo;
+      BBF_TRY(run_sparse_impl(g, p, false, true, 0, 1, BN, cb, cn, cid, cap, &ncand, tau));
+      break;
+    }
   }
   uint32_t take = (uint32_t)std::min<unsigned long long>(k, ncand);
   *n_out = take;

@@ -374,3 +374,16 @@ def test_schedule_independence(bbf, monkeypatch, env):
     assert (got[0]["balanced"], got[0]["unbalanced"]) == (ref[0]["balanced"], ref[0]["unbalanced"])
     for a, b in zip(got[1:], ref[1:]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("cap", ["120", "400", "3000"])
+def test_topk_threshold_search(bbf, monkeypatch, cap):
+    """Top-k pairs when the candidate buffer is smaller than the number of pairs: the threshold
+    search (raise tau from a sample, lower on too few, exact buffer on ties) still returns the
+    oracle's ranking."""
+    g = G.config2()
+    want = O.topk_pairs(g, 100, side=1, threads=THREADS)
+    monkeypatch.setenv("BBF_TOPK_CAP", cap)
+    with bbf.Graph.from_synth(g) as h:
+        assert h.count_pairs_topk(100, side=1) == want
+        assert h.count_pairs_topk(7, side=0) == O.topk_pairs(g, 7, side=0, threads=THREADS)
