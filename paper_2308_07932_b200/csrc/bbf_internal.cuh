@@ -145,12 +145,15 @@ __host__ __device__ inline uint32_t encode_caddr(const Zones& z, uint32_t l) {
 }
 
 // Compact encoding (graphs without 64-bit fields and at most 2^20 counter words per side):
-// bits 0-19 word g, 20-21 width code wc (half-field h = 2 << wc), 22-26 P0, 27-31 P1, where P0 /
-// P1 is the bit of the field to increment when the start->middle edge is positive / negative:
-// the wedge is symmetric (a, at bit sh) iff both edges have the same sign, asymmetric (d, at
-// bit sh + h) otherwise, so the middle->end sign is folded into the two positions.
+// bits 0-1 width code wc (half-field h = 2 << wc), 2-21 word g (so ev & kCpAddrMask is the
+// word's byte offset 4g), 22-26 P0, 27-31 P1, where P0 / P1 is the bit of the field to
+// increment when the start->middle edge is positive / negative: the wedge is symmetric (a, at
+// bit sh) iff both edges have the same sign, asymmetric (d, at bit sh + h) otherwise, so the
+// middle->end sign is folded into the two positions.
 constexpr uint32_t kCpWordBits = 20;
 constexpr uint32_t kCpWordMask = (1u << kCpWordBits) - 1u;
+constexpr uint32_t kCpAddrMask = kCpWordMask << 2;
+__host__ __device__ inline uint32_t cp_word(uint32_t ev) { return (ev >> 2) & kCpWordMask; }
 
 __host__ __device__ inline uint32_t encode_caddr_compact(const Zones& z, uint32_t l, uint32_t neg) {
   uint32_t g = 0, sh = 0, wc = 0;
@@ -160,7 +163,7 @@ __host__ __device__ inline uint32_t encode_caddr_compact(const Zones& z, uint32_
   else if (l < z.L[4]) { uint32_t i = l - z.L[3]; g = z.WB[4] + (i >> 3); sh = (i & 7u) << 2; wc = 0; }
   const uint32_t pa = sh, pd = sh + (2u << wc);
   const uint32_t p0 = neg ? pd : pa, p1 = neg ? pa : pd;
-  return (g & kCpWordMask) | (wc << 20) | (p0 << 22) | (p1 << 27);
+  return ((g & kCpWordMask) << 2) | wc | (p0 << 22) | (p1 << 27);
 }
 
 __host__ __device__ inline unsigned long long comb2(unsigned long long x) {

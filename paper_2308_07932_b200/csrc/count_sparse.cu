@@ -126,7 +126,10 @@ __device__ unsigned long long g_prof_cnt[4];  // nonzero counter words, contribu
 #else
 #define T3_MARK(slot) do {} while (0)
 #endif
-constexpr int kU = 1;  // flattened steps per iteration of the hub kernel's record loop
+#ifndef BBF_T3_KU
+#define BBF_T3_KU 1
+#endif
+constexpr int kU = BBF_T3_KU;  // flattened steps per iteration of the hub kernel's record loop
 #ifndef BBF_T3_CE
 #define BBF_T3_CE 8
 #endif
@@ -231,27 +234,37 @@ __device__ __forceinline__ uint32_t sh_load_if(uint32_t addr, uint32_t on) {
   return r;
 }
 
+// zero-extend the low `len` bits (one SGXT.W)
+__device__ __forceinline__ uint32_t zext(uint32_t t, uint32_t len) {
+  uint32_t r;
+  asm("szext.wrap.u32 %0, %1, %2;" : "=r"(r) : "r"(t), "r"(len));
+  return r;
+}
+// the field at bit (ev >> sh) & 31 of counter word v, h bits wide
+__device__ __forceinline__ uint32_t cp_field(uint32_t v, uint32_t ev, uint32_t sh, uint32_t h) {
+  return zext(v >> ((ev >> sh) & 31u), h);
+}
+
 template <bool BM>
 __device__ __forceinline__ void t3_inc_cp(uint32_t cbase, uint32_t* bm, uint32_t word0, uint32_t ev,
                                           uint32_t shamt) {
-  const uint32_t gw = ev & kCpWordMask;
   const uint32_t inc = 1u << ((ev >> shamt) & 31u);
   if (BM) {
-    const uint32_t prev = sh_atom_add(cbase + 4u * gw, inc);
-    const uint32_t g = gw - word0;
+    const uint32_t prev = sh_atom_add(cbase + (ev & kCpAddrMask), inc);
+    const uint32_t g = cp_word(ev) - word0;
     if (prev == 0) atomicOr(&bm[g >> 5], 1u << (g & 31));
   } else {
-    sh_red_add(cbase + 4u * gw, inc);
+    sh_red_add(cbase + (ev & kCpAddrMask), inc);
   }
 }
 
 // middle share of one wedge: its own class count - 1 balanced, the other class unbalanced
 __device__ __forceinline__ void t3_share_cp(uint32_t cbase, uint32_t ev, uint32_t shamt, uint32_t oshamt,
                                             uint32_t& b, uint32_t& nn) {
-  const uint32_t v = sh_load(cbase + 4u * (ev & kCpWordMask));
-  const uint32_t msk = (1u << (2u << ((ev >> 20) & 3u))) - 1u;
-  b += ((v >> ((ev >> shamt) & 31u)) & msk) - 1u;
-  nn += (v >> ((ev >> oshamt) & 31u)) & msk;
+  const uint32_t v = sh_load(cbase + (ev & kCpAddrMask));
+  const uint32_t h = 2u << (ev & 3u);
+  b += cp_field(v, ev, shamt, h) - 1u;
+  nn += cp_field(v, ev, oshamt, h);
 }
 
 // Lemma 2 on one packed counter word (global word gw >= WB[1]); skipped unless some field has
@@ -319,17 +332,17 @@ __device__ __forceinline__ void t3_chunk(const uint32_t (&ev)[kCE], uint32_t vm,
   if (CP && MODE == 0) {  // pass 1, dense window: branch-free predicated updates
 #pragma unroll
     for (int j = 0; j < (int)kCE; ++j)
-      sh_red_add_if(cbase + 4u * (ev[j] & kCpWordMask), 1u << ((ev[j] >> shamt) & 31u), vm & (1u << j));
+      sh_red_add_if(cbase + (ev[j] & kCpAddrMask), 1u << ((ev[j] >> shamt) & 31u), vm & (1u << j));
     return;
   }
   if (CP && MODE == 2) {  // pass 2: predicated loads; sum of own-class counts minus #entries
     uint32_t own = 0, oth = 0;
 #pragma unroll
     for (int j = 0; j < (int)kCE; ++j) {
-      const uint32_t v = sh_load_if(cbase + 4u * (ev[j] & kCpWordMask), vm & (1u << j));
-      const uint32_t msk = (1u << (2u << ((ev[j] >> 20) & 3u))) - 1u;
-      own += (v >> ((ev[j] >> shamt) & 31u)) & msk;
-      oth += (v >> ((ev[j] >> oshamt) & 31u)) & msk;
+      const uint32_t v = sh_load_if(cbase + (ev[j] & kCpAddrMask), vm & (1u << j));
+      const uint32_t h = 2u << (ev[j] & 3u);
+      own += cp_field(v, ev[j], shamt, h);
+      oth += cp_field(v, ev[j], oshamt, h);
     }
     cb += own - (uint32_t)__popc(vm);
     cn += oth;

@@ -193,23 +193,24 @@ __global__ void k_row_starts(const uint32_t* __restrict__ off, uint32_t n, uint3
 }
 
 // entry e starts a run if it starts its row (flag preset) or its window differs from e-1's
-__global__ void k_run_flags(const uint32_t* __restrict__ adjc, uint64_t m, uint32_t wmask,
+__global__ void k_run_flags(const uint32_t* __restrict__ adjc, uint64_t m, uint32_t wshift, uint32_t wmask,
                             uint32_t* __restrict__ flag) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
        e += (uint64_t)gridDim.x * blockDim.x) {
     if (flag[e]) continue;
-    uint32_t k = (adjc[e] & wmask) / kWin, kp = (adjc[e - 1] & wmask) / kWin;
+    uint32_t k = ((adjc[e] >> wshift) & wmask) / kWin, kp = ((adjc[e - 1] >> wshift) & wmask) / kWin;
     flag[e] = k != kp ? 1u : 0u;
   }
 }
 
 __global__ void k_runs(const uint32_t* __restrict__ adjc, const uint32_t* __restrict__ flag,
-                       uint64_t m, uint32_t wmask, uint32_t* __restrict__ runid, uint2* __restrict__ runs) {
+                       uint64_t m, uint32_t wshift, uint32_t wmask, uint32_t* __restrict__ runid,
+                       uint2* __restrict__ runs) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
        e += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t r = runid[e] - 1u;  // inclusive scan -> 0-based run index
     runid[e] = r;
-    if (flag[e]) runs[r] = make_uint2((uint32_t)e, (adjc[e] & wmask) / kWin);
+    if (flag[e]) runs[r] = make_uint2((uint32_t)e, ((adjc[e] >> wshift) & wmask) / kWin);
   }
 }
 
@@ -568,7 +569,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     }
   g->compact = g->zones[0].L[0] == 0 && g->zones[1].L[0] == 0 && g->zones[0].WB[5] <= kCpWordMask &&
                g->zones[1].WB[5] <= kCpWordMask && !getenv("BBF_NO_COMPACT");  // env: test hook
-  const uint32_t wmask = g->compact ? kCpWordMask : kCWordMask;
+  const uint32_t wmask = g->compact ? kCpWordMask : kCWordMask, wshift = g->compact ? 2u : 0u;
   BBF_CUDA(dmalloc(&g->adjc, 4ull * (m + 32), st));  // padded: 32-B chunk loads
   BBF_CUDA(dmalloc(&g->runid, 4ull * (m + 1), st));
   g->nruns = 0;
@@ -579,7 +580,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     k_caddr<<<grid_for(m, 256), 256, 0, st>>>(g->adj, m, nnz, g->zones[0], g->zones[1], g->compact,
                                             g->adjc);
     k_row_starts<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(g->off, n, flag);
-    k_run_flags<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, m, wmask, flag);
+    k_run_flags<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, m, wshift, wmask, flag);
     size_t ts = 0;
     cub::DeviceScan::InclusiveSum(nullptr, ts, flag, g->runid, (int64_t)m, st);
     void* tmp2;
@@ -588,7 +589,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     BBF_CUDA(cudaMemcpyAsync(&g->nruns, g->runid + (m - 1), 4, cudaMemcpyDeviceToHost, st));
     BBF_CUDA(cudaStreamSynchronize(st));
     BBF_CUDA(dmalloc(&g->runs, sizeof(uint2) * (g->nruns + 1), st));
-    k_runs<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, flag, m, wmask, g->runid, g->runs);
+    k_runs<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, flag, m, wshift, wmask, g->runid, g->runs);
     g->launches += 6;
     dfree(tmp2, st);
     dfree(flag, st);
