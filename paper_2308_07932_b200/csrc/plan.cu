@@ -36,20 +36,11 @@ __device__ __forceinline__ uint32_t upper_bound_col(const uint32_t* __restrict__
   return b;
 }
 
-__device__ __forceinline__ uint32_t row_of_entry(const uint32_t* __restrict__ off, uint32_t n,
-                                                 uint32_t e) {
-  uint32_t lo = 0, hi = n;  // largest x with off[x] <= e
-  while (hi - lo > 1) {
-    uint32_t mid = lo + (hi - lo) / 2;
-    if (off[mid] <= e) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
 // one thread per adjacency entry: if the entry is a middle of its row for this route, compute
 // ub, the pruned segment length (ends of degree >= 2) and the full count (all ends; W_G)
 __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
-                               const uint32_t* __restrict__ adj, const uint32_t* __restrict__ mid,
+                               const uint32_t* __restrict__ adj, const uint32_t* __restrict__ erow,
+                               const uint32_t* __restrict__ mid,
                                const uint32_t* __restrict__ end1, uint64_t m,
                                uint32_t* __restrict__ ub, uint64_t* __restrict__ len,
                                unsigned long long* __restrict__ w_full) {
@@ -57,7 +48,7 @@ __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
   for (uint64_t e64 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e64 < m;
        e64 += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t e = (uint32_t)e64;
-    uint32_t x = row_of_entry(off, rr.n, e);
+    uint32_t x = erow[e];
     uint32_t lo = rr.route == 0 ? mid[x] : off[x];
     uint64_t l_seg = 0;
     if (rr.in_route(x) && e >= lo && e < end1[x]) {
@@ -231,7 +222,7 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
   BBF_CUDA(cudaMemsetAsync(p->work, 0, 8ull * (n + 1), st));
   if (m) {
-    k_plan_entries<<<grid_for(m, 256), 256, 0, st>>>(rr, g->off, g->adj, g->mid, g->end1, m, p->ub,
+    k_plan_entries<<<grid_for(m, 256), 256, 0, st>>>(rr, g->off, g->adj, g->erow, g->mid, g->end1, m, p->ub,
                                                    len, &acc[0]);
     g->launches += 1;
   }
