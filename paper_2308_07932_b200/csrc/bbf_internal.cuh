@@ -221,6 +221,7 @@ struct bbf_graph {
   uint32_t* off;      // n+1
   uint32_t* adj;      // 2*nnz
   uint32_t* erow;     // 2*nnz: row of each entry (plan kernels; no binary search over off)
+  uint32_t* rev;      // 2*nnz: position of the same edge's entry in the other side's row
   uint32_t* mid;      // n   (mid_start)
   uint32_t* end1;     // n
   uint32_t* inv;      // n   : row -> input id on its side

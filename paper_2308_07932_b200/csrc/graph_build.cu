@@ -108,7 +108,9 @@ __device__ __forceinline__ uint32_t row_of_edge(const uint64_t* __restrict__ rp,
 //   B  a stable radix sort by V rank (bits(n_v) bits) groups them into V rows whose entries keep
 //      the U-rank order: the values are the V-side adjacency (l | neg << 31) as is;
 //   C  k_transpose_keys + a stable radix sort by U rank (bits(n_u) bits) gives the U rows with
-//      their entries in V-rank order: the values are the U-side adjacency, the keys its rows.
+//      their entries in V-rank order; its 8-byte values carry the U-side adjacency word and the
+//      V-side position of the same edge, from which k_u_adj writes both directions' reverse
+//      positions (rev: the plan's upper bound of a start in its middle's row is rev + 1).
 // Two sorts of 4+4-byte items over ~bits(n_side) bits replace one sort of 8-byte keys over
 // bits(n) + bits(n_side) + 1 bits (half the radix traffic).
 __global__ void k_entries(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ col,
@@ -127,16 +129,31 @@ __global__ void k_entries(const uint64_t* __restrict__ rp, const uint32_t* __res
   }
 }
 
-// after B: V-side rows (erow), and the inputs of C (key = U rank, value = V rank | neg)
+// after B: V-side rows (erow), and the inputs of C (key = U rank, value = the U-side adjacency
+// word (V rank | neg) << 32 | the V-side position)
 __global__ void k_transpose_keys(const uint32_t* __restrict__ vkey, const uint32_t* __restrict__ vadj,
                                  uint64_t nnz, uint32_t n_u, uint32_t* __restrict__ verow,
-                                 uint32_t* __restrict__ key, uint32_t* __restrict__ val) {
+                                 uint32_t* __restrict__ key, uint64_t* __restrict__ val) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nnz;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t l = vkey[i], w = vadj[i];
     verow[i] = n_u + l;
     key[i] = w & kMask;
-    val[i] = l | (w & kNegBit);
+    val[i] = ((uint64_t)(l | (w & kNegBit)) << 32) | (uint64_t)i;
+  }
+}
+
+// after C: U entry i -> its adjacency word and the reverse positions of both entries of the
+// edge (absolute indices into adj)
+__global__ void k_u_adj(const uint64_t* __restrict__ val, uint64_t nnz, uint32_t* __restrict__ adj,
+                        uint32_t* __restrict__ rev) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = val[i];
+    const uint64_t r = nnz + (uint32_t)v;
+    adj[i] = (uint32_t)(v >> 32);
+    rev[i] = (uint32_t)r;
+    rev[r] = (uint32_t)i;
   }
 }
 
@@ -564,8 +581,12 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
   BBF_CUDA(cudaMemsetAsync(d_err, 0, 4 * sizeof(uint32_t), st));
   size_t t3 = 0, t5 = 0;
   const int bits_u = bits_for(std::max<uint32_t>(n_u, 1)), bits_v = bits_for(std::max<uint32_t>(n_v, 1));
+  size_t t3b = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, t3, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
                                   (uint32_t*)nullptr, (int)nnz, 0, std::max(bits_u, bits_v), st);
+  cub::DeviceRadixSort::SortPairs(nullptr, t3b, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint64_t*)nullptr,
+                                  (uint64_t*)nullptr, (int)nnz, 0, std::max(bits_u, bits_v), st);
+  t3 = std::max(t3, t3b);
   cub::DeviceScan::InclusiveSum(nullptr, t5, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n, st);
   void* tmp;
   BBF_CUDA(dmalloc(&tmp, std::max(t3, t5) + 16, st));
@@ -573,21 +594,28 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
   BBF_CUDA(dmalloc(&g->end1, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&g->adj, 4ull * (m + 1), st));
   BBF_CUDA(dmalloc(&g->erow, 4ull * (m + 1), st));
+  BBF_CUDA(dmalloc(&g->rev, 4ull * (m + 1), st));
   BBF_CUDA(dmalloc(&g->degpre, 8ull * (n + 1), st));
   if (m) {
     uint32_t *ka, *va, *kb;
+    uint64_t *wa, *wb;
     BBF_CUDA(dmalloc(&ka, 4ull * nnz, st));
     BBF_CUDA(dmalloc(&va, 4ull * nnz, st));
     BBF_CUDA(dmalloc(&kb, 4ull * nnz, st));
+    BBF_CUDA(dmalloc(&wa, 8ull * nnz, st));
+    BBF_CUDA(dmalloc(&wb, 8ull * nnz, st));
     k_entries<<<grid_for(nnz, 256), 256, 0, st>>>(d_rp, d_col, d_sg, nnz, n_u, lr_u, lr_v, g->off, ka, va);
     BBF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t3, ka, kb, va, g->adj + nnz, (int)nnz, 0, bits_v, st));
-    k_transpose_keys<<<grid_for(nnz, 256), 256, 0, st>>>(kb, g->adj + nnz, nnz, n_u, g->erow + nnz, ka, va);
-    BBF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t3, ka, g->erow, va, g->adj, (int)nnz, 0, bits_u, st));
+    k_transpose_keys<<<grid_for(nnz, 256), 256, 0, st>>>(kb, g->adj + nnz, nnz, n_u, g->erow + nnz, ka, wa);
+    BBF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t3, ka, g->erow, wa, wb, (int)nnz, 0, bits_u, st));
+    k_u_adj<<<grid_for(nnz, 256), 256, 0, st>>>(wb, nnz, g->adj, g->rev);
     k_dup_check<<<grid_for(nnz, 256), 256, 0, st>>>(g->erow, g->adj, nnz, d_err);
-    g->launches += 9;
+    g->launches += 10;
     dfree(ka, st);
     dfree(va, st);
     dfree(kb, st);
+    dfree(wa, st);
+    dfree(wb, st);
   }
   uint32_t h_err = 0;
   BBF_CUDA(cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, st));

@@ -27,19 +27,11 @@ struct RouteRows {
   }
 };
 
-__device__ __forceinline__ uint32_t upper_bound_col(const uint32_t* __restrict__ adj, uint32_t b,
-                                                    uint32_t e, uint32_t t) {
-  while (b < e) {
-    uint32_t mid = b + (e - b) / 2;
-    if ((adj[mid] & kMask) <= t) b = mid + 1; else e = mid;
-  }
-  return b;
-}
-
 // one thread per adjacency entry: if the entry is a middle of its row for this route, compute
 // ub, the pruned segment length (ends of degree >= 2) and the full count (all ends; W_G)
 __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
-                               const uint32_t* __restrict__ adj, const uint32_t* __restrict__ erow,
+                               const uint32_t* __restrict__ adj, const uint32_t* __restrict__ rev,
+                               const uint32_t* __restrict__ erow,
                                const uint32_t* __restrict__ mid,
                                const uint32_t* __restrict__ end1, uint64_t m,
                                uint32_t* __restrict__ ub, uint64_t* __restrict__ len,
@@ -52,11 +44,10 @@ __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
     uint32_t lo = rr.route == 0 ? mid[x] : off[x];
     uint64_t l_seg = 0;
     if (rr.in_route(x) && e >= lo && e < end1[x]) {
-      uint32_t sb = x < rr.n_u ? 0 : rr.n_u, ob = x < rr.n_u ? rr.n_u : 0;
-      uint32_t lx = x - sb;
+      uint32_t ob = x < rr.n_u ? rr.n_u : 0;
       uint32_t rv = ob + (adj[e] & kMask);
-      uint32_t b = off[rv], f = off[rv + 1];
-      uint32_t u = upper_bound_col(adj, b, f, lx);
+      uint32_t f = off[rv + 1];
+      uint32_t u = rev[e] + 1;  // x's entry in its middle's row is the reverse entry
       uint32_t en = end1[rv];
       ub[e] = u;
       full += f - u;
@@ -222,7 +213,7 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
   BBF_CUDA(cudaMemsetAsync(p->work, 0, 8ull * (n + 1), st));
   if (m) {
-    k_plan_entries<<<grid_for(m, 256), 256, 0, st>>>(rr, g->off, g->adj, g->erow, g->mid, g->end1, m, p->ub,
+    k_plan_entries<<<grid_for(m, 256), 256, 0, st>>>(rr, g->off, g->adj, g->rev, g->erow, g->mid, g->end1, m, p->ub,
                                                    len, &acc[0]);
     g->launches += 1;
   }
