@@ -109,6 +109,12 @@ constexpr uint32_t kRecMax = 1024;
 #ifdef BBF_T3_PROF
 __device__ unsigned long long g_prof_cnt[4];  // nonzero counter words, contributing fields
 #define T3_COUNT(i, v) atomicAdd(&g_prof_cnt[i], (unsigned long long)(v))
+__device__ unsigned long long g_prof_t[3] = {~0ull, ~0ull, 0ull};  // min CTA start, min CTA end, max CTA end (globaltimer ns)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 #else
 #define T3_COUNT(i, v) do {} while (0)
 #endif
@@ -410,6 +416,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
   __shared__ unsigned long long sh_prof[8];  // pre-scan, window setup, pass 1, pass 2, epilogue, unit tail, small-window passes
   long long t_prof = clock64();
   if (threadIdx.x < 8) sh_prof[threadIdx.x] = 0;
+  if (threadIdx.x == 0) atomicMin(&g_prof_t[0], gtimer());
 #endif
   if (threadIdx.x < 4) sh_dbg[threadIdx.x] = 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -791,6 +798,9 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
 #ifdef BBF_T3_PROF
   if (tid == 0) {
     for (int i = 0; i < 5; ++i) atomicAdd(&a.acc[11 + i], sh_prof[i]);
+    const unsigned long long t_end = gtimer();
+    atomicMin(&g_prof_t[1], t_end);
+    atomicMax(&g_prof_t[2], t_end);
   }
 #endif
   if (tid == 0) {
@@ -1243,6 +1253,12 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     const double clk = 1.965e6 * g->num_sms * kT3Ctas;  // cycles per ms summed over CTAs
     fprintf(stderr, "[bbf] t3 phases (ms of CTA time): prescan %.2f setup %.2f pass1 %.2f pass2 %.2f epi %.2f\n",
             h[11] / clk, h[12] / clk, h[13] / clk, h[14] / clk, h[15] / clk);
+    unsigned long long t[3];
+    cudaMemcpyFromSymbol(t, g_prof_t, sizeof(t));
+    fprintf(stderr, "[bbf] t3 CTA ends: first %.3f ms, last %.3f ms after the first start\n", (t[1] - t[0]) * 1e-6,
+            (t[2] - t[0]) * 1e-6);
+    const unsigned long long init[3] = {~0ull, ~0ull, 0ull};
+    cudaMemcpyToSymbol(g_prof_t, init, sizeof(init));
   }
 #endif
   // algorithmic bytes of the hub kernel k_t3: 4 B column word per

@@ -598,26 +598,65 @@ __global__ void k_dense_fill(const uint32_t* __restrict__ off, const uint32_t* _
   }
 }
 
-// A and S of both sides straight from the input U-side CSR (input ids -> local ranks)
-__global__ void k_dense_fill_input(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ col,
-                                   const uint8_t* __restrict__ sg, uint64_t nnz, uint32_t n_u,
-                                   const uint32_t* __restrict__ lr, uint8_t* __restrict__ Au,
-                                   uint8_t* __restrict__ Su, uint64_t ku, uint8_t* __restrict__ Av,
-                                   uint8_t* __restrict__ Sv, uint64_t kv) {
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t lo = 0, hi = n_u;  // row: largest u with rp[u] <= e
-    while (hi - lo > 1) {
-      const uint32_t md = lo + (hi - lo) / 2;
-      if (rp[md] <= e) lo = md; else hi = md;
-    }
-    const uint64_t ru = lr[lo], rv = lr[n_u + col[e]];
-    const uint8_t s = sg[e] ? (uint8_t)1 : (uint8_t)0xFF;  // weight 1 = +1, 0 = -1
-    Au[ru * ku + rv] = 1;
-    Su[ru * ku + rv] = s;
-    Av[rv * kv + ru] = 1;
-    Sv[rv * kv + ru] = s;
+// A_U and S_U straight from the input U-side CSR, one CTA per rank row: the row is assembled in
+// shared memory (A = 1, S = +1 / -1 per edge; weight 1 = +1, 0 = -1) and
+// written out with 16-byte stores, so the operands need no memset and no scattered byte stores
+__global__ void k_dense_rows(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                             const uint8_t* __restrict__ sg, uint32_t n_u, const uint32_t* __restrict__ inv,
+                             const uint32_t* __restrict__ lr_v, uint8_t* __restrict__ Au,
+                             uint8_t* __restrict__ Su, uint32_t ku) {
+  extern __shared__ uint4 rowbuf[];
+  uint8_t* ba = reinterpret_cast<uint8_t*>(rowbuf);
+  uint8_t* bs = ba + ku;
+  const uint32_t r = blockIdx.x, n16 = ku / 16;
+  uint4* a4 = reinterpret_cast<uint4*>(Au + (uint64_t)r * ku);
+  uint4* s4 = reinterpret_cast<uint4*>(Su + (uint64_t)r * ku);
+  if (r >= n_u) {  // padding rows
+    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) { a4[i] = make_uint4(0u, 0u, 0u, 0u); s4[i] = a4[i]; }
+    return;
   }
+  for (uint32_t i = threadIdx.x; i < 2 * n16; i += blockDim.x) rowbuf[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  const uint32_t u = inv[r];
+  for (uint64_t e = rp[u] + threadIdx.x; e < rp[u + 1]; e += blockDim.x) {
+    const uint32_t c = lr_v[col[e]];
+    ba[c] = 1;
+    bs[c] = sg[e] ? (uint8_t)1 : (uint8_t)0xFF;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) { a4[i] = rowbuf[i]; s4[i] = rowbuf[n16 + i]; }
+}
+
+// Av = Au^T and Sv = Su^T (64 x 64 byte tiles through shared memory).  Av is rv x kv with
+// rv >= n_v, kv >= n_u; rows of Av at or beyond ku (the width of Au) are zero.
+__global__ void k_dense_transpose(const uint8_t* __restrict__ Au, const uint8_t* __restrict__ Su, uint32_t ku,
+                                  uint8_t* __restrict__ Av, uint8_t* __restrict__ Sv, uint32_t kv) {
+  __shared__ uint8_t ta[64][64 + 4], ts[64][64 + 4];
+  const uint32_t r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;  // tile of Av: rows r0.., cols c0..
+  const uint32_t t = threadIdx.x, lr = t >> 2, lc = (t & 3) * 16;
+  uint4 qa = make_uint4(0u, 0u, 0u, 0u), qs = qa;
+  if (r0 < ku) {  // source: Au rows c0 + lr, columns r0 + lc .. + 16
+    const uint64_t src = (uint64_t)(c0 + lr) * ku + r0 + lc;
+    qa = *reinterpret_cast<const uint4*>(Au + src);
+    qs = *reinterpret_cast<const uint4*>(Su + src);
+  }
+  const uint32_t wa[4] = {qa.x, qa.y, qa.z, qa.w}, ws[4] = {qs.x, qs.y, qs.z, qs.w};
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    ta[lr][lc + b] = (uint8_t)(wa[b >> 2] >> (8 * (b & 3)));
+    ts[lr][lc + b] = (uint8_t)(ws[b >> 2] >> (8 * (b & 3)));
+  }
+  __syncthreads();
+  // destination row r0 + lr, columns c0 + lc .. + 16  <-  tile column lr, tile rows lc ..
+  uint32_t oa[4] = {0u, 0u, 0u, 0u}, os[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    oa[b >> 2] |= (uint32_t)ta[lc + b][lr] << (8 * (b & 3));
+    os[b >> 2] |= (uint32_t)ts[lc + b][lr] << (8 * (b & 3));
+  }
+  const uint64_t dst = (uint64_t)(r0 + lr) * kv + c0 + lc;
+  *reinterpret_cast<uint4*>(Av + dst) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+  *reinterpret_cast<uint4*>(Sv + dst) = make_uint4(os[0], os[1], os[2], os[3]);
 }
 
 // number of nonzero bytes (duplicate check: a duplicate (u,v) writes one cell twice)
@@ -698,7 +737,7 @@ bool dense_preferred(bbf_graph* g, bool per_vertex) {
   return t_dense < t_sparse;
 }
 
-bbf_status alloc_dense_operands(bbf_graph* g) {
+bbf_status alloc_dense_operands(bbf_graph* g, bool zero) {
   cudaStream_t st = g->stream;
   g->drows[0] = round_up(std::max<uint32_t>(g->n_u, 1), kBN);
   g->drows[1] = round_up(std::max<uint32_t>(g->n_v, 1), kBN);
@@ -708,8 +747,10 @@ bbf_status alloc_dense_operands(bbf_graph* g) {
     const uint64_t bytes = g->drows[s2] * g->dk[s2];
     BBF_CUDA(dmalloc(&g->dA[s2], bytes, st));
     BBF_CUDA(dmalloc(&g->dS[s2], bytes, st));
-    BBF_CUDA(cudaMemsetAsync(g->dA[s2], 0, bytes, st));
-    BBF_CUDA(cudaMemsetAsync(g->dS[s2], 0, bytes, st));
+    if (zero) {
+      BBF_CUDA(cudaMemsetAsync(g->dA[s2], 0, bytes, st));
+      BBF_CUDA(cudaMemsetAsync(g->dS[s2], 0, bytes, st));
+    }
   }
   return BBF_OK;
 }
@@ -719,11 +760,19 @@ bbf_status alloc_dense_operands(bbf_graph* g) {
 bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col,
                                 const uint8_t* d_sg) {
   cudaStream_t st = g->stream;
-  BBF_TRY(alloc_dense_operands(g));
+  BBF_TRY(alloc_dense_operands(g, false));
+  {
+    const uint32_t ku = (uint32_t)g->dk[0], kv = (uint32_t)g->dk[1];
+    const int smem = 2 * (int)ku;
+    if (smem > 48 * 1024)
+      BBF_CUDA(cudaFuncSetAttribute(k_dense_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_dense_rows<<<(unsigned)g->drows[0], 256, smem, st>>>(d_rp, d_col, d_sg, g->n_u, g->inv, g->lr + g->n_u,
+                                                          g->dA[0], g->dS[0], ku);
+    k_dense_transpose<<<dim3(kv / 64, (unsigned)(g->drows[1] / 64)), 256, 0, st>>>(g->dA[0], g->dS[0], ku,
+                                                                                g->dA[1], g->dS[1], kv);
+    g->launches += 2;
+  }
   if (g->nnz) {
-    unsigned grid = (unsigned)std::min<uint64_t>((g->nnz + 255) / 256, 148u * 64u);
-    k_dense_fill_input<<<grid, 256, 0, st>>>(d_rp, d_col, d_sg, g->nnz, g->n_u, g->lr, g->dA[0], g->dS[0],
-                                             g->dk[0], g->dA[1], g->dS[1], g->dk[1]);
     unsigned long long* d_nz;
     BBF_CUDA(dmalloc(&d_nz, 8, st));
     BBF_CUDA(cudaMemsetAsync(d_nz, 0, 8, st));
@@ -760,7 +809,7 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
       BBF_TRY(build_dense_operands(g, g->in_rp, g->in_col, g->in_sg));
     } else {
       BBF_TRY(ensure_adj(g));
-      BBF_TRY(alloc_dense_operands(g));
+      BBF_TRY(alloc_dense_operands(g, true));
       const uint64_t m = 2 * g->nnz;
       if (m) {
         unsigned grid = (unsigned)std::min<uint64_t>((m + 255) / 256, 148u * 64u);

@@ -316,14 +316,23 @@ __global__ void k_pos_compact(uint64_t nnz, const uint32_t* __restrict__ keep, c
 // middle v, the eligible starts are its m_v neighbours of higher priority, and the k-th of them
 // (k = 0.. in priority order) sees deg(v) - 1 - k eligible ends, so v contributes
 // m_v (deg v - 1) - m_v (m_v - 1) / 2.  (Cross-checked against the plan's per-entry count.)
-__global__ void k_wg_m(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ col, uint64_t nnz,
-                       uint32_t n_u, const uint64_t* __restrict__ key_u, const uint64_t* __restrict__ key_v,
+// one warp per U row: the row's own count (eligible starts v of middle u) is a warp sum written
+// once; middle v's counter gets an atomic per eligible start u (consecutive edges of a row share
+// u, so per-edge atomics on mcnt[u] would serialise inside the warp)
+__global__ void k_wg_m(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ col, uint32_t n_u,
+                       const uint64_t* __restrict__ key_u, const uint64_t* __restrict__ key_v,
                        uint32_t* __restrict__ mcnt) {
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t u = row_of_edge(rp, n_u, e), v = col[e];
-    if (key_u[u] > key_v[v]) atomicAdd(&mcnt[n_u + v], 1u);  // u is an eligible start for middle v
-    else atomicAdd(&mcnt[u], 1u);
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n_u; u += (gridDim.x * blockDim.x) >> 5) {
+    const uint64_t ku = key_u[u];
+    uint32_t c = 0;
+    for (uint64_t e = rp[u] + lane; e < rp[u + 1]; e += 32) {
+      const uint32_t v = col[e];
+      if (ku > key_v[v]) atomicAdd(&mcnt[n_u + v], 1u);  // u is an eligible start for middle v
+      else ++c;
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) mcnt[u] = c;
   }
 }
 
@@ -517,7 +526,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     BBF_CUDA(dmalloc(&d_wg, 8, st));
     BBF_CUDA(cudaMemsetAsync(mcnt, 0, 4ull * (n + 1), st));
     BBF_CUDA(cudaMemsetAsync(d_wg, 0, 8, st));
-    if (nnz) k_wg_m<<<grid_for(nnz, 256), 256, 0, st>>>(d_rp, d_col, nnz, n_u, key_u, key_v, mcnt);
+    if (n_u) k_wg_m<<<grid_for(32ull * n_u, 256), 256, 0, st>>>(d_rp, d_col, n_u, key_u, key_v, mcnt);
     if (n) k_wg_sum<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(mcnt, key_u, key_v, n_u, n, d_wg);
     g->launches += 2;
     unsigned long long wg = 0;
