@@ -604,7 +604,7 @@ __global__ void k_dense_fill(const uint32_t* __restrict__ off, const uint32_t* _
 __global__ void k_dense_rows(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ col,
                              const uint8_t* __restrict__ sg, uint32_t n_u, const uint32_t* __restrict__ inv,
                              const uint32_t* __restrict__ lr_v, uint8_t* __restrict__ Au,
-                             uint8_t* __restrict__ Su, uint32_t ku) {
+                             uint8_t* __restrict__ Su, uint32_t ku, unsigned long long* __restrict__ nz) {
   extern __shared__ uint4 rowbuf[];
   uint8_t* ba = reinterpret_cast<uint8_t*>(rowbuf);
   uint8_t* bs = ba + ku;
@@ -624,55 +624,55 @@ __global__ void k_dense_rows(const uint64_t* __restrict__ rp, const uint32_t* __
     bs[c] = sg[e] ? (uint8_t)1 : (uint8_t)0xFF;
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) { a4[i] = rowbuf[i]; s4[i] = rowbuf[n16 + i]; }
+  uint32_t ones = 0;  // bytes are 0 / 1: a duplicate (u,v) sets one cell twice (count < nnz)
+  for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
+    const uint4 q = rowbuf[i];
+    ones += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+    a4[i] = q;
+    s4[i] = rowbuf[n16 + i];
+  }
+  ones = __reduce_add_sync(0xffffffffu, ones);
+  if ((threadIdx.x & 31) == 0 && ones) atomicAdd(nz, (unsigned long long)ones);
 }
 
-// Av = Au^T and Sv = Su^T (64 x 64 byte tiles through shared memory).  Av is rv x kv with
-// rv >= n_v, kv >= n_u; rows of Av at or beyond ku (the width of Au) are zero.
-__global__ void k_dense_transpose(const uint8_t* __restrict__ Au, const uint8_t* __restrict__ Su, uint32_t ku,
-                                  uint8_t* __restrict__ Av, uint8_t* __restrict__ Sv, uint32_t kv) {
-  __shared__ uint8_t ta[64][64 + 4], ts[64][64 + 4];
+// Av = Au^T and Sv = Su^T, 64 x 64 byte tiles: each thread loads a 4 x 4 byte block (four 4-byte
+// row pieces), transposes it in registers (__byte_perm) and stages the words in shared memory so
+// that the stores are 16-byte row pieces.  Av is rv x kv with rv >= n_v, kv >= n_u; rows of Av
+// at or beyond ku (the width of Au) are zero.
+__device__ __forceinline__ void transpose4x4(uint32_t (&w)[4]) {
+  const uint32_t t0 = __byte_perm(w[0], w[1], 0x5140), t1 = __byte_perm(w[2], w[3], 0x5140);
+  const uint32_t t2 = __byte_perm(w[0], w[1], 0x7362), t3 = __byte_perm(w[2], w[3], 0x7362);
+  w[0] = __byte_perm(t0, t1, 0x5410);
+  w[1] = __byte_perm(t0, t1, 0x7632);
+  w[2] = __byte_perm(t2, t3, 0x5410);
+  w[3] = __byte_perm(t2, t3, 0x7632);
+}
+
+__global__ void __launch_bounds__(256) k_dense_transpose(const uint8_t* __restrict__ Au,
+                                                         const uint8_t* __restrict__ Su, uint32_t ku,
+                                                         uint8_t* __restrict__ Av, uint8_t* __restrict__ Sv,
+                                                         uint32_t kv) {
+  __shared__ uint32_t ta[64][17], ts[64][17];
   const uint32_t r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;  // tile of Av: rows r0.., cols c0..
-  const uint32_t t = threadIdx.x, lr = t >> 2, lc = (t & 3) * 16;
-  uint4 qa = make_uint4(0u, 0u, 0u, 0u), qs = qa;
-  if (r0 < ku) {  // source: Au rows c0 + lr, columns r0 + lc .. + 16
-    const uint64_t src = (uint64_t)(c0 + lr) * ku + r0 + lc;
-    qa = *reinterpret_cast<const uint4*>(Au + src);
-    qs = *reinterpret_cast<const uint4*>(Su + src);
-  }
-  const uint32_t wa[4] = {qa.x, qa.y, qa.z, qa.w}, ws[4] = {qs.x, qs.y, qs.z, qs.w};
-#pragma unroll
-  for (int b = 0; b < 16; ++b) {
-    ta[lr][lc + b] = (uint8_t)(wa[b >> 2] >> (8 * (b & 3)));
-    ts[lr][lc + b] = (uint8_t)(ws[b >> 2] >> (8 * (b & 3)));
-  }
-  __syncthreads();
-  // destination row r0 + lr, columns c0 + lc .. + 16  <-  tile column lr, tile rows lc ..
-  uint32_t oa[4] = {0u, 0u, 0u, 0u}, os[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-  for (int b = 0; b < 16; ++b) {
-    oa[b >> 2] |= (uint32_t)ta[lc + b][lr] << (8 * (b & 3));
-    os[b >> 2] |= (uint32_t)ts[lc + b][lr] << (8 * (b & 3));
-  }
-  const uint64_t dst = (uint64_t)(r0 + lr) * kv + c0 + lc;
-  *reinterpret_cast<uint4*>(Av + dst) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
-  *reinterpret_cast<uint4*>(Sv + dst) = make_uint4(os[0], os[1], os[2], os[3]);
-}
-
-// number of nonzero bytes (duplicate check: a duplicate (u,v) writes one cell twice)
-__global__ void k_count_nz(const uint4* __restrict__ a, uint64_t n16, unsigned long long* out) {
-  unsigned long long c = 0;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint4 q = a[i];
-    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+  const uint32_t t = threadIdx.x, bi = t >> 4, bj = t & 15;   // source rows c0 + 4 bi.., bytes r0 + 4 bj..
+  uint32_t wa[4] = {0u, 0u, 0u, 0u}, ws[4] = {0u, 0u, 0u, 0u};
+  if (r0 < ku) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t x = w[k];  // bytes are 0 or 1
-      c += __popc(x);
+      const uint64_t src = (uint64_t)(c0 + 4 * bi + k) * ku + r0 + 4 * bj;
+      wa[k] = *reinterpret_cast<const uint32_t*>(Au + src);
+      ws[k] = *reinterpret_cast<const uint32_t*>(Su + src);
     }
   }
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+  transpose4x4(wa);
+  transpose4x4(ws);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) { ta[4 * bj + k][bi] = wa[k]; ts[4 * bj + k][bi] = ws[k]; }
+  __syncthreads();
+  const uint32_t orow = t >> 2, oq = (t & 3) * 4;  // destination row r0 + orow, words oq .. oq + 3
+  const uint64_t dst = (uint64_t)(r0 + orow) * kv + c0 + 4 * oq;
+  *reinterpret_cast<uint4*>(Av + dst) = make_uint4(ta[orow][oq], ta[orow][oq + 1], ta[orow][oq + 2], ta[orow][oq + 3]);
+  *reinterpret_cast<uint4*>(Sv + dst) = make_uint4(ts[orow][oq], ts[orow][oq + 1], ts[orow][oq + 2], ts[orow][oq + 3]);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -761,24 +761,21 @@ bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32
                                 const uint8_t* d_sg) {
   cudaStream_t st = g->stream;
   BBF_TRY(alloc_dense_operands(g, false));
+  unsigned long long* d_nz;
+  BBF_CUDA(dmalloc(&d_nz, 8, st));
+  BBF_CUDA(cudaMemsetAsync(d_nz, 0, 8, st));
   {
     const uint32_t ku = (uint32_t)g->dk[0], kv = (uint32_t)g->dk[1];
     const int smem = 2 * (int)ku;
     if (smem > 48 * 1024)
       BBF_CUDA(cudaFuncSetAttribute(k_dense_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     k_dense_rows<<<(unsigned)g->drows[0], 256, smem, st>>>(d_rp, d_col, d_sg, g->n_u, g->inv, g->lr + g->n_u,
-                                                          g->dA[0], g->dS[0], ku);
+                                                          g->dA[0], g->dS[0], ku, d_nz);
     k_dense_transpose<<<dim3(kv / 64, (unsigned)(g->drows[1] / 64)), 256, 0, st>>>(g->dA[0], g->dS[0], ku,
                                                                                 g->dA[1], g->dS[1], kv);
     g->launches += 2;
   }
-  if (g->nnz) {
-    unsigned long long* d_nz;
-    BBF_CUDA(dmalloc(&d_nz, 8, st));
-    BBF_CUDA(cudaMemsetAsync(d_nz, 0, 8, st));
-    const uint64_t n16 = g->drows[0] * g->dk[0] / 16;  // k padded to 128: whole uint4s
-    k_count_nz<<<148 * 8, 256, 0, st>>>(reinterpret_cast<const uint4*>(g->dA[0]), n16, d_nz);
-    g->launches += 2;
+  {
     unsigned long long nz = 0;
     BBF_CUDA(cudaMemcpyAsync(&nz, d_nz, 8, cudaMemcpyDeviceToHost, st));
     BBF_CUDA(cudaStreamSynchronize(st));
