@@ -52,9 +52,10 @@ struct EngineArgs {
   const uint64_t* work;
   const uint32_t* inv;
   const uint32_t* t1;
-  const uint32_t* t2;
+  const uint32_t* t2;    // the T2 starts of one k_t2 instance
   const Unit* units;
   uint32_t n_t1, n_t2, n_units;
+  uint32_t t2ctr;        // acc index of that instance's start cursor
   uint32_t n_u, n;
   Zones z[2];
   int rank, nranks;
@@ -963,17 +964,19 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
 // (end rank + 1 -> a | d << 16) with S = pow2 >= 2 * work slots, so a start is done in one sweep
 // of its wedges (no counter windows, no records).  Warps take chunks of 32 middles; inside a
 // chunk the wedges are spread over the lanes as in k_t1.  a + d <= #middles <= work < 2^16.
-constexpr int kT2Threads = 512;
-constexpr int kT2Warps = kT2Threads / 32;
+// Two instances: <512 threads, kT2Slots> for starts above kT2SmallMax wedges (3 CTAs per SM) and
+// <256, kT2Slots / 2> for the rest (6 per SM): a start is latency-bound, so more starts in flight
+// per SM is what raises throughput.
 constexpr uint32_t kT2Per = 5 * 32;  // per-warp scratch words
 
-template <bool PV, bool PAIRS>
+template <bool PV, bool PAIRS, int kT2Threads, int kSlots>
 __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
+  constexpr int kT2Warps = kT2Threads / 32;
   extern __shared__ uint32_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   volatile uint32_t* keys = smem;
-  uint32_t* vals = smem + kT2Slots;
-  uint32_t* sh_incl = vals + kT2Slots + warp * kT2Per;
+  uint32_t* vals = smem + kSlots;
+  uint32_t* sh_incl = vals + kSlots + warp * kT2Per;
   uint32_t* sh_s = sh_incl + 32;
   uint32_t* sh_wv = sh_s + 32;
   uint32_t* sh_mb = sh_wv + 32;
@@ -981,14 +984,14 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
   __shared__ uint32_t sh_item, sh_c[2];
   __shared__ unsigned long long sh_red[2][kT2Warps];
   __shared__ uint8_t sh_own2[kT2Warps][32];
-  for (uint32_t i = tid; i < 2 * kT2Slots; i += kT2Threads) ((uint32_t*)keys)[i] = 0;
+  for (uint32_t i = tid; i < 2 * kSlots; i += kT2Threads) ((uint32_t*)keys)[i] = 0;
   sh_mb[lane] = 0;
   sh_mn[lane] = 0;
   unsigned long long totB = 0, totN = 0;
   __syncthreads();
   while (true) {
     if (tid == 0) {
-      sh_item = (uint32_t)atomicAdd(&a.acc[16], 1ull);
+      sh_item = (uint32_t)atomicAdd(&a.acc[a.t2ctr], 1ull);
       sh_c[0] = 0;
       sh_c[1] = 0;
     }
@@ -1002,7 +1005,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
     const uint32_t m = a.end1[x] - m_lo;
     const uint32_t W = (uint32_t)a.work[x];
     uint32_t S = 64;
-    while (S < 2 * W && S < kT2Slots) S <<= 1;
+    while (S < 2 * W && S < kSlots) S <<= 1;
     const uint32_t mask = S - 1;
     // middles spread over all warps: chunks of cs <= 32 middles, chunk ck to warp ck mod warps
     const uint32_t cs = min(32u, max(1u, (m + kT2Warps - 1) / kT2Warps));
@@ -1161,10 +1164,21 @@ cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, P
     g->launches++;
   }
   if (p->n_t2) {
-    const size_t smem2 = sizeof(uint32_t) * (2 * kT2Slots + kT2Warps * kT2Per);
-    err = cudaFuncSetAttribute(k_t2<PV, PAIRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+    EngineArgs eb = ea;
+    eb.t2 = p->t2; eb.n_t2 = p->n_t2; eb.t2ctr = 16;
+    const size_t smem2 = sizeof(uint32_t) * (2 * kT2Slots + 16 * kT2Per);
+    err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 512, kT2Slots>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     if (err != cudaSuccess) return err;
-    k_t2<PV, PAIRS><<<g->num_sms * 3, kT2Threads, smem2, st>>>(ea);
+    k_t2<PV, PAIRS, 512, kT2Slots><<<g->num_sms * 3, 512, smem2, st>>>(eb);
+    g->launches++;
+  }
+  if (p->n_t2s) {
+    EngineArgs es = ea;
+    es.t2 = p->t2s; es.n_t2 = p->n_t2s; es.t2ctr = 17;
+    const size_t smem2 = sizeof(uint32_t) * (kT2Slots + 8 * kT2Per);
+    err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 256, kT2Slots / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+    if (err != cudaSuccess) return err;
+    k_t2<PV, PAIRS, 256, kT2Slots / 2><<<g->num_sms * 6, 256, smem2, st>>>(es);
     g->launches++;
   }
   cudaEventRecord(e2, st);

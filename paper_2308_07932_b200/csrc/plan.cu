@@ -112,12 +112,12 @@ __global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, uint64_t w
   }
 }
 
-struct IsT2 {
+struct IsT2 {  // lo < work <= hi
   const uint64_t* work;
-  uint64_t t2max;
+  uint64_t lo, hi;
   __device__ __forceinline__ bool operator()(uint32_t x) const {
     uint64_t w = work[x];
-    return w > kT1Max && w <= t2max;
+    return w > lo && w <= hi;
   }
 };
 
@@ -188,6 +188,7 @@ void free_plan(Plan* p, cudaStream_t st) {
   if (p->work) dfree(p->work, st);
   if (p->t1) dfree(p->t1, st);
   if (p->t2) dfree(p->t2, st);
+  if (p->t2s) dfree(p->t2s, st);
   if (p->units) dfree(p->units, st);
   *p = Plan{};
 }
@@ -266,33 +267,38 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   }
   BBF_CUDA(dmalloc(&p->t1, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&p->t2, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&p->t2s, 4ull * (n + 1), st));
   uint32_t* d_nsel;
-  BBF_CUDA(dmalloc(&d_nsel, 8, st));
+  BBF_CUDA(dmalloc(&d_nsel, 12, st));
+  const uint64_t t2mid = std::min<uint64_t>(kT2SmallMax, t2max);
+  const IsT2 big{p->work, t2mid, t2max}, small{p->work, kT1Max, t2mid};
   {
     cub::CountingInputIterator<uint32_t> it(0);
     size_t tb = 0, tb3 = 0;
     cub::DeviceSelect::If(nullptr, tb, it, p->t1, d_nsel, (int)n, IsT1{p->work}, st);
-    cub::DeviceSelect::If(nullptr, tb3, it, p->t2, d_nsel + 1, (int)n, IsT2{p->work, t2max}, st);
+    cub::DeviceSelect::If(nullptr, tb3, it, p->t2, d_nsel + 1, (int)n, big, st);
     size_t tb2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb2, nunits, ustart, (int)(n + 1), st);
     tb = std::max(std::max(tb, tb2), tb3);
     void* tmp;
     BBF_CUDA(dmalloc(&tmp, tb + 16, st));
     BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t1, d_nsel, (int)n, IsT1{p->work}, st));
-    BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t2, d_nsel + 1, (int)n, IsT2{p->work, t2max}, st));
+    BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t2, d_nsel + 1, (int)n, big, st));
+    BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t2s, d_nsel + 2, (int)n, small, st));
     BBF_CUDA(cudaMemsetAsync(nunits + n, 0, 4, st));
     BBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nunits, ustart, (int)(n + 1), st));
-    g->launches += 5;
+    g->launches += 6;
     dfree(tmp, st);
   }
-  uint32_t h_nsel[2] = {0, 0}, h_nunits = 0;
+  uint32_t h_nsel[3] = {0, 0, 0}, h_nunits = 0;
   unsigned long long h_acc[4];
-  BBF_CUDA(cudaMemcpyAsync(h_nsel, d_nsel, 8, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaMemcpyAsync(h_nsel, d_nsel, 12, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaMemcpyAsync(&h_nunits, ustart + n, 4, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaMemcpyAsync(h_acc, acc, 32, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaStreamSynchronize(st));
   p->n_t1 = h_nsel[0];
   p->n_t2 = h_nsel[1];
+  p->n_t2s = h_nsel[2];
   p->n_units = h_nunits;
   p->W_t1 = h_acc[0];
   p->W_t3 = h_acc[1];
