@@ -153,6 +153,26 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
   return v;
 }
 
+// Segmented sums of (b, n) over groups of consecutive lanes (a group starts at lane gs; the
+// sums are valid at each group's last lane): inclusive scans minus the scan at lane gs - 1.
+// When every lane's b and n are < 2^11 (the common case) one scan of b | n << 16 does both
+// halves exactly (a full-warp sum stays < 2^16 per half).
+__device__ __forceinline__ void seg_sums2(uint32_t b, uint32_t n, int gs, int lane, uint32_t& sb, uint32_t& sn) {
+  const int src = gs > 0 ? gs - 1 : 0;
+  if (__all_sync(0xffffffffu, (b | n) < 2048u)) {
+    const uint32_t ip = warp_incl_scan(b | (n << 16), lane);
+    const uint32_t pp = __shfl_sync(0xffffffffu, ip, src);
+    const uint32_t d = ip - (gs > 0 ? pp : 0u);
+    sb = d & 0xffffu;
+    sn = d >> 16;
+  } else {
+    const uint32_t ib = warp_incl_scan(b, lane), in = warp_incl_scan(n, lane);
+    const uint32_t pb = __shfl_sync(0xffffffffu, ib, src), pn = __shfl_sync(0xffffffffu, in, src);
+    sb = ib - (gs > 0 ? pb : 0u);
+    sn = in - (gs > 0 ? pn : 0u);
+  }
+}
+
 // Flattened-step owner lookup: lanes hold items (len, excl = exclusive prefix); for flattened
 // index f = base + lane returns the lane that owns f.  nz = ballot(len > 0).
 __device__ __forceinline__ int flat_owner(uint32_t len, uint32_t excl, uint32_t nz, uint32_t base,
@@ -696,13 +716,12 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
               if (pass == 1 && __any_sync(0xffffffffu, (cb | cn) != 0)) {
                 // segmented sum over each owner's lane group; its last lane adds it (one writer
                 // per owner per step, so no atomics)
-                const uint32_t ib = warp_incl_scan(cb, lane), in = warp_incl_scan(cn, lane);
-                const int src = gs[u] > 0 ? (int)gs[u] - 1 : 0;
-                const uint32_t pb = __shfl_sync(0xffffffffu, ib, src), pn = __shfl_sync(0xffffffffu, in, src);
+                uint32_t sb, sn;
+                seg_sums2(cb, cn, (int)gs[u], lane, sb, sn);
                 const bool last = c < T && (c + 1 == T || lane == 31 || ((smask[u] >> (lane + 1)) & 1u));
                 if (last) {
-                  sh_acc[warp][0][ow[u]] += ib - (gs[u] > 0 ? pb : 0u);
-                  sh_acc[warp][1][ow[u]] += in - (gs[u] > 0 ? pn : 0u);
+                  sh_acc[warp][0][ow[u]] += sb;
+                  sh_acc[warp][1][ow[u]] += sn;
                 }
                 __syncwarp();
               }
