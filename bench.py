@@ -232,6 +232,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
     main_ms = []
+    count_ms = []
     algo_bytes = 0
     algo_ops = 0.0
     e0.record(stream)
@@ -239,6 +240,7 @@ def main():
         tot, st = step()
         launches += st["kernel_launches"]
         main_ms.append(st["ms_main_kernel"])
+        count_ms.append(tot["ms_count"])
         algo_bytes = st["algo_bytes"]
         algo_ops = st["algo_ops"]
     e1.record(stream)
@@ -254,6 +256,11 @@ def main():
         ms = float(t.item())
     ms_step = ms / args.steps
     W_G = tot["wedges_G"]
+    cms = float(np.mean(count_ms))
+    if world > 1:
+        t = torch.tensor([cms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        cms = float(t.item())
     value = W_G * args.steps / (ms * 1e-3)
     bfly = tot["balanced"] * args.steps / (ms * 1e-3)
 
@@ -319,9 +326,15 @@ def main():
         "config": {"workload": WORKLOADS[args.config], "counts": "global + per-vertex (both sides)",
                    "wedges_G": W_G, "balanced": tot["balanced"], "unbalanced": tot["unbalanced"],
                    "step": "bbf_graph_load_csr(device CSR) + bbf_count_per_vertex + free",
-                   "l2": "inputs larger than L2 (CSR 450 MB + build buffers > 126 MB); no flush",
+                   "l2": f"inputs larger than L2 (input CSR {(g.row_ptr.nbytes + g.col.nbytes + g.sign.nbytes) / 1e6:.0f} MB "
+                         f"+ rank-space CSR + build buffers > 126 MB); no flush",
                    "parallelism": f"dp{world} (start-vertex units sharded, CSR replicated)"},
         "balanced_butterflies_per_s": bfly,
+        # SURVEY §8(d)'s t_count reading: graph already resident and built, the count call alone
+        # (plan + wedge kernels + NCCL all-reduce; bbf_counts.ms_count)
+        "count_only": {"value": W_G / (cms * 1e-3) if cms > 0 else None, "unit": "wedges/s",
+                       "ms_per_step": cms, "definition": "W_G / device time of the count inside "
+                       "bbf_count_per_vertex (plan + kernels + all-reduce); load/build excluded"},
         "e2e": {"value": (W_G / (e2e_ms * 1e-3)) if e2e_ms else None, "unit": "wedges/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms},
