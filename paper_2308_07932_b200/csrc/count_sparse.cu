@@ -36,8 +36,6 @@ namespace {
 constexpr int kT3Threads = BBF_T3_THREADS;
 constexpr int kT3Warps = kT3Threads / 32;
 constexpr uint32_t kBm = kWin / 32;   // bitmap words
-constexpr int kT1Warps = 12;
-constexpr uint32_t kT1Slots = 1024;
 
 struct EngineArgs {
   const uint32_t* off;
@@ -56,6 +54,7 @@ struct EngineArgs {
   const Unit* units;
   uint32_t n_t1, n_t2, n_units;
   uint32_t t2ctr;        // acc index of that instance's start cursor
+  uint32_t t1ctr;        // acc index of the k_t1 instance's start cursor
   uint32_t n_u, n;
   Zones z[2];
   int rank, nranks;
@@ -836,7 +835,9 @@ __device__ __forceinline__ uint32_t hslot(uint32_t l, uint32_t mask) {
   return (l * 0x9E3779B1u) >> 16 & mask;
 }
 
-template <bool PV, bool PAIRS>
+// Two instances: <32 warps, 256 slots> for starts with <= kT1SmallMax wedges (2 CTAs = 64 warps
+// per SM) and <12 warps, kT1Slots> for the rest (24 warps per SM, shared-memory bound).
+template <bool PV, bool PAIRS, int kT1Warps, uint32_t kT1Slots>
 __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
   extern __shared__ uint32_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -853,7 +854,7 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
   unsigned long long totB = 0, totN = 0;
   while (true) {
     unsigned long long q = 0;
-    if (lane == 0) q = atomicAdd(&a.acc[3], 1ull);
+    if (lane == 0) q = atomicAdd(&a.acc[a.t1ctr], 1ull);
     q = __shfl_sync(0xffffffffu, q, 0);
     const uint64_t ti = q * a.nranks + a.rank;
     if (ti >= a.n_t1) break;
@@ -1166,11 +1167,14 @@ template <bool PV, bool PAIRS, int ENC>
 cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, Plan* p,
                           cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2) {
   const size_t smem3 = sizeof(uint32_t) * (kWin + kBm + 2 * kMaxWin);
-  const size_t smem1 = sizeof(uint32_t) * kT1Warps * (2 * kT1Slots + 3 * 32 + 64);
+  const size_t smem1 = sizeof(uint32_t) * 32 * (2 * 256 + 3 * 32 + 64);
+  const size_t smem1b = sizeof(uint32_t) * 12 * (2 * 1024 + 3 * 32 + 64);
   cudaError_t err;
   err = cudaFuncSetAttribute(k_t3<PV, PAIRS, ENC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
   if (err != cudaSuccess) return err;
-  err = cudaFuncSetAttribute(k_t1<PV, PAIRS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+  err = cudaFuncSetAttribute(k_t1<PV, PAIRS, 32, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+  if (err != cudaSuccess) return err;
+  err = cudaFuncSetAttribute(k_t1<PV, PAIRS, 12, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1b);
   if (err != cudaSuccess) return err;
   cudaEventRecord(e0, st);
   if (p->n_units) {
@@ -1179,7 +1183,15 @@ cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, P
   }
   cudaEventRecord(e1, st);
   if (p->n_t1) {
-    k_t1<PV, PAIRS><<<g->num_sms * 2, kT1Warps * 32, smem1, st>>>(ea);
+    EngineArgs e1a = ea;
+    e1a.t1 = p->t1; e1a.n_t1 = p->n_t1; e1a.t1ctr = 3;
+    k_t1<PV, PAIRS, 32, 256><<<g->num_sms * 2, 32 * 32, smem1, st>>>(e1a);
+    g->launches++;
+  }
+  if (p->n_t1b) {
+    EngineArgs e1b = ea;
+    e1b.t1 = p->t1b; e1b.n_t1 = p->n_t1b; e1b.t1ctr = 18;
+    k_t1<PV, PAIRS, 12, 1024><<<g->num_sms * 2, 12 * 32, smem1b, st>>>(e1b);
     g->launches++;
   }
   if (p->n_t2) {

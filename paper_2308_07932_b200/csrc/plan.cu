@@ -121,13 +121,7 @@ struct IsT2 {  // lo < work <= hi
   }
 };
 
-struct IsT1 {
-  const uint64_t* work;
-  __device__ __forceinline__ bool operator()(uint32_t x) const {
-    uint64_t w = work[x];
-    return w > 0 && w <= kT1Max;
-  }
-};
+
 
 // fill the units of every T3 row: split [l(x)+1, L4) into nunits pieces of ~equal sum of end
 // degrees (expected wedges per end rank are proportional to the end's degree)
@@ -189,6 +183,7 @@ void free_plan(Plan* p, cudaStream_t st) {
   if (p->t1) dfree(p->t1, st);
   if (p->t2) dfree(p->t2, st);
   if (p->t2s) dfree(p->t2s, st);
+  if (p->t1b) dfree(p->t1b, st);
   if (p->units) dfree(p->units, st);
   *p = Plan{};
 }
@@ -268,37 +263,41 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   BBF_CUDA(dmalloc(&p->t1, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&p->t2, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&p->t2s, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&p->t1b, 4ull * (n + 1), st));
   uint32_t* d_nsel;
-  BBF_CUDA(dmalloc(&d_nsel, 12, st));
+  BBF_CUDA(dmalloc(&d_nsel, 16, st));
   const uint64_t t2mid = std::min<uint64_t>(kT2SmallMax, t2max);
   const IsT2 big{p->work, t2mid, t2max}, small{p->work, kT1Max, t2mid};
+  const IsT2 t1s{p->work, 0, kT1SmallMax}, t1b{p->work, kT1SmallMax, kT1Max};
   {
     cub::CountingInputIterator<uint32_t> it(0);
     size_t tb = 0, tb3 = 0;
-    cub::DeviceSelect::If(nullptr, tb, it, p->t1, d_nsel, (int)n, IsT1{p->work}, st);
+    cub::DeviceSelect::If(nullptr, tb, it, p->t1, d_nsel, (int)n, t1s, st);
     cub::DeviceSelect::If(nullptr, tb3, it, p->t2, d_nsel + 1, (int)n, big, st);
     size_t tb2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb2, nunits, ustart, (int)(n + 1), st);
     tb = std::max(std::max(tb, tb2), tb3);
     void* tmp;
     BBF_CUDA(dmalloc(&tmp, tb + 16, st));
-    BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t1, d_nsel, (int)n, IsT1{p->work}, st));
+    BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t1, d_nsel, (int)n, t1s, st));
+    BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t1b, d_nsel + 3, (int)n, t1b, st));
     BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t2, d_nsel + 1, (int)n, big, st));
     BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t2s, d_nsel + 2, (int)n, small, st));
     BBF_CUDA(cudaMemsetAsync(nunits + n, 0, 4, st));
     BBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nunits, ustart, (int)(n + 1), st));
-    g->launches += 6;
+    g->launches += 7;
     dfree(tmp, st);
   }
-  uint32_t h_nsel[3] = {0, 0, 0}, h_nunits = 0;
+  uint32_t h_nsel[4] = {0, 0, 0, 0}, h_nunits = 0;
   unsigned long long h_acc[4];
-  BBF_CUDA(cudaMemcpyAsync(h_nsel, d_nsel, 12, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaMemcpyAsync(h_nsel, d_nsel, 16, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaMemcpyAsync(&h_nunits, ustart + n, 4, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaMemcpyAsync(h_acc, acc, 32, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaStreamSynchronize(st));
   p->n_t1 = h_nsel[0];
   p->n_t2 = h_nsel[1];
   p->n_t2s = h_nsel[2];
+  p->n_t1b = h_nsel[3];
   p->n_units = h_nunits;
   p->W_t1 = h_acc[0];
   p->W_t3 = h_acc[1];
