@@ -984,37 +984,33 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
 // (end rank + 1 -> a | d << 16) with S = pow2 >= 2 * work slots, so a start is done in one sweep
 // of its wedges (no counter windows, no records).  Warps take chunks of 32 middles; inside a
 // chunk the wedges are spread over the lanes as in k_t1.  a + d <= #middles <= work < 2^16.
-// Two instances: <512 threads, kT2Slots> for starts above kT2SmallMax wedges (3 CTAs per SM) and
-// <256, kT2Slots / 2> for the rest (6 per SM): a start is latency-bound, so more starts in flight
-// per SM is what raises throughput.
-constexpr uint32_t kT2Per = 5 * 32;  // per-warp scratch words
-
+// Two instances: <512 threads, kT2Slots> for starts above kT2SmallMax wedges and <256,
+// kT2Slots / 2> for the rest.  The start's wedges are flattened over ALL warps of the CTA (not
+// middle chunks per warp: per-chunk work varied so much that barrier waits were most of the
+// kernel's time): the middles of a round (<= 2 per thread) are loaded with their segment lengths,
+// a CTA scan gives each middle's first wedge, and warp w takes wedge steps w, w + warps, ... ;
+// a lane finds its middle by binary search in the shared prefix.  Pass 2 sums the middle shares
+// per run of equal middles in a step and adds them to per-middle shared totals.
 template <bool PV, bool PAIRS, int kT2Threads, int kSlots>
 __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
   constexpr int kT2Warps = kT2Threads / 32;
+  constexpr uint32_t kM = 2 * kT2Threads;  // middles per round
   extern __shared__ uint32_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   volatile uint32_t* keys = smem;
   uint32_t* vals = smem + kSlots;
-  uint32_t* sh_incl = vals + kSlots + warp * kT2Per;
-  uint32_t* sh_s = sh_incl + 32;
-  uint32_t* sh_wv = sh_s + 32;
-  uint32_t* sh_mb = sh_wv + 32;
-  uint32_t* sh_mn = sh_mb + 32;
-  __shared__ uint32_t sh_item, sh_c[2];
+  uint32_t* mP = vals + kSlots;  // kM + 1: mP[i] = first flattened wedge of middle i
+  uint32_t* mS = mP + kM + 1;    // kM: first eligible end entry (ub)
+  uint32_t* mW = mS + kM;        // kM: middle word
+  uint32_t* mB = mW + kM;        // kM: pass-2 balanced share of the middle
+  uint32_t* mN = mB + kM;        // kM: pass-2 unbalanced share
+  __shared__ uint32_t sh_item, sh_wsum[kT2Warps];
   __shared__ unsigned long long sh_red[2][kT2Warps];
-  __shared__ uint8_t sh_own2[kT2Warps][32];
   for (uint32_t i = tid; i < 2 * kSlots; i += kT2Threads) ((uint32_t*)keys)[i] = 0;
-  sh_mb[lane] = 0;
-  sh_mn[lane] = 0;
   unsigned long long totB = 0, totN = 0;
   __syncthreads();
   while (true) {
-    if (tid == 0) {
-      sh_item = (uint32_t)atomicAdd(&a.acc[a.t2ctr], 1ull);
-      sh_c[0] = 0;
-      sh_c[1] = 0;
-    }
+    if (tid == 0) sh_item = (uint32_t)atomicAdd(&a.acc[a.t2ctr], 1ull);
     __syncthreads();
     const uint64_t ti = (uint64_t)sh_item * a.nranks + a.rank;
     if (ti >= a.n_t2) break;
@@ -1027,46 +1023,51 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
     uint32_t S = 64;
     while (S < 2 * W && S < kSlots) S <<= 1;
     const uint32_t mask = S - 1;
-    // middles spread over all warps: chunks of cs <= 32 middles, chunk ck to warp ck mod warps
-    const uint32_t cs = min(32u, max(1u, (m + kT2Warps - 1) / kT2Warps));
 #pragma unroll 1
     for (int pass = 0; pass < (PV ? 2 : 1); ++pass) {
-      for (uint32_t ck = warp; ck * cs < m; ck += kT2Warps) {
-        const uint32_t cb = ck * cs;
-        const uint32_t i = cb + lane;
-        uint32_t wv = 0, s = 0, len = 0;
-        if ((uint32_t)lane < cs && i < m) {
-          wv = a.adj[m_lo + i];
-          s = a.ub[m_lo + i];
-          const uint32_t en = a.end1[ob + (wv & kMask)];
-          len = en > s ? en - s : 0;
+#pragma unroll 1
+      for (uint32_t r0 = 0; r0 < m; r0 += kM) {
+        const uint32_t mc = min(kM, m - r0);
+        // round set-up: two consecutive middles per thread, CTA-wide exclusive scan of lengths
+        uint32_t len2[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t i = 2 * tid + q;
+          len2[q] = 0;
+          if (i < mc) {
+            const uint32_t wv = a.adj[m_lo + r0 + i];
+            const uint32_t s0 = a.ub[m_lo + r0 + i];
+            const uint32_t en = a.end1[ob + (wv & kMask)];
+            len2[q] = en > s0 ? en - s0 : 0;
+            mS[i] = s0;
+            mW[i] = wv;
+            if (pass == 1) { mB[i] = 0; mN[i] = 0; }
+          }
         }
-        const uint32_t incl = warp_incl_scan(len, lane), excl = incl - len;
-        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-        if (tot == 0) continue;
-        // wedges flattened over the lanes; the owner middle of lane L's wedge is the last middle
-        // starting at or before it in this step (start bitmask + owner table), else the carried one
-        int carry = 0;
-        uint32_t accb = 0, accn = 0;  // pass 2: this lane's middle totals (lane = middle)
-        for (uint32_t base = 0; base < tot; base += 32) {
-          const bool st = len > 0 && excl >= base && excl < base + 32;
-          if (st) sh_own2[warp][excl - base] = (uint8_t)lane;
-          const uint32_t smask = __reduce_or_sync(0xffffffffu, st ? 1u << (excl - base) : 0u);
-          __syncwarp();
-          const uint32_t mm = smask & (0xffffffffu >> (31 - lane));
-          const int gs = mm ? 31 - __clz(mm) : 0;
-          const int ow = mm ? (int)sh_own2[warp][gs] : carry;
-          __syncwarp();
-          carry = __shfl_sync(0xffffffffu, ow, 31);
-          const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, ow);
-          const uint32_t o_s = __shfl_sync(0xffffffffu, s, ow);
-          const uint32_t o_wv = __shfl_sync(0xffffffffu, wv, ow);
+        const uint32_t tsum = len2[0] + len2[1];
+        const uint32_t wincl = warp_incl_scan(tsum, lane);
+        if (lane == 31) sh_wsum[warp] = wincl;
+        __syncthreads();
+        uint32_t wbase = 0;
+        for (int w2 = 0; w2 < warp; ++w2) wbase += sh_wsum[w2];
+        const uint32_t ex = wbase + wincl - tsum;
+        if (2 * tid < kM) { mP[2 * tid] = ex; mP[2 * tid + 1] = ex + len2[0]; }
+        if (tid == kT2Threads - 1) mP[kM] = ex + tsum;
+        __syncthreads();
+        const uint32_t T = mP[kM];
+        for (uint32_t base = 32u * warp; base < T; base += 32u * kT2Warps) {
           const uint32_t t = base + lane;
-          uint32_t b2 = 0, n2 = 0;
-          if (t < tot) {
-            const uint32_t ev = a.adj[o_s + (t - o_excl)];
+          uint32_t j = kM, b2 = 0, n2 = 0;
+          if (t < T) {
+            uint32_t lo = 0, hi = mc - 1;  // last middle with mP[j] <= t
+            while (lo < hi) {
+              const uint32_t md = (lo + hi + 1) >> 1;
+              if (mP[md] <= t) lo = md; else hi = md - 1;
+            }
+            j = lo;
+            const uint32_t ev = a.adj[mS[j] + (t - mP[j])];
             const uint32_t l = ev & kMask;
-            const uint32_t cls = (ev ^ o_wv) >> 31;
+            const uint32_t cls = (ev ^ mW[j]) >> 31;
             const uint32_t key = l + 1;
             uint32_t h = hslot(l, mask);
             if (pass == 0) {
@@ -1089,34 +1090,33 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
             }
           }
           if (pass == 1 && __any_sync(0xffffffffu, (b2 | n2) != 0)) {
-            // per-owner sums by a segmented scan; the owner's last lane in this step hands the
-            // sum to the owner lane through shared memory
-            const uint32_t ib = warp_incl_scan(b2, lane), in = warp_incl_scan(n2, lane);
-            const int src = gs > 0 ? gs - 1 : 0;
-            const uint32_t pb = __shfl_sync(0xffffffffu, ib, src), pn = __shfl_sync(0xffffffffu, in, src);
-            const bool last = t < tot && (t + 1 == tot || lane == 31 || ((smask >> (lane + 1)) & 1u));
-            if (last) {
-              sh_mb[ow] += ib - (gs > 0 ? pb : 0u);
-              sh_mn[ow] += in - (gs > 0 ? pn : 0u);
+            // lanes' middles are non-decreasing: sum each run of equal j, its last lane adds it
+            const uint32_t jp = __shfl_up_sync(0xffffffffu, j, 1);
+            const uint32_t starts = __ballot_sync(0xffffffffu, lane == 0 || jp != j);
+            const uint32_t mm = starts & (0xffffffffu >> (31 - lane));
+            const int gs = 31 - __clz(mm);
+            uint32_t sb2, sn2;
+            seg_sums2(b2, n2, gs, lane, sb2, sn2);
+            const bool last = lane == 31 || ((starts >> (lane + 1)) & 1u);
+            if (last && j < kM && (sb2 | sn2)) {
+              if (sb2) atomicAdd(&mB[j], sb2);
+              if (sn2) atomicAdd(&mN[j], sn2);
             }
-            __syncwarp();
           }
         }
+        __syncthreads();
         if (pass == 1) {
-          __syncwarp();
-          accb = sh_mb[lane];
-          accn = sh_mn[lane];
-          if (accb | accn) {
-            const uint32_t vr = ob + (wv & kMask);
-            if (accb) atomicAdd(&a.pv[2ull * vr], (unsigned long long)accb);
-            if (accn) atomicAdd(&a.pv[2ull * vr + 1], (unsigned long long)accn);
+          for (uint32_t i = tid; i < mc; i += kT2Threads) {
+            const uint32_t cb = mB[i], cn = mN[i];
+            if (cb | cn) {
+              const uint32_t vr = ob + (mW[i] & kMask);
+              if (cb) atomicAdd(&a.pv[2ull * vr], (unsigned long long)cb);
+              if (cn) atomicAdd(&a.pv[2ull * vr + 1], (unsigned long long)cn);
+            }
           }
-          sh_mb[lane] = 0;
-          sh_mn[lane] = 0;
+          __syncthreads();
         }
-        __syncwarp();
       }
-      __syncthreads();
     }
     // ---- epilogue: Lemma 2 per end (Alg. 2 lines 15-18), clear
     unsigned long long xB = 0, xN = 0;
@@ -1197,19 +1197,19 @@ cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, P
   if (p->n_t2) {
     EngineArgs eb = ea;
     eb.t2 = p->t2; eb.n_t2 = p->n_t2; eb.t2ctr = 16;
-    const size_t smem2 = sizeof(uint32_t) * (2 * kT2Slots + 16 * kT2Per);
+    const size_t smem2 = sizeof(uint32_t) * (2 * kT2Slots + 5 * 1024 + 1);
     err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 512, kT2Slots>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     if (err != cudaSuccess) return err;
-    k_t2<PV, PAIRS, 512, kT2Slots><<<g->num_sms * 3, 512, smem2, st>>>(eb);
+    k_t2<PV, PAIRS, 512, kT2Slots><<<g->num_sms * 2, 512, smem2, st>>>(eb);
     g->launches++;
   }
   if (p->n_t2s) {
     EngineArgs es = ea;
     es.t2 = p->t2s; es.n_t2 = p->n_t2s; es.t2ctr = 17;
-    const size_t smem2 = sizeof(uint32_t) * (kT2Slots + 8 * kT2Per);
+    const size_t smem2 = sizeof(uint32_t) * (kT2Slots + 5 * 512 + 1);
     err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 256, kT2Slots / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     if (err != cudaSuccess) return err;
-    k_t2<PV, PAIRS, 256, kT2Slots / 2><<<g->num_sms * 6, 256, smem2, st>>>(es);
+    k_t2<PV, PAIRS, 256, kT2Slots / 2><<<g->num_sms * 5, 256, smem2, st>>>(es);
     g->launches++;
   }
   cudaEventRecord(e2, st);
