@@ -178,7 +178,8 @@ __host__ __device__ inline unsigned long long comb2(unsigned long long x) {
 //            PAPER.md:875 "we drop the rank comparison"), starts = rows of `side`, middles =
 //            [off, end1), ends = l(w) > l(x) (each unordered pair once).
 constexpr uint32_t kT2Slots = 8192;               // k_t2 shared hash slots (64 KB)
-constexpr uint64_t kT2MaxDefault = kT2Slots / 2;  // T2 tier: at most this many wedges per start
+constexpr uint32_t kT2HugeSlots = 2 * kT2Slots;    // k_t2 1024-thread instance (128 KB hash)
+constexpr uint64_t kT2MaxDefault = 10240;  // T2 tier: at most this many wedges per start (swept: 6144..12288)
 constexpr uint64_t kT2SmallMax = kT2Slots / 4;   // T2 starts with at most this many wedges use the small k_t2
 constexpr uint64_t kT1SmallMax = 128;             // T1 starts with at most this many wedges use the small k_t1
 struct Unit {  // one T3 work unit: start row x, end-rank range [lo, hi)
@@ -191,10 +192,11 @@ struct Plan {
   uint64_t* work;      // per row: pruned wedge count
   uint32_t* t1;        // rows with 0 < work <= kT1SmallMax (k_t1, 256-slot warp hash)
   uint32_t* t1b;       // rows with kT1SmallMax < work <= kT1Max (k_t1, 1024-slot warp hash)
-  uint32_t* t2;        // rows with kT2SmallMax < work <= T2 max (k_t2, CTA shared hash)
+  uint32_t* t2;        // rows with kT2SmallMax < work <= kT2Slots * 3/4 (k_t2, CTA shared hash)
   uint32_t* t2s;       // rows with kT1Max < work <= kT2SmallMax (k_t2, half-size CTA)
+  uint32_t* t2h;       // rows with kT2Slots * 3/4 < work <= T2 max (k_t2, 1024 threads, kT2HugeSlots)
   Unit* units;         // T3 units
-  uint32_t n_t1, n_t1b, n_t2, n_t2s, n_units;
+  uint32_t n_t1, n_t1b, n_t2, n_t2s, n_t2h, n_units;
   uint32_t max_mid;    // max middles of a T3 start
   unsigned long long max_work;  // max wedges of a T3 start
   unsigned long long W_full;    // un-pruned wedge count (route G: W_G of the paper)

@@ -1203,6 +1203,15 @@ cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, P
     k_t2<PV, PAIRS, 512, kT2Slots><<<g->num_sms * 2, 512, smem2, st>>>(eb);
     g->launches++;
   }
+  if (p->n_t2h) {
+    EngineArgs eh = ea;
+    eh.t2 = p->t2h; eh.n_t2 = p->n_t2h; eh.t2ctr = 19;
+    const size_t smem2 = sizeof(uint32_t) * (2 * kT2HugeSlots + 5 * 2048 + 1);
+    err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 1024, kT2HugeSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+    if (err != cudaSuccess) return err;
+    k_t2<PV, PAIRS, 1024, kT2HugeSlots><<<g->num_sms, 1024, smem2, st>>>(eh);
+    g->launches++;
+  }
   if (p->n_t2s) {
     EngineArgs es = ea;
     es.t2 = p->t2s; es.n_t2 = p->n_t2s; es.t2ctr = 17;

@@ -184,6 +184,7 @@ void free_plan(Plan* p, cudaStream_t st) {
   if (p->t2) dfree(p->t2, st);
   if (p->t2s) dfree(p->t2s, st);
   if (p->t1b) dfree(p->t1b, st);
+  if (p->t2h) dfree(p->t2h, st);
   if (p->units) dfree(p->units, st);
   *p = Plan{};
 }
@@ -254,7 +255,7 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   // tiers and units
   // a T2 start's distinct ends (<= its wedges) must fit the k_t2 hash at load <= 1/2
   const uint64_t t2max = std::min<uint64_t>(
-      getenv("BBF_T2_MAX") ? (uint64_t)atoll(getenv("BBF_T2_MAX")) : kT2MaxDefault, kT2Slots * 3 / 4);
+      getenv("BBF_T2_MAX") ? (uint64_t)atoll(getenv("BBF_T2_MAX")) : kT2MaxDefault, kT2HugeSlots * 3 / 4);
   BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
   if (n) {
     k_tier<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, p->work, w_target, t2max, sb, se, nunits, acc);
@@ -264,10 +265,11 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   BBF_CUDA(dmalloc(&p->t2, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&p->t2s, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&p->t1b, 4ull * (n + 1), st));
+  BBF_CUDA(dmalloc(&p->t2h, 4ull * (n + 1), st));
   uint32_t* d_nsel;
-  BBF_CUDA(dmalloc(&d_nsel, 16, st));
-  const uint64_t t2mid = std::min<uint64_t>(kT2SmallMax, t2max);
-  const IsT2 big{p->work, t2mid, t2max}, small{p->work, kT1Max, t2mid};
+  BBF_CUDA(dmalloc(&d_nsel, 20, st));
+  const uint64_t t2mid = std::min<uint64_t>(kT2SmallMax, t2max), t2big = std::min<uint64_t>(kT2Slots * 3 / 4, t2max);
+  const IsT2 big{p->work, t2mid, t2big}, small{p->work, kT1Max, t2mid}, huge{p->work, t2big, t2max};
   const IsT2 t1s{p->work, 0, kT1SmallMax}, t1b{p->work, kT1SmallMax, kT1Max};
   {
     cub::CountingInputIterator<uint32_t> it(0);
@@ -281,16 +283,17 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     BBF_CUDA(dmalloc(&tmp, tb + 16, st));
     BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t1, d_nsel, (int)n, t1s, st));
     BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t1b, d_nsel + 3, (int)n, t1b, st));
+    BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t2h, d_nsel + 4, (int)n, huge, st));
     BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t2, d_nsel + 1, (int)n, big, st));
     BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t2s, d_nsel + 2, (int)n, small, st));
     BBF_CUDA(cudaMemsetAsync(nunits + n, 0, 4, st));
     BBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nunits, ustart, (int)(n + 1), st));
-    g->launches += 7;
+    g->launches += 8;
     dfree(tmp, st);
   }
-  uint32_t h_nsel[4] = {0, 0, 0, 0}, h_nunits = 0;
+  uint32_t h_nsel[5] = {0, 0, 0, 0, 0}, h_nunits = 0;
   unsigned long long h_acc[4];
-  BBF_CUDA(cudaMemcpyAsync(h_nsel, d_nsel, 16, cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(cudaMemcpyAsync(h_nsel, d_nsel, 20, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaMemcpyAsync(&h_nunits, ustart + n, 4, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaMemcpyAsync(h_acc, acc, 32, cudaMemcpyDeviceToHost, st));
   BBF_CUDA(cudaStreamSynchronize(st));
@@ -298,6 +301,7 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   p->n_t2 = h_nsel[1];
   p->n_t2s = h_nsel[2];
   p->n_t1b = h_nsel[3];
+  p->n_t2h = h_nsel[4];
   p->n_units = h_nunits;
   p->W_t1 = h_acc[0];
   p->W_t3 = h_acc[1];
