@@ -203,6 +203,9 @@ struct Plan {
   unsigned long long W_pruned;  // wedges the kernels actually visit
   unsigned long long W_t1, W_t2, W_t3;
   unsigned long long M_t3;     // eligible middles of T3 starts
+  // end-role packing (route G): ends of local rank >= rsafe[side] have provably < 2^32 end-role
+  // balanced and unbalanced totals, so both go in ONE 64-bit RED (fb | fn << 32) into g->pe
+  uint32_t rsafe[2];
   bool valid;
 };
 
@@ -265,6 +268,7 @@ struct bbf_graph {
   size_t scratch_words;
   unsigned long long* d_acc;  // [0]=B [1]=N [2..] misc counters, [8]=unit cursor, [9]=t1 cursor
   uint64_t* pv;              // 2*n per-vertex counts, (B, N) interleaved per row: pv[2r], pv[2r+1]
+  uint64_t* pe;              // n packed end-role counts (B | N << 32) of "safe" ends, merged into pv
   // stats
   uint64_t launches;
   uint64_t algo_bytes;  // algorithmic bytes of the last count's main kernel (sparse path)

@@ -60,6 +60,8 @@ struct EngineArgs {
   int rank, nranks;
   unsigned long long* acc;  // [0] B [1] N [2] unit cursor [3] t1 cursor [4] cand count
   unsigned long long* pv;   // [0, n) balanced per row, [n, 2n) unbalanced per row
+  unsigned long long* pe;   // packed end-role counts (fb | fn << 32) of ends of rank >= rsafe
+  uint32_t rsafe[2];        // per side: first local rank whose end-role totals stay < 2^32
   uint32_t* scratch;
   uint32_t max_mid;
   uint32_t kwin_cap;  // max windows per side
@@ -89,6 +91,28 @@ __device__ __forceinline__ void emit_pair(const EngineArgs& a, uint32_t x, uint3
     a.cb[slot] = fb;
     a.cn[slot] = fn;
     a.cid[slot] = (lo << 32) | hi;
+  }
+}
+
+// pe (packed end-role counts) -> pv
+__global__ void k_merge_pe(unsigned long long* __restrict__ pe, unsigned long long* __restrict__ pv, uint32_t n) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const unsigned long long q = pe[r];
+  if (!q) return;
+  pv[2ull * r] += q & 0xffffffffull;
+  pv[2ull * r + 1] += q >> 32;
+}
+
+// End-role contribution of pair (x, w): one packed 64-bit RED when w's end-role totals are
+// provably < 2^32 (local rank >= rs, plan.cu k_rsafe), else one RED per non-zero count.
+__device__ __forceinline__ void end_red(const EngineArgs& a, uint32_t rs, uint32_t lrank, uint32_t wrow,
+                                        uint32_t fb, uint32_t fn) {
+  if (lrank >= rs) {
+    atomicAdd(&a.pe[wrow], (unsigned long long)fb | ((unsigned long long)fn << 32));
+  } else {
+    if (fb) atomicAdd(&a.pv[2ull * wrow], (unsigned long long)fb);
+    if (fn) atomicAdd(&a.pv[2ull * wrow + 1], (unsigned long long)fn);
   }
 }
 
@@ -297,8 +321,8 @@ __device__ __forceinline__ void t3_share_cp(uint32_t cbase, uint32_t ev, uint32_
 // a + d >= 2 (SWAR test: a or d >= 2, or a and d both odd).  Fields narrower than 32 bits hold
 // a, d < 2^16, so C(a,2) + C(d,2) and a*d fit 32 bits.
 template <bool PV, bool PAIRS>
-__device__ __forceinline__ void epi_packed(const EngineArgs& a, const Zones& Z, uint32_t sb, uint32_t x,
-                                           uint32_t gw, uint32_t v, unsigned long long& xB,
+__device__ __forceinline__ void epi_packed(const EngineArgs& a, const Zones& Z, uint32_t sb, uint32_t rs,
+                                           uint32_t x, uint32_t gw, uint32_t v, unsigned long long& xB,
                                            unsigned long long& xN) {
   uint32_t h, lfw, lbase, hi, lo;  // half-field width, log2 field width, first rank, SWAR masks
   if (gw < Z.WB[2]) { h = 16; lfw = 5; lbase = Z.L[0] + (gw - Z.WB[1]); hi = 0xfffefffeu; lo = 0x00000001u; }
@@ -317,12 +341,7 @@ __device__ __forceinline__ void epi_packed(const EngineArgs& a, const Zones& Z, 
     xB += fb;
     xN += fn;
     const uint32_t wrow = sb + lbase + f;
-    if (PV) {
-#ifndef BBF_T3_NO_END_RED
-      if (fb) atomicAdd(&a.pv[2ull * (wrow)], (unsigned long long)fb);  // skip zero REDs
-      if (fn) atomicAdd(&a.pv[2ull * (wrow) + 1], (unsigned long long)fn);
-#endif
-    }
+    if (PV) end_red(a, rs, lbase + f, wrow, fb, fn);  // fb | fn != 0 here
     if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
   }
 }
@@ -457,6 +476,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
     const uint32_t x = u.x;
     const bool xu = x < a.n_u;
     const uint32_t sb = xu ? 0 : a.n_u, ob = xu ? a.n_u : 0, lx = x - sb;
+    const uint32_t rs = a.rsafe[xu ? 0 : 1];  // end-role packing threshold of this unit's end side
     // the end side's zone table in shared memory (an indexed kernel-parameter read is an LDC
     // with a long-scoreboard dependency on every epilogue word)
     if (tid < 11) reinterpret_cast<uint32_t*>(&sh_z)[tid] = reinterpret_cast<const uint32_t*>(&a.z[xu ? 0 : 1])[tid];
@@ -754,15 +774,15 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             epi_wide<PV, PAIRS>(a, sb, x, gw, q.x, q.y, xB, xN);
             if (gw + 2 < Z.WB[1]) epi_wide<PV, PAIRS>(a, sb, x, gw + 2, q.z, q.w, xB, xN);
             else {
-              if (q.z) epi_packed<PV, PAIRS>(a, Z, sb, x, gw + 2, q.z, xB, xN);
-              if (q.w) epi_packed<PV, PAIRS>(a, Z, sb, x, gw + 3, q.w, xB, xN);
+              if (q.z) epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw + 2, q.z, xB, xN);
+              if (q.w) epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw + 3, q.w, xB, xN);
             }
             continue;
           }
-          if (q.x) epi_packed<PV, PAIRS>(a, Z, sb, x, gw, q.x, xB, xN);
-          if (q.y) epi_packed<PV, PAIRS>(a, Z, sb, x, gw + 1, q.y, xB, xN);
-          if (q.z) epi_packed<PV, PAIRS>(a, Z, sb, x, gw + 2, q.z, xB, xN);
-          if (q.w) epi_packed<PV, PAIRS>(a, Z, sb, x, gw + 3, q.w, xB, xN);
+          if (q.x) epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw, q.x, xB, xN);
+          if (q.y) epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw + 1, q.y, xB, xN);
+          if (q.z) epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw + 2, q.z, xB, xN);
+          if (q.w) epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw + 3, q.w, xB, xN);
         }
       } else {
         for (uint32_t bw = tid; bw < kBm; bw += kT3Threads) {
@@ -781,7 +801,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
               ctr[wi + 1] = 0;
               epi_wide<PV, PAIRS>(a, sb, x, gw, v, vd, xB, xN);
             } else {
-              epi_packed<PV, PAIRS>(a, Z, sb, x, gw, v, xB, xN);
+              epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw, v, xB, xN);
             }
           }
         }
@@ -953,10 +973,7 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
       xB += fb;
       xN += fn;
       uint32_t wrow = sb + key - 1;
-      if (PV) {
-        atomicAdd(&a.pv[2ull * (wrow)], fb);
-        atomicAdd(&a.pv[2ull * (wrow) + 1], fn);
-      }
+      if (PV) end_red(a, a.rsafe[sb ? 1 : 0], key - 1, wrow, (uint32_t)fb, (uint32_t)fn);  // a, d < 2^16
       if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
     }
     __syncwarp();
@@ -1132,10 +1149,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
       xB += fb;
       xN += fn;
       const uint32_t wrow = sb + key - 1;
-      if (PV) {
-        if (fb) atomicAdd(&a.pv[2ull * wrow], (unsigned long long)fb);
-        if (fn) atomicAdd(&a.pv[2ull * wrow + 1], (unsigned long long)fn);
-      }
+      if (PV) end_red(a, a.rsafe[sb ? 1 : 0], key - 1, wrow, fb, fn);
       if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
     }
     totB += xB;
@@ -1258,6 +1272,9 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   ea.z[0] = g->zones[0]; ea.z[1] = g->zones[1];
   ea.rank = rank; ea.nranks = nranks;
   ea.acc = g->d_acc; ea.pv = (unsigned long long*)g->pv; ea.scratch = g->scratch;
+  ea.pe = (unsigned long long*)g->pe;
+  ea.rsafe[0] = per_vertex ? p->rsafe[0] : 0xffffffffu;
+  ea.rsafe[1] = per_vertex ? p->rsafe[1] : 0xffffffffu;
   ea.max_mid = std::max<uint32_t>(p->max_mid, 1);
   ea.kwin_cap = kwin_cap;
   ea.rec_stride = (uint32_t)(std::max<uint32_t>(p->max_mid, 1) + p->max_work / kRecMax + 1);
@@ -1285,6 +1302,10 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   if (err != cudaSuccess) {
     cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
     return cuda_status(err, "sparse engine launch");
+  }
+  if (per_vertex && (p->rsafe[0] != 0xffffffffu || p->rsafe[1] != 0xffffffffu) && g->n) {
+    k_merge_pe<<<(g->n + 255) / 256, 256, 0, st>>>((unsigned long long*)g->pe, (unsigned long long*)g->pv, g->n);
+    g->launches++;
   }
   unsigned long long h[16];
   BBF_CUDA(cudaMemcpyAsync(h, g->d_acc, sizeof(h), cudaMemcpyDeviceToHost, st));

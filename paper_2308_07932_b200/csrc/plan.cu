@@ -27,6 +27,50 @@ struct RouteRows {
   }
 };
 
+// Upper bound of the wedges that END at each vertex w (route G): for the entry (w -> v) the
+// eligible starts x are v's neighbours before both w (higher priority than w: rev[e] - off[v]
+// entries) and v itself (mid[v] - off[v]).  Consecutive entries of a warp share rows, so the
+// per-row sums are reduced over runs of equal rows before one atomic per run.
+__global__ void k_end_bound(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                            const uint32_t* __restrict__ rev, const uint32_t* __restrict__ erow,
+                            const uint32_t* __restrict__ mid, uint32_t n_u, uint64_t m,
+                            unsigned long long* __restrict__ win) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t e0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; e0 < m;
+       e0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = e0 + lane;
+    uint32_t w = 0xffffffffu;
+    unsigned long long c = 0;
+    if (e < m) {
+      w = erow[e];
+      const uint32_t v = (w < n_u ? n_u : 0u) + (adj[e] & kMask);
+      const uint32_t pos = rev[e] - off[v], hi = mid[v] - off[v];
+      c = pos < hi ? pos : hi;
+    }
+    const uint32_t wp = __shfl_up_sync(0xffffffffu, w, 1);
+    const uint32_t starts = __ballot_sync(0xffffffffu, lane == 0 || wp != w);
+    for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive scan by row
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, c, o);
+      const uint32_t seg = starts & (0xffffffffu >> (31 - lane));
+      const int gs = 31 - __clz(seg);
+      if ((int)lane - o >= gs) c += t;
+    }
+    const bool last = lane == 31 || ((starts >> (lane + 1)) & 1u);
+    if (last && w != 0xffffffffu && c) atomicAdd(&win[w], c);
+  }
+}
+
+// rsafe[side] = 1 + the largest local rank of an end whose end-role totals could reach 2^32:
+// sum_x C(c_xw, 2) <= min(C(W, 2), W * (deg(w) - 1) / 2) with W = the wedges ending at w
+__global__ void k_rsafe(const unsigned long long* __restrict__ win, const uint32_t* __restrict__ degs, uint32_t n_u,
+                        uint32_t n, uint32_t* __restrict__ rsafe) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const unsigned long long W = win[r], d = degs[r];
+  const bool safe = W <= 92681ull || W * d < (1ull << 33);
+  if (!safe) atomicMax(&rsafe[r < n_u ? 0 : 1], (r < n_u ? r : r - n_u) + 1u);
+}
+
 // one thread per adjacency entry: if the entry is a middle of its row for this route, compute
 // ub, the pruned segment length (ends of degree >= 2) and the full count (all ends; W_G)
 __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
@@ -228,6 +272,21 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     }
     k_row_work<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, len, sb, se, p->work);
     g->launches += 2;
+  }
+  p->rsafe[0] = p->rsafe[1] = 0xffffffffu;  // no packing (route S, or empty graph)
+  if (route == 0 && m && !getenv("BBF_NO_PACKED_END")) {  // env: test hook (all ends take two REDs)
+    unsigned long long* win;
+    uint32_t* d_rs;
+    BBF_CUDA(dmalloc(&win, 8ull * (n + 1), st));
+    BBF_CUDA(dmalloc(&d_rs, 8, st));
+    BBF_CUDA(cudaMemsetAsync(win, 0, 8ull * (n + 1), st));
+    BBF_CUDA(cudaMemsetAsync(d_rs, 0, 8, st));
+    k_end_bound<<<grid_for(m, 256), 256, 0, st>>>(g->off, g->adj, g->rev, g->erow, g->mid, g->n_u, m, win);
+    k_rsafe<<<(n + 255) / 256, 256, 0, st>>>(win, g->degs, g->n_u, n, d_rs);
+    g->launches += 2;
+    BBF_CUDA(cudaMemcpyAsync(p->rsafe, d_rs, 8, cudaMemcpyDeviceToHost, st));
+    dfree(win, st);
+    dfree(d_rs, st);
   }
   // pruned total, to size units
   unsigned long long* d_wp;

@@ -284,6 +284,36 @@ def test_counter_encodings_agree(bbf, monkeypatch):
         assert np.array_equal(a, b)
 
 
+def test_end_role_packing_agrees(bbf, monkeypatch):
+    """End-role counts of "safe" ends go through one packed 64-bit RED (plan.cu k_rsafe); the
+    unpacked path (BBF_NO_PACKED_END) gives identical per-vertex arrays on config 3."""
+    g = G.config3()
+    with bbf.Graph.from_synth(g, flags=bbf.BBF_FORCE_SPARSE) as h:
+        ref = h.count_per_vertex()
+    monkeypatch.setenv("BBF_NO_PACKED_END", "1")
+    with bbf.Graph.from_synth(g, flags=bbf.BBF_FORCE_SPARSE) as h:
+        got = h.count_per_vertex()
+    assert got[0]["balanced"] == ref[0]["balanced"] and got[0]["unbalanced"] == ref[0]["unbalanced"]
+    for a, b in zip(got[1:], ref[1:]):
+        assert np.array_equal(a, b)
+
+
+def test_kmn_per_vertex_beyond_2_32(bbf):
+    """All-positive K_{120,9000} on the sparse path: per-U-vertex counts (m-1)C(n,2) = 4.8e9 and
+    per-V-vertex (n-1)C(m,2) exceed 2^32, and the low-priority U ends have ~1e6 incoming wedges
+    at degree 9,000, so the end-role packing must fall back to 64-bit REDs for them (closed
+    forms, SV §8(c) P2)."""
+    m, n = 120, 9000
+    g = G.complete(m, n)
+    with bbf.Graph.from_synth(g, flags=bbf.BBF_FORCE_SPARSE) as h:
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+    c2 = lambda k: k * (k - 1) // 2
+    assert tot["balanced"] == c2(m) * c2(n) and tot["unbalanced"] == 0
+    assert (bu == (m - 1) * c2(n)).all() and (nu == 0).all()
+    assert (bv == (n - 1) * c2(m)).all() and (nv == 0).all()
+    assert (m - 1) * c2(n) > 2**32
+
+
 @pytest.mark.parametrize("path", ["sparse", "dense"])
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_fake_world_shards_sum_to_full_count(bbf, monkeypatch, path, world):
