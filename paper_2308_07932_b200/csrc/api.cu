@@ -164,6 +164,7 @@ bbf_status do_count(bbf_graph* g, bool per_vertex, uint32_t flags, unsigned long
   if (per_vertex) {
     BBF_CUDA(cudaMemsetAsync(g->pv, 0, 16ull * g->n, g->stream));
     BBF_CUDA(cudaMemsetAsync(g->pe, 0, 8ull * g->n, g->stream));
+    BBF_CUDA(cudaMemsetAsync(g->pm, 0, 8ull * g->n, g->stream));
   }
   bbf_status s = BBF_OK;
   if (!g->wg_valid) s = ensure_plan_g(g);  // W_G of the graph (and the sparse plan)
@@ -289,6 +290,7 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_pt
   cudaError_t e = dmalloc(&g->d_acc, 32 * sizeof(unsigned long long), g->stream);
   if (e == cudaSuccess) e = dmalloc(&g->pv, 16ull * (g->n + 1), g->stream);
   if (e == cudaSuccess) e = dmalloc(&g->pe, 8ull * (g->n + 1), g->stream);
+  if (e == cudaSuccess) e = dmalloc(&g->pm, 8ull * (g->n + 1), g->stream);
   if (e != cudaSuccess) s = cuda_status(e, "cudaMalloc");
   if (s == BBF_OK) s = build_graph(g, row_ptr, col, sign, dptr);
   if (s == BBF_OK) {
@@ -311,7 +313,7 @@ bbf_status bbf_graph_free(bbf_graph* g) {
   free_plan(&g->plan_g, g->stream);
   free_plan(&g->plan_s[0], g->stream);
   free_plan(&g->plan_s[1], g->stream);
-  void* ptrs[] = {g->off, g->adj, g->erow, g->rev, g->mid, g->end1, g->inv, g->degs, g->degpre, g->scratch, g->d_acc, g->pv, g->pe,
+  void* ptrs[] = {g->off, g->adj, g->erow, g->rev, g->mid, g->end1, g->inv, g->degs, g->degpre, g->scratch, g->d_acc, g->pv, g->pe, g->pm,
                   g->adjc, g->runid, g->runs, g->skey, g->lr, g->in_rp, g->in_col, g->in_sg,
                   g->dA[0], g->dA[1], g->dS[0], g->dS[1]};
   for (void* p : ptrs)

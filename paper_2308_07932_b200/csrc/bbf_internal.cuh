@@ -206,6 +206,9 @@ struct Plan {
   // end-role packing (route G): ends of local rank >= rsafe[side] have provably < 2^32 end-role
   // balanced and unbalanced totals, so both go in ONE 64-bit RED (fb | fn << 32) into g->pe
   uint32_t rsafe[2];
+  // middle-role packing: middles of local rank >= rmid[side] (C(deg,2) * max degree of the
+  // other side < 2^32) put (B | N << 32) of a record in ONE 64-bit RED into g->pm
+  uint32_t rmid[2];
   bool valid;
 };
 
@@ -269,6 +272,7 @@ struct bbf_graph {
   unsigned long long* d_acc;  // [0]=B [1]=N [2..] misc counters, [8]=unit cursor, [9]=t1 cursor
   uint64_t* pv;              // 2*n per-vertex counts, (B, N) interleaved per row: pv[2r], pv[2r+1]
   uint64_t* pe;              // n packed end-role counts (B | N << 32) of "safe" ends, merged into pv
+  uint64_t* pm;              // n packed middle-role counts of "safe" middles, merged into pv
   // stats
   uint64_t launches;
   uint64_t algo_bytes;  // algorithmic bytes of the last count's main kernel (sparse path)

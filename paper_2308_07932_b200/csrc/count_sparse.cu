@@ -62,6 +62,8 @@ struct EngineArgs {
   unsigned long long* pv;   // [0, n) balanced per row, [n, 2n) unbalanced per row
   unsigned long long* pe;   // packed end-role counts (fb | fn << 32) of ends of rank >= rsafe
   uint32_t rsafe[2];        // per side: first local rank whose end-role totals stay < 2^32
+  unsigned long long* pm;   // packed middle-role counts of middles of rank >= rmid
+  uint32_t rmid[2];
   uint32_t* scratch;
   uint32_t max_mid;
   uint32_t kwin_cap;  // max windows per side
@@ -95,13 +97,14 @@ __device__ __forceinline__ void emit_pair(const EngineArgs& a, uint32_t x, uint3
 }
 
 // pe (packed end-role counts) -> pv
-__global__ void k_merge_pe(unsigned long long* __restrict__ pe, unsigned long long* __restrict__ pv, uint32_t n) {
+__global__ void k_merge_pe(const unsigned long long* __restrict__ pe, const unsigned long long* __restrict__ pm,
+                           unsigned long long* __restrict__ pv, uint32_t n) {
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
-  const unsigned long long q = pe[r];
-  if (!q) return;
-  pv[2ull * r] += q & 0xffffffffull;
-  pv[2ull * r + 1] += q >> 32;
+  const unsigned long long q = pe[r], w = pm[r];
+  if (!(q | w)) return;
+  pv[2ull * r] += (q & 0xffffffffull) + (w & 0xffffffffull);
+  pv[2ull * r + 1] += (q >> 32) + (w >> 32);
 }
 
 // End-role contribution of pair (x, w): one packed 64-bit RED when w's end-role totals are
@@ -113,6 +116,17 @@ __device__ __forceinline__ void end_red(const EngineArgs& a, uint32_t rs, uint32
   } else {
     if (fb) atomicAdd(&a.pv[2ull * wrow], (unsigned long long)fb);
     if (fn) atomicAdd(&a.pv[2ull * wrow + 1], (unsigned long long)fn);
+  }
+}
+
+// Middle-role share of one record / middle: packed like end_red (pm, threshold rmid).
+__device__ __forceinline__ void mid_red(const EngineArgs& a, uint32_t rm, uint32_t lrank, uint32_t vrow,
+                                        uint32_t cb, uint32_t cn) {
+  if (lrank >= rm) {
+    atomicAdd(&a.pm[vrow], (unsigned long long)cb | ((unsigned long long)cn << 32));
+  } else {
+    if (cb) atomicAdd(&a.pv[2ull * vrow], (unsigned long long)cb);
+    if (cn) atomicAdd(&a.pv[2ull * vrow + 1], (unsigned long long)cn);
   }
 }
 
@@ -477,6 +491,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
     const bool xu = x < a.n_u;
     const uint32_t sb = xu ? 0 : a.n_u, ob = xu ? a.n_u : 0, lx = x - sb;
     const uint32_t rs = a.rsafe[xu ? 0 : 1];  // end-role packing threshold of this unit's end side
+    const uint32_t rmv = a.rmid[xu ? 1 : 0];  // middle-role packing threshold (middles: other side)
     // the end side's zone table in shared memory (an indexed kernel-parameter read is an LDC
     // with a long-scoreboard dependency on every epilogue word)
     if (tid < 11) reinterpret_cast<uint32_t*>(&sh_z)[tid] = reinterpret_cast<const uint32_t*>(&a.z[xu ? 0 : 1])[tid];
@@ -750,11 +765,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           if (pass == 1) {
             __syncwarp();
             const uint32_t cb = sh_acc[warp][0][lane], cn = sh_acc[warp][1][lane];
-            if (cb | cn) {
-              const uint32_t vr = ob + (rc.wv & kMask);
-              if (cb) atomicAdd(&a.pv[2ull * (vr)], (unsigned long long)cb);
-              if (cn) atomicAdd(&a.pv[2ull * (vr) + 1], (unsigned long long)cn);
-            }
+            if (cb | cn) mid_red(a, rmv, rc.wv & kMask, ob + (rc.wv & kMask), cb, cn);
             __syncwarp();
           }
         }
@@ -948,11 +959,7 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
         __syncwarp();
         if (pass == 1) {
           uint32_t b2 = sh_mb[lane], n2 = sh_mn[lane];
-          if (b2 | n2) {
-            uint32_t vr = ob + (wv & kMask);
-            atomicAdd(&a.pv[2ull * (vr)], (unsigned long long)b2);
-            atomicAdd(&a.pv[2ull * (vr) + 1], (unsigned long long)n2);
-          }
+          if (b2 | n2) mid_red(a, a.rmid[xu ? 1 : 0], wv & kMask, ob + (wv & kMask), b2, n2);
           sh_mb[lane] = 0;
           sh_mn[lane] = 0;
         }
@@ -1125,11 +1132,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
         if (pass == 1) {
           for (uint32_t i = tid; i < mc; i += kT2Threads) {
             const uint32_t cb = mB[i], cn = mN[i];
-            if (cb | cn) {
-              const uint32_t vr = ob + (mW[i] & kMask);
-              if (cb) atomicAdd(&a.pv[2ull * vr], (unsigned long long)cb);
-              if (cn) atomicAdd(&a.pv[2ull * vr + 1], (unsigned long long)cn);
-            }
+            if (cb | cn) mid_red(a, a.rmid[xu ? 1 : 0], mW[i] & kMask, ob + (mW[i] & kMask), cb, cn);
           }
           __syncthreads();
         }
@@ -1275,6 +1278,9 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   ea.pe = (unsigned long long*)g->pe;
   ea.rsafe[0] = per_vertex ? p->rsafe[0] : 0xffffffffu;
   ea.rsafe[1] = per_vertex ? p->rsafe[1] : 0xffffffffu;
+  ea.pm = (unsigned long long*)g->pm;
+  ea.rmid[0] = per_vertex ? p->rmid[0] : 0xffffffffu;
+  ea.rmid[1] = per_vertex ? p->rmid[1] : 0xffffffffu;
   ea.max_mid = std::max<uint32_t>(p->max_mid, 1);
   ea.kwin_cap = kwin_cap;
   ea.rec_stride = (uint32_t)(std::max<uint32_t>(p->max_mid, 1) + p->max_work / kRecMax + 1);
@@ -1303,8 +1309,10 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
     return cuda_status(err, "sparse engine launch");
   }
-  if (per_vertex && (p->rsafe[0] != 0xffffffffu || p->rsafe[1] != 0xffffffffu) && g->n) {
-    k_merge_pe<<<(g->n + 255) / 256, 256, 0, st>>>((unsigned long long*)g->pe, (unsigned long long*)g->pv, g->n);
+  if (per_vertex && (p->rsafe[0] != 0xffffffffu || p->rsafe[1] != 0xffffffffu || p->rmid[0] != 0xffffffffu ||
+                     p->rmid[1] != 0xffffffffu) && g->n) {
+    k_merge_pe<<<(g->n + 255) / 256, 256, 0, st>>>((unsigned long long*)g->pe, (unsigned long long*)g->pm,
+                                                  (unsigned long long*)g->pv, g->n);
     g->launches++;
   }
   unsigned long long h[16];

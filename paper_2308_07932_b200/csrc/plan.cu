@@ -62,13 +62,19 @@ __global__ void k_end_bound(const uint32_t* __restrict__ off, const uint32_t* __
 
 // rsafe[side] = 1 + the largest local rank of an end whose end-role totals could reach 2^32:
 // sum_x C(c_xw, 2) <= min(C(W, 2), W * (deg(w) - 1) / 2) with W = the wedges ending at w
+// rmid[side] likewise for the middle role: a middle's totals are at most (wedges through it) x
+// (the largest pair count c_xw) <= C(deg, 2) x (the largest degree on the other side)
 __global__ void k_rsafe(const unsigned long long* __restrict__ win, const uint32_t* __restrict__ degs, uint32_t n_u,
                         uint32_t n, uint32_t* __restrict__ rsafe) {
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const unsigned long long W = win[r], d = degs[r];
   const bool safe = W <= 92681ull || W * d < (1ull << 33);
-  if (!safe) atomicMax(&rsafe[r < n_u ? 0 : 1], (r < n_u ? r : r - n_u) + 1u);
+  const uint32_t side = r < n_u ? 0 : 1, lr = r < n_u ? r : r - n_u;
+  if (!safe) atomicMax(&rsafe[side], lr + 1u);
+  const unsigned long long dmax = n_u < n ? degs[side ? 0 : n_u] : 0ull;  // other side's rank 0
+  const unsigned long long pairs = d * (d - (d ? 1ull : 0ull)) / 2ull;
+  if (d > 1 && (pairs >= (1ull << 32) || pairs * dmax >= (1ull << 32))) atomicMax(&rsafe[2 + side], lr + 1u);
 }
 
 // one thread per adjacency entry: if the entry is a middle of its row for this route, compute
@@ -273,18 +279,21 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     k_row_work<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, len, sb, se, p->work);
     g->launches += 2;
   }
-  p->rsafe[0] = p->rsafe[1] = 0xffffffffu;  // no packing (route S, or empty graph)
+  p->rsafe[0] = p->rsafe[1] = p->rmid[0] = p->rmid[1] = 0xffffffffu;  // no packing (route S, or empty graph)
   if (route == 0 && m && !getenv("BBF_NO_PACKED_END")) {  // env: test hook (all ends take two REDs)
     unsigned long long* win;
     uint32_t* d_rs;
     BBF_CUDA(dmalloc(&win, 8ull * (n + 1), st));
-    BBF_CUDA(dmalloc(&d_rs, 8, st));
+    BBF_CUDA(dmalloc(&d_rs, 16, st));
     BBF_CUDA(cudaMemsetAsync(win, 0, 8ull * (n + 1), st));
-    BBF_CUDA(cudaMemsetAsync(d_rs, 0, 8, st));
+    BBF_CUDA(cudaMemsetAsync(d_rs, 0, 16, st));
     k_end_bound<<<grid_for(m, 256), 256, 0, st>>>(g->off, g->adj, g->rev, g->erow, g->mid, g->n_u, m, win);
     k_rsafe<<<(n + 255) / 256, 256, 0, st>>>(win, g->degs, g->n_u, n, d_rs);
     g->launches += 2;
-    BBF_CUDA(cudaMemcpyAsync(p->rsafe, d_rs, 8, cudaMemcpyDeviceToHost, st));
+    uint32_t h_rs[4];
+    BBF_CUDA(cudaMemcpyAsync(h_rs, d_rs, 16, cudaMemcpyDeviceToHost, st));
+    BBF_CUDA(cudaStreamSynchronize(st));
+    p->rsafe[0] = h_rs[0]; p->rsafe[1] = h_rs[1]; p->rmid[0] = h_rs[2]; p->rmid[1] = h_rs[3];
     dfree(win, st);
     dfree(d_rs, st);
   }
