@@ -701,15 +701,14 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
               const uint32_t base = base0 + 32 * u;
+              // records start at distinct chunks, in lane order: my owner = the records started
+              // before this step + those starting at or before my chunk in it, minus one
               const bool st = nch > 0 && excl >= base && excl < base + 32;
-              if (st) sh_own[warp][excl - base] = (uint8_t)lane;
               smask[u] = __reduce_or_sync(0xffffffffu, st ? 1u << (excl - base) : 0u);
-              __syncwarp();
               const uint32_t m = smask[u] & (0xffffffffu >> (31 - lane));
               gs[u] = m ? 31 - __clz(m) : 0;  // first lane of my owner's group in this step
-              ow[u] = m ? (uint32_t)sh_own[warp][gs[u]] : (uint32_t)carry;
-              __syncwarp();
-              carry = __shfl_sync(0xffffffffu, (int)ow[u], 31);
+              ow[u] = (uint32_t)(carry + __popc(m) - 1);
+              carry += __popc(smask[u]);
               const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, ow[u]);
               o_p[u] = __shfl_sync(0xffffffffu, rc.p, ow[u]);
               o_len[u] = __shfl_sync(0xffffffffu, rc.len, ow[u]);
