@@ -171,7 +171,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define T3_MARK(slot) do {} while (0)
 #endif
 #ifndef BBF_T3_KU
-#define BBF_T3_KU 1
+#define BBF_T3_KU 2
 #endif
 constexpr int kU = BBF_T3_KU;  // flattened steps per iteration of the hub kernel's record loop
 #ifndef BBF_T3_CE
