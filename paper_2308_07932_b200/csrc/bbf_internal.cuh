@@ -242,6 +242,7 @@ struct bbf_graph {
   bbf::Zones zones[2];
   uint32_t* adjc;     // 2*nnz counter addresses of the end vertex (+ sign bit), see encode_caddr
   uint32_t* runid;    // 2*nnz: index of the window run containing the entry
+  uint32_t* rlast;    // n: run index of each row's last entry before end1 (hub pre-scan)
   uint2* runs;        // nruns: {first entry, window id} of every maximal same-window run of a row
   uint32_t nruns;
   bool compact;       // adjc uses encode_caddr_compact (else encode_caddr + sign bit)

@@ -42,6 +42,7 @@ struct EngineArgs {
   const uint32_t* adj;
   const uint32_t* adjc;
   const uint32_t* runid;
+  const uint32_t* rlast;   // run index of each row's last entry before end1
   const uint2* runs;
   uint32_t nruns;
   const uint32_t* mid;   // route G middle start; nullptr for route S (off used)
@@ -510,12 +511,13 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       bt = __shfl_sync(0xffffffffu, bt, 0);
       if (bt * 32 >= m) break;
       const uint32_t i = bt * 32 + lane;
-      uint32_t wv = 0, s = 0, en = 0;
+      uint32_t wv = 0, s = 0, en = 0, rl = 0;
       if (i < m) {
         const uint32_t e = m_lo + i;
         wv = a.adj[e];
         s = a.ub[e];
         en = a.end1[ob + (wv & kMask)];
+        rl = a.rlast[ob + (wv & kMask)];  // same level as end1: no dependent runid[en - 1] load
         if (split_lo && s < en) {
           uint32_t b = s, f = en;
           while (b < f) {
@@ -535,7 +537,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       }
       // records of this middle = the graph's window runs of row v clipped to [s, en)
       const uint32_t r0 = s < en ? a.runid[s] : 0;
-      const uint32_t nr = s < en ? a.runid[en - 1] - r0 + 1 : 0;
+      const uint32_t nr = s < en ? (split_hi ? a.runid[en - 1] : rl) - r0 + 1 : 0;
       const uint32_t incl = warp_incl_scan(nr, lane), excl = incl - nr;
       const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
       const uint32_t nz = __ballot_sync(0xffffffffu, nr > 0);
@@ -1268,6 +1270,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   BBF_CUDA(cudaMemsetAsync(g->d_acc, 0, 32 * sizeof(unsigned long long), st));
   EngineArgs ea{};
   ea.off = g->off; ea.adj = g->adj; ea.adjc = g->adjc; ea.runid = g->runid; ea.runs = g->runs;
+  ea.rlast = g->rlast;
   ea.nruns = g->nruns; ea.mid = p->route == 0 ? g->mid : nullptr; ea.end1 = g->end1;
   ea.ub = p->ub; ea.work = p->work; ea.inv = g->inv; ea.t1 = p->t1; ea.t2 = p->t2; ea.units = p->units;
   ea.n_t1 = p->n_t1; ea.n_t2 = p->n_t2; ea.n_units = p->n_units; ea.n_u = g->n_u; ea.n = g->n;

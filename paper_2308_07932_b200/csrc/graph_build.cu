@@ -256,6 +256,12 @@ __global__ void k_row_starts(const uint32_t* __restrict__ off, uint32_t n, uint3
 }
 
 // entry e starts a run if it starts its row (flag preset) or its window differs from e-1's
+__global__ void k_rlast(const uint32_t* __restrict__ off, const uint32_t* __restrict__ end1,
+                        const uint32_t* __restrict__ runid, uint32_t n, uint32_t* __restrict__ rlast) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < n) rlast[x] = end1[x] > off[x] ? runid[end1[x] - 1] : 0u;
+}
+
 __global__ void k_run_flags(const uint32_t* __restrict__ adjc, uint64_t m, uint32_t wshift, uint32_t wmask,
                             uint32_t* __restrict__ flag) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
@@ -677,11 +683,15 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     BBF_CUDA(cudaStreamSynchronize(st));
     BBF_CUDA(dmalloc(&g->runs, sizeof(uint2) * (g->nruns + 1), st));
     k_runs<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, flag, m, wshift, wmask, g->runid, g->runs);
-    g->launches += 6;
+    BBF_CUDA(dmalloc(&g->rlast, 4ull * (n + 1), st));
+    if (n) k_rlast<<<(n + 255) / 256, 256, 0, st>>>(g->off, g->end1, g->runid, n, g->rlast);
+    g->launches += 7;
     dfree(tmp2, st);
     dfree(flag, st);
   } else {
     BBF_CUDA(dmalloc(&g->runs, sizeof(uint2), st));
+    BBF_CUDA(dmalloc(&g->rlast, 4ull * (n + 1), st));
+    BBF_CUDA(cudaMemsetAsync(g->rlast, 0, 4ull * (n + 1), st));
   }
   BBF_CUDA(cudaGetLastError());
   g->adj_built = true;
