@@ -332,33 +332,51 @@ __device__ __forceinline__ void t3_share_cp(uint32_t cbase, uint32_t ev, uint32_
   nn += cp_field(v, ev, oshamt, h);
 }
 
-// Lemma 2 on one packed counter word (global word gw >= WB[1]); skipped unless some field has
-// a + d >= 2 (SWAR test: a or d >= 2, or a and d both odd).  Fields narrower than 32 bits hold
-// a, d < 2^16, so C(a,2) + C(d,2) and a*d fit 32 bits.
+// Zone of a packed counter word, from zone bounds held in registers for the epilogue (the
+// per-word if-chain on the shared zone table was ~8% of the hub kernel's instructions).
+struct ZoneRegs {
+  uint32_t wb2, wb3, wb4, l0, l1, l2, l3, wb1;
+};
+struct ZoneP {
+  uint32_t h, lfw, lb, wb, hi, lo, end;  // half-field bits, log2 field bits, first rank / word, SWAR masks, zone end
+};
+__device__ __forceinline__ ZoneRegs zone_regs(const Zones& Z) {
+  return ZoneRegs{Z.WB[2], Z.WB[3], Z.WB[4], Z.L[0], Z.L[1], Z.L[2], Z.L[3], Z.WB[1]};
+}
+__device__ __forceinline__ ZoneP zone_of(const ZoneRegs& z, uint32_t gw) {
+  if (gw < z.wb2) return ZoneP{16, 5, z.l0, z.wb1, 0xfffefffeu, 0x00000001u, z.wb2};
+  if (gw < z.wb3) return ZoneP{8, 4, z.l1, z.wb2, 0xfefefefeu, 0x00010001u, z.wb3};
+  if (gw < z.wb4) return ZoneP{4, 3, z.l2, z.wb3, 0xeeeeeeeeu, 0x01010101u, z.wb4};
+  return ZoneP{2, 2, z.l3, z.wb4, 0xaaaaaaaau, 0x11111111u, 0xffffffffu};
+}
+
+// Lemma 2 on one packed counter word gw of zone zp; skipped unless some field has a + d >= 2
+// (SWAR test: a or d >= 2, or a and d both odd).  Fields narrower than 32 bits hold a, d < 2^16,
+// so C(a,2) + C(d,2) and a*d fit 32 bits, and so do their sums over one word's fields.
 template <bool PV, bool PAIRS>
-__device__ __forceinline__ void epi_packed(const EngineArgs& a, const Zones& Z, uint32_t sb, uint32_t rs,
+__device__ __forceinline__ void epi_packed(const EngineArgs& a, const ZoneP& zp, uint32_t sb, uint32_t rs,
                                            uint32_t x, uint32_t gw, uint32_t v, unsigned long long& xB,
                                            unsigned long long& xN) {
-  uint32_t h, lfw, lbase, hi, lo;  // half-field width, log2 field width, first rank, SWAR masks
-  if (gw < Z.WB[2]) { h = 16; lfw = 5; lbase = Z.L[0] + (gw - Z.WB[1]); hi = 0xfffefffeu; lo = 0x00000001u; }
-  else if (gw < Z.WB[3]) { h = 8; lfw = 4; lbase = Z.L[1] + 2 * (gw - Z.WB[2]); hi = 0xfefefefeu; lo = 0x00010001u; }
-  else if (gw < Z.WB[4]) { h = 4; lfw = 3; lbase = Z.L[2] + 4 * (gw - Z.WB[3]); hi = 0xeeeeeeeeu; lo = 0x01010101u; }
-  else { h = 2; lfw = 2; lbase = Z.L[3] + 8 * (gw - Z.WB[4]); hi = 0xaaaaaaaau; lo = 0x11111111u; }
-  uint32_t cm = (v & hi) | (v & (v >> h) & lo);  // non-zero bits only in contributing fields
+  const uint32_t h = zp.h, lfw = zp.lfw;
+  const uint32_t lbase = zp.lb + ((gw - zp.wb) << (5 - lfw));
+  uint32_t cm = (v & zp.hi) | (v & (v >> h) & zp.lo);  // non-zero bits only in contributing fields
   const uint32_t fw = 2 * h, fmask = (1u << h) - 1u;
   const uint32_t fclr = (fw == 32) ? 0xffffffffu : ((1u << fw) - 1u);
+  uint32_t wb = 0, wn = 0;
   while (cm) {
     const uint32_t f = (uint32_t)(__ffs(cm) - 1) >> lfw;  // field index
     cm &= ~(fclr << (f * fw));
     const uint32_t q = v >> (f * fw);
     const uint32_t A = q & fmask, D = (q >> h) & fmask;
     const uint32_t fb = ((A * (A - 1u)) >> 1) + ((D * (D - 1u)) >> 1), fn = A * D;
-    xB += fb;
-    xN += fn;
+    wb += fb;
+    wn += fn;
     const uint32_t wrow = sb + lbase + f;
     if (PV) end_red(a, rs, lbase + f, wrow, fb, fn);  // fb | fn != 0 here
     if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
   }
+  xB += wb;
+  xN += wn;
 }
 
 // Lemma 2 on one 64-bit field (zone 0: a word, d word at global words gw, gw + 1)
@@ -775,6 +793,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       }
 
       // ---------------- epilogue: Lemma 2 per touched end (Alg. 2 lines 15-18), clear the window
+      const ZoneRegs zr = zone_regs(Z);
       if (dense) {
         uint4* c4 = reinterpret_cast<uint4*>(ctr);
         for (uint32_t i4 = tid; i4 < (nwk + 3) / 4; i4 += kT3Threads) {
@@ -786,15 +805,23 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             epi_wide<PV, PAIRS>(a, sb, x, gw, q.x, q.y, xB, xN);
             if (gw + 2 < Z.WB[1]) epi_wide<PV, PAIRS>(a, sb, x, gw + 2, q.z, q.w, xB, xN);
             else {
-              if (q.z) epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw + 2, q.z, xB, xN);
-              if (q.w) epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw + 3, q.w, xB, xN);
+              if (q.z) epi_packed<PV, PAIRS>(a, zone_of(zr, gw + 2), sb, rs, x, gw + 2, q.z, xB, xN);
+              if (q.w) epi_packed<PV, PAIRS>(a, zone_of(zr, gw + 3), sb, rs, x, gw + 3, q.w, xB, xN);
             }
             continue;
           }
-          if (q.x) epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw, q.x, xB, xN);
-          if (q.y) epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw + 1, q.y, xB, xN);
-          if (q.z) epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw + 2, q.z, xB, xN);
-          if (q.w) epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw + 3, q.w, xB, xN);
+          const ZoneP zp = zone_of(zr, gw);
+          if (gw + 3 < zp.end) {  // the four words share a zone (the common case)
+            if (q.x) epi_packed<PV, PAIRS>(a, zp, sb, rs, x, gw, q.x, xB, xN);
+            if (q.y) epi_packed<PV, PAIRS>(a, zp, sb, rs, x, gw + 1, q.y, xB, xN);
+            if (q.z) epi_packed<PV, PAIRS>(a, zp, sb, rs, x, gw + 2, q.z, xB, xN);
+            if (q.w) epi_packed<PV, PAIRS>(a, zp, sb, rs, x, gw + 3, q.w, xB, xN);
+          } else {
+            if (q.x) epi_packed<PV, PAIRS>(a, zp, sb, rs, x, gw, q.x, xB, xN);
+            if (q.y) epi_packed<PV, PAIRS>(a, zone_of(zr, gw + 1), sb, rs, x, gw + 1, q.y, xB, xN);
+            if (q.z) epi_packed<PV, PAIRS>(a, zone_of(zr, gw + 2), sb, rs, x, gw + 2, q.z, xB, xN);
+            if (q.w) epi_packed<PV, PAIRS>(a, zone_of(zr, gw + 3), sb, rs, x, gw + 3, q.w, xB, xN);
+          }
         }
       } else {
         for (uint32_t bw = tid; bw < kBm; bw += kT3Threads) {
@@ -813,7 +840,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
               ctr[wi + 1] = 0;
               epi_wide<PV, PAIRS>(a, sb, x, gw, v, vd, xB, xN);
             } else {
-              epi_packed<PV, PAIRS>(a, Z, sb, rs, x, gw, v, xB, xN);
+              epi_packed<PV, PAIRS>(a, zone_of(zr, gw), sb, rs, x, gw, v, xB, xN);
             }
           }
         }
