@@ -291,6 +291,10 @@ __device__ __forceinline__ void sh_red_add_if(uint32_t addr, uint32_t v, uint32_
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr),
                "r"(v), "r"(on));
 }
+__device__ __forceinline__ void sh_red_or_if(uint32_t addr, uint32_t v, uint32_t on) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(addr),
+               "r"(v), "r"(on));
+}
 __device__ __forceinline__ uint32_t sh_load_if(uint32_t addr, uint32_t on) {
   uint32_t r;
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\tmov.u32 %0, 0;\n\t@p ld.shared.u32 %0, [%1];\n\t}"
@@ -413,6 +417,18 @@ __device__ __forceinline__ void t3_chunk(const uint32_t (&ev)[kCE], uint32_t vm,
       sh_red_add_if(cbase + (ev[j] & kCpAddrMask), 1u << ((ev[j] >> shamt) & 31u), vm & (1u << j));
     return;
   }
+#ifndef BBF_T3_BM_ATOM
+  if (CP && MODE == 1) {  // pass 1 with the touched-word bitmap: fire-and-forget add and bit-or
+    const uint32_t bmbase = (uint32_t)__cvta_generic_to_shared(bm);
+#pragma unroll
+    for (int j = 0; j < (int)kCE; ++j) {
+      const uint32_t on = vm & (1u << j), g = cp_word(ev[j]) - word0;
+      sh_red_add_if(cbase + (ev[j] & kCpAddrMask), 1u << ((ev[j] >> shamt) & 31u), on);
+      sh_red_or_if(bmbase + 4u * (g >> 5), 1u << (g & 31u), on);
+    }
+    return;
+  }
+#endif
   if (CP && MODE == 2) {  // pass 2: predicated loads; sum of own-class counts minus #entries
     uint32_t own = 0, oth = 0;
 #pragma unroll
