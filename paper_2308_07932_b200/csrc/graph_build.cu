@@ -91,17 +91,6 @@ __global__ void k_rank_tables(const uint64_t* __restrict__ skey, uint32_t cnt, u
   lr[id] = l;
 }
 
-__device__ __forceinline__ uint32_t row_of_edge(const uint64_t* __restrict__ rp, uint32_t n_u,
-                                                uint64_t e) {
-  // largest u with rp[u] <= e  (rows may be empty)
-  uint32_t lo = 0, hi = n_u;  // answer in [lo, hi)
-  while (hi - lo > 1) {
-    uint32_t mid = lo + (hi - lo) / 2;
-    if (rp[mid] <= e) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
 // Rank-space adjacency in three stable passes ("Build"):
 //   A  k_entries: each input row u is copied to its rank row lr_u[u] (keys = lr_v[v],
 //      values = lr_u[u] | neg << 31), so the entries are in U-rank-major order;
@@ -118,14 +107,17 @@ __global__ void k_entries(const uint64_t* __restrict__ rp, const uint32_t* __res
                           const uint32_t* __restrict__ lr_u, const uint32_t* __restrict__ lr_v,
                           const uint32_t* __restrict__ off, uint32_t* __restrict__ key,
                           uint32_t* __restrict__ val) {
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t u = row_of_edge(rp, n_u, e);
-    const uint32_t neg = sg[e] ? 0u : kNegBit;  // weight 0 = negative
+  // one warp per input row (no per-edge row search)
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n_u; u += (gridDim.x * blockDim.x) >> 5) {
+    const uint64_t b = rp[u], e1 = rp[u + 1];
     const uint32_t a = lr_u[u];
-    const uint64_t dst = off[a] + (e - rp[u]);
-    key[dst] = lr_v[col[e]];
-    val[dst] = a | neg;
+    const uint64_t d0 = off[a];
+    for (uint64_t e = b + lane; e < e1; e += 32) {
+      const uint32_t neg = sg[e] ? 0u : kNegBit;  // weight 0 = negative
+      key[d0 + (e - b)] = lr_v[col[e]];
+      val[d0 + (e - b)] = a | neg;
+    }
   }
 }
 
@@ -239,37 +231,32 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint32_t n, uint64_
 }
 
 // counter address of each entry's end vertex (entries [0, nnz) are U rows -> V ends)
-__global__ void k_caddr(const uint32_t* __restrict__ adj, uint64_t m, uint64_t nnz, Zones zu, Zones zv,
-                        bool compact, uint32_t* __restrict__ adjc) {
+// counter address of each entry's end, and the window-run start flags: an entry starts a run if
+// it starts its row or its counter window differs from the previous entry's
+__device__ __forceinline__ uint32_t caddr_of(uint32_t w, const Zones& z, bool compact) {
+  return compact ? encode_caddr_compact(z, w & kMask, w >> 31) : encode_caddr(z, w & kMask) | (w & kNegBit);
+}
+__global__ void k_caddr(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ erow, uint64_t m,
+                        uint64_t nnz, Zones zu, Zones zv, bool compact, uint32_t wshift, uint32_t wmask,
+                        uint32_t* __restrict__ adjc, uint32_t* __restrict__ flag) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
        e += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t w = adj[e];
     const Zones& z = e < nnz ? zv : zu;
-    adjc[e] = compact ? encode_caddr_compact(z, w & kMask, w >> 31)
-                      : encode_caddr(z, w & kMask) | (w & kNegBit);
+    const uint32_t c = caddr_of(adj[e], z, compact);
+    adjc[e] = c;
+    uint32_t f = 1u;
+    if (e > 0 && erow[e] == erow[e - 1]) {
+      const uint32_t cp = caddr_of(adj[e - 1], z, compact);
+      f = ((c >> wshift) & wmask) / kWin != ((cp >> wshift) & wmask) / kWin ? 1u : 0u;
+    }
+    flag[e] = f;
   }
 }
 
-__global__ void k_row_starts(const uint32_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ flag) {
-  uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x < n && off[x + 1] > off[x]) flag[off[x]] = 1u;
-}
-
-// entry e starts a run if it starts its row (flag preset) or its window differs from e-1's
 __global__ void k_rlast(const uint32_t* __restrict__ off, const uint32_t* __restrict__ end1,
                         const uint32_t* __restrict__ runid, uint32_t n, uint32_t* __restrict__ rlast) {
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x < n) rlast[x] = end1[x] > off[x] ? runid[end1[x] - 1] : 0u;
-}
-
-__global__ void k_run_flags(const uint32_t* __restrict__ adjc, uint64_t m, uint32_t wshift, uint32_t wmask,
-                            uint32_t* __restrict__ flag) {
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    if (flag[e]) continue;
-    uint32_t k = ((adjc[e] >> wshift) & wmask) / kWin, kp = ((adjc[e - 1] >> wshift) & wmask) / kWin;
-    flag[e] = k != kp ? 1u : 0u;
-  }
 }
 
 __global__ void k_runs(const uint32_t* __restrict__ adjc, const uint32_t* __restrict__ flag,
@@ -619,7 +606,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     BBF_CUDA(dmalloc(&kb, 4ull * nnz, st));
     BBF_CUDA(dmalloc(&wa, 8ull * nnz, st));
     BBF_CUDA(dmalloc(&wb, 8ull * nnz, st));
-    k_entries<<<grid_for(nnz, 256), 256, 0, st>>>(d_rp, d_col, d_sg, nnz, n_u, lr_u, lr_v, g->off, ka, va);
+    k_entries<<<grid_for(32ull * n_u, 256), 256, 0, st>>>(d_rp, d_col, d_sg, nnz, n_u, lr_u, lr_v, g->off, ka, va);
     BBF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t3, ka, kb, va, g->adj + nnz, (int)nnz, 0, bits_v, st));
     k_transpose_keys<<<grid_for(nnz, 256), 256, 0, st>>>(kb, g->adj + nnz, nnz, n_u, g->erow + nnz, ka, wa);
     BBF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t3, ka, g->erow, wa, wb, (int)nnz, 0, bits_u, st));
@@ -669,11 +656,8 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
   if (m) {
     uint32_t* flag;
     BBF_CUDA(dmalloc(&flag, 4ull * (m + 1), st));
-    BBF_CUDA(cudaMemsetAsync(flag, 0, 4ull * (m + 1), st));
-    k_caddr<<<grid_for(m, 256), 256, 0, st>>>(g->adj, m, nnz, g->zones[0], g->zones[1], g->compact,
-                                            g->adjc);
-    k_row_starts<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(g->off, n, flag);
-    k_run_flags<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, m, wshift, wmask, flag);
+    k_caddr<<<grid_for(m, 256), 256, 0, st>>>(g->adj, g->erow, m, nnz, g->zones[0], g->zones[1], g->compact,
+                                            wshift, wmask, g->adjc, flag);
     size_t ts = 0;
     cub::DeviceScan::InclusiveSum(nullptr, ts, flag, g->runid, (int64_t)m, st);
     void* tmp2;
@@ -685,7 +669,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     k_runs<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, flag, m, wshift, wmask, g->runid, g->runs);
     BBF_CUDA(dmalloc(&g->rlast, 4ull * (n + 1), st));
     if (n) k_rlast<<<(n + 255) / 256, 256, 0, st>>>(g->off, g->end1, g->runid, n, g->rlast);
-    g->launches += 7;
+    g->launches += 5;
     dfree(tmp2, st);
     dfree(flag, st);
   } else {

@@ -27,39 +27,6 @@ struct RouteRows {
   }
 };
 
-// Upper bound of the wedges that END at each vertex w (route G): for the entry (w -> v) the
-// eligible starts x are v's neighbours before both w (higher priority than w: rev[e] - off[v]
-// entries) and v itself (mid[v] - off[v]).  Consecutive entries of a warp share rows, so the
-// per-row sums are reduced over runs of equal rows before one atomic per run.
-__global__ void k_end_bound(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
-                            const uint32_t* __restrict__ rev, const uint32_t* __restrict__ erow,
-                            const uint32_t* __restrict__ mid, uint32_t n_u, uint64_t m,
-                            unsigned long long* __restrict__ win) {
-  const uint32_t lane = threadIdx.x & 31;
-  for (uint64_t e0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; e0 < m;
-       e0 += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t e = e0 + lane;
-    uint32_t w = 0xffffffffu;
-    unsigned long long c = 0;
-    if (e < m) {
-      w = erow[e];
-      const uint32_t v = (w < n_u ? n_u : 0u) + (adj[e] & kMask);
-      const uint32_t pos = rev[e] - off[v], hi = mid[v] - off[v];
-      c = pos < hi ? pos : hi;
-    }
-    const uint32_t wp = __shfl_up_sync(0xffffffffu, w, 1);
-    const uint32_t starts = __ballot_sync(0xffffffffu, lane == 0 || wp != w);
-    for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive scan by row
-      const unsigned long long t = __shfl_up_sync(0xffffffffu, c, o);
-      const uint32_t seg = starts & (0xffffffffu >> (31 - lane));
-      const int gs = 31 - __clz(seg);
-      if ((int)lane - o >= gs) c += t;
-    }
-    const bool last = lane == 31 || ((starts >> (lane + 1)) & 1u);
-    if (last && w != 0xffffffffu && c) atomicAdd(&win[w], c);
-  }
-}
-
 // rsafe[side] = 1 + the largest local rank of an end whose end-role totals could reach 2^32:
 // sum_x C(c_xw, 2) <= min(C(W, 2), W * (deg(w) - 1) / 2) with W = the wedges ending at w
 // rmid[side] likewise for the middle role: a middle's totals are at most (wedges through it) x
@@ -79,31 +46,55 @@ __global__ void k_rsafe(const unsigned long long* __restrict__ win, const uint32
 
 // one thread per adjacency entry: if the entry is a middle of its row for this route, compute
 // ub, the pruned segment length (ends of degree >= 2) and the full count (all ends; W_G)
+// (win != nullptr, route G) also the per-end bound of incoming wedges (see make_plan): the same entry's
+// middle and reverse position give the eligible starts before it (one pass over erow/adj/rev)
 __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
                                const uint32_t* __restrict__ adj, const uint32_t* __restrict__ rev,
                                const uint32_t* __restrict__ erow,
                                const uint32_t* __restrict__ mid,
                                const uint32_t* __restrict__ end1, uint64_t m,
                                uint32_t* __restrict__ ub, uint64_t* __restrict__ len,
-                               unsigned long long* __restrict__ w_full) {
+                               unsigned long long* __restrict__ w_full, unsigned long long* __restrict__ win) {
   unsigned long long full = 0;
-  for (uint64_t e64 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e64 < m;
-       e64 += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t e = (uint32_t)e64;
-    uint32_t x = erow[e];
-    uint32_t lo = rr.route == 0 ? mid[x] : off[x];
-    uint64_t l_seg = 0;
-    if (rr.in_route(x) && e >= lo && e < end1[x]) {
-      uint32_t ob = x < rr.n_u ? rr.n_u : 0;
-      uint32_t rv = ob + (adj[e] & kMask);
-      uint32_t f = off[rv + 1];
-      uint32_t u = rev[e] + 1;  // x's entry in its middle's row is the reverse entry
-      uint32_t en = end1[rv];
-      ub[e] = u;
-      full += f - u;
-      l_seg = en > u ? en - u : 0;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t e0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; e0 < m;
+       e0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e64 = e0 + lane;
+    uint32_t x = 0xffffffffu;
+    unsigned long long c = 0;
+    if (e64 < m) {
+      const uint32_t e = (uint32_t)e64;
+      x = erow[e];
+      const uint32_t ob = x < rr.n_u ? rr.n_u : 0;
+      const uint32_t rv = ob + (adj[e] & kMask);
+      const uint32_t r = rev[e];
+      const uint32_t lo = rr.route == 0 ? mid[x] : off[x];
+      uint64_t l_seg = 0;
+      if (rr.in_route(x) && e >= lo && e < end1[x]) {
+        const uint32_t f = off[rv + 1];
+        const uint32_t u = r + 1;  // x's entry in its middle's row is the reverse entry
+        const uint32_t en = end1[rv];
+        ub[e] = u;
+        full += f - u;
+        l_seg = en > u ? en - u : 0;
+      }
+      len[e] = l_seg;
+      if (win) {
+        const uint32_t o = off[rv], pos = r - o, hi = mid[rv] - o;
+        c = pos < hi ? pos : hi;
+      }
     }
-    len[e] = l_seg;
+    if (win) {  // segmented sum over runs of equal rows, one atomic per run
+      const uint32_t xp = __shfl_up_sync(0xffffffffu, x, 1);
+      const uint32_t starts = __ballot_sync(0xffffffffu, lane == 0 || xp != x);
+      const int gs = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, c, o);
+        if ((int)lane - o >= gs) c += t;
+      }
+      const bool last = lane == 31 || ((starts >> (lane + 1)) & 1u);
+      if (last && x != 0xffffffffu && c) atomicAdd(&win[x], c);
+    }
   }
   for (int o = 16; o; o >>= 1) full += __shfl_xor_sync(0xffffffffu, full, o);
   if ((threadIdx.x & 31) == 0 && full) atomicAdd(w_full, full);
@@ -259,9 +250,18 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   BBF_CUDA(dmalloc(&acc, 8 * sizeof(unsigned long long), st));
   BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
   BBF_CUDA(cudaMemsetAsync(p->work, 0, 8ull * (n + 1), st));
+  // per-end bound of incoming wedges (route G, per-vertex REDs packing):
+  // the wedges ending at w from starts before both w and the middle v, per entry (w -> v):
+  // min(position of w in N(v), mid(v) - off(v))
+  const bool want_pack = route == 0 && m && !getenv("BBF_NO_PACKED_END");  // env: test hook
+  unsigned long long* win = nullptr;
+  if (want_pack) {
+    BBF_CUDA(dmalloc(&win, 8ull * (n + 1), st));
+    BBF_CUDA(cudaMemsetAsync(win, 0, 8ull * (n + 1), st));
+  }
   if (m) {
     k_plan_entries<<<grid_for(m, 256), 256, 0, st>>>(rr, g->off, g->adj, g->rev, g->erow, g->mid, g->end1, m, p->ub,
-                                                   len, &acc[0]);
+                                                   len, &acc[0], win);
     g->launches += 1;
   }
   if (n) {
@@ -280,16 +280,12 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     g->launches += 2;
   }
   p->rsafe[0] = p->rsafe[1] = p->rmid[0] = p->rmid[1] = 0xffffffffu;  // no packing (route S, or empty graph)
-  if (route == 0 && m && !getenv("BBF_NO_PACKED_END")) {  // env: test hook (all ends take two REDs)
-    unsigned long long* win;
+  if (want_pack) {  // (env BBF_NO_PACKED_END: every end / middle takes two REDs)
     uint32_t* d_rs;
-    BBF_CUDA(dmalloc(&win, 8ull * (n + 1), st));
     BBF_CUDA(dmalloc(&d_rs, 16, st));
-    BBF_CUDA(cudaMemsetAsync(win, 0, 8ull * (n + 1), st));
     BBF_CUDA(cudaMemsetAsync(d_rs, 0, 16, st));
-    k_end_bound<<<grid_for(m, 256), 256, 0, st>>>(g->off, g->adj, g->rev, g->erow, g->mid, g->n_u, m, win);
     k_rsafe<<<(n + 255) / 256, 256, 0, st>>>(win, g->degs, g->n_u, n, d_rs);
-    g->launches += 2;
+    g->launches += 1;
     uint32_t h_rs[4];
     BBF_CUDA(cudaMemcpyAsync(h_rs, d_rs, 16, cudaMemcpyDeviceToHost, st));
     BBF_CUDA(cudaStreamSynchronize(st));
