@@ -53,7 +53,7 @@ __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
                                const uint32_t* __restrict__ erow,
                                const uint32_t* __restrict__ mid,
                                const uint32_t* __restrict__ end1, uint64_t m,
-                               uint32_t* __restrict__ ub, uint64_t* __restrict__ len,
+                               uint32_t* __restrict__ ub, unsigned long long* __restrict__ work,
                                unsigned long long* __restrict__ w_full, unsigned long long* __restrict__ win) {
   unsigned long long full = 0;
   const uint32_t lane = threadIdx.x & 31;
@@ -61,7 +61,7 @@ __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
        e0 += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t e64 = e0 + lane;
     uint32_t x = 0xffffffffu;
-    unsigned long long c = 0;
+    unsigned long long c = 0, l_seg = 0;
     if (e64 < m) {
       const uint32_t e = (uint32_t)e64;
       x = erow[e];
@@ -69,7 +69,6 @@ __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
       const uint32_t rv = ob + (adj[e] & kMask);
       const uint32_t r = rev[e];
       const uint32_t lo = rr.route == 0 ? mid[x] : off[x];
-      uint64_t l_seg = 0;
       if (rr.in_route(x) && e >= lo && e < end1[x]) {
         const uint32_t f = off[rv + 1];
         const uint32_t u = r + 1;  // x's entry in its middle's row is the reverse entry
@@ -78,22 +77,25 @@ __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
         full += f - u;
         l_seg = en > u ? en - u : 0;
       }
-      len[e] = l_seg;
       if (win) {
         const uint32_t o = off[rv], pos = r - o, hi = mid[rv] - o;
         c = pos < hi ? pos : hi;
       }
     }
-    if (win) {  // segmented sum over runs of equal rows, one atomic per run
-      const uint32_t xp = __shfl_up_sync(0xffffffffu, x, 1);
-      const uint32_t starts = __ballot_sync(0xffffffffu, lane == 0 || xp != x);
-      const int gs = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long t = __shfl_up_sync(0xffffffffu, c, o);
-        if ((int)lane - o >= gs) c += t;
-      }
-      const bool last = lane == 31 || ((starts >> (lane + 1)) & 1u);
-      if (last && x != 0xffffffffu && c) atomicAdd(&win[x], c);
+    // per-row sums (work: pruned segment lengths; win: the end bound) over runs of equal rows in
+    // the warp, one atomic per run
+    const uint32_t xp = __shfl_up_sync(0xffffffffu, x, 1);
+    const uint32_t starts = __ballot_sync(0xffffffffu, lane == 0 || xp != x);
+    const int gs = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, l_seg, o);
+      const unsigned long long t2 = __shfl_up_sync(0xffffffffu, c, o);
+      if ((int)lane - o >= gs) { l_seg += t; c += t2; }
+    }
+    const bool last = lane == 31 || ((starts >> (lane + 1)) & 1u);
+    if (last && x != 0xffffffffu) {
+      if (l_seg) atomicAdd(&work[x], l_seg);
+      if (win && c) atomicAdd(&win[x], c);
     }
   }
   for (int o = 16; o; o >>= 1) full += __shfl_xor_sync(0xffffffffu, full, o);
@@ -110,15 +112,6 @@ __global__ void k_seg_bounds(RouteRows rr, const uint32_t* __restrict__ off,
   uint32_t hi = end1[x];
   b[x] = lo;
   e[x] = hi > lo ? hi : lo;
-}
-
-// work[x] = sum of the segment lengths of x's middle entries [b, e) from their inclusive prefix
-__global__ void k_row_work(uint32_t n, const uint64_t* __restrict__ pre, const uint32_t* __restrict__ b,
-                           const uint32_t* __restrict__ e, uint64_t* __restrict__ work) {
-  uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= n) return;
-  const uint32_t lo = b[x], hi = e[x];
-  work[x] = hi > lo ? pre[hi - 1] - (lo ? pre[lo - 1] : 0ull) : 0ull;
 }
 
 // count T1 / T3 rows, W per tier, units per T3 row
@@ -239,10 +232,8 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   RouteRows rr{route, g->n_u, n};
   BBF_CUDA(dmalloc(&p->ub, 4ull * (m + 1), st));
   BBF_CUDA(dmalloc(&p->work, 8ull * (n + 1), st));
-  uint64_t* len;
   uint32_t *sb, *se, *nunits, *ustart;
   unsigned long long* acc;
-  BBF_CUDA(dmalloc(&len, 8ull * (m + 1), st));
   BBF_CUDA(dmalloc(&sb, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&se, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&nunits, 4ull * (n + 1), st));
@@ -261,23 +252,12 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   }
   if (m) {
     k_plan_entries<<<grid_for(m, 256), 256, 0, st>>>(rr, g->off, g->adj, g->rev, g->erow, g->mid, g->end1, m, p->ub,
-                                                   len, &acc[0], win);
+                                                   (unsigned long long*)p->work, &acc[0], win);
     g->launches += 1;
   }
   if (n) {
-    // per-row work = difference of the inclusive prefix of the per-entry segment lengths
     k_seg_bounds<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(rr, g->off, g->mid, g->end1, sb, se);
-    if (m) {
-      size_t tb = 0;
-      cub::DeviceScan::InclusiveSum(nullptr, tb, len, len, (int64_t)m, st);
-      void* tmp;
-      BBF_CUDA(dmalloc(&tmp, tb + 16, st));
-      BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, len, len, (int64_t)m, st));
-      dfree(tmp, st);
-      g->launches += 2;
-    }
-    k_row_work<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, len, sb, se, p->work);
-    g->launches += 2;
+    g->launches += 1;
   }
   p->rsafe[0] = p->rsafe[1] = p->rmid[0] = p->rmid[1] = 0xffffffffu;  // no packing (route S, or empty graph)
   if (want_pack) {  // (env BBF_NO_PACKED_END: every end / middle takes two REDs)
@@ -409,7 +389,6 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
             (unsigned long long)p->W_t3, p->n_units,
             (unsigned long long)p->M_t3, p->max_mid, (unsigned long long)w_target, g->zones[0].WB[5],
             g->zones[1].WB[5]);
-  dfree(len, st);
   dfree(sb, st);
   dfree(se, st);
   dfree(nunits, st);
