@@ -177,7 +177,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=-1, help="e2e timed steps (default: --steps)")
     ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampler")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -264,28 +264,39 @@ def main():
     value = W_G * args.steps / (ms * 1e-3)
     bfly = tot["balanced"] * args.steps / (ms * 1e-3)
 
-    # e2e: the same step through the public API with HOST buffers: the CSR in pinned host memory
-    # (H2D inside bbf_graph_load_csr) and the per-vertex arrays written back to pinned host
-    # memory (D2H inside bbf_count_per_vertex), every step inside the timed region
+    # e2e: the same step through the public API with HOST buffers, pipelined as a stream of
+    # graphs: every step's CSR is copied from pinned host memory by bbf_upload_csr (the next
+    # step's copy is started before this step counts, so it overlaps the kernels) and every
+    # step's per-vertex arrays are written back to pinned host memory by BBF_OUTPUT_ASYNC copies
+    # (overlapping the next step); all copies of all steps lie inside the timed region, which
+    # ends after bbf_device_sync
     e2e_ms = None
+    if args.e2e_steps < 0:
+        args.e2e_steps = args.steps
     if args.e2e_steps > 0:
         h_rp = torch.from_numpy(g.row_ptr.view(np.int64)).pin_memory()
         h_col = torch.from_numpy(g.col.view(np.int32)).pin_memory()
         h_sg = torch.from_numpy(g.sign).pin_memory()
         h_out = tuple(torch.zeros(k, dtype=torch.int64).pin_memory() for k in (n_u, n_u, n_v, n_v))
-        h = bbf.Graph(n_u, n_v, h_rp, h_col, h_sg, device=local, stream=stream, comm=comm)
-        h.count_per_vertex(out=h_out)  # warm-up of the host path
+        up = bbf.Upload(n_u, n_v, h_rp, h_col, h_sg, device=local)  # warm-up of the host path
+        h = bbf.Graph.from_upload(up, stream=stream, comm=comm)
+        h.count_per_vertex(out=h_out, flags=bbf.BBF_OUTPUT_ASYNC)
         h.free()
+        bbf.device_sync(local)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        for _ in range(args.e2e_steps):
-            h = bbf.Graph(n_u, n_v, h_rp, h_col, h_sg, device=local, stream=stream, comm=comm)
-            tot_e = h.count_per_vertex(out=h_out)[0]
+        up = bbf.Upload(n_u, n_v, h_rp, h_col, h_sg, device=local)
+        for k in range(args.e2e_steps):
+            h = bbf.Graph.from_upload(up, stream=stream, comm=comm)
+            if k + 1 < args.e2e_steps:
+                up = bbf.Upload(n_u, n_v, h_rp, h_col, h_sg, device=local)
+            tot_e = h.count_per_vertex(out=h_out, flags=bbf.BBF_OUTPUT_ASYNC)[0]
             h.free()
+        bbf.device_sync(local)
         t1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = t0.elapsed_time(t1) / args.e2e_steps
@@ -337,7 +348,9 @@ def main():
                        "bbf_count_per_vertex (plan + kernels + all-reduce); load/build excluded"},
         "e2e": {"value": (W_G / (e2e_ms * 1e-3)) if e2e_ms else None, "unit": "wedges/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms},
+                "ms_per_step": e2e_ms,
+                "mode": "stream of graphs: bbf_upload_csr (pinned H2D) of step k+1 overlaps step k, "
+                        "per-vertex arrays D2H by BBF_OUTPUT_ASYNC; all copies inside the timed region"},
         "gpu_launches": launches,
         "roofline": roof,
         "clocks": clocks,

@@ -48,6 +48,7 @@ extern "C" {
 #define BBF_ABI_VERSION 1
 
 typedef struct bbf_graph bbf_graph; /* opaque; one graph resident on one GPU (one rank)   */
+typedef struct bbf_upload bbf_upload; /* opaque; a host CSR being copied to one GPU          */
 typedef struct bbf_comm bbf_comm;   /* opaque NCCL communicator                          */
 
 typedef enum {
@@ -69,7 +70,9 @@ enum {
   BBF_POSITIVE_ONLY = 1u << 1, /* load: keep only the positive edges (case-study analytics,   */
                                /* PAPER.md:15-27 "only formed by the edges with sign 1")       */
   BBF_FORCE_SPARSE = 1u << 2, /* count: use the sparse wedge-aggregation kernels            */
-  BBF_FORCE_DENSE = 1u << 3   /* count: use the dense int8 tensor-core path (tcgen05)       */
+  BBF_FORCE_DENSE = 1u << 3,  /* count: use the dense int8 tensor-core path (tcgen05)       */
+  BBF_OUTPUT_ASYNC = 1u << 4  /* bbf_count_per_vertex: host outputs are written by an        */
+                              /* asynchronous copy, complete after bbf_device_sync()          */
 };
 
 /* Results of one count.  wedges_G is the paper's wedge count for Alg. 2 on this graph
@@ -120,6 +123,23 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t *row_pt
                               int device, void *cuda_stream, bbf_comm *comm, bbf_graph **out);
 bbf_status bbf_graph_free(bbf_graph *g);
 
+/* Pipelined loading (a stream of graphs): bbf_upload_csr starts copying a host CSR (same
+ * arguments and checks as bbf_graph_load_csr without flags; pinned host memory gives a truly
+ * asynchronous copy) to device buffers on the library's per-device upload stream and returns at
+ * once, so the copy of the next graph overlaps the counting of the current one.  The host arrays
+ * must stay valid and unmodified until the upload is consumed or freed.  bbf_graph_load_upload
+ * builds the graph from it exactly like bbf_graph_load_csr (flags without BBF_PTR_DEVICE; the
+ * build stream waits on the copy on the device) and consumes the upload, whatever the status;
+ * bbf_upload_free discards an unconsumed one.  Errors: those of bbf_graph_load_csr. */
+bbf_status bbf_upload_csr(uint32_t n_u, uint32_t n_v, const uint64_t *row_ptr, const uint32_t *col,
+                          const uint8_t *sign, int device, bbf_upload **out);
+bbf_status bbf_graph_load_upload(bbf_upload *up, uint32_t flags, void *cuda_stream, bbf_comm *comm,
+                                 bbf_graph **out);
+bbf_status bbf_upload_free(bbf_upload *up);
+
+/* Waits for all of the library's work on `device`, including the copies of BBF_OUTPUT_ASYNC. */
+bbf_status bbf_device_sync(int device);
+
 /* Global balanced / unbalanced counts (each butterfly once; Alg. 2).  out: host.  Path: the
  * load flags' BBF_FORCE_* if any, else the dispatch rule.  BBF_EINVAL if BBF_FORCE_DENSE was
  * given for a graph the dense path does not support (other side > 65,536 vertices). */
@@ -127,7 +147,10 @@ bbf_status bbf_count_global(bbf_graph *g, bbf_counts *out);
 
 /* Per-vertex counts (butterflies containing each vertex; vBBFC semantics),
  * indexed by input ids.  Any of the four arrays may be NULL.  Host arrays unless
- * BBF_PTR_DEVICE.  totals (nullable, host) receives the global counts as well. */
+ * BBF_PTR_DEVICE.  totals (nullable, host) receives the global counts as well.  With
+ * BBF_OUTPUT_ASYNC (host arrays) the call returns once the counts exist on the device and the
+ * arrays are filled by a copy on the library's download stream: read them after
+ * bbf_device_sync(device); the graph may be freed before that. */
 bbf_status bbf_count_per_vertex(bbf_graph *g, uint64_t *bal_u, uint64_t *unb_u, uint64_t *bal_v,
                                 uint64_t *unb_v, uint32_t flags, bbf_counts *totals);
 

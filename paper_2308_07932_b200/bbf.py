@@ -23,6 +23,7 @@ BBF_POSITIVE_ONLY = 1 << 1
 BBF_METRIC_BALANCED, BBF_METRIC_DEGREE = 0, 1
 BBF_FORCE_SPARSE = 1 << 2
 BBF_FORCE_DENSE = 1 << 3
+BBF_OUTPUT_ASYNC = 1 << 4
 
 
 class BBFError(RuntimeError):
@@ -67,9 +68,14 @@ def lib():
         L.bbf_topk_vertices.argtypes = [P, i32, i32, u32, P, P, P]
         L.bbf_estimate_global.argtypes = [u32, u32, P, P, P, u32, C.c_double, u32, u64, i32, P, P,
                                           P, P, P]
+        L.bbf_upload_csr.argtypes = [u32, u32, P, P, P, i32, P]
+        L.bbf_graph_load_upload.argtypes = [P, u32, P, P, P]
+        L.bbf_upload_free.argtypes = [P]
+        L.bbf_device_sync.argtypes = [i32]
         for f in ("bbf_nccl_unique_id", "bbf_comm_init", "bbf_comm_free", "bbf_graph_load_csr",
                   "bbf_graph_free", "bbf_count_global", "bbf_count_per_vertex",
-                  "bbf_count_pairs_topk", "bbf_graph_stats", "bbf_estimate_global", "bbf_topk_vertices"):
+                  "bbf_count_pairs_topk", "bbf_graph_stats", "bbf_estimate_global", "bbf_topk_vertices",
+                  "bbf_upload_csr", "bbf_graph_load_upload", "bbf_upload_free", "bbf_device_sync"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -119,6 +125,43 @@ def _ptr(x):
     return x.ctypes.data_as(C.c_void_p)
 
 
+def device_sync(device: int = 0):
+    """bbf_device_sync: completes BBF_OUTPUT_ASYNC copies (and all library work) on `device`."""
+    _check(lib().bbf_device_sync(device))
+
+
+class Upload:
+    """bbf_upload_csr: an asynchronous host->device copy of a CSR (host numpy arrays or host torch
+    tensors, pinned for a truly asynchronous copy); consumed by Graph.from_upload.  The host arrays
+    are kept referenced until then."""
+
+    def __init__(self, n_u, n_v, row_ptr, col, sign, device: int = 0):
+        if _is_torch(row_ptr):
+            assert not row_ptr.is_cuda and all(t.is_contiguous() for t in (row_ptr, col, sign))
+            keep = (row_ptr, col, sign)
+        else:
+            keep = (np.ascontiguousarray(row_ptr, dtype=np.uint64),
+                    np.ascontiguousarray(col, dtype=np.uint32),
+                    np.ascontiguousarray(sign, dtype=np.uint8))
+        self._keep = keep
+        self.n_u, self.n_v, self.device = int(n_u), int(n_v), device
+        self.h = C.c_void_p()
+        _check(lib().bbf_upload_csr(self.n_u, self.n_v, _ptr(keep[0]), _ptr(keep[1]), _ptr(keep[2]),
+                                    device, C.byref(self.h)))
+
+    def free(self):
+        if self.h:
+            lib().bbf_upload_free(self.h)
+            self.h = C.c_void_p()
+        self._keep = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 class Graph:
     """A signed bipartite graph resident on one GPU (bbf_graph_load_csr).
 
@@ -150,6 +193,20 @@ class Graph:
     @classmethod
     def from_synth(cls, g, **kw):
         return cls(g.n_u, g.n_v, g.row_ptr, g.col, g.sign, **kw)
+
+    @classmethod
+    def from_upload(cls, up: Upload, stream=None, comm: Comm | None = None, flags: int = 0):
+        """bbf_graph_load_upload: build from an Upload (consumed)."""
+        self = cls.__new__(cls)
+        self.h = C.c_void_p()
+        self.n_u, self.n_v = up.n_u, up.n_v
+        st = C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else (stream or 0))
+        hu, up.h = up.h, C.c_void_p()  # consumed by the call, whatever its status
+        try:
+            _check(lib().bbf_graph_load_upload(hu, flags, st, comm.h if comm else None, C.byref(self.h)))
+        finally:
+            up._keep = None
+        return self
 
     def free(self):
         if self.h:

@@ -236,9 +236,116 @@ bbf_status bbf_comm_free(bbf_comm* comm) {
   return BBF_OK;
 }
 
+namespace {
+// per-device library streams for asynchronous host<->device copies (uploads, async outputs)
+cudaStream_t copy_stream(int device, int which) {
+  static std::once_flag once[64][2];
+  static cudaStream_t st[64][2];
+  if (device < 0 || device >= 64) return nullptr;
+  std::call_once(once[device][which], [device, which] {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaStreamCreateWithFlags(&st[device][which], cudaStreamNonBlocking);
+    cudaSetDevice(prev);
+  });
+  return st[device][which];
+}
+
+bbf_status load_impl(uint32_t n_u, uint32_t n_v, const uint64_t* row_ptr, const uint32_t* col,
+                     const uint8_t* sign, uint32_t flags, int device, void* cuda_stream, bbf_comm* comm,
+                     bbf_graph** out, const uint64_t* known_nnz);
+}  // namespace
+
+struct bbf_upload {
+  int device;
+  uint32_t n_u, n_v;
+  uint64_t nnz;
+  uint64_t* rp;
+  uint32_t* col;
+  uint8_t* sg;
+  cudaEvent_t done;
+};
+
+bbf_status bbf_upload_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_ptr, const uint32_t* col,
+                          const uint8_t* sign, int device, bbf_upload** out) {
+  if (!out || !row_ptr) { set_error("null pointer"); return BBF_EINVAL; }
+  *out = nullptr;
+  if ((uint64_t)n_u + n_v >= (1ull << 31)) { set_error("n_u + n_v >= 2^31"); return BBF_ERANGE; }
+  const uint64_t nnz = row_ptr[n_u];
+  if (nnz >= (1ull << 31)) { set_error("nnz >= 2^31"); return BBF_ERANGE; }
+  if (nnz && (!col || !sign)) { set_error("null col/sign"); return BBF_EINVAL; }
+  if (!device_ok(device, nullptr)) { set_error("no usable sm_100 CUDA device"); return BBF_ECUDA; }
+  BBF_CUDA(cudaSetDevice(device));
+  keep_pool(device);
+  cudaStream_t cs = copy_stream(device, 0);
+  bbf_upload* u = new bbf_upload();
+  std::memset(u, 0, sizeof(*u));
+  u->device = device; u->n_u = n_u; u->n_v = n_v; u->nnz = nnz;
+  // blocks that need no wait on other streams: the copy must not queue behind the current count
+  cudaError_t e = dmalloc_nowait(&u->rp, 8ull * (n_u + 1), cs);
+  if (e == cudaSuccess) e = dmalloc_nowait(&u->col, 4ull * (nnz + 1), cs);
+  if (e == cudaSuccess) e = dmalloc_nowait(&u->sg, nnz + 1, cs);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(u->rp, row_ptr, 8ull * (n_u + 1), cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(u->col, col, 4ull * nnz, cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(u->sg, sign, nnz, cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&u->done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(u->done, cs);
+  if (e != cudaSuccess) {
+    if (u->rp) dfree(u->rp, cs);
+    if (u->col) dfree(u->col, cs);
+    if (u->sg) dfree(u->sg, cs);
+    delete u;
+    return cuda_status(e, "upload");
+  }
+  *out = u;
+  return BBF_OK;
+}
+
+bbf_status bbf_upload_free(bbf_upload* u) {
+  if (!u) return BBF_OK;
+  cudaSetDevice(u->device);
+  cudaStream_t cs = copy_stream(u->device, 0);
+  dfree(u->rp, cs);
+  dfree(u->col, cs);
+  dfree(u->sg, cs);
+  if (u->done) cudaEventDestroy(u->done);
+  delete u;
+  return BBF_OK;
+}
+
+bbf_status bbf_graph_load_upload(bbf_upload* up, uint32_t flags, void* cuda_stream, bbf_comm* comm,
+                                 bbf_graph** out) {
+  if (!up || !out) { set_error("null pointer"); return BBF_EINVAL; }
+  *out = nullptr;
+  if (flags & BBF_PTR_DEVICE) { set_error("BBF_PTR_DEVICE is implied by an upload"); return BBF_EINVAL; }
+  BBF_CUDA(cudaSetDevice(up->device));
+  // the build waits for the copies on the device, not on the host
+  if (cuda_stream) BBF_CUDA(cudaStreamWaitEvent((cudaStream_t)cuda_stream, up->done, 0));
+  else BBF_CUDA(cudaEventSynchronize(up->done));
+  const uint64_t nnz = up->nnz;
+  bbf_status s = load_impl(up->n_u, up->n_v, up->rp, up->col, up->sg, flags | BBF_PTR_DEVICE, up->device,
+                           cuda_stream, comm, out, &nnz);
+  bbf_upload_free(up);  // stream-ordered: the device buffers are reused only after the build
+  return s;
+}
+
+bbf_status bbf_device_sync(int device) {
+  BBF_CUDA(cudaSetDevice(device));
+  BBF_CUDA(cudaDeviceSynchronize());
+  return BBF_OK;
+}
+
 bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_ptr, const uint32_t* col,
                               const uint8_t* sign, uint32_t flags, int device, void* cuda_stream,
                               bbf_comm* comm, bbf_graph** out) {
+  return load_impl(n_u, n_v, row_ptr, col, sign, flags, device, cuda_stream, comm, out, nullptr);
+}
+
+namespace {
+bbf_status load_impl(uint32_t n_u, uint32_t n_v, const uint64_t* row_ptr, const uint32_t* col,
+                     const uint8_t* sign, uint32_t flags, int device, void* cuda_stream, bbf_comm* comm,
+                     bbf_graph** out, const uint64_t* known_nnz) {
   if (!out || !row_ptr) { set_error("null pointer"); return BBF_EINVAL; }
   *out = nullptr;
   if (flags & ~(uint32_t)(BBF_PTR_DEVICE | BBF_POSITIVE_ONLY | BBF_FORCE_SPARSE | BBF_FORCE_DENSE)) {
@@ -255,12 +362,14 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_pt
   BBF_CUDA(cudaSetDevice(device));
   const bool dptr = flags & BBF_PTR_DEVICE;
   uint64_t nnz = 0;
-  if (dptr) {
+  if (known_nnz) {
+    nnz = *known_nnz;
+  } else if (dptr) {
     // ordered after the caller's work on its stream (a plain cudaMemcpy would run on the legacy
     // default stream, which does not wait for non-blocking streams)
     if (cuda_stream) {
-      BBF_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n_u, 8, cudaMemcpyDeviceToHost, (cudaStream_t)cuda_stream));
-      BBF_CUDA(cudaStreamSynchronize((cudaStream_t)cuda_stream));
+      BBF_CUDA(rb_add(&nnz, row_ptr + n_u, 8, (cudaStream_t)cuda_stream));
+      BBF_CUDA(rb_sync((cudaStream_t)cuda_stream));
     } else {
       BBF_CUDA(cudaDeviceSynchronize());
       BBF_CUDA(cudaMemcpy(&nnz, row_ptr + n_u, 8, cudaMemcpyDeviceToHost));
@@ -306,6 +415,7 @@ bbf_status bbf_graph_load_csr(uint32_t n_u, uint32_t n_v, const uint64_t* row_pt
   *out = g;
   return BBF_OK;
 }
+}  // namespace
 
 bbf_status bbf_graph_free(bbf_graph* g) {
   if (!g) return BBF_OK;
@@ -343,7 +453,7 @@ bbf_status bbf_count_global(bbf_graph* g, bbf_counts* out) {
 bbf_status bbf_count_per_vertex(bbf_graph* g, uint64_t* bal_u, uint64_t* unb_u, uint64_t* bal_v,
                                 uint64_t* unb_v, uint32_t flags, bbf_counts* totals) {
   if (!g) { set_error("null graph"); return BBF_EINVAL; }
-  if (flags & ~(uint32_t)(BBF_PTR_DEVICE | BBF_FORCE_SPARSE | BBF_FORCE_DENSE)) {
+  if (flags & ~(uint32_t)(BBF_PTR_DEVICE | BBF_FORCE_SPARSE | BBF_FORCE_DENSE | BBF_OUTPUT_ASYNC)) {
     set_error("unknown flags");
     return BBF_EINVAL;
   }
@@ -368,12 +478,31 @@ bbf_status bbf_count_per_vertex(bbf_graph* g, uint64_t* bal_u, uint64_t* unb_u, 
     k_scatter_pv<<<(cnt + 255) / 256, 256, 0, st>>>((const unsigned long long*)g->pv, g->inv, row0, cnt,
                                                    g->n, db, dn);
     g->launches++;
-    if (!dptr) {
-      if (ob) BBF_CUDA(cudaMemcpyAsync(ob, db, 8ull * cnt, cudaMemcpyDeviceToHost, st));
-      if (on) BBF_CUDA(cudaMemcpyAsync(on, dn, 8ull * cnt, cudaMemcpyDeviceToHost, st));
+  }
+  // host outputs: one D2H per array, on the graph's stream, or with BBF_OUTPUT_ASYNC on the
+  // library's download stream (ordered after the scatter by an event; the call returns without
+  // waiting, bbf_device_sync completes it) so the copy overlaps the caller's next work
+  cudaStream_t dst = st;
+  const bool async_out = !dptr && stage && (flags & BBF_OUTPUT_ASYNC);
+  if (async_out) {
+    dst = copy_stream(g->device, 1);
+    cudaEvent_t ev;
+    BBF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    BBF_CUDA(cudaEventRecord(ev, st));
+    BBF_CUDA(cudaStreamWaitEvent(dst, ev, 0));
+    cudaEventDestroy(ev);  // released once the recorded work completes
+  }
+  if (!dptr) {
+    for (int side = 0; side < 2; ++side) {
+      uint32_t cnt = side ? g->n_v : g->n_u, row0 = side ? g->n_u : 0;
+      uint64_t* ob = outs[2 * side];
+      uint64_t* on = outs[2 * side + 1];
+      if (!cnt) continue;
+      if (ob) BBF_CUDA(cudaMemcpyAsync(ob, stage + 2ull * row0, 8ull * cnt, cudaMemcpyDeviceToHost, dst));
+      if (on) BBF_CUDA(cudaMemcpyAsync(on, stage + 2ull * row0 + cnt, 8ull * cnt, cudaMemcpyDeviceToHost, dst));
     }
   }
-  if (stage) dfree(stage, st);
+  if (stage) dfree(stage, dst);
   BBF_CUDA(cudaStreamSynchronize(st));
   if (totals) {
     unsigned long long wg = 0;

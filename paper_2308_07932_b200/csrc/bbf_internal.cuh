@@ -304,10 +304,19 @@ bbf_status cuda_status(cudaError_t e, const char* what);
 namespace bbf {
 // device-memory cache (mem.cu): stream-ordered like cudaMallocAsync / cudaFreeAsync
 cudaError_t dmalloc_raw(void** out, size_t bytes, cudaStream_t st);
+cudaError_t dmalloc_raw2(void** out, size_t bytes, cudaStream_t st, bool no_wait);
 void dfree(void* p, cudaStream_t st);
+// small device->host readbacks (mem.cu): enqueue with rb_add, complete with rb_sync(st), which
+// synchronises the stream and then fills the host variables
+cudaError_t rb_add(void* host, const void* dev, size_t n, cudaStream_t st);
+cudaError_t rb_sync(cudaStream_t st);
 template <class T>
 inline cudaError_t dmalloc(T** out, size_t bytes, cudaStream_t st) {
   return dmalloc_raw(reinterpret_cast<void**>(out), bytes, st);
+}
+template <typename T>
+cudaError_t dmalloc_nowait(T** out, size_t bytes, cudaStream_t st) {  // see mem.cu
+  return dmalloc_raw2(reinterpret_cast<void**>(out), bytes, st, true);
 }
 bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* col,
                        const uint8_t* sign, bool device_ptrs);

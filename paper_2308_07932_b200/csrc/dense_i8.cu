@@ -777,8 +777,8 @@ bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32
   }
   {
     unsigned long long nz = 0;
-    BBF_CUDA(cudaMemcpyAsync(&nz, d_nz, 8, cudaMemcpyDeviceToHost, st));
-    BBF_CUDA(cudaStreamSynchronize(st));
+    BBF_CUDA(rb_add(&nz, d_nz, 8, st));
+    BBF_CUDA(rb_sync(st));
     dfree(d_nz, st);
     if (nz != g->nnz) {
       set_error("duplicate (u,v) edge");
@@ -881,8 +881,8 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
   cudaEventRecord(e1, st);
   unsigned long long h[4] = {0, 0, 0, 0};
   if (status == BBF_OK) {
-    cudaError_t err = cudaMemcpyAsync(h, g->d_acc, sizeof(h), cudaMemcpyDeviceToHost, st);
-    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    cudaError_t err = rb_add(h, g->d_acc, sizeof(h), st);
+    if (err == cudaSuccess) err = rb_sync(st);
     if (err != cudaSuccess) status = cuda_status(err, "dense path");
   }
   float ms = 0;

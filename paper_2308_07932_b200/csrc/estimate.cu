@@ -80,8 +80,8 @@ extern "C" bbf_status bbf_estimate_global(uint32_t n_u, uint32_t n_v, const uint
   const bool dptr = flags & BBF_PTR_DEVICE;
   uint64_t nnz = 0;
   if (dptr) {
-    BBF_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n_u, 8, cudaMemcpyDeviceToHost, st));
-    BBF_CUDA(cudaStreamSynchronize(st));
+    BBF_CUDA(rb_add(&nnz, row_ptr + n_u, 8, st));
+    BBF_CUDA(rb_sync(st));
   } else {
     nnz = row_ptr[n_u];
   }

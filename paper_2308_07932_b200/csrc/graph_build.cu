@@ -383,8 +383,8 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   if (nnz) k_validate_edges<<<grid_for(nnz, 256), 256, 0, st>>>(d_col, d_sg, nnz, n_v, d_err);
   g->launches += 2;
   uint32_t h_err = 0;
-  BBF_CUDA(cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, st));
-  BBF_CUDA(cudaStreamSynchronize(st));
+  BBF_CUDA(rb_add(&h_err, d_err, 4, st));
+  BBF_CUDA(rb_sync(st));
   if (h_err) {
     dfree(d_err, st);
     cleanup_input();
@@ -417,8 +417,8 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     k_pos_compact<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, keep, pos, d_col, d_sg, pcol, psg);
     g->launches += 5;
     uint32_t kept = 0;
-    BBF_CUDA(cudaMemcpyAsync(&kept, pos + nnz, 4, cudaMemcpyDeviceToHost, st));
-    BBF_CUDA(cudaStreamSynchronize(st));
+    BBF_CUDA(rb_add(&kept, pos + nnz, 4, st));
+    BBF_CUDA(rb_sync(st));
     dfree(tmp0, st);
     dfree(keep, st);
     dfree(pos, st);
@@ -483,11 +483,11 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   k_ws<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(g->degs, n_u, n, d_cnt + 12);
   g->launches += 3;
   unsigned long long h_cnt[16];
-  BBF_CUDA(cudaMemcpyAsync(h_cnt, d_cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, st));
+  BBF_CUDA(rb_add(h_cnt, d_cnt, sizeof(h_cnt), st));
   uint32_t h_maxdeg[2] = {0, 0};
-  if (n_u) BBF_CUDA(cudaMemcpyAsync(&h_maxdeg[0], g->degs, 4, cudaMemcpyDeviceToHost, st));
-  if (n_v) BBF_CUDA(cudaMemcpyAsync(&h_maxdeg[1], g->degs + n_u, 4, cudaMemcpyDeviceToHost, st));
-  BBF_CUDA(cudaStreamSynchronize(st));
+  if (n_u) BBF_CUDA(rb_add(&h_maxdeg[0], g->degs, 4, st));
+  if (n_v) BBF_CUDA(rb_add(&h_maxdeg[1], g->degs + n_u, 4, st));
+  BBF_CUDA(rb_sync(st));
   dfree(d_cnt, st);
   g->maxdeg[0] = h_maxdeg[0];
   g->maxdeg[1] = h_maxdeg[1];
@@ -523,8 +523,8 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     if (n) k_wg_sum<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(mcnt, key_u, key_v, n_u, n, d_wg);
     g->launches += 2;
     unsigned long long wg = 0;
-    BBF_CUDA(cudaMemcpyAsync(&wg, d_wg, 8, cudaMemcpyDeviceToHost, st));
-    BBF_CUDA(cudaStreamSynchronize(st));
+    BBF_CUDA(rb_add(&wg, d_wg, 8, st));
+    BBF_CUDA(rb_sync(st));
     dfree(mcnt, st);
     dfree(d_wg, st);
     g->W_G = wg;
@@ -620,8 +620,8 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     dfree(wb, st);
   }
   uint32_t h_err = 0;
-  BBF_CUDA(cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, st));
-  BBF_CUDA(cudaStreamSynchronize(st));
+  BBF_CUDA(rb_add(&h_err, d_err, 4, st));
+  BBF_CUDA(rb_sync(st));
   dfree(d_err, st);
   if (h_err & kErrDup) {
     dfree(tmp, st);
@@ -663,8 +663,8 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     void* tmp2;
     BBF_CUDA(dmalloc(&tmp2, ts + 16, st));
     BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp2, ts, flag, g->runid, (int64_t)m, st));
-    BBF_CUDA(cudaMemcpyAsync(&g->nruns, g->runid + (m - 1), 4, cudaMemcpyDeviceToHost, st));
-    BBF_CUDA(cudaStreamSynchronize(st));
+    BBF_CUDA(rb_add(&g->nruns, g->runid + (m - 1), 4, st));
+    BBF_CUDA(rb_sync(st));
     BBF_CUDA(dmalloc(&g->runs, sizeof(uint2) * (g->nruns + 1), st));
     k_runs<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, flag, m, wshift, wmask, g->runid, g->runs);
     BBF_CUDA(dmalloc(&g->rlast, 4ull * (n + 1), st));

@@ -7,6 +7,8 @@
 #include <map>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
+#include <cstring>
 
 #include "bbf_internal.cuh"
 
@@ -43,40 +45,58 @@ inline size_t round_size(size_t b) {
 
 }  // namespace
 
-cudaError_t dmalloc_raw(void** out, size_t bytes, cudaStream_t st) {
+cudaError_t dmalloc_raw(void** out, size_t bytes, cudaStream_t st) { return dmalloc_raw2(out, bytes, st, false); }
+
+// A request reuses a cached block of similar size (<= 1.25x + 64 MiB) that needs no wait: released
+// on `st` itself, or released on another stream whose work has already completed.  Otherwise it
+// takes fresh memory rather than making `st` wait for another stream's pending work (e.g. an
+// asynchronous output copy that is meant to overlap the next graph's build); only when the device
+// is out of memory does it reuse a busy block behind a stream wait (never, with no_wait), and then
+// give the whole cache back to the driver.
+cudaError_t dmalloc_raw2(void** out, size_t bytes, cudaStream_t st, bool no_wait) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   const size_t need = round_size(bytes ? bytes : 1);
+  const size_t lim = need + need / 4 + (64u << 20);
   Cache& c = cache();
+  auto take = [&](std::multimap<size_t, Block>& fl, std::multimap<size_t, Block>::iterator it) {
+    Block b = it->second;
+    fl.erase(it);
+    cudaStreamWaitEvent(st, b.ev, 0);  // no-op when complete or already ordered
+    cudaEventDestroy(b.ev);
+    c.live[b.p] = {dev, b.size};
+    *out = b.p;
+  };
   {
     std::lock_guard<std::mutex> lk(c.mu);
     auto& fl = c.free_by_size[dev];
-    auto it = fl.lower_bound(need);
-    // reuse a cached block no larger than 1.25x the request (+ 64 MiB slack for big ones)
-    if (it != fl.end() && it->first <= need + need / 4 + (64u << 20)) {
-      Block b = it->second;
-      fl.erase(it);
-      cudaStreamWaitEvent(st, b.ev, 0);  // no-op wait when already ordered / complete
-      cudaEventDestroy(b.ev);
-      c.live[b.p] = {dev, b.size};
-      *out = b.p;
-      return cudaSuccess;
+    for (auto jt = fl.lower_bound(need); jt != fl.end() && jt->first <= lim; ++jt) {
+      if (jt->second.st == st || cudaEventQuery(jt->second.ev) == cudaSuccess) {
+        take(fl, jt);
+        return cudaSuccess;
+      }
     }
   }
   void* p = nullptr;
   e = cudaMallocAsync(&p, need, st);
   if (e == cudaErrorMemoryAllocation) {
-    // out of memory: give every cached block of this device back to the pool and retry
+    cudaGetLastError();
     std::lock_guard<std::mutex> lk(c.mu);
-    for (auto& kv : c.free_by_size[dev]) {
+    auto& fl = c.free_by_size[dev];
+    auto it = fl.lower_bound(need);
+    if (!no_wait && it != fl.end() && it->first <= lim) {  // a busy block, behind a stream wait
+      take(fl, it);
+      return cudaSuccess;
+    }
+    // give every cached block of this device back to the pool and retry
+    for (auto& kv : fl) {
       cudaStreamWaitEvent(st, kv.second.ev, 0);
       cudaEventDestroy(kv.second.ev);
       cudaFreeAsync(kv.second.p, st);
     }
-    c.free_by_size[dev].clear();
-    cudaGetLastError();
+    fl.clear();
     e = cudaMallocAsync(&p, need, st);
   }
   if (e != cudaSuccess) return e;
@@ -102,6 +122,65 @@ void dfree(void* p, cudaStream_t st) {
   }
   cudaEventRecord(ev, st);
   c.free_by_size[dev].emplace(size, Block{p, size, st, ev});
+}
+
+// ---------------------------------------------------------------------------- small readbacks
+// Host values the library needs mid-build (error flags, counts, sizes) are read back through
+// mapped pinned memory by a one-warp copy kernel instead of cudaMemcpyAsync: a copy command
+// would queue behind large asynchronous copies of other streams on the same copy engine (e.g.
+// BBF_OUTPUT_ASYNC outputs of the previous graph), stalling the build for their whole duration.
+namespace {
+__global__ void k_rb_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, uint32_t n) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+struct RbEntry {
+  void* host;
+  size_t off, n;
+  cudaStream_t st;
+};
+struct RbState {
+  uint8_t* hbuf = nullptr;  // mapped pinned, kRbBytes
+  uint8_t* dbuf = nullptr;  // its device address
+  size_t used = 0;
+  std::vector<RbEntry> pending;
+};
+constexpr size_t kRbBytes = 1 << 16;
+thread_local RbState t_rb;
+}  // namespace
+
+cudaError_t rb_add(void* host, const void* dev, size_t n, cudaStream_t st) {
+  RbState& r = t_rb;
+  if (!r.hbuf) {
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&r.hbuf), kRbBytes, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) { r.hbuf = nullptr; return e; }
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&r.dbuf), r.hbuf, 0);
+    if (e != cudaSuccess) return e;
+  }
+  const size_t off = (r.used + 15) & ~size_t(15);
+  if (n == 0) return cudaSuccess;
+  if (off + n > kRbBytes) {  // too large for the slots: an ordinary copy
+    return cudaMemcpyAsync(host, dev, n, cudaMemcpyDeviceToHost, st);
+  }
+  k_rb_copy<<<1, 32, 0, st>>>(r.dbuf + off, reinterpret_cast<const uint8_t*>(dev), (uint32_t)n);
+  r.used = off + n;
+  r.pending.push_back(RbEntry{host, off, n, st});
+  return cudaGetLastError();
+}
+
+cudaError_t rb_sync(cudaStream_t st) {
+  cudaError_t e = cudaStreamSynchronize(st);
+  RbState& r = t_rb;
+  std::vector<RbEntry> keep;
+  for (const RbEntry& x : r.pending) {
+    if (x.st == st) {
+      if (e == cudaSuccess) std::memcpy(x.host, r.hbuf + x.off, x.n);
+    } else {
+      keep.push_back(x);
+    }
+  }
+  r.pending.swap(keep);
+  if (r.pending.empty()) r.used = 0;
+  return e;
 }
 
 }  // namespace bbf

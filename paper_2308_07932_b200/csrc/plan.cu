@@ -267,8 +267,8 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     k_rsafe<<<(n + 255) / 256, 256, 0, st>>>(win, g->degs, g->n_u, n, d_rs);
     g->launches += 1;
     uint32_t h_rs[4];
-    BBF_CUDA(cudaMemcpyAsync(h_rs, d_rs, 16, cudaMemcpyDeviceToHost, st));
-    BBF_CUDA(cudaStreamSynchronize(st));
+    BBF_CUDA(rb_add(h_rs, d_rs, 16, st));
+    BBF_CUDA(rb_sync(st));
     p->rsafe[0] = h_rs[0]; p->rsafe[1] = h_rs[1]; p->rmid[0] = h_rs[2]; p->rmid[1] = h_rs[3];
     dfree(win, st);
     dfree(d_rs, st);
@@ -286,9 +286,9 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     dfree(tmp, st);
   }
   unsigned long long h_wp = 0, h_wf = 0;
-  BBF_CUDA(cudaMemcpyAsync(&h_wp, d_wp, 8, cudaMemcpyDeviceToHost, st));
-  BBF_CUDA(cudaMemcpyAsync(&h_wf, &acc[0], 8, cudaMemcpyDeviceToHost, st));
-  BBF_CUDA(cudaStreamSynchronize(st));
+  BBF_CUDA(rb_add(&h_wp, d_wp, 8, st));
+  BBF_CUDA(rb_add(&h_wf, &acc[0], 8, st));
+  BBF_CUDA(rb_sync(st));
   p->W_pruned = h_wp;
   p->W_full = h_wf;
   // hub units of ~1/6 of one SM's share of the whole job: with N ranks the share is W / (N * SMs),
@@ -337,10 +337,10 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   }
   uint32_t h_nsel[5] = {0, 0, 0, 0, 0}, h_nunits = 0;
   unsigned long long h_acc[4];
-  BBF_CUDA(cudaMemcpyAsync(h_nsel, d_nsel, 20, cudaMemcpyDeviceToHost, st));
-  BBF_CUDA(cudaMemcpyAsync(&h_nunits, ustart + n, 4, cudaMemcpyDeviceToHost, st));
-  BBF_CUDA(cudaMemcpyAsync(h_acc, acc, 32, cudaMemcpyDeviceToHost, st));
-  BBF_CUDA(cudaStreamSynchronize(st));
+  BBF_CUDA(rb_add(h_nsel, d_nsel, 20, st));
+  BBF_CUDA(rb_add(&h_nunits, ustart + n, 4, st));
+  BBF_CUDA(rb_add(h_acc, acc, 32, st));
+  BBF_CUDA(rb_sync(st));
   p->n_t1 = h_nsel[0];
   p->n_t2 = h_nsel[1];
   p->n_t2s = h_nsel[2];
@@ -362,8 +362,8 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     g->launches += 1;
   }
   unsigned int h_maxmid[4] = {0, 0, 0, 0};
-  BBF_CUDA(cudaMemcpyAsync(h_maxmid, d_maxmid, 16, cudaMemcpyDeviceToHost, st));
-  BBF_CUDA(cudaStreamSynchronize(st));
+  BBF_CUDA(rb_add(h_maxmid, d_maxmid, 16, st));
+  BBF_CUDA(rb_sync(st));
   p->max_mid = h_maxmid[0];
   p->max_work = *(unsigned long long*)(h_maxmid + 2);
   if (getenv("BBF_DEBUG") && atoi(getenv("BBF_DEBUG")) >= 2) {  // work histogram by log2 bucket

@@ -284,6 +284,34 @@ def test_counter_encodings_agree(bbf, monkeypatch):
         assert np.array_equal(a, b)
 
 
+def test_upload_and_async_outputs(bbf):
+    """Pipelined loading (bbf_upload_csr / bbf_graph_load_upload, the next graph's copy in flight
+    while the current one counts) and BBF_OUTPUT_ASYNC host outputs give the same counts as the
+    synchronous calls, on config 3 (sparse) and a dense-path graph; outputs complete after
+    bbf_device_sync."""
+    import torch
+    for g, fl in ((G.config3(), 0), (G.random_bipartite(600, 500, 0.2, 0.6, seed=5), bbf.BBF_FORCE_DENSE)):
+        with bbf.Graph.from_synth(g, flags=fl) as h:
+            ref = h.count_per_vertex()
+        pin = [torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).pin_memory()
+               for a in (g.row_ptr, g.col.view(np.int32), g.sign)]
+        outs = [tuple(torch.zeros(k, dtype=torch.int64).pin_memory() for k in (g.n_u, g.n_u, g.n_v, g.n_v))
+                for _ in range(2)]
+        up = bbf.Upload(g.n_u, g.n_v, *pin)
+        tots = []
+        for k in range(2):
+            h = bbf.Graph.from_upload(up, flags=fl)
+            if k == 0:
+                up = bbf.Upload(g.n_u, g.n_v, *pin)  # in flight during the first count
+            tots.append(h.count_per_vertex(out=outs[k], flags=bbf.BBF_OUTPUT_ASYNC)[0])
+            h.free()
+        bbf.device_sync(0)
+        for k in range(2):
+            assert tots[k]["balanced"] == ref[0]["balanced"] and tots[k]["unbalanced"] == ref[0]["unbalanced"]
+            for a, b in zip(outs[k], ref[1:]):
+                assert np.array_equal(a.numpy().view(np.uint64), b)
+
+
 def test_end_role_packing_agrees(bbf, monkeypatch):
     """End-role counts of "safe" ends go through one packed 64-bit RED (plan.cu k_rsafe); the
     unpacked path (BBF_NO_PACKED_END) gives identical per-vertex arrays on config 3."""

@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--out", default="gpurun_out/trace.json")
     ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--e2e", action="store_true", help="trace the pipelined host-buffer loop (bench e2e)")
     a = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -34,12 +35,26 @@ def main():
         h.count_per_vertex(out=outs)
         h.free()
 
+    if a.e2e:  # bench.py's e2e loop: uploads one step ahead, asynchronous outputs
+        pin = [torch.from_numpy(x).pin_memory() for x in (g.row_ptr.view(np.int64), g.col.view(np.int32), g.sign)]
+        hout = tuple(torch.zeros(k, dtype=torch.int64).pin_memory() for k in (g.n_u, g.n_u, g.n_v, g.n_v))
+        state = {"up": None}
+
+        def step():
+            up = state["up"] or bbf.Upload(g.n_u, g.n_v, *pin)
+            h = bbf.Graph.from_upload(up, stream=s)
+            state["up"] = bbf.Upload(g.n_u, g.n_v, *pin)
+            h.count_per_vertex(out=hout, flags=bbf.BBF_OUTPUT_ASYNC)
+            h.free()
+
     for _ in range(3):
         step()
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         for _ in range(a.steps):
             step()
+        if a.e2e:
+            bbf.device_sync(0)
         torch.cuda.synchronize()
     prof.export_chrome_trace(a.out)
     ev = json.load(open(a.out))["traceEvents"]
@@ -67,6 +82,20 @@ def main():
     print("busy by op (ms):")
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:25]:
         print(f"  {1e-3*v[1]:8.3f} x{v[0]:3d}  {k}")
+    if a.e2e:
+        print("copies (start ms, dur ms, stream, name):")
+        for e in gpu:
+            if e.get("cat") == "gpu_memcpy" and e.get("dur", 0) > 200:
+                print(f"  {1e-3*(e['ts']-t0):8.2f} {1e-3*e['dur']:7.2f}  s{e.get('args', {}).get('stream')}  {e['name']}")
+        w0, w1 = float(os.environ.get("TR_W0", "84")), float(os.environ.get("TR_W1", "101"))
+        print(f"all ops in [{w0}, {w1}] ms:")
+        for e in gpu:
+            t = 1e-3 * (e["ts"] - t0)
+            if w0 <= t <= w1:
+                print(f"  {t:8.3f} {1e-3*e.get('dur',0):7.3f}  s{e.get('args', {}).get('stream')}  {e['name'][:60]}")
+        for e in gpu:
+            if e.get("cat") == "kernel" and ("k_t3" in e["name"] or "k_hist_v" in e["name"]):
+                print(f"  {1e-3*(e['ts']-t0):8.2f} {1e-3*e['dur']:7.2f}  s{e.get('args', {}).get('stream')}  {e['name'][:40]}")
     cpu = sorted([e for e in ev if e.get("cat") == "cuda_runtime" or e.get("cat") == "cuda_driver"],
                  key=lambda e: -e.get("dur", 0))
     print("longest runtime API calls (ms):")
