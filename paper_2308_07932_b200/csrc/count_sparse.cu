@@ -1072,7 +1072,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
   uint32_t* mW = mS + kM;        // kM: middle word
   uint32_t* mB = mW + kM;        // kM: pass-2 balanced share of the middle
   uint32_t* mN = mB + kM;        // kM: pass-2 unbalanced share
-  __shared__ uint32_t sh_item, sh_wsum[kT2Warps];
+  __shared__ uint32_t sh_item, sh_mcc, sh_wsum[kT2Warps];
   __shared__ unsigned long long sh_red[2][kT2Warps];
   for (uint32_t i = tid; i < 2 * kSlots; i += kT2Threads) ((uint32_t*)keys)[i] = 0;
   unsigned long long totB = 0, totN = 0;
@@ -1096,43 +1096,68 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
 #pragma unroll 1
       for (uint32_t r0 = 0; r0 < m; r0 += kM) {
         const uint32_t mc = min(kM, m - r0);
-        // round set-up: two consecutive middles per thread, CTA-wide exclusive scan of lengths
-        uint32_t len2[2];
+        // round set-up: two consecutive middles per thread; one CTA-wide exclusive scan of
+        // (segment length << 12 | non-empty) compacts the non-empty middles (so their first
+        // wedges strictly increase) and gives each one's first flattened wedge
+        uint32_t len2[2], wv2[2] = {0, 0}, s2[2] = {0, 0};
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const uint32_t i = 2 * tid + q;
           len2[q] = 0;
           if (i < mc) {
-            const uint32_t wv = a.adj[m_lo + r0 + i];
-            const uint32_t s0 = a.ub[m_lo + r0 + i];
-            const uint32_t en = a.end1[ob + (wv & kMask)];
-            len2[q] = en > s0 ? en - s0 : 0;
-            mS[i] = s0;
-            mW[i] = wv;
-            if (pass == 1) { mB[i] = 0; mN[i] = 0; }
+            wv2[q] = a.adj[m_lo + r0 + i];
+            s2[q] = a.ub[m_lo + r0 + i];
+            const uint32_t en = a.end1[ob + (wv2[q] & kMask)];
+            len2[q] = en > s2[q] ? en - s2[q] : 0;
           }
         }
-        const uint32_t tsum = len2[0] + len2[1];
+        const uint32_t tsum = ((len2[0] + len2[1]) << 12) | ((len2[0] > 0) + (len2[1] > 0));
         const uint32_t wincl = warp_incl_scan(tsum, lane);
         if (lane == 31) sh_wsum[warp] = wincl;
         __syncthreads();
         uint32_t wbase = 0;
         for (int w2 = 0; w2 < warp; ++w2) wbase += sh_wsum[w2];
-        const uint32_t ex = wbase + wincl - tsum;
-        if (2 * tid < kM) { mP[2 * tid] = ex; mP[2 * tid + 1] = ex + len2[0]; }
-        if (tid == kT2Threads - 1) mP[kM] = ex + tsum;
-        __syncthreads();
-        const uint32_t T = mP[kM];
-        for (uint32_t base = 32u * warp; base < T; base += 32u * kT2Warps) {
-          const uint32_t t = base + lane;
-          uint32_t j = kM, b2 = 0, n2 = 0;
-          if (t < T) {
-            uint32_t lo = 0, hi = mc - 1;  // last middle with mP[j] <= t
-            while (lo < hi) {
-              const uint32_t md = (lo + hi + 1) >> 1;
-              if (mP[md] <= t) lo = md; else hi = md - 1;
+        const uint32_t ex = wbase + wincl - tsum;  // (wedges before << 12) | non-empty middles before
+        {
+          uint32_t k = ex & 0xfffu, pos = ex >> 12;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (len2[q]) {
+              mP[k] = pos; mS[k] = s2[q]; mW[k] = wv2[q];
+              if (pass == 1) { mB[k] = 0; mN[k] = 0; }
+              ++k;
+              pos += len2[q];
             }
-            j = lo;
+          }
+        }
+        if (tid == kT2Threads - 1) { sh_mcc = (ex + tsum) & 0xfffu; mP[(ex + tsum) & 0xfffu] = (ex + tsum) >> 12; }
+        __syncthreads();
+        const uint32_t mcc = sh_mcc;  // non-empty middles of the round
+        const uint32_t T = mP[mcc];
+        // each warp takes a contiguous range of 32-wedge steps; a lane's middle = the middle owning
+        // the previous step's last wedge + the middles starting in this step at or before the lane
+        const uint32_t nsteps = (T + 31) / 32, per = (nsteps + kT2Warps - 1) / kT2Warps;
+        const uint32_t st0 = min(nsteps, per * warp), st1 = min(nsteps, st0 + per);
+        int carry = -1;
+        if (st0 < st1 && st0 > 0) {  // owner of wedge 32 * st0 - 1: last middle starting at or before it
+          uint32_t lo = 0, hi = mcc - 1;
+          const uint32_t t0 = 32u * st0 - 1u;
+          while (lo < hi) {
+            const uint32_t md = (lo + hi + 1) >> 1;
+            if (mP[md] <= t0) lo = md; else hi = md - 1;
+          }
+          carry = (int)lo;
+        }
+        for (uint32_t stp = st0; stp < st1; ++stp) {
+          const uint32_t base = 32u * stp, t = base + lane;
+          const uint32_t nx = (uint32_t)(carry + 1) + lane;
+          const uint32_t nstart = nx < mcc ? mP[nx] : 0xffffffffu;
+          const uint32_t smask = __reduce_or_sync(0xffffffffu, nstart < base + 32u ? 1u << (nstart - base) : 0u);
+          const uint32_t mm = smask & (0xffffffffu >> (31 - lane));
+          const uint32_t j = (uint32_t)(carry + __popc(mm));
+          carry += __popc(smask);
+          uint32_t b2 = 0, n2 = 0;
+          if (t < T) {
             const uint32_t ev = a.adj[mS[j] + (t - mP[j])];
             const uint32_t l = ev & kMask;
             const uint32_t cls = (ev ^ mW[j]) >> 31;
@@ -1159,14 +1184,11 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
           }
           if (pass == 1 && __any_sync(0xffffffffu, (b2 | n2) != 0)) {
             // lanes' middles are non-decreasing: sum each run of equal j, its last lane adds it
-            const uint32_t jp = __shfl_up_sync(0xffffffffu, j, 1);
-            const uint32_t starts = __ballot_sync(0xffffffffu, lane == 0 || jp != j);
-            const uint32_t mm = starts & (0xffffffffu >> (31 - lane));
-            const int gs = 31 - __clz(mm);
+            const int gs = mm ? 31 - __clz(mm) : 0;
             uint32_t sb2, sn2;
             seg_sums2(b2, n2, gs, lane, sb2, sn2);
-            const bool last = lane == 31 || ((starts >> (lane + 1)) & 1u);
-            if (last && j < kM && (sb2 | sn2)) {
+            const bool last = t < T && (lane == 31 || t + 1 == T || ((smask >> (lane + 1)) & 1u));
+            if (last && (sb2 | sn2)) {
               if (sb2) atomicAdd(&mB[j], sb2);
               if (sn2) atomicAdd(&mN[j], sn2);
             }
@@ -1174,7 +1196,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
         }
         __syncthreads();
         if (pass == 1) {
-          for (uint32_t i = tid; i < mc; i += kT2Threads) {
+          for (uint32_t i = tid; i < mcc; i += kT2Threads) {
             const uint32_t cb = mB[i], cn = mN[i];
             if (cb | cn) mid_red(a, a.rmid[xu ? 1 : 0], mW[i] & kMask, ob + (mW[i] & kMask), cb, cn);
           }
