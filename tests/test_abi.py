@@ -66,3 +66,23 @@ def test_binding_never_imports_oracle():
     for f in os.listdir(os.path.join(ROOT, "paper_2308_07932_b200", "csrc")):
         txt = open(os.path.join(ROOT, "paper_2308_07932_b200", "csrc", f)).read()
         assert "oracle" not in txt.lower()
+
+
+def test_upload_api_argument_errors_without_gpu(libpath):
+    """The pipelined-loading entry points validate their arguments before touching a device and,
+    with no GPU, refuse (no CPU fallback); freeing a NULL upload is a no-op."""
+    import torch
+    from paper_2308_07932_b200 import bbf
+    L = bbf.lib()
+    out = ctypes.c_void_p()
+    assert L.bbf_upload_csr(2, 2, None, None, None, 0, ctypes.byref(out)) == bbf.BBF_EINVAL
+    rp = np.array([0, 2, 4], np.uint64)
+    assert L.bbf_upload_csr(2, 2, rp.ctypes.data_as(ctypes.c_void_p), None, None, 0,
+                            ctypes.byref(out)) == bbf.BBF_EINVAL  # nnz > 0 without col / sign
+    assert L.bbf_graph_load_upload(None, 0, None, None, ctypes.byref(out)) == bbf.BBF_EINVAL
+    assert L.bbf_upload_free(None) == bbf.BBF_OK
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: refusal path not applicable")
+    with pytest.raises(bbf.BBFError) as e:
+        bbf.Upload(2, 2, rp, np.array([0, 1, 0, 1], np.uint32), np.ones(4, np.uint8))
+    assert e.value.name == "BBF_ECUDA"
