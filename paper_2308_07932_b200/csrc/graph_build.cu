@@ -137,8 +137,8 @@ __global__ void k_transpose_keys(const uint32_t* __restrict__ vkey, const uint32
 
 // after C: U entry i -> its adjacency word and the reverse positions of both entries of the
 // edge (absolute indices into adj)
-__global__ void k_u_adj(const uint64_t* __restrict__ val, uint64_t nnz, uint32_t* __restrict__ adj,
-                        uint32_t* __restrict__ rev) {
+__global__ void k_u_adj(const uint64_t* __restrict__ val, uint64_t nnz, const uint32_t* __restrict__ erow,
+                        uint32_t* __restrict__ adj, uint32_t* __restrict__ rev, uint32_t* err) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nnz;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t v = val[i];
@@ -146,15 +146,10 @@ __global__ void k_u_adj(const uint64_t* __restrict__ val, uint64_t nnz, uint32_t
     adj[i] = (uint32_t)(v >> 32);
     rev[i] = (uint32_t)r;
     rev[r] = (uint32_t)i;
+    // duplicate (u, v) edges are adjacent in the sorted U rows
+    if (i > 0 && erow[i] == erow[i - 1] && (((uint32_t)(v >> 32) ^ (uint32_t)(val[i - 1] >> 32)) & kMask) == 0)
+      atomicOr(err, kErrDup);
   }
-}
-
-// duplicate (u, v) edges are adjacent in the sorted U rows
-__global__ void k_dup_check(const uint32_t* __restrict__ erow, const uint32_t* __restrict__ adj, uint64_t nnz,
-                            uint32_t* err) {
-  for (uint64_t i = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nnz;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    if (erow[i] == erow[i - 1] && ((adj[i] ^ adj[i - 1]) & kMask) == 0) atomicOr(err, kErrDup);
 }
 
 // number of entries of the descending array a[0..cnt) that are > key
@@ -260,14 +255,11 @@ __global__ void k_rlast(const uint32_t* __restrict__ off, const uint32_t* __rest
 }
 
 __global__ void k_runs(const uint32_t* __restrict__ adjc, const uint32_t* __restrict__ flag,
-                       uint64_t m, uint32_t wshift, uint32_t wmask, uint32_t* __restrict__ runid,
+                       uint64_t m, uint32_t wshift, uint32_t wmask, const uint32_t* __restrict__ runid,
                        uint2* __restrict__ runs) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t r = runid[e] - 1u;  // inclusive scan -> 0-based run index
-    runid[e] = r;
-    if (flag[e]) runs[r] = make_uint2((uint32_t)e, ((adjc[e] >> wshift) & wmask) / kWin);
-  }
+       e += (uint64_t)gridDim.x * blockDim.x)
+    if (e == 0 || flag[e]) runs[runid[e]] = make_uint2((uint32_t)e, ((adjc[e] >> wshift) & wmask) / kWin);
 }
 
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {
@@ -610,9 +602,8 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     BBF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t3, ka, kb, va, g->adj + nnz, (int)nnz, 0, bits_v, st));
     k_transpose_keys<<<grid_for(nnz, 256), 256, 0, st>>>(kb, g->adj + nnz, nnz, n_u, g->erow + nnz, ka, wa);
     BBF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t3, ka, g->erow, wa, wb, (int)nnz, 0, bits_u, st));
-    k_u_adj<<<grid_for(nnz, 256), 256, 0, st>>>(wb, nnz, g->adj, g->rev);
-    k_dup_check<<<grid_for(nnz, 256), 256, 0, st>>>(g->erow, g->adj, nnz, d_err);
-    g->launches += 10;
+    k_u_adj<<<grid_for(nnz, 256), 256, 0, st>>>(wb, nnz, g->erow, g->adj, g->rev, d_err);
+    g->launches += 13;  // k_entries, 2 CUB radix sorts (histogram, exclusive sum, 3 onesweep passes each), k_transpose_keys, k_u_adj
     dfree(ka, st);
     dfree(va, st);
     dfree(kb, st);
@@ -658,6 +649,8 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     BBF_CUDA(dmalloc(&flag, 4ull * (m + 1), st));
     k_caddr<<<grid_for(m, 256), 256, 0, st>>>(g->adj, g->erow, m, nnz, g->zones[0], g->zones[1], g->compact,
                                             wshift, wmask, g->adjc, flag);
+    // entry 0 always starts a run: with its flag cleared the inclusive scan is the 0-based run index
+    BBF_CUDA(cudaMemsetAsync(flag, 0, 4, st));
     size_t ts = 0;
     cub::DeviceScan::InclusiveSum(nullptr, ts, flag, g->runid, (int64_t)m, st);
     void* tmp2;
@@ -665,6 +658,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp2, ts, flag, g->runid, (int64_t)m, st));
     BBF_CUDA(rb_add(&g->nruns, g->runid + (m - 1), 4, st));
     BBF_CUDA(rb_sync(st));
+    g->nruns += 1;
     BBF_CUDA(dmalloc(&g->runs, sizeof(uint2) * (g->nruns + 1), st));
     k_runs<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, flag, m, wshift, wmask, g->runid, g->runs);
     BBF_CUDA(dmalloc(&g->rlast, 4ull * (n + 1), st));
