@@ -953,30 +953,31 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
           uint32_t en = a.end1[ob + (wv & kMask)];
           len = en > s ? en - s : 0;
         }
-        uint32_t incl = len;
-        for (int o = 1; o < 32; o <<= 1) {
-          uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t incl = warp_incl_scan(len, lane), excl = incl - len;
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         if (tot == 0) continue;
-        sh_incl[lane] = incl;
-        sh_s[lane] = s;
-        sh_wv[lane] = wv;
+        // the chunk's non-empty middles in lane order (their first wedges strictly increase); a
+        // wedge's middle = those started before this step + those starting in it at or before
+        // the lane (start-mask popcount), looked up in the compacted lane list
+        const uint32_t nzm = __ballot_sync(0xffffffffu, len > 0);
+        if (len) sh_incl[__popc(nzm & ((1u << lane) - 1u))] = lane;
         __syncwarp();
-        for (uint32_t t = lane; t < tot + 31 - (tot + 31) % 32; t += 32) {
-          bool act = t < tot;
-          if (act) {
-            uint32_t lo = 0, hi = 31;  // first j with incl[j] > t
-            while (lo < hi) {
-              uint32_t md = (lo + hi) >> 1;
-              if (sh_incl[md] > t) hi = md; else lo = md + 1;
-            }
-            uint32_t j = lo;
-            uint32_t excl = j ? sh_incl[j - 1] : 0;
-            uint32_t ev = a.adj[sh_s[j] + (t - excl)];
+        int carry = -1;
+        for (uint32_t base = 0; base < tot; base += 32) {
+          const uint32_t t = base + lane;
+          const bool stt = len > 0 && excl >= base && excl < base + 32;
+          const uint32_t smask = __reduce_or_sync(0xffffffffu, stt ? 1u << (excl - base) : 0u);
+          const uint32_t mm = smask & (0xffffffffu >> (31 - lane));
+          const int rk = carry + __popc(mm);
+          carry += __popc(smask);
+          const int jl = (int)sh_incl[rk < 0 ? 0 : rk];  // owner lane
+          const uint32_t o_s = __shfl_sync(0xffffffffu, s, jl), o_excl = __shfl_sync(0xffffffffu, excl, jl);
+          const uint32_t o_wv = __shfl_sync(0xffffffffu, wv, jl);
+          uint32_t b2 = 0, n2 = 0;
+          if (t < tot) {
+            uint32_t ev = a.adj[o_s + (t - o_excl)];
             uint32_t l = ev & kMask;
-            uint32_t cls = (ev ^ sh_wv[j]) >> 31;
+            uint32_t cls = (ev ^ o_wv) >> 31;
             uint32_t key = l + 1;
             uint32_t h = hslot(l, mask);
             if (pass == 0) {
@@ -994,11 +995,22 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
               while (keys[h] != key) h = (h + 1) & mask;
               uint32_t v = vals[h];
               uint32_t ad = v & 0xffffu, dd = v >> 16;
-              uint32_t b2 = cls ? dd - 1 : ad - 1, n2 = cls ? ad : dd;
-              if (b2) atomicAdd(&sh_mb[j], b2);
-              if (n2) atomicAdd(&sh_mn[j], n2);
+              b2 = cls ? dd - 1 : ad - 1;
+              n2 = cls ? ad : dd;
             }
           }
+          if (pass == 1 && __any_sync(0xffffffffu, (b2 | n2) != 0)) {
+            // per-middle sums over runs of equal owners, one shared add per run
+            const int gs = mm ? 31 - __clz(mm) : 0;
+            uint32_t sb2, sn2;
+            seg_sums2(b2, n2, gs, lane, sb2, sn2);
+            const bool last = t < tot && (lane == 31 || t + 1 == tot || ((smask >> (lane + 1)) & 1u));
+            if (last && (sb2 | sn2)) {
+              sh_mb[jl] += sb2;  // one writer per middle per step
+              sh_mn[jl] += sn2;
+            }
+          }
+          __syncwarp();
         }
         __syncwarp();
         if (pass == 1) {
