@@ -425,7 +425,7 @@ bbf_status bbf_graph_free(bbf_graph* g) {
   free_plan(&g->plan_s[1], g->stream);
   void* ptrs[] = {g->off, g->adj, g->erow, g->rev, g->rlast, g->mid, g->end1, g->inv, g->degs, g->degpre, g->scratch, g->d_acc, g->pv, g->pe, g->pm,
                   g->adjc, g->runid, g->runs, g->skey, g->lr, g->in_rp, g->in_col, g->in_sg,
-                  g->dA[0], g->dA[1], g->dS[0], g->dS[1]};
+                  g->dA[0], g->dA[1], g->dS[0], g->dS[1], g->dA4[0], g->dA4[1], g->dS4[0], g->dS4[1]};
   for (void* p : ptrs)
     if (p) dfree(p, g->stream);
   cudaStreamSynchronize(g->stream);

@@ -260,6 +260,9 @@ struct bbf_graph {
   uint8_t* dA[2];
   uint8_t* dS[2];
   uint64_t drows[2], dk[2];
+  uint8_t* dA4[2];           // fp4 (e2m1) packed copies of dA / dS for the block-scaled MMA path
+  uint8_t* dS4[2];
+  uint64_t dk4[2];            // bytes per fp4 row (K padded to 256 elements, / 2)
   bool dense_built;
   uint32_t L4[2];     // #vertices with degree >= 2 per side
   uint32_t Llong[2];  // #vertices with degree > 32 per side ("long" middles of the hub kernel)

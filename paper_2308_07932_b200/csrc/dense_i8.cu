@@ -561,6 +561,260 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// ================================================================================ FP4 variant
+// The same pair kernel on the block-scaled FP4 tensor path (tcgen05.mma.cta_group::2.kind::mxf4,
+// 2x the int8 rate, half the operand bytes): A and S as e2m1 (0, +1.0, -1.0) packed two per byte,
+// every E8M0 block scale 1.0 (127), so T = A A^T and P = S S^T are integer sums of +-1 products,
+// accumulated in fp32 — exact while every partial sum stays far below 2^24; the path is used only
+// when the rows' maximum degree (which bounds |T|, |P| and every partial sum) is <= 8,192.
+// TMEM: T in columns [0, 224), P in [224, 448) (N = 224: both accumulators and the scale factors
+// must fit the 512 columns), scale factors in [448, 512), filled once with 0x7F bytes.
+constexpr uint32_t kF4N = 224;                    // tile columns (MMA N); each CTA holds 112 B rows
+constexpr uint32_t kF4JRows = kF4N / 2;
+constexpr uint32_t kF4Stages = 3;
+constexpr uint32_t kF4StageBytes = 4 * kPHalf;    // A_i, S_i (128 rows), A_j, S_j (112 rows) slots
+constexpr size_t kF4SmemBytes = kF4Stages * kF4StageBytes + 1024 + 2 * kBN * 8 + 256;
+constexpr uint32_t kF4SfCol = 2 * kF4N;           // 448
+// block-scaled descriptor: a/b format E2M1 (MXF4Format 1) at bits 7 / 10, N >> 3 at 17, scale
+// format E8M0 at bit 23, M >> 4 at 24, K = 64 (bit 31 clear), scale-factor ids 0
+constexpr uint32_t kIdescF4 = (1u << 7) | (1u << 10) | ((kF4N >> 3) << 17) | (1u << 23) | ((256u >> 4) << 24);
+
+__device__ __forceinline__ void mma_f4_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t sf,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdescF4), "r"(acc), "r"(sf)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16_const(uint32_t taddr, uint32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(v)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_dense_f4(const __grid_constant__ CUtensorMap mAi, const __grid_constant__ CUtensorMap mSi,
+               const __grid_constant__ CUtensorMap mAj, const __grid_constant__ CUtensorMap mSj,
+               const DenseArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned long long* colB = reinterpret_cast<unsigned long long*>(smem + kF4Stages * kF4StageBytes);
+  unsigned long long* colN = colB + kBN;
+  __shared__ __align__(8) uint64_t bar_full[kF4Stages], bar_empty[kF4Stages], bar_tfull, bar_tempty;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  for (uint32_t i = threadIdx.x; i < 2 * kBN; i += kThreads) colB[i] = 0;
+  if (threadIdx.x == 0) {
+    for (uint32_t st = 0; st < kF4Stages; ++st) {
+      mbar_init(smem_u32(&bar_full[st]), 1);
+      mbar_init(smem_u32(&bar_empty[st]), 1);
+    }
+    mbar_init(smem_u32(&bar_tfull), 1);
+    mbar_init(smem_u32(&bar_tempty), 2 * 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tmem_base_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  if (warp >= kEpiWarp0) {  // scale factors: every byte of columns [448, 512) = 127 (2^0)
+    const uint32_t q = (uint32_t)(warp & 3);
+#pragma unroll
+    for (uint32_t h = 0; h < 4; ++h) tmem_st16_const(tmem + ((q * 32) << 16) + kF4SfCol + 16 * h, 0x7F7F7F7Fu);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAi)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mSi)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAj)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mSj)) : "memory");
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t t = pair * a.nranks + a.rank; t < a.n_tiles; t += npairs * a.nranks) {
+        const uint2 tile = a.tiles[t];
+        const int32_t ri = (int32_t)(tile.x * kPB + crank * 128);
+        const int32_t rj = (int32_t)(tile.y * kF4N + crank * kF4JRows);
+        for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
+          mbar_wait(smem_u32(&bar_empty[stage]), phase ^ 1u);
+          const uint32_t fb = mapa_rank(smem_u32(&bar_full[stage]), 0);
+          if (leader) mbar_arrive_expect_tx(smem_u32(&bar_full[stage]), 2 * (2 * kPHalf + 2 * kF4JRows * kBK));
+          const uint32_t base = smem_u32(smem + stage * kF4StageBytes);
+          const int32_t k0 = (int32_t)(kb * kBK);
+          tma_load_2d_pair(base, &mAi, fb, k0, ri);
+          tma_load_2d_pair(base + kPHalf, &mSi, fb, k0, ri);
+          tma_load_2d_pair(base + 2 * kPHalf, &mAj, fb, k0, rj);
+          tma_load_2d_pair(base + 3 * kPHalf, &mSj, fb, k0, rj);
+          if (++stage == kF4Stages) { stage = 0; phase ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      uint32_t stage = 0, phase = 0, lt = 0;
+      for (uint32_t t = pair * a.nranks + a.rank; t < a.n_tiles; t += npairs * a.nranks, ++lt) {
+        if (lt > 0) {
+          mbar_wait(smem_u32(&bar_tempty), (lt - 1) & 1u);
+          tc_fence_after();
+        }
+        for (uint32_t kb = 0; kb < a.n_kb; ++kb) {
+          mbar_wait(smem_u32(&bar_full[stage]), phase);
+          tc_fence_after();
+          const uint32_t base = smem_u32(smem + stage * kF4StageBytes);
+#pragma unroll
+          for (uint32_t kk = 0; kk < kBK / 32; ++kk) {  // 32 B = 64 e2m1 values per MMA
+            const uint32_t acc = (kb | kk) ? 1u : 0u;
+            const uint32_t off = kk * 32;
+            mma_f4_pair(tmem, smem_desc(base + off), smem_desc(base + 2 * kPHalf + off), tmem + kF4SfCol, acc);
+            mma_f4_pair(tmem + kF4N, smem_desc(base + kPHalf + off), smem_desc(base + 3 * kPHalf + off),
+                        tmem + kF4SfCol, acc);
+          }
+          mma_commit_pair(smem_u32(&bar_empty[stage]));
+          if (++stage == kF4Stages) { stage = 0; phase ^= 1u; }
+        }
+        mma_commit_pair(smem_u32(&bar_tfull));
+      }
+    }
+  } else {
+    const uint32_t q = (uint32_t)(warp & 3);
+    const uint32_t etid = threadIdx.x - kEpiWarp0 * 32;
+    const uint32_t tempty_leader = mapa_rank(smem_u32(&bar_tempty), 0);
+    unsigned long long totB = 0, totN = 0;
+    uint32_t lt = 0;
+    for (uint32_t t = pair * a.nranks + a.rank; t < a.n_tiles; t += npairs * a.nranks, ++lt) {
+      const uint2 tile = a.tiles[t];
+      const uint32_t i = tile.x * kPB + crank * 128 + q * 32 + lane;  // this thread's row
+      const uint32_t j0 = tile.y * kF4N;
+      mbar_wait(smem_u32(&bar_tfull), lt & 1u);
+      tc_fence_after();
+      unsigned long long rB = 0, rN = 0;
+#pragma unroll 1
+      for (uint32_t c = 0; c < kF4N / 32; ++c) {
+        uint32_t tv[32], pv[32];
+        const uint32_t ta = tmem + ((q * 32) << 16) + c * 32;
+        tmem_ld32(ta, tv);
+        tmem_ld32(ta + kF4N, pv);
+        tmem_wait_ld();
+        unsigned long long vb[32], vn[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const uint32_t tt = (uint32_t)__float2int_rn(__int_as_float((int)tv[e]));
+          const uint32_t pp = (uint32_t)__float2int_rn(__int_as_float((int)pv[e]));
+          const uint32_t ad = (tt + pp) >> 1, dd = (tt - pp) >> 1;
+          uint32_t fb = ((ad * (ad - 1u)) >> 1) + ((dd * (dd - 1u)) >> 1);
+          uint32_t fn = ad * dd;
+          if (j0 + c * 32 + (uint32_t)e <= i) { fb = 0; fn = 0; }  // pairs i < j only
+          rB += fb;
+          rN += fn;
+          vb[e] = fb;
+          vn[e] = fn;
+        }
+        if (a.pv) {
+          xpose_step<16>(vb, lane); xpose_step<16>(vn, lane);
+          xpose_step<8>(vb, lane);  xpose_step<8>(vn, lane);
+          xpose_step<4>(vb, lane);  xpose_step<4>(vn, lane);
+          xpose_step<2>(vb, lane);  xpose_step<2>(vn, lane);
+          xpose_step<1>(vb, lane);  xpose_step<1>(vn, lane);
+          if (vb[0]) atomicAdd(&colB[c * 32 + lane], vb[0]);
+          if (vn[0]) atomicAdd(&colN[c * 32 + lane], vn[0]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(tempty_leader)
+                     : "memory");
+      totB += rB;
+      totN += rN;
+      if (a.pv) {
+        if ((rB | rN) && i < a.n_rows) {
+          atomicAdd(&a.pv[2ull * (a.pv_row0 + i)], rB);
+          atomicAdd(&a.pv[2ull * (a.pv_row0 + i) + 1], rN);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (uint32_t jj = etid; jj < kF4N; jj += 128) {
+          const unsigned long long b = colB[jj], nn = colN[jj];
+          colB[jj] = 0;
+          colN[jj] = 0;
+          const uint32_t j = j0 + jj;
+          if ((b | nn) && j < a.n_rows) {
+            atomicAdd(&a.pv[2ull * (a.pv_row0 + j)], b);
+            atomicAdd(&a.pv[2ull * (a.pv_row0 + j) + 1], nn);
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      totB += __shfl_xor_sync(0xffffffffu, totB, o);
+      totN += __shfl_xor_sync(0xffffffffu, totN, o);
+    }
+    if (lane == 0 && (totB | totN)) {
+      atomicAdd(&a.acc[0], totB);
+      atomicAdd(&a.acc[1], totN);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// u8 A (0/1) / S (0, 1, 0xFF) rows -> e2m1 packed two per byte (element 2b in the low nibble):
+// 0 -> 0x0, +1 -> 0x2 (1.0), -1 -> 0xA (-1.0); bytes beyond the u8 row are zero padding
+__global__ void k_dense_pack_f4(const uint8_t* __restrict__ in, uint64_t k_in, uint8_t* __restrict__ out,
+                                uint64_t k_out, uint64_t rows) {
+  const uint64_t n8 = rows * (k_out / 8);  // 8 output bytes per thread
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n8; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = t / (k_out / 8), b0 = (t % (k_out / 8)) * 8;  // first output byte
+    uint32_t w[2] = {0u, 0u};
+    if (2 * b0 < k_in) {
+      const uint4 q = *reinterpret_cast<const uint4*>(in + r * k_in + 2 * b0);  // 16 input bytes
+      const uint32_t iw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const uint32_t v = (iw[e >> 2] >> (8 * (e & 3))) & 0xFFu;
+        const uint32_t nib = v == 1u ? 0x2u : (v == 0xFFu ? 0xAu : 0u);
+        w[e >> 3] |= nib << (4 * (e & 7));
+      }
+    }
+    *reinterpret_cast<uint2*>(out + r * k_out + b0) = make_uint2(w[0], w[1]);
+  }
+}
+
+// tiles of the FP4 kernel: I over 256-row blocks, J over 224-row blocks, kept when the tile holds
+// a pair i < j; super-tiles of 8 x 8 blocks for L2 reuse as in pair_tile_list
+std::vector<uint2> f4_tile_list(uint32_t rows_pad) {
+  std::vector<uint2> t;
+  const uint32_t nI = rows_pad / kPB, nJ = (rows_pad + kF4N - 1) / kF4N, sb = 8;
+  for (uint32_t JS = 0; JS < (nJ + sb - 1) / sb; ++JS)
+    for (uint32_t IS = 0; IS < (nI + sb - 1) / sb; ++IS)
+      for (uint32_t J = JS * sb; J < std::min(nJ, JS * sb + sb); ++J)
+        for (uint32_t I = IS * sb; I < std::min(nI, IS * sb + sb); ++I)
+          if (J * kF4N + kF4N - 1 > I * kPB) t.push_back(make_uint2(I, J));
+  return t;
+}
+
 // upper-triangle pair tiles (I <= J over 256-row blocks) in super-tiles of 8 x 8 blocks, so the
 // ~74 tiles in flight read ~16 distinct operand blocks (L2 reuse) instead of ~75
 std::vector<uint2> pair_tile_list(uint32_t rows_pad) {
@@ -839,6 +1093,55 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
     uint8_t* A = side ? Av : Au;
     uint8_t* S = side ? Sv : Su;
     const bool pair_kernel = !getenv("BBF_DENSE_1CTA");
+    // FP4 block-scaled path when exact (|T|, |P| and every partial sum <= the rows' max degree)
+    const bool f4 = pair_kernel && !getenv("BBF_DENSE_I8") && g->maxdeg[side] <= 8192u;
+    if (f4) {
+      if (!g->dA4[side]) {  // packed operands, built once per graph
+        const uint64_t k4 = round_up(k, 256) / 2;
+        cudaError_t err = dmalloc(&g->dA4[side], rows_pad * k4, st);
+        if (err == cudaSuccess) err = dmalloc(&g->dS4[side], rows_pad * k4, st);
+        if (err != cudaSuccess) { status = cuda_status(err, "fp4 operands"); break; }
+        const uint64_t n8 = rows_pad * (k4 / 8);
+        const unsigned grid = (unsigned)std::min<uint64_t>((n8 + 255) / 256, 148ull * 32);
+        k_dense_pack_f4<<<grid, 256, 0, st>>>(A, k, g->dA4[side], k4, rows_pad);
+        k_dense_pack_f4<<<grid, 256, 0, st>>>(S, k, g->dS4[side], k4, rows_pad);
+        g->launches += 2;
+        g->dk4[side] = k4;
+      }
+      const uint64_t k4 = g->dk4[side];
+      CUtensorMap fAi, fSi, fAj, fSj;
+      if (!(make_map(&fAi, g->dA4[side], rows_pad, k4, 128) && make_map(&fSi, g->dS4[side], rows_pad, k4, 128) &&
+            make_map(&fAj, g->dA4[side], rows_pad, k4, kF4JRows) && make_map(&fSj, g->dS4[side], rows_pad, k4, kF4JRows))) {
+        set_error("cuTensorMapEncodeTiled failed");
+        status = BBF_ECUDA;
+        break;
+      }
+      std::vector<uint2> tl = f4_tile_list((uint32_t)rows_pad);
+      cudaError_t err = dmalloc(&dtiles[side], sizeof(uint2) * (tl.size() + 1), st);
+      if (err == cudaSuccess)
+        err = cudaMemcpyAsync(dtiles[side], tl.data(), sizeof(uint2) * tl.size(), cudaMemcpyHostToDevice, st);
+      if (err != cudaSuccess) { status = cuda_status(err, "dense tiles"); break; }
+      DenseArgs da{};
+      da.tiles = dtiles[side];
+      da.n_tiles = (uint32_t)tl.size();
+      da.n_rows = side ? g->n_v : g->n_u;
+      da.n_kb = (uint32_t)(k4 / kBK);
+      da.pv_row0 = side ? g->n_u : 0;
+      da.n = g->n;
+      da.rank = rank;
+      da.nranks = nranks;
+      da.pv = per_vertex ? (unsigned long long*)g->pv : nullptr;
+      da.acc = g->d_acc + 2 * side;
+      BBF_CUDA(cudaFuncSetAttribute(k_dense_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4SmemBytes));
+      const unsigned pairs = (unsigned)std::min<uint64_t>(g->num_sms / 2, tl.size());
+      k_dense_f4<<<2 * pairs, kThreads, kF4SmemBytes, st>>>(fAi, fSi, fAj, fSj, da);
+      g->launches++;
+      const double nr = side ? g->n_v : g->n_u, kk = side ? g->n_u : g->n_v;
+      ops += 2.0 * 2.0 * (nr * (nr - 1.0) / 2.0) * kk;
+      err = cudaGetLastError();
+      if (err != cudaSuccess) { status = cuda_status(err, "k_dense_f4 launch"); break; }
+      continue;
+    }
     CUtensorMap mAi, mSi, mAj, mSj;
     bool ok = pair_kernel ? (make_map(&mAi, A, rows_pad, k, 128) && make_map(&mSi, S, rows_pad, k, 128))
                           : (make_map(&mAi, A, rows_pad, k, kBM) && make_map(&mSi, S, rows_pad, k, kBM) &&
