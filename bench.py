@@ -310,7 +310,23 @@ def main():
 
     (hbm_peak, hbm_src), (i8_peak, i8_src) = peaks()
     kms = float(np.mean(main_ms)) if main_ms else 0.0
-    if algo_ops > 0:  # dense int8 tensor-core path (k_dense_tiles)
+    # the dense path runs on the block-scaled FP4 tensor cores when the rows' max degree keeps
+    # the fp32 accumulation exact (<= 8192, csrc/dense_i8.cu), else on the int8 ones
+    maxdeg = int(max(np.diff(g.row_ptr.astype(np.int64)).max(initial=0),
+                     np.bincount(g.col, minlength=1).max(initial=0)))
+    f4 = maxdeg <= 8192 and not os.environ.get("BBF_DENSE_I8")
+    if algo_ops > 0 and f4:
+        achieved = algo_ops / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
+        f4_peak = 2.0 * i8_peak  # measured bf16 burst x 4 (nominal fp4 / bf16 = 9 / 2.25)
+        roof = {"bound": "tensor",
+                "kernel": "k_dense_f4 (tcgen05.mma.cta_group::2 kind::mxf4, e2m1 operands, T=AA^T and P=SS^T)",
+                "achieved": achieved, "peak": f4_peak,
+                "peak_source": i8_src.replace("x 2 (nominal int8/bf16 ratio 4.5/2.25)", "x 4 (nominal fp4/bf16 ratio 9/2.25)"),
+                "unit": "TOP/s (fp4, ops = 2 per MAC of the exact integer products)",
+                "frac": achieved / f4_peak, "traffic": ncu_traffic(args.config, "k_dense_f4"),
+                "nominal_peak": 9000.0, "frac_of_nominal": achieved / 9000.0,
+                "algo_ops_per_launch": algo_ops, "kernels_per_step": 2}
+    elif algo_ops > 0:  # dense int8 tensor-core path (k_dense_pair)
         achieved = algo_ops / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
         roof = {"bound": "tensor",
                 "kernel": "k_dense_pair (tcgen05.mma.cta_group::2 kind::i8, T=AA^T and P=SS^T)",
@@ -328,12 +344,14 @@ def main():
                 "frac": achieved / hbm_peak, "traffic": ncu_traffic(args.config, "k_t3"),
                 "algo_bytes_per_launch": algo_bytes}
     roof.update({"ms_per_launch": kms, "share_of_step": kms / ms_step if ms_step else None})
+    dtype = ("e2m1 x e2m1 -> fp32 (exact integers) + uint64" if algo_ops > 0 and f4 else
+             "int8 x int8 -> int32 + uint64" if algo_ops > 0 else "uint32 + uint64")
 
     line = {
         "metric": METRIC, "value": value, "unit": "wedges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "strong" if world > 1 else "strong",
-        "vs_baseline": None, "dtype": "uint32+uint64", "data": "synthetic",
+        "vs_baseline": None, "dtype": dtype, "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "counts": "global + per-vertex (both sides)",
                    "wedges_G": W_G, "balanced": tot["balanced"], "unbalanced": tot["unbalanced"],
                    "step": "bbf_graph_load_csr(device CSR) + bbf_count_per_vertex + free",

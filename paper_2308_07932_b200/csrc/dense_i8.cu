@@ -852,13 +852,28 @@ __global__ void k_dense_fill(const uint32_t* __restrict__ off, const uint32_t* _
   }
 }
 
+// 16 u8 operand bytes (0, 1 or 0xFF) -> 8 bytes of e2m1 pairs (element 2b in the low nibble):
+// 0 -> 0x0, +1 -> 0x2 (1.0), -1 -> 0xA (-1.0)
+__device__ __forceinline__ uint2 pack_e2m1(const uint4 q) {
+  const uint32_t iw[4] = {q.x, q.y, q.z, q.w};
+  uint32_t w[2] = {0u, 0u};
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const uint32_t v = (iw[e >> 2] >> (8 * (e & 3))) & 0xFFu;
+    const uint32_t nib = v == 1u ? 0x2u : (v == 0xFFu ? 0xAu : 0u);
+    w[e >> 3] |= nib << (4 * (e & 7));
+  }
+  return make_uint2(w[0], w[1]);
+}
+
 // A_U and S_U straight from the input U-side CSR, one CTA per rank row: the row is assembled in
 // shared memory (A = 1, S = +1 / -1 per edge; weight 1 = +1, 0 = -1) and
 // written out with 16-byte stores, so the operands need no memset and no scattered byte stores
 __global__ void k_dense_rows(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ col,
                              const uint8_t* __restrict__ sg, uint32_t n_u, const uint32_t* __restrict__ inv,
                              const uint32_t* __restrict__ lr_v, uint8_t* __restrict__ Au,
-                             uint8_t* __restrict__ Su, uint32_t ku, unsigned long long* __restrict__ nz) {
+                             uint8_t* __restrict__ Su, uint32_t ku, unsigned long long* __restrict__ nz,
+                             uint8_t* __restrict__ A4, uint8_t* __restrict__ S4, uint32_t k4) {
   extern __shared__ uint4 rowbuf[];
   uint8_t* ba = reinterpret_cast<uint8_t*>(rowbuf);
   uint8_t* bs = ba + ku;
@@ -867,6 +882,11 @@ __global__ void k_dense_rows(const uint64_t* __restrict__ rp, const uint32_t* __
   uint4* s4 = reinterpret_cast<uint4*>(Su + (uint64_t)r * ku);
   if (r >= n_u) {  // padding rows
     for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) { a4[i] = make_uint4(0u, 0u, 0u, 0u); s4[i] = a4[i]; }
+    if (A4)
+      for (uint32_t i = threadIdx.x; i < k4 / 8; i += blockDim.x) {
+        reinterpret_cast<uint2*>(A4 + (uint64_t)r * k4)[i] = make_uint2(0u, 0u);
+        reinterpret_cast<uint2*>(S4 + (uint64_t)r * k4)[i] = make_uint2(0u, 0u);
+      }
     return;
   }
   for (uint32_t i = threadIdx.x; i < 2 * n16; i += blockDim.x) rowbuf[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -887,6 +907,12 @@ __global__ void k_dense_rows(const uint64_t* __restrict__ rp, const uint32_t* __
   }
   ones = __reduce_add_sync(0xffffffffu, ones);
   if ((threadIdx.x & 31) == 0 && ones) atomicAdd(nz, (unsigned long long)ones);
+  if (A4)  // the FP4 path's packed copy of the row (zero beyond the u8 row)
+    for (uint32_t i = threadIdx.x; i < k4 / 8; i += blockDim.x) {
+      const bool in = 16u * i < ku;
+      reinterpret_cast<uint2*>(A4 + (uint64_t)r * k4)[i] = in ? pack_e2m1(rowbuf[i]) : make_uint2(0u, 0u);
+      reinterpret_cast<uint2*>(S4 + (uint64_t)r * k4)[i] = in ? pack_e2m1(rowbuf[n16 + i]) : make_uint2(0u, 0u);
+    }
 }
 
 // Av = Au^T and Sv = Su^T, 64 x 64 byte tiles: each thread loads a 4 x 4 byte block (four 4-byte
@@ -905,7 +931,8 @@ __device__ __forceinline__ void transpose4x4(uint32_t (&w)[4]) {
 __global__ void __launch_bounds__(256) k_dense_transpose(const uint8_t* __restrict__ Au,
                                                          const uint8_t* __restrict__ Su, uint32_t ku,
                                                          uint8_t* __restrict__ Av, uint8_t* __restrict__ Sv,
-                                                         uint32_t kv) {
+                                                         uint32_t kv, uint8_t* __restrict__ Av4,
+                                                         uint8_t* __restrict__ Sv4, uint32_t kv4) {
   __shared__ uint32_t ta[64][17], ts[64][17];
   const uint32_t r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;  // tile of Av: rows r0.., cols c0..
   const uint32_t t = threadIdx.x, bi = t >> 4, bj = t & 15;   // source rows c0 + 4 bi.., bytes r0 + 4 bj..
@@ -925,8 +952,15 @@ __global__ void __launch_bounds__(256) k_dense_transpose(const uint8_t* __restri
   __syncthreads();
   const uint32_t orow = t >> 2, oq = (t & 3) * 4;  // destination row r0 + orow, words oq .. oq + 3
   const uint64_t dst = (uint64_t)(r0 + orow) * kv + c0 + 4 * oq;
-  *reinterpret_cast<uint4*>(Av + dst) = make_uint4(ta[orow][oq], ta[orow][oq + 1], ta[orow][oq + 2], ta[orow][oq + 3]);
-  *reinterpret_cast<uint4*>(Sv + dst) = make_uint4(ts[orow][oq], ts[orow][oq + 1], ts[orow][oq + 2], ts[orow][oq + 3]);
+  const uint4 qa = make_uint4(ta[orow][oq], ta[orow][oq + 1], ta[orow][oq + 2], ta[orow][oq + 3]);
+  const uint4 qs = make_uint4(ts[orow][oq], ts[orow][oq + 1], ts[orow][oq + 2], ts[orow][oq + 3]);
+  *reinterpret_cast<uint4*>(Av + dst) = qa;
+  *reinterpret_cast<uint4*>(Sv + dst) = qs;
+  if (Av4) {  // packed e2m1 copy (16 columns -> 8 bytes)
+    const uint64_t d4 = (uint64_t)(r0 + orow) * kv4 + (c0 + 4 * oq) / 2;
+    *reinterpret_cast<uint2*>(Av4 + d4) = pack_e2m1(qa);
+    *reinterpret_cast<uint2*>(Sv4 + d4) = pack_e2m1(qs);
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -985,7 +1019,9 @@ bool dense_preferred(bbf_graph* g, bool per_vertex) {
   const double nu = g->n_u, nv = g->n_v;
   const double cu = nu * nu * round_up(g->n_v, kBK), cv = nv * nv * round_up(g->n_u, kBK);
   const double ops = 2.0 * (per_vertex ? cu + cv : std::min(cu, cv));
-  const double t_dense = ops / 2.5e15 + 1e-4;
+  // measured rates: the FP4 kernel ~5e15 int-ops/s (exact while max degree <= 8192), int8 ~3.5e15
+  const bool f4 = std::max(g->maxdeg[0], g->maxdeg[1]) <= 8192u && !getenv("BBF_DENSE_I8");
+  const double t_dense = ops / (f4 ? 5.0e15 : 3.5e15) + 1e-4;
   const double w = g->wg_valid ? (double)g->W_G : (double)g->plan_g.W_pruned;
   const double t_sparse = w / 2.0e11 + 1e-4;
   return t_dense < t_sparse;
@@ -1023,10 +1059,23 @@ bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32
     const int smem = 2 * (int)ku;
     if (smem > 48 * 1024)
       BBF_CUDA(cudaFuncSetAttribute(k_dense_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    // FP4 copies for the sides whose rows' max degree keeps the fp32 accumulation exact
+    for (int s2 = 0; s2 < 2; ++s2) {
+      if (g->maxdeg[s2] > 8192u || getenv("BBF_DENSE_I8") || g->dA4[s2]) continue;
+      const uint64_t k4 = round_up(g->dk[s2], 256) / 2;
+      BBF_CUDA(dmalloc(&g->dA4[s2], g->drows[s2] * k4, st));
+      BBF_CUDA(dmalloc(&g->dS4[s2], g->drows[s2] * k4, st));
+      g->dk4[s2] = k4;
+      if (s2 == 1 && 2 * k4 > g->dk[1]) {  // the transpose leaves the padding columns unwritten
+        BBF_CUDA(cudaMemsetAsync(g->dA4[1], 0, g->drows[1] * k4, st));
+        BBF_CUDA(cudaMemsetAsync(g->dS4[1], 0, g->drows[1] * k4, st));
+      }
+    }
     k_dense_rows<<<(unsigned)g->drows[0], 256, smem, st>>>(d_rp, d_col, d_sg, g->n_u, g->inv, g->lr + g->n_u,
-                                                          g->dA[0], g->dS[0], ku, d_nz);
-    k_dense_transpose<<<dim3(kv / 64, (unsigned)(g->drows[1] / 64)), 256, 0, st>>>(g->dA[0], g->dS[0], ku,
-                                                                                g->dA[1], g->dS[1], kv);
+                                                          g->dA[0], g->dS[0], ku, d_nz, g->dA4[0], g->dS4[0],
+                                                          (uint32_t)g->dk4[0]);
+    k_dense_transpose<<<dim3(kv / 64, (unsigned)(g->drows[1] / 64)), 256, 0, st>>>(
+        g->dA[0], g->dS[0], ku, g->dA[1], g->dS[1], kv, g->dA4[1], g->dS4[1], (uint32_t)g->dk4[1]);
     g->launches += 2;
   }
   {
