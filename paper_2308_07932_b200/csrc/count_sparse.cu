@@ -417,7 +417,6 @@ __device__ __forceinline__ void t3_chunk(const uint32_t (&ev)[kCE], uint32_t vm,
       sh_red_add_if(cbase + (ev[j] & kCpAddrMask), 1u << ((ev[j] >> shamt) & 31u), vm & (1u << j));
     return;
   }
-#ifndef BBF_T3_BM_ATOM
   if (CP && MODE == 1) {  // pass 1 with the touched-word bitmap: fire-and-forget add and bit-or
     const uint32_t bmbase = (uint32_t)__cvta_generic_to_shared(bm);
 #pragma unroll
@@ -428,7 +427,6 @@ __device__ __forceinline__ void t3_chunk(const uint32_t (&ev)[kCE], uint32_t vm,
     }
     return;
   }
-#endif
   if (CP && MODE == 2) {  // pass 2: predicated loads; sum of own-class counts minus #entries
     uint32_t own = 0, oth = 0;
 #pragma unroll
@@ -457,34 +455,6 @@ __device__ __forceinline__ void t3_chunk(const uint32_t (&ev)[kCE], uint32_t vm,
   }
 }
 
-// One flattened step of a record batch: lane L takes chunk base + L; its owner is the last record
-// starting at or before it in this step (start bitmask + per-warp owner table), else the owner
-// carried over from the previous step.
-struct StepMeta {
-  uint32_t c, ch, p, len, wv, ow, gs, smask;
-};
-
-__device__ __forceinline__ StepMeta step_lookup(uint32_t base, uint32_t nch, uint32_t excl, const Rec& rc,
-                                                int& carry, uint8_t* own, int lane) {
-  StepMeta m;
-  const bool st = nch > 0 && excl >= base && excl < base + 32;
-  if (st) own[excl - base] = (uint8_t)lane;
-  m.smask = __reduce_or_sync(0xffffffffu, st ? 1u << (excl - base) : 0u);
-  __syncwarp();
-  const uint32_t mm = m.smask & (0xffffffffu >> (31 - lane));
-  m.gs = mm ? 31 - __clz(mm) : 0;
-  m.ow = mm ? (uint32_t)own[m.gs] : (uint32_t)carry;
-  __syncwarp();
-  carry = __shfl_sync(0xffffffffu, (int)m.ow, 31);
-  const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, m.ow);
-  m.p = __shfl_sync(0xffffffffu, rc.p, m.ow);
-  m.len = __shfl_sync(0xffffffffu, rc.len, m.ow);
-  m.wv = __shfl_sync(0xffffffffu, rc.wv, m.ow);
-  m.c = base + lane;
-  m.ch = m.p / kCE + (m.c - o_excl);
-  return m;
-}
-
 template <bool PV, bool PAIRS, int ENC>
 __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) {
   constexpr bool WIDE = ENC == kEncWide, CP = ENC == kEncCompact;
@@ -495,7 +465,6 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
   uint32_t* sh_wc = sh_cnt + kMaxWin;     // kMaxWin wedge counts
   __shared__ uint32_t sh_unit, sh_c[4];
   __shared__ uint32_t sh_acc[kT3Warps][2][32];  // per-warp pass-2 accumulators of a batch
-  __shared__ uint8_t sh_own[kT3Warps][32];      // per-warp owner table of a flattened step
   __shared__ Zones sh_z;                        // the current unit's end-side zone table
   const uint32_t* __restrict__ adjc = a.adjc;
   __shared__ unsigned long long sh_red[2][kT3Warps];
@@ -653,12 +622,11 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           if (cnt == 0) break;
           fetch(cnt_next, rc_next);
           if (pass == 1) { sh_acc[warp][0][lane] = 0; sh_acc[warp][1][lane] = 0; __syncwarp(); }
-          // The batch's records are flattened over the lanes in 16-B chunks of the adjacency
-          // (4 entries, one LDG.128 per lane, consecutive lanes on consecutive chunks of a
+          // The batch's records are flattened over the lanes in 32-B chunks of the adjacency
+          // (kCE = 8 entries, two LDG.128 per lane, consecutive lanes on consecutive chunks of a
           // record; a record's first / last chunk is masked to [p, p + len)).  Step `base` gives
-          // lane L chunk base + L; its owner (the record holding it) is the last record starting
-          // at or before it in this step (start bitmask + owner table), else the owner carried
-          // over from the previous step.
+          // lane L chunk base + L; its owner (the record holding it) = the records started before
+          // the step + the popcount of the step's record-start mask up to the lane, minus one.
           const uint32_t nch = rc.len ? (rc.p + rc.len + kCE - 1) / kCE - rc.p / kCE : 0;
           const uint32_t incl = warp_incl_scan(nch, lane), excl = incl - nch;
           const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
@@ -669,66 +637,6 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             atomicAdd(&sh_dbg[1], (unsigned long long)T);
           }
 #endif
-#ifdef BBF_T3_PREFETCH
-          // software pipeline: step base + 32's owner lookup and chunk loads are issued before
-          // step base's counter updates (needs the registers of <= 768 threads per CTA)
-          StepMeta cur{}, nxt{};
-          uint4 qc[kCE / 4], qn[kCE / 4];
-          if (T) {
-            cur = step_lookup(0, nch, excl, rc, carry, sh_own[warp], lane);
-#pragma unroll
-            for (int h = 0; h < (int)(kCE / 4); ++h)
-              qc[h] = cur.c < T ? reinterpret_cast<const uint4*>(adjc)[cur.ch * (kCE / 4) + h] : make_uint4(0u, 0u, 0u, 0u);
-          }
-          for (uint32_t base = 0; base < T; base += 32) {
-            if (base + 32 < T) {
-              nxt = step_lookup(base + 32, nch, excl, rc, carry, sh_own[warp], lane);
-#pragma unroll
-              for (int h = 0; h < (int)(kCE / 4); ++h)
-                qn[h] = nxt.c < T ? reinterpret_cast<const uint4*>(adjc)[nxt.ch * (kCE / 4) + h] : make_uint4(0u, 0u, 0u, 0u);
-            }
-            const uint32_t c = cur.c;
-            const uint32_t shamt = 22u + 5u * (cur.wv >> 31), oshamt = 49u - shamt;
-            uint32_t cb = 0, cn = 0;
-            if (c < T) {
-              const uint32_t e0 = kCE * cur.ch;
-              uint32_t ev[kCE];
-#pragma unroll
-              for (int h = 0; h < (int)(kCE / 4); ++h) {
-                ev[4 * h] = qc[h].x; ev[4 * h + 1] = qc[h].y; ev[4 * h + 2] = qc[h].z; ev[4 * h + 3] = qc[h].w;
-              }
-#pragma unroll
-              for (int j = 0; j < (int)kCE; ++j) {
-                const uint32_t e = e0 + j;
-                if (e >= cur.p && e < cur.p + cur.len) {
-                  if (CP) {
-                    if (pass == 1) t3_share_cp(cbase, ev[j], shamt, oshamt, cb, cn);
-                    else if (dense) t3_inc_cp<false>(cbase, bm, word0, ev[j], shamt);
-                    else t3_inc_cp<true>(cbase, bm, word0, ev[j], shamt);
-                  } else {
-                    if (pass == 1) t3_share_c<WIDE>(ctr, word0, ev[j], cur.wv, cb, cn);
-                    else if (dense) t3_inc_c<WIDE, false>(ctr, bm, word0, ev[j], cur.wv);
-                    else t3_inc_c<WIDE, true>(ctr, bm, word0, ev[j], cur.wv);
-                  }
-                }
-              }
-            }
-            if (pass == 1 && __any_sync(0xffffffffu, (cb | cn) != 0)) {
-              const uint32_t ib = warp_incl_scan(cb, lane), in = warp_incl_scan(cn, lane);
-              const int src = cur.gs > 0 ? (int)cur.gs - 1 : 0;
-              const uint32_t pb = __shfl_sync(0xffffffffu, ib, src), pn = __shfl_sync(0xffffffffu, in, src);
-              const bool last = c < T && (c + 1 == T || lane == 31 || ((cur.smask >> (lane + 1)) & 1u));
-              if (last) {
-                sh_acc[warp][0][cur.ow] += ib - (cur.gs > 0 ? pb : 0u);
-                sh_acc[warp][1][cur.ow] += in - (cur.gs > 0 ? pn : 0u);
-              }
-              __syncwarp();
-            }
-            cur = nxt;
-#pragma unroll
-            for (int h = 0; h < (int)(kCE / 4); ++h) qc[h] = qn[h];
-          }
-#else
           // kU steps per iteration: owner lookups first, then all chunk loads in flight, then
           // the counter updates (hides the global-load latency behind the other steps' work)
           for (uint32_t base0 = 0; base0 < T; base0 += 32 * kU) {
@@ -755,11 +663,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             for (int u = 0; u < kU; ++u)
 #pragma unroll
               for (int h = 0; h < kCE / 4; ++h)
-#if defined(BBF_T3_EXPT) && BBF_T3_EXPT == 2
-                q[u][h] = (base0 + 32 * u + lane < T) ? make_uint4(word0 + (((ch[u] * 2654435761u + h * 40503u) >> 8) & 0x3FFFu), word0 + (((ch[u] * 2654435761u + h * 40503u) >> 11) & 0x3FFFu), word0 + (((ch[u] * 2654435761u + h * 40503u) >> 14) & 0x3FFFu), word0 + (((ch[u] * 2654435761u + h * 40503u) >> 17) & 0x3FFFu))
-#else
                 q[u][h] = (base0 + 32 * u + lane < T) ? reinterpret_cast<const uint4*>(adjc)[ch[u] * (kCE / 4) + h]
-#endif
                                                      : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
@@ -796,7 +700,6 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
               }
             }
           }
-#endif
           if (pass == 1) {
             __syncwarp();
             const uint32_t cb = sh_acc[warp][0][lane], cn = sh_acc[warp][1][lane];
