@@ -318,12 +318,16 @@ def main():
     if algo_ops > 0 and f4:
         achieved = algo_ops / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
         f4_peak = 2.0 * i8_peak  # measured bf16 burst x 4 (nominal fp4 / bf16 = 9 / 2.25)
+        kname = ("k_dense_f4q (tcgen05.mma.cta_group::2 kind::mxf4, e2m1 operands, one accumulator "
+                 "Q = T + 2048 P via block scales, double-buffered TMEM)" if maxdeg < 2048 and
+                 not os.environ.get("BBF_DENSE_F4_TP") else
+                 "k_dense_f4 (tcgen05.mma.cta_group::2 kind::mxf4, e2m1 operands, T=AA^T and P=SS^T)")
         roof = {"bound": "tensor",
-                "kernel": "k_dense_f4 (tcgen05.mma.cta_group::2 kind::mxf4, e2m1 operands, T=AA^T and P=SS^T)",
+                "kernel": kname,
                 "achieved": achieved, "peak": f4_peak,
                 "peak_source": i8_src.replace("x 2 (nominal int8/bf16 ratio 4.5/2.25)", "x 4 (nominal fp4/bf16 ratio 9/2.25)"),
                 "unit": "TOP/s (fp4, ops = 2 per MAC of the exact integer products)",
-                "frac": achieved / f4_peak, "traffic": ncu_traffic(args.config, "k_dense_f4"),
+                "frac": achieved / f4_peak, "traffic": ncu_traffic(args.config, kname.split()[0]),
                 "nominal_peak": 9000.0, "frac_of_nominal": achieved / 9000.0,
                 "algo_ops_per_launch": algo_ops, "kernels_per_step": 2}
     elif algo_ops > 0:  # dense int8 tensor-core path (k_dense_pair)

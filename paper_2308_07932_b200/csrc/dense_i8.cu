@@ -780,6 +780,217 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// ====================================================== FP4, one packed accumulator (k_dense_f4q)
+// When the rows' max degree is < 2048, T and P are produced by ONE accumulation over a K axis of
+// twice the length: the first half multiplies A_i by A_j with unit block scales, the second S_i by
+// S_j with block scales 2^5 (A operand) and 2^6 (B operand), so the accumulator holds
+// Q = T + 2048 P exactly (|Q| < 2^22, integer fp32 sums), decoded as P = floor(Q / 2048),
+// T = Q - 2048 P (T in [0, 2047]).  One 224-column accumulator per tile leaves room for TWO in
+// TMEM: tile t+1 accumulates into the other buffer while the epilogue drains tile t.
+constexpr uint32_t kQStages = 6;
+constexpr uint32_t kQStageBytes = 2 * kPHalf;     // i operand (128 rows), j operand (112-row slot)
+constexpr size_t kQSmemBytes = kQStages * kQStageBytes + 1024 + 2 * kBN * 8 + 256;
+constexpr uint32_t kQSf1 = 2 * kF4N, kQSfA = kQSf1 + 16, kQSfB = kQSf1 + 32;  // scale regions
+
+__device__ __forceinline__ void mma_f4q(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t sfa, uint32_t sfb,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdescF4), "r"(acc), "r"(sfa), "r"(sfb)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_dense_f4q(const __grid_constant__ CUtensorMap mAi, const __grid_constant__ CUtensorMap mSi,
+                const __grid_constant__ CUtensorMap mAj, const __grid_constant__ CUtensorMap mSj,
+                const DenseArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned long long* colB = reinterpret_cast<unsigned long long*>(smem + kQStages * kQStageBytes);
+  unsigned long long* colN = colB + kBN;
+  __shared__ __align__(8) uint64_t bar_full[kQStages], bar_empty[kQStages], bar_tfull[2], bar_tempty[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const uint32_t nk = 2 * a.n_kb;  // K steps: A half, then S half
+
+  for (uint32_t i = threadIdx.x; i < 2 * kBN; i += kThreads) colB[i] = 0;
+  if (threadIdx.x == 0) {
+    for (uint32_t st = 0; st < kQStages; ++st) {
+      mbar_init(smem_u32(&bar_full[st]), 1);
+      mbar_init(smem_u32(&bar_empty[st]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&bar_tfull[b]), 1);
+      mbar_init(smem_u32(&bar_tempty[b]), 2 * 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tmem_base_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  if (warp >= kEpiWarp0) {  // scale regions: 2^0 everywhere, 2^5 (0x84) and 2^6 (0x85)
+    const uint32_t lb = tmem + (((uint32_t)(warp & 3) * 32) << 16);
+    tmem_st16_const(lb + kQSf1, 0x7F7F7F7Fu);
+    tmem_st16_const(lb + kQSfA, 0x84848484u);
+    tmem_st16_const(lb + kQSfB, 0x85858585u);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAi)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mSi)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAj)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mSj)) : "memory");
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t t = pair * a.nranks + a.rank; t < a.n_tiles; t += npairs * a.nranks) {
+        const uint2 tile = a.tiles[t];
+        const int32_t ri = (int32_t)(tile.x * kPB + crank * 128);
+        const int32_t rj = (int32_t)(tile.y * kF4N + crank * kF4JRows);
+        for (uint32_t kb = 0; kb < nk; ++kb) {
+          mbar_wait(smem_u32(&bar_empty[stage]), phase ^ 1u);
+          const uint32_t fb = mapa_rank(smem_u32(&bar_full[stage]), 0);
+          if (leader) mbar_arrive_expect_tx(smem_u32(&bar_full[stage]), 2 * (kPHalf + kF4JRows * kBK));
+          const uint32_t base = smem_u32(smem + stage * kQStageBytes);
+          const bool shalf = kb >= a.n_kb;
+          const int32_t k0 = (int32_t)((shalf ? kb - a.n_kb : kb) * kBK);
+          tma_load_2d_pair(base, shalf ? &mSi : &mAi, fb, k0, ri);
+          tma_load_2d_pair(base + kPHalf, shalf ? &mSj : &mAj, fb, k0, rj);
+          if (++stage == kQStages) { stage = 0; phase ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      uint32_t stage = 0, phase = 0, lt = 0;
+      for (uint32_t t = pair * a.nranks + a.rank; t < a.n_tiles; t += npairs * a.nranks, ++lt) {
+        const uint32_t b = lt & 1u;
+        if (lt >= 2) {
+          mbar_wait(smem_u32(&bar_tempty[b]), ((lt >> 1) - 1) & 1u);
+          tc_fence_after();
+        }
+        const uint32_t dq = tmem + b * kF4N;
+        for (uint32_t kb = 0; kb < nk; ++kb) {
+          mbar_wait(smem_u32(&bar_full[stage]), phase);
+          tc_fence_after();
+          const uint32_t base = smem_u32(smem + stage * kQStageBytes);
+          const bool shalf = kb >= a.n_kb;
+          const uint32_t sfa = tmem + (shalf ? kQSfA : kQSf1), sfb = tmem + (shalf ? kQSfB : kQSf1);
+#pragma unroll
+          for (uint32_t kk = 0; kk < kBK / 32; ++kk) {  // 32 B = 64 e2m1 values per MMA
+            const uint32_t off = kk * 32;
+            mma_f4q(dq, smem_desc(base + off), smem_desc(base + kPHalf + off), sfa, sfb, (kb | kk) ? 1u : 0u);
+          }
+          mma_commit_pair(smem_u32(&bar_empty[stage]));
+          if (++stage == kQStages) { stage = 0; phase ^= 1u; }
+        }
+        mma_commit_pair(smem_u32(&bar_tfull[b]));
+      }
+    }
+  } else {
+    const uint32_t q = (uint32_t)(warp & 3);
+    const uint32_t etid = threadIdx.x - kEpiWarp0 * 32;
+    unsigned long long totB = 0, totN = 0;
+    uint32_t lt = 0;
+    for (uint32_t t = pair * a.nranks + a.rank; t < a.n_tiles; t += npairs * a.nranks, ++lt) {
+      const uint32_t b = lt & 1u;
+      const uint2 tile = a.tiles[t];
+      const uint32_t i = tile.x * kPB + crank * 128 + q * 32 + lane;  // this thread's row
+      const uint32_t j0 = tile.y * kF4N;
+      mbar_wait(smem_u32(&bar_tfull[b]), (lt >> 1) & 1u);
+      tc_fence_after();
+      unsigned long long rB = 0, rN = 0;
+#pragma unroll 1
+      for (uint32_t c = 0; c < kF4N / 32; ++c) {
+        uint32_t qv[32];
+        tmem_ld32(tmem + ((q * 32) << 16) + b * kF4N + c * 32, qv);
+        tmem_wait_ld();
+        unsigned long long vb[32], vn[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int32_t qq = __float2int_rn(__int_as_float((int)qv[e]));
+          const int32_t pp = qq >> 11;                          // floor(Q / 2048)
+          const uint32_t tt = (uint32_t)(qq - (pp << 11));      // in [0, 2047]
+          const uint32_t ad = (tt + (uint32_t)pp) >> 1, dd = (tt - (uint32_t)pp) >> 1;
+          uint32_t fb = ((ad * (ad - 1u)) >> 1) + ((dd * (dd - 1u)) >> 1);
+          uint32_t fn = ad * dd;
+          if (j0 + c * 32 + (uint32_t)e <= i) { fb = 0; fn = 0; }  // pairs i < j only
+          rB += fb;
+          rN += fn;
+          vb[e] = fb;
+          vn[e] = fn;
+        }
+        if (a.pv) {
+          xpose_step<16>(vb, lane); xpose_step<16>(vn, lane);
+          xpose_step<8>(vb, lane);  xpose_step<8>(vn, lane);
+          xpose_step<4>(vb, lane);  xpose_step<4>(vn, lane);
+          xpose_step<2>(vb, lane);  xpose_step<2>(vn, lane);
+          xpose_step<1>(vb, lane);  xpose_step<1>(vn, lane);
+          if (vb[0]) atomicAdd(&colB[c * 32 + lane], vb[0]);
+          if (vn[0]) atomicAdd(&colN[c * 32 + lane], vn[0]);
+        }
+      }
+      // buffer b drained: one arrival per warp on the leader's tmem_empty[b]
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                         mapa_rank(smem_u32(&bar_tempty[b]), 0))
+                     : "memory");
+      totB += rB;
+      totN += rN;
+      if (a.pv) {
+        if ((rB | rN) && i < a.n_rows) {
+          atomicAdd(&a.pv[2ull * (a.pv_row0 + i)], rB);
+          atomicAdd(&a.pv[2ull * (a.pv_row0 + i) + 1], rN);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (uint32_t jj = etid; jj < kF4N; jj += 128) {
+          const unsigned long long bb = colB[jj], nn = colN[jj];
+          colB[jj] = 0;
+          colN[jj] = 0;
+          const uint32_t j = j0 + jj;
+          if ((bb | nn) && j < a.n_rows) {
+            atomicAdd(&a.pv[2ull * (a.pv_row0 + j)], bb);
+            atomicAdd(&a.pv[2ull * (a.pv_row0 + j) + 1], nn);
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      totB += __shfl_xor_sync(0xffffffffu, totB, o);
+      totN += __shfl_xor_sync(0xffffffffu, totN, o);
+    }
+    if (lane == 0 && (totB | totN)) {
+      atomicAdd(&a.acc[0], totB);
+      atomicAdd(&a.acc[1], totN);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
 // u8 A (0/1) / S (0, 1, 0xFF) rows -> e2m1 packed two per byte (element 2b in the low nibble):
 // 0 -> 0x0, +1 -> 0x2 (1.0), -1 -> 0xA (-1.0); bytes beyond the u8 row are zero padding
 __global__ void k_dense_pack_f4(const uint8_t* __restrict__ in, uint64_t k_in, uint8_t* __restrict__ out,
@@ -1181,9 +1392,14 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
       da.nranks = nranks;
       da.pv = per_vertex ? (unsigned long long*)g->pv : nullptr;
       da.acc = g->d_acc + 2 * side;
-      BBF_CUDA(cudaFuncSetAttribute(k_dense_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4SmemBytes));
       const unsigned pairs = (unsigned)std::min<uint64_t>(g->num_sms / 2, tl.size());
-      k_dense_f4<<<2 * pairs, kThreads, kF4SmemBytes, st>>>(fAi, fSi, fAj, fSj, da);
+      if (g->maxdeg[side] < 2048u && !getenv("BBF_DENSE_F4_TP")) {  // one packed accumulator, double-buffered
+        BBF_CUDA(cudaFuncSetAttribute(k_dense_f4q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmemBytes));
+        k_dense_f4q<<<2 * pairs, kThreads, kQSmemBytes, st>>>(fAi, fSi, fAj, fSj, da);
+      } else {
+        BBF_CUDA(cudaFuncSetAttribute(k_dense_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4SmemBytes));
+        k_dense_f4<<<2 * pairs, kThreads, kF4SmemBytes, st>>>(fAi, fSi, fAj, fSj, da);
+      }
       g->launches++;
       const double nr = side ? g->n_v : g->n_u, kk = side ? g->n_u : g->n_v;
       ops += 2.0 * 2.0 * (nr * (nr - 1.0) / 2.0) * kk;

@@ -284,6 +284,31 @@ def test_counter_encodings_agree(bbf, monkeypatch):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("m,n", [(300, 2040), (2047, 96)])
+def test_dense_fp4_packed_accumulator_near_limit(bbf, monkeypatch, m, n):
+    """The FP4 dense kernels at degrees just under the packed-accumulator limit (|Q| = |T + 2048 P|
+    up to ~2^22): all-positive K_{m,n} per-vertex closed forms, and a random-sign graph of the same
+    degrees bit-identical to the int8 tensor path (BBF_DENSE_I8) and to the two-accumulator FP4
+    kernel (BBF_DENSE_F4_TP)."""
+    c2 = lambda k: k * (k - 1) // 2
+    with bbf.Graph.from_synth(G.complete(m, n), flags=bbf.BBF_FORCE_DENSE) as h:
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+    assert tot["balanced"] == c2(m) * c2(n) and tot["unbalanced"] == 0
+    assert (bu == (m - 1) * c2(n)).all() and (bv == (n - 1) * c2(m)).all()
+    assert (nu == 0).all() and (nv == 0).all()
+    g = G.random_bipartite(m, n, 0.97, 0.5, seed=m + n)
+    with bbf.Graph.from_synth(g, flags=bbf.BBF_FORCE_DENSE) as h:
+        ref = h.count_per_vertex()
+    for env in ("BBF_DENSE_I8", "BBF_DENSE_F4_TP"):
+        monkeypatch.setenv(env, "1")
+        with bbf.Graph.from_synth(g, flags=bbf.BBF_FORCE_DENSE) as h:
+            got = h.count_per_vertex()
+        monkeypatch.delenv(env)
+        assert got[0]["balanced"] == ref[0]["balanced"] and got[0]["unbalanced"] == ref[0]["unbalanced"]
+        for x, y in zip(got[1:], ref[1:]):
+            assert np.array_equal(x, y)
+
+
 def test_upload_and_async_outputs(bbf):
     """Pipelined loading (bbf_upload_csr / bbf_graph_load_upload, the next graph's copy in flight
     while the current one counts) and BBF_OUTPUT_ASYNC host outputs give the same counts as the
