@@ -10,6 +10,6 @@ python tools/step_once.py --config 3 --steps 1 > gpurun_out/pr_step3.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:k_t3 -c 1 -o gpurun_out/pr_k_t3_c3 \
   python tools/step_once.py --config 3 --steps 1 > gpurun_out/pr_ncu3.log 2>&1
 python tools/step_once.py --config 4 --steps 1 --path dense > gpurun_out/pr_step4.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_dense_f4 -c 1 -o gpurun_out/pr_k_dense_f4_c4 \
+ncu --set full --clock-control none --import-source on -k regex:k_dense_f4 -c 1 -o gpurun_out/pr_k_dense_f4q_c4 \
   python tools/step_once.py --config 4 --steps 1 --path dense > gpurun_out/pr_ncu4.log 2>&1
 ls -la gpurun_out | grep pr_
