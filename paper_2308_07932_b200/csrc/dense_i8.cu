@@ -1165,8 +1165,10 @@ __global__ void __launch_bounds__(256) k_dense_transpose(const uint8_t* __restri
   const uint64_t dst = (uint64_t)(r0 + orow) * kv + c0 + 4 * oq;
   const uint4 qa = make_uint4(ta[orow][oq], ta[orow][oq + 1], ta[orow][oq + 2], ta[orow][oq + 3]);
   const uint4 qs = make_uint4(ts[orow][oq], ts[orow][oq + 1], ts[orow][oq + 2], ts[orow][oq + 3]);
-  *reinterpret_cast<uint4*>(Av + dst) = qa;
-  *reinterpret_cast<uint4*>(Sv + dst) = qs;
+  if (Av) {  // u8 copy (int8 kernels); skipped when only the FP4 kernels will read this side
+    *reinterpret_cast<uint4*>(Av + dst) = qa;
+    *reinterpret_cast<uint4*>(Sv + dst) = qs;
+  }
   if (Av4) {  // packed e2m1 copy (16 columns -> 8 bytes)
     const uint64_t d4 = (uint64_t)(r0 + orow) * kv4 + (c0 + 4 * oq) / 2;
     *reinterpret_cast<uint2*>(Av4 + d4) = pack_e2m1(qa);
@@ -1285,8 +1287,11 @@ bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32
     k_dense_rows<<<(unsigned)g->drows[0], 256, smem, st>>>(d_rp, d_col, d_sg, g->n_u, g->inv, g->lr + g->n_u,
                                                           g->dA[0], g->dS[0], ku, d_nz, g->dA4[0], g->dS4[0],
                                                           (uint32_t)g->dk4[0]);
+    const bool v_u8 = !g->dA4[1] || getenv("BBF_DENSE_1CTA");
     k_dense_transpose<<<dim3(kv / 64, (unsigned)(g->drows[1] / 64)), 256, 0, st>>>(
-        g->dA[0], g->dS[0], ku, g->dA[1], g->dS[1], kv, g->dA4[1], g->dS4[1], (uint32_t)g->dk4[1]);
+        g->dA[0], g->dS[0], ku, v_u8 ? g->dA[1] : nullptr, v_u8 ? g->dS[1] : nullptr, kv, g->dA4[1], g->dS4[1],
+        (uint32_t)g->dk4[1]);
+    g->dense_v_u8 = v_u8;
     g->launches += 2;
   }
   {
@@ -1329,6 +1334,7 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
         g->launches++;
       }
       g->dense_built = true;
+      g->dense_v_u8 = true;
     }
   }
   // global only: the cheaper side (cost ~ rows^2 * K); per-vertex: both sides
@@ -1353,6 +1359,13 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
     uint8_t* A = side ? Av : Au;
     uint8_t* S = side ? Sv : Su;
     const bool pair_kernel = !getenv("BBF_DENSE_1CTA");
+    const bool f4_ok = pair_kernel && !getenv("BBF_DENSE_I8") && g->maxdeg[side] <= 8192u;
+    if (side == 1 && !f4_ok && g->dense_built && !g->dense_v_u8) {  // int8 wanted: u8 V side on demand
+      k_dense_transpose<<<dim3((unsigned)(kv / 64), (unsigned)(rv / 64)), 256, 0, st>>>(
+          Au, Su, (uint32_t)ku, Av, Sv, (uint32_t)kv, nullptr, nullptr, 0u);
+      g->launches++;
+      g->dense_v_u8 = true;
+    }
     // FP4 block-scaled path when exact (|T|, |P| and every partial sum <= the rows' max degree)
     const bool f4 = pair_kernel && !getenv("BBF_DENSE_I8") && g->maxdeg[side] <= 8192u;
     if (f4) {
