@@ -115,9 +115,13 @@ __global__ void k_seg_bounds(RouteRows rr, const uint32_t* __restrict__ off,
 }
 
 // count T1 / T3 rows, W per tier, units per T3 row
-__global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, uint64_t w_target, uint64_t t2max,
-                       const uint32_t* __restrict__ mlo, const uint32_t* __restrict__ mhi,
-                       uint32_t* __restrict__ nunits, unsigned long long* __restrict__ acc) {
+// w_target = max(W_pruned / (nranks * SMs * 6 + 1), 2^16), from the device-side W_pruned (no host
+// round trip between the work reduction and the tiers)
+__global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, const unsigned long long* __restrict__ d_wp,
+                       uint64_t w_div, uint64_t t2max, const uint32_t* __restrict__ mlo,
+                       const uint32_t* __restrict__ mhi, uint32_t* __restrict__ nunits,
+                       unsigned long long* __restrict__ acc) {
+  const uint64_t wt = *d_wp / w_div, w_target = wt > (1ull << 16) ? wt : (1ull << 16);
   uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long w1 = 0, w3 = 0, m3 = 0, w2 = 0;
   uint32_t u = 0;
@@ -259,17 +263,14 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     k_seg_bounds<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(rr, g->off, g->mid, g->end1, sb, se);
     g->launches += 1;
   }
-  p->rsafe[0] = p->rsafe[1] = p->rmid[0] = p->rmid[1] = 0xffffffffu;  // no packing (route S, or empty graph)
+  uint32_t h_rs[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};  // no packing (route S, empty graph)
   if (want_pack) {  // (env BBF_NO_PACKED_END: every end / middle takes two REDs)
     uint32_t* d_rs;
     BBF_CUDA(dmalloc(&d_rs, 16, st));
     BBF_CUDA(cudaMemsetAsync(d_rs, 0, 16, st));
     k_rsafe<<<(n + 255) / 256, 256, 0, st>>>(win, g->degs, g->n_u, n, d_rs);
     g->launches += 1;
-    uint32_t h_rs[4];
-    BBF_CUDA(rb_add(h_rs, d_rs, 16, st));
-    BBF_CUDA(rb_sync(st));
-    p->rsafe[0] = h_rs[0]; p->rsafe[1] = h_rs[1]; p->rmid[0] = h_rs[2]; p->rmid[1] = h_rs[3];
+    BBF_CUDA(rb_add(h_rs, d_rs, 16, st));  // delivered by the next rb_sync
     dfree(win, st);
     dfree(d_rs, st);
   }
@@ -286,15 +287,12 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     dfree(tmp, st);
   }
   unsigned long long h_wp = 0, h_wf = 0;
-  BBF_CUDA(rb_add(&h_wp, d_wp, 8, st));
+  BBF_CUDA(rb_add(&h_wp, d_wp, 8, st));  // delivered by the next rb_sync
   BBF_CUDA(rb_add(&h_wf, &acc[0], 8, st));
-  BBF_CUDA(rb_sync(st));
-  p->W_pruned = h_wp;
-  p->W_full = h_wf;
   // hub units of ~1/6 of one SM's share of the whole job: with N ranks the share is W / (N * SMs),
   // so a rank's largest unit stays well below its per-SM work at any N
   const uint64_t nranks = g->comm ? (uint64_t)g->comm->nranks : 1ull;
-  uint64_t w_target = std::max<uint64_t>(h_wp / (nranks * (uint64_t)g->num_sms * 6ull + 1), 1ull << 16);
+  const uint64_t w_div = nranks * (uint64_t)g->num_sms * 6ull + 1;
 
   // tiers and units
   // a T2 start's distinct ends (<= its wedges) must fit the k_t2 hash at load <= 1/2
@@ -302,7 +300,7 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
       getenv("BBF_T2_MAX") ? (uint64_t)atoll(getenv("BBF_T2_MAX")) : kT2MaxDefault, kT2HugeSlots * 3 / 4);
   BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
   if (n) {
-    k_tier<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, p->work, w_target, t2max, sb, se, nunits, acc);
+    k_tier<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, p->work, d_wp, w_div, t2max, sb, se, nunits, acc);
     g->launches += 1;
   }
   BBF_CUDA(dmalloc(&p->t1, 4ull * (n + 1), st));
@@ -341,6 +339,10 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   BBF_CUDA(rb_add(&h_nunits, ustart + n, 4, st));
   BBF_CUDA(rb_add(h_acc, acc, 32, st));
   BBF_CUDA(rb_sync(st));
+  p->W_pruned = h_wp;
+  p->W_full = h_wf;
+  p->rsafe[0] = h_rs[0]; p->rsafe[1] = h_rs[1]; p->rmid[0] = h_rs[2]; p->rmid[1] = h_rs[3];
+  const uint64_t w_target = std::max<uint64_t>(h_wp / w_div, 1ull << 16);  // (debug print)
   p->n_t1 = h_nsel[0];
   p->n_t2 = h_nsel[1];
   p->n_t2s = h_nsel[2];
