@@ -264,6 +264,7 @@ struct bbf_graph {
   uint8_t* dS4[2];
   uint64_t dk4[2];            // bytes per fp4 row (K padded to 256 elements, / 2)
   bool dense_built;
+  uint32_t rb_err;       // small readback target that outlives one host round trip (build flags)
   bool dense_v_u8;     // the V side's u8 operands are written (else only its FP4 copies)
   uint32_t L4[2];     // #vertices with degree >= 2 per side
   uint32_t Llong[2];  // #vertices with degree > 32 per side ("long" middles of the hub kernel)

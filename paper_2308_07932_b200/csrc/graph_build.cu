@@ -610,16 +610,12 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     dfree(wa, st);
     dfree(wb, st);
   }
-  uint32_t h_err = 0;
-  BBF_CUDA(rb_add(&h_err, d_err, 4, st));
-  BBF_CUDA(rb_sync(st));
+  // the duplicate-edge flag is read back with the run count below (one host round trip): the
+  // steps in between are harmless on a graph that turns out to be rejected
+  g->rb_err = 0;
+  BBF_CUDA(rb_add(&g->rb_err, d_err, 4, st));
   dfree(d_err, st);
-  if (h_err & kErrDup) {
-    dfree(tmp, st);
-    cudaStreamSynchronize(st);
-    set_error("duplicate (u,v) edge");
-    return BBF_EDUP;
-  }
+  if (m == 0) BBF_CUDA(rb_sync(st));
   if (n) {
     k_cuts<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(g->off, g->adj, skey_u, skey_v, n_u, n_v,
                                                       g->L4[0], g->L4[1], g->mid, g->end1);
@@ -658,6 +654,13 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp2, ts, flag, g->runid, (int64_t)m, st));
     BBF_CUDA(rb_add(&g->nruns, g->runid + (m - 1), 4, st));
     BBF_CUDA(rb_sync(st));
+    if (g->rb_err & kErrDup) {
+      dfree(tmp2, st);
+      dfree(flag, st);
+      cudaStreamSynchronize(st);
+      set_error("duplicate (u,v) edge");
+      return BBF_EDUP;
+    }
     g->nruns += 1;
     BBF_CUDA(dmalloc(&g->runs, sizeof(uint2) * (g->nruns + 1), st));
     k_runs<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, flag, m, wshift, wmask, g->runid, g->runs);
