@@ -315,6 +315,11 @@ void dfree(void* p, cudaStream_t st);
 // synchronises the stream and then fills the host variables
 cudaError_t rb_add(void* host, const void* dev, size_t n, cudaStream_t st);
 cudaError_t rb_sync(cudaStream_t st);
+// kernels launched by one CUB device-wide call (counted in bbf_graph_stats): a radix sort over
+// `bits` key bits = histogram + exclusive sum + one onesweep pass per 8 bits; scans, selects and
+// reductions launch two kernels each
+constexpr uint32_t cub_sort_kernels(int bits) { return 2u + (uint32_t)((bits + 7) / 8); }
+constexpr uint32_t kCubScanKernels = 2, kCubSelectKernels = 2, kCubReduceKernels = 2;
 template <class T>
 inline cudaError_t dmalloc(T** out, size_t bytes, cudaStream_t st) {
   return dmalloc_raw(reinterpret_cast<void**>(out), bytes, st);

@@ -1298,7 +1298,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     g->launches++;
   }
   unsigned long long h[16];
-  BBF_CUDA(rb_add(h, g->d_acc, sizeof(h), st));
+  BBF_CUDA(rb_add(h, g->d_acc, sizeof(h), st)); g->launches++;
   BBF_CUDA(rb_sync(st));
   float ms1 = 0, ms2 = 0;
   cudaEventElapsedTime(&ms1, e0, e1);

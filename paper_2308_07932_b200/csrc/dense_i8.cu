@@ -1296,7 +1296,7 @@ bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32
   }
   {
     unsigned long long nz = 0;
-    BBF_CUDA(rb_add(&nz, d_nz, 8, st));
+    BBF_CUDA(rb_add(&nz, d_nz, 8, st)); g->launches++;
     BBF_CUDA(rb_sync(st));
     dfree(d_nz, st);
     if (nz != g->nnz) {
@@ -1463,6 +1463,7 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
   unsigned long long h[4] = {0, 0, 0, 0};
   if (status == BBF_OK) {
     cudaError_t err = rb_add(h, g->d_acc, sizeof(h), st);
+    g->launches++;
     if (err == cudaSuccess) err = rb_sync(st);
     if (err != cudaSuccess) status = cuda_status(err, "dense path");
   }

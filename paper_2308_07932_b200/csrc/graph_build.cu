@@ -375,7 +375,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   if (nnz) k_validate_edges<<<grid_for(nnz, 256), 256, 0, st>>>(d_col, d_sg, nnz, n_v, d_err);
   g->launches += 2;
   uint32_t h_err = 0;
-  BBF_CUDA(rb_add(&h_err, d_err, 4, st));
+  BBF_CUDA(rb_add(&h_err, d_err, 4, st)); g->launches++;
   BBF_CUDA(rb_sync(st));
   if (h_err) {
     dfree(d_err, st);
@@ -409,7 +409,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     k_pos_compact<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, keep, pos, d_col, d_sg, pcol, psg);
     g->launches += 5;
     uint32_t kept = 0;
-    BBF_CUDA(rb_add(&kept, pos + nnz, 4, st));
+    BBF_CUDA(rb_add(&kept, pos + nnz, 4, st)); g->launches++;
     BBF_CUDA(rb_sync(st));
     dfree(tmp0, st);
     dfree(keep, st);
@@ -452,7 +452,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   BBF_CUDA(dmalloc(&tmp, tmp_bytes + 16, st));
   if (n_u) BBF_CUDA(cub::DeviceRadixSort::SortKeysDescending(tmp, t1, key_u, skey_u, (int)n_u, 0, kbits, st));
   if (n_v) BBF_CUDA(cub::DeviceRadixSort::SortKeysDescending(tmp, t2, key_v, skey_v, (int)n_v, 0, kbits, st));
-  g->launches += 8;
+  g->launches += (n_u ? cub_sort_kernels(kbits) : 0) + (n_v ? cub_sort_kernels(kbits) : 0);
 
   BBF_CUDA(dmalloc(&g->inv, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&g->degs, 4ull * (n + 1), st));
@@ -463,7 +463,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   // row offsets: exclusive scan of degrees in row order (rows U by rank, then V by rank)
   BBF_CUDA(cudaMemsetAsync(g->degs + n, 0, 4, st));
   BBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t4, g->degs, g->off, (int)(n + 1), st));
-  g->launches += 1;
+  g->launches += kCubScanKernels;
   dfree(tmp, st);
 
   // zone boundaries per side (rank counts of degree thresholds), overflow bound
@@ -475,10 +475,10 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   k_ws<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(g->degs, n_u, n, d_cnt + 12);
   g->launches += 3;
   unsigned long long h_cnt[16];
-  BBF_CUDA(rb_add(h_cnt, d_cnt, sizeof(h_cnt), st));
+  BBF_CUDA(rb_add(h_cnt, d_cnt, sizeof(h_cnt), st)); g->launches++;
   uint32_t h_maxdeg[2] = {0, 0};
-  if (n_u) BBF_CUDA(rb_add(&h_maxdeg[0], g->degs, 4, st));
-  if (n_v) BBF_CUDA(rb_add(&h_maxdeg[1], g->degs + n_u, 4, st));
+  if (n_u) { BBF_CUDA(rb_add(&h_maxdeg[0], g->degs, 4, st)); g->launches++; }
+  if (n_v) { BBF_CUDA(rb_add(&h_maxdeg[1], g->degs + n_u, 4, st)); g->launches++; }
   BBF_CUDA(rb_sync(st));
   dfree(d_cnt, st);
   g->maxdeg[0] = h_maxdeg[0];
@@ -515,7 +515,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     if (n) k_wg_sum<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(mcnt, key_u, key_v, n_u, n, d_wg);
     g->launches += 2;
     unsigned long long wg = 0;
-    BBF_CUDA(rb_add(&wg, d_wg, 8, st));
+    BBF_CUDA(rb_add(&wg, d_wg, 8, st)); g->launches++;
     BBF_CUDA(rb_sync(st));
     dfree(mcnt, st);
     dfree(d_wg, st);
@@ -603,7 +603,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     k_transpose_keys<<<grid_for(nnz, 256), 256, 0, st>>>(kb, g->adj + nnz, nnz, n_u, g->erow + nnz, ka, wa);
     BBF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t3, ka, g->erow, wa, wb, (int)nnz, 0, bits_u, st));
     k_u_adj<<<grid_for(nnz, 256), 256, 0, st>>>(wb, nnz, g->erow, g->adj, g->rev, d_err);
-    g->launches += 13;  // k_entries, 2 CUB radix sorts (histogram, exclusive sum, 3 onesweep passes each), k_transpose_keys, k_u_adj
+    g->launches += 3 + cub_sort_kernels(bits_v) + cub_sort_kernels(bits_u);  // + k_entries, k_transpose_keys, k_u_adj
     dfree(ka, st);
     dfree(va, st);
     dfree(kb, st);
@@ -613,7 +613,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
   // the duplicate-edge flag is read back with the run count below (one host round trip): the
   // steps in between are harmless on a graph that turns out to be rejected
   g->rb_err = 0;
-  BBF_CUDA(rb_add(&g->rb_err, d_err, 4, st));
+  BBF_CUDA(rb_add(&g->rb_err, d_err, 4, st)); g->launches++;
   dfree(d_err, st);
   if (m == 0) BBF_CUDA(rb_sync(st));
   if (n) {
@@ -624,7 +624,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     BBF_CUDA(dmalloc(&d64, 8ull * n, st));
     k_u32_to_u64<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(g->degs, n, d64);
     BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp, t5, d64, g->degpre, (int)n, st));
-    g->launches += 3;
+    g->launches += 2 + kCubScanKernels;
     dfree(d64, st);
   }
   dfree(tmp, st);
@@ -652,7 +652,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     void* tmp2;
     BBF_CUDA(dmalloc(&tmp2, ts + 16, st));
     BBF_CUDA(cub::DeviceScan::InclusiveSum(tmp2, ts, flag, g->runid, (int64_t)m, st));
-    BBF_CUDA(rb_add(&g->nruns, g->runid + (m - 1), 4, st));
+    BBF_CUDA(rb_add(&g->nruns, g->runid + (m - 1), 4, st)); g->launches++;
     BBF_CUDA(rb_sync(st));
     if (g->rb_err & kErrDup) {
       dfree(tmp2, st);
@@ -666,7 +666,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
     k_runs<<<grid_for(m, 256), 256, 0, st>>>(g->adjc, flag, m, wshift, wmask, g->runid, g->runs);
     BBF_CUDA(dmalloc(&g->rlast, 4ull * (n + 1), st));
     if (n) k_rlast<<<(n + 255) / 256, 256, 0, st>>>(g->off, g->end1, g->runid, n, g->rlast);
-    g->launches += 5;
+    g->launches += 3 + kCubScanKernels;  // k_caddr, scan, k_runs, k_rlast
     dfree(tmp2, st);
     dfree(flag, st);
   } else {

@@ -270,7 +270,7 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     BBF_CUDA(cudaMemsetAsync(d_rs, 0, 16, st));
     k_rsafe<<<(n + 255) / 256, 256, 0, st>>>(win, g->degs, g->n_u, n, d_rs);
     g->launches += 1;
-    BBF_CUDA(rb_add(h_rs, d_rs, 16, st));  // delivered by the next rb_sync
+    BBF_CUDA(rb_add(h_rs, d_rs, 16, st)); g->launches++;  // delivered by the next rb_sync
     dfree(win, st);
     dfree(d_rs, st);
   }
@@ -283,12 +283,12 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     void* tmp;
     BBF_CUDA(dmalloc(&tmp, tb + 16, st));
     BBF_CUDA(cub::DeviceReduce::Sum(tmp, tb, p->work, d_wp, (int)n, st));
-    g->launches += 1;
+    g->launches += kCubReduceKernels;
     dfree(tmp, st);
   }
   unsigned long long h_wp = 0, h_wf = 0;
-  BBF_CUDA(rb_add(&h_wp, d_wp, 8, st));  // delivered by the next rb_sync
-  BBF_CUDA(rb_add(&h_wf, &acc[0], 8, st));
+  BBF_CUDA(rb_add(&h_wp, d_wp, 8, st)); g->launches++;  // delivered by the next rb_sync
+  BBF_CUDA(rb_add(&h_wf, &acc[0], 8, st)); g->launches++;
   // hub units of ~1/6 of one SM's share of the whole job: with N ranks the share is W / (N * SMs),
   // so a rank's largest unit stays well below its per-SM work at any N
   const uint64_t nranks = g->comm ? (uint64_t)g->comm->nranks : 1ull;
@@ -330,14 +330,14 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     BBF_CUDA(cub::DeviceSelect::If(tmp, tb, it, p->t2s, d_nsel + 2, (int)n, small, st));
     BBF_CUDA(cudaMemsetAsync(nunits + n, 0, 4, st));
     BBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, nunits, ustart, (int)(n + 1), st));
-    g->launches += 8;
+    g->launches += 5 * kCubSelectKernels + kCubScanKernels;
     dfree(tmp, st);
   }
   uint32_t h_nsel[5] = {0, 0, 0, 0, 0}, h_nunits = 0;
   unsigned long long h_acc[4];
-  BBF_CUDA(rb_add(h_nsel, d_nsel, 20, st));
-  BBF_CUDA(rb_add(&h_nunits, ustart + n, 4, st));
-  BBF_CUDA(rb_add(h_acc, acc, 32, st));
+  BBF_CUDA(rb_add(h_nsel, d_nsel, 20, st)); g->launches++;
+  BBF_CUDA(rb_add(&h_nunits, ustart + n, 4, st)); g->launches++;
+  BBF_CUDA(rb_add(h_acc, acc, 32, st)); g->launches++;
   BBF_CUDA(rb_sync(st));
   p->W_pruned = h_wp;
   p->W_full = h_wf;
@@ -364,7 +364,7 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
     g->launches += 1;
   }
   unsigned int h_maxmid[4] = {0, 0, 0, 0};
-  BBF_CUDA(rb_add(h_maxmid, d_maxmid, 16, st));
+  BBF_CUDA(rb_add(h_maxmid, d_maxmid, 16, st)); g->launches++;
   BBF_CUDA(rb_sync(st));
   p->max_mid = h_maxmid[0];
   p->max_work = *(unsigned long long*)(h_maxmid + 2);
