@@ -1011,42 +1011,49 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
 #pragma unroll 1
       for (uint32_t r0 = 0; r0 < m; r0 += kM) {
         const uint32_t mc = min(kM, m - r0);
-        // round set-up: two consecutive middles per thread; one CTA-wide exclusive scan of
-        // (segment length << 12 | non-empty) compacts the non-empty middles (so their first
-        // wedges strictly increase) and gives each one's first flattened wedge
-        uint32_t len2[2], wv2[2] = {0, 0}, s2[2] = {0, 0};
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const uint32_t i = 2 * tid + q;
-          len2[q] = 0;
-          if (i < mc) {
-            wv2[q] = a.adj[m_lo + r0 + i];
-            s2[q] = a.ub[m_lo + r0 + i];
-            const uint32_t en = a.end1[ob + (wv2[q] & kMask)];
-            len2[q] = en > s2[q] ? en - s2[q] : 0;
-          }
-        }
-        const uint32_t tsum = ((len2[0] + len2[1]) << 12) | ((len2[0] > 0) + (len2[1] > 0));
-        const uint32_t wincl = warp_incl_scan(tsum, lane);
-        if (lane == 31) sh_wsum[warp] = wincl;
-        __syncthreads();
-        uint32_t wbase = 0;
-        for (int w2 = 0; w2 < warp; ++w2) wbase += sh_wsum[w2];
-        const uint32_t ex = wbase + wincl - tsum;  // (wedges before << 12) | non-empty middles before
-        {
-          uint32_t k = ex & 0xfffu, pos = ex >> 12;
-#pragma unroll
+        if (pass == 1 && m <= kM) {
+          // single-round start: pass 2 reuses pass 1's middle table (mS, mW, mP are only read by
+          // the steps); just clear the per-middle share totals
+          for (uint32_t i2 = tid; i2 < sh_mcc; i2 += kT2Threads) { mB[i2] = 0; mN[i2] = 0; }
+          __syncthreads();
+        } else {
+          // round set-up: two consecutive middles per thread; one CTA-wide exclusive scan of
+          // (segment length << 12 | non-empty) compacts the non-empty middles (so their first
+          // wedges strictly increase) and gives each one's first flattened wedge
+          uint32_t len2[2], wv2[2] = {0, 0}, s2[2] = {0, 0};
+  #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            if (len2[q]) {
-              mP[k] = pos; mS[k] = s2[q]; mW[k] = wv2[q];
-              if (pass == 1) { mB[k] = 0; mN[k] = 0; }
-              ++k;
-              pos += len2[q];
+            const uint32_t i = 2 * tid + q;
+            len2[q] = 0;
+            if (i < mc) {
+              wv2[q] = a.adj[m_lo + r0 + i];
+              s2[q] = a.ub[m_lo + r0 + i];
+              const uint32_t en = a.end1[ob + (wv2[q] & kMask)];
+              len2[q] = en > s2[q] ? en - s2[q] : 0;
             }
           }
+          const uint32_t tsum = ((len2[0] + len2[1]) << 12) | ((len2[0] > 0) + (len2[1] > 0));
+          const uint32_t wincl = warp_incl_scan(tsum, lane);
+          if (lane == 31) sh_wsum[warp] = wincl;
+          __syncthreads();
+          uint32_t wbase = 0;
+          for (int w2 = 0; w2 < warp; ++w2) wbase += sh_wsum[w2];
+          const uint32_t ex = wbase + wincl - tsum;  // (wedges before << 12) | non-empty middles before
+          {
+            uint32_t k = ex & 0xfffu, pos = ex >> 12;
+  #pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              if (len2[q]) {
+                mP[k] = pos; mS[k] = s2[q]; mW[k] = wv2[q];
+                if (pass == 1) { mB[k] = 0; mN[k] = 0; }
+                ++k;
+                pos += len2[q];
+              }
+            }
+          }
+          if (tid == kT2Threads - 1) { sh_mcc = (ex + tsum) & 0xfffu; mP[(ex + tsum) & 0xfffu] = (ex + tsum) >> 12; }
+          __syncthreads();
         }
-        if (tid == kT2Threads - 1) { sh_mcc = (ex + tsum) & 0xfffu; mP[(ex + tsum) & 0xfffu] = (ex + tsum) >> 12; }
-        __syncthreads();
         const uint32_t mcc = sh_mcc;  // non-empty middles of the round
         const uint32_t T = mP[mcc];
         // each warp takes a contiguous range of 32-wedge steps; a lane's middle = the middle owning
