@@ -1,1 +1,1 @@
-timeout 600 python tools/trace_step.py --config 5 --steps 3 --e2e > gpurun_out/tr_e2e.txt 2>&1; grep span gpurun_out/tr_e2e.txt; grep -A30 "all ops" gpurun_out/tr_e2e.txt | head -32; grep -A12 "longest runtime" gpurun_out/tr_e2e.txt; grep -A8 "^copies" gpurun_out/tr_e2e.txt
+timeout 600 python tools/trace_step.py --config 5 --steps 4 --e2e > gpurun_out/tr_e2e.txt 2>&1; grep -A30 "^copies" gpurun_out/tr_e2e.txt | grep -v "all ops" | head -32
