@@ -561,6 +561,66 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// 8 x 8 nibble transpose in registers: w[k] = row k (nibble j = column j) becomes w[j] = column j
+// (nibble k = row k), by swapping 2 x 2 blocks of nibbles, then bytes, then half-words
+__device__ __forceinline__ void transpose8x8_nibbles(uint32_t (&w)[8]) {
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    const uint32_t t = ((w[k] >> 4) ^ w[k + 1]) & 0x0F0F0F0Fu;
+    w[k + 1] ^= t;
+    w[k] ^= t << 4;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; k += (k & 1) ? 3 : 1) {  // k = 0, 1, 4, 5
+    const uint32_t t = ((w[k] >> 8) ^ w[k + 2]) & 0x00FF00FFu;
+    w[k + 2] ^= t;
+    w[k] ^= t << 8;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t t = ((w[k] >> 16) ^ w[k + 4]) & 0x0000FFFFu;
+    w[k + 4] ^= t;
+    w[k] ^= t << 16;
+  }
+}
+
+// Av4 = Au4^T and Sv4 = Su4^T on the packed e2m1 operands, 128 x 128 element tiles: each thread
+// loads an 8 x 8 nibble block (eight 4-byte row pieces), transposes it in registers and stages the
+// words in shared memory (lanes spread so the staging stores hit 32 distinct banks); the tile is
+// written as 64-byte row pieces.  U rows at or beyond rows_u read as zero.  Lets an FP4-only
+// graph skip the u8 operands altogether.
+__global__ void __launch_bounds__(256) k_dense_transpose_f4(const uint8_t* __restrict__ Au4,
+                                                            const uint8_t* __restrict__ Su4, uint32_t ku4,
+                                                            uint32_t rows_u, uint8_t* __restrict__ Av4,
+                                                            uint8_t* __restrict__ Sv4, uint32_t kv4) {
+  __shared__ uint32_t ta[128][17], ts[128][17];
+  const uint32_t c0 = blockIdx.x * 128, r0 = blockIdx.y * 128;  // U rows c0.. (V columns), V rows r0..
+  const uint32_t wp = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const uint32_t bi = 8 * (wp & 1) + (l & 7), bj = 4 * (wp >> 1) + (l >> 3);  // U rows c0 + 8 bi, V rows r0 + 8 bj
+  uint32_t a[8], s[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t row = c0 + 8 * bi + k;
+    const uint64_t src = (uint64_t)row * ku4 + r0 / 2 + 4 * bj;
+    const bool in = row < rows_u && r0 / 2 + 4 * bj < ku4;
+    a[k] = in ? __ldg(reinterpret_cast<const uint32_t*>(Au4 + src)) : 0u;
+    s[k] = in ? __ldg(reinterpret_cast<const uint32_t*>(Su4 + src)) : 0u;
+  }
+  transpose8x8_nibbles(a);
+  transpose8x8_nibbles(s);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) { ta[8 * bj + k][bi] = a[k]; ts[8 * bj + k][bi] = s[k]; }
+  __syncthreads();
+  const uint32_t orow = threadIdx.x >> 1, h = 8 * (threadIdx.x & 1);  // V row r0 + orow, words h .. h + 7
+  const uint64_t dst = (uint64_t)(r0 + orow) * kv4 + c0 / 2 + 4 * h;
+  uint4* da = reinterpret_cast<uint4*>(Av4 + dst);
+  uint4* ds = reinterpret_cast<uint4*>(Sv4 + dst);
+  da[0] = make_uint4(ta[orow][h], ta[orow][h + 1], ta[orow][h + 2], ta[orow][h + 3]);
+  da[1] = make_uint4(ta[orow][h + 4], ta[orow][h + 5], ta[orow][h + 6], ta[orow][h + 7]);
+  ds[0] = make_uint4(ts[orow][h], ts[orow][h + 1], ts[orow][h + 2], ts[orow][h + 3]);
+  ds[1] = make_uint4(ts[orow][h + 4], ts[orow][h + 5], ts[orow][h + 6], ts[orow][h + 7]);
+}
+
 // ================================================================================ FP4 variant
 // The same pair kernel on the block-scaled FP4 tensor path (tcgen05.mma.cta_group::2.kind::mxf4,
 // 2x the int8 rate, half the operand bytes): A and S as e2m1 (0, +1.0, -1.0) packed two per byte,
@@ -1089,10 +1149,11 @@ __global__ void k_dense_rows(const uint64_t* __restrict__ rp, const uint32_t* __
   uint8_t* ba = reinterpret_cast<uint8_t*>(rowbuf);
   uint8_t* bs = ba + ku;
   const uint32_t r = blockIdx.x, n16 = ku / 16;
-  uint4* a4 = reinterpret_cast<uint4*>(Au + (uint64_t)r * ku);
-  uint4* s4 = reinterpret_cast<uint4*>(Su + (uint64_t)r * ku);
+  uint4* a4 = Au ? reinterpret_cast<uint4*>(Au + (uint64_t)r * ku) : nullptr;  // u8 copy optional
+  uint4* s4 = Au ? reinterpret_cast<uint4*>(Su + (uint64_t)r * ku) : nullptr;
   if (r >= n_u) {  // padding rows
-    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) { a4[i] = make_uint4(0u, 0u, 0u, 0u); s4[i] = a4[i]; }
+    if (a4)
+      for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) { a4[i] = make_uint4(0u, 0u, 0u, 0u); s4[i] = a4[i]; }
     if (A4)
       for (uint32_t i = threadIdx.x; i < k4 / 8; i += blockDim.x) {
         reinterpret_cast<uint2*>(A4 + (uint64_t)r * k4)[i] = make_uint2(0u, 0u);
@@ -1113,8 +1174,10 @@ __global__ void k_dense_rows(const uint64_t* __restrict__ rp, const uint32_t* __
   for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
     const uint4 q = rowbuf[i];
     ones += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
-    a4[i] = q;
-    s4[i] = rowbuf[n16 + i];
+    if (a4) {
+      a4[i] = q;
+      s4[i] = rowbuf[n16 + i];
+    }
   }
   ones = __reduce_add_sync(0xffffffffu, ones);
   if ((threadIdx.x & 31) == 0 && ones) atomicAdd(nz, (unsigned long long)ones);
@@ -1124,6 +1187,46 @@ __global__ void k_dense_rows(const uint64_t* __restrict__ rp, const uint32_t* __
       reinterpret_cast<uint2*>(A4 + (uint64_t)r * k4)[i] = in ? pack_e2m1(rowbuf[i]) : make_uint2(0u, 0u);
       reinterpret_cast<uint2*>(S4 + (uint64_t)r * k4)[i] = in ? pack_e2m1(rowbuf[n16 + i]) : make_uint2(0u, 0u);
     }
+}
+
+// FP4-only variant of k_dense_rows: the row is assembled directly as packed e2m1 nibbles in shared
+// memory (A = 0x2, S = 0x2 / 0xA, set with shared atomicOr) and written with 16-byte stores; every
+// present cell has exactly one set bit in A, so the popcount still counts distinct edges
+__global__ void __launch_bounds__(256) k_dense_rows_f4(const uint64_t* __restrict__ rp,
+                                                       const uint32_t* __restrict__ col,
+                                                       const uint8_t* __restrict__ sg, uint32_t n_u,
+                                                       const uint32_t* __restrict__ inv,
+                                                       const uint32_t* __restrict__ lr_v,
+                                                       unsigned long long* __restrict__ nz,
+                                                       uint8_t* __restrict__ A4, uint8_t* __restrict__ S4,
+                                                       uint32_t k4) {
+  extern __shared__ uint4 rowbuf[];
+  uint32_t* rw = reinterpret_cast<uint32_t*>(rowbuf);
+  const uint32_t r = blockIdx.x, n16 = k4 / 16, nw = k4 / 4;
+  uint4* a4 = reinterpret_cast<uint4*>(A4 + (uint64_t)r * k4);
+  uint4* s4 = reinterpret_cast<uint4*>(S4 + (uint64_t)r * k4);
+  if (r >= n_u) {  // padding rows
+    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) { a4[i] = make_uint4(0u, 0u, 0u, 0u); s4[i] = a4[i]; }
+    return;
+  }
+  for (uint32_t i = threadIdx.x; i < 2 * n16; i += blockDim.x) rowbuf[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  const uint32_t u = inv[r];
+  for (uint64_t e = rp[u] + threadIdx.x; e < rp[u + 1]; e += blockDim.x) {
+    const uint32_t c = lr_v[col[e]], sh = 4 * (c & 7);
+    atomicOr(&rw[c >> 3], 0x2u << sh);
+    atomicOr(&rw[nw + (c >> 3)], (sg[e] ? 0x2u : 0xAu) << sh);  // weight 1 = +1, 0 = -1
+  }
+  __syncthreads();
+  uint32_t ones = 0;
+  for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
+    const uint4 q = rowbuf[i];
+    ones += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+    a4[i] = q;
+    s4[i] = rowbuf[n16 + i];
+  }
+  ones = __reduce_add_sync(0xffffffffu, ones);
+  if ((threadIdx.x & 31) == 0 && ones) atomicAdd(nz, (unsigned long long)ones);
 }
 
 // Av = Au^T and Sv = Su^T, 64 x 64 byte tiles: each thread loads a 4 x 4 byte block (four 4-byte
@@ -1258,11 +1361,53 @@ bbf_status alloc_dense_operands(bbf_graph* g, bool zero) {
   return BBF_OK;
 }
 
+bbf_status build_dense_operands_f4(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col,
+                                   const uint8_t* d_sg) {
+  cudaStream_t st = g->stream;
+  g->drows[0] = round_up(std::max<uint32_t>(g->n_u, 1), kBN);
+  g->drows[1] = round_up(std::max<uint32_t>(g->n_v, 1), kBN);
+  g->dk[0] = round_up(std::max<uint32_t>(g->n_v, 1), kBK);
+  g->dk[1] = round_up(std::max<uint32_t>(g->n_u, 1), kBK);
+  for (int s2 = 0; s2 < 2; ++s2) {
+    g->dk4[s2] = round_up(g->dk[s2], 256) / 2;
+    BBF_CUDA(dmalloc(&g->dA4[s2], g->drows[s2] * g->dk4[s2], st));
+    BBF_CUDA(dmalloc(&g->dS4[s2], g->drows[s2] * g->dk4[s2], st));
+  }
+  unsigned long long* d_nz;
+  BBF_CUDA(dmalloc(&d_nz, 8, st));
+  BBF_CUDA(cudaMemsetAsync(d_nz, 0, 8, st));
+  const int smem = 2 * (int)g->dk4[0];
+  if (smem > 48 * 1024)
+    BBF_CUDA(cudaFuncSetAttribute(k_dense_rows_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_dense_rows_f4<<<(unsigned)g->drows[0], 256, smem, st>>>(d_rp, d_col, d_sg, g->n_u, g->inv, g->lr + g->n_u,
+                                                           d_nz, g->dA4[0], g->dS4[0], (uint32_t)g->dk4[0]);
+  // V side: every V row (drows[1]) x every packed column (2 * dk4[1] elements)
+  k_dense_transpose_f4<<<dim3((unsigned)(2 * g->dk4[1] / 128), (unsigned)(g->drows[1] / 128)), 256, 0, st>>>(
+      g->dA4[0], g->dS4[0], (uint32_t)g->dk4[0], (uint32_t)g->drows[0], g->dA4[1], g->dS4[1], (uint32_t)g->dk4[1]);
+  g->launches += 2;
+  unsigned long long nz = 0;
+  BBF_CUDA(rb_add(&nz, d_nz, 8, st)); g->launches++;
+  BBF_CUDA(rb_sync(st));
+  dfree(d_nz, st);
+  if (nz != g->nnz) {
+    set_error("duplicate (u,v) edge");
+    return BBF_EDUP;
+  }
+  g->dense_built = true;
+  g->dense_v_u8 = false;
+  return BBF_OK;
+}
+
 // dense operands of both sides from the input CSR (device arrays), with the duplicate-edge check
 // (SPEC.md:56): every edge sets one cell of A_U, so a duplicate leaves fewer than nnz ones
 bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col,
                                 const uint8_t* d_sg) {
   cudaStream_t st = g->stream;
+  // FP4-only graphs (both sides exact on the FP4 kernels, no int8 test hook): the packed operands
+  // are built directly (rows, then a nibble transpose) and the u8 ones are skipped
+  const bool f4_only = std::max(g->maxdeg[0], g->maxdeg[1]) <= 8192u && !getenv("BBF_DENSE_I8") &&
+                       !getenv("BBF_DENSE_1CTA");
+  if (f4_only) return build_dense_operands_f4(g, d_rp, d_col, d_sg);
   BBF_TRY(alloc_dense_operands(g, false));
   unsigned long long* d_nz;
   BBF_CUDA(dmalloc(&d_nz, 8, st));
@@ -1336,6 +1481,25 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
       g->dense_built = true;
       g->dense_v_u8 = true;
     }
+  }
+  // an FP4-only graph asked for the int8 kernels (test hooks set after the load): u8 U side from
+  // the kept input CSR; the V side follows from it on demand below
+  if (!g->dA[0] && (getenv("BBF_DENSE_I8") || getenv("BBF_DENSE_1CTA") ||
+                    std::max(g->maxdeg[0], g->maxdeg[1]) > 8192u)) {
+    if (!g->in_rp) { set_error("internal: u8 dense operands requested without the input CSR"); return BBF_ECUDA; }
+    BBF_TRY(alloc_dense_operands(g, false));
+    unsigned long long* d_nz;
+    BBF_CUDA(dmalloc(&d_nz, 8, st));
+    const uint32_t ku = (uint32_t)g->dk[0];
+    const int smem = 2 * (int)ku;
+    if (smem > 48 * 1024)
+      BBF_CUDA(cudaFuncSetAttribute(k_dense_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_dense_rows<<<(unsigned)g->drows[0], 256, smem, st>>>(g->in_rp, g->in_col, g->in_sg, g->n_u, g->inv,
+                                                          g->lr + g->n_u, g->dA[0], g->dS[0], ku, d_nz, nullptr,
+                                                          nullptr, 0u);
+    g->launches++;
+    dfree(d_nz, st);
+    g->dense_v_u8 = false;
   }
   // global only: the cheaper side (cost ~ rows^2 * K); per-vertex: both sides
   const bool do_u = per_vertex || (uint64_t)g->n_u * g->n_u * g->n_v <= (uint64_t)g->n_v * g->n_v * g->n_u;

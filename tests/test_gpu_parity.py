@@ -309,6 +309,25 @@ def test_dense_fp4_packed_accumulator_near_limit(bbf, monkeypatch, m, n):
             assert np.array_equal(x, y)
 
 
+def test_dense_fp4_only_operands_then_int8(bbf, monkeypatch):
+    """A graph loaded FP4-only (packed operands built by the row kernel and the nibble transpose,
+    no u8 copies) counted first on the FP4 kernels, then on the same handle with the int8 pair
+    kernel and the 1-CTA int8 kernel (u8 operands built on demand): identical per-vertex arrays,
+    equal to the oracle's vBBFC."""
+    g = G.random_bipartite(517, 391, 0.4, 0.6, seed=11)   # ragged on both sides
+    bal, unb = O.route_s(g, threads=THREADS)
+    with bbf.Graph.from_synth(g, flags=bbf.BBF_FORCE_DENSE) as h:
+        runs = [h.count_per_vertex()]
+        for env in ("BBF_DENSE_I8", "BBF_DENSE_1CTA"):
+            monkeypatch.setenv(env, "1")
+            runs.append(h.count_per_vertex())
+            monkeypatch.delenv(env)
+        runs.append(h.count_per_vertex())
+    for tot, bu, nu, bv, nv in runs:
+        assert np.array_equal(bu, bal[:g.n_u]) and np.array_equal(nu, unb[:g.n_u])
+        assert np.array_equal(bv, bal[g.n_u:]) and np.array_equal(nv, unb[g.n_u:])
+
+
 def test_upload_and_async_outputs(bbf):
     """Pipelined loading (bbf_upload_csr / bbf_graph_load_upload, the next graph's copy in flight
     while the current one counts) and BBF_OUTPUT_ASYNC host outputs give the same counts as the
