@@ -72,6 +72,23 @@ __global__ void __launch_bounds__(kHistThreads) k_hist_v(const uint32_t* __restr
   }
 }
 
+// Narrow V sides (n_v <= kHistDirectMax): one persistent CTA per SM keeps a private counter per
+// column in shared memory over its whole share of the edges and flushes the non-zero ones once
+// (uniform columns defeat the 4096-slot table above: most edges would miss it and contend on
+// the global counters)
+constexpr uint32_t kHistDirectMax = 49152;
+__global__ void __launch_bounds__(kHistThreads) k_hist_v_direct(const uint32_t* __restrict__ col, uint64_t nnz,
+                                                                uint32_t n_v, uint32_t* __restrict__ dv) {
+  extern __shared__ uint32_t hcnt[];
+  for (uint32_t i = threadIdx.x; i < n_v; i += kHistThreads) hcnt[i] = 0;
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * (uint64_t)kHistThreads + threadIdx.x; e < nnz; e += (uint64_t)gridDim.x * kHistThreads)
+    atomicAdd(&hcnt[col[e]], 1u);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n_v; i += kHistThreads)
+    if (hcnt[i]) atomicAdd(&dv[i], hcnt[i]);
+}
+
 __global__ void k_keys_v(const uint32_t* __restrict__ dv, uint32_t n_u, uint32_t n_v,
                          uint64_t* __restrict__ key) {
   uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -321,6 +338,33 @@ __global__ void k_wg_m(const uint64_t* __restrict__ rp, const uint32_t* __restri
   }
 }
 
+// k_wg_m with the V-side middle counters in shared memory (n_v <= kHistDirectMax): one CTA per
+// SM, warp per start row, flushed once per CTA
+__global__ void __launch_bounds__(1024) k_wg_m_direct(const uint64_t* __restrict__ rp,
+                                                      const uint32_t* __restrict__ col, uint32_t n_u,
+                                                      uint32_t n_v, const uint64_t* __restrict__ key_u,
+                                                      const uint64_t* __restrict__ key_v,
+                                                      uint32_t* __restrict__ mcnt) {
+  extern __shared__ uint32_t vcnt[];
+  for (uint32_t i = threadIdx.x; i < n_v; i += blockDim.x) vcnt[i] = 0;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n_u; u += (gridDim.x * blockDim.x) >> 5) {
+    const uint64_t ku = key_u[u];
+    uint32_t c = 0;
+    for (uint64_t e = rp[u] + lane; e < rp[u + 1]; e += 32) {
+      const uint32_t v = col[e];
+      if (ku > key_v[v]) atomicAdd(&vcnt[v], 1u);  // u is an eligible start for middle v
+      else ++c;
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) mcnt[u] = c;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n_v; i += blockDim.x)
+    if (vcnt[i]) atomicAdd(&mcnt[n_u + i], vcnt[i]);
+}
+
 __global__ void k_wg_sum(const uint32_t* __restrict__ mcnt, const uint64_t* __restrict__ key_u,
                          const uint64_t* __restrict__ key_v, uint32_t n_u, uint32_t n,
                          unsigned long long* __restrict__ out) {
@@ -433,7 +477,15 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   if (n_u) k_keys_u<<<grid_for(n_u, 256, 1u << 30), 256, 0, st>>>(d_rp, n_u, key_u);
   if (nnz) {
     const uint64_t chunks = (nnz + kHistChunk - 1) / kHistChunk;
-    k_hist_v<<<(unsigned)std::min<uint64_t>(chunks, 2ull * g->num_sms), kHistThreads, 0, st>>>(d_col, nnz, dv);
+    if (n_v <= kHistDirectMax) {
+      const int smem = 4 * (int)n_v;
+      if (smem > 48 * 1024)
+        BBF_CUDA(cudaFuncSetAttribute(k_hist_v_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_hist_v_direct<<<(unsigned)std::min<uint64_t>(chunks, g->num_sms), kHistThreads, smem, st>>>(d_col, nnz,
+                                                                                                  n_v, dv);
+    } else {
+      k_hist_v<<<(unsigned)std::min<uint64_t>(chunks, 2ull * g->num_sms), kHistThreads, 0, st>>>(d_col, nnz, dv);
+    }
   }
   if (n_v) k_keys_v<<<grid_for(n_v, 256, 1u << 30), 256, 0, st>>>(dv, n_u, n_v, key_v);
   g->launches += 3;
@@ -511,7 +563,15 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     BBF_CUDA(dmalloc(&d_wg, 8, st));
     BBF_CUDA(cudaMemsetAsync(mcnt, 0, 4ull * (n + 1), st));
     BBF_CUDA(cudaMemsetAsync(d_wg, 0, 8, st));
-    if (n_u) k_wg_m<<<grid_for(32ull * n_u, 256), 256, 0, st>>>(d_rp, d_col, n_u, key_u, key_v, mcnt);
+    if (n_u && n_v <= kHistDirectMax) {
+      const int smem = 4 * (int)n_v;
+      if (smem > 48 * 1024)
+        BBF_CUDA(cudaFuncSetAttribute(k_wg_m_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_wg_m_direct<<<(unsigned)std::min<uint64_t>((n_u + 31) / 32, g->num_sms), 1024, smem, st>>>(
+          d_rp, d_col, n_u, n_v, key_u, key_v, mcnt);
+    } else if (n_u) {
+      k_wg_m<<<grid_for(32ull * n_u, 256), 256, 0, st>>>(d_rp, d_col, n_u, key_u, key_v, mcnt);
+    }
     if (n) k_wg_sum<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(mcnt, key_u, key_v, n_u, n, d_wg);
     g->launches += 2;
     unsigned long long wg = 0;
