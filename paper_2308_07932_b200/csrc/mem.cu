@@ -8,6 +8,8 @@
 #include <mutex>
 #include <unordered_map>
 #include <vector>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "bbf_internal.cuh"
@@ -22,11 +24,45 @@ struct Block {
   cudaEvent_t ev;
 };
 
+struct Live {
+  int dev;
+  size_t size;   // block size
+  void* base;    // block start (the returned pointer is base + kGuard in guard mode)
+  size_t bytes;  // requested bytes
+};
 struct Cache {
   std::mutex mu;
-  std::multimap<size_t, Block> free_by_size[64];        // per device
-  std::unordered_map<void*, std::pair<int, size_t>> live;  // ptr -> (device, size)
+  std::multimap<size_t, Block> free_by_size[64];  // per device
+  std::unordered_map<void*, Live> live;            // returned ptr -> block
 };
+
+// Guard mode (BBF_GUARD=1, a debugging aid in place of compute-sanitizer, which this pool does
+// not offer): every block gets kGuard bytes of 0xA5 before the returned pointer and from the end
+// of the requested bytes to the end of the block; dfree synchronises the stream, reads both
+// guards back and aborts the process on any changed byte (an out-of-bounds write by a kernel).
+constexpr size_t kGuard = 256;
+constexpr uint8_t kGuardByte = 0xA5;
+bool guard_mode() {
+  static const bool on = [] { const char* e = getenv("BBF_GUARD"); return e && atoi(e) != 0; }();
+  return on;
+}
+
+void guard_check(const Live& L, cudaStream_t st) {
+  if (cudaStreamSynchronize(st) != cudaSuccess) return;  // the error surfaces elsewhere
+  const size_t tail_off = kGuard + L.bytes, tail = L.size - tail_off;
+  std::vector<uint8_t> h(kGuard + tail);
+  if (cudaMemcpy(h.data(), L.base, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(h.data() + kGuard, (uint8_t*)L.base + tail_off, tail, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return;
+  for (size_t i = 0; i < h.size(); ++i)
+    if (h[i] != kGuardByte) {
+      const bool front = i < kGuard;
+      fprintf(stderr, "[bbf] BBF_GUARD: out-of-bounds write %s a block of %zu bytes (guard byte %zd: 0x%02x)\n",
+              front ? "before" : "after", L.bytes, front ? (ssize_t)i - (ssize_t)kGuard : (ssize_t)(i - kGuard),
+              h[i]);
+      abort();
+    }
+}
 
 Cache& cache() {
   static Cache* c = new Cache();  // intentionally leaked: blocks outlive static destruction
@@ -58,16 +94,25 @@ cudaError_t dmalloc_raw2(void** out, size_t bytes, cudaStream_t st, bool no_wait
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  const size_t need = round_size(bytes ? bytes : 1);
-  const size_t lim = need + need / 4 + (64u << 20);
   Cache& c = cache();
+  const bool gm = guard_mode();
+  const size_t need = round_size((bytes ? bytes : 1) + (gm ? 2 * kGuard : 0));
+  const size_t lim = need + need / 4 + (64u << 20);
+  auto hand_out = [&](void* base, size_t size) {  // caller holds c.mu
+    void* user = gm ? (void*)((uint8_t*)base + kGuard) : base;
+    c.live[user] = Live{dev, size, base, bytes};
+    if (gm) {
+      cudaMemsetAsync(base, kGuardByte, kGuard, st);
+      cudaMemsetAsync((uint8_t*)base + kGuard + bytes, kGuardByte, size - kGuard - bytes, st);
+    }
+    *out = user;
+  };
   auto take = [&](std::multimap<size_t, Block>& fl, std::multimap<size_t, Block>::iterator it) {
     Block b = it->second;
     fl.erase(it);
     cudaStreamWaitEvent(st, b.ev, 0);  // no-op when complete or already ordered
     cudaEventDestroy(b.ev);
-    c.live[b.p] = {dev, b.size};
-    *out = b.p;
+    hand_out(b.p, b.size);
   };
   {
     std::lock_guard<std::mutex> lk(c.mu);
@@ -101,8 +146,7 @@ cudaError_t dmalloc_raw2(void** out, size_t bytes, cudaStream_t st, bool no_wait
   }
   if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> lk(c.mu);
-  c.live[p] = {dev, need};
-  *out = p;
+  hand_out(p, need);
   return cudaSuccess;
 }
 
@@ -112,9 +156,12 @@ void dfree(void* p, cudaStream_t st) {
   std::lock_guard<std::mutex> lk(c.mu);
   auto it = c.live.find(p);
   if (it == c.live.end()) return;  // not ours
-  const int dev = it->second.first;
-  const size_t size = it->second.second;
+  const Live L = it->second;
+  const int dev = L.dev;
+  const size_t size = L.size;
+  p = L.base;
   c.live.erase(it);
+  if (guard_mode()) guard_check(L, st);
   cudaEvent_t ev;
   if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
     cudaFreeAsync(p, st);
