@@ -110,8 +110,17 @@ __global__ void k_merge_pe(const unsigned long long* __restrict__ pe, const unsi
 
 // End-role contribution of pair (x, w): one packed 64-bit RED when w's end-role totals are
 // provably < 2^32 (local rank >= rs, plan.cu k_rsafe), else one RED per non-zero count.
+#ifdef BBF_T3_PROF
+__device__ unsigned long long g_red_cnt[8];  // end: unpacked, packed, rank < 1024, rank < 8192; mid: unpacked, packed
+#define RED_CNT(i) atomicAdd(&g_red_cnt[i], 1ull)
+#else
+#define RED_CNT(i) do {} while (0)
+#endif
 __device__ __forceinline__ void end_red(const EngineArgs& a, uint32_t rs, uint32_t lrank, uint32_t wrow,
                                         uint32_t fb, uint32_t fn) {
+  RED_CNT(lrank >= rs ? 1 : 0);
+  if (lrank < 1024) RED_CNT(2);
+  if (lrank < 8192) RED_CNT(3);
   if (lrank >= rs) {
     atomicAdd(&a.pe[wrow], (unsigned long long)fb | ((unsigned long long)fn << 32));
   } else {
@@ -123,6 +132,8 @@ __device__ __forceinline__ void end_red(const EngineArgs& a, uint32_t rs, uint32
 // Middle-role share of one record / middle: packed like end_red (pm, threshold rmid).
 __device__ __forceinline__ void mid_red(const EngineArgs& a, uint32_t rm, uint32_t lrank, uint32_t vrow,
                                         uint32_t cb, uint32_t cn) {
+  RED_CNT(lrank >= rm ? 5 : 4);
+  if (lrank < 1024) RED_CNT(6);
   if (lrank >= rm) {
     atomicAdd(&a.pm[vrow], (unsigned long long)cb | ((unsigned long long)cn << 32));
   } else {
@@ -1325,6 +1336,10 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     const double clk = 1.965e6 * g->num_sms * kT3Ctas;  // cycles per ms summed over CTAs
     fprintf(stderr, "[bbf] t3 phases (ms of CTA time): prescan %.2f setup %.2f pass1 %.2f pass2 %.2f epi %.2f\n",
             h[11] / clk, h[12] / clk, h[13] / clk, h[14] / clk, h[15] / clk);
+    unsigned long long rc[8];
+    cudaMemcpyFromSymbol(rc, g_red_cnt, sizeof(rc));
+    fprintf(stderr, "[bbf] REDs (cumulative): end unpacked %llu packed %llu (rank<1024 %llu, <8192 %llu); mid unpacked %llu packed %llu (rank<1024 %llu)\n",
+            rc[0], rc[1], rc[2], rc[3], rc[4], rc[5], rc[6]);
     unsigned long long t[3];
     cudaMemcpyFromSymbol(t, g_prof_t, sizeof(t));
     fprintf(stderr, "[bbf] t3 CTA ends: first %.3f ms, last %.3f ms after the first start\n", (t[1] - t[0]) * 1e-6,
