@@ -489,3 +489,46 @@ def test_topk_threshold_search(bbf, monkeypatch, cap):
     with bbf.Graph.from_synth(g) as h:
         assert h.count_pairs_topk(100, side=1) == want
         assert h.count_pairs_topk(7, side=0) == O.topk_pairs(g, 7, side=0, threads=THREADS)
+
+
+def _sweep_graph(seed):
+    """Seeded shapes for the randomized sweep: uniform random bipartite graphs of mixed aspect
+    ratio, density and sign balance, and small Chung-Lu power-law graphs (hubs on both sides)."""
+    rng = np.random.default_rng(1000 + seed)
+    if seed % 3 == 2:
+        n_u, n_v = int(rng.integers(200, 3000)), int(rng.integers(100, 2000))
+        m = int(min(n_u * n_v // 3, rng.integers(2000, 30000)))
+        keys, r2 = G.chung_lu(n_u, n_v, m, float(rng.uniform(2.1, 2.8)), n_v / 3.0, n_u / 3.0, seed=seed)
+        s = (r2.random(keys.size) < rng.uniform(0.0, 1.0)).astype(np.uint8)
+        return G.from_edges(n_u, n_v, (keys // n_v).tolist(), (keys % n_v).tolist(), s.tolist())
+    n_u, n_v = int(rng.integers(1, 500)), int(rng.integers(1, 500))
+    return G.random_bipartite(n_u, n_v, float(rng.uniform(0.005, 0.5)), float(rng.uniform(0.0, 1.0)),
+                              seed=seed)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_sweep_tiers_dense_topk(bbf, monkeypatch, seed):
+    """Randomized sweep: per-vertex counts of the default tiering, of T3-only (T2 disabled, every
+    start above the warp tier goes through the hub kernel) and of the dense path equal the
+    oracle's vBBFC element by element; global B/N/W_G equal Alg. 2; top-k pairs of both sides
+    equal the oracle's."""
+    g = _sweep_graph(seed)
+    rg = O.route_g(g, threads=THREADS)
+    bal, unb = O.route_s(g, threads=THREADS)
+    runs = [("default", {}, 0), ("t3-only", {"BBF_T2_MAX": "0"}, bbf.BBF_FORCE_SPARSE)]
+    if max(g.n_u, g.n_v) <= 65536:
+        runs.append(("dense", {}, bbf.BBF_FORCE_DENSE))
+    for name, env, fl in runs:
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with bbf.Graph.from_synth(g, flags=fl) as h:
+            c = h.count_global()
+            tot, bu, nu, bv, nv = h.count_per_vertex()
+            if name == "default":
+                for side in (0, 1):
+                    assert h.count_pairs_topk(10, side=side) == O.topk_pairs(g, 10, side=side, threads=THREADS)
+        for k in env:
+            monkeypatch.delenv(k)
+        assert (c["balanced"], c["unbalanced"], c["wedges_G"]) == (rg["B"], rg["N"], rg["W_G"]), name
+        assert np.array_equal(bu, bal[:g.n_u]) and np.array_equal(nu, unb[:g.n_u]), name
+        assert np.array_equal(bv, bal[g.n_u:]) and np.array_equal(nv, unb[g.n_u:]), name
