@@ -19,6 +19,8 @@
  *   oracle_route_s   Alg. vBBFC for a list of vertices: all wedges
  *                    u-v-w, no rank comparison, w != u (reading R9),
  *                    buckets H1/H2, sum C(H1,2)+C(H2,2); the unbalanced count H1*H2 alongside.
+ *   oracle_bb_base   Alg. 1 BB-Base: per start, lists H(w) of middles, every
+ *                    pair of a list checked for balance explicitly (the paper's baseline).
  *   oracle_pairs     Lemma 2 per same-side pair: C(l,2)+C(m,2) with l / m
  *                    symmetric / asymmetric wedges between the pair, each unordered pair once.
  *
@@ -268,6 +270,115 @@ int oracle_route_g(uint32_t n_u, uint32_t n_v, const uint64_t *row_ptr, const ui
     tasks[i].g = &g; tasks[i].starts = starts; tasks[i].n_starts = n_starts;
     tasks[i].tid = i; tasks[i].nthreads = nthreads;
     pthread_create(&th[i], NULL, route_g_worker, &tasks[i]);
+  }
+  u128 B = 0, N = 0, W = 0;
+  rc = 0;
+  for (int i = 0; i < nthreads; ++i) {
+    pthread_join(th[i], NULL);
+    B += tasks[i].B; N += tasks[i].N; W += tasks[i].W;
+    if (tasks[i].rc) rc = tasks[i].rc;
+  }
+  clock_gettime(CLOCK_MONOTONIC, &t1);
+  free(tasks); free(th); graph_free(&g);
+  if (rc) return rc;
+  if (B >> 64 || N >> 64 || W >> 64) return 7;
+  out[0] = (uint64_t)B; out[1] = (uint64_t)N; out[2] = (uint64_t)W;
+  out[3] = (uint64_t)(t1.tv_sec - t0.tv_sec) * 1000000000ull + (uint64_t)(t1.tv_nsec - t0.tv_nsec);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Alg. 1 BB-Base: the same priority-eligible wedges as Alg. 2, but each start
+ * u stores the middles of every end w in a list H(w) (line 9: "H(w).add(v)") and then checks
+ * every pair (v1, v2) of H(w) explicitly (lines 10-13: "if butterfly (u,v1,w,v2) is balanced,
+ * count++").  Balanced = an even number of negative edges among the four (Def. Balanced
+ * butterfly); the pairs that fail the check are the unbalanced butterflies.
+ * Each unordered pair {v1, v2} is visited once.  Parallel over starts like route_g.
+ * ---------------------------------------------------------------------------------------- */
+typedef struct {
+  const graph_t *g;
+  int tid, nthreads;
+  u128 B, N, W;
+  int rc;
+} bb_task;
+
+static void *bb_base_worker(void *arg) {
+  bb_task *t = (bb_task *)arg;
+  const graph_t *g = t->g;
+  uint64_t *cnt = (uint64_t *)calloc((size_t)g->n + 1, sizeof(uint64_t));   /* |H(w)| */
+  uint64_t *pos = (uint64_t *)calloc((size_t)g->n + 1, sizeof(uint64_t));   /* H(w) start */
+  uint32_t *touched = (uint32_t *)malloc(sizeof(uint32_t) * ((size_t)g->n + 1));
+  uint64_t cap = 1024;
+  int8_t *hs = (int8_t *)malloc(cap * 2);   /* H entries: (σ(u,v), σ(v,w)) of each stored v */
+  if (!cnt || !pos || !touched || !hs) { t->rc = 4; goto done; }
+  for (uint32_t u = (uint32_t)t->tid; u < g->n; u += (uint32_t)t->nthreads) {
+    uint64_t pu = g->prio[u], nt = 0, tot = 0;
+    /* lines 7-9, first sweep: |H(w)| (so every list can be stored contiguously) */
+    for (uint64_t e = g->off[u]; e < g->off[u + 1]; ++e) {
+      uint32_t v = g->nbr[e];
+      if (!(g->prio[v] < pu)) break;                                  /* | p(v) < p(u) */
+      for (uint64_t f = g->off[v]; f < g->off[v + 1]; ++f) {
+        uint32_t w = g->nbr[f];
+        if (!(g->prio[w] < pu)) break;                                /* | p(w) < p(u) */
+        if (cnt[w] == 0) touched[nt++] = w;
+        cnt[w]++;
+        tot++;
+      }
+    }
+    t->W += tot;
+    if (tot > cap) {
+      free(hs);
+      cap = tot;
+      hs = (int8_t *)malloc(cap * 2);
+      if (!hs) { t->rc = 4; goto done; }
+    }
+    uint64_t acc = 0;
+    for (uint64_t k = 0; k < nt; ++k) { pos[touched[k]] = acc; acc += cnt[touched[k]]; cnt[touched[k]] = 0; }
+    /* second sweep: H(w).add(v), keeping the two signs the balance check needs */
+    for (uint64_t e = g->off[u]; e < g->off[u + 1]; ++e) {
+      uint32_t v = g->nbr[e];
+      if (!(g->prio[v] < pu)) break;
+      for (uint64_t f = g->off[v]; f < g->off[v + 1]; ++f) {
+        uint32_t w = g->nbr[f];
+        if (!(g->prio[w] < pu)) break;
+        uint64_t i = pos[w] + cnt[w]++;
+        hs[2 * i] = g->sgn[e];
+        hs[2 * i + 1] = g->sgn[f];
+      }
+    }
+    /* lines 10-13: every pair of H(w), |H(w)| > 1 */
+    for (uint64_t k = 0; k < nt; ++k) {
+      uint32_t w = touched[k];
+      uint64_t o = pos[w], c = cnt[w];
+      for (uint64_t i = 0; i + 1 < c; ++i)
+        for (uint64_t j = i + 1; j < c; ++j) {
+          int prod = hs[2 * (o + i)] * hs[2 * (o + i) + 1] * hs[2 * (o + j)] * hs[2 * (o + j) + 1];
+          if (prod > 0) t->B++;                                       /* is_Balanced */
+          else t->N++;
+        }
+      cnt[w] = 0;
+    }
+  }
+done:
+  free(cnt); free(pos); free(touched); free(hs);
+  return NULL;
+}
+
+/* out[0]=B, out[1]=N, out[2]=W_G, out[3]=wall ns of the counting loop (after lines 2-3). */
+int oracle_bb_base(uint32_t n_u, uint32_t n_v, const uint64_t *row_ptr, const uint32_t *col,
+                   const uint8_t *sign, int nthreads, uint64_t *out) {
+  graph_t g;
+  int rc = graph_build(&g, n_u, n_v, row_ptr, col, sign);
+  if (rc) return rc;
+  if ((rc = sort_adjacency_by_priority(&g))) { graph_free(&g); return rc; }
+  if (nthreads < 1) nthreads = 1;
+  bb_task *tasks = (bb_task *)calloc((size_t)nthreads, sizeof(bb_task));
+  pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+  struct timespec t0, t1;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+  for (int i = 0; i < nthreads; ++i) {
+    tasks[i].g = &g; tasks[i].tid = i; tasks[i].nthreads = nthreads;
+    pthread_create(&th[i], NULL, bb_base_worker, &tasks[i]);
   }
   u128 B = 0, N = 0, W = 0;
   rc = 0;

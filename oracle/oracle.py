@@ -45,6 +45,8 @@ def _load():
         lib.oracle_brute.argtypes = [u32, u32, P, P, P, P, P, P, P, P, P]
         lib.oracle_route_g.argtypes = [u32, u32, P, P, P, P, u64, i32, P]
         lib.oracle_route_s.argtypes = [u32, u32, P, P, P, P, u64, i32, P, P]
+        lib.oracle_bb_base.argtypes = [u32, u32, P, P, P, i32, P]
+        lib.oracle_bb_base.restype = i32
         lib.oracle_pairs.argtypes = [u32, u32, P, P, P, i32, i32, P, P, P, P, u64, P]
         lib.oracle_priority_order.argtypes = [u32, u32, P, P, P, P]
         lib.oracle_sm64.argtypes = [u64]
@@ -101,6 +103,18 @@ def route_g(g, starts=None, threads=None):
     out = np.zeros(4, np.uint64)
     rc = lib.oracle_route_g(*a, _ptr(st), C.c_uint64(0 if st is None else st.size),
                             _threads(threads), _ptr(out))
+    if rc:
+        raise OracleError(rc)
+    return dict(B=int(out[0]), N=int(out[1]), W_G=int(out[2]), count_s=float(out[3]) * 1e-9)
+
+
+def bb_base(g, threads=None):
+    """Alg. 1 BB-Base: explicit balance check of every pair in each H(w).
+    Returns dict(B, N, W_G, count_s)."""
+    lib = _load()
+    keep, a = _graph_args(g)
+    out = np.zeros(4, np.uint64)
+    rc = lib.oracle_bb_base(*a, _threads(threads), _ptr(out))
     if rc:
         raise OracleError(rc)
     return dict(B=int(out[0]), N=int(out[1]), W_G=int(out[2]), count_s=float(out[3]) * 1e-9)
