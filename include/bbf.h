@@ -145,6 +145,16 @@ bbf_status bbf_device_sync(int device);
  * given for a graph the dense path does not support (other side > 65,536 vertices). */
 bbf_status bbf_count_global(bbf_graph *g, bbf_counts *out);
 
+/* The same global counts by Alg. 1 BB-Base, the paper's baseline: per start
+ * the middles of every end w are collected in a list H(w) and every pair of a list is checked
+ * for balance one by one (cost = the number of butterflies instead of the number of wedges).
+ * Kept to reproduce the BB-Base vs BB-Bucket regime; results equal
+ * bbf_count_global's.  Sparse path only; starts sharded over the ranks of comm like
+ * bbf_count_global, counts all-reduced.  out: host (ms_count = device time of this call).
+ * Errors: BBF_EINVAL if a start has more than 8,192 distinct ends (the per-CTA table),
+ * BBF_ENOMEM if a start has more than 8 GiB of wedges, BBF_EOVERFLOW, BBF_ECUDA, BBF_ENCCL. */
+bbf_status bbf_count_global_base(bbf_graph *g, bbf_counts *out);
+
 /* Per-vertex counts (butterflies containing each vertex; vBBFC semantics),
  * indexed by input ids.  Any of the four arrays may be NULL.  Host arrays unless
  * BBF_PTR_DEVICE.  totals (nullable, host) receives the global counts as well.  With

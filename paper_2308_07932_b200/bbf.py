@@ -62,6 +62,7 @@ def lib():
         L.bbf_graph_load_csr.argtypes = [u32, u32, P, P, P, u32, i32, P, P, P]
         L.bbf_graph_free.argtypes = [P]
         L.bbf_count_global.argtypes = [P, P]
+        L.bbf_count_global_base.argtypes = [P, P]
         L.bbf_count_per_vertex.argtypes = [P, P, P, P, P, u32, P]
         L.bbf_count_pairs_topk.argtypes = [P, i32, u32, P, P, u32]
         L.bbf_graph_stats.argtypes = [P, P, P, P, P]
@@ -73,7 +74,7 @@ def lib():
         L.bbf_upload_free.argtypes = [P]
         L.bbf_device_sync.argtypes = [i32]
         for f in ("bbf_nccl_unique_id", "bbf_comm_init", "bbf_comm_free", "bbf_graph_load_csr",
-                  "bbf_graph_free", "bbf_count_global", "bbf_count_per_vertex",
+                  "bbf_graph_free", "bbf_count_global", "bbf_count_global_base", "bbf_count_per_vertex",
                   "bbf_count_pairs_topk", "bbf_graph_stats", "bbf_estimate_global", "bbf_topk_vertices",
                   "bbf_upload_csr", "bbf_graph_load_upload", "bbf_upload_free", "bbf_device_sync"):
             getattr(L, f).restype = i32
@@ -231,6 +232,13 @@ class Graph:
         return dict(balanced=c.balanced, unbalanced=c.unbalanced, total=c.total,
                     wedges_G=c.wedges_G, ms_count=c.ms_count)
 
+    def count_global_base(self) -> dict:
+        """Global counts by Alg. 1 BB-Base (explicit pair checks; the paper's baseline)."""
+        c = bbf_counts()
+        _check(lib().bbf_count_global_base(self.h, C.byref(c)))
+        return dict(balanced=c.balanced, unbalanced=c.unbalanced, total=c.total,
+                    wedges_G=c.wedges_G, ms_count=c.ms_count)
+
     def count_per_vertex(self, out=None, flags: int = 0):
         """Returns (totals dict, bal_u, unb_u, bal_v, unb_v).  `out` may be a tuple of four
         int64/uint64 torch tensors: CUDA tensors (device outputs, BBF_PTR_DEVICE) or host
@@ -310,6 +318,10 @@ def bbf_graph_free(g: Graph):
 
 def bbf_comm_free(c: Comm):
     c.free()
+
+
+def bbf_count_global_base(g: Graph):
+    return g.count_global_base()
 
 
 def bbf_count_global(g: Graph):

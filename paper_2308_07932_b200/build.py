@@ -16,7 +16,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["mem.cu", "graph_build.cu", "plan.cu", "count_sparse.cu", "dense_i8.cu", "estimate.cu", "api.cu"]
+SOURCES = ["mem.cu", "graph_build.cu", "plan.cu", "count_sparse.cu", "dense_i8.cu", "estimate.cu", "base.cu", "api.cu"]
 HEADERS = ["bbf_internal.cuh"]
 
 

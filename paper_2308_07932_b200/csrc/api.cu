@@ -450,6 +450,44 @@ bbf_status bbf_count_global(bbf_graph* g, bbf_counts* out) {
   return BBF_OK;
 }
 
+bbf_status bbf_count_global_base(bbf_graph* g, bbf_counts* out) {
+  if (!g || !out) { set_error("null pointer"); return BBF_EINVAL; }
+  BBF_CUDA(cudaSetDevice(g->device));
+  BBF_TRY(check_overflow(g));
+  BBF_TRY(ensure_plan_g(g));
+  const int rank = g->comm ? g->comm->rank : 0, nranks = g->comm ? g->comm->nranks : 1;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, g->stream);
+  unsigned long long BN[2] = {0, 0};
+  bbf_status s = run_base(g, &g->plan_g, rank, nranks, BN);
+  if (s == BBF_OK && g->comm && g->comm->nranks > 1) {
+    cudaError_t e = cudaMemcpyAsync(g->d_acc + 12, BN, 16, cudaMemcpyHostToDevice, g->stream);
+    if (e != cudaSuccess) s = cuda_status(e, "cudaMemcpyAsync");
+    if (s == BBF_OK) s = allreduce_u64(g, g->d_acc + 12, 2);
+    if (s == BBF_OK) {
+      e = cudaMemcpyAsync(BN, g->d_acc + 12, 16, cudaMemcpyDeviceToHost, g->stream);
+      if (e != cudaSuccess) s = cuda_status(e, "cudaMemcpyAsync");
+    }
+  }
+  cudaEventRecord(b, g->stream);
+  cudaStreamSynchronize(g->stream);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (s != BBF_OK) return s;
+  unsigned long long wg = 0;
+  BBF_TRY(wedges_g(g, &wg));
+  out->balanced = BN[0];
+  out->unbalanced = BN[1];
+  out->total = BN[0] + BN[1];
+  out->wedges_G = wg;
+  out->ms_count = ms;
+  return BBF_OK;
+}
+
 bbf_status bbf_count_per_vertex(bbf_graph* g, uint64_t* bal_u, uint64_t* unb_u, uint64_t* bal_v,
                                 uint64_t* unb_v, uint32_t flags, bbf_counts* totals) {
   if (!g) { set_error("null graph"); return BBF_EINVAL; }

@@ -346,6 +346,8 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
 bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uint32_t* n_out);
 bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks,
                      unsigned long long* host_BN);
+// Alg. 1 BB-Base (base.cu): explicit pair checks, the paper's baseline
+bbf_status run_base(bbf_graph* g, Plan* p, int rank, int nranks, unsigned long long* host_BN);
 bool dense_supported(bbf_graph* g);
 bool dense_preferred(bbf_graph* g, bool per_vertex);
 }  // namespace bbf

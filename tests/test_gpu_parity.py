@@ -532,3 +532,39 @@ def test_random_sweep_tiers_dense_topk(bbf, monkeypatch, seed):
         assert (c["balanced"], c["unbalanced"], c["wedges_G"]) == (rg["B"], rg["N"], rg["W_G"]), name
         assert np.array_equal(bu, bal[:g.n_u]) and np.array_equal(nu, unb[:g.n_u]), name
         assert np.array_equal(bv, bal[g.n_u:]) and np.array_equal(nv, unb[g.n_u:]), name
+
+
+@pytest.mark.parametrize("name", ["config1", "config2", "skewed", "sweep5", "sweep11", "chung_lu"])
+def test_bb_base_gpu_equals_oracle_alg1(bbf, name):
+    """bbf_count_global_base (Alg. 1 BB-Base on the GPU: explicit pair checks per H(w)) equals the
+    oracle's Alg. 1 and Alg. 2 counts and the bucketed GPU count."""
+    g = {"config1": G.config1, "config2": G.config2,
+         "skewed": lambda: G.random_bipartite(10, 1000, 0.5, 0.5, seed=7),
+         "sweep5": lambda: _sweep_graph(5), "sweep11": lambda: _sweep_graph(11),
+         "chung_lu": lambda: _sweep_graph(2)}[name]()
+    ob = O.bb_base(g, threads=THREADS)
+    with bbf.Graph.from_synth(g) as h:
+        base = h.count_global_base()
+        buck = h.count_global()
+    assert (base["balanced"], base["unbalanced"]) == (ob["B"], ob["N"])
+    assert (buck["balanced"], buck["unbalanced"]) == (ob["B"], ob["N"])
+    assert base["wedges_G"] == ob["W_G"]
+
+
+def test_bb_base_gpu_table_limit_error(bbf):
+    """A start with more distinct ends than BB-Base's 8,192-slot table: BBF_EINVAL, not a wrong
+    count (u0 adjacent to all 200 V vertices; 12,000 other U vertices of degree 2, so every V
+    vertex has degree 121 < 200 and u0 is the top-priority start with 12,000 distinct ends)."""
+    n_v, n_e = 200, 12000
+    us, vs = [0] * n_v, list(range(n_v))
+    for i in range(n_e):
+        a = i % n_v
+        b = (a + 1 + (i // n_v) % (n_v - 1)) % n_v
+        us += [1 + i, 1 + i]
+        vs += [a, b]
+    g = G.from_edges(1 + n_e, n_v, us, vs, [1] * len(us))
+    with bbf.Graph.from_synth(g) as h:
+        with pytest.raises(bbf.BBFError) as e:
+            h.count_global_base()
+        assert e.value.name == "BBF_EINVAL"
+        assert h.count_global()["balanced"] == O.route_g(g)["B"]
