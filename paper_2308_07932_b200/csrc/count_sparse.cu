@@ -110,7 +110,7 @@ __global__ void k_merge_pe(const unsigned long long* __restrict__ pe, const unsi
 
 // End-role contribution of pair (x, w): one packed 64-bit RED when w's end-role totals are
 // provably < 2^32 (local rank >= rs, plan.cu k_rsafe), else one RED per non-zero count.
-#ifdef BBF_T3_PROF
+#ifdef BBF_RED_PROF  // RED counts by role (diagnostics; the global counters distort timings)
 __device__ unsigned long long g_red_cnt[8];  // end: unpacked, packed, rank < 1024, rank < 8192; mid: unpacked, packed
 #define RED_CNT(i) atomicAdd(&g_red_cnt[i], 1ull)
 #else
@@ -1286,7 +1286,11 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   ea.rec_stride = (uint32_t)(std::max<uint32_t>(p->max_mid, 1) + p->max_work / kRecMax + 1);
   ea.cb = cb; ea.cn = cn; ea.cid = cid; ea.cap = cap; ea.tau = tau;
   ea.dense_div = getenv("BBF_DENSE_DIV") ? (uint32_t)atoi(getenv("BBF_DENSE_DIV")) : 2u;
-  ea.bsz = getenv("BBF_T3_BSZ") ? (uint32_t)std::min(32, std::max(0, atoi(getenv("BBF_T3_BSZ")))) : 16u;
+  // hub-kernel record batch: 32 amortises the batch set-up when each CTA has a long share of the
+  // hub wedges (config 5: -1.3% k_t3), 16 balances the tail of a short one (config 3: 32 is +3%)
+  const uint64_t w_per_cta = p->W_t3 / ((uint64_t)g->num_sms * kT3Ctas * (uint64_t)std::max(1, nranks));
+  ea.bsz = getenv("BBF_T3_BSZ") ? (uint32_t)std::min(32, std::max(0, atoi(getenv("BBF_T3_BSZ"))))
+                                : (w_per_cta > (1ull << 24) ? 32u : 16u);
   cudaEvent_t e0, e1, e2;
   cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
   cudaError_t err;
@@ -1326,6 +1330,14 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   host_BN[0] = h[0];
   host_BN[1] = h[1];
   if (n_cand) *n_cand = h[4];
+#ifdef BBF_RED_PROF
+  {
+    unsigned long long rc[8];
+    cudaMemcpyFromSymbol(rc, g_red_cnt, sizeof(rc));
+    fprintf(stderr, "[bbf] REDs (cumulative): end unpacked %llu packed %llu (rank<1024 %llu, <8192 %llu); mid unpacked %llu packed %llu (rank<1024 %llu)\n",
+            rc[0], rc[1], rc[2], rc[3], rc[4], rc[5], rc[6]);
+  }
+#endif
   if (getenv("BBF_DEBUG"))
     fprintf(stderr,
             "[bbf] engine: t3 %.3f ms, t1 %.3f ms, records %llu, windows %llu (small %llu, dense %llu), "
@@ -1336,10 +1348,6 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     const double clk = 1.965e6 * g->num_sms * kT3Ctas;  // cycles per ms summed over CTAs
     fprintf(stderr, "[bbf] t3 phases (ms of CTA time): prescan %.2f setup %.2f pass1 %.2f pass2 %.2f epi %.2f\n",
             h[11] / clk, h[12] / clk, h[13] / clk, h[14] / clk, h[15] / clk);
-    unsigned long long rc[8];
-    cudaMemcpyFromSymbol(rc, g_red_cnt, sizeof(rc));
-    fprintf(stderr, "[bbf] REDs (cumulative): end unpacked %llu packed %llu (rank<1024 %llu, <8192 %llu); mid unpacked %llu packed %llu (rank<1024 %llu)\n",
-            rc[0], rc[1], rc[2], rc[3], rc[4], rc[5], rc[6]);
     unsigned long long t[3];
     cudaMemcpyFromSymbol(t, g_prof_t, sizeof(t));
     fprintf(stderr, "[bbf] t3 CTA ends: first %.3f ms, last %.3f ms after the first start\n", (t[1] - t[0]) * 1e-6,
