@@ -455,7 +455,14 @@ bbf_status bbf_count_global_base(bbf_graph* g, bbf_counts* out) {
   BBF_CUDA(cudaSetDevice(g->device));
   BBF_TRY(check_overflow(g));
   BBF_TRY(ensure_plan_g(g));
-  const int rank = g->comm ? g->comm->rank : 0, nranks = g->comm ? g->comm->nranks : 1;
+  int rank = g->comm ? g->comm->rank : 0, nranks = g->comm ? g->comm->nranks : 1;
+  if (!g->comm && getenv("BBF_FAKE_WORLD")) {  // test hook, as in do_count: one rank's shard only
+    int r = 0, N = 1;
+    if (sscanf(getenv("BBF_FAKE_WORLD"), "%d/%d", &r, &N) == 2 && N >= 1 && r >= 0 && r < N) {
+      rank = r;
+      nranks = N;
+    }
+  }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);

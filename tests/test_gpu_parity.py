@@ -568,3 +568,22 @@ def test_bb_base_gpu_table_limit_error(bbf):
             h.count_global_base()
         assert e.value.name == "BBF_EINVAL"
         assert h.count_global()["balanced"] == O.route_g(g)["B"]
+
+
+@pytest.mark.parametrize("world", [2, 5])
+def test_bb_base_fake_world_shards_sum(bbf, monkeypatch, world):
+    """BB-Base's start sharding (start x on rank x mod N): the shards' counts, each counted alone
+    without the all-reduce, sum to the single-GPU count."""
+    g = _sweep_graph(8)
+    with bbf.Graph.from_synth(g) as h:
+        full = h.count_global_base()
+    tb = tn = 0
+    for r in range(world):
+        monkeypatch.setenv("BBF_FAKE_WORLD", f"{r}/{world}")
+        with bbf.Graph.from_synth(g) as h:
+            part = h.count_global_base()
+        tb += part["balanced"]
+        tn += part["unbalanced"]
+    monkeypatch.delenv("BBF_FAKE_WORLD")
+    assert (tb, tn) == (full["balanced"], full["unbalanced"])
+    assert full["balanced"] == O.route_g(g)["B"]
