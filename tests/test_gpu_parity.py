@@ -587,3 +587,26 @@ def test_bb_base_fake_world_shards_sum(bbf, monkeypatch, world):
     monkeypatch.delenv("BBF_FAKE_WORLD")
     assert (tb, tn) == (full["balanced"], full["unbalanced"])
     assert full["balanced"] == O.route_g(g)["B"]
+
+
+def test_dense_mixed_fp4_int8_sides(bbf):
+    """Dense path where one side's rows exceed the FP4 exactness bound (U rows of degree 9,000 >
+    8,192: int8 kernel on the u8 operands) and the other side's do not (V rows of degree 120: FP4
+    kernel): the load builds u8 operands with FP4 copies for the eligible side only.  Random signs
+    vs the oracle's vBBFC on sampled vertices, and K_{120,9000} closed forms beyond 2^32."""
+    m, n = 120, 9000
+    c2 = lambda k: k * (k - 1) // 2
+    with bbf.Graph.from_synth(G.complete(m, n), flags=bbf.BBF_FORCE_DENSE) as h:
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+    assert tot["balanced"] == c2(m) * c2(n) and tot["unbalanced"] == 0
+    assert (bu == (m - 1) * c2(n)).all() and (bv == (n - 1) * c2(m)).all()
+    assert (m - 1) * c2(n) > 2**32
+    g = G.random_bipartite(m, n, 0.95, 0.5, seed=21)
+    with bbf.Graph.from_synth(g, flags=bbf.BBF_FORCE_DENSE) as h:
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+    rg = O.route_g(g, threads=THREADS)
+    assert (tot["balanced"], tot["unbalanced"]) == (rg["B"], rg["N"])
+    sv = np.arange(0, n, 450)
+    bal, unb = O.route_s(g, verts=np.concatenate([np.arange(m), m + sv]), threads=THREADS)
+    assert np.array_equal(bu, bal[:m]) and np.array_equal(nu, unb[:m])
+    assert np.array_equal(bv[sv], bal[m:]) and np.array_equal(nv[sv], unb[m:])
