@@ -610,3 +610,19 @@ def test_dense_mixed_fp4_int8_sides(bbf):
     bal, unb = O.route_s(g, verts=np.concatenate([np.arange(m), m + sv]), threads=THREADS)
     assert np.array_equal(bu, bal[:m]) and np.array_equal(nu, unb[:m])
     assert np.array_equal(bv[sv], bal[m:]) and np.array_equal(nv[sv], unb[m:])
+
+
+def test_dense_wide_v_side_global_wedge_pass(bbf):
+    """A dense-path candidate whose V side (60,000) is beyond the shared-memory column
+    histograms (49,152): V degrees and the load-time W_G take the hashed / global-atomic kernels;
+    counts and W_G equal the oracle's, per-vertex arrays equal vBBFC on sampled vertices."""
+    g = G.random_bipartite(300, 60000, 0.02, 0.5, seed=31)
+    rg = O.route_g(g, threads=THREADS)
+    with bbf.Graph.from_synth(g, flags=bbf.BBF_FORCE_DENSE) as h:
+        c = h.count_global()
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+    assert (c["balanced"], c["unbalanced"], c["wedges_G"]) == (rg["B"], rg["N"], rg["W_G"])
+    sv = np.arange(0, g.n_v, 997)
+    bal, unb = O.route_s(g, verts=np.concatenate([np.arange(g.n_u), g.n_u + sv]), threads=THREADS)
+    assert np.array_equal(bu, bal[:g.n_u]) and np.array_equal(nu, unb[:g.n_u])
+    assert np.array_equal(bv[sv], bal[g.n_u:]) and np.array_equal(nv[sv], unb[g.n_u:])
