@@ -4,7 +4,7 @@ shape of the paper's Senate/House roll-call graphs; seeded, synthetic), counted 
 (bbf_count_global_base) and Alg. 2 (bbf_count_global, sparse path) through the C ABI; device
 time per call (median of --reps), counts checked equal.  The smallest shape is also timed on
 the oracle (both algorithms, one host thread) for the CPU regime.
-python tools/base_vs_bucket.py [--json profiles/r1_base_vs_bucket.json]"""
+python tests/scripts/base_vs_bucket.py [--json profiles/r1_base_vs_bucket.json]"""
 import argparse
 import json
 import os
@@ -12,7 +12,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
 
 def main():

@@ -1,6 +1,6 @@
 """Small end-to-end driver for compute-sanitizer (memcheck / racecheck / synccheck): every kernel
 family of libbbf.so on tiny graphs, each result checked against the oracle.
-  compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_run.py
+  compute-sanitizer --tool memcheck --error-exitcode 9 python tests/scripts/sanitize_run.py
 Covers: build (hashed and shared-memory histograms), plan, the T1 / T2 / T3 tiers (T2_MAX lowered so
 hubs take the hub kernel), a hub with a large end side, both counter encodings, top-k pairs and vertices,
 the positive-only mask, the dense FP4 (one and two accumulators), int8 pair and 1-CTA kernels, the
@@ -11,7 +11,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
 import oracle as O  # noqa: E402  (test infrastructure: this script is a checker)
 from synth import graphs as G  # noqa: E402
