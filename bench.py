@@ -118,52 +118,106 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def cpu_baseline(g, target_s: float = 15.0, seed: int = 0):
-    """The oracle (oracle/bbf_oracle.c, Alg. 2 route G with ParBB-Bucket threading) on a
-    bounded random sample of start vertices of the same graph; value = wedges/s of its
-    counting loop.  Returns the cpu_baseline object."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def expected_counts(config: int):
+    """The oracle's counts for `config` (tests/golden/expected_counts.json, written by
+    tests/scripts/write_expected.py, which calls only oracle/)."""
+    with open(os.path.join(ROOT, "tests", "golden", "expected_counts.json")) as f:
+        return json.load(f)[f"config{config}"]
+
+
+def pv_sha256(arrays) -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a, dtype="<u8").tobytes())
+    return h.hexdigest()
+
+
+def check_parity(g, config: int, tot: dict, pv) -> dict:
+    """Bit-exact parity gate run before any throughput number is printed: B, N, W_G and the
+    per-vertex arrays of this run against the oracle's expected-counts file.  Raises on a
+    mismatch."""
+    exp = expected_counts(config)
+    assert exp["graph_sha256"] == g.sha256(), "synthetic graph differs from the one the oracle counted"
+    got = (tot["balanced"], tot["unbalanced"], tot["wedges_G"])
+    want = (exp["B"], exp["N"], exp["W_G"])
+    assert got == want, f"parity: (B, N, W_G) {got} != oracle {want}"
+    sha = pv_sha256(pv)
+    assert sha == exp["pv_sha256"], "parity: per-vertex arrays differ from the oracle's"
+    return {"B": exp["B"], "N": exp["N"], "W_G": exp["W_G"], "pv_sha256": sha,
+            "source": "tests/golden/expected_counts.json (oracle_route_g_pv)"}
+
+
+def cpu_baseline(g, pv=None, single_thread_configs=(1, 2, 3)):
+    """The oracle as it stands (oracle/bbf_oracle.c oracle_route_g_pv: Alg. 2 / ParBB-Bucket with
+    the 4-role scatter, dynamic start chunks over all host threads) on the WHOLE graph — global
+    and per-vertex counts, the same outputs as the GPU step.  value = W_G / its counting-loop time.
+    When `pv` (the GPU's per-vertex arrays) is given, they are compared with the oracle's element
+    by element in this same run (raises on a mismatch).  Also the single-thread Alg. 2 time
+    (global counts) of the small configs, as the paper reports sequential BB-Bucket."""
     import oracle as O
+    from synth import graphs as G
     threads = os.cpu_count() or 1
-    n = g.n_u + g.n_v
-    rng = np.random.default_rng(seed)
-    frac = 0.01
-    r = None
-    for _ in range(3):
-        starts = np.sort(rng.choice(n, size=max(1, int(n * frac)), replace=False)).astype(np.uint32)
-        r = O.route_g(g, starts=starts, threads=threads)
-        if r["count_s"] > target_s / 4 or frac >= 1.0:
-            break
-        frac = min(1.0, frac * max(2.0, target_s / max(r["count_s"], 1e-3) / 2))
+    r = O.route_g_pv(g, threads=threads)
+    if pv is not None:
+        for name, a in zip(("bal_u", "unb_u", "bal_v", "unb_v"), pv):
+            assert np.array_equal(np.asarray(a).view(np.uint64), r[name]), f"parity vs oracle: {name}"
+    single = {}
+    for c in single_thread_configs:
+        s = O.route_g(G.make_config(c), threads=1)
+        single[f"config{c}"] = {"seconds": s["count_s"], "wedges_G": s["W_G"],
+                                "wedges_per_s": s["W_G"] / max(s["count_s"], 1e-9)}
     return {"value": r["W_G"] / max(r["count_s"], 1e-9), "unit": "wedges/s", "cores": threads,
-            "kind": "oracle",
-            "sample": (f"route G (Alg. 2 / ParBB-Bucket) over a random {frac:.4f} fraction of the "
-                       f"start vertices ({r['W_G']:.3e} priority-eligible wedges), counting loop "
-                       f"{r['count_s']:.2f} s on {threads} threads; per-vertex counting not included"),
-            "wedges": r["W_G"], "seconds": r["count_s"]}
+            "kind": "oracle", "cpu_model": cpu_model(),
+            "sample": (f"the whole workload: oracle_route_g_pv (Alg. 2 + 4-role scatter, global + "
+                       f"per-vertex counts) over all {g.n_u + g.n_v} start vertices, "
+                       f"{r['W_G']:.4e} wedges, counting loop {r['count_s']:.2f} s on {threads} threads "
+                       f"(graph build and adjacency sort excluded)"),
+            "seconds": r["count_s"], "wedges": r["W_G"],
+            "parity_vs_gpu_arrays": pv is not None,
+            "single_thread_route_g_global": single}
 
 
 def reference_arm(args):
-    """--impl reference: the CPU oracle as it stands, on this arm's config/metric."""
+    """--impl reference: the CPU oracle as it stands (oracle_route_g_pv, all host threads), on this
+    arm's config/metric.  Step i counts start slice i of W+K deterministic disjoint slices (start x
+    in slice x mod (W+K)), so the whole run is one full pass over the graph and every timed step
+    is a bounded, reproducible sample of it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    import oracle as O
     from synth import graphs as G
     g = G.make_config(args.config)
-    steps = []
-    for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(g, target_s=max(2.0, 60.0 / max(1, args.warmup + args.steps)), seed=i)
+    threads = os.cpu_count() or 1
+    S = args.warmup + args.steps
+    ids = np.arange(g.n_u + g.n_v, dtype=np.uint32)
+    W = T = 0.0
+    for i in range(S):
+        r = O.route_g_pv(g, threads=threads, starts=ids[i::S])
         if i >= args.warmup:
-            steps.append(cb)
-    W = sum(s["wedges"] for s in steps)
-    T = sum(s["seconds"] for s in steps)
+            W += r["W_G"]
+            T += r["count_s"]
     v = W / max(T, 1e-9)
+    sample = (f"oracle_route_g_pv (Alg. 2 + 4-role scatter, global + per-vertex) on {threads} threads; "
+              f"step = start slice (x mod {S}); the {args.steps} timed slices hold {W:.4e} wedges")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "wedges/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * T / max(1, len(steps)), "higher_is_better": True,
+            "ms_per_step": 1e3 * T / max(1, args.steps), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "uint32+uint128", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config], "counts": "global (route G sample)"},
-            "cpu_baseline": {"value": v, "unit": "wedges/s", "cores": steps[0]["cores"],
-                             "kind": "oracle", "sample": steps[0]["sample"]},
+            "config": {"workload": WORKLOADS[args.config], "counts": "global + per-vertex (both sides)"},
+            "cpu_baseline": {"value": v, "unit": "wedges/s", "cores": threads, "kind": "oracle",
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": v, "unit": "wedges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -263,6 +317,10 @@ def main():
         cms = float(t.item())
     value = W_G * args.steps / (ms * 1e-3)
     bfly = tot["balanced"] * args.steps / (ms * 1e-3)
+    # parity gate (bit-exact, before anything is printed): the last timed step's counts and
+    # per-vertex arrays against the oracle's
+    pv_host = [o.cpu().numpy().view(np.uint64) for o in outs]
+    parity = check_parity(g, args.config, tot, pv_host)
 
     # e2e: the same step through the public API with HOST buffers, pipelined as a stream of
     # graphs: every step's CSR is copied from pinned host memory by bbf_upload_csr (the next
@@ -308,6 +366,8 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         assert tot_e["balanced"] == tot["balanced"]
+        # the host-buffer path's outputs pass the same parity gate
+        assert pv_sha256([o.numpy().view(np.uint64) for o in h_out]) == parity["pv_sha256"]
     h2d = g.row_ptr.nbytes + g.col.nbytes + g.sign.nbytes
     d2h = 8 * 2 * (n_u + n_v)
 
@@ -357,7 +417,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "wedges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "strong" if world > 1 else "strong",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": dtype, "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "counts": "global + per-vertex (both sides)",
                    "wedges_G": W_G, "balanced": tot["balanced"], "unbalanced": tot["unbalanced"],
@@ -380,10 +440,11 @@ def main():
         "roofline": roof,
         "clocks": clocks,
     }
+    line["parity"] = parity
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(g)
+        line["cpu_baseline"] = cpu_baseline(g, pv=pv_host)
         line["cpu_baseline"].pop("wedges", None)
-        line["cpu_baseline"].pop("seconds", None)
+        line["parity"]["oracle_run_in_this_job"] = True
     if rank == 0:
         print(json.dumps(line), flush=True)
     if comm:

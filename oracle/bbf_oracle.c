@@ -16,7 +16,9 @@
  *                    thread.  Global B; N = sum B1[w]*B2[w] (Theorem proof, PAPER.md:784:
  *                    "one symmetric and one asymmetric wedge are an unbalanced butterfly");
  *                    W_G = number of priority-eligible wedges.
- *   oracle_route_s   Alg. vBBFC for a list of vertices: all wedges
+ *   oracle_route_g_pv  the same Alg. 2 buckets plus the 4-role scatter (SURVEY.md §8(c) O4.3,
+ *                    DESIGN.md reading R22): per-vertex B_z, N_z for every vertex of both sides.
+ *   oracle_route_s  Alg. vBBFC for a list of vertices: all wedges
  *                    u-v-w, no rank comparison, w != u (reading R9),
  *                    buckets H1/H2, sum C(H1,2)+C(H2,2); the unbalanced count H1*H2 alongside.
  *   oracle_bb_base   Alg. 1 BB-Base: per start, lists H(w) of middles, every
@@ -178,9 +180,12 @@ typedef struct {
   const uint32_t *starts;  /* NULL: all vertices */
   uint64_t n_starts;
   int tid, nthreads;
+  uint64_t *cursor;        /* shared start cursor: starts are handed out in chunks (ForPar) */
   u128 B, N, W;
   int rc;
 } rg_task;
+
+#define ORACLE_CHUNK 64u
 
 static const graph_t *g_sort_graph;  /* qsort context for line 3 of Alg. 2 */
 static int cmp_by_prio(const void *a, const void *b) {
@@ -220,7 +225,12 @@ static void *route_g_worker(void *arg) {
   uint32_t *touched = (uint32_t *)malloc(sizeof(uint32_t) * ((size_t)g->n + 1));
   if (!B1 || !B2 || !touched) { t->rc = 4; free(B1); free(B2); free(touched); return NULL; }
   uint64_t total = t->starts ? t->n_starts : g->n;
-  for (uint64_t i = (uint64_t)t->tid; i < total; i += (uint64_t)t->nthreads) {
+  for (uint64_t i = 0, lim = 0;; ++i) {
+    if (i == lim) {
+      i = __atomic_fetch_add(t->cursor, ORACLE_CHUNK, __ATOMIC_RELAXED);
+      lim = i + ORACLE_CHUNK < total ? i + ORACLE_CHUNK : total;
+    }
+    if (i >= total) break;
     uint32_t u = t->starts ? t->starts[i] : (uint32_t)i;
     uint64_t pu = g->prio[u];
     uint64_t nt = 0;
@@ -264,12 +274,149 @@ int oracle_route_g(uint32_t n_u, uint32_t n_v, const uint64_t *row_ptr, const ui
   if (nthreads < 1) nthreads = 1;
   rg_task *tasks = (rg_task *)calloc((size_t)nthreads, sizeof(rg_task));
   pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+  uint64_t cursor = 0;
   struct timespec t0, t1;
   clock_gettime(CLOCK_MONOTONIC, &t0);
   for (int i = 0; i < nthreads; ++i) {
     tasks[i].g = &g; tasks[i].starts = starts; tasks[i].n_starts = n_starts;
-    tasks[i].tid = i; tasks[i].nthreads = nthreads;
+    tasks[i].tid = i; tasks[i].nthreads = nthreads; tasks[i].cursor = &cursor;
     pthread_create(&th[i], NULL, route_g_worker, &tasks[i]);
+  }
+  u128 B = 0, N = 0, W = 0;
+  rc = 0;
+  for (int i = 0; i < nthreads; ++i) {
+    pthread_join(th[i], NULL);
+    B += tasks[i].B; N += tasks[i].N; W += tasks[i].W;
+    if (tasks[i].rc) rc = tasks[i].rc;
+  }
+  clock_gettime(CLOCK_MONOTONIC, &t1);
+  free(tasks); free(th); graph_free(&g);
+  if (rc) return rc;
+  if (B >> 64 || N >> 64 || W >> 64) return 7;
+  out[0] = (uint64_t)B; out[1] = (uint64_t)N; out[2] = (uint64_t)W;
+  out[3] = (uint64_t)(t1.tv_sec - t0.tv_sec) * 1000000000ull + (uint64_t)(t1.tv_nsec - t0.tv_nsec);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Alg. 2 with the 4-role scatter (reading R22): per-vertex
+ * balanced / unbalanced counts from the same per-start buckets.  Alg. 2 counts every butterfly
+ * once, at its maximum-priority vertex u, as a pair (u,w) of its two same-side vertices with
+ * two middles v, v' among the l = B1[w] symmetric and m = B2[w] asymmetric wedges u-v-w
+ * (Lemma 2: two wedges of the same class form a balanced butterfly, one of
+ * each class an unbalanced one; Theorem proof).  So, per start u and end w:
+ *   - u and w are in every butterfly of the pair:  C(l,2)+C(m,2) balanced, l*m unbalanced;
+ *   - a middle v of a symmetric wedge is in the balanced butterflies it forms with the other
+ *     l-1 symmetric middles and in the unbalanced ones it forms with the m asymmetric middles;
+ *     a middle of an asymmetric wedge: m-1 balanced, l unbalanced.
+ * Step by step: lines 7-14 of Alg. 2 fill B1/B2 (as route_g_worker); then a second sweep over
+ * the same wedges hands each middle its share; then lines 15-18 hand u and w theirs.
+ * bal / unb are indexed by global id (U: u, V: n_u + v).  Every per-vertex count is at most the
+ * global count of its class (a butterfly containing z is counted once for z), so once the global
+ * u128 sums are checked to fit uint64 every per-vertex uint64 sum is exact.
+ * ---------------------------------------------------------------------------------------- */
+typedef struct {
+  const graph_t *g;
+  const uint32_t *starts;  /* NULL: all vertices */
+  uint64_t n_starts;
+  int tid, nthreads;
+  uint64_t *bal, *unb;
+  uint64_t *cursor;
+  u128 B, N, W;
+  int rc;
+} rgpv_task;
+
+static void *route_g_pv_worker(void *arg) {
+  rgpv_task *t = (rgpv_task *)arg;
+  const graph_t *g = t->g;
+  uint32_t *B1 = (uint32_t *)calloc((size_t)g->n + 1, sizeof(uint32_t));
+  uint32_t *B2 = (uint32_t *)calloc((size_t)g->n + 1, sizeof(uint32_t));
+  uint32_t *touched = (uint32_t *)malloc(sizeof(uint32_t) * ((size_t)g->n + 1));
+  if (!B1 || !B2 || !touched) { t->rc = 4; free(B1); free(B2); free(touched); return NULL; }
+  uint64_t total = t->starts ? t->n_starts : g->n;
+  for (uint64_t i = 0, lim = 0;; ++i) {
+    if (i == lim) {
+      i = __atomic_fetch_add(t->cursor, ORACLE_CHUNK, __ATOMIC_RELAXED);
+      lim = i + ORACLE_CHUNK < total ? i + ORACLE_CHUNK : total;
+    }
+    if (i >= total) break;
+    uint32_t u = t->starts ? t->starts[i] : (uint32_t)i;
+    uint64_t pu = g->prio[u];
+    uint64_t nt = 0;
+    /* lines 7-14: buckets of the eligible wedges u-v-w */
+    for (uint64_t e = g->off[u]; e < g->off[u + 1]; ++e) {
+      uint32_t v = g->nbr[e];
+      if (!(g->prio[v] < pu)) break;
+      for (uint64_t f = g->off[v]; f < g->off[v + 1]; ++f) {
+        uint32_t w = g->nbr[f];
+        if (!(g->prio[w] < pu)) break;
+        if (B1[w] == 0 && B2[w] == 0) touched[nt++] = w;
+        if (g->sgn[e] == g->sgn[f]) B1[w]++;
+        else B2[w]++;
+        t->W++;
+      }
+    }
+    /* middle role: the same wedges again, each middle v summing its shares over its ends */
+    for (uint64_t e = g->off[u]; e < g->off[u + 1]; ++e) {
+      uint32_t v = g->nbr[e];
+      if (!(g->prio[v] < pu)) break;
+      u128 bv = 0, nv = 0;
+      for (uint64_t f = g->off[v]; f < g->off[v + 1]; ++f) {
+        uint32_t w = g->nbr[f];
+        if (!(g->prio[w] < pu)) break;
+        if (g->sgn[e] == g->sgn[f]) { bv += B1[w] - 1; nv += B2[w]; }  /* symmetric wedge */
+        else { bv += B2[w] - 1; nv += B1[w]; }                        /* asymmetric wedge */
+      }
+      __atomic_fetch_add(&t->bal[v], (uint64_t)bv, __ATOMIC_RELAXED);
+      __atomic_fetch_add(&t->unb[v], (uint64_t)nv, __ATOMIC_RELAXED);
+    }
+    /* lines 15-18, plus the shares of the pair's two same-side vertices u and w */
+    u128 bu = 0, nu = 0;
+    for (uint64_t k = 0; k < nt; ++k) {
+      uint32_t w = touched[k];
+      u128 l = B1[w], m = B2[w];
+      u128 fb = l * (l - (l > 0)) / 2 + m * (m - (m > 0)) / 2;   /* C(l,2) + C(m,2) */
+      u128 fn = l * m;
+      bu += fb; nu += fn;
+      __atomic_fetch_add(&t->bal[w], (uint64_t)fb, __ATOMIC_RELAXED);
+      __atomic_fetch_add(&t->unb[w], (uint64_t)fn, __ATOMIC_RELAXED);
+      B1[w] = 0; B2[w] = 0;
+    }
+    t->B += bu; t->N += nu;
+    __atomic_fetch_add(&t->bal[u], (uint64_t)bu, __ATOMIC_RELAXED);
+    __atomic_fetch_add(&t->unb[u], (uint64_t)nu, __ATOMIC_RELAXED);
+  }
+  free(B1); free(B2); free(touched);
+  return NULL;
+}
+
+/* out[0]=B, out[1]=N, out[2]=W_G, out[3]=wall ns of the counting loop; bal / unb: n_u + n_v
+ * entries each (global ids), overwritten.  starts: optional list of global ids (NULL = all);
+ * with a list, the counts are those of the butterflies counted at the listed starts. */
+int oracle_route_g_pv(uint32_t n_u, uint32_t n_v, const uint64_t *row_ptr, const uint32_t *col,
+                      const uint8_t *sign, const uint32_t *starts, uint64_t n_starts,
+                      int nthreads, uint64_t *out, uint64_t *bal, uint64_t *unb) {
+  if (!bal || !unb || !out) return 1;
+  graph_t g;
+  int rc = graph_build(&g, n_u, n_v, row_ptr, col, sign);
+  if (rc) return rc;
+  if ((rc = sort_adjacency_by_priority(&g))) { graph_free(&g); return rc; }
+  if (starts)
+    for (uint64_t i = 0; i < n_starts; ++i)
+      if (starts[i] >= g.n) { graph_free(&g); return 2; }
+  memset(bal, 0, sizeof(uint64_t) * (size_t)g.n);
+  memset(unb, 0, sizeof(uint64_t) * (size_t)g.n);
+  if (nthreads < 1) nthreads = 1;
+  rgpv_task *tasks = (rgpv_task *)calloc((size_t)nthreads, sizeof(rgpv_task));
+  pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+  uint64_t cursor = 0;
+  struct timespec t0, t1;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+  for (int i = 0; i < nthreads; ++i) {
+    tasks[i].g = &g; tasks[i].tid = i; tasks[i].nthreads = nthreads;
+    tasks[i].starts = starts; tasks[i].n_starts = n_starts;
+    tasks[i].bal = bal; tasks[i].unb = unb; tasks[i].cursor = &cursor;
+    pthread_create(&th[i], NULL, route_g_pv_worker, &tasks[i]);
   }
   u128 B = 0, N = 0, W = 0;
   rc = 0;

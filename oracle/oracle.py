@@ -45,6 +45,8 @@ def _load():
         lib.oracle_brute.argtypes = [u32, u32, P, P, P, P, P, P, P, P, P]
         lib.oracle_route_g.argtypes = [u32, u32, P, P, P, P, u64, i32, P]
         lib.oracle_route_s.argtypes = [u32, u32, P, P, P, P, u64, i32, P, P]
+        lib.oracle_route_g_pv.argtypes = [u32, u32, P, P, P, P, u64, i32, P, P, P]
+        lib.oracle_route_g_pv.restype = i32
         lib.oracle_bb_base.argtypes = [u32, u32, P, P, P, i32, P]
         lib.oracle_bb_base.restype = i32
         lib.oracle_pairs.argtypes = [u32, u32, P, P, P, i32, i32, P, P, P, P, u64, P]
@@ -106,6 +108,25 @@ def route_g(g, starts=None, threads=None):
     if rc:
         raise OracleError(rc)
     return dict(B=int(out[0]), N=int(out[1]), W_G=int(out[2]), count_s=float(out[3]) * 1e-9)
+
+
+def route_g_pv(g, threads=None, starts=None):
+    """Alg. 2 BB-Bucket plus the 4-role scatter (bbf_oracle.c oracle_route_g_pv): global counts
+    and the per-vertex arrays of both sides.  starts: optional global ids (the butterflies
+    counted at those starts only).  Returns dict(B, N, W_G, count_s, bal_u, unb_u, bal_v,
+    unb_v)."""
+    lib = _load()
+    keep, a = _graph_args(g)
+    out = np.zeros(4, np.uint64)
+    n = g.n_u + g.n_v
+    bal, unb = np.zeros(n, np.uint64), np.zeros(n, np.uint64)
+    st = None if starts is None else np.ascontiguousarray(starts, dtype=np.uint32)
+    rc = lib.oracle_route_g_pv(*a, _ptr(st), C.c_uint64(0 if st is None else st.size),
+                               _threads(threads), _ptr(out), _ptr(bal), _ptr(unb))
+    if rc:
+        raise OracleError(rc)
+    return dict(B=int(out[0]), N=int(out[1]), W_G=int(out[2]), count_s=float(out[3]) * 1e-9,
+                bal_u=bal[:g.n_u], unb_u=unb[:g.n_u], bal_v=bal[g.n_u:], unb_v=unb[g.n_u:])
 
 
 def bb_base(g, threads=None):

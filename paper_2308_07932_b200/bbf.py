@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbbf.so")
+# BBF_LIB: load a diagnostic variant built by `python -m paper_2308_07932_b200.build --variant`
+LIB_PATH = os.environ.get("BBF_LIB") or os.path.join(_HERE, "libbbf.so")
 
 BBF_OK, BBF_EINVAL, BBF_ERANGE, BBF_EDUP, BBF_ENOMEM, BBF_ECUDA, BBF_ENCCL, BBF_EOVERFLOW = range(8)
 STATUS_NAMES = {0: "BBF_OK", 1: "BBF_EINVAL", 2: "BBF_ERANGE", 3: "BBF_EDUP", 4: "BBF_ENOMEM",

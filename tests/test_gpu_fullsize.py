@@ -1,0 +1,105 @@
+"""Full-size GPU parity: the ENTIRE per-vertex arrays (both sides) of BASELINE configs 3, 4 and 5
+and of the zoned graph against the oracle's Alg. 2 + 4-role scatter (oracle_route_g_pv), plus
+global B, N and W_G, plus the expected-counts file bench.py asserts against
+(tests/golden/expected_counts.json, written by tests/scripts/write_expected.py from oracle/ only).
+
+Also the multi-GPU decomposition on hub graphs: BBF_FAKE_WORLD=r/N counts rank r's shard of the
+work items alone (hub units of k_t3, k_t2 starts, k_t1 starts) on one GPU; the shards must sum to
+the oracle's arrays element by element, and every shard must hold part of the work."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from synth import graphs as G
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 8
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "expected_counts.json")
+_cache = {}
+
+
+@pytest.fixture(scope="module")
+def bbf():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2308_07932_b200 import build
+    build.build()
+    from paper_2308_07932_b200 import bbf as B
+    return B
+
+
+def graph(name):
+    if name not in _cache:
+        if name == "zoned":
+            from test_gpu_parity import zoned_graph
+            g = zoned_graph()
+        else:
+            g = G.make_config(int(name[-1]))
+        _cache[name] = (g, O.route_g_pv(g, threads=THREADS))
+    return _cache[name]
+
+
+def pv_sha256(bu, nu, bv, nv):
+    h = hashlib.sha256()
+    for a in (bu, nu, bv, nv):
+        h.update(np.ascontiguousarray(a, dtype="<u8").tobytes())
+    return h.hexdigest()
+
+
+def assert_equal_arrays(got, want, tag):
+    for k, a in zip(("bal_u", "unb_u", "bal_v", "unb_v"), got):
+        b = want[k]
+        if not np.array_equal(a, b):
+            bad = np.nonzero(a != b)[0]
+            raise AssertionError(f"{tag} {k}: {bad.size} vertices differ, first {bad[:5].tolist()} "
+                                 f"got {a[bad[:5]].tolist()} want {b[bad[:5]].tolist()}")
+
+
+@pytest.mark.parametrize("name,flags", [("config3", "default"), ("config4", "default"),
+                                        ("config4", "sparse"), ("config5", "default"),
+                                        ("zoned", "sparse")])
+def test_full_per_vertex_vs_oracle(bbf, name, flags):
+    g, want = graph(name)
+    fl = {"default": 0, "sparse": bbf.BBF_FORCE_SPARSE}[flags]
+    with bbf.Graph.from_synth(g, flags=fl) as h:
+        c = h.count_global()
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+        st = h.stats()
+    if name == "config4" and flags == "default":
+        assert st["algo_ops"] > 0  # the dispatch sent it to the tensor-core path
+    assert (c["balanced"], c["unbalanced"], c["wedges_G"]) == (want["B"], want["N"], want["W_G"])
+    assert (tot["balanced"], tot["unbalanced"]) == (want["B"], want["N"])
+    assert_equal_arrays((bu, nu, bv, nv), want, name)
+    if name.startswith("config"):
+        exp = json.load(open(GOLDEN))[name]
+        assert exp["graph_sha256"] == g.sha256()
+        assert (exp["B"], exp["N"], exp["W_G"]) == (want["B"], want["N"], want["W_G"])
+        assert exp["pv_sha256"] == pv_sha256(bu, nu, bv, nv)
+
+
+@pytest.mark.parametrize("name", ["config3", "zoned"])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_fake_world_shards_on_hub_graphs(bbf, monkeypatch, name, world):
+    """The sharded work items of every tier (k_t3 hub units, k_t2 and k_t1 starts; item i on rank
+    i mod N) counted rank by rank: shards sum to the oracle's global and per-vertex counts, and
+    no shard is empty or the whole."""
+    g, want = graph(name)
+    acc = None
+    parts = []
+    for r in range(world):
+        monkeypatch.setenv("BBF_FAKE_WORLD", f"{r}/{world}")
+        with bbf.Graph.from_synth(g, flags=bbf.BBF_FORCE_SPARSE) as h:
+            part = h.count_per_vertex()
+        parts.append(part[0]["balanced"])
+        vals = [part[0]["balanced"], part[0]["unbalanced"]] + [a.astype(object) for a in part[1:]]
+        acc = vals if acc is None else [x + y for x, y in zip(acc, vals)]
+    monkeypatch.delenv("BBF_FAKE_WORLD")
+    assert (acc[0], acc[1]) == (want["B"], want["N"])
+    assert all(0 < p < want["B"] for p in parts), parts
+    assert_equal_arrays([a.astype(np.uint64) for a in acc[2:]], want, f"{name} world {world}")

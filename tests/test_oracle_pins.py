@@ -351,3 +351,73 @@ def test_bb_base_vs_bucket_regime_desk_scale():
     r = min((O.route_g(g, threads=1) for _ in range(3)), key=lambda r: r["count_s"])
     assert (b["B"], b["N"], b["W_G"]) == (r["B"], r["N"], r["W_G"])
     assert b["count_s"] > r["count_s"]
+
+
+# ----------------------------------------------------------------------------- 4-role scatter
+
+def test_route_g_pv_corpus_against_brute_force():
+    """oracle_route_g_pv (Alg. 2 + the 4-role scatter) equals the brute-force
+    4-tuple classification per vertex of both sides, on the SPEC-style corpus.
+    A swapped middle share ((a, d-1) for (a-1, d)), a missing end share or a start share sent to
+    the wrong vertex changes some vertex of some graph here."""
+    for g in corpus(1000):
+        br = O.brute(g)
+        pv = O.route_g_pv(g, threads=1 + g.n_u % 3)
+        assert (pv["B"], pv["N"]) == (br["B"], br["N"]), g.name
+        for k in ("bal_u", "unb_u", "bal_v", "unb_v"):
+            assert np.array_equal(pv[k], br[k]), (g.name, k)
+        assert pv["W_G"] == O.route_g(g)["W_G"]
+
+
+@pytest.mark.parametrize("m,n", [(2, 2), (3, 5), (9, 4), (1, 6)])
+def test_route_g_pv_complete_closed_form(m, n):
+    """K_{m,n}, all positive: every U vertex is in (m-1) C(n,2) butterflies, every V
+    vertex in (n-1) C(m,2), all balanced."""
+    g = G.complete(m, n)
+    c = lambda k: k * (k - 1) // 2
+    pv = O.route_g_pv(g)
+    assert np.all(pv["bal_u"] == (m - 1) * c(n)) and np.all(pv["bal_v"] == (n - 1) * c(m))
+    assert not pv["unb_u"].any() and not pv["unb_v"].any()
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_route_g_pv_against_vbbfc_medium(seed):
+    """On graphs too large for brute force, the route-G per-vertex arrays equal the definition
+    path vBBFC vertex by vertex, and each side sums to 2B."""
+    g = G.random_bipartite(300, 200, 0.04 + 0.03 * seed, 0.3 + 0.3 * seed, seed=4242 + seed)
+    pv = O.route_g_pv(g, threads=4)
+    bal, unb = O.route_s(g, threads=4)
+    assert np.array_equal(np.concatenate([pv["bal_u"], pv["bal_v"]]), bal)
+    assert np.array_equal(np.concatenate([pv["unb_u"], pv["unb_v"]]), unb)
+    assert int(pv["bal_u"].sum()) == 2 * pv["B"] == int(pv["bal_v"].sum())
+    assert int(pv["unb_v"].sum()) == 2 * pv["N"]
+
+
+def test_route_g_pv_switching_invariant_and_powerlaw():
+    """A skewed Chung-Lu graph (hub starts with many ends): route-G per-vertex == vBBFC, and
+    switching the signs at a hub leaves every per-vertex count unchanged."""
+    key, rng = G.chung_lu(3000, 800, 20000, 2.0, 400.0, 400.0, seed=31)
+    s = rng.random(key.size) < 0.6
+    g = G._from_sorted_keys(3000, 800, key, s, "cl")
+    pv = O.route_g_pv(g, threads=3)
+    bal, unb = O.route_s(g, threads=8)
+    assert np.array_equal(np.concatenate([pv["bal_u"], pv["bal_v"]]), bal)
+    assert np.array_equal(np.concatenate([pv["unb_u"], pv["unb_v"]]), unb)
+    hub = int(np.argmax(np.diff(g.row_ptr.astype(np.int64))))
+    h = switch(g, hub)
+    q = O.route_g_pv(h, threads=2)
+    for k in ("bal_u", "unb_u", "bal_v", "unb_v"):
+        assert np.array_equal(q[k], pv[k])
+
+
+def test_route_g_pv_start_partition_additive():
+    """Per-vertex counts of disjoint start sets sum to the whole (the property the
+    reference arm's start slices and the multi-GPU split rely on)."""
+    g = G.random_bipartite(90, 60, 0.25, 0.6, seed=12)
+    full = O.route_g_pv(g)
+    lab = np.random.default_rng(2).integers(0, 4, size=g.n_u + g.n_v)
+    parts = [O.route_g_pv(g, starts=np.nonzero(lab == k)[0], threads=2) for k in range(4)]
+    for key in ("B", "N", "W_G"):
+        assert sum(p[key] for p in parts) == full[key]
+    for key in ("bal_u", "unb_u", "bal_v", "unb_v"):
+        assert np.array_equal(sum(p[key] for p in parts), full[key])
