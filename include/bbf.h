@@ -28,8 +28,13 @@
  *   Synchronisation: calls return after host outputs are written.
  *   Threading: calls on one handle must be serialised; distinct handles are independent.
  *   Collectives: with a bbf_comm, every rank calls the same functions in the same order with
- *     the same graph; each rank counts its shard of the work and the library all-reduces
- *     (NCCL, u64 sum) so every rank receives the full results.
+ *     the same graph; each rank counts its shard of the work (work item i on rank i mod N) and
+ *     the library all-reduces (NCCL, u64 sum) so every rank receives the full results; top-k
+ *     pairs are all-gathered per rank and merged.  Every rank enters the collectives whatever
+ *     its local status and the ranks' status codes are max-reduced, so a local failure (an
+ *     allocation, a table limit) is returned by every rank instead of blocking the others.
+ *     Waits on a communicator poll ncclCommGetAsyncError: an asynchronous NCCL failure returns
+ *     BBF_ENCCL and aborts the communicator (free it with bbf_comm_free).
  *   Errors: every function returns a bbf_status; on failure outputs are unspecified, the
  *     message is available from bbf_last_error() (thread-local), and the handle stays valid
  *     except after BBF_ECUDA.  No C++ exception crosses the ABI.
@@ -141,8 +146,21 @@ bbf_status bbf_upload_free(bbf_upload *up);
 bbf_status bbf_device_sync(int device);
 
 /* Global balanced / unbalanced counts (each butterfly once; Alg. 2).  out: host.  Path: the
- * load flags' BBF_FORCE_* if any, else the dispatch rule.  BBF_EINVAL if BBF_FORCE_DENSE was
- * given for a graph the dense path does not support (other side > 65,536 vertices). */
+ * load flags' BBF_FORCE_* if any, else the dispatch rule.
+ * Limits and errors (also for bbf_count_per_vertex and bbf_count_pairs_topk):
+ *   BBF_EINVAL if BBF_FORCE_DENSE was given for a graph the dense path does not support (other
+ *     side > 65,536 vertices, or operands > 16 GB);
+ *   BBF_ERANGE if the sparse hub kernel would need more than 256 counter windows on one side:
+ *     a window holds 52,224 words of degree-zoned (a, d) fields (8 ends of degree 2-3 per word
+ *     down to one end of degree >= 256 per word, two words above 65,535), so a side holds at
+ *     most ~13.4M counter words — e.g. 107M ends of degree <= 3, or 13.4M ends of degree >= 256;
+ *   BBF_EOVERFLOW if B + N could exceed 2^64 - 1 (host bound, reading R13);
+ *   BBF_ENOMEM, BBF_ECUDA, BBF_ENCCL.
+ * The dense path's block-scaled FP4 kernels (tcgen05 kind::mxf4) multiply exact +-1/0 e2m1
+ * operands with unit scales and accumulate in fp32; they are used only while every partial sum
+ * is an integer of magnitude <= 2^13 (rows' max degree <= 8,192; packed-accumulator variant
+ * |T + 2048 P| < 2^22 for degree < 2,048), where fp32 — even a reduced-precision tensor-core
+ * accumulator — is exact; beyond that the int8 kernels (exact s32) run. */
 bbf_status bbf_count_global(bbf_graph *g, bbf_counts *out);
 
 /* The same global counts by Alg. 1 BB-Base, the paper's baseline: per start
@@ -152,7 +170,8 @@ bbf_status bbf_count_global(bbf_graph *g, bbf_counts *out);
  * bbf_count_global's.  Sparse path only; starts sharded over the ranks of comm like
  * bbf_count_global, counts all-reduced.  out: host (ms_count = device time of this call).
  * Errors: BBF_EINVAL if a start has more than 8,192 distinct ends (the per-CTA table),
- * BBF_ENOMEM if a start has more than 8 GiB of wedges, BBF_EOVERFLOW, BBF_ECUDA, BBF_ENCCL. */
+ * BBF_ENOMEM if a start has 2^32 or more wedges (32-bit list offsets; the 8 GiB scratch holds
+ * them), BBF_EOVERFLOW, BBF_ECUDA, BBF_ENCCL. */
 bbf_status bbf_count_global_base(bbf_graph *g, bbf_counts *out);
 
 /* Per-vertex counts (butterflies containing each vertex; vBBFC semantics),
@@ -165,7 +184,10 @@ bbf_status bbf_count_per_vertex(bbf_graph *g, uint64_t *bal_u, uint64_t *unb_u, 
                                 uint64_t *unb_v, uint32_t flags, bbf_counts *totals);
 
 /* Top-k same-side pairs by balanced count on `side` (BBF_SIDE_U / BBF_SIDE_V).  out: host
- * array of k slots; *n_out receives min(k, #pairs with balanced > 0).  k >= 1. */
+ * array of k slots; *n_out receives min(k, #pairs with balanced > 0).  k >= 1.  With a comm,
+ * each rank finds the top-k of its shard of the pairs (every pair lies in exactly one work item)
+ * and the ranks' lists are all-gathered and merged (the global top-k is within their union).
+ * Errors: BBF_EINVAL (k == 0, side, flags, null pointers), and those of bbf_count_global. */
 bbf_status bbf_count_pairs_topk(bbf_graph *g, int side, uint32_t k, bbf_pair *out,
                                 uint32_t *n_out, uint32_t flags);
 
@@ -187,7 +209,9 @@ bbf_status bbf_topk_vertices(bbf_graph *g, int side, int metric, uint32_t k, uin
  *   n_u, n_v, row_ptr, col, sign, flags (BBF_PTR_DEVICE, BBF_FORCE_*), device, cuda_stream, comm:
  *     as bbf_graph_load_csr; rho in (0, 1]; trials >= 1.
  *   sampled_balanced / sampled_unbalanced: host u64[trials] (nullable) — exact counts of each
- *     sampled graph; estimates: host double[trials] — sampled balanced count * rho^-4.
+ *     sampled graph; estimates: host double[trials] — sampled balanced count * rho^-4.  (The
+ *     mean and spread over trials are the caller's statistics; the Python binding reports them
+ *     next to the per-trial estimates.)
  * Errors: BBF_EINVAL (rho, trials, null estimates), those of bbf_graph_load_csr. */
 bbf_status bbf_estimate_global(uint32_t n_u, uint32_t n_v, const uint64_t *row_ptr, const uint32_t *col,
                                const uint8_t *sign, uint32_t flags, double rho, uint32_t trials,

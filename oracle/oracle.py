@@ -47,6 +47,12 @@ def _load():
         lib.oracle_route_s.argtypes = [u32, u32, P, P, P, P, u64, i32, P, P]
         lib.oracle_route_g_pv.argtypes = [u32, u32, P, P, P, P, u64, i32, P, P, P]
         lib.oracle_route_g_pv.restype = i32
+        lib.oracle_prepare.argtypes = [u32, u32, P, P, P, P]
+        lib.oracle_prepare.restype = P
+        lib.oracle_release.argtypes = [P]
+        lib.oracle_release.restype = None
+        lib.oracle_route_g_pv_h.argtypes = [P, P, u64, i32, P, P, P]
+        lib.oracle_route_g_pv_h.restype = i32
         lib.oracle_bb_base.argtypes = [u32, u32, P, P, P, i32, P]
         lib.oracle_bb_base.restype = i32
         lib.oracle_pairs.argtypes = [u32, u32, P, P, P, i32, i32, P, P, P, P, u64, P]
@@ -127,6 +133,44 @@ def route_g_pv(g, threads=None, starts=None):
         raise OracleError(rc)
     return dict(B=int(out[0]), N=int(out[1]), W_G=int(out[2]), count_s=float(out[3]) * 1e-9,
                 bal_u=bal[:g.n_u], unb_u=unb[:g.n_u], bal_v=bal[g.n_u:], unb_v=unb[g.n_u:])
+
+
+class Prepared:
+    """A graph preprocessed once (Alg. 2 lines 2-3: adjacency built, validated, sorted by
+    priority) for repeated route-G counts over start subsets."""
+
+    def __init__(self, g):
+        lib = _load()
+        self._keep, a = _graph_args(g)
+        rc = C.c_int(0)
+        self.h = lib.oracle_prepare(*a, C.byref(rc))
+        if not self.h:
+            raise OracleError(rc.value)
+        self.n_u, self.n_v = g.n_u, g.n_v
+
+    def route_g_pv(self, starts=None, threads=None):
+        lib = _load()
+        out = np.zeros(4, np.uint64)
+        n = self.n_u + self.n_v
+        bal, unb = np.zeros(n, np.uint64), np.zeros(n, np.uint64)
+        st = None if starts is None else np.ascontiguousarray(starts, dtype=np.uint32)
+        rc = lib.oracle_route_g_pv_h(C.c_void_p(self.h), _ptr(st), C.c_uint64(0 if st is None else st.size),
+                                     _threads(threads), _ptr(out), _ptr(bal), _ptr(unb))
+        if rc:
+            raise OracleError(rc)
+        return dict(B=int(out[0]), N=int(out[1]), W_G=int(out[2]), count_s=float(out[3]) * 1e-9,
+                    bal_u=bal[:self.n_u], unb_u=unb[:self.n_u], bal_v=bal[self.n_u:], unb_v=unb[self.n_u:])
+
+    def close(self):
+        if self.h:
+            _load().oracle_release(C.c_void_p(self.h))
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
 
 
 def bb_base(g, threads=None):

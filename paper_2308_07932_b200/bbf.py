@@ -284,7 +284,9 @@ class Graph:
 def estimate_global(n_u, n_v, row_ptr, col, sign, rho: float, trials: int, seed: int = 0,
                     device: int = 0, stream=None, comm: Comm | None = None, flags: int = 0) -> dict:
     """SBESPAR sparsification estimate (bbf_estimate_global).  Returns dict(sampled_B, sampled_N
-    (uint64 arrays), estimates (float64 array), mean, stddev)."""
+    (uint64 arrays), estimates (float64 array), mean, stddev).  The per-trial estimates come from
+    the library; mean and stddev are summary statistics of those returned values, computed here
+    for the caller (harness statistics, not a step of the method)."""
     dev = _is_torch(row_ptr) and row_ptr.is_cuda
     if dev:
         flags |= BBF_PTR_DEVICE

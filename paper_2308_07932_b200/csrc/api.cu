@@ -10,6 +10,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "bbf_internal.cuh"
 
@@ -34,6 +35,9 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -47,8 +51,12 @@ NcclApi& nccl() {
     api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
     api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
     api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+    api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+    api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+    api.CommAbort = (decltype(api.CommAbort))dlsym(h, "ncclCommAbort");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce;
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.AllGather &&
+             api.CommGetAsyncError && api.CommAbort;
   });
   return api;
 }
@@ -108,11 +116,84 @@ __global__ void k_rank_scores(const unsigned long long* __restrict__ pv, const u
   id[i] = i;
 }
 
-bbf_status allreduce_u64(bbf_graph* g, unsigned long long* dbuf, size_t count) {
-  if (!g->comm || g->comm->nranks <= 1 || !count) return BBF_OK;
-  return nccl_status(nccl().AllReduce(dbuf, dbuf, count, ncclUint64, ncclSum,
-                                      (ncclComm_t)g->comm->nccl, g->stream),
+// a communicator is attached (also with one rank: the collectives then run as single-rank NCCL
+// operations, which is how the N > 1 code path is exercised on a one-GPU box)
+bool multi_rank(const bbf_graph* g) { return g->comm && g->comm->nccl; }
+
+bbf_status allreduce_u64(bbf_graph* g, unsigned long long* dbuf, size_t count, ncclRedOp_t op = ncclSum) {
+  if (!multi_rank(g) || !count) return BBF_OK;
+  return nccl_status(nccl().AllReduce(dbuf, dbuf, count, ncclUint64, op, (ncclComm_t)g->comm->nccl, g->stream),
                      "ncclAllReduce");
+}
+
+// Wait for the graph's stream.  With a communicator the wait polls ncclCommGetAsyncError, so a
+// peer that failed (or a network error) surfaces as BBF_ENCCL instead of a hang; the
+// communicator is then aborted and unusable (bbf_comm_free still releases it).
+bbf_status sync_stream(bbf_graph* g) {
+  if (!multi_rank(g)) {
+    BBF_CUDA(cudaStreamSynchronize(g->stream));
+    return BBF_OK;
+  }
+  while (true) {
+    const cudaError_t e = cudaStreamQuery(g->stream);
+    if (e == cudaSuccess) return BBF_OK;
+    if (e != cudaErrorNotReady) return cuda_status(e, "stream wait");
+    ncclResult_t ar = ncclSuccess;
+    nccl().CommGetAsyncError((ncclComm_t)g->comm->nccl, &ar);
+    if (ar != ncclSuccess && ar != ncclInProgress) {
+      nccl().CommAbort((ncclComm_t)g->comm->nccl);
+      g->comm->nccl = nullptr;
+      return nccl_status(ar, "communicator (asynchronous error)");
+    }
+  }
+}
+
+// Collective completion of a count on every rank: every rank enters the same
+// collectives whatever its local status — the local (B, N) partials are summed, the per-vertex
+// array (per_vertex) is summed, and the ranks' status codes are max-reduced — so a rank that
+// failed locally (an allocation, a table limit) makes every rank return that error instead of
+// leaving the others blocked in the all-reduce.  BN: host (B, N), replaced by the global sums.
+bbf_status finish_collective(bbf_graph* g, bbf_status local, bool per_vertex, unsigned long long* BN) {
+  if (!multi_rank(g)) return local;
+  unsigned long long h[3] = {local == BBF_OK ? BN[0] : 0ull, local == BBF_OK ? BN[1] : 0ull,
+                             (unsigned long long)local};
+  const std::string msg = local == BBF_OK ? std::string() : g_last_error;
+  BBF_CUDA(cudaMemcpyAsync(g->d_acc + 12, h, 24, cudaMemcpyHostToDevice, g->stream));
+  BBF_TRY(allreduce_u64(g, g->d_acc + 12, 2));
+  BBF_TRY(allreduce_u64(g, g->d_acc + 14, 1, ncclMax));
+  if (per_vertex) BBF_TRY(allreduce_u64(g, (unsigned long long*)g->pv, 2ull * g->n));
+  BBF_CUDA(cudaMemcpyAsync(h, g->d_acc + 12, 24, cudaMemcpyDeviceToHost, g->stream));
+  BBF_TRY(sync_stream(g));
+  if (h[2] != BBF_OK) {
+    set_error(local != BBF_OK ? msg : "a peer rank failed (status " + std::to_string(h[2]) + ")");
+    return (bbf_status)h[2];
+  }
+  BN[0] = h[0];
+  BN[1] = h[1];
+  return BBF_OK;
+}
+
+// two CUDA events, destroyed on every return path
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  EventPair() { cudaEventCreate(&a); cudaEventCreate(&b); }
+  ~EventPair() { if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
+  EventPair(const EventPair&) = delete;
+  EventPair& operator=(const EventPair&) = delete;
+};
+
+// the (rank, nranks) shard this process counts: the communicator's, or the BBF_FAKE_WORLD test
+// hook's ("r/N": count rank r's shard of an N-rank job on this single GPU, no collective)
+void shard_of(const bbf_graph* g, int* rank, int* nranks) {
+  *rank = g->comm ? g->comm->rank : 0;
+  *nranks = g->comm ? g->comm->nranks : 1;
+  if (!g->comm && getenv("BBF_FAKE_WORLD")) {
+    int r = 0, N = 1;
+    if (sscanf(getenv("BBF_FAKE_WORLD"), "%d/%d", &r, &N) == 2 && N >= 1 && r >= 0 && r < N) {
+      *rank = r;
+      *nranks = N;
+    }
+  }
 }
 
 bbf_status check_overflow(bbf_graph* g) {
@@ -144,53 +225,37 @@ bool use_dense(bbf_graph* g, uint32_t flags, bool per_vertex) {
   return dense_preferred(g, per_vertex);
 }
 
-bbf_status do_count(bbf_graph* g, bool per_vertex, uint32_t flags, unsigned long long* BN,
-                    float* ms) {
-  BBF_TRY(check_overflow(g));
-  int rank = g->comm ? g->comm->rank : 0, nranks = g->comm ? g->comm->nranks : 1;
-  // test hook: BBF_FAKE_WORLD="r/N" counts only rank r's shard of an N-rank job on this single
-  // GPU (no collective), so tests can check that the shards of every rank sum to the full count
-  if (!g->comm && getenv("BBF_FAKE_WORLD")) {
-    int r = 0, N = 1;
-    if (sscanf(getenv("BBF_FAKE_WORLD"), "%d/%d", &r, &N) == 2 && N >= 1 && r >= 0 && r < N) {
-      rank = r;
-      nranks = N;
-    }
-  }
-  cudaEvent_t a, b;
-  cudaEventCreate(&a);
-  cudaEventCreate(&b);
-  cudaEventRecord(a, g->stream);
+bbf_status do_count_local(bbf_graph* g, bool per_vertex, uint32_t flags, int rank, int nranks,
+                          unsigned long long* BN) {
   if (per_vertex) {
     BBF_CUDA(cudaMemsetAsync(g->pv, 0, 16ull * g->n, g->stream));
     BBF_CUDA(cudaMemsetAsync(g->pe, 0, 8ull * g->n, g->stream));
     BBF_CUDA(cudaMemsetAsync(g->pm, 0, 8ull * g->n, g->stream));
   }
-  bbf_status s = BBF_OK;
-  if (!g->wg_valid) s = ensure_plan_g(g);  // W_G of the graph (and the sparse plan)
-  if (s != BBF_OK) { cudaEventDestroy(a); cudaEventDestroy(b); return s; }
+  if (!g->wg_valid) BBF_TRY(ensure_plan_g(g));  // W_G of the graph (and the sparse plan)
   if (use_dense(g, flags, per_vertex)) {
     if (!dense_supported(g)) {
       set_error("BBF_FORCE_DENSE: graph not supported by the dense int8 path");
       return BBF_EINVAL;
     }
-    s = run_dense(g, per_vertex, rank, nranks, BN);
-  } else {
-    s = ensure_plan_g(g);
-    if (s == BBF_OK) s = run_sparse(g, &g->plan_g, per_vertex, rank, nranks, BN);
+    return run_dense(g, per_vertex, rank, nranks, BN);
   }
-  if (s != BBF_OK) { cudaEventDestroy(a); cudaEventDestroy(b); return s; }
-  if (g->comm && g->comm->nranks > 1) {
-    BBF_CUDA(cudaMemcpyAsync(g->d_acc + 12, BN, 16, cudaMemcpyHostToDevice, g->stream));
-    BBF_TRY(allreduce_u64(g, g->d_acc + 12, 2));
-    if (per_vertex) BBF_TRY(allreduce_u64(g, (unsigned long long*)g->pv, 2ull * g->n));
-    BBF_CUDA(cudaMemcpyAsync(BN, g->d_acc + 12, 16, cudaMemcpyDeviceToHost, g->stream));
-  }
-  cudaEventRecord(b, g->stream);
-  BBF_CUDA(cudaStreamSynchronize(g->stream));
-  cudaEventElapsedTime(ms, a, b);
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
+  BBF_TRY(ensure_plan_g(g));
+  return run_sparse(g, &g->plan_g, per_vertex, rank, nranks, BN);
+}
+
+bbf_status do_count(bbf_graph* g, bool per_vertex, uint32_t flags, unsigned long long* BN,
+                    float* ms) {
+  BBF_TRY(check_overflow(g));  // a property of the graph: identical on every rank
+  int rank, nranks;
+  shard_of(g, &rank, &nranks);
+  EventPair ev;
+  cudaEventRecord(ev.a, g->stream);
+  const bbf_status local = do_count_local(g, per_vertex, flags, rank, nranks, BN);
+  BBF_TRY(finish_collective(g, local, per_vertex, BN));
+  cudaEventRecord(ev.b, g->stream);
+  BBF_TRY(sync_stream(g));
+  cudaEventElapsedTime(ms, ev.a, ev.b);
   return BBF_OK;
 }
 
@@ -454,37 +519,20 @@ bbf_status bbf_count_global_base(bbf_graph* g, bbf_counts* out) {
   if (!g || !out) { set_error("null pointer"); return BBF_EINVAL; }
   BBF_CUDA(cudaSetDevice(g->device));
   BBF_TRY(check_overflow(g));
-  BBF_TRY(ensure_plan_g(g));
-  int rank = g->comm ? g->comm->rank : 0, nranks = g->comm ? g->comm->nranks : 1;
-  if (!g->comm && getenv("BBF_FAKE_WORLD")) {  // test hook, as in do_count: one rank's shard only
-    int r = 0, N = 1;
-    if (sscanf(getenv("BBF_FAKE_WORLD"), "%d/%d", &r, &N) == 2 && N >= 1 && r >= 0 && r < N) {
-      rank = r;
-      nranks = N;
-    }
-  }
-  cudaEvent_t a, b;
-  cudaEventCreate(&a);
-  cudaEventCreate(&b);
-  cudaEventRecord(a, g->stream);
+  int rank, nranks;
+  shard_of(g, &rank, &nranks);
+  EventPair ev;
+  cudaEventRecord(ev.a, g->stream);
   unsigned long long BN[2] = {0, 0};
-  bbf_status s = run_base(g, &g->plan_g, rank, nranks, BN);
-  if (s == BBF_OK && g->comm && g->comm->nranks > 1) {
-    cudaError_t e = cudaMemcpyAsync(g->d_acc + 12, BN, 16, cudaMemcpyHostToDevice, g->stream);
-    if (e != cudaSuccess) s = cuda_status(e, "cudaMemcpyAsync");
-    if (s == BBF_OK) s = allreduce_u64(g, g->d_acc + 12, 2);
-    if (s == BBF_OK) {
-      e = cudaMemcpyAsync(BN, g->d_acc + 12, 16, cudaMemcpyDeviceToHost, g->stream);
-      if (e != cudaSuccess) s = cuda_status(e, "cudaMemcpyAsync");
-    }
-  }
-  cudaEventRecord(b, g->stream);
-  cudaStreamSynchronize(g->stream);
+  // every rank enters the collective whatever its local status (a table-limit or allocation
+  // failure on one rank is returned by all of them, none is left blocked in the all-reduce)
+  bbf_status local = ensure_plan_g(g);
+  if (local == BBF_OK) local = run_base(g, &g->plan_g, rank, nranks, BN);
+  BBF_TRY(finish_collective(g, local, false, BN));
+  cudaEventRecord(ev.b, g->stream);
+  BBF_TRY(sync_stream(g));
   float ms = 0;
-  cudaEventElapsedTime(&ms, a, b);
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
-  if (s != BBF_OK) return s;
+  cudaEventElapsedTime(&ms, ev.a, ev.b);
   unsigned long long wg = 0;
   BBF_TRY(wedges_g(g, &wg));
   out->balanced = BN[0];
@@ -569,8 +617,59 @@ bbf_status bbf_count_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* ou
   if (flags & ~(uint32_t)(BBF_FORCE_SPARSE)) { set_error("unsupported flags for topk"); return BBF_EINVAL; }
   BBF_CUDA(cudaSetDevice(g->device));
   BBF_TRY(check_overflow(g));
-  BBF_TRY(ensure_adj(g));
-  return run_pairs_topk(g, side, k, out, n_out);
+  int rank, nranks;
+  shard_of(g, &rank, &nranks);
+  *n_out = 0;
+  bbf_status local = ensure_adj(g);
+  if (local == BBF_OK) local = run_pairs_topk(g, side, k, out, n_out, rank, nranks);
+  if (!multi_rank(g)) return local;
+  // S12: all-gather of every rank's local top-k (k slots of (balanced, unbalanced, a << 32 | b),
+  // empty slots zero, plus the rank's status) and a deterministic merge, identical on all ranks
+  const int N = g->comm->nranks;
+  const size_t rec = 3ull * k + 1;
+  std::vector<unsigned long long> mine(rec, 0ull), all(rec * N, 0ull);
+  if (local == BBF_OK)
+    for (uint32_t i = 0; i < *n_out; ++i) {
+      mine[3 * i] = out[i].balanced;
+      mine[3 * i + 1] = out[i].unbalanced;
+      mine[3 * i + 2] = ((unsigned long long)out[i].a << 32) | out[i].b;
+    }
+  mine[3ull * k] = (unsigned long long)local;
+  unsigned long long* d = nullptr;
+  BBF_CUDA(dmalloc(&d, 8ull * rec * (N + 1), g->stream));
+  BBF_CUDA(cudaMemcpyAsync(d, mine.data(), 8ull * rec, cudaMemcpyHostToDevice, g->stream));
+  bbf_status s = nccl_status(nccl().AllGather(d, d + rec, rec, ncclUint64, (ncclComm_t)g->comm->nccl, g->stream),
+                             "ncclAllGather");
+  if (s == BBF_OK) {
+    cudaError_t e = cudaMemcpyAsync(all.data(), d + rec, 8ull * rec * N, cudaMemcpyDeviceToHost, g->stream);
+    if (e != cudaSuccess) s = cuda_status(e, "cudaMemcpyAsync");
+  }
+  if (s == BBF_OK) s = sync_stream(g);
+  dfree(d, g->stream);
+  if (s != BBF_OK) return s;
+  unsigned long long worst = 0;
+  std::vector<bbf_pair> cand;
+  for (int r = 0; r < N; ++r) {
+    const unsigned long long* q = all.data() + rec * r;
+    worst = std::max(worst, q[3ull * k]);
+    for (uint32_t i = 0; i < k; ++i)
+      if (q[3 * i])  // balanced > 0: a listed pair (reading R11 lists only those)
+        cand.push_back(bbf_pair{(uint32_t)(q[3 * i + 2] >> 32), (uint32_t)(q[3 * i + 2] & 0xffffffffu), q[3 * i],
+                                q[3 * i + 1]});
+  }
+  if (worst != BBF_OK) {
+    if (local == BBF_OK) set_error("a peer rank failed (status " + std::to_string(worst) + ")");
+    *n_out = 0;
+    return (bbf_status)worst;
+  }
+  std::sort(cand.begin(), cand.end(), [](const bbf_pair& x, const bbf_pair& y) {
+    if (x.balanced != y.balanced) return x.balanced > y.balanced;
+    if (x.a != y.a) return x.a < y.a;
+    return x.b < y.b;
+  });
+  *n_out = (uint32_t)std::min<size_t>(k, cand.size());
+  for (uint32_t i = 0; i < *n_out; ++i) out[i] = cand[i];
+  return BBF_OK;
 }
 
 bbf_status bbf_topk_vertices(bbf_graph* g, int side, int metric, uint32_t k, uint32_t* ids,

@@ -202,9 +202,11 @@ bbf_status run_base(bbf_graph* g, Plan* p, int rank, int nranks, unsigned long l
   BBF_CUDA(rb_sync(st));
   if (max_work == 0) { dfree(d, st); return BBF_OK; }
   const uint64_t budget = 8ull << 30;  // scratch bytes
-  if (max_work > budget) {
+  // the per-start list offsets (pos, cnt, the CTA scan) are 32-bit: a start's wedges must stay
+  // below 2^32 as well as within the scratch
+  if (max_work > budget || max_work >= (1ull << 32)) {
     dfree(d, st);
-    set_error("BB-Base: a start has more wedges than the 8 GiB list scratch holds");
+    set_error("BB-Base: a start has more wedges than the list scratch holds (8 GiB, 2^32 - 1 entries)");
     return BBF_ENOMEM;
   }
   const uint64_t per_cta = (max_work + 15) & ~15ull;

@@ -330,6 +330,8 @@ cudaError_t dmalloc_nowait(T** out, size_t bytes, cudaStream_t st) {  // see mem
 }
 bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* col,
                        const uint8_t* sign, bool device_ptrs);
+bbf_status validate_csr(const uint64_t* d_rp, uint32_t n_u, const uint32_t* d_col, const uint8_t* d_sg,
+                        uint64_t nnz, uint32_t n_v, cudaStream_t st);
 bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, const uint8_t* d_sg);
 bbf_status ensure_adj(bbf_graph* g);
 bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col,
@@ -343,7 +345,8 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
                            unsigned long long* host_BN, unsigned long long* cb, unsigned long long* cn,
                            unsigned long long* cid, unsigned long long cap, unsigned long long* n_cand,
                            unsigned long long tau);
-bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uint32_t* n_out);
+bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uint32_t* n_out, int rank,
+                          int nranks);
 bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks,
                      unsigned long long* host_BN);
 // Alg. 1 BB-Base (base.cu): explicit pair checks, the paper's baseline

@@ -1389,9 +1389,13 @@ __global__ void k_gather_u64(const unsigned long long* __restrict__ src, const u
 
 // S11: top-k same-side pairs by balanced count (route S on `side`, every unordered pair once).
 // Order: balanced desc, then smaller input id asc, then larger input id asc (reading R11) —
-// two stable radix sorts (ids ascending, then balanced descending).  Every rank computes the
-// full candidate set (top-k is requested only on small graphs).
-bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uint32_t* n_out) {
+// two stable radix sorts (ids ascending, then balanced descending).  With nranks > 1 this rank
+// counts only its shard of the work items (item i on rank i mod nranks; every pair is produced by
+// exactly one item: its start's unit that holds the end's window) and returns the shard's own
+// top-k; api.cu all-gathers the shards' lists and merges them (the global top-k is a subset of
+// the union of the shards' top-k lists).
+bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uint32_t* n_out, int rank,
+                          int nranks) {
   cudaStream_t st = g->stream;
   Plan* p = &g->plan_s[side];
   if (!p->valid) BBF_TRY(make_plan(g, 1 + side, p));
@@ -1410,7 +1414,7 @@ bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uin
   BBF_CUDA(dmalloc(&cid, 8 * cap, st));
   for (int it = 0;; ++it) {
     unsigned long long BN[2];
-    BBF_TRY(run_sparse_impl(g, p, false, true, 0, 1, BN, cb, cn, cid, cap, &ncand, tau));
+    BBF_TRY(run_sparse_impl(g, p, false, true, rank, nranks, BN, cb, cn, cid, cap, &ncand, tau));
     if (ncand <= cap && (ncand >= k || tau == 1)) break;  // complete candidate set
     if (it >= 64) { set_error("top-k threshold search did not converge"); return BBF_ENOMEM; }
     if (ncand > cap) {
@@ -1438,7 +1442,7 @@ bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uin
       BBF_CUDA(dmalloc(&cn, 8 * cap, st));
       BBF_CUDA(dmalloc(&cid, 8 * cap, st));
       tau = lo;
-      BBF_TRY(run_sparse_impl(g, p, false, true, 0, 1, BN, cb, cn, cid, cap, &ncand, tau));
+      BBF_TRY(run_sparse_impl(g, p, false, true, rank, nranks, BN, cb, cn, cid, cap, &ncand, tau));
       break;
     }
   }

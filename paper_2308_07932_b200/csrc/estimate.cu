@@ -86,7 +86,8 @@ extern "C" bbf_status bbf_estimate_global(uint32_t n_u, uint32_t n_v, const uint
     nnz = row_ptr[n_u];
   }
   if (nnz >= (1ull << 31)) { set_error("nnz >= 2^31"); return BBF_ERANGE; }
-  // device copies of the input (validation happens in bbf_graph_load_csr of each sample)
+  // device copies of the input, validated once (S1) before the sampling kernels read them
+  // (each sample is validated again by its own load)
   uint64_t *d_rp = nullptr, *n_rp = nullptr;
   uint32_t *d_col = nullptr, *keep = nullptr, *pos = nullptr, *n_col = nullptr;
   uint8_t *d_sg = nullptr, *n_sg = nullptr;
@@ -116,6 +117,7 @@ extern "C" bbf_status bbf_estimate_global(uint32_t n_u, uint32_t n_v, const uint
     e = dmalloc(&tmp, tb + 16, st);
   }
   if (e != cudaSuccess) fail(e, "estimate setup");
+  if (s == BBF_OK) s = validate_csr(rp, n_u, cl, sg, nnz, n_v, st);
   const bool all = rho >= 1.0;
   const uint64_t thr = all ? ~0ull : (uint64_t)(rho * 18446744073709551616.0);  // floor(rho * 2^64)
   const double scale = 1.0 / (rho * rho * rho * rho);

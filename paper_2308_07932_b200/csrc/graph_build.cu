@@ -383,6 +383,25 @@ __global__ void k_wg_sum(const uint32_t* __restrict__ mcnt, const uint64_t* __re
 // S1-S3 and the row offsets / zones; then either the rank-space adjacency (S4, sparse path) or,
 // for a graph the dispatch rule sends to the dense path, the dense operands (adjacency deferred
 // until a sparse call needs it; the input CSR is then kept on the device).
+// S1 validation of a device CSR on its own (bbf_estimate_global validates its input once before
+// any sampling kernel reads it): the same checks and status codes as the load.
+bbf_status validate_csr(const uint64_t* d_rp, uint32_t n_u, const uint32_t* d_col, const uint8_t* d_sg,
+                        uint64_t nnz, uint32_t n_v, cudaStream_t st) {
+  uint32_t* d_err;
+  BBF_CUDA(dmalloc(&d_err, 4, st));
+  BBF_CUDA(cudaMemsetAsync(d_err, 0, 4, st));
+  k_validate_rows<<<grid_for(n_u + 1, 256, 1u << 30), 256, 0, st>>>(d_rp, n_u, d_err);
+  if (nnz) k_validate_edges<<<grid_for(nnz, 256), 256, 0, st>>>(d_col, d_sg, nnz, n_v, d_err);
+  uint32_t h_err = 0;
+  BBF_CUDA(rb_add(&h_err, d_err, 4, st));
+  BBF_CUDA(rb_sync(st));
+  dfree(d_err, st);
+  if (h_err & kErrRowPtr) { set_error("row_ptr[0] != 0 or row_ptr not non-decreasing"); return BBF_ERANGE; }
+  if (h_err & kErrCol) { set_error("col index >= n_v"); return BBF_ERANGE; }
+  if (h_err & kErrSign) { set_error("sign byte not in {0,1}"); return BBF_EINVAL; }
+  return BBF_OK;
+}
+
 bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* col,
                        const uint8_t* sign, bool device_ptrs) {
   cudaStream_t st = g->stream;

@@ -1,19 +1,19 @@
 """Multi-GPU plumbing over torch.distributed (one process per GPU).
 
-The library shards the work itself (unit i of the work plan goes to rank i mod N, see
-DESIGN.md §Multi-GPU) and all-reduces the counts with NCCL; this module only bootstraps the
-NCCL communicator (the 128-byte ncclUniqueId travels over the torch process group) and
-provides the max-over-ranks timing reduction.  Works with the nccl backend (CUDA tensors) and
-with gloo (CPU tensors, used by the CPU tests)."""
+The library shards the work itself (work item i of the plan goes to rank i mod N, DESIGN.md
+§Multi-GPU) and combines the counts with NCCL collectives of its own communicator; this module
+only bootstraps that communicator (the 128-byte ncclUniqueId travels over the torch process
+group) and provides the max-over-ranks timing reduction and an exact uint64 sum the harness uses.
+Works with the nccl backend (CUDA tensors) and with gloo (CPU tensors, the CPU tests)."""
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
 
 def _dev(group=None):
-    backend = dist.get_backend(group)
-    if backend == "nccl":
+    if dist.get_backend(group) == "nccl":
         return torch.device("cuda", torch.cuda.current_device())
     return torch.device("cpu")
 
@@ -29,7 +29,7 @@ def broadcast_unique_id(uid: bytes | None, src: int = 0, group=None) -> bytes:
 
 
 def make_comm(device: int, group=None):
-    """NCCL communicator of the library for this rank (collective over the group)."""
+    """The library's NCCL communicator for this rank (collective over the group)."""
     from . import bbf
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     uid = bbf.nccl_unique_id() if rank == 0 else None
@@ -43,14 +43,13 @@ def max_over_ranks(x: float, group=None) -> float:
     return float(t.item())
 
 
-def sum_over_ranks_u64(vals, group=None):
-    """Exact integer sum across ranks (int64 lanes; counts < 2^63 here)."""
-    t = torch.tensor([int(v) for v in vals], dtype=torch.int64, device=_dev(group))
-    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    return [int(v) for v in t.cpu().tolist()]
-
-
-def shard_owner(item: int, nranks: int) -> int:
-    """Host mirror of the device sharding rule: work item i (T3 unit or T1 start, in plan
-    order) is processed by rank i mod nranks."""
-    return item % nranks
+def sum_over_ranks_u64(vals, group=None) -> np.ndarray:
+    """Exact uint64 sum across ranks (mod 2^64, like the library's ncclUint64 all-reduce): the
+    values travel as 32-bit halves in int64 lanes, whose sums cannot overflow for < 2^31 ranks."""
+    a = np.ascontiguousarray(np.asarray(vals, dtype=np.uint64))
+    lo = torch.from_numpy((a & np.uint64(0xffffffff)).astype(np.int64)).to(_dev(group))
+    hi = torch.from_numpy((a >> np.uint64(32)).astype(np.int64)).to(_dev(group))
+    dist.all_reduce(lo, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(hi, op=dist.ReduceOp.SUM, group=group)
+    lo, hi = lo.cpu().numpy().astype(np.uint64), hi.cpu().numpy().astype(np.uint64)
+    return lo + (hi << np.uint64(32))

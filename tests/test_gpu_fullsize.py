@@ -103,3 +103,57 @@ def test_fake_world_shards_on_hub_graphs(bbf, monkeypatch, name, world):
     assert (acc[0], acc[1]) == (want["B"], want["N"])
     assert all(0 < p < want["B"] for p in parts), parts
     assert_equal_arrays([a.astype(np.uint64) for a in acc[2:]], want, f"{name} world {world}")
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fake_world_topk_shards_merge(bbf, monkeypatch, world):
+    """S12 top-k: each rank's shard returns its local top-k; the merged lists (what the library's
+    ncclAllGather + merge does across ranks) equal the oracle's global top-k."""
+    g = G.config2()
+    lists = []
+    for r in range(world):
+        monkeypatch.setenv("BBF_FAKE_WORLD", f"{r}/{world}")
+        with bbf.Graph.from_synth(g) as h:
+            lists.append(h.count_pairs_topk(100, side=0))
+    monkeypatch.delenv("BBF_FAKE_WORLD")
+    merged = sorted([t for lst in lists for t in lst], key=lambda t: (-t[2], t[0], t[1]))[:100]
+    assert merged == O.topk_pairs(g, 100, side=0, threads=THREADS)
+    assert all(len(lst) > 0 for lst in lists)
+
+
+def test_single_rank_nccl_communicator(bbf):
+    """The collective path with a real NCCL communicator of one rank (bbf_comm_init, the u64
+    all-reduces with the status max-reduce, the top-k all-gather, the async-error polling wait):
+    counts equal the oracle's."""
+    g = G.config2()
+    comm = bbf.Comm(bbf.nccl_unique_id(), 1, 0, 0)
+    try:
+        with bbf.Graph.from_synth(g, comm=comm) as h:
+            c = h.count_global()
+            tot, bu, nu, bv, nv = h.count_per_vertex()
+            top = h.count_pairs_topk(100, side=1)
+            base = h.count_global_base()
+    finally:
+        comm.free()
+    want = O.route_g_pv(g, threads=THREADS)
+    assert (c["balanced"], c["unbalanced"], c["wedges_G"]) == (want["B"], want["N"], want["W_G"])
+    assert (base["balanced"], base["unbalanced"]) == (want["B"], want["N"])
+    assert_equal_arrays((bu, nu, bv, nv), want, "comm1")
+    assert top == O.topk_pairs(g, 100, side=1, threads=THREADS)
+
+
+def test_estimate_rejects_malformed_input_before_sampling(bbf):
+    """bbf_estimate_global validates its input CSR (S1) before the sampling kernels read it: a
+    row_ptr entry beyond nnz, a column out of range and a bad sign byte return the load's codes."""
+    rp = np.array([0, 5, 2], np.uint64)  # not monotone, and rp[1] > nnz
+    col = np.array([0, 1], np.uint32)
+    sg = np.array([1, 1], np.uint8)
+    with pytest.raises(bbf.BBFError) as e:
+        bbf.estimate_global(2, 2, rp, col, sg, 0.5, 2)
+    assert e.value.name == "BBF_ERANGE"
+    with pytest.raises(bbf.BBFError) as e:
+        bbf.estimate_global(2, 2, np.array([0, 1, 2], np.uint64), np.array([0, 7], np.uint32), sg, 0.5, 2)
+    assert e.value.name == "BBF_ERANGE"
+    with pytest.raises(bbf.BBFError) as e:
+        bbf.estimate_global(2, 2, np.array([0, 1, 2], np.uint64), col, np.array([1, 2], np.uint8), 0.5, 2)
+    assert e.value.name == "BBF_EINVAL"

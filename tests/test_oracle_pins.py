@@ -417,6 +417,11 @@ def test_route_g_pv_start_partition_additive():
     full = O.route_g_pv(g)
     lab = np.random.default_rng(2).integers(0, 4, size=g.n_u + g.n_v)
     parts = [O.route_g_pv(g, starts=np.nonzero(lab == k)[0], threads=2) for k in range(4)]
+    with O.Prepared(g) as h:  # the prepared-graph form used by bench.py's reference arm
+        parts2 = [h.route_g_pv(starts=np.nonzero(lab == k)[0], threads=3) for k in range(4)]
+    for p, q in zip(parts, parts2):
+        assert (p["B"], p["N"], p["W_G"]) == (q["B"], q["N"], q["W_G"])
+        assert np.array_equal(p["bal_v"], q["bal_v"]) and np.array_equal(p["unb_u"], q["unb_u"])
     for key in ("B", "N", "W_G"):
         assert sum(p[key] for p in parts) == full[key]
     for key in ("bal_u", "unb_u", "bal_v", "unb_v"):
