@@ -157,7 +157,11 @@ __device__ __forceinline__ void mid_red(const EngineArgs& a, uint32_t rm, uint32
 // per lane per step), so every lane is busy whatever the record lengths.
 constexpr uint32_t kRecMax = 1024;
 #ifdef BBF_T3_PROF
-__device__ unsigned long long g_prof_cnt[4];  // nonzero counter words, contributing fields
+// record-shape and window statistics (profiling build): [0] record entries, [1..3] aligned
+// 64/32/16-entry blocks the records touch, [4] records shorter than 8 entries, [5] entries of
+// records shorter than 64, [6] wedges in dense windows, [7] wedges in bitmap windows, [8] touched
+// words in the epilogue, [9] contributing fields, [10] records
+__device__ unsigned long long g_prof_cnt[16];
 #define T3_COUNT(i, v) atomicAdd(&g_prof_cnt[i], (unsigned long long)(v))
 __device__ unsigned long long g_prof_t[3] = {~0ull, ~0ull, 0ull};  // min CTA start, min CTA end, max CTA end (globaltimer ns)
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -573,6 +577,17 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             const uint32_t slot = atomicAdd(&sh_cnt[run.y], 1u);
             R[(size_t)run.y * RS + slot] = Rec{p, min(kRecMax, re - p), o_wv, 0u};
           }
+#ifdef BBF_T3_PROF
+          if (re > rs) {
+            T3_COUNT(0, re - rs);
+            T3_COUNT(1, (re + 63) / 64 - rs / 64);
+            T3_COUNT(2, (re + 31) / 32 - rs / 32);
+            T3_COUNT(3, (re + 15) / 16 - rs / 16);
+            if (re - rs < 8) T3_COUNT(4, 1);
+            if (re - rs < 64) T3_COUNT(5, re - rs);
+            T3_COUNT(10, 1);
+          }
+#endif
         }
       }
     }
@@ -595,6 +610,9 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       const uint32_t nwk = min(kWin, Z.WB[5] - word0);
       const bool dense = sh_wc[k] * a.dense_div >= nwk;
       if (tid < 4) sh_c[tid] = 0;
+#ifdef BBF_T3_PROF
+      if (tid == 0) T3_COUNT(dense ? 6 : 7, sh_wc[k]);
+#endif
       if (tid == 0) {
         atomicAdd(&a.acc[6], (unsigned long long)nrec);
         atomicAdd(&a.acc[7], 1ull);
@@ -1352,6 +1370,14 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     cudaMemcpyFromSymbol(t, g_prof_t, sizeof(t));
     fprintf(stderr, "[bbf] t3 CTA ends: first %.3f ms, last %.3f ms after the first start\n", (t[1] - t[0]) * 1e-6,
             (t[2] - t[0]) * 1e-6);
+    unsigned long long pc[16];
+    cudaMemcpyFromSymbol(pc, g_prof_cnt, sizeof(pc));
+    fprintf(stderr, "[bbf] t3 records %llu entries %llu blocks64 %llu (fill %.3f) blocks32 %llu (fill %.3f) blocks16 %llu "
+            "(fill %.3f) short<8 %llu, entries in records<64 %llu; wedges dense %llu bitmap %llu\n",
+            pc[10], pc[0], pc[1], pc[0] / (64.0 * pc[1] + 1e-9), pc[2], pc[0] / (32.0 * pc[2] + 1e-9), pc[3],
+            pc[0] / (16.0 * pc[3] + 1e-9), pc[4], pc[5], pc[6], pc[7]);
+    const unsigned long long z16[16] = {};
+    cudaMemcpyToSymbol(g_prof_cnt, z16, sizeof(z16));
     const unsigned long long init[3] = {~0ull, ~0ull, 0ull};
     cudaMemcpyToSymbol(g_prof_t, init, sizeof(init));
   }
