@@ -470,6 +470,75 @@ __device__ __forceinline__ void t3_chunk(const uint32_t (&ev)[kCE], uint32_t vm,
   }
 }
 
+// ---------------------------------------------------------------------------- long records
+// A record of at least kLongMin entries (compact encoding) is walked by ONE warp: steps of
+// 256 entries, lane L holding entries 4L..4L+3 and 128+4L..131+4L of the step (two LDG.128, the
+// warp's loads cover 1 KB contiguous), so there is no owner lookup, interior steps need no entry
+// masks (a warp-uniform test), and pass 2 sums the record's shares in lane registers and reduces
+// them once per record.  Records shorter than kLongMin go through the flattened batches.
+#ifndef BBF_T3_LONG_MIN
+#define BBF_T3_LONG_MIN 256
+#endif
+constexpr uint32_t kLongMin = BBF_T3_LONG_MIN;
+
+// 1 << (x mod 32) in one funnel shift (no separate "& 31")
+__device__ __forceinline__ uint32_t bit_of(uint32_t x) {
+  uint32_t r;
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(0u), "r"(1u), "r"(x));
+  return r;
+}
+// v >> (x mod 32)
+__device__ __forceinline__ uint32_t shr_wrap(uint32_t v, uint32_t x) {
+  uint32_t r;
+  asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "r"(0u), "r"(x));
+  return r;
+}
+
+// MODE 0: pass 1, dense window; 1: pass 1 with the touched-word bitmap; 2: pass 2.
+template <int MODE>
+__device__ __forceinline__ void t3_long_entry(uint32_t ev, uint32_t on, uint32_t cbase, uint32_t bmbase,
+                                              uint32_t word0, uint32_t shamt, uint32_t oshamt, uint32_t& own,
+                                              uint32_t& oth) {
+  if (MODE == 2) {
+    const uint32_t v = sh_load_if(cbase + (ev & kCpAddrMask), on);
+    const uint32_t h = 2u << (ev & 3u);
+    own += zext(shr_wrap(v, ev >> shamt), h);
+    oth += zext(shr_wrap(v, ev >> oshamt), h);
+  } else {
+    sh_red_add_if(cbase + (ev & kCpAddrMask), bit_of(ev >> shamt), on);
+    if (MODE == 1) {
+      const uint32_t g = cp_word(ev) - word0;
+      sh_red_or_if(bmbase + 4u * (g >> 5), bit_of(g), on);
+    }
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void t3_long(const uint32_t* __restrict__ adjc, const Rec& rc, uint32_t cbase,
+                                        uint32_t bmbase, uint32_t word0, int lane, uint32_t& own,
+                                        uint32_t& oth) {
+  const uint32_t shamt = 22u + 5u * (rc.wv >> 31), oshamt = 49u - shamt;
+  const uint32_t p = rc.p, e_end = rc.p + rc.len;
+#pragma unroll 1
+  for (uint32_t b = p & ~3u; b < e_end; b += 256) {
+    const uint32_t e0 = b + 4u * lane, e1 = e0 + 128u;
+    uint4 q0 = make_uint4(0u, 0u, 0u, 0u), q1 = make_uint4(0u, 0u, 0u, 0u);
+    if (e0 < e_end) q0 = *reinterpret_cast<const uint4*>(adjc + e0);
+    if (e1 < e_end) q1 = *reinterpret_cast<const uint4*>(adjc + e1);
+    const uint32_t ev[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    if (b >= p && b + 256u <= e_end) {  // interior step (warp-uniform): every entry is the record's
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t3_long_entry<MODE>(ev[j], 1u, cbase, bmbase, word0, shamt, oshamt, own, oth);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t e = (j < 4 ? e0 : e1) + (uint32_t)(j & 3);
+        t3_long_entry<MODE>(ev[j], (e >= p) & (e < e_end), cbase, bmbase, word0, shamt, oshamt, own, oth);
+      }
+    }
+  }
+}
+
 template <bool PV, bool PAIRS, int ENC>
 __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) {
   constexpr bool WIDE = ENC == kEncWide, CP = ENC == kEncCompact;
@@ -478,6 +547,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
   uint32_t* bm = smem + kWin;             // kBm
   uint32_t* sh_cnt = bm + kBm;            // kMaxWin record counts
   uint32_t* sh_wc = sh_cnt + kMaxWin;     // kMaxWin wedge counts
+  uint32_t* sh_cntl = sh_wc + kMaxWin;    // kMaxWin long-record counts (stored from the slot end)
   __shared__ uint32_t sh_unit, sh_c[4];
   __shared__ uint32_t sh_acc[kT3Warps][2][32];  // per-warp pass-2 accumulators of a batch
   __shared__ Zones sh_z;                        // the current unit's end-side zone table
@@ -493,7 +563,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
   if (threadIdx.x < 4) sh_dbg[threadIdx.x] = 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  for (uint32_t i = tid; i < kWin + kBm + 2 * kMaxWin; i += kT3Threads) smem[i] = 0;
+  for (uint32_t i = tid; i < kWin + kBm + 3 * kMaxWin; i += kT3Threads) smem[i] = 0;
   const size_t RS = a.rec_stride;
   Rec* R = reinterpret_cast<Rec*>(a.scratch) + (size_t)blockIdx.x * RS * a.kwin_cap;
   unsigned long long totB = 0, totN = 0;
@@ -574,10 +644,16 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           const uint32_t re = (r + 1 < a.nruns) ? min(a.runs[r + 1].x, o_en) : o_en;
           if (re > rs) atomicAdd(&sh_wc[run.y], re - rs);
           for (uint32_t p = rs; p < re; p += kRecMax) {
-            const uint32_t slot = atomicAdd(&sh_cnt[run.y], 1u);
-            R[(size_t)run.y * RS + slot] = Rec{p, min(kRecMax, re - p), o_wv, 0u};
+            const uint32_t len = min(kRecMax, re - p);
+            if (CP && len >= kLongMin) {
+              const uint32_t slot = atomicAdd(&sh_cntl[run.y], 1u);
+              R[(size_t)run.y * RS + (RS - 1 - slot)] = Rec{p, len, o_wv, 0u};
+            } else {
+              const uint32_t slot = atomicAdd(&sh_cnt[run.y], 1u);
+              R[(size_t)run.y * RS + slot] = Rec{p, len, o_wv, 0u};
+            }
           }
-#ifdef BBF_T3_PROF
+#ifdef BBF_T3_RECSTAT
           if (re > rs) {
             T3_COUNT(0, re - rs);
             T3_COUNT(1, (re + 63) / 64 - rs / 64);
@@ -586,6 +662,10 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             if (re - rs < 8) T3_COUNT(4, 1);
             if (re - rs < 64) T3_COUNT(5, re - rs);
             T3_COUNT(10, 1);
+            {  // entries by run length: [0] <8 [1] <32 [2] <128 [3] <512 [4] >= 512 (runs, before kRecMax splits)
+              const uint32_t L = re - rs;
+              T3_COUNT(11 + (L < 8 ? 0 : L < 32 ? 1 : L < 128 ? 2 : L < 512 ? 3 : 4), L);
+            }
           }
 #endif
         }
@@ -596,8 +676,8 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
     unsigned long long xB = 0, xN = 0;
 
     for (uint32_t k = 0; k < K; ++k) {
-      const uint32_t nrec = sh_cnt[k];
-      if (nrec == 0) continue;
+      const uint32_t nrec = sh_cnt[k], nlong = sh_cntl[k];
+      if (nrec + nlong == 0) continue;
       const uint32_t word0 = k * kWin;
       const uint32_t cbase = (uint32_t)__cvta_generic_to_shared(ctr) - 4u * word0;
       const Rec* rw = R + (size_t)k * RS;
@@ -610,13 +690,13 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       const uint32_t nwk = min(kWin, Z.WB[5] - word0);
       const bool dense = sh_wc[k] * a.dense_div >= nwk;
       if (tid < 4) sh_c[tid] = 0;
-#ifdef BBF_T3_PROF
+#ifdef BBF_T3_RECSTAT
       if (tid == 0) T3_COUNT(dense ? 6 : 7, sh_wc[k]);
 #endif
       if (tid == 0) {
         atomicAdd(&a.acc[6], (unsigned long long)nrec);
         atomicAdd(&a.acc[7], 1ull);
-        if (nrec < 64) sh_dbg[2]++;
+        if (nrec + nlong < 64) sh_dbg[2]++;
         if (dense) sh_dbg[3]++;
       }
       __syncthreads();
@@ -624,6 +704,27 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       // ---------------- pass 1 (Alg. 2 lines 9-14) and pass 2 (per-vertex shares)
 #pragma unroll 1
       for (int pass = 0; pass < (PV ? 2 : 1); ++pass) {
+        if (CP && nlong) {  // long records first, one warp each (sh_c[2 + pass] is the cursor)
+          const uint32_t bmbase = (uint32_t)__cvta_generic_to_shared(bm);
+          while (true) {
+            uint32_t r = 0;
+            if (lane == 0) r = atomicAdd(&sh_c[2 + pass], 1u);
+            r = __shfl_sync(0xffffffffu, r, 0);
+            if (r >= nlong) break;
+            const Rec rl = rw[RS - 1 - r];
+            uint32_t own = 0, oth = 0;
+            if (pass == 1) t3_long<2>(adjc, rl, cbase, bmbase, word0, lane, own, oth);
+            else if (dense) t3_long<0>(adjc, rl, cbase, bmbase, word0, lane, own, oth);
+            else t3_long<1>(adjc, rl, cbase, bmbase, word0, lane, own, oth);
+            if (pass == 1) {
+              // the record's own-class sum and other-class sum (each < 2^26: <= 1024 entries of
+              // 16-bit fields), minus one per wedge for the own class (Lemma 2 shares)
+              own = __reduce_add_sync(0xffffffffu, own);
+              oth = __reduce_add_sync(0xffffffffu, oth);
+              if (lane == 0 && ((own - rl.len) | oth)) mid_red(a, rmv, rl.wv & kMask, ob + (rl.wv & kMask), own - rl.len, oth);
+            }
+          }
+        }
         // batches of bsz records; the next batch's records are loaded while this one is
         // processed (their global-load latency was the kernel's top stall)
         // guided batches: up to bsz records, shrinking near the end of the window so the warps
@@ -796,7 +897,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       __syncthreads();
       T3_MARK(4);
     }
-    for (uint32_t k = tid; k < K; k += kT3Threads) { sh_cnt[k] = 0; sh_wc[k] = 0; }
+    for (uint32_t k = tid; k < K; k += kT3Threads) { sh_cnt[k] = 0; sh_wc[k] = 0; sh_cntl[k] = 0; }
     // unit totals -> start vertex
     totB += xB;
     totN += xN;
@@ -1200,7 +1301,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
 template <bool PV, bool PAIRS, int ENC>
 cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, Plan* p,
                           cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2) {
-  const size_t smem3 = sizeof(uint32_t) * (kWin + kBm + 2 * kMaxWin);
+  const size_t smem3 = sizeof(uint32_t) * (kWin + kBm + 3 * kMaxWin);
   const size_t smem1 = sizeof(uint32_t) * 32 * (2 * 256 + 3 * 32 + 64);
   const size_t smem1b = sizeof(uint32_t) * 12 * (2 * 1024 + 3 * 32 + 64);
   cudaError_t err;
@@ -1376,6 +1477,9 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
             "(fill %.3f) short<8 %llu, entries in records<64 %llu; wedges dense %llu bitmap %llu\n",
             pc[10], pc[0], pc[1], pc[0] / (64.0 * pc[1] + 1e-9), pc[2], pc[0] / (32.0 * pc[2] + 1e-9), pc[3],
             pc[0] / (16.0 * pc[3] + 1e-9), pc[4], pc[5], pc[6], pc[7]);
+    fprintf(stderr, "[bbf] t3 entries by run length: <8 %.3f <32 %.3f <128 %.3f <512 %.3f >=512 %.3f\n",
+            pc[11] / (double)pc[0], pc[12] / (double)pc[0], pc[13] / (double)pc[0], pc[14] / (double)pc[0],
+            pc[15] / (double)pc[0]);
     const unsigned long long z16[16] = {};
     cudaMemcpyToSymbol(g_prof_cnt, z16, sizeof(z16));
     const unsigned long long init[3] = {~0ull, ~0ull, 0ull};
