@@ -161,7 +161,7 @@ constexpr uint32_t kRecMax = 1024;
 // 64/32/16-entry blocks the records touch, [4] records shorter than 8 entries, [5] entries of
 // records shorter than 64, [6] wedges in dense windows, [7] wedges in bitmap windows, [8] touched
 // words in the epilogue, [9] contributing fields, [10] records
-__device__ unsigned long long g_prof_cnt[16];
+__device__ unsigned long long g_prof_cnt[64];  // [16..33]: window-size bins, [40..57] per-phase cycles (BBF_T3_WINPROF)
 #define T3_COUNT(i, v) atomicAdd(&g_prof_cnt[i], (unsigned long long)(v))
 __device__ unsigned long long g_prof_t[3] = {~0ull, ~0ull, 0ull};  // min CTA start, min CTA end, max CTA end (globaltimer ns)
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -287,7 +287,11 @@ __device__ __forceinline__ void t3_share_c(const uint32_t* ctr, uint32_t word0, 
 // volatile (ordered with each other and with barriers) but without a "memory" clobber, so the
 // compiler may still move the global chunk loads across them
 __device__ __forceinline__ void sh_red_add(uint32_t addr, uint32_t v) {
+#ifdef BBF_EXP_NOATOM  // timing experiment only: no counter update (results are wrong)
+  if ((addr ^ v) == 0x12345677u) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));
+#else
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v));
+#endif
 }
 __device__ __forceinline__ uint32_t sh_atom_add(uint32_t addr, uint32_t v) {
   uint32_t r;
@@ -296,7 +300,11 @@ __device__ __forceinline__ uint32_t sh_atom_add(uint32_t addr, uint32_t v) {
 }
 __device__ __forceinline__ uint32_t sh_load(uint32_t addr) {
   uint32_t r;
+#ifdef BBF_EXP_NOLDS  // timing experiment only: no counter read (results are wrong)
+  r = addr * 0x9E3779B1u;
+#else
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
+#endif
   return r;
 }
 
@@ -391,7 +399,11 @@ __device__ __forceinline__ void epi_packed(const EngineArgs& a, const ZoneP& zp,
     wb += fb;
     wn += fn;
     const uint32_t wrow = sb + lbase + f;
+#ifndef BBF_EXP_NOEPI
     if (PV) end_red(a, rs, lbase + f, wrow, fb, fn);  // fb | fn != 0 here
+#else
+    if (PV && fb == 0x7fffffffu) end_red(a, rs, lbase + f, wrow, fb, fn);
+#endif
     if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
   }
   xB += wb;
@@ -425,11 +437,17 @@ struct Rec {  // 16 B segment record
 template <int MODE, bool CP, bool WIDE>
 __device__ __forceinline__ void t3_chunk(const uint32_t (&ev)[kCE], uint32_t vm, uint32_t cbase,
                                          uint32_t* ctr, uint32_t* bm, uint32_t word0, uint32_t shamt,
-                                         uint32_t oshamt, uint32_t wv, uint32_t& cb, uint32_t& cn) {
-  if (CP && MODE == 0) {  // pass 1, dense window: branch-free predicated updates
+                                         uint32_t oshamt, uint32_t wv, uint32_t& cb, uint32_t& cn, uint32_t dummy) {
+  if (CP && MODE == 0) {  // pass 1, dense window: an entry outside the record adds 0 to the lane's own word
 #pragma unroll
-    for (int j = 0; j < (int)kCE; ++j)
-      sh_red_add_if(cbase + (ev[j] & kCpAddrMask), 1u << ((ev[j] >> shamt) & 31u), vm & (1u << j));
+    for (int j = 0; j < (int)kCE; ++j) {
+      const bool on = (vm >> j) & 1u;
+      uint32_t sh;
+      asm("shr.b32 %0, %1, %2;" : "=r"(sh) : "r"(ev[j]), "r"(shamt));
+      uint32_t inc;
+      asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(inc) : "r"(0u), "r"(1u), "r"(sh));
+      sh_red_add(on ? cbase + (ev[j] & kCpAddrMask) : dummy, on ? inc : 0u);
+    }
     return;
   }
   if (CP && MODE == 1) {  // pass 1 with the touched-word bitmap: fire-and-forget add and bit-or
@@ -442,11 +460,13 @@ __device__ __forceinline__ void t3_chunk(const uint32_t (&ev)[kCE], uint32_t vm,
     }
     return;
   }
-  if (CP && MODE == 2) {  // pass 2: predicated loads; sum of own-class counts minus #entries
+  if (CP && MODE == 2) {  // pass 2: an entry outside the record reads the lane's own word, counted as 0
     uint32_t own = 0, oth = 0;
 #pragma unroll
     for (int j = 0; j < (int)kCE; ++j) {
-      const uint32_t v = sh_load_if(cbase + (ev[j] & kCpAddrMask), vm & (1u << j));
+      const bool on = (vm >> j) & 1u;
+      uint32_t v = sh_load(on ? cbase + (ev[j] & kCpAddrMask) : dummy);
+      v = on ? v : 0u;
       const uint32_t h = 2u << (ev[j] & 3u);
       own += cp_field(v, ev[j], shamt, h);
       oth += cp_field(v, ev[j], oshamt, h);
@@ -471,15 +491,20 @@ __device__ __forceinline__ void t3_chunk(const uint32_t (&ev)[kCE], uint32_t vm,
 }
 
 // ---------------------------------------------------------------------------- long records
-// A record of at least kLongMin entries (compact encoding) is walked by ONE warp: steps of
-// 256 entries, lane L holding entries 4L..4L+3 and 128+4L..131+4L of the step (two LDG.128, the
-// warp's loads cover 1 KB contiguous), so there is no owner lookup, interior steps need no entry
-// masks (a warp-uniform test), and pass 2 sums the record's shares in lane registers and reduces
-// them once per record.  Records shorter than kLongMin go through the flattened batches.
+// A record of at least kLongMin entries (compact encoding) is walked by ONE warp in 128-entry
+// blocks starting at its first entry's 16-B aligned position: lane L holds entries 4L..4L+3 of a
+// block (one LDG.128; the warp's load is 512 contiguous bytes) and the next two blocks are loaded
+// while the current two are processed.  Only the first block (entries before the record, all in
+// lane 0) and the last one (entries past it) are masked; a masked entry updates (pass 1: adds 0
+// to) or reads (pass 2: counts 0 from) the lane's own word of the window, so there is no branch
+// per entry and no two lanes collide.  Pass 2 sums the record's shares in lane registers and
+// reduces them once per record.  No owner lookup: shorter records go through the flattened
+// batches.
 #ifndef BBF_T3_LONG_MIN
 #define BBF_T3_LONG_MIN 256
 #endif
 constexpr uint32_t kLongMin = BBF_T3_LONG_MIN;
+constexpr uint32_t kAdjcPad = 512;  // adjc padding (entries): the block prefetch may run 388 past a record
 
 // 1 << (x mod 32) in one funnel shift (no separate "& 31")
 __device__ __forceinline__ uint32_t bit_of(uint32_t x) {
@@ -494,48 +519,60 @@ __device__ __forceinline__ uint32_t shr_wrap(uint32_t v, uint32_t x) {
   return r;
 }
 
-// MODE 0: pass 1, dense window; 1: pass 1 with the touched-word bitmap; 2: pass 2.
-template <int MODE>
-__device__ __forceinline__ void t3_long_entry(uint32_t ev, uint32_t on, uint32_t cbase, uint32_t bmbase,
-                                              uint32_t word0, uint32_t shamt, uint32_t oshamt, uint32_t& own,
-                                              uint32_t& oth) {
-  if (MODE == 2) {
-    const uint32_t v = sh_load_if(cbase + (ev & kCpAddrMask), on);
-    const uint32_t h = 2u << (ev & 3u);
-    own += zext(shr_wrap(v, ev >> shamt), h);
-    oth += zext(shr_wrap(v, ev >> oshamt), h);
-  } else {
-    sh_red_add_if(cbase + (ev & kCpAddrMask), bit_of(ev >> shamt), on);
-    if (MODE == 1) {
-      const uint32_t g = cp_word(ev) - word0;
-      sh_red_or_if(bmbase + 4u * (g >> 5), bit_of(g), on);
+// one block's 4 entries of this lane.  MODE 0: pass 1, dense window; 1: pass 1 with the
+// touched-word bitmap; 2: pass 2 (own / other class sums).  MASKED: entry j counts iff bit j of
+// vm4; dummy = the shared address of the lane's own window word.
+template <int MODE, bool MASKED>
+__device__ __forceinline__ void t3_long4(const uint4& q, uint32_t vm4, uint32_t dummy, uint32_t cbase,
+                                         uint32_t bmbase, uint32_t word0, uint32_t shamt, uint32_t oshamt,
+                                         uint32_t& own, uint32_t& oth) {
+  const uint32_t ev[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool on = !MASKED || ((vm4 >> j) & 1u);
+    const uint32_t addr = on ? cbase + (ev[j] & kCpAddrMask) : dummy;
+    if (MODE == 2) {
+      uint32_t v = sh_load(addr);
+      if (MASKED) v = on ? v : 0u;
+      const uint32_t h = 2u << (ev[j] & 3u);
+      own += zext(shr_wrap(v, ev[j] >> shamt), h);
+      oth += zext(shr_wrap(v, ev[j] >> oshamt), h);
+    } else {
+      sh_red_add(addr, on ? bit_of(ev[j] >> shamt) : 0u);
+      if (MODE == 1 && on) {
+        const uint32_t g = cp_word(ev[j]) - word0;
+        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(bmbase + 4u * (g >> 5)), "r"(bit_of(g)));
+      }
     }
   }
 }
 
 template <int MODE>
 __device__ __forceinline__ void t3_long(const uint32_t* __restrict__ adjc, const Rec& rc, uint32_t cbase,
-                                        uint32_t bmbase, uint32_t word0, int lane, uint32_t& own,
-                                        uint32_t& oth) {
+                                        uint32_t ctr0, uint32_t bmbase, uint32_t word0, int lane,
+                                        uint32_t& own, uint32_t& oth) {
   const uint32_t shamt = 22u + 5u * (rc.wv >> 31), oshamt = 49u - shamt;
-  const uint32_t p = rc.p, e_end = rc.p + rc.len;
+  const uint32_t p = rc.p, e_end = rc.p + rc.len, b0 = p & ~3u;
+  const uint32_t nb = (e_end - b0 + 127u) >> 7;
+  const uint32_t dummy = ctr0 + 4u * (uint32_t)lane;
+  const uint4* src = reinterpret_cast<const uint4*>(adjc + b0) + lane;
+  auto vmask = [&](uint32_t b) {  // valid entries of block b in this lane, as 4 bits
+    const uint32_t off = b0 + 128u * b + 4u * (uint32_t)lane;
+    const uint32_t lo = p > off ? min(p - off, 4u) : 0u, hi = e_end > off ? min(e_end - off, 4u) : 0u;
+    return ((1u << hi) - 1u) & ~((1u << lo) - 1u);
+  };
+  uint4 c0 = src[0], c1 = src[32];  // adjc is padded past its last entry
 #pragma unroll 1
-  for (uint32_t b = p & ~3u; b < e_end; b += 256) {
-    const uint32_t e0 = b + 4u * lane, e1 = e0 + 128u;
-    uint4 q0 = make_uint4(0u, 0u, 0u, 0u), q1 = make_uint4(0u, 0u, 0u, 0u);
-    if (e0 < e_end) q0 = *reinterpret_cast<const uint4*>(adjc + e0);
-    if (e1 < e_end) q1 = *reinterpret_cast<const uint4*>(adjc + e1);
-    const uint32_t ev[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-    if (b >= p && b + 256u <= e_end) {  // interior step (warp-uniform): every entry is the record's
-#pragma unroll
-      for (int j = 0; j < 8; ++j) t3_long_entry<MODE>(ev[j], 1u, cbase, bmbase, word0, shamt, oshamt, own, oth);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t e = (j < 4 ? e0 : e1) + (uint32_t)(j & 3);
-        t3_long_entry<MODE>(ev[j], (e >= p) & (e < e_end), cbase, bmbase, word0, shamt, oshamt, own, oth);
-      }
+  for (uint32_t b = 0; b < nb; b += 2) {
+    const uint4 n0 = src[32 * (b + 2)], n1 = src[32 * (b + 3)];  // the next two blocks, in flight
+    if (b == 0 || b + 1 == nb) t3_long4<MODE, true>(c0, vmask(b), dummy, cbase, bmbase, word0, shamt, oshamt, own, oth);
+    else t3_long4<MODE, false>(c0, 0u, dummy, cbase, bmbase, word0, shamt, oshamt, own, oth);
+    if (b + 1 < nb) {
+      if (b + 2 == nb) t3_long4<MODE, true>(c1, vmask(b + 1), dummy, cbase, bmbase, word0, shamt, oshamt, own, oth);
+      else t3_long4<MODE, false>(c1, 0u, dummy, cbase, bmbase, word0, shamt, oshamt, own, oth);
     }
+    c0 = n0;
+    c1 = n1;
   }
 }
 
@@ -645,7 +682,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           if (re > rs) atomicAdd(&sh_wc[run.y], re - rs);
           for (uint32_t p = rs; p < re; p += kRecMax) {
             const uint32_t len = min(kRecMax, re - p);
-            if (CP && len >= kLongMin) {
+            if (CP && len >= kLongMin) {  // long record: walked by one warp (t3_long)
               const uint32_t slot = atomicAdd(&sh_cntl[run.y], 1u);
               R[(size_t)run.y * RS + (RS - 1 - slot)] = Rec{p, len, o_wv, 0u};
             } else {
@@ -701,21 +738,31 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       }
       __syncthreads();
       T3_MARK(1);
+#ifdef BBF_T3_WINPROF  // CTA cycles of the window's passes + epilogue, binned by its wedge count
+      const long long t_win = clock64();
+      const uint32_t wbin = sh_wc[k] < 2048 ? 0 : sh_wc[k] < 8192 ? 1 : sh_wc[k] < 32768 ? 2 : sh_wc[k] < 131072 ? 3 : sh_wc[k] < 524288 ? 4 : 5;
+#endif
       // ---------------- pass 1 (Alg. 2 lines 9-14) and pass 2 (per-vertex shares)
 #pragma unroll 1
       for (int pass = 0; pass < (PV ? 2 : 1); ++pass) {
         if (CP && nlong) {  // long records first, one warp each (sh_c[2 + pass] is the cursor)
           const uint32_t bmbase = (uint32_t)__cvta_generic_to_shared(bm);
-          while (true) {
-            uint32_t r = 0;
-            if (lane == 0) r = atomicAdd(&sh_c[2 + pass], 1u);
-            r = __shfl_sync(0xffffffffu, r, 0);
-            if (r >= nlong) break;
-            const Rec rl = rw[RS - 1 - r];
+          uint32_t r = 0;
+          if (lane == 0) r = atomicAdd(&sh_c[2 + pass], 1u);
+          r = __shfl_sync(0xffffffffu, r, 0);
+          Rec rn = r < nlong ? rw[RS - 1 - r] : Rec{0, 0, 0, 0};
+          while (r < nlong) {
+            const Rec rl = rn;
+            uint32_t r2 = 0;  // the warp's next record, loaded while this one is walked
+            if (lane == 0) r2 = atomicAdd(&sh_c[2 + pass], 1u);
+            r2 = __shfl_sync(0xffffffffu, r2, 0);
+            if (r2 < nlong) rn = rw[RS - 1 - r2];
+            r = r2;
             uint32_t own = 0, oth = 0;
-            if (pass == 1) t3_long<2>(adjc, rl, cbase, bmbase, word0, lane, own, oth);
-            else if (dense) t3_long<0>(adjc, rl, cbase, bmbase, word0, lane, own, oth);
-            else t3_long<1>(adjc, rl, cbase, bmbase, word0, lane, own, oth);
+            const uint32_t ctr0 = (uint32_t)__cvta_generic_to_shared(ctr);
+            if (pass == 1) t3_long<2>(adjc, rl, cbase, ctr0, bmbase, word0, lane, own, oth);
+            else if (dense) t3_long<0>(adjc, rl, cbase, ctr0, bmbase, word0, lane, own, oth);
+            else t3_long<1>(adjc, rl, cbase, ctr0, bmbase, word0, lane, own, oth);
             if (pass == 1) {
               // the record's own-class sum and other-class sum (each < 2^26: <= 1024 entries of
               // 16-bit fields), minus one per wedge for the own class (Lemma 2 shares)
@@ -812,9 +859,10 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
                 const uint32_t end = o_p[u] + o_len[u];
                 const int hi = (int)(end - e0 < kCE ? end - e0 : kCE);
                 const uint32_t vm = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
-                if (pass == 1) t3_chunk<2, CP, WIDE>(ev, vm, cbase, ctr, bm, word0, shamt, oshamt, o_wv[u], cb, cn);
-                else if (dense) t3_chunk<0, CP, WIDE>(ev, vm, cbase, ctr, bm, word0, shamt, oshamt, o_wv[u], cb, cn);
-                else t3_chunk<1, CP, WIDE>(ev, vm, cbase, ctr, bm, word0, shamt, oshamt, o_wv[u], cb, cn);
+                const uint32_t dummy = (uint32_t)__cvta_generic_to_shared(ctr) + 4u * (uint32_t)lane;
+                if (pass == 1) t3_chunk<2, CP, WIDE>(ev, vm, cbase, ctr, bm, word0, shamt, oshamt, o_wv[u], cb, cn, dummy);
+                else if (dense) t3_chunk<0, CP, WIDE>(ev, vm, cbase, ctr, bm, word0, shamt, oshamt, o_wv[u], cb, cn, dummy);
+                else t3_chunk<1, CP, WIDE>(ev, vm, cbase, ctr, bm, word0, shamt, oshamt, o_wv[u], cb, cn, dummy);
               }
               if (pass == 1 && __any_sync(0xffffffffu, (cb | cn) != 0)) {
                 // segmented sum over each owner's lane group; its last lane adds it (one writer
@@ -839,6 +887,9 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
         }
         __syncthreads();
         T3_MARK(nrec < 64 ? 1 : 2 + pass);  // slot 1: set-up + passes of small windows
+#ifdef BBF_T3_WINPROF
+        if (tid == 0) T3_COUNT(40 + 3 * wbin + pass, clock64() - t_win);
+#endif
       }
 
       // ---------------- epilogue: Lemma 2 per touched end (Alg. 2 lines 15-18), clear the window
@@ -896,6 +947,14 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       }
       __syncthreads();
       T3_MARK(4);
+#ifdef BBF_T3_WINPROF
+      if (tid == 0) {
+        T3_COUNT(42 + 3 * wbin, clock64() - t_win);
+        T3_COUNT(16 + 3 * wbin, 1);
+        T3_COUNT(17 + 3 * wbin, sh_wc[k]);
+        T3_COUNT(18 + 3 * wbin, clock64() - t_win);
+      }
+#endif
     }
     for (uint32_t k = tid; k < K; k += kT3Threads) { sh_cnt[k] = 0; sh_wc[k] = 0; sh_cntl[k] = 0; }
     // unit totals -> start vertex
@@ -1471,8 +1530,20 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     cudaMemcpyFromSymbol(t, g_prof_t, sizeof(t));
     fprintf(stderr, "[bbf] t3 CTA ends: first %.3f ms, last %.3f ms after the first start\n", (t[1] - t[0]) * 1e-6,
             (t[2] - t[0]) * 1e-6);
-    unsigned long long pc[16];
+    unsigned long long pc[64];
     cudaMemcpyFromSymbol(pc, g_prof_cnt, sizeof(pc));
+    const char* bn[6] = {"<2K", "<8K", "<32K", "<128K", "<512K", ">=512K"};
+    for (int b = 0; b < 6; ++b)
+      if (pc[16 + 3 * b])
+        fprintf(stderr, "[bbf] t3 windows %-7s n %8llu wedges %.3e  ms(CTA) %7.2f  cyc/window %8.0f  wedges/cyc %.2f\n", bn[b],
+                pc[16 + 3 * b], (double)pc[17 + 3 * b], pc[18 + 3 * b] / (1.965e6 * g->num_sms * kT3Ctas),
+                pc[18 + 3 * b] / (double)pc[16 + 3 * b], pc[17 + 3 * b] / (double)(pc[18 + 3 * b] + 1));
+    for (int b = 0; b < 6; ++b)
+      if (pc[16 + 3 * b]) {  // cumulative marks: end of pass 1, end of pass 2, end of epilogue
+        const double n = (double)pc[16 + 3 * b];
+        fprintf(stderr, "[bbf] t3 windows %-7s cyc/window pass1 %8.0f pass2 %8.0f epi %8.0f\n", bn[b], pc[40 + 3 * b] / n,
+                (pc[41 + 3 * b] - pc[40 + 3 * b]) / n, (pc[42 + 3 * b] - pc[41 + 3 * b]) / n);
+      }
     fprintf(stderr, "[bbf] t3 records %llu entries %llu blocks64 %llu (fill %.3f) blocks32 %llu (fill %.3f) blocks16 %llu "
             "(fill %.3f) short<8 %llu, entries in records<64 %llu; wedges dense %llu bitmap %llu\n",
             pc[10], pc[0], pc[1], pc[0] / (64.0 * pc[1] + 1e-9), pc[2], pc[0] / (32.0 * pc[2] + 1e-9), pc[3],
@@ -1480,8 +1551,8 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     fprintf(stderr, "[bbf] t3 entries by run length: <8 %.3f <32 %.3f <128 %.3f <512 %.3f >=512 %.3f\n",
             pc[11] / (double)pc[0], pc[12] / (double)pc[0], pc[13] / (double)pc[0], pc[14] / (double)pc[0],
             pc[15] / (double)pc[0]);
-    const unsigned long long z16[16] = {};
-    cudaMemcpyToSymbol(g_prof_cnt, z16, sizeof(z16));
+    const unsigned long long z40[64] = {};
+    cudaMemcpyToSymbol(g_prof_cnt, z40, sizeof(z40));
     const unsigned long long init[3] = {~0ull, ~0ull, 0ull};
     cudaMemcpyToSymbol(g_prof_t, init, sizeof(init));
   }

@@ -716,7 +716,8 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
   g->compact = g->zones[0].L[0] == 0 && g->zones[1].L[0] == 0 && g->zones[0].WB[5] <= kCpWordMask &&
                g->zones[1].WB[5] <= kCpWordMask && !getenv("BBF_NO_COMPACT");  // env: test hook
   const uint32_t wmask = g->compact ? kCpWordMask : kCWordMask, wshift = g->compact ? 2u : 0u;
-  BBF_CUDA(dmalloc(&g->adjc, 4ull * (m + 32), st));  // padded: 32-B chunk loads
+  BBF_CUDA(dmalloc(&g->adjc, 4ull * (m + 512), st));  // padded: chunk loads and the hub kernel's
+  // long-record prefetch (count_sparse.cu kAdjcPad) may read past the last entry
   BBF_CUDA(dmalloc(&g->runid, 4ull * (m + 1), st));
   g->nruns = 0;
   if (m) {
