@@ -182,6 +182,7 @@ struct EventPair {
   EventPair& operator=(const EventPair&) = delete;
 };
 
+}  // namespace
 // the (rank, nranks) shard this process counts: the communicator's, or the BBF_FAKE_WORLD test
 // hook's ("r/N": count rank r's shard of an N-rank job on this single GPU, no collective)
 void shard_of(const bbf_graph* g, int* rank, int* nranks) {
@@ -195,6 +196,7 @@ void shard_of(const bbf_graph* g, int* rank, int* nranks) {
     }
   }
 }
+namespace {
 
 bbf_status check_overflow(bbf_graph* g) {
   if (g->ws_bound >= 18446744073709551615.0L) {
@@ -206,6 +208,9 @@ bbf_status check_overflow(bbf_graph* g) {
 
 bbf_status ensure_plan_g(bbf_graph* g) {
   BBF_TRY(ensure_adj(g));
+  int rank, nranks;
+  shard_of(g, &rank, &nranks);
+  if (g->plan_g.valid && g->plan_g.nranks != nranks) free_plan(&g->plan_g, g->stream);  // units sized per N
   if (!g->plan_g.valid) BBF_TRY(make_plan(g, 0, &g->plan_g));
   return BBF_OK;
 }

@@ -209,6 +209,7 @@ struct Plan {
   // middle-role packing: middles of local rank >= rmid[side] (C(deg,2) * max degree of the
   // other side < 2^32) put (B | N << 32) of a record in ONE 64-bit RED into g->pm
   uint32_t rmid[2];
+  int nranks;          // ranks the hub units were sized for
   bool valid;
 };
 
@@ -352,5 +353,7 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks,
 // Alg. 1 BB-Base (base.cu): explicit pair checks, the paper's baseline
 bbf_status run_base(bbf_graph* g, Plan* p, int rank, int nranks, unsigned long long* host_BN);
 bool dense_supported(bbf_graph* g);
+// the (rank, nranks) shard of the work this process counts (communicator, or BBF_FAKE_WORLD)
+void shard_of(const bbf_graph* g, int* rank, int* nranks);
 bool dense_preferred(bbf_graph* g, bool per_vertex);
 }  // namespace bbf

@@ -1599,6 +1599,7 @@ bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uin
                           int nranks) {
   cudaStream_t st = g->stream;
   Plan* p = &g->plan_s[side];
+  if (p->valid && p->nranks != nranks) free_plan(p, st);  // hub units are sized per rank count
   if (!p->valid) BBF_TRY(make_plan(g, 1 + side, p));
   // Candidates are the pairs with balanced >= tau (reading R11 ranks by balanced count).  tau
   // starts at 1 (every pair with a balanced butterfly); if the candidates overflow the buffer,

@@ -291,8 +291,14 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   BBF_CUDA(rb_add(&h_wf, &acc[0], 8, st)); g->launches++;
   // hub units of ~1/6 of one SM's share of the whole job: with N ranks the share is W / (N * SMs),
   // so a rank's largest unit stays well below its per-SM work at any N
-  const uint64_t nranks = g->comm ? (uint64_t)g->comm->nranks : 1ull;
-  const uint64_t w_div = nranks * (uint64_t)g->num_sms * 6ull + 1;
+  int shard_rank = 0, shard_n = 1;
+  shard_of(g, &shard_rank, &shard_n);
+  p->nranks = shard_n;
+  const uint64_t nranks = (uint64_t)shard_n;
+  // hub units of ~1/3 of an SM share (BBF_UNIT_DIV tunes it; 3 measured best at N = 1 and 8:
+  // finer units repeat the unit pre-scan of the hub's middles, coarser ones leave a tail)
+  const uint64_t udiv = getenv("BBF_UNIT_DIV") ? std::max<uint64_t>(1, strtoull(getenv("BBF_UNIT_DIV"), nullptr, 10)) : 3ull;
+  const uint64_t w_div = nranks * (uint64_t)g->num_sms * udiv + 1;
 
   // tiers and units
   // a T2 start's distinct ends (<= its wedges) must fit the k_t2 hash at load <= 1/2
