@@ -51,6 +51,36 @@ def peaks():
     return hbm, i8
 
 
+def measured_tensor_peaks():
+    """Library GEMM peaks measured on this pool (tools/microbench/fp4_peak.py ->
+    profiles/r2_microbench_peaks.jsonl, best of 10 at 8192^3): FP4 block-scaled and int8, TOP/s."""
+    out = {}
+    try:
+        for line in open(os.path.join(ROOT, "profiles", "r2_microbench_peaks.jsonl")):
+            r = json.loads(line)
+            if r.get("n") != 8192:
+                continue
+            if r["bench"] == "fp4_block_scaled_mm":
+                out["fp4"] = r["tflops"]
+            elif r["bench"] == "int8_int_mm":
+                out["int8"] = r["tops"]
+    except OSError:
+        pass
+    return out
+
+
+def ncu_tensor_util(kernel: str):
+    """Tensor-pipe utilisation of `kernel` from its committed ncu capture summary
+    (profiles/r2_ncu_dense_tensor_pipe.json: sm__pipe_tensor_cycles_active, % of peak elapsed)."""
+    try:
+        for r in json.load(open(os.path.join(ROOT, "profiles", "r2_ncu_dense_tensor_pipe.json"))):
+            if kernel in r["kernel"]:
+                return float(r["metrics"]["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"][0]) / 100
+    except (OSError, KeyError, ValueError):
+        pass
+    return None
+
+
 def ncu_traffic(config: int, kernel: str):
     """dram read+write bytes per launch of `kernel` on `config` from the committed ncu --set full
     summary (profiles/ncu_traffic.json), or None."""
@@ -390,6 +420,10 @@ def main():
                 "unit": "TOP/s (fp4, ops = 2 per MAC of the exact integer products)",
                 "frac": achieved / f4_peak, "traffic": ncu_traffic(args.config, kname.split()[0]),
                 "nominal_peak": 9000.0, "frac_of_nominal": achieved / 9000.0,
+                "measured_library_peak": measured_tensor_peaks().get("fp4"),
+                "measured_library_peak_source": "cuBLASLt FP4 block-scaled GEMM via torch._scaled_mm, 8192^3 best of 10 "
+                                                "(profiles/r2_microbench_peaks.jsonl); the kernel exceeds it",
+                "tensor_pipe_util_ncu": ncu_tensor_util(kname.split()[0]),
                 "algo_ops_per_launch": algo_ops, "kernels_per_step": 2}
     elif algo_ops > 0:  # dense int8 tensor-core path (k_dense_pair)
         achieved = algo_ops / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
@@ -398,6 +432,8 @@ def main():
                 "achieved": achieved, "peak": i8_peak, "peak_source": i8_src, "unit": "TOP/s (int8)",
                 "frac": achieved / i8_peak, "traffic": ncu_traffic(args.config, "k_dense_pair"),
                 "nominal_peak": 4500.0, "frac_of_nominal": achieved / 4500.0,
+                "measured_library_peak": measured_tensor_peaks().get("int8"),
+                "tensor_pipe_util_ncu": ncu_tensor_util("k_dense_pair"),
                 "note": "int8 has no measured peak on this pool; the derived one (bf16 burst x 2) is "
                         "below what the kernel reaches (cuBLASLt int8 8192^3 measured 3322 TOP/s, "
                         "profiles/r1_microbench_int8_bf16_hbm.jsonl)",
