@@ -79,6 +79,13 @@ struct EngineArgs {
   unsigned long long cap;
 };
 
+// The q-th work item (hub unit, T1 / T2 start; plan order = descending work, roughly) of `rank` in
+// an N-rank job: items are dealt in snake order (0..N-1, N-1..0, ...) so no rank takes the larger
+// item of every round; every item lands on exactly one rank.
+__device__ __forceinline__ uint64_t shard_item(uint64_t q, int rank, int nranks) {
+  return q * (uint64_t)nranks + ((q & 1ull) ? (uint64_t)(nranks - 1 - rank) : (uint64_t)rank);
+}
+
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
@@ -610,7 +617,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
     if (tid == 0) sh_unit = (uint32_t)atomicAdd(&a.acc[2], 1ull);
     if (tid < 4) sh_c[tid] = 0;
     __syncthreads();
-    const uint64_t ui = (uint64_t)sh_unit * a.nranks + a.rank;
+    const uint64_t ui = shard_item(sh_unit, a.rank, a.nranks);
     if (ui >= a.n_units) break;
     const Unit u = a.units[ui];
     const uint32_t x = u.x;
@@ -1023,7 +1030,7 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
     unsigned long long q = 0;
     if (lane == 0) q = atomicAdd(&a.acc[a.t1ctr], 1ull);
     q = __shfl_sync(0xffffffffu, q, 0);
-    const uint64_t ti = q * a.nranks + a.rank;
+    const uint64_t ti = shard_item(q, a.rank, a.nranks);
     if (ti >= a.n_t1) break;
     const uint32_t x = a.t1[ti];
     const bool xu = x < a.n_u;
@@ -1184,7 +1191,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
   while (true) {
     if (tid == 0) sh_item = (uint32_t)atomicAdd(&a.acc[a.t2ctr], 1ull);
     __syncthreads();
-    const uint64_t ti = (uint64_t)sh_item * a.nranks + a.rank;
+    const uint64_t ti = shard_item(sh_item, a.rank, a.nranks);
     if (ti >= a.n_t2) break;
     const uint32_t x = a.t2[ti];
     const bool xu = x < a.n_u;
@@ -1591,7 +1598,7 @@ __global__ void k_gather_u64(const unsigned long long* __restrict__ src, const u
 // S11: top-k same-side pairs by balanced count (route S on `side`, every unordered pair once).
 // Order: balanced desc, then smaller input id asc, then larger input id asc (reading R11) —
 // two stable radix sorts (ids ascending, then balanced descending).  With nranks > 1 this rank
-// counts only its shard of the work items (item i on rank i mod nranks; every pair is produced by
+// counts only its shard of the work items (shard_item: snake order over ranks; every pair is produced by
 // exactly one item: its start's unit that holds the end's window) and returns the shard's own
 // top-k; api.cu all-gathers the shards' lists and merges them (the global top-k is a subset of
 // the union of the shards' top-k lists).
