@@ -5,6 +5,6 @@ TEST INFRASTRUCTURE ONLY: tests/, __graft_entry__.smoke() and bench.py's cpu_bas
 never imports this package, and this package never imports the product path.
 """
 from .oracle import (  # noqa: F401
-    OracleError, build, brute, route_g, route_g_pv, Prepared, route_s, bb_base, pairs, topk_pairs, priority_order, sm64,
+    OracleError, build, brute, route_g, route_g_pv, Prepared, route_s, edge_brute, edge_counts, bb_base, pairs, topk_pairs, priority_order, sm64,
     sparsify, estimate, positive_subgraph, topk_vertices,
 )

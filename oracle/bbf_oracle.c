@@ -25,6 +25,14 @@
  *                    pair of a list checked for balance explicitly (the paper's baseline).
  *   oracle_pairs     Lemma 2 per same-side pair: C(l,2)+C(m,2) with l / m
  *                    symmetric / asymmetric wedges between the pair, each unordered pair once.
+ *   oracle_edge_brute  per-edge counts by brute force: every butterfly of the 4-tuple enumeration
+ *                    adds one to each of its four edges (Def. Butterfly).
+ *   oracle_edge      per-edge counts by the definition, edge by edge (the butterflies containing
+ *                    e = (u,v), "count the number of balanced butterflies
+ *                    containing the edge e = (u,v)"; the section's eBBFC pseudocode sits in a block
+ *                    the authors removed and indexes its buckets inconsistently, so the oracle
+ *                    follows the sentence, reading R24): for each w in Γ(v) \ {u} and each
+ *                    x in Γ(w) \ {v} with x in Γ(u), the 4-cycle u-v-w-x is classified by its signs.
  *
  * Arithmetic: wedge buckets are uint32 (a bucket is bounded by a vertex degree); every sum of
  * butterflies is accumulated in unsigned __int128 and checked to fit uint64 (SPEC.md:223,
@@ -750,4 +758,119 @@ int oracle_sparsify(uint32_t n_u, const uint64_t *row_ptr, const uint32_t *col, 
   }
   *out_nnz = k;
   return 0;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Per-edge counts.  Edge e of the input U-side CSR (u, col[e]); outputs in
+ * input CSR order.  oracle_edge_brute: dense sign matrix, all 4-tuples (tiny graphs only).
+ * ---------------------------------------------------------------------------------------- */
+int oracle_edge_brute(uint32_t n_u, uint32_t n_v, const uint64_t *row_ptr, const uint32_t *col,
+                      const uint8_t *sign, uint64_t *bal, uint64_t *unb) {
+  graph_t g;
+  int rc = graph_build(&g, n_u, n_v, row_ptr, col, sign);
+  if (rc) return rc;
+  graph_free(&g);
+  const uint64_t nnz = row_ptr[n_u];
+  int8_t *S = (int8_t *)calloc((size_t)n_u * n_v + 1, 1);
+  int64_t *E = (int64_t *)malloc(sizeof(int64_t) * ((size_t)n_u * n_v + 1));  /* edge id or -1 */
+  if (!S || !E) { free(S); free(E); return 4; }
+  for (size_t i = 0; i < (size_t)n_u * n_v; ++i) E[i] = -1;
+  for (uint32_t u = 0; u < n_u; ++u)
+    for (uint64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) {
+      S[(size_t)u * n_v + col[e]] = sign[e] ? 1 : -1;
+      E[(size_t)u * n_v + col[e]] = (int64_t)e;
+    }
+  memset(bal, 0, sizeof(uint64_t) * nnz);
+  memset(unb, 0, sizeof(uint64_t) * nnz);
+  for (uint32_t ui = 0; ui < n_u; ++ui)
+    for (uint32_t uj = ui + 1; uj < n_u; ++uj)
+      for (uint32_t vi = 0; vi < n_v; ++vi) {
+        if (!S[(size_t)ui * n_v + vi] || !S[(size_t)uj * n_v + vi]) continue;
+        for (uint32_t vj = vi + 1; vj < n_v; ++vj) {
+          if (!S[(size_t)ui * n_v + vj] || !S[(size_t)uj * n_v + vj]) continue;
+          const int prod = S[(size_t)ui * n_v + vi] * S[(size_t)ui * n_v + vj] * S[(size_t)uj * n_v + vi] *
+                           S[(size_t)uj * n_v + vj];
+          uint64_t *t = prod > 0 ? bal : unb;   /* Def. Balanced butterfly: even # negatives */
+          t[E[(size_t)ui * n_v + vi]]++; t[E[(size_t)ui * n_v + vj]]++;
+          t[E[(size_t)uj * n_v + vi]]++; t[E[(size_t)uj * n_v + vj]]++;
+        }
+      }
+  free(S); free(E);
+  return 0;
+}
+
+static int8_t sign_of(const graph_t *g, uint32_t a, uint32_t b) {  /* 0 if (a, b) is no edge */
+  for (uint64_t f = g->off[a]; f < g->off[a + 1]; ++f)
+    if (g->nbr[f] == b) return g->sgn[f];
+  return 0;
+}
+
+typedef struct {
+  const graph_t *g;
+  const uint64_t *row_ptr;
+  const uint32_t *col;
+  uint32_t n_u;
+  uint64_t *bal, *unb, *cursor;
+  int rc;
+} edge_task;
+
+static void *edge_worker(void *arg) {
+  edge_task *t = (edge_task *)arg;
+  const graph_t *g = t->g;
+  const uint64_t nnz = t->row_ptr[t->n_u];
+  for (uint64_t i = 0, lim = 0;; ++i) {
+    if (i == lim) {
+      i = __atomic_fetch_add(t->cursor, ORACLE_CHUNK, __ATOMIC_RELAXED);
+      lim = i + ORACLE_CHUNK < nnz ? i + ORACLE_CHUNK : nnz;
+    }
+    if (i >= nnz) break;
+    uint32_t lo = 0, hi = t->n_u;               /* u: the row holding edge i (row_ptr[u] <= i) */
+    while (hi - lo > 1) {
+      const uint32_t md = lo + (hi - lo) / 2;
+      if (t->row_ptr[md] <= i) lo = md; else hi = md;
+    }
+    const uint32_t u = lo;
+    const uint32_t v = t->n_u + t->col[i];
+    const int8_t s_uv = sign_of(g, u, v);
+    u128 b = 0, n = 0;
+    for (uint64_t f = g->off[v]; f < g->off[v + 1]; ++f) {       /* w in Γ(v) \ {u} */
+      const uint32_t w = g->nbr[f];
+      if (w == u) continue;
+      const int8_t s_vw = g->sgn[f];
+      for (uint64_t h = g->off[w]; h < g->off[w + 1]; ++h) {     /* x in Γ(w) \ {v} */
+        const uint32_t x = g->nbr[h];
+        if (x == v) continue;
+        const int8_t s_ux = sign_of(g, u, x);                  /* x in Γ(u)? */
+        if (!s_ux) continue;
+        if (s_uv * s_vw * g->sgn[h] * s_ux > 0) b++; else n++;  /* the 4-cycle u-v-w-x */
+      }
+    }
+    if ((b >> 64) || (n >> 64)) t->rc = 7;
+    t->bal[i] = (uint64_t)b;
+    t->unb[i] = (uint64_t)n;
+  }
+  return NULL;
+}
+
+int oracle_edge(uint32_t n_u, uint32_t n_v, const uint64_t *row_ptr, const uint32_t *col,
+                const uint8_t *sign, int nthreads, uint64_t *bal, uint64_t *unb) {
+  graph_t g;
+  int rc = graph_build(&g, n_u, n_v, row_ptr, col, sign);
+  if (rc) return rc;
+  if (nthreads < 1) nthreads = 1;
+  edge_task *tasks = (edge_task *)calloc((size_t)nthreads, sizeof(edge_task));
+  pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+  uint64_t cursor = 0;
+  for (int i = 0; i < nthreads; ++i) {
+    tasks[i].g = &g; tasks[i].row_ptr = row_ptr; tasks[i].col = col; tasks[i].n_u = n_u;
+    tasks[i].bal = bal; tasks[i].unb = unb; tasks[i].cursor = &cursor;
+    pthread_create(&th[i], NULL, edge_worker, &tasks[i]);
+  }
+  rc = 0;
+  for (int i = 0; i < nthreads; ++i) {
+    pthread_join(th[i], NULL);
+    if (tasks[i].rc) rc = tasks[i].rc;
+  }
+  free(tasks); free(th); graph_free(&g);
+  return rc;
 }

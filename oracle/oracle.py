@@ -53,6 +53,10 @@ def _load():
         lib.oracle_release.restype = None
         lib.oracle_route_g_pv_h.argtypes = [P, P, u64, i32, P, P, P]
         lib.oracle_route_g_pv_h.restype = i32
+        lib.oracle_edge_brute.argtypes = [u32, u32, P, P, P, P, P]
+        lib.oracle_edge_brute.restype = i32
+        lib.oracle_edge.argtypes = [u32, u32, P, P, P, i32, P, P]
+        lib.oracle_edge.restype = i32
         lib.oracle_bb_base.argtypes = [u32, u32, P, P, P, i32, P]
         lib.oracle_bb_base.restype = i32
         lib.oracle_pairs.argtypes = [u32, u32, P, P, P, i32, i32, P, P, P, P, u64, P]
@@ -171,6 +175,29 @@ class Prepared:
 
     def __exit__(self, *a):
         self.close()
+
+
+def edge_brute(g):
+    """Per-edge (balanced, unbalanced) counts by brute force over 4-tuples, input CSR order."""
+    lib = _load()
+    keep, a = _graph_args(g)
+    bal, unb = np.zeros(max(g.nnz, 1), np.uint64), np.zeros(max(g.nnz, 1), np.uint64)
+    rc = lib.oracle_edge_brute(*a, _ptr(bal), _ptr(unb))
+    if rc:
+        raise OracleError(rc)
+    return bal[:g.nnz], unb[:g.nnz]
+
+
+def edge_counts(g, threads=None):
+    """Per-edge (balanced, unbalanced) counts by the definition, edge by edge,
+    input CSR order."""
+    lib = _load()
+    keep, a = _graph_args(g)
+    bal, unb = np.zeros(max(g.nnz, 1), np.uint64), np.zeros(max(g.nnz, 1), np.uint64)
+    rc = lib.oracle_edge(*a, _threads(threads), _ptr(bal), _ptr(unb))
+    if rc:
+        raise OracleError(rc)
+    return bal[:g.nnz], unb[:g.nnz]
 
 
 def bb_base(g, threads=None):

@@ -168,7 +168,7 @@ constexpr uint32_t kRecMax = 1024;
 // 64/32/16-entry blocks the records touch, [4] records shorter than 8 entries, [5] entries of
 // records shorter than 64, [6] wedges in dense windows, [7] wedges in bitmap windows, [8] touched
 // words in the epilogue, [9] contributing fields, [10] records
-__device__ unsigned long long g_prof_cnt[64];  // [16..33]: window-size bins, [40..57] per-phase cycles (BBF_T3_WINPROF)
+__device__ unsigned long long g_prof_cnt[96];  // [64..83]: unit-size bins (BBF_T3_WINPROF)  // [16..33]: window-size bins, [40..57] per-phase cycles (BBF_T3_WINPROF)
 #define T3_COUNT(i, v) atomicAdd(&g_prof_cnt[i], (unsigned long long)(v))
 __device__ unsigned long long g_prof_t[3] = {~0ull, ~0ull, 0ull};  // min CTA start, min CTA end, max CTA end (globaltimer ns)
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -635,6 +635,9 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
     const uint32_t m = a.end1[x] - m_lo;
     const bool split_lo = u.lo > lx + 1, split_hi = u.hi < Z.L[4];
     T3_MARK(5);
+#ifdef BBF_T3_WINPROF
+    const long long t_unit = clock64();
+#endif
 
     // ---------------- pre-scan: segment records per window
     while (true) {
@@ -963,6 +966,18 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       }
 #endif
     }
+#ifdef BBF_T3_WINPROF  // per unit: wedges, windows with records, CTA cycles (pre-scan to end), binned by wedges
+    if (tid == 0) {
+      unsigned long long wu = 0, nw = 0;
+      for (uint32_t k = 0; k < K; ++k) { wu += sh_wc[k]; nw += (sh_cnt[k] + sh_cntl[k]) ? 1 : 0; }
+      const uint32_t ub = wu < 16384 ? 0 : wu < 65536 ? 1 : wu < 262144 ? 2 : wu < 1048576 ? 3 : 4;
+      T3_COUNT(64 + 4 * ub, 1);
+      T3_COUNT(65 + 4 * ub, wu);
+      T3_COUNT(66 + 4 * ub, nw);
+      T3_COUNT(67 + 4 * ub, clock64() - t_unit);
+    }
+    __syncthreads();
+#endif
     for (uint32_t k = tid; k < K; k += kT3Threads) { sh_cnt[k] = 0; sh_wc[k] = 0; sh_cntl[k] = 0; }
     // unit totals -> start vertex
     totB += xB;
@@ -1537,7 +1552,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     cudaMemcpyFromSymbol(t, g_prof_t, sizeof(t));
     fprintf(stderr, "[bbf] t3 CTA ends: first %.3f ms, last %.3f ms after the first start\n", (t[1] - t[0]) * 1e-6,
             (t[2] - t[0]) * 1e-6);
-    unsigned long long pc[64];
+    unsigned long long pc[96];
     cudaMemcpyFromSymbol(pc, g_prof_cnt, sizeof(pc));
     const char* bn[6] = {"<2K", "<8K", "<32K", "<128K", "<512K", ">=512K"};
     for (int b = 0; b < 6; ++b)
@@ -1545,6 +1560,12 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
         fprintf(stderr, "[bbf] t3 windows %-7s n %8llu wedges %.3e  ms(CTA) %7.2f  cyc/window %8.0f  wedges/cyc %.2f\n", bn[b],
                 pc[16 + 3 * b], (double)pc[17 + 3 * b], pc[18 + 3 * b] / (1.965e6 * g->num_sms * kT3Ctas),
                 pc[18 + 3 * b] / (double)pc[16 + 3 * b], pc[17 + 3 * b] / (double)(pc[18 + 3 * b] + 1));
+    const char* ubn[5] = {"<16K", "<64K", "<256K", "<1M", ">=1M"};
+    for (int b = 0; b < 5; ++b)
+      if (pc[64 + 4 * b])
+        fprintf(stderr, "[bbf] t3 units %-6s n %7llu wedges %.3e windows/unit %5.1f  ms(CTA) %7.2f  wedges/cyc %.2f\n", ubn[b],
+                pc[64 + 4 * b], (double)pc[65 + 4 * b], pc[66 + 4 * b] / (double)pc[64 + 4 * b],
+                pc[67 + 4 * b] / (1.965e6 * g->num_sms * kT3Ctas), pc[65 + 4 * b] / (double)(pc[67 + 4 * b] + 1));
     for (int b = 0; b < 6; ++b)
       if (pc[16 + 3 * b]) {  // cumulative marks: end of pass 1, end of pass 2, end of epilogue
         const double n = (double)pc[16 + 3 * b];
@@ -1558,7 +1579,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     fprintf(stderr, "[bbf] t3 entries by run length: <8 %.3f <32 %.3f <128 %.3f <512 %.3f >=512 %.3f\n",
             pc[11] / (double)pc[0], pc[12] / (double)pc[0], pc[13] / (double)pc[0], pc[14] / (double)pc[0],
             pc[15] / (double)pc[0]);
-    const unsigned long long z40[64] = {};
+    const unsigned long long z40[96] = {};
     cudaMemcpyToSymbol(g_prof_cnt, z40, sizeof(z40));
     const unsigned long long init[3] = {~0ull, ~0ull, 0ull};
     cudaMemcpyToSymbol(g_prof_t, init, sizeof(init));

@@ -426,3 +426,44 @@ def test_route_g_pv_start_partition_additive():
         assert sum(p[key] for p in parts) == full[key]
     for key in ("bal_u", "unb_u", "bal_v", "unb_v"):
         assert np.array_equal(sum(p[key] for p in parts), full[key])
+
+
+# ----------------------------------------------------------------------------- per-edge counts
+
+def test_edge_counts_corpus_against_brute_force():
+    """oracle_edge (the definition, edge by edge) equals brute force (every
+    butterfly adds one to each of its 4 edges) on the corpus; per-edge sums are 4B / 4N, and the
+    edges at a vertex sum to twice its per-vertex count (each butterfly containing z has exactly
+    two edges at z)."""
+    for g in corpus(400):
+        bb, bn = O.edge_brute(g)
+        eb, en = O.edge_counts(g, threads=1 + g.n_v % 3)
+        assert np.array_equal(bb, eb) and np.array_equal(bn, en), g.name
+        br = O.brute(g)
+        assert int(eb.sum()) == 4 * br["B"] and int(en.sum()) == 4 * br["N"]
+        u = np.repeat(np.arange(g.n_u), np.diff(g.row_ptr.astype(np.int64)))
+        assert np.array_equal(np.bincount(u, weights=eb.astype(np.float64), minlength=g.n_u).astype(np.int64),
+                              2 * br["bal_u"].astype(np.int64))
+        assert np.array_equal(np.bincount(g.col.astype(np.int64), weights=en.astype(np.float64),
+                                          minlength=g.n_v).astype(np.int64), 2 * br["unb_v"].astype(np.int64))
+
+
+@pytest.mark.parametrize("m,n", [(2, 2), (4, 5), (7, 3)])
+def test_edge_counts_complete_closed_form(m, n):
+    """K_{m,n} all positive: every edge lies in (m-1)(n-1) butterflies, all balanced."""
+    eb, en = O.edge_counts(G.complete(m, n))
+    assert np.all(eb == (m - 1) * (n - 1)) and not en.any()
+
+
+def test_edge_counts_medium_switching_invariant():
+    """On a graph beyond brute force: switching a vertex's signs leaves every edge count unchanged
+    (a butterfly has 0 or 2 edges at the vertex), and the vertex relation holds."""
+    g = G.random_bipartite(150, 120, 0.08, 0.6, seed=77)
+    eb, en = O.edge_counts(g, threads=4)
+    h = switch(g, 7)
+    hb, hn = O.edge_counts(h, threads=4)
+    assert np.array_equal(eb, hb) and np.array_equal(en, hn)
+    pv = O.route_g_pv(g)
+    u = np.repeat(np.arange(g.n_u), np.diff(g.row_ptr.astype(np.int64)))
+    assert np.array_equal(np.bincount(u, weights=en.astype(np.float64), minlength=g.n_u).astype(np.int64),
+                          2 * pv["unb_u"].astype(np.int64))
