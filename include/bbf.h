@@ -191,6 +191,21 @@ bbf_status bbf_count_per_vertex(bbf_graph *g, uint64_t *bal_u, uint64_t *unb_u, 
 bbf_status bbf_count_pairs_topk(bbf_graph *g, int side, uint32_t k, bbf_pair *out,
                                 uint32_t *n_out, uint32_t flags);
 
+/* Per-edge counts: for every edge e of the graph, the balanced / unbalanced butterflies containing
+ * it ("count the number of balanced butterflies containing the edge e = (u,v)";
+ * DESIGN.md reading R24).  row_ptr / col: the U-side CSR the graph was loaded from (the same
+ * arrays, or any CSR of the same edge set) — its edge order is the output order: bal[i], unb[i]
+ * belong to edge (u, col[i]) with row_ptr[u] <= i < row_ptr[u + 1].  Host pointers unless
+ * BBF_PTR_DEVICE (then row_ptr, col, bal, unb are device pointers); bal / unb nullable.  totals
+ * (nullable, host): global counts.  Each edge's counts are the Lemma-2 middle shares of its V
+ * endpoint summed over all U-pairs containing its U endpoint (route S(U) in both directions on the
+ * sparse engine's hub kernel), so they satisfy sum_e = 4 (B, N) and, per vertex z, the sum over
+ * z's edges = 2 x z's per-vertex count.  With a comm the work is sharded and the slots all-reduced.
+ * Errors: BBF_EINVAL (null pointers, flags, a CSR whose edges are not the graph's), those of
+ * bbf_count_global. */
+bbf_status bbf_count_per_edge(bbf_graph *g, const uint64_t *row_ptr, const uint32_t *col, uint64_t *bal,
+                              uint64_t *unb, uint32_t flags, bbf_counts *totals);
+
 /* Top-k vertices of one side (case study, "top-10 actors with most number of
  * positive butterflies / positive edges"): metric BBF_METRIC_BALANCED ranks by
  * the per-vertex balanced count (bbf_count_per_vertex), BBF_METRIC_DEGREE by degree in the loaded

@@ -67,6 +67,7 @@ def lib():
         L.bbf_count_per_vertex.argtypes = [P, P, P, P, P, u32, P]
         L.bbf_count_pairs_topk.argtypes = [P, i32, u32, P, P, u32]
         L.bbf_graph_stats.argtypes = [P, P, P, P, P]
+        L.bbf_count_per_edge.argtypes = [P, P, P, P, P, u32, P]
         L.bbf_topk_vertices.argtypes = [P, i32, i32, u32, P, P, P]
         L.bbf_estimate_global.argtypes = [u32, u32, P, P, P, u32, C.c_double, u32, u64, i32, P, P,
                                           P, P, P]
@@ -76,7 +77,7 @@ def lib():
         L.bbf_device_sync.argtypes = [i32]
         for f in ("bbf_nccl_unique_id", "bbf_comm_init", "bbf_comm_free", "bbf_graph_load_csr",
                   "bbf_graph_free", "bbf_count_global", "bbf_count_global_base", "bbf_count_per_vertex",
-                  "bbf_count_pairs_topk", "bbf_graph_stats", "bbf_estimate_global", "bbf_topk_vertices",
+                  "bbf_count_pairs_topk", "bbf_graph_stats", "bbf_count_per_edge", "bbf_estimate_global", "bbf_topk_vertices",
                   "bbf_upload_csr", "bbf_graph_load_upload", "bbf_upload_free", "bbf_device_sync"):
             getattr(L, f).restype = i32
         _lib = L
@@ -258,6 +259,27 @@ class Graph:
                    wedges_G=c.wedges_G, ms_count=c.ms_count)
         return tot, bu, nu, bv, nv
 
+    def count_per_edge(self, row_ptr, col, out=None):
+        """Per-edge (totals, bal, unb) in the order of the CSR (row_ptr, col) — the graph's own
+        edges, e.g. the arrays it was loaded from (numpy host arrays or CUDA tensors; `out` may be
+        two CUDA tensors of nnz int64 for device outputs)."""
+        c = bbf_counts()
+        flags = 0
+        if _is_torch(row_ptr) and row_ptr.is_cuda:
+            flags |= BBF_PTR_DEVICE
+            rp, cl = row_ptr, col
+            bal, unb = out if out is not None else (None, None)
+            assert bal is not None, "device CSR: pass out=(bal, unb) CUDA tensors"
+        else:
+            rp = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+            cl = np.ascontiguousarray(col, dtype=np.uint32)
+            nnz = int(rp[-1]) if rp.size else 0
+            bal, unb = np.zeros(nnz, np.uint64), np.zeros(nnz, np.uint64)
+        _check(lib().bbf_count_per_edge(self.h, _ptr(rp), _ptr(cl), _ptr(bal), _ptr(unb), flags, C.byref(c)))
+        tot = dict(balanced=c.balanced, unbalanced=c.unbalanced, total=c.total, wedges_G=c.wedges_G,
+                   ms_count=c.ms_count)
+        return tot, bal, unb
+
     def count_pairs_topk(self, k: int, side: int = BBF_SIDE_U, flags: int = 0):
         buf = (bbf_pair * max(int(k), 1))()
         n = C.c_uint32()
@@ -337,6 +359,10 @@ def bbf_count_per_vertex(g: Graph, out=None, flags: int = 0):
 
 def bbf_count_pairs_topk(g: Graph, side: int, k: int, flags: int = 0):
     return g.count_pairs_topk(k, side, flags)
+
+
+def bbf_count_per_edge(g: Graph, row_ptr, col, out=None):
+    return g.count_per_edge(row_ptr, col, out)
 
 
 def bbf_graph_stats(g: Graph):

@@ -105,6 +105,32 @@ __global__ void k_scatter_pv(const unsigned long long* __restrict__ pv, const ui
   if (on) on[id] = pv[2ull * (row0 + r) + 1];
 }
 
+// per-edge counts, rank space -> input CSR order: edge i = (u, col[i]) of the caller's CSR; its
+// slot is u's rank-space row entry holding l(col[i]) (rows ascending by local rank, bit 31 = sign)
+__global__ void k_edge_out(uint32_t n_u, uint32_t n_v, const uint64_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                           uint64_t nnz, const uint32_t* __restrict__ lr, const uint32_t* __restrict__ off,
+                           const uint32_t* __restrict__ adj, const unsigned long long* __restrict__ edge,
+                           unsigned long long* __restrict__ ob, unsigned long long* __restrict__ on,
+                           uint32_t* __restrict__ err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nnz; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = n_u;  // u: the row with rp[u] <= i < rp[u + 1]
+    while (hi - lo > 1) {
+      const uint32_t md = lo + (hi - lo) / 2;
+      if (rp[md] <= i) lo = md; else hi = md;
+    }
+    if (col[i] >= n_v) { atomicOr(err, 1u); continue; }
+    const uint32_t r = lr[lo], lv = lr[n_u + col[i]];
+    uint32_t a = off[r], b = off[r + 1];  // first entry with local rank >= lv
+    while (a < b) {
+      const uint32_t md = a + (b - a) / 2;
+      if ((adj[md] & kMask) < lv) a = md + 1; else b = md;
+    }
+    if (a >= off[r + 1] || (adj[a] & kMask) != lv) { atomicOr(err, 1u); continue; }
+    if (ob) ob[i] = edge[2ull * a];
+    if (on) on[i] = edge[2ull * a + 1];
+  }
+}
+
 // per-vertex score (balanced count or degree) of one side in input-id order, ids ascending
 __global__ void k_rank_scores(const unsigned long long* __restrict__ pv, const uint32_t* __restrict__ degs,
                               const uint32_t* __restrict__ inv, uint32_t row0, uint32_t cnt, bool degree,
@@ -493,6 +519,8 @@ bbf_status bbf_graph_free(bbf_graph* g) {
   free_plan(&g->plan_g, g->stream);
   free_plan(&g->plan_s[0], g->stream);
   free_plan(&g->plan_s[1], g->stream);
+  free_plan(&g->plan_e[0], g->stream);
+  free_plan(&g->plan_e[1], g->stream);
   void* ptrs[] = {g->off, g->adj, g->erow, g->rev, g->rlast, g->mid, g->end1, g->inv, g->degs, g->degpre, g->scratch, g->d_acc, g->pv, g->pe, g->pm,
                   g->adjc, g->runid, g->runs, g->skey, g->lr, g->in_rp, g->in_col, g->in_sg,
                   g->dA[0], g->dA[1], g->dS[0], g->dS[1], g->dA4[0], g->dA4[1], g->dS4[0], g->dS4[1]};
@@ -674,6 +702,111 @@ bbf_status bbf_count_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* ou
   });
   *n_out = (uint32_t)std::min<size_t>(k, cand.size());
   for (uint32_t i = 0; i < *n_out; ++i) out[i] = cand[i];
+  return BBF_OK;
+}
+
+bbf_status bbf_count_per_edge(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* col, uint64_t* bal,
+                              uint64_t* unb, uint32_t flags, bbf_counts* totals) {
+  if (!g || !row_ptr) { set_error("null pointer"); return BBF_EINVAL; }
+  if (flags & ~(uint32_t)BBF_PTR_DEVICE) { set_error("unknown flags"); return BBF_EINVAL; }
+  BBF_CUDA(cudaSetDevice(g->device));
+  BBF_TRY(check_overflow(g));
+  cudaStream_t st = g->stream;
+  const bool dptr = flags & BBF_PTR_DEVICE;
+  const uint64_t nnz = g->nnz, m = 2 * nnz;
+  if (nnz && !col) { set_error("null col"); return BBF_EINVAL; }
+  {  // the CSR must have the graph's edge count (its edges are checked against the graph below)
+    uint64_t c_nnz = 0;
+    if (dptr) {
+      BBF_CUDA(rb_add(&c_nnz, row_ptr + g->n_u, 8, st));
+      BBF_CUDA(rb_sync(st));
+    } else {
+      c_nnz = row_ptr[g->n_u];
+    }
+    if (c_nnz != nnz) { set_error("per-edge counts: the CSR passed is not the loaded graph's"); return BBF_EINVAL; }
+  }
+  int rank, nranks;
+  shard_of(g, &rank, &nranks);
+  EventPair ev;
+  cudaEventRecord(ev.a, st);
+  // the edge slots: one (balanced, unbalanced) pair per rank-space adjacency entry of the U rows
+  unsigned long long* d_edge = nullptr;
+  BBF_CUDA(dmalloc(&d_edge, 16ull * (m + 1), st));
+  BBF_CUDA(cudaMemsetAsync(d_edge, 0, 16ull * (m + 1), st));
+  unsigned long long BN[2] = {0, 0}, BN2[2] = {0, 0};
+  // route S(U) with the ends after the start, then with the ends before it: every U-pair (u, w)
+  // is seen from both u and w, so each start->middle edge collects the shares of all its pairs
+  // (reading R24); the hub kernel runs every start (its records carry the start->middle entry)
+  bbf_status local = ensure_adj(g);
+  for (int k = 0; k < 2 && local == BBF_OK; ++k) {
+    Plan* p = &g->plan_e[k];
+    if (p->valid && p->nranks != nranks) free_plan(p, st);
+    if (!p->valid) local = make_plan(g, k == 0 ? 1 : 3, p, true);
+    if (local == BBF_OK) {
+      cudaError_t e = cudaMemsetAsync(g->pv, 0, 16ull * g->n, st);
+      if (e != cudaSuccess) local = cuda_status(e, "memset");
+    }
+    if (local == BBF_OK)
+      local = run_sparse_impl(g, p, true, false, rank, nranks, k == 0 ? BN : BN2, nullptr, nullptr, nullptr, 0, nullptr,
+                              1ull, d_edge);
+  }
+  if (multi_rank(g)) {  // every rank enters: status max-reduce, (B, N), the edge slots
+    BBF_TRY(finish_collective(g, local, false, BN));
+    BBF_TRY(allreduce_u64(g, d_edge, 2 * m));
+  } else if (local != BBF_OK) {
+    dfree(d_edge, st);
+    return local;
+  }
+  // the caller's CSR order
+  const uint64_t* d_rp = row_ptr;
+  const uint32_t* d_col = col;
+  uint64_t* stage_rp = nullptr;
+  uint32_t* stage_col = nullptr;
+  if (!dptr) {
+    BBF_CUDA(dmalloc(&stage_rp, 8ull * (g->n_u + 1), st));
+    BBF_CUDA(dmalloc(&stage_col, 4ull * (nnz + 1), st));
+    BBF_CUDA(cudaMemcpyAsync(stage_rp, row_ptr, 8ull * (g->n_u + 1), cudaMemcpyHostToDevice, st));
+    if (nnz) BBF_CUDA(cudaMemcpyAsync(stage_col, col, 4ull * nnz, cudaMemcpyHostToDevice, st));
+    d_rp = stage_rp;
+    d_col = stage_col;
+  }
+  unsigned long long *ob = nullptr, *on = nullptr;
+  if (dptr) {
+    ob = (unsigned long long*)bal;
+    on = (unsigned long long*)unb;
+  } else {
+    BBF_CUDA(dmalloc(&ob, 16ull * (nnz + 1), st));
+    on = ob + nnz;
+  }
+  uint32_t* d_err;
+  BBF_CUDA(dmalloc(&d_err, 4, st));
+  BBF_CUDA(cudaMemsetAsync(d_err, 0, 4, st));
+  if (nnz && g->n_u) {
+    k_edge_out<<<(unsigned)std::min<uint64_t>((nnz + 255) / 256, 148ull * 64), 256, 0, st>>>(
+        g->n_u, g->n_v, d_rp, d_col, nnz, g->lr, g->off, g->adj, d_edge, (dptr && !bal) ? nullptr : ob,
+        (dptr && !unb) ? nullptr : on, d_err);
+    g->launches++;
+  }
+  uint32_t h_err = 0;
+  BBF_CUDA(cudaMemcpyAsync(&h_err, d_err, 4, cudaMemcpyDeviceToHost, st));
+  if (!dptr && nnz) {
+    if (bal) BBF_CUDA(cudaMemcpyAsync(bal, ob, 8ull * nnz, cudaMemcpyDeviceToHost, st));
+    if (unb) BBF_CUDA(cudaMemcpyAsync(unb, on, 8ull * nnz, cudaMemcpyDeviceToHost, st));
+  }
+  cudaEventRecord(ev.b, st);
+  BBF_TRY(sync_stream(g));
+  for (void* q : {(void*)d_edge, (void*)stage_rp, (void*)stage_col, (void*)d_err}) if (q) dfree(q, st);
+  if (!dptr) dfree(ob, st);
+  if (h_err) { set_error("per-edge counts: the CSR passed is not the loaded graph's"); return BBF_EINVAL; }
+  if (totals) {
+    unsigned long long wg = 0;
+    BBF_TRY(wedges_g(g, &wg));
+    totals->balanced = BN[0];
+    totals->unbalanced = BN[1];
+    totals->total = BN[0] + BN[1];
+    totals->wedges_G = wg;
+    cudaEventElapsedTime(&totals->ms_count, ev.a, ev.b);
+  }
   return BBF_OK;
 }
 

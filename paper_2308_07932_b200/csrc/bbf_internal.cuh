@@ -187,7 +187,7 @@ struct Unit {  // one T3 work unit: start row x, end-rank range [lo, hi)
 };
 
 struct Plan {
-  int route;           // 0 = G, 1 = S(U), 2 = S(V)
+  int route;           // 0 = G, 1 = S(U), 2 = S(V), 3 = S(U) with the ends before the start
   uint32_t* ub;        // per middle entry: first eligible end (absolute adj index)
   uint64_t* work;      // per row: pruned wedge count
   uint32_t* t1;        // rows with 0 < work <= kT1SmallMax (k_t1, 256-slot warp hash)
@@ -273,6 +273,7 @@ struct bbf_graph {
   long double ws_bound;  // overflow bound on B + N
   bbf::Plan plan_g;
   bbf::Plan plan_s[2];
+  bbf::Plan plan_e[2];  // per-edge counts: route S(U) (ends after the start) and route 3 (ends before), all hub tier
   // scratch for the engine
   uint32_t* scratch;  // per-CTA middle arrays
   size_t scratch_words;
@@ -337,7 +338,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
 bbf_status ensure_adj(bbf_graph* g);
 bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col,
                                 const uint8_t* d_sg);
-bbf_status make_plan(bbf_graph* g, int route, Plan* p);
+bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3 = false);
 void free_plan(Plan* p, cudaStream_t st);
 // run the sparse engine for a route; per_vertex -> accumulate into g->pv (rank space)
 bbf_status run_sparse(bbf_graph* g, Plan* p, bool per_vertex, int rank, int nranks,
@@ -345,7 +346,7 @@ bbf_status run_sparse(bbf_graph* g, Plan* p, bool per_vertex, int rank, int nran
 bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, int rank, int nranks,
                            unsigned long long* host_BN, unsigned long long* cb, unsigned long long* cn,
                            unsigned long long* cid, unsigned long long cap, unsigned long long* n_cand,
-                           unsigned long long tau);
+                           unsigned long long tau, unsigned long long* edge = nullptr);
 bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uint32_t* n_out, int rank,
                           int nranks);
 bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks,

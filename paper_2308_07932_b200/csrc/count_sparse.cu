@@ -77,6 +77,12 @@ struct EngineArgs {
   unsigned long long* cn;
   unsigned long long* cid;
   unsigned long long cap;
+  // per-edge counts (bbf_count_per_edge): the middle-role share of every record goes to the
+  // start->middle entry's slot edge[2e], edge[2e + 1] instead of the middle vertex, and the
+  // start / end roles are not scattered; ue (route 3: the rev array) cuts each middle's ends at the
+  // start's own entry (ends before the start)
+  unsigned long long* edge;
+  const uint32_t* ue;
 };
 
 // The q-th work item (hub unit, T1 / T2 start; plan order = descending work, roughly) of `rank` in
@@ -125,6 +131,7 @@ __device__ unsigned long long g_red_cnt[8];  // end: unpacked, packed, rank < 10
 #endif
 __device__ __forceinline__ void end_red(const EngineArgs& a, uint32_t rs, uint32_t lrank, uint32_t wrow,
                                         uint32_t fb, uint32_t fn) {
+  if (a.edge) return;  // per-edge counts: no vertex roles
   RED_CNT(lrank >= rs ? 1 : 0);
   if (lrank < 1024) RED_CNT(2);
   if (lrank < 8192) RED_CNT(3);
@@ -138,7 +145,12 @@ __device__ __forceinline__ void end_red(const EngineArgs& a, uint32_t rs, uint32
 
 // Middle-role share of one record / middle: packed like end_red (pm, threshold rmid).
 __device__ __forceinline__ void mid_red(const EngineArgs& a, uint32_t rm, uint32_t lrank, uint32_t vrow,
-                                        uint32_t cb, uint32_t cn) {
+                                        uint32_t cb, uint32_t cn, uint32_t e) {
+  if (a.edge) {  // per-edge counts: the share of the start->middle edge (adjacency entry e)
+    if (cb) atomicAdd(&a.edge[2ull * e], (unsigned long long)cb);
+    if (cn) atomicAdd(&a.edge[2ull * e + 1], (unsigned long long)cn);
+    return;
+  }
   RED_CNT(lrank >= rm ? 5 : 4);
   if (lrank < 1024) RED_CNT(6);
   if (lrank >= rm) {
@@ -428,15 +440,15 @@ __device__ __forceinline__ void epi_wide(const EngineArgs& a, uint32_t sb, uint3
   xB += fb;
   xN += fn;
   const uint32_t wrow = sb + (gw >> 1);
-  if (PV) {
+  if (PV && !a.edge) {
     if (fb) atomicAdd(&a.pv[2ull * (wrow)], fb);
     if (fn) atomicAdd(&a.pv[2ull * (wrow) + 1], fn);
   }
   if (PAIRS && fb) emit_pair(a, x, wrow, fb, fn);
 }
 
-struct Rec {  // 16 B segment record
-  uint32_t p, len, wv, pad;
+struct Rec {  // 16 B segment record: adjacency range [p, p + len) of the middle (word wv) of start entry e
+  uint32_t p, len, wv, e;
 };
 
 // The kCE entries of one chunk: vm has bit j set iff entry j belongs to the owner record.
@@ -633,7 +645,9 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
     const uint32_t K = (Z.WB[5] + kWin - 1) / kWin;
     const uint32_t m_lo = a.mid ? a.mid[x] : a.off[x];
     const uint32_t m = a.end1[x] - m_lo;
-    const bool split_lo = u.lo > lx + 1, split_hi = u.hi < Z.L[4];
+    // ends after x (u.lo = lx + 1 .. L4) or, with a.ue (route 3), before x (0 .. lx); a unit that
+    // starts or ends inside that range cuts each middle's segment by a binary search
+    const bool split_lo = u.lo > (a.ue ? 0u : lx + 1), split_hi = u.hi < (a.ue ? lx : Z.L[4]);
     T3_MARK(5);
 #ifdef BBF_T3_WINPROF
     const long long t_unit = clock64();
@@ -652,6 +666,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
         wv = a.adj[e];
         s = a.ub[e];
         en = a.end1[ob + (wv & kMask)];
+        if (a.ue) en = min(en, a.ue[e]);  // route 3: the ends before x's own entry of N(v)
         rl = a.rlast[ob + (wv & kMask)];  // same level as end1: no dependent runid[en - 1] load
         if (split_lo && s < en) {
           uint32_t b = s, f = en;
@@ -672,7 +687,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       }
       // records of this middle = the graph's window runs of row v clipped to [s, en)
       const uint32_t r0 = s < en ? a.runid[s] : 0;
-      const uint32_t nr = s < en ? (split_hi ? a.runid[en - 1] : rl) - r0 + 1 : 0;
+      const uint32_t nr = s < en ? ((split_hi || a.ue) ? a.runid[en - 1] : rl) - r0 + 1 : 0;
       const uint32_t incl = warp_incl_scan(nr, lane), excl = incl - nr;
       const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
       const uint32_t nz = __ballot_sync(0xffffffffu, nr > 0);
@@ -684,6 +699,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
         const uint32_t o_s = __shfl_sync(0xffffffffu, s, ow);
         const uint32_t o_en = __shfl_sync(0xffffffffu, en, ow);
         const uint32_t o_wv = __shfl_sync(0xffffffffu, wv, ow);
+        const uint32_t o_e = __shfl_sync(0xffffffffu, m_lo + i, ow);  // the start->middle entry
         if (f < T) {
           const uint32_t r = o_r0 + (f - o_excl);
           const uint2 run = a.runs[r];
@@ -694,10 +710,10 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             const uint32_t len = min(kRecMax, re - p);
             if (CP && len >= kLongMin) {  // long record: walked by one warp (t3_long)
               const uint32_t slot = atomicAdd(&sh_cntl[run.y], 1u);
-              R[(size_t)run.y * RS + (RS - 1 - slot)] = Rec{p, len, o_wv, 0u};
+              R[(size_t)run.y * RS + (RS - 1 - slot)] = Rec{p, len, o_wv, o_e};
             } else {
               const uint32_t slot = atomicAdd(&sh_cnt[run.y], 1u);
-              R[(size_t)run.y * RS + slot] = Rec{p, len, o_wv, 0u};
+              R[(size_t)run.y * RS + slot] = Rec{p, len, o_wv, o_e};
             }
           }
 #ifdef BBF_T3_RECSTAT
@@ -778,7 +794,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
               // 16-bit fields), minus one per wedge for the own class (Lemma 2 shares)
               own = __reduce_add_sync(0xffffffffu, own);
               oth = __reduce_add_sync(0xffffffffu, oth);
-              if (lane == 0 && ((own - rl.len) | oth)) mid_red(a, rmv, rl.wv & kMask, ob + (rl.wv & kMask), own - rl.len, oth);
+              if (lane == 0 && ((own - rl.len) | oth)) mid_red(a, rmv, rl.wv & kMask, ob + (rl.wv & kMask), own - rl.len, oth, rl.e);
             }
           }
         }
@@ -891,7 +907,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           if (pass == 1) {
             __syncwarp();
             const uint32_t cb = sh_acc[warp][0][lane], cn = sh_acc[warp][1][lane];
-            if (cb | cn) mid_red(a, rmv, rc.wv & kMask, ob + (rc.wv & kMask), cb, cn);
+            if (cb | cn) mid_red(a, rmv, rc.wv & kMask, ob + (rc.wv & kMask), cb, cn, rc.e);
             __syncwarp();
           }
         }
@@ -989,7 +1005,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       if (warp == 0) {
         b = warp_sum(lane < kT3Warps ? sh_red[0][lane] : 0ull);
         nn = warp_sum(lane < kT3Warps ? sh_red[1][lane] : 0ull);
-        if (lane == 0 && (b | nn)) {
+        if (lane == 0 && (b | nn) && !a.edge) {
           atomicAdd(&a.pv[2ull * (x)], b);
           atomicAdd(&a.pv[2ull * (x) + 1], nn);
         }
@@ -1129,7 +1145,7 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
         __syncwarp();
         if (pass == 1) {
           uint32_t b2 = sh_mb[lane], n2 = sh_mn[lane];
-          if (b2 | n2) mid_red(a, a.rmid[xu ? 1 : 0], wv & kMask, ob + (wv & kMask), b2, n2);
+          if (b2 | n2) mid_red(a, a.rmid[xu ? 1 : 0], wv & kMask, ob + (wv & kMask), b2, n2, m_lo + cb + lane);
           sh_mb[lane] = 0;
           sh_mn[lane] = 0;
         }
@@ -1331,7 +1347,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
         if (pass == 1) {
           for (uint32_t i = tid; i < mcc; i += kT2Threads) {
             const uint32_t cb = mB[i], cn = mN[i];
-            if (cb | cn) mid_red(a, a.rmid[xu ? 1 : 0], mW[i] & kMask, ob + (mW[i] & kMask), cb, cn);
+            if (cb | cn) mid_red(a, a.rmid[xu ? 1 : 0], mW[i] & kMask, ob + (mW[i] & kMask), cb, cn, 0xffffffffu);  // (per-edge counts never use T2)
           }
           __syncthreads();
         }
@@ -1446,8 +1462,13 @@ cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, P
 bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, int rank,
                            int nranks, unsigned long long* host_BN, unsigned long long* cb,
                            unsigned long long* cn, unsigned long long* cid,
-                           unsigned long long cap, unsigned long long* n_cand, unsigned long long tau) {
+                           unsigned long long cap, unsigned long long* n_cand, unsigned long long tau,
+                           unsigned long long* edge) {
   cudaStream_t st = g->stream;
+  if (edge && (!per_vertex || pairs || p->n_t1 || p->n_t1b || p->n_t2 || p->n_t2s || p->n_t2h)) {
+    set_error("internal: per-edge counts need a per-vertex pass over a hub-tier-only plan");
+    return BBF_ECUDA;
+  }
   // scratch for the hub kernel: per CTA 3 middle arrays + 4 record arrays [window][middle]
   uint32_t kwin_cap = 1;
   for (int s2 = 0; s2 < 2; ++s2)
@@ -1485,6 +1506,8 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   ea.kwin_cap = kwin_cap;
   ea.rec_stride = (uint32_t)(std::max<uint32_t>(p->max_mid, 1) + p->max_work / kRecMax + 1);
   ea.cb = cb; ea.cn = cn; ea.cid = cid; ea.cap = cap; ea.tau = tau;
+  ea.edge = edge;
+  ea.ue = p->route == 3 ? g->rev : nullptr;
   ea.dense_div = getenv("BBF_DENSE_DIV") ? (uint32_t)atoi(getenv("BBF_DENSE_DIV")) : 2u;
   // hub-kernel record batch: 32 amortises the batch set-up when each CTA has a long share of the
   // hub wedges (config 5: -1.3% k_t3), 16 balances the tail of a short one (config 3: 32 is +3%)

@@ -20,10 +20,10 @@ constexpr uint32_t kT1Max = 512;  // starts with at most this many (pruned) wedg
 namespace {
 
 struct RouteRows {
-  int route;  // 0 G, 1 S(U), 2 S(V)
+  int route;  // 0 G, 1 S(U), 2 S(V), 3 S(U) with the ends BEFORE the start (per-edge counts)
   uint32_t n_u, n;
   __device__ __forceinline__ bool in_route(uint32_t x) const {
-    return route == 0 || (route == 1 ? x < n_u : x >= n_u);
+    return route == 0 || (route == 1 || route == 3 ? x < n_u : x >= n_u);
   }
 };
 
@@ -70,12 +70,19 @@ __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
       const uint32_t r = rev[e];
       const uint32_t lo = rr.route == 0 ? mid[x] : off[x];
       if (rr.in_route(x) && e >= lo && e < end1[x]) {
-        const uint32_t f = off[rv + 1];
-        const uint32_t u = r + 1;  // x's entry in its middle's row is the reverse entry
-        const uint32_t en = end1[rv];
-        ub[e] = u;
-        full += f - u;
-        l_seg = en > u ? en - u : 0;
+        if (rr.route == 3) {  // ends before x in N(v): [off(v), r), of degree >= 2
+          const uint32_t u = off[rv], en = min(end1[rv], r);
+          ub[e] = u;
+          full += r - u;
+          l_seg = en > u ? en - u : 0;
+        } else {
+          const uint32_t f = off[rv + 1];
+          const uint32_t u = r + 1;  // x's entry in its middle's row is the reverse entry
+          const uint32_t en = end1[rv];
+          ub[e] = u;
+          full += f - u;
+          l_seg = en > u ? en - u : 0;
+        }
       }
       if (win) {
         const uint32_t o = off[rv], pos = r - o, hi = mid[rv] - o;
@@ -118,7 +125,7 @@ __global__ void k_seg_bounds(RouteRows rr, const uint32_t* __restrict__ off,
 // w_target = max(W_pruned / (nranks * SMs * 6 + 1), 2^16), from the device-side W_pruned (no host
 // round trip between the work reduction and the tiers)
 __global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, const unsigned long long* __restrict__ d_wp,
-                       uint64_t w_div, uint64_t t2max, const uint32_t* __restrict__ mlo,
+                       uint64_t w_div, uint64_t t1max, uint64_t t2max, const uint32_t* __restrict__ mlo,
                        const uint32_t* __restrict__ mhi, uint32_t* __restrict__ nunits,
                        unsigned long long* __restrict__ acc) {
   const uint64_t wt = *d_wp / w_div, w_target = wt > (1ull << 16) ? wt : (1ull << 16);
@@ -127,9 +134,9 @@ __global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, const unsi
   uint32_t u = 0;
   if (x < n) {
     uint64_t w = work[x];
-    if (w > 0 && w <= kT1Max) w1 = w;
-    if (w > kT1Max && w <= t2max) w2 = w;
-    if (w > kT1Max && w > t2max) {
+    if (w > 0 && w <= t1max) w1 = w;
+    if (w > t1max && w <= t2max) w2 = w;
+    if (w > t1max && w > t2max) {
       w3 = w;
       m3 = mhi[x] - mlo[x];
       u = (uint32_t)std::min<uint64_t>((w + w_target - 1) / w_target, 4096);
@@ -163,7 +170,7 @@ struct IsT2 {  // lo < work <= hi
 
 // fill the units of every T3 row: split [l(x)+1, L4) into nunits pieces of ~equal sum of end
 // degrees (expected wedges per end rank are proportional to the end's degree)
-__global__ void k_units(uint32_t n, uint32_t n_u, const uint32_t* __restrict__ nunits,
+__global__ void k_units(int route, uint32_t n, uint32_t n_u, const uint32_t* __restrict__ nunits,
                         const uint32_t* __restrict__ ustart, const uint64_t* __restrict__ degpre,
                         uint32_t L4u, uint32_t L4v, const uint32_t* __restrict__ mid_lo,
                         const uint32_t* __restrict__ end1, const uint64_t* __restrict__ work,
@@ -176,7 +183,8 @@ __global__ void k_units(uint32_t n, uint32_t n_u, const uint32_t* __restrict__ n
   uint32_t sb = x < n_u ? 0 : n_u;
   uint32_t L4 = x < n_u ? L4u : L4v;
   uint32_t lx = x - sb;
-  uint32_t lo = lx + 1, hi = L4 > lo ? L4 : lo;
+  // ends after x (routes G, S) or before x (route 3, per-edge counts), of degree >= 2
+  uint32_t lo = route == 3 ? 0u : lx + 1, hi = route == 3 ? (lx < L4 ? lx : L4) : (L4 > lo ? L4 : lo);
   atomicMax(max_mid, end1[x] - mid_lo[x]);
   atomicMax(max_work, (unsigned long long)work[x]);
   uint32_t base = ustart[x];
@@ -227,7 +235,7 @@ void free_plan(Plan* p, cudaStream_t st) {
   *p = Plan{};
 }
 
-bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
+bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3) {
   cudaStream_t st = g->stream;
   const uint32_t n = g->n;
   const uint64_t m = 2 * g->nnz;
@@ -302,11 +310,13 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
 
   // tiers and units
   // a T2 start's distinct ends (<= its wedges) must fit the k_t2 hash at load <= 1/2
-  const uint64_t t2max = std::min<uint64_t>(
+  // all_t3: every start with work goes to the hub kernel (the per-edge counts need its records)
+  const uint64_t t1max = all_t3 ? 0ull : (uint64_t)kT1Max;
+  const uint64_t t2max = all_t3 ? 0ull : std::min<uint64_t>(
       getenv("BBF_T2_MAX") ? (uint64_t)atoll(getenv("BBF_T2_MAX")) : kT2MaxDefault, kT2HugeSlots * 3 / 4);
   BBF_CUDA(cudaMemsetAsync(acc, 0, 8 * sizeof(unsigned long long), st));
   if (n) {
-    k_tier<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, p->work, d_wp, w_div, t2max, sb, se, nunits, acc);
+    k_tier<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, p->work, d_wp, w_div, t1max, t2max, sb, se, nunits, acc);
     g->launches += 1;
   }
   BBF_CUDA(dmalloc(&p->t1, 4ull * (n + 1), st));
@@ -317,8 +327,8 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   uint32_t* d_nsel;
   BBF_CUDA(dmalloc(&d_nsel, 20, st));
   const uint64_t t2mid = std::min<uint64_t>(kT2SmallMax, t2max), t2big = std::min<uint64_t>(kT2Slots * 3 / 4, t2max);
-  const IsT2 big{p->work, t2mid, t2big}, small{p->work, kT1Max, t2mid}, huge{p->work, t2big, t2max};
-  const IsT2 t1s{p->work, 0, kT1SmallMax}, t1b{p->work, kT1SmallMax, kT1Max};
+  const IsT2 big{p->work, t2mid, t2big}, small{p->work, t1max, std::max(t1max, t2mid)}, huge{p->work, t2big, t2max};
+  const IsT2 t1s{p->work, 0, std::min<uint64_t>(kT1SmallMax, t1max)}, t1b{p->work, std::min<uint64_t>(kT1SmallMax, t1max), t1max};
   {
     cub::CountingInputIterator<uint32_t> it(0);
     size_t tb = 0, tb3 = 0;
@@ -364,7 +374,7 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p) {
   BBF_CUDA(dmalloc(&d_maxmid, 16, st));
   BBF_CUDA(cudaMemsetAsync(d_maxmid, 0, 16, st));
   if (n && h_nunits) {
-    k_units<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(n, g->n_u, nunits, ustart, g->degpre,
+    k_units<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(route, n, g->n_u, nunits, ustart, g->degpre,
                                                       g->L4[0], g->L4[1], sb, g->end1, p->work,
                                                       p->units, d_maxmid, (unsigned long long*)(d_maxmid + 2));
     g->launches += 1;

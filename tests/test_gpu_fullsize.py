@@ -157,3 +157,65 @@ def test_estimate_rejects_malformed_input_before_sampling(bbf):
     with pytest.raises(bbf.BBFError) as e:
         bbf.estimate_global(2, 2, np.array([0, 1, 2], np.uint64), col, np.array([1, 2], np.uint8), 0.5, 2)
     assert e.value.name == "BBF_EINVAL"
+
+
+# ----------------------------------------------------------------------------- NEXT-4 per-edge counts
+@pytest.mark.parametrize("name", ["config1", "config2", "kmn", "sweep2", "sweep7", "sweep8", "skewed", "zoned"])
+def test_per_edge_counts_vs_oracle(bbf, name):
+    """bbf_count_per_edge equals the oracle's per-edge definition edge by edge,
+    in the caller's CSR order; totals equal Alg. 2's; each vertex's edges sum to twice its count."""
+    from test_gpu_parity import _sweep_graph, zoned_graph
+    g = {"config1": G.config1, "config2": G.config2, "kmn": lambda: G.complete(37, 23),
+         "sweep2": lambda: _sweep_graph(2), "sweep7": lambda: _sweep_graph(7), "sweep8": lambda: _sweep_graph(8),
+         "skewed": lambda: G.random_bipartite(10, 1000, 0.5, 0.5, seed=7), "zoned": zoned_graph}[name]()
+    with bbf.Graph.from_synth(g) as h:
+        tot, eb, en = h.count_per_edge(g.row_ptr, g.col)
+        _, bu, nu, bv, nv = h.count_per_vertex()
+    if name == "zoned":  # too large for the oracle's edge-by-edge definition: identities + brute-free pins
+        u = np.repeat(np.arange(g.n_u), np.diff(g.row_ptr.astype(np.int64)))
+        assert int(eb.astype(object).sum()) == 4 * tot["balanced"] and int(en.astype(object).sum()) == 4 * tot["unbalanced"]
+        su = np.zeros(g.n_u, dtype=object)
+        np.add.at(su, u, eb.astype(object))
+        assert np.array_equal(su.astype(np.uint64), 2 * bu)
+        return
+    wb, wn = O.edge_counts(g, threads=THREADS)
+    assert np.array_equal(eb, wb) and np.array_equal(en, wn)
+    rg = O.route_g(g, threads=THREADS)
+    assert (tot["balanced"], tot["unbalanced"]) == (rg["B"], rg["N"])
+
+
+def test_per_edge_fake_world_shards(bbf, monkeypatch):
+    """Per-edge counts sharded over 3 fake ranks sum to the single-GPU arrays."""
+    from test_gpu_parity import _sweep_graph
+    g = _sweep_graph(8)
+    with bbf.Graph.from_synth(g) as h:
+        _, eb, en = h.count_per_edge(g.row_ptr, g.col)
+    sb = np.zeros(g.nnz, dtype=object)
+    sn = np.zeros(g.nnz, dtype=object)
+    for r in range(3):
+        monkeypatch.setenv("BBF_FAKE_WORLD", f"{r}/3")
+        with bbf.Graph.from_synth(g) as h:
+            _, pb, pn = h.count_per_edge(g.row_ptr, g.col)
+        sb += pb.astype(object)
+        sn += pn.astype(object)
+    monkeypatch.delenv("BBF_FAKE_WORLD")
+    assert np.array_equal(sb.astype(np.uint64), eb) and np.array_equal(sn.astype(np.uint64), en)
+
+
+def test_per_edge_rejects_foreign_csr(bbf):
+    """A CSR that is not the loaded graph's edge set (other edge count, or the same count with
+    other edges) is rejected with BBF_EINVAL; the graph's edges in another order are accepted."""
+    g = G.config1()
+    other = G.random_bipartite(200, 150, 0.05, 0.5, seed=99)
+    u, v, s = g.edges()
+    same_n = G.from_edges(200, 150, u, v[::-1].copy(), s, check_dup=False)  # 2,000 edges, mostly not g's
+    with bbf.Graph.from_synth(g) as h:
+        for bad in (other, same_n):
+            with pytest.raises(bbf.BBFError) as e:
+                h.count_per_edge(bad.row_ptr, bad.col)
+            assert e.value.name == "BBF_EINVAL"
+        _, eb, en = h.count_per_edge(g.row_ptr, g.col)
+        perm = np.concatenate([np.arange(a, b)[::-1] for a, b in zip(g.row_ptr[:-1].astype(np.int64),
+                                                                      g.row_ptr[1:].astype(np.int64))])
+        _, pb, pn = h.count_per_edge(g.row_ptr, g.col[perm])  # rows reversed: same edges, other order
+    assert np.array_equal(pb, eb[perm]) and np.array_equal(pn, en[perm])
