@@ -190,7 +190,7 @@ def check_parity(g, config: int, tot: dict, pv) -> dict:
 
 def cpu_baseline(g, pv=None, single_thread_configs=(1, 2, 3)):
     """The oracle as it stands (oracle/bbf_oracle.c oracle_route_g_pv: Alg. 2 / ParBB-Bucket with
-    the 4-role scatter, dynamic start chunks over all host threads) on the WHOLE graph — global
+    the 4-role scatter, dynamic chunks of 4 starts over all host threads) on the WHOLE graph — global
     and per-vertex counts, the same outputs as the GPU step.  value = W_G / its counting-loop time.
     When `pv` (the GPU's per-vertex arrays) is given, they are compared with the oracle's element
     by element in this same run (raises on a mismatch).  Also the single-thread Alg. 2 time
@@ -221,8 +221,8 @@ def cpu_baseline(g, pv=None, single_thread_configs=(1, 2, 3)):
 def reference_arm(args):
     """--impl reference: the CPU oracle as it stands (oracle_route_g_pv, all host threads), on this
     arm's config/metric.  Step i counts start slice i of W+K deterministic disjoint slices (start x
-    in slice x mod (W+K)), so the whole run is one full pass over the graph and every timed step
-    is a bounded, reproducible sample of it."""
+    in slice x mod (W+K)), so the whole run is one full pass over the graph and every timed step is
+    a bounded, reproducible sample of it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0

@@ -193,7 +193,7 @@ typedef struct {
   int rc;
 } rg_task;
 
-#define ORACLE_CHUNK 64u
+#define ORACLE_CHUNK 4u  /* small chunks: the hubs (low ids of the Chung-Lu configs) spread over the threads */
 
 static const graph_t *g_sort_graph;  /* qsort context for line 3 of Alg. 2 */
 static int cmp_by_prio(const void *a, const void *b) {
@@ -330,6 +330,7 @@ typedef struct {
   int tid, nthreads;
   uint64_t *bal, *unb;
   uint64_t *cursor;
+  uint32_t *B1, *B2, *touched;  /* per-thread buckets, zeroed, allocated before the clock starts */
   u128 B, N, W;
   int rc;
 } rgpv_task;
@@ -337,10 +338,7 @@ typedef struct {
 static void *route_g_pv_worker(void *arg) {
   rgpv_task *t = (rgpv_task *)arg;
   const graph_t *g = t->g;
-  uint32_t *B1 = (uint32_t *)calloc((size_t)g->n + 1, sizeof(uint32_t));
-  uint32_t *B2 = (uint32_t *)calloc((size_t)g->n + 1, sizeof(uint32_t));
-  uint32_t *touched = (uint32_t *)malloc(sizeof(uint32_t) * ((size_t)g->n + 1));
-  if (!B1 || !B2 || !touched) { t->rc = 4; free(B1); free(B2); free(touched); return NULL; }
+  uint32_t *B1 = t->B1, *B2 = t->B2, *touched = t->touched;
   uint64_t total = t->starts ? t->n_starts : g->n;
   for (uint64_t i = 0, lim = 0;; ++i) {
     if (i == lim) {
@@ -394,7 +392,6 @@ static void *route_g_pv_worker(void *arg) {
     __atomic_fetch_add(&t->bal[u], (uint64_t)bu, __ATOMIC_RELAXED);
     __atomic_fetch_add(&t->unb[u], (uint64_t)nu, __ATOMIC_RELAXED);
   }
-  free(B1); free(B2); free(touched);
   return NULL;
 }
 
@@ -431,6 +428,18 @@ int oracle_route_g_pv_h(void *h, const uint32_t *starts, uint64_t n_starts, int 
   if (nthreads < 1) nthreads = 1;
   rgpv_task *tasks = (rgpv_task *)calloc((size_t)nthreads, sizeof(rgpv_task));
   pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+  int oom = !tasks || !th;
+  for (int i = 0; i < nthreads && !oom; ++i) {  /* buckets allocated (and zeroed) before the clock */
+    tasks[i].B1 = (uint32_t *)calloc((size_t)g.n + 1, sizeof(uint32_t));
+    tasks[i].B2 = (uint32_t *)calloc((size_t)g.n + 1, sizeof(uint32_t));
+    tasks[i].touched = (uint32_t *)malloc(sizeof(uint32_t) * ((size_t)g.n + 1));
+    oom = !tasks[i].B1 || !tasks[i].B2 || !tasks[i].touched;
+  }
+  if (oom) {
+    for (int i = 0; tasks && i < nthreads; ++i) { free(tasks[i].B1); free(tasks[i].B2); free(tasks[i].touched); }
+    free(tasks); free(th);
+    return 4;
+  }
   uint64_t cursor = 0;
   struct timespec t0, t1;
   clock_gettime(CLOCK_MONOTONIC, &t0);
@@ -448,6 +457,7 @@ int oracle_route_g_pv_h(void *h, const uint32_t *starts, uint64_t n_starts, int 
     if (tasks[i].rc) rc = tasks[i].rc;
   }
   clock_gettime(CLOCK_MONOTONIC, &t1);
+  for (int i = 0; i < nthreads; ++i) { free(tasks[i].B1); free(tasks[i].B2); free(tasks[i].touched); }
   free(tasks); free(th);
   if (rc) return rc;
   if (B >> 64 || N >> 64 || W >> 64) return 7;
