@@ -196,6 +196,13 @@ struct Plan {
   uint32_t* t2s;       // rows with kT1Max < work <= kT2SmallMax (k_t2, half-size CTA)
   uint32_t* t2h;       // rows with kT2Slots * 3/4 < work <= T2 max (k_t2, 1024 threads, kT2HugeSlots)
   Unit* units;         // T3 units
+  // split hubs: for every boundary between two units of one start, the cut position of each of its
+  // middles' end segments (the first entry with rank >= the boundary), computed once in parallel
+  // (k_split_cuts) instead of two binary searches per middle in every unit's pre-scan;
+  // unit_cut[2i], unit_cut[2i + 1] = offsets of unit i's lower / upper cut array (~0 = none)
+  uint32_t* cut_tab;
+  unsigned long long* unit_cut;
+
   uint32_t n_t1, n_t1b, n_t2, n_t2s, n_t2h, n_units;
   uint32_t max_mid;    // max middles of a T3 start
   unsigned long long max_work;  // max wedges of a T3 start

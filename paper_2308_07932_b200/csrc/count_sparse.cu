@@ -53,6 +53,9 @@ struct EngineArgs {
   const uint32_t* t1;
   const uint32_t* t2;    // the T2 starts of one k_t2 instance
   const Unit* units;
+  const uint32_t* cut_tab;               // split starts: precomputed segment cuts (plan.cu k_split_cuts)
+
+  const unsigned long long* unit_cut;    // per unit: offsets of its lower / upper cut arrays
   uint32_t n_t1, n_t2, n_units;
   uint32_t t2ctr;        // acc index of that instance's start cursor
   uint32_t t1ctr;        // acc index of the k_t1 instance's start cursor
@@ -668,7 +671,11 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
         en = a.end1[ob + (wv & kMask)];
         if (a.ue) en = min(en, a.ue[e]);  // route 3: the ends before x's own entry of N(v)
         rl = a.rlast[ob + (wv & kMask)];  // same level as end1: no dependent runid[en - 1] load
-        if (split_lo && s < en) {
+        const unsigned long long clo = a.unit_cut ? a.unit_cut[2ull * ui] : ~0ull;
+        const unsigned long long chi = a.unit_cut ? a.unit_cut[2ull * ui + 1] : ~0ull;
+        if (split_lo && clo != ~0ull) {
+          s = max(s, a.cut_tab[clo + i]);
+        } else if (split_lo && s < en) {
           uint32_t b = s, f = en;
           while (b < f) {
             uint32_t md = b + (f - b) / 2;
@@ -676,7 +683,9 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           }
           s = b;
         }
-        if (split_hi && s < en) {
+        if (split_hi && chi != ~0ull) {
+          en = min(en, a.cut_tab[chi + i]);
+        } else if (split_hi && s < en) {
           uint32_t b = s, f = en;
           while (b < f) {
             uint32_t md = b + (f - b) / 2;
@@ -1492,6 +1501,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
   ea.rlast = g->rlast;
   ea.nruns = g->nruns; ea.mid = p->route == 0 ? g->mid : nullptr; ea.end1 = g->end1;
   ea.ub = p->ub; ea.work = p->work; ea.inv = g->inv; ea.t1 = p->t1; ea.t2 = p->t2; ea.units = p->units;
+  ea.cut_tab = p->cut_tab; ea.unit_cut = p->cut_tab ? p->unit_cut : nullptr;
   ea.n_t1 = p->n_t1; ea.n_t2 = p->n_t2; ea.n_units = p->n_units; ea.n_u = g->n_u; ea.n = g->n;
   ea.z[0] = g->zones[0]; ea.z[1] = g->zones[1];
   ea.rank = rank; ea.nranks = nranks;

@@ -215,6 +215,33 @@ __global__ void k_units(int route, uint32_t n, uint32_t n_u, const uint32_t* __r
   }
 }
 
+// one CTA per boundary between two units of a split start: for each middle entry of the start, the
+// first entry of its end segment [ub, en) with rank >= the boundary (the search the hub kernel's
+// pre-scan would otherwise repeat in both units)
+struct CutDesc {
+  uint32_t x, cut;
+  unsigned long long off;
+};
+__global__ void k_split_cuts(const CutDesc* __restrict__ d, const uint32_t* __restrict__ mid_lo,
+                             const uint32_t* __restrict__ end1, const uint32_t* __restrict__ adj,
+                             const uint32_t* __restrict__ ub, const uint32_t* __restrict__ ue, uint32_t n_u,
+                             uint32_t* __restrict__ tab) {
+  const CutDesc c = d[blockIdx.x];
+  const uint32_t ob = c.x < n_u ? n_u : 0;
+  const uint32_t m_lo = mid_lo[c.x], m = end1[c.x] - m_lo;
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const uint32_t e = m_lo + i;
+    const uint32_t v = adj[e] & kMask;
+    uint32_t b = ub[e], f = end1[ob + v];
+    if (ue) f = min(f, ue[e]);
+    while (b < f) {
+      const uint32_t md = b + (f - b) / 2;
+      if ((adj[md] & kMask) < c.cut) b = md + 1; else f = md;
+    }
+    tab[c.off + i] = b;
+  }
+}
+
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {
   uint64_t g = (n + block - 1) / block;
   if (g == 0) g = 1;
@@ -232,6 +259,9 @@ void free_plan(Plan* p, cudaStream_t st) {
   if (p->t1b) dfree(p->t1b, st);
   if (p->t2h) dfree(p->t2h, st);
   if (p->units) dfree(p->units, st);
+  if (p->cut_tab) dfree(p->cut_tab, st);
+  if (p->unit_cut) dfree(p->unit_cut, st);
+
   *p = Plan{};
 }
 
@@ -301,6 +331,7 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3) {
   // so a rank's largest unit stays well below its per-SM work at any N
   int shard_rank = 0, shard_n = 1;
   shard_of(g, &shard_rank, &shard_n);
+  (void)shard_rank;  // every rank builds the same plan
   p->nranks = shard_n;
   const uint64_t nranks = (uint64_t)shard_n;
   // hub units of ~1/3 of an SM share (BBF_UNIT_DIV tunes it; 3 measured best at N = 1 and 8:
@@ -384,6 +415,41 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3) {
   BBF_CUDA(rb_sync(st));
   p->max_mid = h_maxmid[0];
   p->max_work = *(unsigned long long*)(h_maxmid + 2);
+  // cut tables of the split starts (consecutive units of one start share a boundary)
+  if (h_nunits > 1) {
+    std::vector<Unit> hu(h_nunits);
+    BBF_CUDA(cudaMemcpyAsync(hu.data(), p->units, sizeof(Unit) * h_nunits, cudaMemcpyDeviceToHost, st));
+    std::vector<CutDesc> cd;
+    std::vector<unsigned long long> uc(2ull * h_nunits, ~0ull);
+    BBF_CUDA(cudaStreamSynchronize(st));
+    bool any = false;
+    for (uint32_t i = 0; i + 1 < h_nunits; ++i) any |= hu[i].x == hu[i + 1].x;
+    if (any) {
+      std::vector<uint32_t> hlo(n), hend1(n);
+      BBF_CUDA(cudaMemcpyAsync(hlo.data(), sb, 4ull * n, cudaMemcpyDeviceToHost, st));
+      BBF_CUDA(cudaMemcpyAsync(hend1.data(), g->end1, 4ull * n, cudaMemcpyDeviceToHost, st));
+      BBF_CUDA(cudaStreamSynchronize(st));
+      unsigned long long off = 0;
+      for (uint32_t i = 0; i + 1 < h_nunits; ++i) {
+        if (hu[i].x != hu[i + 1].x) continue;
+        const uint32_t x = hu[i].x, m = hend1[x] > hlo[x] ? hend1[x] - hlo[x] : 0;
+        cd.push_back(CutDesc{x, hu[i].hi, off});
+        uc[2ull * i + 1] = off;  // unit i's upper cut, unit i + 1's lower cut
+        uc[2ull * (i + 1)] = off;
+        off += m;
+      }
+      BBF_CUDA(dmalloc(&p->cut_tab, 4ull * (off + 1), st));
+      BBF_CUDA(dmalloc(&p->unit_cut, 8ull * uc.size(), st));
+      CutDesc* dcd;
+      BBF_CUDA(dmalloc(&dcd, sizeof(CutDesc) * cd.size(), st));
+      BBF_CUDA(cudaMemcpyAsync(dcd, cd.data(), sizeof(CutDesc) * cd.size(), cudaMemcpyHostToDevice, st));
+      BBF_CUDA(cudaMemcpyAsync(p->unit_cut, uc.data(), 8ull * uc.size(), cudaMemcpyHostToDevice, st));
+      k_split_cuts<<<(unsigned)cd.size(), 256, 0, st>>>(dcd, sb, g->end1, g->adj, p->ub, route == 3 ? g->rev : nullptr,
+                                                        g->n_u, p->cut_tab);
+      g->launches += 1;
+      dfree(dcd, st);
+    }
+  }
   if (getenv("BBF_DEBUG") && atoi(getenv("BBF_DEBUG")) >= 2) {  // work histogram by log2 bucket
     std::vector<uint64_t> hw(n);
     cudaMemcpy(hw.data(), p->work, 8ull * n, cudaMemcpyDeviceToHost);
