@@ -32,10 +32,17 @@ __global__ void k_validate_edges(const uint32_t* __restrict__ col, const uint8_t
   if (bad) atomicOr(err, bad);
 }
 
-// degree keys: key = deg << 32 | gid  (gid: U -> u, V -> n_u + v)
-__global__ void k_keys_u(const uint64_t* __restrict__ rp, uint32_t n_u, uint64_t* __restrict__ key) {
+// priority sort items (Def. Vertex Priority: degree desc, then gid desc; gid: U -> u, V -> n_u + v,
+// SPEC.md:100): the degree is the key, the gid the value, written in DESCENDING gid order so the
+// stable radix sort by degree keeps equal degrees in descending gid order — a sort over the
+// degree bits only instead of 64-bit (deg << 32 | gid) keys
+__global__ void k_keys_u(const uint64_t* __restrict__ rp, uint32_t n_u, uint32_t* __restrict__ kdeg,
+                         uint32_t* __restrict__ kid) {
   uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u < n_u) key[u] = ((rp[u + 1] - rp[u]) << 32) | u;
+  if (u < n_u) {
+    kdeg[n_u - 1 - u] = (uint32_t)(rp[u + 1] - rp[u]);
+    kid[n_u - 1 - u] = u;
+  }
 }
 
 // V-side degrees.  Hub columns of a power-law graph serialise plain global atomics on their
@@ -90,21 +97,25 @@ __global__ void __launch_bounds__(kHistThreads) k_hist_v_direct(const uint32_t* 
 }
 
 __global__ void k_keys_v(const uint32_t* __restrict__ dv, uint32_t n_u, uint32_t n_v,
-                         uint64_t* __restrict__ key) {
+                         uint32_t* __restrict__ kdeg, uint32_t* __restrict__ kid) {
   uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v < n_v) key[v] = ((uint64_t)dv[v] << 32) | (uint64_t)(n_u + v);
+  if (v < n_v) {
+    kdeg[n_v - 1 - v] = dv[v];
+    kid[n_v - 1 - v] = n_u + v;
+  }
 }
 
-// sorted (descending) keys -> row tables: inv (row -> input id), degs, lr (input id -> local rank)
-__global__ void k_rank_tables(const uint64_t* __restrict__ skey, uint32_t cnt, uint32_t id_base,
-                              uint32_t row_base, uint32_t* __restrict__ inv,
-                              uint32_t* __restrict__ degs, uint32_t* __restrict__ lr) {
+// sorted (degree desc, gid desc) items -> row tables: the priority key skey (deg << 32 | gid, for
+// cross-side comparisons), inv (row -> input id), degs, lr (input id -> local rank)
+__global__ void k_rank_tables(const uint32_t* __restrict__ sdeg, const uint32_t* __restrict__ sid, uint32_t cnt,
+                              uint32_t id_base, uint32_t row_base, uint64_t* __restrict__ skey,
+                              uint32_t* __restrict__ inv, uint32_t* __restrict__ degs, uint32_t* __restrict__ lr) {
   uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= cnt) return;
-  uint64_t k = skey[l];
-  uint32_t id = (uint32_t)(k & 0xffffffffu) - id_base;
+  const uint32_t d = sdeg[l], gid = sid[l], id = gid - id_base;
+  skey[l] = ((uint64_t)d << 32) | gid;
   inv[row_base + l] = id;
-  degs[row_base + l] = (uint32_t)(k >> 32);
+  degs[row_base + l] = d;
   lr[id] = l;
 }
 
@@ -365,6 +376,15 @@ __global__ void __launch_bounds__(1024) k_wg_m_direct(const uint64_t* __restrict
     if (vcnt[i]) atomicAdd(&mcnt[n_u + i], vcnt[i]);
 }
 
+// priority keys by input id (deg << 32 | gid) for the load-time W_G pass of a dense candidate
+__global__ void k_keys64(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ dv, uint32_t n_u, uint32_t n,
+                         uint64_t* __restrict__ key) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t d = i < n_u ? rp[i + 1] - rp[i] : (uint64_t)dv[i - n_u];
+  key[i] = (d << 32) | i;
+}
+
 __global__ void k_wg_sum(const uint32_t* __restrict__ mcnt, const uint64_t* __restrict__ key_u,
                          const uint64_t* __restrict__ key_v, uint32_t n_u, uint32_t n,
                          unsigned long long* __restrict__ out) {
@@ -485,15 +505,18 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   }
 
   // S2-S3: degrees and per-side priority ranks
-  uint64_t *key_u, *key_v;
+  uint32_t *key_u, *key_v;  // per side: degrees [0, cnt), gids [cnt, 2 cnt); sorted copies likewise
+  uint32_t *skd_u, *skd_v;
   uint32_t* dv;
   BBF_CUDA(dmalloc(&key_u, 8ull * (n_u + 1), st));
   BBF_CUDA(dmalloc(&key_v, 8ull * (n_v + 1), st));
+  BBF_CUDA(dmalloc(&skd_u, 8ull * (n_u + 1), st));
+  BBF_CUDA(dmalloc(&skd_v, 8ull * (n_v + 1), st));
   BBF_CUDA(dmalloc(&g->skey, 8ull * (n + 1), st));
   BBF_CUDA(dmalloc(&dv, 4ull * (n_v + 1), st));
   BBF_CUDA(dmalloc(&g->lr, 4ull * (n + 1), st));
   BBF_CUDA(cudaMemsetAsync(dv, 0, 4ull * (n_v + 1), st));
-  if (n_u) k_keys_u<<<grid_for(n_u, 256, 1u << 30), 256, 0, st>>>(d_rp, n_u, key_u);
+  if (n_u) k_keys_u<<<grid_for(n_u, 256, 1u << 30), 256, 0, st>>>(d_rp, n_u, key_u, key_u + n_u);
   if (nnz) {
     const uint64_t chunks = (nnz + kHistChunk - 1) / kHistChunk;
     if (n_v <= kHistDirectMax) {
@@ -506,7 +529,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
       k_hist_v<<<(unsigned)std::min<uint64_t>(chunks, 2ull * g->num_sms), kHistThreads, 0, st>>>(d_col, nnz, dv);
     }
   }
-  if (n_v) k_keys_v<<<grid_for(n_v, 256, 1u << 30), 256, 0, st>>>(dv, n_u, n_v, key_v);
+  if (n_v) k_keys_v<<<grid_for(n_v, 256, 1u << 30), 256, 0, st>>>(dv, n_u, n_v, key_v, key_v + n_v);
   g->launches += 3;
   uint64_t* skey_u = g->skey;
   uint64_t* skey_v = g->skey + n_u;
@@ -514,22 +537,29 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   uint32_t* lr_v = g->lr + n_u;
 
   size_t tmp_bytes = 0, t1 = 0, t2 = 0, t4 = 0;
-  int kbits = std::min(64, 32 + bits_for(std::max<uint64_t>(nnz, 1)));  // deg < 2^31
-  cub::DeviceRadixSort::SortKeysDescending(nullptr, t1, key_u, skey_u, (int)n_u, 0, kbits, st);
-  cub::DeviceRadixSort::SortKeysDescending(nullptr, t2, key_v, skey_v, (int)n_v, 0, kbits, st);
+  const int kbits = bits_for(std::max<uint64_t>(nnz, 1));  // degree <= nnz
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, t1, key_u, skd_u, key_u + n_u, skd_u + n_u, (int)n_u, 0, kbits, st);
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, t2, key_v, skd_v, key_v + n_v, skd_v + n_v, (int)n_v, 0, kbits, st);
   cub::DeviceScan::ExclusiveSum(nullptr, t4, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)(n + 1), st);
   tmp_bytes = std::max(std::max(t1, t2), t4);
   void* tmp;
   BBF_CUDA(dmalloc(&tmp, tmp_bytes + 16, st));
-  if (n_u) BBF_CUDA(cub::DeviceRadixSort::SortKeysDescending(tmp, t1, key_u, skey_u, (int)n_u, 0, kbits, st));
-  if (n_v) BBF_CUDA(cub::DeviceRadixSort::SortKeysDescending(tmp, t2, key_v, skey_v, (int)n_v, 0, kbits, st));
+  if (n_u)
+    BBF_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, t1, key_u, skd_u, key_u + n_u, skd_u + n_u, (int)n_u, 0,
+                                                        kbits, st));
+  if (n_v)
+    BBF_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, t2, key_v, skd_v, key_v + n_v, skd_v + n_v, (int)n_v, 0,
+                                                        kbits, st));
   g->launches += (n_u ? cub_sort_kernels(kbits) : 0) + (n_v ? cub_sort_kernels(kbits) : 0);
 
   BBF_CUDA(dmalloc(&g->inv, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&g->degs, 4ull * (n + 1), st));
   BBF_CUDA(dmalloc(&g->off, 4ull * (n + 1), st));
-  if (n_u) k_rank_tables<<<grid_for(n_u, 256, 1u << 30), 256, 0, st>>>(skey_u, n_u, 0, 0, g->inv, g->degs, lr_u);
-  if (n_v) k_rank_tables<<<grid_for(n_v, 256, 1u << 30), 256, 0, st>>>(skey_v, n_v, n_u, n_u, g->inv, g->degs, lr_v);
+  if (n_u)
+    k_rank_tables<<<grid_for(n_u, 256, 1u << 30), 256, 0, st>>>(skd_u, skd_u + n_u, n_u, 0, 0, skey_u, g->inv, g->degs, lr_u);
+  if (n_v)
+    k_rank_tables<<<grid_for(n_v, 256, 1u << 30), 256, 0, st>>>(skd_v, skd_v + n_v, n_v, n_u, n_u, skey_v, g->inv, g->degs,
+                                                                 lr_v);
   g->launches += 2;
   // row offsets: exclusive scan of degrees in row order (rows U by rank, then V by rank)
   BBF_CUDA(cudaMemsetAsync(g->degs + n, 0, 4, st));
@@ -578,6 +608,12 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
   if (dense_supported(g) && !(g->load_flags & BBF_FORCE_SPARSE)) {
     uint32_t* mcnt;
     unsigned long long* d_wg;
+    uint64_t* key64;  // by input id: U keys [0, n_u), V keys [n_u, n)
+    BBF_CUDA(dmalloc(&key64, 8ull * (n + 1), st));
+    k_keys64<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(d_rp, dv, n_u, n, key64);
+    g->launches += 1;
+    const uint64_t* kk_u = key64;
+    const uint64_t* kk_v = key64 + n_u;
     BBF_CUDA(dmalloc(&mcnt, 4ull * (n + 1), st));
     BBF_CUDA(dmalloc(&d_wg, 8, st));
     BBF_CUDA(cudaMemsetAsync(mcnt, 0, 4ull * (n + 1), st));
@@ -587,23 +623,26 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
       if (smem > 48 * 1024)
         BBF_CUDA(cudaFuncSetAttribute(k_wg_m_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       k_wg_m_direct<<<(unsigned)std::min<uint64_t>((n_u + 31) / 32, g->num_sms), 1024, smem, st>>>(
-          d_rp, d_col, n_u, n_v, key_u, key_v, mcnt);
+          d_rp, d_col, n_u, n_v, kk_u, kk_v, mcnt);
     } else if (n_u) {
-      k_wg_m<<<grid_for(32ull * n_u, 256), 256, 0, st>>>(d_rp, d_col, n_u, key_u, key_v, mcnt);
+      k_wg_m<<<grid_for(32ull * n_u, 256), 256, 0, st>>>(d_rp, d_col, n_u, kk_u, kk_v, mcnt);
     }
-    if (n) k_wg_sum<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(mcnt, key_u, key_v, n_u, n, d_wg);
+    if (n) k_wg_sum<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(mcnt, kk_u, kk_v, n_u, n, d_wg);
     g->launches += 2;
     unsigned long long wg = 0;
     BBF_CUDA(rb_add(&wg, d_wg, 8, st)); g->launches++;
     BBF_CUDA(rb_sync(st));
     dfree(mcnt, st);
     dfree(d_wg, st);
+    dfree(key64, st);
     g->W_G = wg;
     g->wg_valid = true;
     dense_load = (g->load_flags & BBF_FORCE_DENSE) || dense_preferred(g, true);
   }
   dfree(key_u, st);
   dfree(key_v, st);
+  dfree(skd_u, st);
+  dfree(skd_v, st);
   dfree(dv, st);
 
   if (dense_load) {
