@@ -215,7 +215,10 @@ constexpr int kU = BBF_T3_KU;  // flattened steps per iteration of the hub kerne
 #ifndef BBF_T3_CE
 #define BBF_T3_CE 8
 #endif
-constexpr uint32_t kCE = BBF_T3_CE;  // adjacency entries per lane per step (16-B aligned chunks)
+constexpr uint32_t kCE = BBF_T3_CE;
+#ifndef BBF_T3_BMIN
+#define BBF_T3_BMIN 12
+#endif  // adjacency entries per lane per step (16-B aligned chunks)
 constexpr int kEncWide = 0, kEncNarrow = 1, kEncCompact = 2;  // adjc encodings
 constexpr uint32_t kMaxWin = 256;
 
@@ -816,7 +819,7 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           if (lane == 0) {
             const uint32_t seen = *reinterpret_cast<volatile uint32_t*>(&sh_c[pass]);
             const uint32_t rem = seen < nrec ? nrec - seen : 0u;
-            const uint32_t sz = min(bsz, max(12u, rem / kT3Warps));
+            const uint32_t sz = min(bsz, max((uint32_t)BBF_T3_BMIN, rem / kT3Warps));
             s0 = atomicAdd(&sh_c[pass], sz);
             c0 = s0 < nrec ? min(sz, nrec - s0) : 0u;
           }
