@@ -560,6 +560,13 @@ __device__ __forceinline__ void t3_long4(const uint4& q, uint32_t vm4, uint32_t 
       uint32_t v = sh_load(addr);
       if (MASKED) v = on ? v : 0u;
       const uint32_t h = 2u << (ev[j] & 3u);
+#ifdef BBF_T3_RECSTAT  // pass-2 entries of long records, and those whose end has a + d >= 2
+      {
+        const uint32_t o1 = zext(shr_wrap(v, ev[j] >> shamt), h), o2 = zext(shr_wrap(v, ev[j] >> oshamt), h);
+        const uint32_t n_on = __popc(__ballot_sync(0xffffffffu, on)), n_use = __popc(__ballot_sync(0xffffffffu, on && o1 + o2 >= 2));
+        if ((threadIdx.x & 31) == 0) { T3_COUNT(20, n_on); T3_COUNT(21, n_use); }
+      }
+#endif
       own += zext(shr_wrap(v, ev[j] >> shamt), h);
       oth += zext(shr_wrap(v, ev[j] >> oshamt), h);
     } else {
@@ -1616,6 +1623,8 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
             "(fill %.3f) short<8 %llu, entries in records<64 %llu; wedges dense %llu bitmap %llu\n",
             pc[10], pc[0], pc[1], pc[0] / (64.0 * pc[1] + 1e-9), pc[2], pc[0] / (32.0 * pc[2] + 1e-9), pc[3],
             pc[0] / (16.0 * pc[3] + 1e-9), pc[4], pc[5], pc[6], pc[7]);
+    fprintf(stderr, "[bbf] t3 pass-2 long-record entries %llu, with a + d >= 2 at the end: %llu (%.3f)\n", pc[20], pc[21],
+            pc[21] / (pc[20] + 1e-9));
     fprintf(stderr, "[bbf] t3 entries by run length: <8 %.3f <32 %.3f <128 %.3f <512 %.3f >=512 %.3f\n",
             pc[11] / (double)pc[0], pc[12] / (double)pc[0], pc[13] / (double)pc[0], pc[14] / (double)pc[0],
             pc[15] / (double)pc[0]);
