@@ -130,7 +130,7 @@ __global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, const unsi
                        unsigned long long* __restrict__ acc) {
   const uint64_t wt = *d_wp / w_div, w_target = wt > (1ull << 16) ? wt : (1ull << 16);
   uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long w1 = 0, w3 = 0, m3 = 0, w2 = 0;
+  unsigned long long w1 = 0, w3 = 0, m3 = 0, w2 = 0, s3 = 0;  // s3: starts with hub units
   uint32_t u = 0;
   if (x < n) {
     uint64_t w = work[x];
@@ -140,6 +140,7 @@ __global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, const unsi
       w3 = w;
       m3 = mhi[x] - mlo[x];
       u = (uint32_t)std::min<uint64_t>((w + w_target - 1) / w_target, 4096);
+      s3 = 1;
     }
     nunits[x] = u;
   }
@@ -148,12 +149,14 @@ __global__ void k_tier(uint32_t n, const uint64_t* __restrict__ work, const unsi
     w3 += __shfl_xor_sync(0xffffffffu, w3, o);
     m3 += __shfl_xor_sync(0xffffffffu, m3, o);
     w2 += __shfl_xor_sync(0xffffffffu, w2, o);
+    s3 += __shfl_xor_sync(0xffffffffu, s3, o);
   }
   if ((threadIdx.x & 31) == 0) {
     if (w1) atomicAdd(&acc[0], w1);
     if (w3) atomicAdd(&acc[1], w3);
     if (m3) atomicAdd(&acc[2], m3);
     if (w2) atomicAdd(&acc[3], w2);
+    if (s3) atomicAdd(&acc[4], s3);
   }
 }
 
@@ -213,6 +216,13 @@ __global__ void k_units(int route, uint32_t n, uint32_t n_u, const uint32_t* __r
     units[base + j] = Unit{x, prev, cut, 0};
     prev = cut;
   }
+}
+
+// middle counts of the listed starts (the split starts' boundaries)
+__global__ void k_gather_m(const uint32_t* __restrict__ xs, uint32_t cnt, const uint32_t* __restrict__ mid_lo,
+                           const uint32_t* __restrict__ end1, uint32_t* __restrict__ m) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) m[i] = end1[xs[i]] > mid_lo[xs[i]] ? end1[xs[i]] - mid_lo[xs[i]] : 0u;
 }
 
 // one CTA per boundary between two units of a split start: for each middle entry of the start, the
@@ -381,10 +391,10 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3) {
     dfree(tmp, st);
   }
   uint32_t h_nsel[5] = {0, 0, 0, 0, 0}, h_nunits = 0;
-  unsigned long long h_acc[4];
+  unsigned long long h_acc[5];
   BBF_CUDA(rb_add(h_nsel, d_nsel, 20, st)); g->launches++;
   BBF_CUDA(rb_add(&h_nunits, ustart + n, 4, st)); g->launches++;
-  BBF_CUDA(rb_add(h_acc, acc, 32, st)); g->launches++;
+  BBF_CUDA(rb_add(h_acc, acc, 40, st)); g->launches++;
   BBF_CUDA(rb_sync(st));
   p->W_pruned = h_wp;
   p->W_full = h_wf;
@@ -415,8 +425,9 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3) {
   BBF_CUDA(rb_sync(st));
   p->max_mid = h_maxmid[0];
   p->max_work = *(unsigned long long*)(h_maxmid + 2);
-  // cut tables of the split starts (consecutive units of one start share a boundary)
-  if (h_nunits > 1) {
+  // cut tables of the split starts (consecutive units of one start share a boundary), when some
+  // start has more than one unit
+  if (h_nunits > h_acc[4]) {
     std::vector<Unit> hu(h_nunits);
     BBF_CUDA(cudaMemcpyAsync(hu.data(), p->units, sizeof(Unit) * h_nunits, cudaMemcpyDeviceToHost, st));
     std::vector<CutDesc> cd;
@@ -425,18 +436,28 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3) {
     bool any = false;
     for (uint32_t i = 0; i + 1 < h_nunits; ++i) any |= hu[i].x == hu[i + 1].x;
     if (any) {
-      std::vector<uint32_t> hlo(n), hend1(n);
-      BBF_CUDA(cudaMemcpyAsync(hlo.data(), sb, 4ull * n, cudaMemcpyDeviceToHost, st));
-      BBF_CUDA(cudaMemcpyAsync(hend1.data(), g->end1, 4ull * n, cudaMemcpyDeviceToHost, st));
+      // the boundaries' starts, and their middle counts gathered on the device (no n-sized copy)
+      std::vector<uint32_t> bx;
+      for (uint32_t i = 0; i + 1 < h_nunits; ++i)
+        if (hu[i].x == hu[i + 1].x) bx.push_back(hu[i].x);
+      uint32_t* d_bx;
+      BBF_CUDA(dmalloc(&d_bx, 8ull * bx.size(), st));
+      BBF_CUDA(cudaMemcpyAsync(d_bx, bx.data(), 4ull * bx.size(), cudaMemcpyHostToDevice, st));
+      k_gather_m<<<(unsigned)((bx.size() + 255) / 256), 256, 0, st>>>(d_bx, (uint32_t)bx.size(), sb, g->end1,
+                                                                     d_bx + bx.size());
+      g->launches += 1;
+      std::vector<uint32_t> bm(bx.size());
+      BBF_CUDA(cudaMemcpyAsync(bm.data(), d_bx + bx.size(), 4ull * bx.size(), cudaMemcpyDeviceToHost, st));
       BBF_CUDA(cudaStreamSynchronize(st));
+      dfree(d_bx, st);
       unsigned long long off = 0;
+      size_t b = 0;
       for (uint32_t i = 0; i + 1 < h_nunits; ++i) {
         if (hu[i].x != hu[i + 1].x) continue;
-        const uint32_t x = hu[i].x, m = hend1[x] > hlo[x] ? hend1[x] - hlo[x] : 0;
-        cd.push_back(CutDesc{x, hu[i].hi, off});
+        cd.push_back(CutDesc{hu[i].x, hu[i].hi, off});
         uc[2ull * i + 1] = off;  // unit i's upper cut, unit i + 1's lower cut
         uc[2ull * (i + 1)] = off;
-        off += m;
+        off += bm[b++];
       }
       BBF_CUDA(dmalloc(&p->cut_tab, 4ull * (off + 1), st));
       BBF_CUDA(dmalloc(&p->unit_cut, 8ull * uc.size(), st));

@@ -86,3 +86,14 @@ def test_upload_api_argument_errors_without_gpu(libpath):
     with pytest.raises(bbf.BBFError) as e:
         bbf.Upload(2, 2, rp, np.array([0, 1, 0, 1], np.uint32), np.ones(4, np.uint8))
     assert e.value.name == "BBF_ECUDA"
+
+
+def test_build_stamp_records_flags(libpath):
+    """The default build's object directory carries a stamp of the flags it was compiled with and
+    no extra flags (diagnostic variants build into their own directories, _build_<name>)."""
+    import json
+    from paper_2308_07932_b200 import build
+    stamp = json.load(open(os.path.join(build.BUILD, "flags.json")))
+    assert stamp["extra"] == [] and stamp["arch"] == build.ARCH
+    assert "-lineinfo" in stamp["flags"]
+    assert libpath == build.LIB
