@@ -201,6 +201,7 @@ bbf_status bbf_count_pairs_topk(bbf_graph *g, int side, uint32_t k, bbf_pair *ou
  * endpoint summed over all U-pairs containing its U endpoint (route S(U) in both directions on the
  * sparse engine's hub kernel), so they satisfy sum_e = 4 (B, N) and, per vertex z, the sum over
  * z's edges = 2 x z's per-vertex count.  With a comm the work is sharded and the slots all-reduced.
+ * A graph loaded with BBF_POSITIVE_ONLY holds only the positive edges: pass that edge set's CSR.
  * Errors: BBF_EINVAL (null pointers, flags, a CSR whose edges are not the graph's), those of
  * bbf_count_global. */
 bbf_status bbf_count_per_edge(bbf_graph *g, const uint64_t *row_ptr, const uint32_t *col, uint64_t *bal,

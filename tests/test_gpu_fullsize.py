@@ -219,3 +219,23 @@ def test_per_edge_rejects_foreign_csr(bbf):
                                                                       g.row_ptr[1:].astype(np.int64))])
         _, pb, pn = h.count_per_edge(g.row_ptr, g.col[perm])  # rows reversed: same edges, other order
     assert np.array_equal(pb, eb[perm]) and np.array_equal(pn, en[perm])
+
+
+def test_per_edge_device_pointers_and_empty(bbf):
+    """Per-edge counts with device arrays (BBF_PTR_DEVICE: CUDA tensors in and out) equal the host
+    call; an empty graph gives empty arrays and zero totals."""
+    import torch
+    g = G.config2()
+    with bbf.Graph.from_synth(g) as h:
+        tot, eb, en = h.count_per_edge(g.row_ptr, g.col)
+        rp = torch.from_numpy(g.row_ptr.view(np.int64)).cuda()
+        cl = torch.from_numpy(g.col.view(np.int32)).cuda()
+        ob = torch.zeros(g.nnz, dtype=torch.int64, device="cuda")
+        on = torch.zeros(g.nnz, dtype=torch.int64, device="cuda")
+        tot2, _, _ = h.count_per_edge(rp, cl, out=(ob, on))
+    assert (tot2["balanced"], tot2["unbalanced"]) == (tot["balanced"], tot["unbalanced"])
+    assert np.array_equal(ob.cpu().numpy().view(np.uint64), eb) and np.array_equal(on.cpu().numpy().view(np.uint64), en)
+    e = G.from_edges(3, 4, [], [], [])
+    with bbf.Graph.from_synth(e) as h:
+        tot, eb, en = h.count_per_edge(e.row_ptr, e.col)
+    assert eb.size == 0 and en.size == 0 and tot["balanced"] == 0
