@@ -579,10 +579,46 @@ __device__ __forceinline__ void t3_long4(const uint4& q, uint32_t vm4, uint32_t 
   }
 }
 
-template <int MODE>
+// S1: lane L takes entries L, L+32, L+64, L+96 of each block (4 LDG.32), so one shared operation
+// covers 32 consecutive entries: consecutive counter words where ends have one field per word (the
+// high-degree zones) — no bank conflicts; no first-block mask (blocks start at the record).  !S1:
+// lane L takes entries 4L..4L+3 (one LDG.128): one shared operation covers every 4th entry — distinct
+// words where ends pack 4-8 fields per word (the low-degree zones).
+template <int MODE, bool S1>
 __device__ __forceinline__ void t3_long(const uint32_t* __restrict__ adjc, const Rec& rc, uint32_t cbase,
                                         uint32_t ctr0, uint32_t bmbase, uint32_t word0, int lane,
                                         uint32_t& own, uint32_t& oth) {
+  if (S1) {
+    const uint32_t shamt = 22u + 5u * (rc.wv >> 31), oshamt = 49u - shamt;
+    const uint32_t nb = (rc.len + 127u) >> 7;
+    const uint32_t dummy = ctr0 + 4u * (uint32_t)lane;
+    const uint32_t* s1 = adjc + rc.p + lane;
+    auto ld1 = [&](uint32_t blk) {
+      const uint32_t* q = s1 + 128u * blk;
+      return make_uint4(q[0], q[32], q[64], q[96]);
+    };
+    auto vm1 = [&](uint32_t blk) {
+      const uint32_t off = 128u * blk + (uint32_t)lane, rem = rc.len > off ? rc.len - off : 0u;
+      return rem > 96u ? 15u : rem > 64u ? 7u : rem > 32u ? 3u : rem ? 1u : 0u;
+    };
+    uint4 c0 = ld1(0), c1 = make_uint4(0u, 0u, 0u, 0u);
+    if (nb > 1) c1 = ld1(1);
+#pragma unroll 1
+    for (uint32_t b = 0; b < nb; b += 2) {
+      uint4 n0 = make_uint4(0u, 0u, 0u, 0u), n1 = make_uint4(0u, 0u, 0u, 0u);
+      if (b + 2 < nb) n0 = ld1(b + 2);
+      if (b + 3 < nb) n1 = ld1(b + 3);
+      if (b + 1 == nb) t3_long4<MODE, true>(c0, vm1(b), dummy, cbase, bmbase, word0, shamt, oshamt, own, oth);
+      else t3_long4<MODE, false>(c0, 0u, dummy, cbase, bmbase, word0, shamt, oshamt, own, oth);
+      if (b + 1 < nb) {
+        if (b + 2 == nb) t3_long4<MODE, true>(c1, vm1(b + 1), dummy, cbase, bmbase, word0, shamt, oshamt, own, oth);
+        else t3_long4<MODE, false>(c1, 0u, dummy, cbase, bmbase, word0, shamt, oshamt, own, oth);
+      }
+      c0 = n0;
+      c1 = n1;
+    }
+    return;
+  }
   const uint32_t shamt = 22u + 5u * (rc.wv >> 31), oshamt = 49u - shamt;
   const uint32_t p = rc.p, e_end = rc.p + rc.len, b0 = p & ~3u;
   const uint32_t nb = (e_end - b0 + 127u) >> 7;
@@ -593,14 +629,24 @@ __device__ __forceinline__ void t3_long(const uint32_t* __restrict__ adjc, const
     const uint32_t lo = p > off ? min(p - off, 4u) : 0u, hi = e_end > off ? min(e_end - off, 4u) : 0u;
     return ((1u << hi) - 1u) & ~((1u << lo) - 1u);
   };
-  uint4 c0 = src[0], c1 = make_uint4(0u, 0u, 0u, 0u);
-  if (nb > 1) c1 = src[32];
+#ifdef BBF_EXP_NOLDG  // timing experiment only: the long records' entries synthesised, not loaded (results wrong)
+  const uint32_t syn = ((word0 & kCpWordMask) << 2) | (4u << 27);
+  auto ld = [&](uint32_t blk) {
+    const uint32_t hsh = (blk * 32u + (uint32_t)lane) * 2654435761u;
+    return make_uint4(syn + (((hsh >> 8) & 1023u) << 2), syn + (((hsh >> 12) & 1023u) << 2),
+                      syn + (((hsh >> 16) & 1023u) << 2), syn + (((hsh >> 20) & 1023u) << 2));
+  };
+#else
+  auto ld = [&](uint32_t blk) { return src[32 * blk]; };
+#endif
+  uint4 c0 = ld(0), c1 = make_uint4(0u, 0u, 0u, 0u);
+  if (nb > 1) c1 = ld(1);
 #pragma unroll 1
   for (uint32_t b = 0; b < nb; b += 2) {
     // the next two blocks, in flight (not past the record: the overshoot was ~25% extra L2 traffic)
     uint4 n0 = make_uint4(0u, 0u, 0u, 0u), n1 = make_uint4(0u, 0u, 0u, 0u);
-    if (b + 2 < nb) n0 = src[32 * (b + 2)];
-    if (b + 3 < nb) n1 = src[32 * (b + 3)];
+    if (b + 2 < nb) n0 = ld(b + 2);
+    if (b + 3 < nb) n1 = ld(b + 3);
     if (b == 0 || b + 1 == nb) t3_long4<MODE, true>(c0, vmask(b), dummy, cbase, bmbase, word0, shamt, oshamt, own, oth);
     else t3_long4<MODE, false>(c0, 0u, dummy, cbase, bmbase, word0, shamt, oshamt, own, oth);
     if (b + 1 < nb) {
@@ -775,6 +821,12 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       // epilogue scans every word of the window
       const uint32_t nwk = min(kWin, Z.WB[5] - word0);
       const bool dense = sh_wc[k] * a.dense_div >= nwk;
+      // long records' lane layout (t3_long): consecutive entries per shared operation while the
+      // window starts before the 2-bit-field zone (ends of degree 2-3), every 4th entry there
+#ifndef BBF_T3_S1_ZONE
+#define BBF_T3_S1_ZONE 4  // measured: zones 2/3/4/5 -> 71.3/71.4/71.0/71.4 ms on config 5
+#endif
+      const bool s1w = word0 < Z.WB[BBF_T3_S1_ZONE];
       if (tid < 4) sh_c[tid] = 0;
 #ifdef BBF_T3_RECSTAT
       if (tid == 0) T3_COUNT(dense ? 6 : 7, sh_wc[k]);
@@ -809,9 +861,15 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             r = r2;
             uint32_t own = 0, oth = 0;
             const uint32_t ctr0 = (uint32_t)__cvta_generic_to_shared(ctr);
-            if (pass == 1) t3_long<2>(adjc, rl, cbase, ctr0, bmbase, word0, lane, own, oth);
-            else if (dense) t3_long<0>(adjc, rl, cbase, ctr0, bmbase, word0, lane, own, oth);
-            else t3_long<1>(adjc, rl, cbase, ctr0, bmbase, word0, lane, own, oth);
+            if (s1w) {
+              if (pass == 1) t3_long<2, true>(adjc, rl, cbase, ctr0, bmbase, word0, lane, own, oth);
+              else if (dense) t3_long<0, true>(adjc, rl, cbase, ctr0, bmbase, word0, lane, own, oth);
+              else t3_long<1, true>(adjc, rl, cbase, ctr0, bmbase, word0, lane, own, oth);
+            } else {
+              if (pass == 1) t3_long<2, false>(adjc, rl, cbase, ctr0, bmbase, word0, lane, own, oth);
+              else if (dense) t3_long<0, false>(adjc, rl, cbase, ctr0, bmbase, word0, lane, own, oth);
+              else t3_long<1, false>(adjc, rl, cbase, ctr0, bmbase, word0, lane, own, oth);
+            }
             if (pass == 1) {
               // the record's own-class sum and other-class sum (each < 2^26: <= 1024 entries of
               // 16-bit fields), minus one per wedge for the own class (Lemma 2 shares)

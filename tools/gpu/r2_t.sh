@@ -1,0 +1,2 @@
+BBF_LIB=paper_2308_07932_b200/_build_s1/libbbf.so timeout 900 python -m pytest tests/test_gpu_fullsize.py -x -q -k "full_per_vertex and (config3 or zoned)" 2>&1 | tail -1
+bash tools/gpu/ab.sh "default s1"
