@@ -183,8 +183,10 @@ constexpr uint32_t kRecMax = 1024;
 // 64/32/16-entry blocks the records touch, [4] records shorter than 8 entries, [5] entries of
 // records shorter than 64, [6] wedges in dense windows, [7] wedges in bitmap windows, [8] touched
 // words in the epilogue, [9] contributing fields, [10] records
-__device__ unsigned long long g_prof_cnt[96];  // [64..83]: unit-size bins (BBF_T3_WINPROF)  // [16..33]: window-size bins, [40..57] per-phase cycles (BBF_T3_WINPROF)
+__device__ unsigned long long g_prof_cnt[128];  // [96..111]: tiny-window latency marks (BBF_T3_LATPROF)
+//  // [64..83]: unit-size bins (BBF_T3_WINPROF)  // [16..33]: window-size bins, [40..57] per-phase cycles (BBF_T3_WINPROF)
 #define T3_COUNT(i, v) atomicAdd(&g_prof_cnt[i], (unsigned long long)(v))
+#define T3_LAT(i, v) atomicAdd(&sh_lat[(i) - 96], (unsigned long long)(v))
 __device__ unsigned long long g_prof_t[3] = {~0ull, ~0ull, 0ull};  // min CTA start, min CTA end, max CTA end (globaltimer ns)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -680,6 +682,10 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
   if (threadIdx.x == 0) atomicMin(&g_prof_t[0], gtimer());
 #endif
   if (threadIdx.x < 4) sh_dbg[threadIdx.x] = 0;
+#ifdef BBF_T3_LATPROF
+  __shared__ unsigned long long sh_lat[20];
+  if (threadIdx.x < 20) sh_lat[threadIdx.x] = 0;
+#endif
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   for (uint32_t i = tid; i < kWin + kBm + 3 * kMaxWin; i += kT3Threads) smem[i] = 0;
@@ -839,6 +845,10 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       }
       __syncthreads();
       T3_MARK(1);
+#ifdef BBF_T3_LATPROF  // tiny windows (< 2K wedges): when each warp's first batch and chunks arrive
+      const long long t_lat = clock64();
+      const bool tiny = sh_wc[k] < 2048;
+#endif
 #ifdef BBF_T3_WINPROF  // CTA cycles of the window's passes + epilogue, binned by its wedge count
       const long long t_win = clock64();
       const uint32_t wbin = sh_wc[k] < 2048 ? 0 : sh_wc[k] < 8192 ? 1 : sh_wc[k] < 32768 ? 2 : sh_wc[k] < 131072 ? 3 : sh_wc[k] < 524288 ? 4 : 5;
@@ -899,11 +909,24 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
         };
         uint32_t cnt_next;
         Rec rc_next;
+#ifdef BBF_T3_LATPROF
+        bool lat_seen = false;
+        if (tiny && lane == 0) { T3_LAT(106 + pass, clock64() - t_lat); T3_LAT(108 + pass, 1); }  // warp reaches the flattened part
+#endif
         fetch(cnt_next, rc_next);
         while (true) {
           const uint32_t cnt = cnt_next;
           const Rec rc = rc_next;
           if (cnt == 0) break;
+#ifdef BBF_T3_LATPROF
+          bool lat_first = false;
+          if (tiny && !lat_seen) {
+            lat_seen = true;
+            lat_first = true;
+            const uint32_t dep = __shfl_sync(0xffffffffu, rc.len, 0);  // the batch's records have arrived
+            if (lane == 0) { T3_LAT(96 + pass, clock64() - t_lat + (dep & 0)); T3_LAT(98 + pass, 1); }
+          }
+#endif
           fetch(cnt_next, rc_next);
           if (pass == 1) { sh_acc[warp][0][lane] = 0; sh_acc[warp][1][lane] = 0; __syncwarp(); }
           // The batch's records are flattened over the lanes in 32-B chunks of the adjacency
@@ -971,6 +994,12 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
                 else if (dense) t3_chunk<0, CP, WIDE>(ev, vm, cbase, ctr, bm, word0, shamt, oshamt, o_wv[u], cb, cn, dummy);
                 else t3_chunk<1, CP, WIDE>(ev, vm, cbase, ctr, bm, word0, shamt, oshamt, o_wv[u], cb, cn, dummy);
               }
+#ifdef BBF_T3_LATPROF
+              if (lat_first && u == 0 && base0 == 0) {
+                const uint32_t dep = __shfl_sync(0xffffffffu, cb + cn, 0);  // the first step's chunks are processed
+                if (lane == 0) { T3_LAT(100 + pass, clock64() - t_lat + (dep & 0)); T3_LAT(110 + pass, 1); }
+              }
+#endif
               if (pass == 1 && __any_sync(0xffffffffu, (cb | cn) != 0)) {
                 // segmented sum over each owner's lane group; its last lane adds it (one writer
                 // per owner per step, so no atomics)
@@ -992,7 +1021,13 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             __syncwarp();
           }
         }
+#ifdef BBF_T3_LATPROF
+        if (tiny && lane == 0 && lat_seen) { T3_LAT(102 + pass, clock64() - t_lat); T3_LAT(112 + pass, 1); }
+#endif
         __syncthreads();
+#ifdef BBF_T3_LATPROF
+        if (tiny && tid == 0) { T3_LAT(104 + pass, clock64() - t_lat); T3_LAT(114 + pass, 1); }
+#endif
         T3_MARK(nrec < 64 ? 1 : 2 + pass);  // slot 1: set-up + passes of small windows
 #ifdef BBF_T3_WINPROF
         if (tid == 0) T3_COUNT(40 + 3 * wbin + pass, clock64() - t_win);
@@ -1100,6 +1135,9 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
     atomicAdd(&a.acc[0], totB);
     atomicAdd(&a.acc[1], totN);
   }
+#ifdef BBF_T3_LATPROF
+  if (tid < 20) atomicAdd(&g_prof_cnt[96 + tid], sh_lat[tid]);
+#endif
 #ifdef BBF_T3_PROF
   if (tid == 0) {
     for (int i = 0; i < 5; ++i) atomicAdd(&a.acc[11 + i], sh_prof[i]);
@@ -1657,7 +1695,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     cudaMemcpyFromSymbol(t, g_prof_t, sizeof(t));
     fprintf(stderr, "[bbf] t3 CTA ends: first %.3f ms, last %.3f ms after the first start\n", (t[1] - t[0]) * 1e-6,
             (t[2] - t[0]) * 1e-6);
-    unsigned long long pc[96];
+    unsigned long long pc[128];
     cudaMemcpyFromSymbol(pc, g_prof_cnt, sizeof(pc));
     const char* bn[6] = {"<2K", "<8K", "<32K", "<128K", "<512K", ">=512K"};
     for (int b = 0; b < 6; ++b)
@@ -1686,7 +1724,14 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
     fprintf(stderr, "[bbf] t3 entries by run length: <8 %.3f <32 %.3f <128 %.3f <512 %.3f >=512 %.3f\n",
             pc[11] / (double)pc[0], pc[12] / (double)pc[0], pc[13] / (double)pc[0], pc[14] / (double)pc[0],
             pc[15] / (double)pc[0]);
-    const unsigned long long z40[96] = {};
+#ifdef BBF_T3_LATPROF
+    for (int ps = 0; ps < 2; ++ps)
+      fprintf(stderr, "[bbf] t3 tiny windows pass %d (cycles after the window start): warp reaches batches %.0f (n %llu), first batch records %.0f (n %llu), first chunks done %.0f (n %llu), working warp done %.0f (n %llu), barrier exit %.0f (n %llu)\n",
+              ps, pc[106 + ps] / (double)(pc[108 + ps] + 1), pc[108 + ps], pc[96 + ps] / (double)(pc[98 + ps] + 1), pc[98 + ps],
+              pc[100 + ps] / (double)(pc[110 + ps] + 1), pc[110 + ps], pc[102 + ps] / (double)(pc[112 + ps] + 1), pc[112 + ps],
+              pc[104 + ps] / (double)(pc[114 + ps] + 1), pc[114 + ps]);
+#endif
+    const unsigned long long z40[128] = {};
     cudaMemcpyToSymbol(g_prof_cnt, z40, sizeof(z40));
     const unsigned long long init[3] = {~0ull, ~0ull, 0ull};
     cudaMemcpyToSymbol(g_prof_t, init, sizeof(init));
