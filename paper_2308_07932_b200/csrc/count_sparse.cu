@@ -856,7 +856,11 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       // ---------------- pass 1 (Alg. 2 lines 9-14) and pass 2 (per-vertex shares)
 #pragma unroll 1
       for (int pass = 0; pass < (PV ? 2 : 1); ++pass) {
+#ifdef BBF_EXP_NOLONG  // timing experiment only: long records skipped (results wrong)
+        if (false) {
+#else
         if (CP && nlong) {  // long records first, one warp each (sh_c[2 + pass] is the cursor)
+#endif
           const uint32_t bmbase = (uint32_t)__cvta_generic_to_shared(bm);
           uint32_t r = 0;
           if (lane == 0) r = atomicAdd(&sh_c[2 + pass], 1u);
@@ -913,7 +917,11 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
         bool lat_seen = false;
         if (tiny && lane == 0) { T3_LAT(106 + pass, clock64() - t_lat); T3_LAT(108 + pass, 1); }  // warp reaches the flattened part
 #endif
+#ifdef BBF_EXP_NOFLAT  // timing experiment only: short records skipped (results wrong)
+        cnt_next = 0;
+#else
         fetch(cnt_next, rc_next);
+#endif
         while (true) {
           const uint32_t cnt = cnt_next;
           const Rec rc = rc_next;
