@@ -211,7 +211,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define T3_MARK(slot) do {} while (0)
 #endif
 #ifndef BBF_T3_KU
-#define BBF_T3_KU 2
+#define BBF_T3_KU 1  // measured: kU 1 / 2 -> 70.3 / 71.2 ms (config 5), 5.294 / 5.275 ms (config 3)
 #endif
 constexpr int kU = BBF_T3_KU;  // flattened steps per iteration of the hub kernel's record loop
 #ifndef BBF_T3_CE
