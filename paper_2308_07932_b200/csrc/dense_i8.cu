@@ -1077,7 +1077,8 @@ __global__ void k_dense_pack_f4(const uint8_t* __restrict__ in, uint64_t k_in, u
 // a pair i < j; super-tiles of 8 x 8 blocks for L2 reuse as in pair_tile_list
 std::vector<uint2> f4_tile_list(uint32_t rows_pad) {
   std::vector<uint2> t;
-  const uint32_t nI = rows_pad / kPB, nJ = (rows_pad + kF4N - 1) / kF4N, sb = 8;
+  const uint32_t sb = getenv("BBF_F4_SB") ? std::max(1, atoi(getenv("BBF_F4_SB"))) : 8u;  // super-tile side (blocks)
+  const uint32_t nI = rows_pad / kPB, nJ = (rows_pad + kF4N - 1) / kF4N;
   for (uint32_t JS = 0; JS < (nJ + sb - 1) / sb; ++JS)
     for (uint32_t IS = 0; IS < (nI + sb - 1) / sb; ++IS)
       for (uint32_t J = JS * sb; J < std::min(nJ, JS * sb + sb); ++J)
