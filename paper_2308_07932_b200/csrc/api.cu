@@ -180,6 +180,7 @@ bbf_status sync_stream(bbf_graph* g) {
 // failed locally (an allocation, a table limit) makes every rank return that error instead of
 // leaving the others blocked in the all-reduce.  BN: host (B, N), replaced by the global sums.
 bbf_status finish_collective(bbf_graph* g, bbf_status local, bool per_vertex, unsigned long long* BN) {
+  NvtxRange nvtx_("bbf::collective");
   if (!multi_rank(g)) return local;
   unsigned long long h[3] = {local == BBF_OK ? BN[0] : 0ull, local == BBF_OK ? BN[1] : 0ull,
                              (unsigned long long)local};

@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(kBaseThreads) k_bb_base(const BaseArgs a) {
 // Alg. 1 over this rank's share of the starts (start x on rank x mod nranks); host_BN receives
 // this rank's (balanced, unbalanced).  Scratch: one area of max-work bytes per CTA.
 bbf_status run_base(bbf_graph* g, Plan* p, int rank, int nranks, unsigned long long* host_BN) {
+  NvtxRange nvtx_("bbf::bb_base");
   cudaStream_t st = g->stream;
   const uint32_t n = g->n;
   host_BN[0] = host_BN[1] = 0;

@@ -15,11 +15,21 @@
 //     so wedges ending (or centred) there contribute to no count (DESIGN.md §"Pruning").
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <string>
 
 #include "../../include/bbf.h"
+
+// NVTX range over a host-side phase (build, plan, engine, collective): header-only NVTX3, a no-op
+// unless a profiler (nsys, ncu --nvtx) is attached
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace bbf {
 

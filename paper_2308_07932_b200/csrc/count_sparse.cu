@@ -1591,6 +1591,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
                            unsigned long long* cn, unsigned long long* cid,
                            unsigned long long cap, unsigned long long* n_cand, unsigned long long tau,
                            unsigned long long* edge) {
+  NvtxRange nvtx_("bbf::sparse_engine");
   cudaStream_t st = g->stream;
   if (edge && (!per_vertex || pairs || p->n_t1 || p->n_t1b || p->n_t2 || p->n_t2s || p->n_t2h)) {
     set_error("internal: per-edge counts need a per-vertex pass over a hub-tier-only plan");
@@ -1785,6 +1786,7 @@ __global__ void k_gather_u64(const unsigned long long* __restrict__ src, const u
 // the union of the shards' top-k lists).
 bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uint32_t* n_out, int rank,
                           int nranks) {
+  NvtxRange nvtx_("bbf::pairs_topk");
   cudaStream_t st = g->stream;
   Plan* p = &g->plan_s[side];
   if (p->valid && p->nranks != nranks) free_plan(p, st);  // hub units are sized per rank count

@@ -1455,6 +1455,7 @@ bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32
 }
 
 bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsigned long long* host_BN) {
+  NvtxRange nvtx_("bbf::dense_engine");
   cudaStream_t st = g->stream;
   if (!dense_supported(g)) {
     set_error("graph not supported by the dense int8 path");

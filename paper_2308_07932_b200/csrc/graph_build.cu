@@ -424,6 +424,7 @@ bbf_status validate_csr(const uint64_t* d_rp, uint32_t n_u, const uint32_t* d_co
 
 bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* col,
                        const uint8_t* sign, bool device_ptrs) {
+  NvtxRange nvtx_("bbf::build_graph");
   cudaStream_t st = g->stream;
   const uint32_t n_u = g->n_u, n_v = g->n_v, n = g->n;
   uint64_t nnz = g->nnz;  // the positive-only filter may reduce it
@@ -680,6 +681,7 @@ bbf_status ensure_adj(bbf_graph* g) {
 // S4: rank-space adjacency of both directions (one radix sort of the 2*nnz directed entries),
 // duplicate check, mid_start / end1 cuts, degree prefix, hub-kernel counter addresses and runs
 bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, const uint8_t* d_sg) {
+  NvtxRange nvtx_("bbf::build_adj");
   cudaStream_t st = g->stream;
   const uint32_t n_u = g->n_u, n_v = g->n_v, n = g->n;
   const uint64_t nnz = g->nnz;

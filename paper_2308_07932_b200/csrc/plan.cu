@@ -276,6 +276,7 @@ void free_plan(Plan* p, cudaStream_t st) {
 }
 
 bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3) {
+  NvtxRange nvtx_("bbf::make_plan");
   cudaStream_t st = g->stream;
   const uint32_t n = g->n;
   const uint64_t m = 2 * g->nnz;
