@@ -185,6 +185,7 @@ def check_parity(g, config: int, tot: dict, pv) -> dict:
     sha = pv_sha256(pv)
     assert sha == exp["pv_sha256"], "parity: per-vertex arrays differ from the oracle's"
     return {"B": exp["B"], "N": exp["N"], "W_G": exp["W_G"], "pv_sha256": sha,
+            "graph_sha256": exp["graph_sha256"],
             "source": "tests/golden/expected_counts.json (oracle_route_g_pv)"}
 
 
