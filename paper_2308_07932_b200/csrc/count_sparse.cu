@@ -760,6 +760,12 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           en = b;
         }
       }
+#ifdef BBF_T3_RECSTAT  // pre-scan middles: [84] of split units, [85] of those with a non-empty range, [86] of whole starts
+      if (i < m) {
+        if (split_lo || split_hi) { T3_COUNT(84, 1); if (s < en) T3_COUNT(85, 1); }
+        else T3_COUNT(86, 1);
+      }
+#endif
       // records of this middle = the graph's window runs of row v clipped to [s, en)
       const uint32_t r0 = s < en ? a.runid[s] : 0;
       const uint32_t nr = s < en ? ((split_hi || a.ue) ? a.runid[en - 1] : rl) - r0 + 1 : 0;
@@ -1730,6 +1736,7 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
             pc[0] / (16.0 * pc[3] + 1e-9), pc[4], pc[5], pc[6], pc[7]);
     fprintf(stderr, "[bbf] t3 pass-2 long-record entries %llu, with a + d >= 2 at the end: %llu (%.3f)\n", pc[20], pc[21],
             pc[21] / (pc[20] + 1e-9));
+    fprintf(stderr, "[bbf] t3 pre-scan middles: split units %llu (non-empty %llu), whole starts %llu\n", pc[84], pc[85], pc[86]);
     fprintf(stderr, "[bbf] t3 entries by run length: <8 %.3f <32 %.3f <128 %.3f <512 %.3f >=512 %.3f\n",
             pc[11] / (double)pc[0], pc[12] / (double)pc[0], pc[13] / (double)pc[0], pc[14] / (double)pc[0],
             pc[15] / (double)pc[0]);
