@@ -339,6 +339,7 @@ cudaError_t rb_sync(cudaStream_t st);
 // reductions launch two kernels each
 constexpr uint32_t cub_sort_kernels(int bits) { return 2u + (uint32_t)((bits + 7) / 8); }
 constexpr uint32_t kCubScanKernels = 2, kCubSelectKernels = 2, kCubReduceKernels = 2;
+constexpr uint32_t kCubSortKernels64 = 10;  // onesweep radix sort of 64-bit keys: histogram, exclusive sum, 8 passes
 template <class T>
 inline cudaError_t dmalloc(T** out, size_t bytes, cudaStream_t st) {
   return dmalloc_raw(reinterpret_cast<void**>(out), bytes, st);

@@ -103,7 +103,13 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 __device__ __forceinline__ void emit_pair(const EngineArgs& a, uint32_t x, uint32_t wrow,
                                           unsigned long long fb, unsigned long long fn) {
   if (fb < a.tau) return;  // below the current top-k threshold
-  unsigned long long slot = atomicAdd(&a.acc[4], 1ull);
+  // one slot atomic per group of converged lanes (all emitting lanes hit the same counter)
+  const unsigned am = __activemask();
+  const int lane = (int)(threadIdx.x & 31), leader = __ffs(am) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(&a.acc[4], (unsigned long long)__popc(am));
+  base = __shfl_sync(am, base, leader);
+  const unsigned long long slot = base + (unsigned long long)__popc(am & ((1u << lane) - 1u));
   if (slot < a.cap) {
     unsigned long long ix = a.inv[x], iw = a.inv[wrow];
     unsigned long long lo = ix < iw ? ix : iw, hi = ix < iw ? iw : ix;
@@ -1811,6 +1817,34 @@ bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uin
   BBF_CUDA(dmalloc(&cb, 8 * cap, st));
   BBF_CUDA(dmalloc(&cn, 8 * cap, st));
   BBF_CUDA(dmalloc(&cid, 8 * cap, st));
+  // the (r+1)-th largest of the first min(n, cap) stored balanced counts (device sort, one read)
+  auto kth_stored = [&](unsigned long long nstored, size_t r, unsigned long long* val) -> bbf_status {
+    const int ns = (int)std::min<unsigned long long>(nstored, cap);
+    unsigned long long* srt;
+    BBF_CUDA(dmalloc(&srt, 8ull * ns + 8, st));
+    size_t ts = 0;
+    cub::DeviceRadixSort::SortKeysDescending(nullptr, ts, cb, srt, ns, 0, 64, st);
+    void* tmps;
+    BBF_CUDA(dmalloc(&tmps, ts + 16, st));
+    BBF_CUDA(cub::DeviceRadixSort::SortKeysDescending(tmps, ts, cb, srt, ns, 0, 64, st));
+    g->launches += kCubSortKernels64;
+    BBF_CUDA(cudaMemcpyAsync(val, srt + std::min<size_t>(r, (size_t)ns - 1), 8, cudaMemcpyDeviceToHost, st));
+    BBF_CUDA(cudaStreamSynchronize(st));
+    dfree(srt, st);
+    dfree(tmps, st);
+    return BBF_OK;
+  };
+  // Starting threshold from a sample: when a pass at tau = 1 could overflow the buffer, count
+  // 1/16 of the work items first (the shard of one rank in a 16x larger fake world) and start at
+  // the (4k)-th largest balanced count among the sample's pairs — about 64k pairs of the whole
+  // set reach it, so the full pass usually stores a complete candidate set at once.  Any start is
+  // correct: the loop below only stops on a complete set of at least k candidates (or tau = 1).
+  if (p->W_pruned > cap && !getenv("BBF_TOPK_NO_SAMPLE")) {  // env: test hook
+    unsigned long long BN[2];
+    BBF_TRY(run_sparse_impl(g, p, false, true, rank, nranks * 16, BN, cb, cn, cid, cap, &ncand, 1));
+    if (ncand >= 4ull * k) BBF_TRY(kth_stored(ncand, 4ull * k - 1, &tau));
+    if (tau < 1) tau = 1;
+  }
   for (int it = 0;; ++it) {
     unsigned long long BN[2];
     BBF_TRY(run_sparse_impl(g, p, false, true, rank, nranks, BN, cb, cn, cid, cap, &ncand, tau));
@@ -1820,12 +1854,10 @@ bbf_status run_pairs_topk(bbf_graph* g, int side, uint32_t k, bbf_pair* out, uin
       lo = tau;
       lo_count = ncand;
       // the stored candidates are a subset: their (4k)-th largest balanced count bounds tau
-      std::vector<unsigned long long> hb(cap);
-      BBF_CUDA(cudaMemcpyAsync(hb.data(), cb, 8 * cap, cudaMemcpyDeviceToHost, st));
-      BBF_CUDA(cudaStreamSynchronize(st));
-      const size_t r = std::min<size_t>(cap - 1, 4ull * k);
-      std::nth_element(hb.begin(), hb.begin() + r, hb.end(), std::greater<unsigned long long>());
-      tau = std::max(tau + 1, hb[r]);
+      // (a device sort of the stored counts, then one element read back)
+      unsigned long long kth = 0;
+      BBF_TRY(kth_stored(cap, std::min<size_t>(cap - 1, 4ull * k), &kth));
+      tau = std::max(tau + 1, kth);
     } else {
       hi = tau;  // too few candidates at this threshold
     }
