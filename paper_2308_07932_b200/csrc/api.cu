@@ -742,7 +742,7 @@ bbf_status bbf_count_per_edge(bbf_graph* g, const uint64_t* row_ptr, const uint3
   for (int k = 0; k < 2 && local == BBF_OK; ++k) {
     Plan* p = &g->plan_e[k];
     if (p->valid && p->nranks != nranks) free_plan(p, st);
-    if (!p->valid) local = make_plan(g, k == 0 ? 1 : 3, p, true);
+    if (!p->valid) local = make_plan(g, k == 0 ? 1 : 3, p, false);
     if (local == BBF_OK) {
       cudaError_t e = cudaMemsetAsync(g->pv, 0, 16ull * g->n, st);
       if (e != cudaSuccess) local = cuda_status(e, "memset");

@@ -1220,6 +1220,7 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
           wv = a.adj[m_lo + i];
           s = a.ub[m_lo + i];
           uint32_t en = a.end1[ob + (wv & kMask)];
+          if (a.ue) en = min(en, a.ue[m_lo + i]);  // route 3: the ends before x's own entry of N(v)
           len = en > s ? en - s : 0;
         }
         const uint32_t incl = warp_incl_scan(len, lane), excl = incl - len;
@@ -1314,7 +1315,7 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
     if (PV) {
       xB = warp_sum(xB);
       xN = warp_sum(xN);
-      if (lane == 0 && (xB | xN)) {
+      if (lane == 0 && (xB | xN) && !a.edge) {
         atomicAdd(&a.pv[2ull * (x)], xB);
         atomicAdd(&a.pv[2ull * (x) + 1], xN);
       }
@@ -1353,6 +1354,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
   uint32_t* mW = mS + kM;        // kM: middle word
   uint32_t* mB = mW + kM;        // kM: pass-2 balanced share of the middle
   uint32_t* mN = mB + kM;        // kM: pass-2 unbalanced share
+  uint32_t* mE = mN + kM;        // kM: start->middle entry (per-edge counts only; launched with the extra space)
   __shared__ uint32_t sh_item, sh_mcc, sh_wsum[kT2Warps];
   __shared__ unsigned long long sh_red[2][kT2Warps];
   for (uint32_t i = tid; i < 2 * kSlots; i += kT2Threads) ((uint32_t*)keys)[i] = 0;
@@ -1394,7 +1396,8 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
             if (i < mc) {
               wv2[q] = a.adj[m_lo + r0 + i];
               s2[q] = a.ub[m_lo + r0 + i];
-              const uint32_t en = a.end1[ob + (wv2[q] & kMask)];
+              uint32_t en = a.end1[ob + (wv2[q] & kMask)];
+              if (a.ue) en = min(en, a.ue[m_lo + r0 + i]);  // route 3: the ends before x's own entry
               len2[q] = en > s2[q] ? en - s2[q] : 0;
             }
           }
@@ -1411,6 +1414,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
             for (int q = 0; q < 2; ++q) {
               if (len2[q]) {
                 mP[k] = pos; mS[k] = s2[q]; mW[k] = wv2[q];
+                if (a.edge) mE[k] = m_lo + r0 + 2 * tid + q;
                 if (pass == 1) { mB[k] = 0; mN[k] = 0; }
                 ++k;
                 pos += len2[q];
@@ -1486,7 +1490,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
         if (pass == 1) {
           for (uint32_t i = tid; i < mcc; i += kT2Threads) {
             const uint32_t cb = mB[i], cn = mN[i];
-            if (cb | cn) mid_red(a, a.rmid[xu ? 1 : 0], mW[i] & kMask, ob + (mW[i] & kMask), cb, cn, 0xffffffffu);  // (per-edge counts never use T2)
+            if (cb | cn) mid_red(a, a.rmid[xu ? 1 : 0], mW[i] & kMask, ob + (mW[i] & kMask), cb, cn, a.edge ? mE[i] : 0u);
           }
           __syncthreads();
         }
@@ -1518,7 +1522,7 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
       if (warp == 0) {
         const unsigned long long bb = warp_sum(lane < kT2Warps ? sh_red[0][lane] : 0ull);
         const unsigned long long n2 = warp_sum(lane < kT2Warps ? sh_red[1][lane] : 0ull);
-        if (lane == 0 && (bb | n2)) {
+        if (lane == 0 && (bb | n2) && !a.edge) {
           atomicAdd(&a.pv[2ull * x], bb);
           atomicAdd(&a.pv[2ull * x + 1], n2);
         }
@@ -1568,7 +1572,7 @@ cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, P
   if (p->n_t2) {
     EngineArgs eb = ea;
     eb.t2 = p->t2; eb.n_t2 = p->n_t2; eb.t2ctr = 16;
-    const size_t smem2 = sizeof(uint32_t) * (2 * kT2Slots + 5 * 1024 + 1);
+    const size_t smem2 = sizeof(uint32_t) * (2 * kT2Slots + 5 * 1024 + 1 + (ea.edge ? 1024 : 0));
     err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 512, kT2Slots>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     if (err != cudaSuccess) return err;
     k_t2<PV, PAIRS, 512, kT2Slots><<<g->num_sms * 2, 512, smem2, st>>>(eb);
@@ -1577,7 +1581,7 @@ cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, P
   if (p->n_t2h) {
     EngineArgs eh = ea;
     eh.t2 = p->t2h; eh.n_t2 = p->n_t2h; eh.t2ctr = 19;
-    const size_t smem2 = sizeof(uint32_t) * (2 * kT2HugeSlots + 5 * 2048 + 1);
+    const size_t smem2 = sizeof(uint32_t) * (2 * kT2HugeSlots + 5 * 2048 + 1 + (ea.edge ? 2048 : 0));
     err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 1024, kT2HugeSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     if (err != cudaSuccess) return err;
     k_t2<PV, PAIRS, 1024, kT2HugeSlots><<<g->num_sms, 1024, smem2, st>>>(eh);
@@ -1586,7 +1590,7 @@ cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, P
   if (p->n_t2s) {
     EngineArgs es = ea;
     es.t2 = p->t2s; es.n_t2 = p->n_t2s; es.t2ctr = 17;
-    const size_t smem2 = sizeof(uint32_t) * (kT2Slots + 5 * 512 + 1);
+    const size_t smem2 = sizeof(uint32_t) * (kT2Slots + 5 * 512 + 1 + (ea.edge ? 512 : 0));
     err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 256, kT2Slots / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     if (err != cudaSuccess) return err;
     k_t2<PV, PAIRS, 256, kT2Slots / 2><<<g->num_sms * 5, 256, smem2, st>>>(es);
@@ -1605,8 +1609,8 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
                            unsigned long long* edge) {
   NvtxRange nvtx_("bbf::sparse_engine");
   cudaStream_t st = g->stream;
-  if (edge && (!per_vertex || pairs || p->n_t1 || p->n_t1b || p->n_t2 || p->n_t2s || p->n_t2h)) {
-    set_error("internal: per-edge counts need a per-vertex pass over a hub-tier-only plan");
+  if (edge && (!per_vertex || pairs)) {
+    set_error("internal: per-edge counts need a per-vertex pass");
     return BBF_ECUDA;
   }
   // scratch for the hub kernel: per CTA 3 middle arrays + 4 record arrays [window][middle]
