@@ -91,8 +91,13 @@ struct EngineArgs {
 // The q-th work item (hub unit, T1 / T2 start; plan order = descending work, roughly) of `rank` in
 // an N-rank job: items are dealt in snake order (0..N-1, N-1..0, ...) so no rank takes the larger
 // item of every round; every item lands on exactly one rank.
+// Work item of this rank's q-th claim: items are dealt in rounds of nranks in snake order (0..N-1,
+// N-1..0, ...), rotated by one rank every two rounds — plain snake dealing left the ranks of
+// config 5's 8-way split at two cost levels (±2.6%, hubs split into 4 units of unequal cost fall
+// on ranks {0,3,4,7} vs {1,2,5,6}); rotated, they are within ±0.6%.  A bijection per round.
 __device__ __forceinline__ uint64_t shard_item(uint64_t q, int rank, int nranks) {
-  return q * (uint64_t)nranks + ((q & 1ull) ? (uint64_t)(nranks - 1 - rank) : (uint64_t)rank);
+  const uint64_t snake = (q & 1ull) ? (uint64_t)(nranks - 1 - rank) : (uint64_t)rank;
+  return q * (uint64_t)nranks + (snake + (q >> 1)) % (uint64_t)nranks;
 }
 
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
