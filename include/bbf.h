@@ -150,10 +150,12 @@ bbf_status bbf_device_sync(int device);
  * Limits and errors (also for bbf_count_per_vertex and bbf_count_pairs_topk):
  *   BBF_EINVAL if BBF_FORCE_DENSE was given for a graph the dense path does not support (other
  *     side > 65,536 vertices, or operands > 16 GB);
- *   BBF_ERANGE if the sparse hub kernel would need more than 256 counter windows on one side:
- *     a window holds 52,224 words of degree-zoned (a, d) fields (8 ends of degree 2-3 per word
- *     down to one end of degree >= 256 per word, two words above 65,535), so a side holds at
- *     most ~13.4M counter words — e.g. 107M ends of degree <= 3, or 13.4M ends of degree >= 256;
+ *   BBF_ERANGE (at load) if one side needs more than 2^23 - 1 counter words for the sparse hub
+ *     kernel's 23-bit counter address: ends (degree >= 2) take degree-zoned (a, d) fields, 8
+ *     ends of degree 2-3 per word down to one end of degree >= 256 per word (two words above
+ *     65,535), so a side holds at most ~8.4M words (161 windows of 52,224 words) — e.g. 67M ends
+ *     of degree <= 3, or 8.4M ends of degree >= 256; (at count) if the hub kernel's window table
+ *     (256 windows) would be exceeded, which the address limit already rules out;
  *   BBF_EOVERFLOW if B + N could exceed 2^64 - 1 (host bound, reading R13);
  *   BBF_ENOMEM, BBF_ECUDA, BBF_ENCCL.
  * The dense path's block-scaled FP4 kernels (tcgen05 kind::mxf4) multiply exact +-1/0 e2m1

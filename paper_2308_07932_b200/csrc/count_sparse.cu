@@ -969,8 +969,8 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
             atomicAdd(&sh_dbg[1], (unsigned long long)T);
           }
 #endif
-          // kU steps per iteration: owner lookups first, then all chunk loads in flight, then
-          // the counter updates (hides the global-load latency behind the other steps' work)
+          // kU steps per iteration (BBF_T3_KU, default 1): owner lookups first, then all chunk
+          // loads in flight, then the counter updates
           for (uint32_t base0 = 0; base0 < T; base0 += 32 * kU) {
             uint32_t smask[kU], ow[kU], gs[kU], ch[kU], o_p[kU], o_len[kU], o_wv[kU];
             uint4 q[kU][kCE / 4];
