@@ -693,6 +693,10 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
   if (threadIdx.x == 0) atomicMin(&g_prof_t[0], gtimer());
 #endif
   if (threadIdx.x < 4) sh_dbg[threadIdx.x] = 0;
+#ifdef BBF_T3_BUSYPROF  // per window size class: warp-cycles in long records, in short batches, and the pass span x warps
+  __shared__ unsigned long long sh_busy[6][4];
+  if (threadIdx.x < 24) (&sh_busy[0][0])[threadIdx.x] = 0;
+#endif
 #ifdef BBF_T3_LATPROF
   __shared__ unsigned long long sh_lat[20];
   if (threadIdx.x < 20) sh_lat[threadIdx.x] = 0;
@@ -873,6 +877,10 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
       // ---------------- pass 1 (Alg. 2 lines 9-14) and pass 2 (per-vertex shares)
 #pragma unroll 1
       for (int pass = 0; pass < (PV ? 2 : 1); ++pass) {
+#ifdef BBF_T3_BUSYPROF
+        const long long tb0 = clock64();
+        const uint32_t bcls = sh_wc[k] < 2048 ? 0 : sh_wc[k] < 8192 ? 1 : sh_wc[k] < 32768 ? 2 : sh_wc[k] < 131072 ? 3 : sh_wc[k] < 524288 ? 4 : 5;
+#endif
 #ifdef BBF_EXP_NOLONG  // timing experiment only: long records skipped (results wrong)
         if (false) {
 #else
@@ -928,6 +936,9 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
           rx = Rec{0, 0, 0, 0};
           if ((uint32_t)lane < cntx) rx = rw[r0x + lane];
         };
+#ifdef BBF_T3_BUSYPROF
+        const long long tb1 = clock64();
+#endif
         uint32_t cnt_next;
         Rec rc_next;
 #ifdef BBF_T3_LATPROF
@@ -1049,7 +1060,14 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
 #ifdef BBF_T3_LATPROF
         if (tiny && lane == 0 && lat_seen) { T3_LAT(102 + pass, clock64() - t_lat); T3_LAT(112 + pass, 1); }
 #endif
+#ifdef BBF_T3_BUSYPROF
+        const long long tb2 = clock64();
+        if (lane == 0) { atomicAdd(&sh_busy[bcls][0], (unsigned long long)(tb1 - tb0)); atomicAdd(&sh_busy[bcls][1], (unsigned long long)(tb2 - tb1)); }
+#endif
         __syncthreads();
+#ifdef BBF_T3_BUSYPROF
+        if (tid == 0) { atomicAdd(&sh_busy[bcls][2], (unsigned long long)(clock64() - tb0) * kT3Warps); atomicAdd(&sh_busy[bcls][3], 1ull); }
+#endif
 #ifdef BBF_T3_LATPROF
         if (tiny && tid == 0) { T3_LAT(104 + pass, clock64() - t_lat); T3_LAT(114 + pass, 1); }
 #endif
@@ -1162,6 +1180,9 @@ __global__ void __launch_bounds__(kT3Threads, kT3Ctas) k_t3(const EngineArgs a) 
   }
 #ifdef BBF_T3_LATPROF
   if (tid < 20) atomicAdd(&g_prof_cnt[96 + tid], sh_lat[tid]);
+#endif
+#ifdef BBF_T3_BUSYPROF
+  if (tid < 24) atomicAdd(&g_prof_cnt[96 + tid], (&sh_busy[0][0])[tid]);
 #endif
 #ifdef BBF_T3_PROF
   if (tid == 0) {
@@ -1761,6 +1782,17 @@ bbf_status run_sparse_impl(bbf_graph* g, Plan* p, bool per_vertex, bool pairs, i
               ps, pc[106 + ps] / (double)(pc[108 + ps] + 1), pc[108 + ps], pc[96 + ps] / (double)(pc[98 + ps] + 1), pc[98 + ps],
               pc[100 + ps] / (double)(pc[110 + ps] + 1), pc[110 + ps], pc[102 + ps] / (double)(pc[112 + ps] + 1), pc[112 + ps],
               pc[104 + ps] / (double)(pc[114 + ps] + 1), pc[114 + ps]);
+#endif
+#ifdef BBF_T3_BUSYPROF
+    {
+      const char* bn2[6] = {"<2K", "<8K", "<32K", "<128K", "<512K", ">=512K"};
+      for (int b = 0; b < 6; ++b) {
+        const double span = (double)pc[96 + 4 * b + 2] + 1;
+        fprintf(stderr, "[bbf] t3 busy %-7s passes %8llu: long-record phase %.3f, short batches %.3f, barrier wait %.3f of warp-cycles\n",
+                bn2[b], pc[96 + 4 * b + 3], pc[96 + 4 * b] / span, pc[96 + 4 * b + 1] / span,
+                1.0 - (pc[96 + 4 * b] + pc[96 + 4 * b + 1]) / span);
+      }
+    }
 #endif
     const unsigned long long z40[128] = {};
     cudaMemcpyToSymbol(g_prof_cnt, z40, sizeof(z40));
