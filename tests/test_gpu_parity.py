@@ -506,7 +506,11 @@ def _sweep_graph(seed):
                               seed=seed)
 
 
-@pytest.mark.parametrize("seed", range(40))
+# BBF_SWEEP_SEEDS="a:b" widens the sweep (e.g. 40:400 for an extended run on the GPU box)
+_SWEEP = range(*map(int, os.environ.get("BBF_SWEEP_SEEDS", "0:40").split(":")))
+
+
+@pytest.mark.parametrize("seed", _SWEEP)
 def test_random_sweep_tiers_dense_topk(bbf, monkeypatch, seed):
     """Randomized sweep: per-vertex counts of the default tiering, of T3-only (T2 disabled, every
     start above the warp tier goes through the hub kernel) and of the dense path equal the
