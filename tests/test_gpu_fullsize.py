@@ -239,3 +239,34 @@ def test_per_edge_device_pointers_and_empty(bbf):
     with bbf.Graph.from_synth(e) as h:
         tot, eb, en = h.count_per_edge(e.row_ptr, e.col)
     assert eb.size == 0 and en.size == 0 and tot["balanced"] == 0
+
+
+_EDGE_SWEEP = range(*map(int, os.environ.get("BBF_EDGE_SWEEP_SEEDS", "0:12").split(":")))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", _EDGE_SWEEP)
+def test_per_edge_and_shards_sweep(bbf, monkeypatch, seed):
+    """Randomized sweep of the per-edge counts (all three tiers, both route-S directions) against
+    the oracle's per-edge definition, and of the per-vertex counts of an N-way fake world (N = 2..8
+    by seed) summed over the shards against the oracle's route-G per-vertex arrays."""
+    from test_gpu_parity import _sweep_graph
+    g = _sweep_graph(seed)
+    with bbf.Graph.from_synth(g) as h:
+        _, eb, en = h.count_per_edge(g.row_ptr, g.col)
+    wb, wn = O.edge_counts(g, threads=THREADS)
+    assert np.array_equal(eb, wb) and np.array_equal(en, wn)
+    N = 2 + seed % 7
+    acc = [np.zeros(g.n_u, dtype=object), np.zeros(g.n_u, dtype=object),
+           np.zeros(g.n_v, dtype=object), np.zeros(g.n_v, dtype=object)]
+    for r in range(N):
+        monkeypatch.setenv("BBF_FAKE_WORLD", f"{r}/{N}")
+        with bbf.Graph.from_synth(g) as h:
+            _, bu, nu, bv, nv = h.count_per_vertex()
+        for i, arr in enumerate((bu, nu, bv, nv)):
+            acc[i] += arr.astype(object)
+    monkeypatch.delenv("BBF_FAKE_WORLD")
+    want = O.route_g_pv(g, threads=THREADS)
+    got = [a.astype(np.uint64) for a in acc]
+    assert np.array_equal(got[0], want["bal_u"]) and np.array_equal(got[1], want["unb_u"])
+    assert np.array_equal(got[2], want["bal_v"]) and np.array_equal(got[3], want["unb_v"])
