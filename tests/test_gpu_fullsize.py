@@ -270,3 +270,31 @@ def test_per_edge_and_shards_sweep(bbf, monkeypatch, seed):
     got = [a.astype(np.uint64) for a in acc]
     assert np.array_equal(got[0], want["bal_u"]) and np.array_equal(got[1], want["unb_u"])
     assert np.array_equal(got[2], want["bal_v"]) and np.array_equal(got[3], want["unb_v"])
+
+
+def _large_variant(i):
+    """Large skewed stand-ins beyond the five configs (other sizes, exponents, hub weights and
+    sign mixes), same recipe as config 5: Chung-Lu keys, per-V Beta sign bias."""
+    spec = [(4_000_000, 1_000_000, 25_000_000, 1.8, 60_000.0, 80_000.0, (2.0, 2.0)),
+            (2_000_000, 3_000_000, 30_000_000, 2.1, 150_000.0, 40_000.0, (1.0, 3.0)),
+            (6_000_000, 500_000, 20_000_000, 2.4, 20_000.0, 200_000.0, (5.0, 1.0))][i]
+    n_u, n_v, m, gamma, wu, wv, (ba, bb) = spec
+    key, rng = G.chung_lu(n_u, n_v, m, gamma, wu, wv, 700 + i)
+    b = rng.beta(ba, bb, size=n_v)
+    s = rng.random(key.size) < b[key % n_v]
+    return G._from_sorted_keys(n_u, n_v, key, s, f"large{i}")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.environ.get("BBF_FULLSIZE_EXTRA"), reason="extended run: set BBF_FULLSIZE_EXTRA=1")
+@pytest.mark.parametrize("i", [0, 1, 2])
+def test_full_per_vertex_large_variants(bbf, i):
+    """The whole per-vertex arrays of large skewed graphs other than the configs equal the
+    oracle's route-G 4-role scatter element by element (extended run, minutes of oracle time)."""
+    g = _large_variant(i)
+    want = O.route_g_pv(g, threads=THREADS)
+    with bbf.Graph.from_synth(g) as h:
+        c = h.count_global()
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+    assert (c["balanced"], c["unbalanced"], c["wedges_G"]) == (want["B"], want["N"], want["W_G"])
+    assert_equal_arrays((bu, nu, bv, nv), want, f"large{i}")
