@@ -246,6 +246,18 @@ bbf_status bbf_estimate_global(uint32_t n_u, uint32_t n_v, const uint64_t *row_p
 bbf_status bbf_graph_stats(bbf_graph *g, uint64_t *kernel_launches, uint64_t *algo_bytes,
                            double *algo_ops, float *ms_main_kernel);
 
+/* Hybrid dense-core dispatch of the last bbf_count_global / bbf_count_per_vertex on this handle
+ * (NEXT-3, BASELINE north-star (3)): core_u / core_v = the number of top-priority
+ * vertices of U / V (side-local ranks, Def. Vertex Priority PAPER.md:600-609) whose induced
+ * subgraph was counted on the tensor cores while the rest of Alg. 2 ran on
+ * the sparse engine, the pairs between the two merged per pair before Lemma 2's f
+ * (PAPER.md:720-733); 0, 0 = no hybrid (plain sparse or whole-graph dense).  The counts are
+ * identical either way.  The dispatch is automatic (estimated engine time of the core's wedges
+ * vs the core's tensor time); env BBF_NO_HYBRID disables it, BBF_FORCE_SPARSE / BBF_FORCE_DENSE
+ * (at load or count) bypass it.  Requires every degree < 65,536 (pair counts packed 16 | 16)
+ * and cores of at most 8,192 per side.  Errors: BBF_EINVAL on a null handle. */
+bbf_status bbf_graph_hybrid_core(bbf_graph *g, uint32_t *core_u, uint32_t *core_v);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,7 @@ def lib():
         L.bbf_count_per_vertex.argtypes = [P, P, P, P, P, u32, P]
         L.bbf_count_pairs_topk.argtypes = [P, i32, u32, P, P, u32]
         L.bbf_graph_stats.argtypes = [P, P, P, P, P]
+        L.bbf_graph_hybrid_core.argtypes = [P, P, P]
         L.bbf_count_per_edge.argtypes = [P, P, P, P, P, u32, P]
         L.bbf_topk_vertices.argtypes = [P, i32, i32, u32, P, P, P]
         L.bbf_estimate_global.argtypes = [u32, u32, P, P, P, u32, C.c_double, u32, u64, i32, P, P,
@@ -77,7 +78,7 @@ def lib():
         L.bbf_device_sync.argtypes = [i32]
         for f in ("bbf_nccl_unique_id", "bbf_comm_init", "bbf_comm_free", "bbf_graph_load_csr",
                   "bbf_graph_free", "bbf_count_global", "bbf_count_global_base", "bbf_count_per_vertex",
-                  "bbf_count_pairs_topk", "bbf_graph_stats", "bbf_count_per_edge", "bbf_estimate_global", "bbf_topk_vertices",
+                  "bbf_count_pairs_topk", "bbf_graph_stats", "bbf_graph_hybrid_core", "bbf_count_per_edge", "bbf_estimate_global", "bbf_topk_vertices",
                   "bbf_upload_csr", "bbf_graph_load_upload", "bbf_upload_free", "bbf_device_sync"):
             getattr(L, f).restype = i32
         _lib = L
@@ -302,6 +303,12 @@ class Graph:
         return dict(kernel_launches=L.value, algo_bytes=B.value, algo_ops=ops.value,
                     ms_main_kernel=ms.value)
 
+    def hybrid_core(self) -> tuple:
+        """(core_u, core_v) of the last count's hybrid dispatch, (0, 0) = none (bbf_graph_hybrid_core)."""
+        a, b = C.c_uint32(), C.c_uint32()
+        _check(lib().bbf_graph_hybrid_core(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
 
 def estimate_global(n_u, n_v, row_ptr, col, sign, rho: float, trials: int, seed: int = 0,
                     device: int = 0, stream=None, comm: Comm | None = None, flags: int = 0) -> dict:
@@ -367,6 +374,10 @@ def bbf_count_per_edge(g: Graph, row_ptr, col, out=None):
 
 def bbf_graph_stats(g: Graph):
     return g.stats()
+
+
+def bbf_graph_hybrid_core(g: Graph):
+    return g.hybrid_core()
 
 
 bbf_estimate_global = estimate_global

@@ -25,7 +25,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["mem.cu", "graph_build.cu", "plan.cu", "count_sparse.cu", "dense_i8.cu", "estimate.cu", "base.cu", "api.cu"]
+SOURCES = ["mem.cu", "graph_build.cu", "plan.cu", "count_sparse.cu", "dense_i8.cu", "estimate.cu", "base.cu", "hybrid.cu", "api.cu"]
 HEADERS = ["bbf_internal.cuh"]
 
 
@@ -80,7 +80,7 @@ def build(force: bool = False, verbose: bool = False, variant: str | None = None
             if verbose:
                 print(open(log).read())
     if force or jobs or not os.path.exists(lib) or _stale(lib, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-ldl", "-lpthread"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-ldl", "-lpthread", "-lcublas"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

@@ -254,6 +254,7 @@ bbf_status wedges_g(bbf_graph* g, unsigned long long* w) {
 bool use_dense(bbf_graph* g, uint32_t flags, bool per_vertex) {
   if (flags & BBF_FORCE_SPARSE) return false;
   if (flags & BBF_FORCE_DENSE) return true;
+  if (getenv("BBF_HYBRID_CORE")) return false;  // test hook: a forced hybrid core (hybrid.cu)
   return dense_preferred(g, per_vertex);
 }
 
@@ -265,6 +266,7 @@ bbf_status do_count_local(bbf_graph* g, bool per_vertex, uint32_t flags, int ran
     BBF_CUDA(cudaMemsetAsync(g->pm, 0, 8ull * g->n, g->stream));
   }
   if (!g->wg_valid) BBF_TRY(ensure_plan_g(g));  // W_G of the graph (and the sparse plan)
+  g->last_nc[0] = g->last_nc[1] = 0;
   if (use_dense(g, flags, per_vertex)) {
     if (!dense_supported(g)) {
       set_error("BBF_FORCE_DENSE: graph not supported by the dense int8 path");
@@ -273,6 +275,15 @@ bbf_status do_count_local(bbf_graph* g, bool per_vertex, uint32_t flags, int ran
     return run_dense(g, per_vertex, rank, nranks, BN);
   }
   BBF_TRY(ensure_plan_g(g));
+  if (!(flags & BBF_FORCE_SPARSE)) {  // a dense core, if the graph has one worth it (hybrid.cu)
+    uint32_t nc[2];
+    hybrid_choose(g, per_vertex, nc);
+    if (nc[0] && nc[1]) {
+      g->last_nc[0] = nc[0];
+      g->last_nc[1] = nc[1];
+      return run_hybrid(g, nc, per_vertex, rank, nranks, BN);
+    }
+  }
   return run_sparse(g, &g->plan_g, per_vertex, rank, nranks, BN);
 }
 
@@ -517,6 +528,7 @@ bbf_status load_impl(uint32_t n_u, uint32_t n_v, const uint64_t* row_ptr, const 
 bbf_status bbf_graph_free(bbf_graph* g) {
   if (!g) return BBF_OK;
   cudaSetDevice(g->device);
+  free_hybrid(g);
   free_plan(&g->plan_g, g->stream);
   free_plan(&g->plan_s[0], g->stream);
   free_plan(&g->plan_s[1], g->stream);
@@ -849,6 +861,13 @@ bbf_status bbf_topk_vertices(bbf_graph* g, int side, int metric, uint32_t k, uin
   BBF_CUDA(cudaStreamSynchronize(st));
   for (void* p : {(void*)sc, (void*)sc2, (void*)id, (void*)id2, tmp}) dfree(p, st);
   *n_out = take;
+  return BBF_OK;
+}
+
+bbf_status bbf_graph_hybrid_core(bbf_graph* g, uint32_t* core_u, uint32_t* core_v) {
+  if (!g) { set_error("null graph"); return BBF_EINVAL; }
+  if (core_u) *core_u = g->last_nc[0];
+  if (core_v) *core_v = g->last_nc[1];
   return BBF_OK;
 }
 

@@ -227,7 +227,34 @@ struct Plan {
   // other side < 2^32) put (B | N << 32) of a record in ONE 64-bit RED into g->pm
   uint32_t rmid[2];
   int nranks;          // ranks the hub units were sized for
+  // hybrid dense-core plan (hybrid.cu): core = side-local ranks < nc[side]; the
+  // core wedges (core start, core middle, core end) are skipped (their ub moved past the middle's
+  // core ends); {0, 0} = the plain route
+  uint32_t nc[2];
   bool valid;
+};
+
+// hybrid dense-core state of a graph (hybrid.cu): built once per core size
+struct Hybrid {
+  uint32_t nc[2];          // core sizes the buffers below were built for ({0,0}: none)
+  uint32_t* ccnt;          // n: per row, # entries whose neighbour is in the other side's core
+  uint32_t cmaxdeg[2];     // max core degree (entries inside the core) of each side's core rows
+  uint32_t nwords[2];      // 32-bit bitmap words per core row of side s (over the other side's core)
+  uint32_t* bmA[2];        // core-row bitmaps: neighbour present
+  uint32_t* bmN[2];        //                    neighbour present with a negative edge
+  uint8_t* A[2];           // u8 dense operands of the core G[C] (rows_pad x k), zero padded
+  uint8_t* S[2];
+  uint64_t rows_pad[2], k[2];
+  uint8_t* A4[2];          // FP4 packed copies (dense_core_side)
+  uint8_t* S4[2];
+  uint32_t* R[2];          // nc[s] x nc[s] pair words: (a_r | d_r << 16), then (a_c | d_c << 16)
+  // fp16 copies for the tensor-core (cuBLAS) form of the mixed-pair terms: A, S and A', S' (the
+  // rows masked to each start's eligible core middles), rows_pad x k
+  uint16_t* Ah[2];
+  uint16_t* Sh[2];
+  uint16_t* Aeh[2];
+  uint16_t* Seh[2];
+  bool built;
 };
 
 }  // namespace bbf
@@ -289,6 +316,12 @@ struct bbf_graph {
   uint32_t maxdeg[2];
   long double ws_bound;  // overflow bound on B + N
   bbf::Plan plan_g;
+  bbf::Plan plan_h;     // route G with the hybrid core's wedges skipped
+  bbf::Hybrid hyb;
+  bool hyb_scored;            // hybrid_choose's candidate scores computed (once per graph)
+  uint32_t hyb_pick[2][2];    // chosen core sizes (global, per-vertex); {0, 0} = none
+  uint32_t last_nc[2];        // core sizes of the last count (bbf_graph_hybrid_core)
+  void* cublas;               // cublasHandle_t of the hybrid path's library GEMMs (lazily created)
   bbf::Plan plan_s[2];
   bbf::Plan plan_e[2];  // per-edge counts: route S(U) (ends after the start) and route 3 (ends before), all hub tier
   // scratch for the engine
@@ -356,7 +389,7 @@ bbf_status build_adj(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col, 
 bbf_status ensure_adj(bbf_graph* g);
 bbf_status build_dense_operands(bbf_graph* g, const uint64_t* d_rp, const uint32_t* d_col,
                                 const uint8_t* d_sg);
-bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3 = false);
+bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3 = false, const uint32_t* nc = nullptr);
 void free_plan(Plan* p, cudaStream_t st);
 // run the sparse engine for a route; per_vertex -> accumulate into g->pv (rank space)
 bbf_status run_sparse(bbf_graph* g, Plan* p, bool per_vertex, int rank, int nranks,
@@ -375,4 +408,16 @@ bool dense_supported(bbf_graph* g);
 // the (rank, nranks) shard of the work this process counts (communicator, or BBF_FAKE_WORLD)
 void shard_of(const bbf_graph* g, int* rank, int* nranks);
 bool dense_preferred(bbf_graph* g, bool per_vertex);
+// hybrid dense core (hybrid.cu): core sizes to use for a count ({0,0} = plain sparse route), and
+// the count itself (engine on plan_h + dense core + the mixed-pair correction)
+void hybrid_choose(bbf_graph* g, bool per_vertex, uint32_t nc[2]);
+bbf_status run_hybrid(bbf_graph* g, const uint32_t nc[2], bool per_vertex, int rank, int nranks,
+                      unsigned long long* host_BN);
+void free_hybrid(bbf_graph* g);
+// one side's pair counts of a dense 0/1 / +-1 operand pair (dense_i8.cu): rows_pad x k u8
+// operands, FP4 tensor-core kernels while exact (maxdeg <= 8192), else int8; adds (B, N) into
+// acc[0..1] and, when pv, the per-row counts into pv rows pv_row0 + i
+bbf_status dense_core_side(bbf_graph* g, uint32_t n_rows, uint64_t rows_pad, uint64_t k, uint8_t* A, uint8_t* S,
+                           uint8_t** A4, uint8_t** S4, uint32_t maxdeg, uint32_t pv_row0, bool per_vertex,
+                           int rank, int nranks, unsigned long long* acc, double* ops);
 }  // namespace bbf

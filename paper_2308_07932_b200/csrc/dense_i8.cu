@@ -1654,4 +1654,78 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
   return BBF_OK;
 }
 
+// One side of the hybrid path's dense core (hybrid.cu): the pair counts of the rows of a given u8
+// operand pair, exactly as run_dense does for a whole side (same kernels, same epilogue, per-row
+// counts into pv rows pv_row0 + i).  The FP4 copies are packed on first use into *A4 / *S4.
+bbf_status dense_core_side(bbf_graph* g, uint32_t n_rows, uint64_t rows_pad, uint64_t k, uint8_t* A, uint8_t* S,
+                           uint8_t** A4, uint8_t** S4, uint32_t maxdeg, uint32_t pv_row0, bool per_vertex,
+                           int rank, int nranks, unsigned long long* acc, double* ops) {
+  cudaStream_t st = g->stream;
+  if (n_rows < 2) return BBF_OK;
+  if (!encode_fn()) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return BBF_ECUDA;
+  }
+  const bool f4 = !getenv("BBF_DENSE_I8") && maxdeg <= 8192u;
+  uint2* dt = nullptr;
+  DenseArgs da{};
+  da.n_rows = n_rows;
+  da.pv_row0 = pv_row0;
+  da.n = g->n;
+  da.rank = rank;
+  da.nranks = nranks;
+  da.pv = per_vertex ? (unsigned long long*)g->pv : nullptr;
+  da.acc = acc;
+  std::vector<uint2> tl;
+  CUtensorMap m0, m1, m2, m3;
+  if (f4) {
+    const uint64_t k4 = round_up(k, 256) / 2;
+    if (!*A4) {
+      BBF_CUDA(dmalloc(A4, rows_pad * k4, st));
+      BBF_CUDA(dmalloc(S4, rows_pad * k4, st));
+      const uint64_t n8 = rows_pad * (k4 / 8);
+      const unsigned grid = (unsigned)std::min<uint64_t>((n8 + 255) / 256, 148ull * 32);
+      k_dense_pack_f4<<<grid, 256, 0, st>>>(A, k, *A4, k4, rows_pad);
+      k_dense_pack_f4<<<grid, 256, 0, st>>>(S, k, *S4, k4, rows_pad);
+      g->launches += 2;
+    }
+    if (!(make_map(&m0, *A4, rows_pad, k4, 128) && make_map(&m1, *S4, rows_pad, k4, 128) &&
+          make_map(&m2, *A4, rows_pad, k4, kF4JRows) && make_map(&m3, *S4, rows_pad, k4, kF4JRows))) {
+      set_error("cuTensorMapEncodeTiled failed");
+      return BBF_ECUDA;
+    }
+    tl = f4_tile_list((uint32_t)rows_pad);
+    da.n_kb = (uint32_t)(k4 / kBK);
+  } else {
+    if (!(make_map(&m0, A, rows_pad, k, 128) && make_map(&m1, S, rows_pad, k, 128))) {
+      set_error("cuTensorMapEncodeTiled failed");
+      return BBF_ECUDA;
+    }
+    tl = pair_tile_list((uint32_t)rows_pad);
+    da.n_kb = (uint32_t)(k / kBK);
+  }
+  BBF_CUDA(dmalloc(&dt, sizeof(uint2) * (tl.size() + 1), st));
+  BBF_CUDA(cudaMemcpyAsync(dt, tl.data(), sizeof(uint2) * tl.size(), cudaMemcpyHostToDevice, st));
+  da.tiles = dt;
+  da.n_tiles = (uint32_t)tl.size();
+  const unsigned pairs = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g->num_sms / 2, tl.size()));
+  if (f4 && maxdeg < 2048u && !getenv("BBF_DENSE_F4_TP")) {
+    BBF_CUDA(cudaFuncSetAttribute(k_dense_f4q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmemBytes));
+    k_dense_f4q<<<2 * pairs, kThreads, kQSmemBytes, st>>>(m0, m1, m2, m3, da);
+  } else if (f4) {
+    BBF_CUDA(cudaFuncSetAttribute(k_dense_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4SmemBytes));
+    k_dense_f4<<<2 * pairs, kThreads, kF4SmemBytes, st>>>(m0, m1, m2, m3, da);
+  } else {
+    BBF_CUDA(cudaFuncSetAttribute(k_dense_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmemBytes));
+    k_dense_pair<<<2 * pairs, kThreads, kPSmemBytes, st>>>(m0, m1, da);
+  }
+  g->launches++;
+  const cudaError_t err = cudaGetLastError();
+  dfree(dt, st);
+  if (err != cudaSuccess) return cuda_status(err, "dense core launch");
+  const double nr = n_rows, kk = (double)k;
+  *ops += 2.0 * 2.0 * (nr * (nr - 1.0) / 2.0) * kk;
+  return BBF_OK;
+}
+
 }  // namespace bbf

@@ -1,0 +1,718 @@
+// hybrid.cu — NEXT-3 (BASELINE north-star (3)): hybrid dispatch for graphs with a
+// dense core.  The core C is the top nc[s] vertices of each side by priority (side-local ranks
+// < nc[s]); G[C] is counted on the tensor cores, the rest of route G (Alg. 2)
+// on the sparse engine, and the pairs where the two meet are merged per pair before f (Lemma 2,
+// PAPER.md:720-733).  DESIGN.md §6b has the derivation; in short, every butterfly is counted by
+// route G once, at its highest-priority vertex x, as pair (x, w) with two middles, and
+//   * pair (x, w) not inside C: the engine counts it as always (no wedge of it is skipped);
+//   * pair inside C, both middles in C: the butterfly lies in G[C]; the engine skips these core
+//     wedges (plan.cu moves ub past the core ends of a core middle) and the dense core counts it
+//     with all four roles (the dense path's counts of G[C] are those of route G on G[C], the same
+//     butterflies, "each butterfly is counted once");
+//   * pair inside C with a middle outside C: with a = a_c + a_r, d = d_c + d_r (core / non-core
+//     eligible middles), the engine's bucket holds (a_r, d_r) and gives f(a_r, d_r) with shares
+//     from (a_r, d_r); this file adds the rest: f(a, d) - f(a_c, d_c) - f(a_r, d_r), i.e.
+//     balanced a_c a_r + d_c d_r, unbalanced a_c d_r + a_r d_c, to the pair's x and w and to the
+//     global count; to a non-core middle y of the pair (a_c, d_c) if its wedge is symmetric
+//     (agree) else (d_c, a_c); to a core middle v (a_r, d_r) if agree else (d_r, a_r).
+// (a_r, d_r) of the core pairs are accumulated from the non-core middles (k_mixed, mode 0) into a
+// per-side nc x nc word matrix R; (a_c, d_c) come from core-row bitmaps restricted to x's
+// eligible core middles (k_pairs), for the pairs with R != 0 only.  Every correction term is
+// linear in (a_r, d_r) for fixed (a_c, d_c), so ranks shard the non-core middles and sum.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include <cublas_v2.h>
+#include <cuda_fp16.h>
+
+#include "bbf_internal.cuh"
+
+namespace bbf {
+namespace {
+
+constexpr uint32_t kHybMaxCore = 8192;  // per side: bitmaps of <= 256 words, shared accumulators <= 128 KB
+__host__ __device__ constexpr uint32_t hyb_cand(int c) { return 1024u << c; }  // candidate core sizes 1024 .. 8192
+
+__device__ __forceinline__ bool is_core(uint32_t x, uint32_t n_u, uint32_t nc0, uint32_t nc1) {
+  return x < n_u ? x < nc0 : x - n_u < nc1;
+}
+
+// per row: entries whose neighbour is in the other side's core (a prefix: rows ascend by rank);
+// the largest such count over each side's core rows
+__global__ void k_core_cnt(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t n_u,
+                           uint32_t n, uint32_t nc0, uint32_t nc1, uint32_t* __restrict__ ccnt,
+                           unsigned int* __restrict__ cmax) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const uint32_t t = x < n_u ? nc1 : nc0;
+  uint32_t lo = off[x], hi = off[x + 1];
+  const uint32_t b = lo;
+  while (lo < hi) {
+    const uint32_t md = lo + (hi - lo) / 2;
+    if ((adj[md] & kMask) < t) lo = md + 1; else hi = md;
+  }
+  ccnt[x] = lo - b;
+  if (is_core(x, n_u, nc0, nc1)) atomicMax(&cmax[x < n_u ? 0 : 1], lo - b);
+}
+
+// dispatch statistics: for the first rows of each side, the entries below each candidate core size
+__global__ void k_core_cands(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj, uint32_t n_u,
+                             uint32_t rows0, uint32_t rows1, uint32_t* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows0 + rows1) return;
+  const uint32_t x = i < rows0 ? i : n_u + (i - rows0);
+  for (int c = 0; c < 4; ++c) {
+    uint32_t lo = off[x], hi = off[x + 1];
+    const uint32_t b = lo;
+    while (lo < hi) {
+      const uint32_t md = lo + (hi - lo) / 2;
+      if ((adj[md] & kMask) < hyb_cand(c)) lo = md + 1; else hi = md;
+    }
+    out[4ull * i + c] = lo - b;
+  }
+}
+
+// u8 operands (A = 1, S = +1 / -1 as 0xFF) and bitmaps of one side's core rows over the other
+// side's core columns; one warp per row, buffers zeroed beforehand
+__global__ void k_core_fill(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                            const uint32_t* __restrict__ ccnt, uint32_t row0, uint32_t nrows, uint8_t* __restrict__ A,
+                            uint8_t* __restrict__ S, uint64_t k, uint32_t* __restrict__ bmA, uint32_t* __restrict__ bmN,
+                            uint32_t nw) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows; r += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t x = row0 + r, b = off[x], c = ccnt[x];
+    for (uint32_t i = lane; i < c; i += 32) {
+      const uint32_t w = adj[b + i], col = w & kMask, bit = 1u << (col & 31);
+      A[r * k + col] = 1;
+      S[r * k + col] = (w & kNegBit) ? (uint8_t)0xFF : (uint8_t)1;
+      atomicOr(&bmA[(uint64_t)r * nw + (col >> 5)], bit);
+      if (w & kNegBit) atomicOr(&bmN[(uint64_t)r * nw + (col >> 5)], bit);
+    }
+  }
+}
+
+struct MixArgs {
+  const uint32_t *off, *adj, *rev, *mid, *ccnt;
+  uint32_t n_u, n, nc0, nc1;
+  uint32_t* R0;  // U-side core pairs
+  uint32_t* R1;  // V-side core pairs
+  unsigned long long* pv;
+  int rank, nranks;
+};
+
+// the mixed wedges x - y - w: y a non-core middle, x and w core vertices of the other side, x an
+// eligible start (r(y) > r(x), i.e. y at or after mid[x] in x's row) and l(w) > l(x).  One warp per
+// y (rank shard y mod N).  mode 0: R[x][w] += agree ? 1 : 1 << 16 (a_r, d_r); mode 1 (after
+// k_pairs turned R into (a_c, d_c)): y's share (a_c, d_c) if agree else (d_c, a_c)
+template <int MODE>
+__global__ void __launch_bounds__(256) k_mixed(MixArgs a) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;; t += nw) {
+    const uint64_t y64 = (uint64_t)t * a.nranks + a.rank;
+    if (y64 >= a.n) break;
+    const uint32_t y = (uint32_t)y64;
+    if (is_core(y, a.n_u, a.nc0, a.nc1)) continue;
+    const uint32_t c = a.ccnt[y];
+    if (c < 2) continue;
+    const uint32_t ob = y < a.n_u ? a.n_u : 0u;  // row base of the core side (x, w side)
+    const uint32_t ncs = y < a.n_u ? a.nc1 : a.nc0;
+    uint32_t* R = y < a.n_u ? a.R1 : a.R0;
+    const uint32_t b = a.off[y];
+    // eligible starts: a prefix of the core neighbours (descending priority)
+    uint32_t ky = 0;
+    for (uint32_t i0 = 0; i0 < c; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      bool el = false;
+      if (i < c) el = a.rev[b + i] >= a.mid[ob + (a.adj[b + i] & kMask)];
+      const uint32_t m = __ballot_sync(0xffffffffu, el);
+      ky += __popc(m);
+      if (m != 0xffffffffu) break;
+    }
+    if (ky > c - 1) ky = c - 1;  // the last core neighbour has no end after it
+    unsigned long long sB = 0, sN = 0;
+    for (uint32_t i = 0; i < ky; ++i) {
+      const uint32_t xi = a.adj[b + i];
+      const uint64_t rbase = (uint64_t)(xi & kMask) * ncs;
+      for (uint32_t j = i + 1 + lane; j < c; j += 32) {
+        const uint32_t wj = a.adj[b + j];
+        const bool agree = !((xi ^ wj) & kNegBit);
+        if (MODE == 0) {
+          atomicAdd(&R[rbase + (wj & kMask)], agree ? 1u : 1u << 16);
+        } else {
+          const uint32_t q = R[rbase + (wj & kMask)];
+          const uint32_t ac = q & 0xffffu, dc = q >> 16;
+          sB += agree ? ac : dc;
+          sN += agree ? dc : ac;
+        }
+      }
+    }
+    if (MODE == 1) {
+      for (int o = 16; o; o >>= 1) {
+        sB += __shfl_xor_sync(0xffffffffu, sB, o);
+        sN += __shfl_xor_sync(0xffffffffu, sN, o);
+      }
+      if (lane == 0 && (sB | sN)) {
+        atomicAdd(&a.pv[2ull * y], sB);
+        atomicAdd(&a.pv[2ull * y + 1], sN);
+      }
+    }
+  }
+}
+
+struct PairArgs {
+  uint32_t* R;                  // ncs x ncs
+  const uint32_t *bmA, *bmN;    // ncs x nw
+  const uint32_t *off, *adj, *mid, *ccnt;
+  uint32_t ncs, nco, nw, row0, pv_row0_other;
+  unsigned long long* pv;       // nullptr: global only
+  unsigned long long* acc;      // [0] B, [1] N
+};
+
+// core pairs of one side with R != 0: (a_c, d_c) over x's eligible core middles by bitmap
+// intersection, the cross terms to the global count and to x and w, the core middles' shares
+// into per-CTA shared accumulators (one per core column of the other side), and R[x][w] := (a_c,
+// d_c) for k_mixed<1>.  One warp per start row x.
+__global__ void __launch_bounds__(1024, 1) k_pairs(PairArgs a) {
+  extern __shared__ unsigned long long sacc[];  // 2 * nco (per-vertex only)
+  const uint32_t lane = threadIdx.x & 31;
+  const bool pv = a.pv != nullptr;
+  if (pv)
+    for (uint32_t i = threadIdx.x; i < 2 * a.nco; i += blockDim.x) sacc[i] = 0;
+  __syncthreads();
+  unsigned long long gB = 0, gN = 0;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < a.ncs; x += nwarps) {
+    const uint32_t row = a.row0 + x;
+    const uint32_t p0 = max(a.off[row], a.mid[row]), pe = a.off[row] + a.ccnt[row];
+    const uint32_t t = p0 < pe ? (a.adj[p0] & kMask) : a.nco;  // eligible core middles: rank >= t
+    uint32_t ax[8], nx[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t k = lane + 32u * q;
+      ax[q] = nx[q] = 0;
+      if (k < a.nw) {
+        const uint32_t lo = 32u * k;
+        const uint32_t msk = lo + 32u <= t ? 0u : (lo >= t ? 0xffffffffu : (0xffffffffu << (t - lo)));
+        ax[q] = a.bmA[(uint64_t)x * a.nw + k] & msk;
+        nx[q] = a.bmN[(uint64_t)x * a.nw + k];
+      }
+    }
+    unsigned long long xB = 0, xN = 0;
+    uint32_t* Rx = a.R + (uint64_t)x * a.ncs;
+    for (uint32_t w0 = x + 1; w0 < a.ncs; w0 += 32) {
+      const uint32_t w = w0 + lane;
+      const uint32_t q = w < a.ncs ? Rx[w] : 0u;
+      uint32_t m = __ballot_sync(0xffffffffu, q != 0);
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t wj = w0 + j, qj = __shfl_sync(0xffffffffu, q, j);
+        const uint32_t ar = qj & 0xffffu, dr = qj >> 16;
+        uint32_t ca = 0, cd = 0;
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) {
+          const uint32_t k = lane + 32u * qq;
+          if (k < a.nw && ax[qq]) {
+            const uint32_t both = ax[qq] & a.bmA[(uint64_t)wj * a.nw + k];
+            const uint32_t neg = nx[qq] ^ a.bmN[(uint64_t)wj * a.nw + k];
+            uint32_t ag = both & ~neg, di = both & neg;
+            ca += __popc(ag);
+            cd += __popc(di);
+            if (pv) {
+              while (ag) {
+                const uint32_t v = 32u * k + (__ffs(ag) - 1);
+                ag &= ag - 1;
+                atomicAdd(&sacc[2 * v], (unsigned long long)ar);
+                atomicAdd(&sacc[2 * v + 1], (unsigned long long)dr);
+              }
+              while (di) {
+                const uint32_t v = 32u * k + (__ffs(di) - 1);
+                di &= di - 1;
+                atomicAdd(&sacc[2 * v], (unsigned long long)dr);
+                atomicAdd(&sacc[2 * v + 1], (unsigned long long)ar);
+              }
+            }
+          }
+        }
+        for (int o = 16; o; o >>= 1) {
+          ca += __shfl_xor_sync(0xffffffffu, ca, o);
+          cd += __shfl_xor_sync(0xffffffffu, cd, o);
+        }
+        if (lane == 0) {
+          Rx[wj] = ca | (cd << 16);
+          const unsigned long long B = (unsigned long long)ca * ar + (unsigned long long)cd * dr;
+          const unsigned long long N = (unsigned long long)ca * dr + (unsigned long long)ar * cd;
+          gB += B;
+          gN += N;
+          if (pv && (B | N)) {
+            xB += B;
+            xN += N;
+            atomicAdd(&a.pv[2ull * (a.row0 + wj)], B);
+            atomicAdd(&a.pv[2ull * (a.row0 + wj) + 1], N);
+          }
+        }
+      }
+    }
+    if (pv && lane == 0 && (xB | xN)) {
+      atomicAdd(&a.pv[2ull * row], xB);
+      atomicAdd(&a.pv[2ull * row + 1], xN);
+    }
+  }
+  if (lane == 0 && (gB | gN)) {
+    atomicAdd(&a.acc[0], gB);
+    atomicAdd(&a.acc[1], gN);
+  }
+  __syncthreads();
+  if (pv)
+    for (uint32_t v = threadIdx.x; v < a.nco; v += blockDim.x) {
+      const unsigned long long B = sacc[2 * v], N = sacc[2 * v + 1];
+      if (B | N) {
+        atomicAdd(&a.pv[2ull * (a.pv_row0_other + v)], B);
+        atomicAdd(&a.pv[2ull * (a.pv_row0_other + v) + 1], N);
+      }
+    }
+}
+
+
+// ---------------------------------------------------------------------------- tensor-core form
+// The mixed-pair terms as library GEMMs on the tensor cores (fp16 operands holding small integers
+// exactly, fp32 accumulation, every partial sum < 2^22 checked on the device first):
+//   a_c, d_c of every core pair: G1 = A' A^T, G2 = S' S^T (a_c = (G1 + G2) / 2, d_c = (G1 - G2) / 2),
+//     A' / S' = the start's rows masked to its eligible core middles (rank >= t_x);
+//   the core middles' shares: M1 = TrU A, M2 = PrU S with TrU[x][w] = a_r + d_r, PrU = a_r - d_r
+//     for w > x (0 elsewhere); then B_v = (sum_x A'_xv M1_xv + S'_xv M2_xv) / 2 and
+//     N_v = (sum_x A'_xv M1_xv - S'_xv M2_xv) / 2 (agree ? (a_r, d_r) : (d_r, a_r) summed).
+__device__ __forceinline__ uint32_t elig_t(const uint32_t* off, const uint32_t* adj, const uint32_t* mid,
+                                          const uint32_t* ccnt, uint32_t row, uint32_t nco) {
+  const uint32_t p0 = max(off[row], mid[row]), pe = off[row] + ccnt[row];
+  return p0 < pe ? (adj[p0] & kMask) : nco;
+}
+
+// u8 A / S (rows_pad x k) -> fp16 A, S and the eligibility-masked A', S'
+__global__ void k_core_f16(const uint8_t* __restrict__ A, const uint8_t* __restrict__ S, uint64_t rows_pad, uint64_t k,
+                           uint32_t nrows, uint32_t nco, const uint32_t* __restrict__ off,
+                           const uint32_t* __restrict__ adj, const uint32_t* __restrict__ mid,
+                           const uint32_t* __restrict__ ccnt, uint32_t row0, __half* __restrict__ Ah,
+                           __half* __restrict__ Sh, __half* __restrict__ Aeh, __half* __restrict__ Seh) {
+  for (uint64_t r = blockIdx.x; r < rows_pad; r += gridDim.x) {
+    const uint32_t t = r < nrows ? elig_t(off, adj, mid, ccnt, row0 + (uint32_t)r, nco) : nco;
+    for (uint64_t c = threadIdx.x; c < k; c += blockDim.x) {
+      const uint64_t i = r * k + c;
+      const float a = A[i] ? 1.f : 0.f;
+      const float sv = S[i] == 1 ? 1.f : (S[i] == 0xFF ? -1.f : 0.f);
+      Ah[i] = __float2half(a);
+      Sh[i] = __float2half(sv);
+      Aeh[i] = __float2half(c >= t ? a : 0.f);
+      Seh[i] = __float2half(c >= t ? sv : 0.f);
+    }
+  }
+}
+
+// R -> TrU, PrU (fp16, rp x rp, upper triangle w > x), with the largest |entry| and row sum
+__global__ void k_r_f16(const uint32_t* __restrict__ R, uint32_t ncs, uint32_t rp, __half* __restrict__ Tr,
+                        __half* __restrict__ Pr, unsigned int* __restrict__ lim) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < rp; x += (gridDim.x * blockDim.x) >> 5) {
+    uint32_t mx = 0, sum = 0;
+    for (uint32_t w = lane; w < rp; w += 32) {
+      uint32_t ar = 0, dr = 0;
+      if (x < ncs && w < ncs && w > x) {
+        const uint32_t q = R[(uint64_t)x * ncs + w];
+        ar = q & 0xffffu;
+        dr = q >> 16;
+      }
+      Tr[(uint64_t)x * rp + w] = __float2half((float)(ar + dr));
+      Pr[(uint64_t)x * rp + w] = __float2half((float)ar - (float)dr);
+      mx = max(mx, ar + dr);
+      sum += ar + dr;
+    }
+    for (int o = 16; o; o >>= 1) {
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    }
+    if (lane == 0) {
+      atomicMax(&lim[0], mx);
+      atomicMax(&lim[1], sum);
+    }
+  }
+}
+
+// pairs with R != 0 from the GEMM outputs G1, G2 (row-major rp x rp): cross terms to the global
+// count, x and w; R := (a_c | d_c << 16)
+__global__ void k_pair_epi(uint32_t* __restrict__ R, const float* __restrict__ G1, const float* __restrict__ G2,
+                           uint32_t ncs, uint32_t rp, uint32_t row0, unsigned long long* __restrict__ pv,
+                           unsigned long long* __restrict__ acc) {
+  const uint32_t lane = threadIdx.x & 31;
+  unsigned long long gB = 0, gN = 0;
+  for (uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < ncs; x += (gridDim.x * blockDim.x) >> 5) {
+    unsigned long long xB = 0, xN = 0;
+    for (uint32_t w = x + 1 + lane; w < ncs; w += 32) {
+      const uint64_t i = (uint64_t)x * ncs + w;
+      const uint32_t q = R[i];
+      if (!q) continue;
+      const uint32_t ar = q & 0xffffu, dr = q >> 16;
+      const int g1 = (int)G1[(uint64_t)x * rp + w], g2 = (int)G2[(uint64_t)x * rp + w];
+      const uint32_t ca = (uint32_t)(g1 + g2) >> 1, cd = (uint32_t)(g1 - g2) >> 1;
+      R[i] = ca | (cd << 16);
+      const unsigned long long B = (unsigned long long)ca * ar + (unsigned long long)cd * dr;
+      const unsigned long long N = (unsigned long long)ca * dr + (unsigned long long)ar * cd;
+      gB += B;
+      gN += N;
+      if (pv && (B | N)) {
+        xB += B;
+        xN += N;
+        atomicAdd(&pv[2ull * (row0 + w)], B);
+        atomicAdd(&pv[2ull * (row0 + w) + 1], N);
+      }
+    }
+    if (pv) {
+      for (int o = 16; o; o >>= 1) {
+        xB += __shfl_xor_sync(0xffffffffu, xB, o);
+        xN += __shfl_xor_sync(0xffffffffu, xN, o);
+      }
+      if (lane == 0 && (xB | xN)) {
+        atomicAdd(&pv[2ull * (row0 + x)], xB);
+        atomicAdd(&pv[2ull * (row0 + x) + 1], xN);
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    gB += __shfl_xor_sync(0xffffffffu, gB, o);
+    gN += __shfl_xor_sync(0xffffffffu, gN, o);
+  }
+  if (lane == 0 && (gB | gN)) {
+    atomicAdd(&acc[0], gB);
+    atomicAdd(&acc[1], gN);
+  }
+}
+
+// core middles: X1_v = sum_x A'_xv M1_xv, X2_v = sum_x S'_xv M2_xv over row chunks (two's
+// complement u64 partial sums), then B_v = (X1 + X2) / 2, N_v = (X1 - X2) / 2 into pv
+constexpr uint32_t kMidRows = 128;
+__global__ void k_mid_epi(const __half* __restrict__ Aeh, const __half* __restrict__ Seh, const float* __restrict__ M1,
+                          const float* __restrict__ M2, uint32_t ncs, uint64_t k, uint32_t nco,
+                          unsigned long long* __restrict__ X) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nco) return;
+  const uint32_t x0 = blockIdx.y * kMidRows, x1 = min(ncs, x0 + kMidRows);
+  long long s1 = 0, s2 = 0;
+  for (uint32_t x = x0; x < x1; ++x) {
+    const uint64_t i = (uint64_t)x * k + v;
+    s1 += (long long)__half2float(Aeh[i]) * (long long)M1[i];
+    s2 += (long long)__half2float(Seh[i]) * (long long)M2[i];
+  }
+  if (s1) atomicAdd(&X[2ull * v], (unsigned long long)s1);
+  if (s2) atomicAdd(&X[2ull * v + 1], (unsigned long long)s2);
+}
+__global__ void k_mid_out(const unsigned long long* __restrict__ X, uint32_t nco, uint32_t pv_row0,
+                          unsigned long long* __restrict__ pv) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nco) return;
+  const unsigned long long x1 = X[2ull * v], x2 = X[2ull * v + 1];
+  const unsigned long long B = (x1 + x2) >> 1, N = (x1 - x2) >> 1;
+  if (B | N) {
+    atomicAdd(&pv[2ull * (pv_row0 + v)], B);
+    atomicAdd(&pv[2ull * (pv_row0 + v) + 1], N);
+  }
+}
+
+inline uint64_t rup(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace
+
+void free_hybrid(bbf_graph* g) {
+  Hybrid& h = g->hyb;
+  cudaStream_t st = g->stream;
+  void* ptrs[] = {h.ccnt, h.bmA[0], h.bmA[1], h.bmN[0], h.bmN[1], h.A[0], h.A[1], h.S[0], h.S[1],
+                  h.A4[0], h.A4[1], h.S4[0], h.S4[1], h.R[0], h.R[1], h.Ah[0], h.Ah[1], h.Sh[0], h.Sh[1],
+                  h.Aeh[0], h.Aeh[1], h.Seh[0], h.Seh[1]};
+  for (void* p : ptrs)
+    if (p) dfree(p, st);
+  std::memset(&h, 0, sizeof(h));
+  free_plan(&g->plan_h, st);
+  if (g->cublas) {
+    cublasDestroy((cublasHandle_t)g->cublas);
+    g->cublas = nullptr;
+  }
+}
+
+namespace {
+// the core's per-row counts, bitmaps, dense operands and pair matrices for core sizes nc
+bbf_status ensure_hybrid(bbf_graph* g, const uint32_t nc[2]) {
+  Hybrid& h = g->hyb;
+  if (h.built && h.nc[0] == nc[0] && h.nc[1] == nc[1]) return BBF_OK;
+  free_hybrid(g);
+  cudaStream_t st = g->stream;
+  const uint32_t n = g->n;
+  h.nc[0] = nc[0];
+  h.nc[1] = nc[1];
+  BBF_CUDA(dmalloc(&h.ccnt, 4ull * (n + 1), st));
+  unsigned int* d_cmax;
+  BBF_CUDA(dmalloc(&d_cmax, 8, st));
+  BBF_CUDA(cudaMemsetAsync(d_cmax, 0, 8, st));
+  if (n) {
+    k_core_cnt<<<(n + 255) / 256, 256, 0, st>>>(g->off, g->adj, g->n_u, n, nc[0], nc[1], h.ccnt, d_cmax);
+    g->launches++;
+  }
+  for (int s = 0; s < 2; ++s) {
+    const uint32_t nco = nc[1 - s];
+    h.nwords[s] = (nco + 31) / 32;
+    h.rows_pad[s] = rup(std::max<uint32_t>(nc[s], 1), 256);
+    h.k[s] = rup(std::max<uint32_t>(nco, 1), 128);
+    const uint64_t ob = h.rows_pad[s] * h.k[s], bb = 4ull * nc[s] * h.nwords[s] + 4;
+    BBF_CUDA(dmalloc(&h.A[s], ob, st));
+    BBF_CUDA(dmalloc(&h.S[s], ob, st));
+    BBF_CUDA(dmalloc(&h.bmA[s], bb, st));
+    BBF_CUDA(dmalloc(&h.bmN[s], bb, st));
+    BBF_CUDA(dmalloc(&h.R[s], 4ull * nc[s] * nc[s] + 4, st));
+    BBF_CUDA(cudaMemsetAsync(h.A[s], 0, ob, st));
+    BBF_CUDA(cudaMemsetAsync(h.S[s], 0, ob, st));
+    BBF_CUDA(cudaMemsetAsync(h.bmA[s], 0, bb, st));
+    BBF_CUDA(cudaMemsetAsync(h.bmN[s], 0, bb, st));
+    if (nc[s]) {
+      const unsigned grid = std::min<unsigned>((nc[s] + 7) / 8, 148u * 8u);
+      k_core_fill<<<grid, 256, 0, st>>>(g->off, g->adj, h.ccnt, s ? g->n_u : 0u, nc[s], h.A[s], h.S[s], h.k[s],
+                                        h.bmA[s], h.bmN[s], h.nwords[s]);
+      g->launches++;
+    }
+  }
+  BBF_CUDA(rb_add(h.cmaxdeg, d_cmax, 8, st)); g->launches++;
+  BBF_CUDA(rb_sync(st));
+  dfree(d_cmax, st);
+  h.built = true;
+  return BBF_OK;
+}
+}  // namespace
+
+// Core sizes for a count (DESIGN.md §6b "Hybrid dispatch"): env BBF_HYBRID_CORE=nu,nv forces them
+// (test hook), BBF_NO_HYBRID / a forced path at load disables; otherwise the candidate cores
+// c x c, c in {1024, ..., 8192}, are scored by the engine time of the core wedges they remove
+// (estimated from the core rows' inside-core degrees) against the dense core's tensor time and
+// the correction passes, and the best one with a clear gain is used.
+void hybrid_choose(bbf_graph* g, bool per_vertex, uint32_t nc[2]) {
+  nc[0] = nc[1] = 0;
+  if (g->load_flags & (BBF_FORCE_SPARSE | BBF_FORCE_DENSE)) return;
+  if (getenv("BBF_NO_HYBRID")) return;
+  // (a_r, d_r) and (a_c, d_c) are packed 16 | 16 in the pair words: every pair count of the core
+  // sides must stay below 2^16 (a + d <= min degree of the pair)
+  if (g->maxdeg[0] >= 65536u || g->maxdeg[1] >= 65536u) return;
+  if (const char* e = getenv("BBF_HYBRID_CORE")) {
+    unsigned a = 0, b = 0;
+    if (sscanf(e, "%u,%u", &a, &b) == 2) {
+      nc[0] = std::min<uint32_t>(std::min<uint32_t>(a, kHybMaxCore), g->L4[0]);
+      nc[1] = std::min<uint32_t>(std::min<uint32_t>(b, kHybMaxCore), g->L4[1]);
+      if (nc[0] < 2 || nc[1] < 2) nc[0] = nc[1] = 0;
+    }
+    return;
+  }
+  if (!g->adj_built || !g->plan_g.valid) return;
+  // inside-core degrees of the first rows at each candidate size (computed once per graph)
+  if (!g->hyb_scored) {
+    g->hyb_scored = true;
+    g->hyb_pick[0][0] = g->hyb_pick[0][1] = g->hyb_pick[1][0] = g->hyb_pick[1][1] = 0;
+    const uint32_t r0 = std::min(kHybMaxCore, g->L4[0]), r1 = std::min(kHybMaxCore, g->L4[1]);
+    if (r0 < 1024 || r1 < 1024) return;
+    cudaStream_t st = g->stream;
+    uint32_t* d_out;
+    if (dmalloc(&d_out, 16ull * (r0 + r1), st) != cudaSuccess) return;
+    k_core_cands<<<(r0 + r1 + 255) / 256, 256, 0, st>>>(g->off, g->adj, g->n_u, r0, r1, d_out);
+    g->launches++;
+    std::vector<uint32_t> hc(4ull * (r0 + r1));
+    cudaMemcpyAsync(hc.data(), d_out, 16ull * (r0 + r1), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    dfree(d_out, st);
+    // the engine's full-graph time at its measured rates (per-vertex ~2.7e11, global ~4e11 wedges/s)
+    for (int pvm = 0; pvm < 2; ++pvm) {
+      const double rate = pvm ? 2.7e11 : 4.0e11;
+      double best = 0;
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t cu = std::min(hyb_cand(c), g->L4[0]), cv = std::min(hyb_cand(c), g->L4[1]);
+        if (cu < hyb_cand(c) && cv < hyb_cand(c) && c) break;
+        double wc = 0;  // core wedges (pairs at each core middle), about half of them route G's
+        for (uint32_t i = 0; i < cu; ++i) { const double d = hc[4ull * i + c]; wc += d * (d - 1) / 2; }
+        for (uint32_t i = 0; i < cv; ++i) { const double d = hc[4ull * (r0 + i) + c]; wc += d * (d - 1) / 2; }
+        const double saved = 0.5 * wc / rate;
+        const double ops = 2.0 * 2.0 * ((double)cu * cu / 2 * cv + (pvm ? (double)cv * cv / 2 * cu : 0.0));
+        const double cost = ops / 4.0e15 + 3.0 * 4.0 * ((double)cu * cu + (double)cv * cv) / 5.0e12 + 1.5e-4;
+        const double gain = saved - cost;
+        if (gain > best && gain > 0.05 * ((double)g->plan_g.W_pruned / rate)) {
+          best = gain;
+          g->hyb_pick[pvm][0] = cu;
+          g->hyb_pick[pvm][1] = cv;
+        }
+      }
+    }
+  }
+  nc[0] = g->hyb_pick[per_vertex][0];
+  nc[1] = g->hyb_pick[per_vertex][1];
+}
+
+namespace {
+// The mixed-pair terms of one core side on the tensor cores (library GEMMs, see k_core_f16):
+// returns BBF_OK with *done = false when a bound for exact fp32 accumulation fails (the caller
+// then runs the bitmap kernel k_pairs, exact for any values).
+bbf_status mixed_side_gemm(bbf_graph* g, int s, bool per_vertex, bool* done) {
+  Hybrid& h = g->hyb;
+  cudaStream_t st = g->stream;
+  *done = false;
+  const uint32_t ncs = h.nc[s], nco = h.nc[1 - s];
+  const uint64_t rp = h.rows_pad[s], k = h.k[s];
+  if (ncs < 2) { *done = true; return BBF_OK; }
+  if (!h.Ah[s]) {  // fp16 operands of the core rows (graph-constant)
+    const uint64_t b = 2ull * rp * k;
+    BBF_CUDA(dmalloc(&h.Ah[s], b, st));
+    BBF_CUDA(dmalloc(&h.Sh[s], b, st));
+    BBF_CUDA(dmalloc(&h.Aeh[s], b, st));
+    BBF_CUDA(dmalloc(&h.Seh[s], b, st));
+    k_core_f16<<<(unsigned)std::min<uint64_t>(rp, 148ull * 16), 256, 0, st>>>(
+        h.A[s], h.S[s], rp, k, ncs, nco, g->off, g->adj, g->mid, h.ccnt, s ? g->n_u : 0u, (__half*)h.Ah[s],
+        (__half*)h.Sh[s], (__half*)h.Aeh[s], (__half*)h.Seh[s]);
+    g->launches++;
+  }
+  __half *Tr, *Pr;
+  float *G1, *G2, *M1 = nullptr, *M2 = nullptr;
+  unsigned int* lim;
+  BBF_CUDA(dmalloc(&Tr, 2ull * rp * rp, st));
+  BBF_CUDA(dmalloc(&Pr, 2ull * rp * rp, st));
+  BBF_CUDA(dmalloc(&lim, 8, st));
+  BBF_CUDA(cudaMemsetAsync(lim, 0, 8, st));
+  k_r_f16<<<(unsigned)std::min<uint64_t>((rp + 7) / 8, 148ull * 16), 256, 0, st>>>(h.R[s], ncs, (uint32_t)rp, Tr, Pr,
+                                                                                  lim);
+  g->launches++;
+  unsigned int hl[2] = {0, 0};
+  BBF_CUDA(rb_add(hl, lim, 8, st)); g->launches++;
+  BBF_CUDA(rb_sync(st));
+  dfree(lim, st);
+  // fp16 holds integers <= 2048 exactly; every fp32 partial sum stays below 2^22 (G1, G2 <= nco;
+  // |M1|, |M2| <= the largest row sum of TrU)
+  const bool exact = hl[0] <= 2048u && hl[1] < (1u << 22) && nco < (1u << 22) && !getenv("BBF_HYBRID_BITS");
+  if (!exact) {
+    dfree(Tr, st);
+    dfree(Pr, st);
+    return BBF_OK;
+  }
+  if (!g->cublas) {
+    cublasHandle_t hd;
+    if (cublasCreate(&hd) != CUBLAS_STATUS_SUCCESS) { set_error("cublasCreate failed"); return BBF_ECUDA; }
+    g->cublas = hd;
+  }
+  cublasHandle_t hd = (cublasHandle_t)g->cublas;
+  cublasSetStream(hd, st);
+  BBF_CUDA(dmalloc(&G1, 4ull * rp * rp, st));
+  BBF_CUDA(dmalloc(&G2, 4ull * rp * rp, st));
+  const float one = 1.f, zero = 0.f;
+  bool ok = true;
+  // G1 = A' A^T, G2 = S' S^T (row-major rp x rp; column-major C' = A . A'^T)
+  ok &= cublasGemmEx(hd, CUBLAS_OP_T, CUBLAS_OP_N, (int)rp, (int)rp, (int)k, &one, h.Ah[s], CUDA_R_16F, (int)k,
+                     h.Aeh[s], CUDA_R_16F, (int)k, &zero, G1, CUDA_R_32F, (int)rp, CUBLAS_COMPUTE_32F,
+                     CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
+  ok &= cublasGemmEx(hd, CUBLAS_OP_T, CUBLAS_OP_N, (int)rp, (int)rp, (int)k, &one, h.Sh[s], CUDA_R_16F, (int)k,
+                     h.Seh[s], CUDA_R_16F, (int)k, &zero, G2, CUDA_R_32F, (int)rp, CUBLAS_COMPUTE_32F,
+                     CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
+  if (ok && per_vertex) {
+    BBF_CUDA(dmalloc(&M1, 4ull * rp * k, st));
+    BBF_CUDA(dmalloc(&M2, 4ull * rp * k, st));
+    // M1 = TrU A, M2 = PrU S (row-major rp x k; column-major C' = A^T-view . TrU-view)
+    ok &= cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_N, (int)k, (int)rp, (int)rp, &one, h.Ah[s], CUDA_R_16F, (int)k,
+                       Tr, CUDA_R_16F, (int)rp, &zero, M1, CUDA_R_32F, (int)k, CUBLAS_COMPUTE_32F,
+                       CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
+    ok &= cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_N, (int)k, (int)rp, (int)rp, &one, h.Sh[s], CUDA_R_16F, (int)k,
+                       Pr, CUDA_R_16F, (int)rp, &zero, M2, CUDA_R_32F, (int)k, CUBLAS_COMPUTE_32F,
+                       CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
+  }
+  g->launches += per_vertex ? 4 : 2;
+  if (!ok) { set_error("cublasGemmEx failed"); return BBF_ECUDA; }
+  const unsigned pgrid = (unsigned)std::min<uint64_t>((ncs + 7) / 8, 148ull * 16);
+  k_pair_epi<<<pgrid, 256, 0, st>>>(h.R[s], G1, G2, ncs, (uint32_t)rp, s ? g->n_u : 0u,
+                                    per_vertex ? (unsigned long long*)g->pv : nullptr, g->d_acc + 4);
+  g->launches++;
+  if (per_vertex) {
+    unsigned long long* X;
+    BBF_CUDA(dmalloc(&X, 16ull * nco + 16, st));
+    BBF_CUDA(cudaMemsetAsync(X, 0, 16ull * nco + 16, st));
+    k_mid_epi<<<dim3((nco + 255) / 256, (ncs + kMidRows - 1) / kMidRows), 256, 0, st>>>(
+        (const __half*)h.Aeh[s], (const __half*)h.Seh[s], M1, M2, ncs, k, nco, X);
+    k_mid_out<<<(nco + 255) / 256, 256, 0, st>>>(X, nco, s ? 0u : g->n_u, (unsigned long long*)g->pv);
+    g->launches += 2;
+    dfree(X, st);
+    dfree(M1, st);
+    dfree(M2, st);
+  }
+  dfree(G1, st);
+  dfree(G2, st);
+  dfree(Tr, st);
+  dfree(Pr, st);
+  *done = true;
+  return BBF_OK;
+}
+}  // namespace
+
+bbf_status run_hybrid(bbf_graph* g, const uint32_t nc[2], bool per_vertex, int rank, int nranks,
+                      unsigned long long* host_BN) {
+  NvtxRange nvtx_("bbf::hybrid");
+  cudaStream_t st = g->stream;
+  BBF_TRY(ensure_adj(g));
+  BBF_TRY(ensure_hybrid(g, nc));
+  Plan* p = &g->plan_h;
+  if (p->valid && (p->nranks != nranks || p->nc[0] != nc[0] || p->nc[1] != nc[1])) free_plan(p, st);
+  if (!p->valid) BBF_TRY(make_plan(g, 0, p, false, nc));
+  // 1. the sparse remainder: route G without the core wedges
+  unsigned long long BN_e[2] = {0, 0};
+  BBF_TRY(run_sparse(g, p, per_vertex, rank, nranks, BN_e));
+  const uint64_t algo_bytes = g->algo_bytes;
+  const float ms_engine = g->ms_main;
+  Hybrid& h = g->hyb;
+  // 2. the dense core G[C]: U side (global and U core rows), V side for the V core rows
+  BBF_CUDA(cudaMemsetAsync(g->d_acc, 0, 32 * sizeof(unsigned long long), st));
+  double ops = 0;
+  BBF_TRY(dense_core_side(g, nc[0], h.rows_pad[0], h.k[0], h.A[0], h.S[0], &h.A4[0], &h.S4[0], h.cmaxdeg[0], 0u,
+                          per_vertex, rank, nranks, g->d_acc, &ops));
+  if (per_vertex)
+    BBF_TRY(dense_core_side(g, nc[1], h.rows_pad[1], h.k[1], h.A[1], h.S[1], &h.A4[1], &h.S4[1], h.cmaxdeg[1],
+                            g->n_u, per_vertex, rank, nranks, g->d_acc + 2, &ops));
+  // 3. the mixed core pairs: (a_r, d_r), then (a_c, d_c) and the cross terms, then the non-core
+  // middles' shares
+  for (int s = 0; s < 2; ++s) BBF_CUDA(cudaMemsetAsync(h.R[s], 0, 4ull * nc[s] * nc[s], st));
+  MixArgs ma{g->off, g->adj, g->rev, g->mid, h.ccnt, g->n_u, g->n, nc[0], nc[1], h.R[0], h.R[1],
+             (unsigned long long*)g->pv, rank, nranks};
+  const unsigned mgrid = (unsigned)std::min<uint64_t>((g->n / std::max(nranks, 1) + 7) / 8 + 1, 148ull * 16);
+  k_mixed<0><<<mgrid, 256, 0, st>>>(ma);
+  g->launches++;
+  for (int s = 0; s < 2; ++s) {
+    bool done = false;
+    BBF_TRY(mixed_side_gemm(g, s, per_vertex, &done));
+    if (done) continue;
+    PairArgs pa{h.R[s], h.bmA[s], h.bmN[s], g->off, g->adj, g->mid, h.ccnt, nc[s], nc[1 - s], h.nwords[s],
+                s ? g->n_u : 0u, s ? 0u : g->n_u, per_vertex ? (unsigned long long*)g->pv : nullptr, g->d_acc + 4};
+    const int smem = per_vertex ? (int)(16u * nc[1 - s]) : 0;
+    if (smem > 48 * 1024) BBF_CUDA(cudaFuncSetAttribute(k_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_pairs<<<(unsigned)g->num_sms, 1024, smem, st>>>(pa);
+    g->launches++;
+  }
+  if (per_vertex) {
+    k_mixed<1><<<mgrid, 256, 0, st>>>(ma);
+    g->launches++;
+  }
+  BBF_CUDA(cudaGetLastError());
+  unsigned long long hacc[6] = {0, 0, 0, 0, 0, 0};
+  BBF_CUDA(rb_add(hacc, g->d_acc, sizeof(hacc), st)); g->launches++;
+  BBF_CUDA(rb_sync(st));
+  host_BN[0] = BN_e[0] + hacc[0] + hacc[4];
+  host_BN[1] = BN_e[1] + hacc[1] + hacc[5];
+  g->algo_bytes = algo_bytes;
+  g->algo_ops = ops;
+  g->ms_main = ms_engine;
+  if (getenv("BBF_DEBUG"))
+    fprintf(stderr,
+            "[bbf] hybrid core %ux%u (core degrees <= %u / %u): engine B %llu N %llu (W_pruned %llu of W_G %llu), "
+            "dense core B %llu N %llu, mixed pairs B %llu N %llu\n",
+            nc[0], nc[1], h.cmaxdeg[0], h.cmaxdeg[1], BN_e[0], BN_e[1], (unsigned long long)p->W_pruned,
+            (unsigned long long)p->W_full, hacc[0], hacc[1], hacc[4], hacc[5]);
+  return BBF_OK;
+}
+
+}  // namespace bbf

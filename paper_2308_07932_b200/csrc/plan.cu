@@ -22,6 +22,13 @@ namespace {
 struct RouteRows {
   int route;  // 0 G, 1 S(U), 2 S(V), 3 S(U) with the ends BEFORE the start (per-edge counts)
   uint32_t n_u, n;
+  // hybrid core (route G only): rows of side-local rank < nc[side] are core; ccnt[row] = the
+  // row's entries inside the other side's core (a prefix: rows are sorted by local rank)
+  uint32_t nc0, nc1;
+  const uint32_t* ccnt;
+  __device__ __forceinline__ bool core(uint32_t x) const {
+    return x < n_u ? x < nc0 : x - n_u < nc1;
+  }
   __device__ __forceinline__ bool in_route(uint32_t x) const {
     return route == 0 || (route == 1 || route == 3 ? x < n_u : x >= n_u);
   }
@@ -79,9 +86,12 @@ __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
           const uint32_t f = off[rv + 1];
           const uint32_t u = r + 1;  // x's entry in its middle's row is the reverse entry
           const uint32_t en = end1[rv];
-          ub[e] = u;
+          // hybrid: a core start's wedges through a core middle skip the core ends (counted by
+          // the dense core, hybrid.cu); W_G (full) stays the paper's count
+          const uint32_t u2 = (rr.ccnt && rr.core(x) && rr.core(rv)) ? max(u, off[rv] + rr.ccnt[rv]) : u;
+          ub[e] = u2;
           full += f - u;
-          l_seg = en > u ? en - u : 0;
+          l_seg = en > u2 ? en - u2 : 0;
         }
       }
       if (win) {
@@ -275,14 +285,17 @@ void free_plan(Plan* p, cudaStream_t st) {
   *p = Plan{};
 }
 
-bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3) {
+bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3, const uint32_t* nc) {
   NvtxRange nvtx_("bbf::make_plan");
   cudaStream_t st = g->stream;
   const uint32_t n = g->n;
   const uint64_t m = 2 * g->nnz;
   free_plan(p, st);
   p->route = route;
-  RouteRows rr{route, g->n_u, n};
+  const bool hyb = route == 0 && nc && nc[0] && nc[1] && g->hyb.ccnt;
+  p->nc[0] = hyb ? nc[0] : 0u;
+  p->nc[1] = hyb ? nc[1] : 0u;
+  RouteRows rr{route, g->n_u, n, p->nc[0], p->nc[1], hyb ? g->hyb.ccnt : nullptr};
   BBF_CUDA(dmalloc(&p->ub, 4ull * (m + 1), st));
   BBF_CUDA(dmalloc(&p->work, 8ull * (n + 1), st));
   uint32_t *sb, *se, *nunits, *ustart;

@@ -268,6 +268,41 @@ def config5(seed: int = 5) -> SignedBipartite:
     return _from_sorted_keys(n_u, n_v, key, s, "config5")
 
 
+def core_periphery(n_u: int, n_v: int, m: int, gamma: float, wmax_u: float, wmax_v: float, core_u: int,
+                   core_v: int, p_core: float, p_pos: float, seed: int, name: str = "",
+                   core_random: bool = False) -> SignedBipartite:
+    """A Chung-Lu power-law periphery (chung_lu above, m distinct pairs) plus a planted dense core
+    of core_u x core_v vertices, each of its pairs present w.p. p_core (drawn in row blocks of
+    1,024 after the periphery); the core sits on the highest-weight ids [0, core_u) x [0, core_v),
+    or (core_random) on ids drawn without replacement after the block (a dense community away from
+    the periphery's hubs).  Then every edge of the union positive w.p. p_pos (CSR order).  Stands
+    in for the dense-core / sparse-remainder regime of NEXT-3 (the Senate/House-like dense
+    blocks, inside a power-law graph)."""
+    key, rng = chung_lu(n_u, n_v, m, gamma, wmax_u, wmax_v, seed)
+    blocks = []
+    for r0 in range(0, core_u, 1024):
+        rows = min(1024, core_u - r0)
+        uu, vv = np.nonzero(rng.random((rows, core_v)) < p_core)
+        blocks.append((uu.astype(np.int64) + r0, vv.astype(np.int64)))
+    bu = np.concatenate([b[0] for b in blocks]) if blocks else np.zeros(0, np.int64)
+    bv = np.concatenate([b[1] for b in blocks]) if blocks else np.zeros(0, np.int64)
+    if core_random:
+        bu = rng.choice(n_u, size=core_u, replace=False)[bu]
+        bv = rng.choice(n_v, size=core_v, replace=False)[bv]
+    key = np.unique(np.concatenate([key, bu * n_v + bv]))
+    s = rng.random(key.size) < p_pos
+    return _from_sorted_keys(n_u, n_v, key, s, name or f"cp{n_u}x{n_v}_c{core_u}x{core_v}_s{seed}")
+
+
+def config_hybrid(seed: int = 6) -> SignedBipartite:
+    """The NEXT-3 hybrid workload (not a BASELINE config): a dense community of 8,192 x 8,192
+    vertices at density 0.2 (~13.4M edges, degrees ~1,640; placed on random ids) inside a Chung-Lu
+    power-law periphery of |U|=1M, |V|=200K, 5M distinct pairs, exponent 2.1, weight max 1,000
+    (so the community is the top of the priority order); signs iid positive w.p. 0.8."""
+    return core_periphery(1_000_000, 200_000, 5_000_000, 2.1, 1_000.0, 1_000.0, 8192, 8192, 0.2, 0.8, seed,
+                          "config_hybrid", core_random=True)
+
+
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
 
 
