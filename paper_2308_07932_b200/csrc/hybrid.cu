@@ -521,25 +521,47 @@ void hybrid_choose(bbf_graph* g, bool per_vertex, uint32_t nc[2]) {
     if (dmalloc(&d_out, 16ull * (r0 + r1), st) != cudaSuccess) return;
     k_core_cands<<<(r0 + r1 + 255) / 256, 256, 0, st>>>(g->off, g->adj, g->n_u, r0, r1, d_out);
     g->launches++;
-    std::vector<uint32_t> hc(4ull * (r0 + r1));
+    std::vector<uint32_t> hc(4ull * (r0 + r1)), dg(r0 + r1);
     cudaMemcpyAsync(hc.data(), d_out, 16ull * (r0 + r1), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(dg.data(), g->degs, 4ull * r0, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(dg.data() + r0, g->degs + g->n_u, 4ull * r1, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     dfree(d_out, st);
-    // the engine's full-graph time at its measured rates (per-vertex ~2.7e11, global ~4e11 wedges/s)
+    // A core pays only when it is closed: most of its vertices' edges stay inside it.  Otherwise
+    // (power-law hubs: dense among themselves but with most edges to the periphery) the skipped
+    // core wedges were cheap for the engine anyway (dense counter windows), the remainder keeps
+    // nearly all of the work, and the mixed pairs' counts grow past the exact fp16 range
+    // (measured: configs 3 and 5 are 1.3-7x slower with any core).
     for (int pvm = 0; pvm < 2; ++pvm) {
-      const double rate = pvm ? 2.7e11 : 4.0e11;
+      const double rate = pvm ? 2.7e11 : 4.0e11;  // the engine's measured per-vertex / global rates
       double best = 0;
       for (int c = 0; c < 4; ++c) {
         const uint32_t cu = std::min(hyb_cand(c), g->L4[0]), cv = std::min(hyb_cand(c), g->L4[1]);
         if (cu < hyb_cand(c) && cv < hyb_cand(c) && c) break;
-        double wc = 0;  // core wedges (pairs at each core middle), about half of them route G's
-        for (uint32_t i = 0; i < cu; ++i) { const double d = hc[4ull * i + c]; wc += d * (d - 1) / 2; }
-        for (uint32_t i = 0; i < cv; ++i) { const double d = hc[4ull * (r0 + i) + c]; wc += d * (d - 1) / 2; }
+        double wc = 0, din = 0, dall = 0;  // core wedges (pairs at each core middle); closedness
+        for (uint32_t i = 0; i < cu; ++i) {
+          const double d = hc[4ull * i + c];
+          wc += d * (d - 1) / 2;
+          din += d;
+          dall += dg[i];
+        }
+        for (uint32_t i = 0; i < cv; ++i) {
+          const double d = hc[4ull * (r0 + i) + c];
+          wc += d * (d - 1) / 2;
+          din += d;
+          dall += dg[r0 + i];
+        }
+        const double closed = dall > 0 ? din / dall : 0.0;
         const double saved = 0.5 * wc / rate;
         const double ops = 2.0 * 2.0 * ((double)cu * cu / 2 * cv + (pvm ? (double)cv * cv / 2 * cu : 0.0));
-        const double cost = ops / 4.0e15 + 3.0 * 4.0 * ((double)cu * cu + (double)cv * cv) / 5.0e12 + 1.5e-4;
+        const double gemm = 2.0 * 2.0 * ((double)cu * cu * cv + (double)cv * cv * cu) * (pvm ? 2.0 : 1.0);
+        const double cost = ops / 4.0e15 + gemm / 1.5e15 + 6.0 * 4.0 * ((double)cu * cu + (double)cv * cv) / 5.0e12 +
+                            1.0e-3;
         const double gain = saved - cost;
-        if (gain > best && gain > 0.05 * ((double)g->plan_g.W_pruned / rate)) {
+        if (getenv("BBF_DEBUG"))
+          fprintf(stderr, "[bbf] hybrid candidate %ux%u (%s): closed %.3f, core wedges %.3e, saved %.3f ms, cost %.3f ms\n",
+                  cu, cv, pvm ? "per-vertex" : "global", closed, wc, saved * 1e3, cost * 1e3);
+        if (closed >= 0.5 && gain > best && gain > 0.1 * ((double)g->plan_g.W_pruned / rate)) {
           best = gain;
           g->hyb_pick[pvm][0] = cu;
           g->hyb_pick[pvm][1] = cv;
