@@ -33,6 +33,8 @@ WORKLOADS = {
     3: "configs[2]: Chung-Lu 1M x 200K, 10M edges, gamma=2.1, p+=0.8",
     4: "configs[3]: dense block 16,384^2, density 0.05, p+=0.5",
     5: "configs[4]: Chung-Lu 8M x 2M, 50M edges, gamma=1.9, per-V Beta(3,1) sign bias",
+    6: "NEXT-3 hybrid workload (not a BASELINE config): 8,192^2 community at density 0.2 in a Chung-Lu "
+       "1M x 200K periphery (5M edges, gamma=2.1, weight max 1,000), p+=0.8",
 }
 
 

@@ -303,7 +303,7 @@ def config_hybrid(seed: int = 6) -> SignedBipartite:
                           "config_hybrid", core_random=True)
 
 
-CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
+CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5, 6: config_hybrid}  # 6: NEXT-3 workload
 
 
 def make_config(i: int) -> SignedBipartite:

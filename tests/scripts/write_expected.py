@@ -1,4 +1,5 @@
-"""Write tests/golden/expected_counts.json: the oracle's counts for the five BASELINE configs.
+"""Write tests/golden/expected_counts.json: the oracle's counts for the five BASELINE configs and
+the NEXT-3 hybrid workload (synth.graphs.config_hybrid, "config 6").
 
 Calls only oracle/ (Alg. 2 + 4-role scatter, oracle_route_g_pv) and synth/ (the seeded input
 generators).  Nothing here reads the CUDA path.  bench.py asserts its counts against this file
@@ -7,7 +8,7 @@ directly.  Per config: the graph's SHA-256 (synth.graphs.SignedBipartite.sha256)
 the SHA-256 of the per-vertex arrays (bal_u, unb_u, bal_v, unb_v as little-endian uint64,
 concatenated in that order).
 
-    python tests/scripts/write_expected.py [configs...]      (default: 1 2 3 4 5)
+    python tests/scripts/write_expected.py [configs...]      (default: 1 2 3 4 5 6)
 """
 import hashlib
 import json
@@ -50,4 +51,4 @@ def main(cfgs):
 
 
 if __name__ == "__main__":
-    main([int(a) for a in sys.argv[1:]] or [1, 2, 3, 4, 5])
+    main([int(a) for a in sys.argv[1:]] or [1, 2, 3, 4, 5, 6])

@@ -42,7 +42,7 @@ def test_reference_arm_other_ranks_silent():
     assert not [l for l in r.stdout.splitlines() if l.startswith("{")]
 
 
-@pytest.mark.parametrize("config", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("config", [1, 2, 3, 4, 5, 6])
 def test_expected_counts_complete(config):
     with open(os.path.join(ROOT, "tests", "golden", "expected_counts.json")) as f:
         exp = json.load(f)
