@@ -265,8 +265,24 @@ bbf_status do_count_local(bbf_graph* g, bool per_vertex, uint32_t flags, int ran
     BBF_CUDA(cudaMemsetAsync(g->pe, 0, 8ull * g->n, g->stream));
     BBF_CUDA(cudaMemsetAsync(g->pm, 0, 8ull * g->n, g->stream));
   }
-  if (!g->wg_valid) BBF_TRY(ensure_plan_g(g));  // W_G of the graph (and the sparse plan)
   g->last_nc[0] = g->last_nc[1] = 0;
+  // a dense core, if the graph has one worth it (hybrid.cu); graphs loaded as dense candidates
+  // (W_G known at load) first get the whole-graph dense check
+  const bool dense_first = (g->dense_cand && !getenv("BBF_HYBRID_CORE")) || (flags & BBF_FORCE_DENSE);
+  if (!dense_first && !(flags & BBF_FORCE_SPARSE)) {
+    BBF_TRY(ensure_adj(g));
+    uint32_t nc[2];
+    hybrid_choose(g, per_vertex, nc);
+    if (nc[0] && nc[1]) {
+      g->last_nc[0] = nc[0];
+      g->last_nc[1] = nc[1];
+      BBF_TRY(run_hybrid(g, nc, per_vertex, rank, nranks, BN));
+      g->W_G = g->plan_h.W_full;  // the hybrid plan's unclamped count is the paper's W_G
+      g->wg_valid = true;
+      return BBF_OK;
+    }
+  }
+  if (!g->wg_valid) BBF_TRY(ensure_plan_g(g));  // W_G of the graph (and the sparse plan)
   if (use_dense(g, flags, per_vertex)) {
     if (!dense_supported(g)) {
       set_error("BBF_FORCE_DENSE: graph not supported by the dense int8 path");
@@ -275,15 +291,6 @@ bbf_status do_count_local(bbf_graph* g, bool per_vertex, uint32_t flags, int ran
     return run_dense(g, per_vertex, rank, nranks, BN);
   }
   BBF_TRY(ensure_plan_g(g));
-  if (!(flags & BBF_FORCE_SPARSE)) {  // a dense core, if the graph has one worth it (hybrid.cu)
-    uint32_t nc[2];
-    hybrid_choose(g, per_vertex, nc);
-    if (nc[0] && nc[1]) {
-      g->last_nc[0] = nc[0];
-      g->last_nc[1] = nc[1];
-      return run_hybrid(g, nc, per_vertex, rank, nranks, BN);
-    }
-  }
   return run_sparse(g, &g->plan_g, per_vertex, rank, nranks, BN);
 }
 

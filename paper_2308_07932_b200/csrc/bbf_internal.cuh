@@ -300,6 +300,7 @@ struct bbf_graph {
   uint8_t* in_sg;
   bool adj_built;
   bool wg_valid;
+  bool dense_cand;    // loaded as a dense-path candidate (W_G computed at load, dense checked first)
   unsigned long long W_G;  // paper wedge count (O(nnz) formula), valid if wg_valid
   // dense operands (dense_i8.cu): per side A (u8 0/1) and S (s8 +-1/0), rows_pad x k_pad
   uint8_t* dA[2];

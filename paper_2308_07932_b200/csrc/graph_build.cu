@@ -638,6 +638,7 @@ bbf_status build_graph(bbf_graph* g, const uint64_t* row_ptr, const uint32_t* co
     dfree(key64, st);
     g->W_G = wg;
     g->wg_valid = true;
+    g->dense_cand = true;
     dense_load = (g->load_flags & BBF_FORCE_DENSE) || dense_preferred(g, true);
   }
   dfree(key_u, st);

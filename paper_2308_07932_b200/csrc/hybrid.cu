@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include <cublas_v2.h>
@@ -434,10 +435,6 @@ void free_hybrid(bbf_graph* g) {
     if (p) dfree(p, st);
   std::memset(&h, 0, sizeof(h));
   free_plan(&g->plan_h, st);
-  if (g->cublas) {
-    cublasDestroy((cublasHandle_t)g->cublas);
-    g->cublas = nullptr;
-  }
 }
 
 namespace {
@@ -509,7 +506,7 @@ void hybrid_choose(bbf_graph* g, bool per_vertex, uint32_t nc[2]) {
     }
     return;
   }
-  if (!g->adj_built || !g->plan_g.valid) return;
+  if (!g->adj_built) return;
   // inside-core degrees of the first rows at each candidate size (computed once per graph)
   if (!g->hyb_scored) {
     g->hyb_scored = true;
@@ -561,7 +558,7 @@ void hybrid_choose(bbf_graph* g, bool per_vertex, uint32_t nc[2]) {
         if (getenv("BBF_DEBUG"))
           fprintf(stderr, "[bbf] hybrid candidate %ux%u (%s): closed %.3f, core wedges %.3e, saved %.3f ms, cost %.3f ms\n",
                   cu, cv, pvm ? "per-vertex" : "global", closed, wc, saved * 1e3, cost * 1e3);
-        if (closed >= 0.5 && gain > best && gain > 0.1 * ((double)g->plan_g.W_pruned / rate)) {
+        if (closed >= 0.5 && gain > best && gain > 1.0e-3) {
           best = gain;
           g->hyb_pick[pvm][0] = cu;
           g->hyb_pick[pvm][1] = cv;
@@ -617,10 +614,16 @@ bbf_status mixed_side_gemm(bbf_graph* g, int s, bool per_vertex, bool* done) {
     dfree(Pr, st);
     return BBF_OK;
   }
-  if (!g->cublas) {
-    cublasHandle_t hd;
-    if (cublasCreate(&hd) != CUBLAS_STATUS_SUCCESS) { set_error("cublasCreate failed"); return BBF_ECUDA; }
-    g->cublas = hd;
+  if (!g->cublas) {  // one handle per device for the process (cublasCreate costs milliseconds)
+    static std::mutex mu;
+    static cublasHandle_t handles[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (g->device < 0 || g->device >= 64) { set_error("device index"); return BBF_EINVAL; }
+    if (!handles[g->device] && cublasCreate(&handles[g->device]) != CUBLAS_STATUS_SUCCESS) {
+      set_error("cublasCreate failed");
+      return BBF_ECUDA;
+    }
+    g->cublas = handles[g->device];
   }
   cublasHandle_t hd = (cublasHandle_t)g->cublas;
   cublasSetStream(hd, st);
