@@ -6,7 +6,8 @@ GPU: each rank counts ITS OWN shard of the work with the library (BBF_FAKE_WORLD
 kernels skip the other rank's work items, no NCCL — one GPU is all this environment has), the
 per-vertex arrays and totals are summed across the two processes over gloo, and the sum must
 equal the oracle's Alg. 2 + 4-role scatter element by element; the shards' local top-k pair lists,
-gathered and merged, must equal the oracle's top-k."""
+gathered and merged, must equal the oracle's top-k.  Config 6 (the NEXT-3 workload) runs the
+hybrid dense-core path on each rank (dense tiles, engine items and mixed middles sharded)."""
 import os
 import socket
 
@@ -85,9 +86,11 @@ def _shard_worker(rank, world, port, q, cfg):
         torch.cuda.set_device(0)
         os.environ["BBF_FAKE_WORLD"] = f"{rank}/{world}"
         g = G.make_config(cfg) if isinstance(cfg, int) else _sweep_graph(int(cfg[5:]))
-        with bbf.Graph.from_synth(g, flags=bbf.BBF_FORCE_SPARSE) as h:
+        hybrid = cfg == 6  # the NEXT-3 workload on the automatic dispatch: the hybrid dense-core path
+        with bbf.Graph.from_synth(g, flags=0 if hybrid else bbf.BBF_FORCE_SPARSE) as h:
             tot, bu, nu, bv, nv = h.count_per_vertex()
             top = h.count_pairs_topk(50, side=0) if g.n_u <= 200_000 else []
+            assert not hybrid or h.hybrid_core() != (0, 0)
         vals = np.concatenate([[tot["balanced"], tot["unbalanced"]], bu, nu, bv, nv]).astype(np.uint64)
         summed = D.sum_over_ranks_u64(vals)
         tops = [None] * world
@@ -98,7 +101,7 @@ def _shard_worker(rank, world, port, q, cfg):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg", [3, "sweep2", "sweep8"])
+@pytest.mark.parametrize("cfg", [3, 6, "sweep2", "sweep8"])
 def test_two_rank_library_shards_sum_to_oracle(cfg):
     import torch
     if not torch.cuda.is_available():
