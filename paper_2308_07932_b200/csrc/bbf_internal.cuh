@@ -254,6 +254,10 @@ struct Hybrid {
   uint16_t* Sh[2];
   uint16_t* Aeh[2];
   uint16_t* Seh[2];
+  uint8_t* Ae[2];          // u8 A', S' and their FP4 copies (the fused cross-term kernel's I operand)
+  uint8_t* Se[2];
+  uint8_t* Ae4[2];
+  uint8_t* Se4[2];
   bool built;
 };
 
@@ -415,6 +419,10 @@ void hybrid_choose(bbf_graph* g, bool per_vertex, uint32_t nc[2]);
 bbf_status run_hybrid(bbf_graph* g, const uint32_t nc[2], bool per_vertex, int rank, int nranks,
                       unsigned long long* host_BN);
 void free_hybrid(bbf_graph* g);
+bbf_status dense_core_cross(bbf_graph* g, uint32_t n_rows, uint64_t rows_pad, uint64_t k, uint8_t* Ae, uint8_t* Se,
+                            uint8_t** Ae4, uint8_t** Se4, uint8_t* A, uint8_t* S, uint8_t** A4, uint8_t** S4,
+                            uint32_t* R, uint32_t r_ld, uint32_t pv_row0, bool per_vertex, int rank, int nranks,
+                            unsigned long long* acc, double* ops);
 // one side's pair counts of a dense 0/1 / +-1 operand pair (dense_i8.cu): rows_pad x k u8
 // operands, FP4 tensor-core kernels while exact (maxdeg <= 8192), else int8; adds (B, N) into
 // acc[0..1] and, when pv, the per-row counts into pv rows pv_row0 + i

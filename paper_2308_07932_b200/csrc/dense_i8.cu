@@ -143,6 +143,11 @@ struct DenseArgs {
   int rank, nranks;
   unsigned long long* pv;  // nullptr: global only
   unsigned long long* acc; // [0] B, [1] N
+  // hybrid cross terms (k_dense_f4q<true>, hybrid.cu): the pair words R[i * r_ld + j] hold the
+  // non-core counts (a_r | d_r << 16); the tile's T, P give the core counts (a_c, d_c) and the
+  // epilogue adds a_c a_r + d_c d_r / a_c d_r + a_r d_c, then stores (a_c | d_c << 16) in R
+  uint32_t* R;
+  uint32_t r_ld;
 };
 
 // Column sums of a warp's 32 x 32 block: lane L ends holding the sum over the 32 lanes (rows)
@@ -862,6 +867,7 @@ __device__ __forceinline__ void mma_f4q(uint32_t d_tmem, uint64_t a, uint64_t b,
       : "memory");
 }
 
+template <bool CROSS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_dense_f4q(const __grid_constant__ CUtensorMap mAi, const __grid_constant__ CUtensorMap mSi,
                 const __grid_constant__ CUtensorMap mAj, const __grid_constant__ CUtensorMap mSj,
@@ -980,6 +986,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (uint32_t c = 0; c < kF4N / 32; ++c) {
         uint32_t qv[32];
         tmem_ld32(tmem + ((q * 32) << 16) + b * kF4N + c * 32, qv);
+        uint32_t rw[32];
+        uint32_t* rrow = nullptr;
+        if (CROSS) {  // this row's 32 pair words (one 128-B line), zero outside the core
+          const uint32_t jc = j0 + c * 32;
+          rrow = a.R + (uint64_t)i * a.r_ld + jc;
+          const bool full = i < a.n_rows && jc + 32 <= a.n_rows && !(reinterpret_cast<uintptr_t>(rrow) & 15);
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            uint4 v4 = make_uint4(0, 0, 0, 0);
+            if (full) v4 = *reinterpret_cast<const uint4*>(rrow + e);
+            else if (i < a.n_rows)
+              for (int f = 0; f < 4; ++f)
+                if (jc + e + f < a.n_rows) (&v4.x)[f] = rrow[e + f];
+            rw[e] = v4.x; rw[e + 1] = v4.y; rw[e + 2] = v4.z; rw[e + 3] = v4.w;
+          }
+        }
         tmem_wait_ld();
         unsigned long long vb[32], vn[32];
 #pragma unroll
@@ -988,8 +1010,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int32_t pp = qq >> 11;                          // floor(Q / 2048)
           const uint32_t tt = (uint32_t)(qq - (pp << 11));      // in [0, 2047]
           const uint32_t ad = (tt + (uint32_t)pp) >> 1, dd = (tt - (uint32_t)pp) >> 1;
-          uint32_t fb = ((ad * (ad - 1u)) >> 1) + ((dd * (dd - 1u)) >> 1);
-          uint32_t fn = ad * dd;
+          uint32_t fb, fn;
+          if (CROSS) {  // a_c = ad, d_c = dd over the start's eligible core middles
+            const uint32_t ar = rw[e] & 0xffffu, dr = rw[e] >> 16;
+            fb = ad * ar + dd * dr;
+            fn = ad * dr + ar * dd;
+            if (rw[e] && j0 + c * 32 + (uint32_t)e > i) rrow[e] = ad | (dd << 16);
+            if (!rw[e]) { fb = 0; fn = 0; }
+          } else {
+            fb = ((ad * (ad - 1u)) >> 1) + ((dd * (dd - 1u)) >> 1);
+            fn = ad * dd;
+          }
           if (j0 + c * 32 + (uint32_t)e <= i) { fb = 0; fn = 0; }  // pairs i < j only
           rB += fb;
           rN += fn;
@@ -1573,8 +1604,8 @@ bbf_status run_dense(bbf_graph* g, bool per_vertex, int rank, int nranks, unsign
       da.acc = g->d_acc + 2 * side;
       const unsigned pairs = (unsigned)std::min<uint64_t>(g->num_sms / 2, tl.size());
       if (g->maxdeg[side] < 2048u && !getenv("BBF_DENSE_F4_TP")) {  // one packed accumulator, double-buffered
-        BBF_CUDA(cudaFuncSetAttribute(k_dense_f4q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmemBytes));
-        k_dense_f4q<<<2 * pairs, kThreads, kQSmemBytes, st>>>(fAi, fSi, fAj, fSj, da);
+        BBF_CUDA(cudaFuncSetAttribute(k_dense_f4q<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmemBytes));
+        k_dense_f4q<false><<<2 * pairs, kThreads, kQSmemBytes, st>>>(fAi, fSi, fAj, fSj, da);
       } else {
         BBF_CUDA(cudaFuncSetAttribute(k_dense_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4SmemBytes));
         k_dense_f4<<<2 * pairs, kThreads, kF4SmemBytes, st>>>(fAi, fSi, fAj, fSj, da);
@@ -1710,8 +1741,8 @@ bbf_status dense_core_side(bbf_graph* g, uint32_t n_rows, uint64_t rows_pad, uin
   da.n_tiles = (uint32_t)tl.size();
   const unsigned pairs = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g->num_sms / 2, tl.size()));
   if (f4 && maxdeg < 2048u && !getenv("BBF_DENSE_F4_TP")) {
-    BBF_CUDA(cudaFuncSetAttribute(k_dense_f4q, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmemBytes));
-    k_dense_f4q<<<2 * pairs, kThreads, kQSmemBytes, st>>>(m0, m1, m2, m3, da);
+    BBF_CUDA(cudaFuncSetAttribute(k_dense_f4q<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmemBytes));
+    k_dense_f4q<false><<<2 * pairs, kThreads, kQSmemBytes, st>>>(m0, m1, m2, m3, da);
   } else if (f4) {
     BBF_CUDA(cudaFuncSetAttribute(k_dense_f4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4SmemBytes));
     k_dense_f4<<<2 * pairs, kThreads, kF4SmemBytes, st>>>(m0, m1, m2, m3, da);
@@ -1725,6 +1756,68 @@ bbf_status dense_core_side(bbf_graph* g, uint32_t n_rows, uint64_t rows_pad, uin
   if (err != cudaSuccess) return cuda_status(err, "dense core launch");
   const double nr = n_rows, kk = (double)k;
   *ops += 2.0 * 2.0 * (nr * (nr - 1.0) / 2.0) * kk;
+  return BBF_OK;
+}
+
+// The hybrid path's mixed core pairs of one side (hybrid.cu), fused on the FP4 tensor cores:
+// k_dense_f4q<true> over the I operand A', S' (each start row masked to its eligible core
+// middles) and the J operand A, S, whose epilogue turns (T, P) into the core counts (a_c, d_c) of
+// every pair i < j, adds the cross terms against the pair words R (row sums = the start's share,
+// column sums = the end's, total = the global count) and leaves (a_c | d_c << 16) in R.  Exact
+// while every row's core degree is < 2,048 (the packed accumulator); the caller checks.
+bbf_status dense_core_cross(bbf_graph* g, uint32_t n_rows, uint64_t rows_pad, uint64_t k, uint8_t* Ae, uint8_t* Se,
+                            uint8_t** Ae4, uint8_t** Se4, uint8_t* A, uint8_t* S, uint8_t** A4, uint8_t** S4,
+                            uint32_t* R, uint32_t r_ld, uint32_t pv_row0, bool per_vertex, int rank, int nranks,
+                            unsigned long long* acc, double* ops) {
+  cudaStream_t st = g->stream;
+  if (n_rows < 2) return BBF_OK;
+  if (!encode_fn()) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return BBF_ECUDA;
+  }
+  const uint64_t k4 = round_up(k, 256) / 2;
+  const uint64_t n8 = rows_pad * (k4 / 8);
+  const unsigned pgrid = (unsigned)std::min<uint64_t>((n8 + 255) / 256, 148ull * 32);
+  uint8_t** outs[4] = {Ae4, Se4, A4, S4};
+  uint8_t* ins[4] = {Ae, Se, A, S};
+  for (int q = 0; q < 4; ++q)
+    if (!*outs[q]) {
+      BBF_CUDA(dmalloc(outs[q], rows_pad * k4, st));
+      k_dense_pack_f4<<<pgrid, 256, 0, st>>>(ins[q], k, *outs[q], k4, rows_pad);
+      g->launches++;
+    }
+  CUtensorMap m0, m1, m2, m3;
+  if (!(make_map(&m0, *Ae4, rows_pad, k4, 128) && make_map(&m1, *Se4, rows_pad, k4, 128) &&
+        make_map(&m2, *A4, rows_pad, k4, kF4JRows) && make_map(&m3, *S4, rows_pad, k4, kF4JRows))) {
+    set_error("cuTensorMapEncodeTiled failed");
+    return BBF_ECUDA;
+  }
+  std::vector<uint2> tl = f4_tile_list((uint32_t)rows_pad);
+  uint2* dt = nullptr;
+  BBF_CUDA(dmalloc(&dt, sizeof(uint2) * (tl.size() + 1), st));
+  BBF_CUDA(cudaMemcpyAsync(dt, tl.data(), sizeof(uint2) * tl.size(), cudaMemcpyHostToDevice, st));
+  DenseArgs da{};
+  da.tiles = dt;
+  da.n_tiles = (uint32_t)tl.size();
+  da.n_rows = n_rows;
+  da.n_kb = (uint32_t)(k4 / kBK);
+  da.pv_row0 = pv_row0;
+  da.n = g->n;
+  da.rank = rank;
+  da.nranks = nranks;
+  da.pv = per_vertex ? (unsigned long long*)g->pv : nullptr;
+  da.acc = acc;
+  da.R = R;
+  da.r_ld = r_ld;
+  const unsigned pairs = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g->num_sms / 2, tl.size()));
+  BBF_CUDA(cudaFuncSetAttribute(k_dense_f4q<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmemBytes));
+  k_dense_f4q<true><<<2 * pairs, kThreads, kQSmemBytes, st>>>(m0, m1, m2, m3, da);
+  g->launches++;
+  const cudaError_t err = cudaGetLastError();
+  dfree(dt, st);
+  if (err != cudaSuccess) return cuda_status(err, "dense cross launch");
+  const double nr = n_rows;
+  *ops += 2.0 * 2.0 * (nr * (nr - 1.0) / 2.0) * (double)k;
   return BBF_OK;
 }
 

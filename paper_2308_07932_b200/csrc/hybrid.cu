@@ -293,12 +293,13 @@ __device__ __forceinline__ uint32_t elig_t(const uint32_t* off, const uint32_t* 
   return p0 < pe ? (adj[p0] & kMask) : nco;
 }
 
-// u8 A / S (rows_pad x k) -> fp16 A, S and the eligibility-masked A', S'
+// u8 A / S (rows_pad x k) -> fp16 A, S and the eligibility-masked A', S' (fp16 and u8)
 __global__ void k_core_f16(const uint8_t* __restrict__ A, const uint8_t* __restrict__ S, uint64_t rows_pad, uint64_t k,
                            uint32_t nrows, uint32_t nco, const uint32_t* __restrict__ off,
                            const uint32_t* __restrict__ adj, const uint32_t* __restrict__ mid,
                            const uint32_t* __restrict__ ccnt, uint32_t row0, __half* __restrict__ Ah,
-                           __half* __restrict__ Sh, __half* __restrict__ Aeh, __half* __restrict__ Seh) {
+                           __half* __restrict__ Sh, __half* __restrict__ Aeh, __half* __restrict__ Seh,
+                           uint8_t* __restrict__ Ae, uint8_t* __restrict__ Se) {
   for (uint64_t r = blockIdx.x; r < rows_pad; r += gridDim.x) {
     const uint32_t t = r < nrows ? elig_t(off, adj, mid, ccnt, row0 + (uint32_t)r, nco) : nco;
     for (uint64_t c = threadIdx.x; c < k; c += blockDim.x) {
@@ -309,6 +310,8 @@ __global__ void k_core_f16(const uint8_t* __restrict__ A, const uint8_t* __restr
       Sh[i] = __float2half(sv);
       Aeh[i] = __float2half(c >= t ? a : 0.f);
       Seh[i] = __float2half(c >= t ? sv : 0.f);
+      Ae[i] = c >= t ? A[i] : (uint8_t)0;
+      Se[i] = c >= t ? S[i] : (uint8_t)0;
     }
   }
 }
@@ -430,7 +433,8 @@ void free_hybrid(bbf_graph* g) {
   cudaStream_t st = g->stream;
   void* ptrs[] = {h.ccnt, h.bmA[0], h.bmA[1], h.bmN[0], h.bmN[1], h.A[0], h.A[1], h.S[0], h.S[1],
                   h.A4[0], h.A4[1], h.S4[0], h.S4[1], h.R[0], h.R[1], h.Ah[0], h.Ah[1], h.Sh[0], h.Sh[1],
-                  h.Aeh[0], h.Aeh[1], h.Seh[0], h.Seh[1]};
+                  h.Aeh[0], h.Aeh[1], h.Seh[0], h.Seh[1], h.Ae[0], h.Ae[1], h.Se[0], h.Se[1],
+                  h.Ae4[0], h.Ae4[1], h.Se4[0], h.Se4[1]};
   for (void* p : ptrs)
     if (p) dfree(p, st);
   std::memset(&h, 0, sizeof(h));
@@ -581,64 +585,90 @@ bbf_status mixed_side_gemm(bbf_graph* g, int s, bool per_vertex, bool* done) {
   const uint32_t ncs = h.nc[s], nco = h.nc[1 - s];
   const uint64_t rp = h.rows_pad[s], k = h.k[s];
   if (ncs < 2) { *done = true; return BBF_OK; }
+  if (getenv("BBF_HYBRID_BITS")) return BBF_OK;  // test hook: the bitmap form
+  // (a_c, d_c) and the pair / end cross terms fused on the FP4 tensor cores while the packed
+  // accumulator is exact (core degrees < 2,048), else cuBLAS fp16 G1, G2 + k_pair_epi
+  const bool fused = h.cmaxdeg[s] < 2048u && !getenv("BBF_HYBRID_GEMM");
   if (!h.Ah[s]) {  // fp16 operands of the core rows (graph-constant)
     const uint64_t b = 2ull * rp * k;
     BBF_CUDA(dmalloc(&h.Ah[s], b, st));
     BBF_CUDA(dmalloc(&h.Sh[s], b, st));
     BBF_CUDA(dmalloc(&h.Aeh[s], b, st));
     BBF_CUDA(dmalloc(&h.Seh[s], b, st));
+    BBF_CUDA(dmalloc(&h.Ae[s], rp * k, st));
+    BBF_CUDA(dmalloc(&h.Se[s], rp * k, st));
     k_core_f16<<<(unsigned)std::min<uint64_t>(rp, 148ull * 16), 256, 0, st>>>(
         h.A[s], h.S[s], rp, k, ncs, nco, g->off, g->adj, g->mid, h.ccnt, s ? g->n_u : 0u, (__half*)h.Ah[s],
-        (__half*)h.Sh[s], (__half*)h.Aeh[s], (__half*)h.Seh[s]);
+        (__half*)h.Sh[s], (__half*)h.Aeh[s], (__half*)h.Seh[s], h.Ae[s], h.Se[s]);
     g->launches++;
   }
-  __half *Tr, *Pr;
-  float *G1, *G2, *M1 = nullptr, *M2 = nullptr;
-  unsigned int* lim;
-  BBF_CUDA(dmalloc(&Tr, 2ull * rp * rp, st));
-  BBF_CUDA(dmalloc(&Pr, 2ull * rp * rp, st));
-  BBF_CUDA(dmalloc(&lim, 8, st));
-  BBF_CUDA(cudaMemsetAsync(lim, 0, 8, st));
-  k_r_f16<<<(unsigned)std::min<uint64_t>((rp + 7) / 8, 148ull * 16), 256, 0, st>>>(h.R[s], ncs, (uint32_t)rp, Tr, Pr,
-                                                                                  lim);
-  g->launches++;
-  unsigned int hl[2] = {0, 0};
-  BBF_CUDA(rb_add(hl, lim, 8, st)); g->launches++;
-  BBF_CUDA(rb_sync(st));
-  dfree(lim, st);
-  // fp16 holds integers <= 2048 exactly; every fp32 partial sum stays below 2^22 (G1, G2 <= nco;
-  // |M1|, |M2| <= the largest row sum of TrU)
-  const bool exact = hl[0] <= 2048u && hl[1] < (1u << 22) && nco < (1u << 22) && !getenv("BBF_HYBRID_BITS");
-  if (!exact) {
-    dfree(Tr, st);
-    dfree(Pr, st);
-    return BBF_OK;
-  }
-  if (!g->cublas) {  // one handle per device for the process (cublasCreate costs milliseconds)
-    static std::mutex mu;
-    static cublasHandle_t handles[64] = {};
-    std::lock_guard<std::mutex> lk(mu);
-    if (g->device < 0 || g->device >= 64) { set_error("device index"); return BBF_EINVAL; }
-    if (!handles[g->device] && cublasCreate(&handles[g->device]) != CUBLAS_STATUS_SUCCESS) {
-      set_error("cublasCreate failed");
-      return BBF_ECUDA;
+  __half *Tr = nullptr, *Pr = nullptr;
+  if (per_vertex) {  // TrU, PrU before R is overwritten, and the exactness bounds of M1, M2
+    unsigned int* lim;
+    BBF_CUDA(dmalloc(&Tr, 2ull * rp * rp, st));
+    BBF_CUDA(dmalloc(&Pr, 2ull * rp * rp, st));
+    BBF_CUDA(dmalloc(&lim, 8, st));
+    BBF_CUDA(cudaMemsetAsync(lim, 0, 8, st));
+    k_r_f16<<<(unsigned)std::min<uint64_t>((rp + 7) / 8, 148ull * 16), 256, 0, st>>>(h.R[s], ncs, (uint32_t)rp, Tr,
+                                                                                    Pr, lim);
+    g->launches++;
+    unsigned int hl[2] = {0, 0};
+    BBF_CUDA(rb_add(hl, lim, 8, st)); g->launches++;
+    BBF_CUDA(rb_sync(st));
+    dfree(lim, st);
+    // fp16 holds the integers <= 2048 exactly; every fp32 partial sum of M1, M2 stays below 2^22
+    if (!(hl[0] <= 2048u && hl[1] < (1u << 22))) {
+      dfree(Tr, st);
+      dfree(Pr, st);
+      return BBF_OK;
     }
-    g->cublas = handles[g->device];
   }
-  cublasHandle_t hd = (cublasHandle_t)g->cublas;
-  cublasSetStream(hd, st);
-  BBF_CUDA(dmalloc(&G1, 4ull * rp * rp, st));
-  BBF_CUDA(dmalloc(&G2, 4ull * rp * rp, st));
+  cublasHandle_t hd = nullptr;
+  if (!fused || per_vertex) {
+    if (!g->cublas) {  // one handle per device for the process (cublasCreate costs milliseconds)
+      static std::mutex mu;
+      static cublasHandle_t handles[64] = {};
+      std::lock_guard<std::mutex> lk(mu);
+      if (g->device < 0 || g->device >= 64) { set_error("device index"); return BBF_EINVAL; }
+      if (!handles[g->device] && cublasCreate(&handles[g->device]) != CUBLAS_STATUS_SUCCESS) {
+        set_error("cublasCreate failed");
+        return BBF_ECUDA;
+      }
+      g->cublas = handles[g->device];
+    }
+    hd = (cublasHandle_t)g->cublas;
+    cublasSetStream(hd, st);
+  }
   const float one = 1.f, zero = 0.f;
   bool ok = true;
-  // G1 = A' A^T, G2 = S' S^T (row-major rp x rp; column-major C' = A . A'^T)
-  ok &= cublasGemmEx(hd, CUBLAS_OP_T, CUBLAS_OP_N, (int)rp, (int)rp, (int)k, &one, h.Ah[s], CUDA_R_16F, (int)k,
-                     h.Aeh[s], CUDA_R_16F, (int)k, &zero, G1, CUDA_R_32F, (int)rp, CUBLAS_COMPUTE_32F,
-                     CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
-  ok &= cublasGemmEx(hd, CUBLAS_OP_T, CUBLAS_OP_N, (int)rp, (int)rp, (int)k, &one, h.Sh[s], CUDA_R_16F, (int)k,
-                     h.Seh[s], CUDA_R_16F, (int)k, &zero, G2, CUDA_R_32F, (int)rp, CUBLAS_COMPUTE_32F,
-                     CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
-  if (ok && per_vertex) {
+  double ops = 0;
+  if (fused) {
+    BBF_TRY(dense_core_cross(g, ncs, rp, k, h.Ae[s], h.Se[s], &h.Ae4[s], &h.Se4[s], h.A[s], h.S[s], &h.A4[s],
+                             &h.S4[s], h.R[s], ncs, s ? g->n_u : 0u, per_vertex, 0, 1, g->d_acc + 4, &ops));
+    // every tile on every rank: the terms are linear in this rank's R, which covers all pairs
+  } else {
+    float *G1, *G2;
+    BBF_CUDA(dmalloc(&G1, 4ull * rp * rp, st));
+    BBF_CUDA(dmalloc(&G2, 4ull * rp * rp, st));
+    // G1 = A' A^T, G2 = S' S^T (row-major rp x rp; column-major C' = A . A'^T)
+    ok &= cublasGemmEx(hd, CUBLAS_OP_T, CUBLAS_OP_N, (int)rp, (int)rp, (int)k, &one, h.Ah[s], CUDA_R_16F, (int)k,
+                       h.Aeh[s], CUDA_R_16F, (int)k, &zero, G1, CUDA_R_32F, (int)rp, CUBLAS_COMPUTE_32F,
+                       CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
+    ok &= cublasGemmEx(hd, CUBLAS_OP_T, CUBLAS_OP_N, (int)rp, (int)rp, (int)k, &one, h.Sh[s], CUDA_R_16F, (int)k,
+                       h.Seh[s], CUDA_R_16F, (int)k, &zero, G2, CUDA_R_32F, (int)rp, CUBLAS_COMPUTE_32F,
+                       CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
+    g->launches += 2;
+    if (!ok) { set_error("cublasGemmEx failed"); return BBF_ECUDA; }
+    // rank shard: the pair terms are linear in this rank's R; every rank scans its own R
+    const unsigned pgrid = (unsigned)std::min<uint64_t>((ncs + 7) / 8, 148ull * 16);
+    k_pair_epi<<<pgrid, 256, 0, st>>>(h.R[s], G1, G2, ncs, (uint32_t)rp, s ? g->n_u : 0u,
+                                      per_vertex ? (unsigned long long*)g->pv : nullptr, g->d_acc + 4);
+    g->launches++;
+    dfree(G1, st);
+    dfree(G2, st);
+  }
+  if (per_vertex) {
+    float *M1, *M2;
     BBF_CUDA(dmalloc(&M1, 4ull * rp * k, st));
     BBF_CUDA(dmalloc(&M2, 4ull * rp * k, st));
     // M1 = TrU A, M2 = PrU S (row-major rp x k; column-major C' = A^T-view . TrU-view)
@@ -648,14 +678,8 @@ bbf_status mixed_side_gemm(bbf_graph* g, int s, bool per_vertex, bool* done) {
     ok &= cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_N, (int)k, (int)rp, (int)rp, &one, h.Sh[s], CUDA_R_16F, (int)k,
                        Pr, CUDA_R_16F, (int)rp, &zero, M2, CUDA_R_32F, (int)k, CUBLAS_COMPUTE_32F,
                        CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
-  }
-  g->launches += per_vertex ? 4 : 2;
-  if (!ok) { set_error("cublasGemmEx failed"); return BBF_ECUDA; }
-  const unsigned pgrid = (unsigned)std::min<uint64_t>((ncs + 7) / 8, 148ull * 16);
-  k_pair_epi<<<pgrid, 256, 0, st>>>(h.R[s], G1, G2, ncs, (uint32_t)rp, s ? g->n_u : 0u,
-                                    per_vertex ? (unsigned long long*)g->pv : nullptr, g->d_acc + 4);
-  g->launches++;
-  if (per_vertex) {
+    g->launches += 2;
+    if (!ok) { set_error("cublasGemmEx failed"); return BBF_ECUDA; }
     unsigned long long* X;
     BBF_CUDA(dmalloc(&X, 16ull * nco + 16, st));
     BBF_CUDA(cudaMemsetAsync(X, 0, 16ull * nco + 16, st));
@@ -666,11 +690,9 @@ bbf_status mixed_side_gemm(bbf_graph* g, int s, bool per_vertex, bool* done) {
     dfree(X, st);
     dfree(M1, st);
     dfree(M2, st);
+    dfree(Tr, st);
+    dfree(Pr, st);
   }
-  dfree(G1, st);
-  dfree(G2, st);
-  dfree(Tr, st);
-  dfree(Pr, st);
   *done = true;
   return BBF_OK;
 }

@@ -76,9 +76,10 @@ def test_hybrid_small_forced_cores(bbf, monkeypatch, seed):
              (int(rng.integers(2, 1200)), 2)]
     for core in cores:
         check(bbf, g, rg, core, monkeypatch)
-    monkeypatch.setenv("BBF_HYBRID_BITS", "1")  # the bitmap form of the mixed pairs
-    check(bbf, g, rg, cores[1], monkeypatch)
-    monkeypatch.delenv("BBF_HYBRID_BITS")
+    for hook in ("BBF_HYBRID_BITS", "BBF_HYBRID_GEMM"):  # the bitmap / library-GEMM forms
+        monkeypatch.setenv(hook, "1")
+        check(bbf, g, rg, cores[1], monkeypatch)
+        monkeypatch.delenv(hook)
 
 
 def test_hybrid_complete_bipartite(bbf, monkeypatch):
@@ -91,12 +92,13 @@ def test_hybrid_complete_bipartite(bbf, monkeypatch):
 def test_hybrid_tiers_and_encodings(bbf, monkeypatch):
     """A medium core-periphery graph whose remainder uses all three engine tiers: forced cores of
     1,024 / 2,048, with the T2 tier off (hub kernel only), with the wide counter encoding, and
-    with the mixed pairs on the bitmap kernel instead of the tensor-core GEMM form."""
+    with the mixed pairs on the bitmap kernel, and with the library-GEMM form instead of the
+    fused FP4 cross-term kernel."""
     g = G.core_periphery(60_000, 20_000, 400_000, 2.1, 4000.0, 4000.0, 2048, 2048, 0.15, 0.7, 61)
     rg = O.route_g_pv(g, threads=THREADS)
     for core in [(1024, 1024), (2048, 2048), (2048, 512)]:
         check(bbf, g, rg, core, monkeypatch)
-    for env in ("BBF_T2_MAX=0", "BBF_NO_COMPACT=1", "BBF_NO_PACKED_END=1", "BBF_HYBRID_BITS=1"):
+    for env in ("BBF_T2_MAX=0", "BBF_NO_COMPACT=1", "BBF_NO_PACKED_END=1", "BBF_HYBRID_BITS=1", "BBF_HYBRID_GEMM=1"):
         k, v = env.split("=")
         monkeypatch.setenv(k, v)
         check(bbf, g, rg, (2048, 2048), monkeypatch)
@@ -104,12 +106,15 @@ def test_hybrid_tiers_and_encodings(bbf, monkeypatch):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_hybrid_fake_world_shards_sum(bbf, monkeypatch, world):
+@pytest.mark.parametrize("form", ["fused", "BBF_HYBRID_GEMM", "BBF_HYBRID_BITS"])
+def test_hybrid_fake_world_shards_sum(bbf, monkeypatch, world, form):
     """Rank shards of the hybrid count (engine items, dense tiles, mixed middles y mod N) sum to
     the single-GPU result."""
     g = G.core_periphery(30_000, 10_000, 200_000, 2.2, 2000.0, 2000.0, 1024, 1024, 0.2, 0.6, 62)
     rg = O.route_g_pv(g, threads=THREADS)
     monkeypatch.setenv("BBF_HYBRID_CORE", "1024,1024")
+    if form != "fused":
+        monkeypatch.setenv(form, "1")
     acc = None
     for r in range(world):
         monkeypatch.setenv("BBF_FAKE_WORLD", f"{r}/{world}")
@@ -119,6 +124,8 @@ def test_hybrid_fake_world_shards_sum(bbf, monkeypatch, world):
         acc = vals if acc is None else [x + y for x, y in zip(acc, vals)]
     monkeypatch.delenv("BBF_FAKE_WORLD")
     monkeypatch.delenv("BBF_HYBRID_CORE")
+    if form != "fused":
+        monkeypatch.delenv(form)
     assert (acc[0], acc[1]) == (rg["B"], rg["N"])
     for a, b in zip(acc[2:], (rg["bal_u"], rg["unb_u"], rg["bal_v"], rg["unb_v"])):
         assert np.array_equal(a.astype(np.uint64), b)
