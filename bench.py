@@ -302,6 +302,7 @@ def main():
         h = bbf.Graph(n_u, n_v, rp, col, sg, device=local, stream=stream, comm=comm)
         tot = h.count_per_vertex(out=outs)[0]
         st = h.stats()
+        st["hybrid_core"] = h.hybrid_core()
         h.free()
         return tot, st
 
@@ -457,6 +458,8 @@ def main():
         "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": dtype, "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "counts": "global + per-vertex (both sides)",
+                   "path": ("hybrid dense core %d x %d + sparse remainder (DESIGN.md §6b)" % st["hybrid_core"]
+                            if st["hybrid_core"] != (0, 0) else "dense" if algo_ops > 0 else "sparse"),
                    "wedges_G": W_G, "balanced": tot["balanced"], "unbalanced": tot["unbalanced"],
                    "step": "bbf_graph_load_csr(device CSR) + bbf_count_per_vertex + free",
                    "l2": f"inputs larger than L2 (input CSR {(g.row_ptr.nbytes + g.col.nbytes + g.sign.nbytes) / 1e6:.0f} MB "

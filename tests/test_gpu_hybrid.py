@@ -146,3 +146,20 @@ def test_hybrid_workload_full_size(bbf):
     assert (tot["balanced"], tot["unbalanced"]) == (rg["B"], rg["N"])
     assert np.array_equal(bu, rg["bal_u"]) and np.array_equal(nu, rg["unb_u"])
     assert np.array_equal(bv, rg["bal_v"]) and np.array_equal(nv, rg["unb_v"])
+
+
+def test_hybrid_second_workload_auto(bbf):
+    """Another closed core at a different size, density and sign mix (a 4,096 x 3,072 community at
+    density 0.35 in a 400K x 150K periphery, signs p = 0.5): the automatic dispatch takes a core
+    and the full per-vertex arrays equal the oracle's."""
+    g = G.core_periphery(400_000, 150_000, 2_000_000, 2.3, 600.0, 600.0, 4096, 3072, 0.35, 0.5, 63,
+                         core_random=True)
+    rg = O.route_g_pv(g, threads=THREADS)
+    with bbf.Graph.from_synth(g) as h:
+        c = h.count_global()
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+        core = h.hybrid_core()
+    assert core != (0, 0)
+    assert (c["balanced"], c["unbalanced"], c["wedges_G"]) == (rg["B"], rg["N"], rg["W_G"])
+    assert np.array_equal(bu, rg["bal_u"]) and np.array_equal(nu, rg["unb_u"])
+    assert np.array_equal(bv, rg["bal_v"]) and np.array_equal(nv, rg["unb_v"])
