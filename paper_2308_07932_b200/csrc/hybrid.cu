@@ -491,7 +491,7 @@ bbf_status ensure_hybrid(bbf_graph* g, const uint32_t nc[2]) {
 
 // Core sizes for a count (DESIGN.md §6b "Hybrid dispatch"): env BBF_HYBRID_CORE=nu,nv forces them
 // (test hook), BBF_NO_HYBRID / a forced path at load disables; otherwise the candidate cores
-// c x c, c in {1024, ..., 8192}, are scored by the engine time of the core wedges they remove
+// cu x cv, cu, cv in {1024, ..., 8192}, are scored by the engine time of the core wedges they remove
 // (estimated from the core rows' inside-core degrees) against the dense core's tensor time and
 // the correction passes, and the best one with a clear gain is used.
 void hybrid_choose(bbf_graph* g, bool per_vertex, uint32_t nc[2]) {
@@ -536,26 +536,32 @@ void hybrid_choose(bbf_graph* g, bool per_vertex, uint32_t nc[2]) {
     for (int pvm = 0; pvm < 2; ++pvm) {
       const double rate = pvm ? 2.7e11 : 4.0e11;  // the engine's measured per-vertex / global rates
       double best = 0;
-      for (int c = 0; c < 4; ++c) {
-        const uint32_t cu = std::min(hyb_cand(c), g->L4[0]), cv = std::min(hyb_cand(c), g->L4[1]);
-        if (cu < hyb_cand(c) && cv < hyb_cand(c) && c) break;
+      for (int c = 0; c < 16; ++c) {  // (U, V) core sizes from {1024, 2048, 4096, 8192}^2
+        const int cxu = c & 3, cxv = c >> 2;
+        const uint32_t cu = std::min(hyb_cand(cxu), g->L4[0]), cv = std::min(hyb_cand(cxv), g->L4[1]);
+        if ((cu < hyb_cand(cxu) && cxu && cu <= hyb_cand(cxu - 1)) || (cv < hyb_cand(cxv) && cxv && cv <= hyb_cand(cxv - 1)))
+          continue;  // the side has no more vertices of degree >= 2 than the smaller candidate
         double wc = 0, din = 0, dall = 0;  // core wedges (pairs at each core middle); closedness
-        for (uint32_t i = 0; i < cu; ++i) {
-          const double d = hc[4ull * i + c];
+        for (uint32_t i = 0; i < cu; ++i) {  // U core rows: entries inside V's core of size cv
+          const double d = hc[4ull * i + cxv];
           wc += d * (d - 1) / 2;
           din += d;
           dall += dg[i];
         }
         for (uint32_t i = 0; i < cv; ++i) {
-          const double d = hc[4ull * (r0 + i) + c];
+          const double d = hc[4ull * (r0 + i) + cxu];
           wc += d * (d - 1) / 2;
           din += d;
           dall += dg[r0 + i];
         }
         const double closed = dall > 0 ? din / dall : 0.0;
         const double saved = 0.5 * wc / rate;
-        const double ops = 2.0 * 2.0 * ((double)cu * cu / 2 * cv + (pvm ? (double)cv * cv / 2 * cu : 0.0));
-        const double gemm = 2.0 * 2.0 * ((double)cu * cu * cv + (double)cv * cv * cu) * (pvm ? 2.0 : 1.0);
+        // dense core (U side, + V side per-vertex) and the fused cross terms (both sides) on the
+        // FP4 kernels (~4 POPS), the core-middle GEMMs (per-vertex, fp16 ~1.5 PFLOP/s), the
+        // pair-word passes (~6 sweeps of 4-byte words) and a fixed 1 ms
+        const double half_u = (double)cu * cu / 2 * cv, half_v = (double)cv * cv / 2 * cu;
+        const double ops = 4.0 * (half_u + (pvm ? half_v : 0.0)) + 4.0 * (half_u + half_v);
+        const double gemm = pvm ? 8.0 * (half_u + half_v) : 0.0;
         const double cost = ops / 4.0e15 + gemm / 1.5e15 + 6.0 * 4.0 * ((double)cu * cu + (double)cv * cv) / 5.0e12 +
                             1.0e-3;
         const double gain = saved - cost;
