@@ -188,7 +188,12 @@ bbf_status finish_collective(bbf_graph* g, bbf_status local, bool per_vertex, un
   BBF_CUDA(cudaMemcpyAsync(g->d_acc + 12, h, 24, cudaMemcpyHostToDevice, g->stream));
   BBF_TRY(allreduce_u64(g, g->d_acc + 12, 2));
   BBF_TRY(allreduce_u64(g, g->d_acc + 14, 1, ncclMax));
-  if (per_vertex) BBF_TRY(allreduce_u64(g, (unsigned long long*)g->pv, 2ull * g->n));
+  // per-vertex sums: only the rows of degree >= 2 (a prefix of each side's rank-space rows,
+  // [0, L4)); a vertex of degree <= 1 lies on no butterfly, so its row is 0 on every rank
+  if (per_vertex) {
+    BBF_TRY(allreduce_u64(g, (unsigned long long*)g->pv, 2ull * g->L4[0]));
+    BBF_TRY(allreduce_u64(g, (unsigned long long*)g->pv + 2ull * g->n_u, 2ull * g->L4[1]));
+  }
   BBF_CUDA(cudaMemcpyAsync(h, g->d_acc + 12, 24, cudaMemcpyDeviceToHost, g->stream));
   BBF_TRY(sync_stream(g));
   if (h[2] != BBF_OK) {

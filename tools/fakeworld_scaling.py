@@ -2,7 +2,8 @@
 r's shard of the work items counted alone on one GPU, exactly the kernels an N-GPU run launches on
 rank r, without the NCCL all-reduce).  For N in {1,2,4,8}: per-rank device time of the count call
 (plan + kernels; bbf_counts.ms_count) and of the hub kernel; the projected count time is the max
-over ranks plus an all-reduce estimate (16 n bytes at the given NVLink all-reduce bandwidth).
+over ranks plus an all-reduce estimate (16 bytes per row of degree >= 2 — the rows the library
+reduces — at the given NVLink all-reduce bandwidth).
 
     python tools/fakeworld_scaling.py --config 5 [--steps 3] [--allreduce-gbs 400]
 """
@@ -34,7 +35,11 @@ def main():
     outs = tuple(torch.zeros(k, dtype=torch.int64, device=dev) for k in (g.n_u, g.n_u, g.n_v, g.n_v))
     st = torch.cuda.Stream(dev)
     torch.cuda.set_stream(st)
-    res = {"config": a.config, "n": g.n_u + g.n_v, "ranks": {}}
+    # the per-vertex all-reduce covers the rows of degree >= 2 only (api.cu finish_collective)
+    du = np.diff(g.row_ptr.astype(np.int64))
+    dv = np.bincount(g.col, minlength=g.n_v)
+    res = {"config": a.config, "n": g.n_u + g.n_v, "rows_reduced": int((du >= 2).sum() + (dv >= 2).sum()),
+           "ranks": {}}
     with bbf.Graph(g.n_u, g.n_v, rp, col, sg, stream=st) as h:  # built once; the count is what is sharded
         for N in (1, 2, 4, 8):
             per = []
@@ -51,7 +56,7 @@ def main():
                 per.append({"rank": r, "ms_count": float(np.median(cms[1:])), "ms_t3": float(np.median(kms[1:])),
                             "balanced": int(tot["balanced"])})
             os.environ.pop("BBF_FAKE_WORLD", None)
-            ar_ms = 0.0 if N == 1 else 16.0 * res["n"] * 2 * (N - 1) / N / (a.allreduce_gbs * 1e9) * 1e3
+            ar_ms = 0.0 if N == 1 else 16.0 * res["rows_reduced"] * 2 * (N - 1) / N / (a.allreduce_gbs * 1e9) * 1e3
             res["ranks"][N] = {"per_rank": per, "max_ms_count": max(p["ms_count"] for p in per),
                                "allreduce_ms_est": ar_ms}
     t1 = res["ranks"][1]["max_ms_count"]
