@@ -83,6 +83,19 @@ def ncu_tensor_util(kernel: str):
     return None
 
 
+def hybrid_evidence():
+    """The hybrid path's fused cross-term kernel (k_dense_f4q<true>) from its committed ncu --set
+    full summary (profiles/r2_ncu_k_dense_f4q_cross_c6.json): time and tensor-pipe utilisation."""
+    try:
+        r = json.load(open(os.path.join(ROOT, "profiles", "r2_ncu_k_dense_f4q_cross_c6.json")))[0]["metrics"]
+        return {"kernel": "k_dense_f4q<true> (fused cross terms of the mixed core pairs, tcgen05 kind::mxf4)",
+                "us_per_launch_ncu": float(r["gpu__time_duration.sum"][0]),
+                "tensor_pipe_util_ncu": float(r["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"][0]) / 100,
+                "source": "profiles/r2_ncu_k_dense_f4q_cross_c6.json (config 6)"}
+    except (OSError, KeyError, ValueError, IndexError):
+        return None
+
+
 def ncu_traffic(config: int, kernel: str):
     """dram read+write bytes per launch of `kernel` on `config` from the committed ncu --set full
     summary (profiles/ncu_traffic.json), or None."""
@@ -481,6 +494,10 @@ def main():
         "clocks": clocks,
     }
     line["parity"] = parity
+    if st["hybrid_core"] != (0, 0):
+        line["hybrid"] = {"core": list(st["hybrid_core"]), "fused_cross_kernel": hybrid_evidence(),
+                          "note": "roofline above = the engine's hub kernel on the sparse remainder; the dense "
+                                  "core and cross terms run on the FP4 tensor cores (DESIGN.md §6b)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(g, pv=pv_host)
         line["cpu_baseline"].pop("wedges", None)
