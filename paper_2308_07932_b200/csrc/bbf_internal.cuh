@@ -326,7 +326,6 @@ struct bbf_graph {
   bool hyb_scored;            // hybrid_choose's candidate scores computed (once per graph)
   uint32_t hyb_pick[2][2];    // chosen core sizes (global, per-vertex); {0, 0} = none
   uint32_t last_nc[2];        // core sizes of the last count (bbf_graph_hybrid_core)
-  void* cublas;               // cublasHandle_t of the hybrid path's library GEMMs (lazily created)
   bbf::Plan plan_s[2];
   bbf::Plan plan_e[2];  // per-edge counts: route S(U) (ends after the start) and route 3 (ends before), all hub tier
   // scratch for the engine

@@ -23,7 +23,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <mutex>
 #include <vector>
 
 #include <cublas_v2.h>
@@ -533,6 +532,20 @@ void hybrid_choose(bbf_graph* g, bool per_vertex, uint32_t nc[2]) {
     // core wedges were cheap for the engine anyway (dense counter windows), the remainder keeps
     // nearly all of the work, and the mixed pairs' counts grow past the exact fp16 range
     // (measured: configs 3 and 5 are 1.3-7x slower with any core).
+    // per side and threshold, prefix sums over the rows (each candidate is then O(1))
+    std::vector<double> pw(4ull * (r0 + r1 + 2), 0.0), pin(4ull * (r0 + r1 + 2), 0.0), pall(r0 + r1 + 2, 0.0);
+    auto pre = [&](uint32_t base, uint32_t rows, uint32_t off0) {  // rows [off0, off0 + rows) of hc
+      for (uint32_t i = 0; i < rows; ++i) {
+        pall[base + i + 1] = pall[base + i] + dg[off0 + i];
+        for (int c = 0; c < 4; ++c) {
+          const double d = hc[4ull * (off0 + i) + c];
+          pw[4ull * (base + i + 1) + c] = pw[4ull * (base + i) + c] + d * (d - 1) / 2;
+          pin[4ull * (base + i + 1) + c] = pin[4ull * (base + i) + c] + d;
+        }
+      }
+    };
+    pre(0, r0, 0);            // U rows: entries [0, r0] at base 0
+    pre(r0 + 1, r1, r0);      // V rows: entries [r0 + 1, r0 + 1 + r1]
     for (int pvm = 0; pvm < 2; ++pvm) {
       const double rate = pvm ? 2.7e11 : 4.0e11;  // the engine's measured per-vertex / global rates
       double best = 0;
@@ -541,19 +554,11 @@ void hybrid_choose(bbf_graph* g, bool per_vertex, uint32_t nc[2]) {
         const uint32_t cu = std::min(hyb_cand(cxu), g->L4[0]), cv = std::min(hyb_cand(cxv), g->L4[1]);
         if ((cu < hyb_cand(cxu) && cxu && cu <= hyb_cand(cxu - 1)) || (cv < hyb_cand(cxv) && cxv && cv <= hyb_cand(cxv - 1)))
           continue;  // the side has no more vertices of degree >= 2 than the smaller candidate
-        double wc = 0, din = 0, dall = 0;  // core wedges (pairs at each core middle); closedness
-        for (uint32_t i = 0; i < cu; ++i) {  // U core rows: entries inside V's core of size cv
-          const double d = hc[4ull * i + cxv];
-          wc += d * (d - 1) / 2;
-          din += d;
-          dall += dg[i];
-        }
-        for (uint32_t i = 0; i < cv; ++i) {
-          const double d = hc[4ull * (r0 + i) + cxu];
-          wc += d * (d - 1) / 2;
-          din += d;
-          dall += dg[r0 + i];
-        }
+        // core wedges (pairs at each core middle) and closedness: U core rows count their entries
+        // inside V's core of size cv, V core rows inside U's core of size cu
+        const double wc = pw[4ull * cu + cxv] + pw[4ull * (r0 + 1 + cv) + cxu];
+        const double din = pin[4ull * cu + cxv] + pin[4ull * (r0 + 1 + cv) + cxu];
+        const double dall = pall[cu] + pall[r0 + 1 + cv];
         const double closed = dall > 0 ? din / dall : 0.0;
         const double saved = 0.5 * wc / rate;
         // dense core (U side, + V side per-vertex) and the fused cross terms (both sides) on the
@@ -631,18 +636,15 @@ bbf_status mixed_side_gemm(bbf_graph* g, int s, bool per_vertex, bool* done) {
   }
   cublasHandle_t hd = nullptr;
   if (!fused || per_vertex) {
-    if (!g->cublas) {  // one handle per device for the process (cublasCreate costs milliseconds)
-      static std::mutex mu;
-      static cublasHandle_t handles[64] = {};
-      std::lock_guard<std::mutex> lk(mu);
-      if (g->device < 0 || g->device >= 64) { set_error("device index"); return BBF_EINVAL; }
-      if (!handles[g->device] && cublasCreate(&handles[g->device]) != CUBLAS_STATUS_SUCCESS) {
-        set_error("cublasCreate failed");
-        return BBF_ECUDA;
-      }
-      g->cublas = handles[g->device];
+    // one handle per device and host thread, created once (cublasCreate costs milliseconds); never
+    // cached in the graph, so threads driving different graphs never share a handle
+    static thread_local cublasHandle_t handles[64] = {};
+    if (g->device < 0 || g->device >= 64) { set_error("device index"); return BBF_EINVAL; }
+    if (!handles[g->device] && cublasCreate(&handles[g->device]) != CUBLAS_STATUS_SUCCESS) {
+      set_error("cublasCreate failed");
+      return BBF_ECUDA;
     }
-    hd = (cublasHandle_t)g->cublas;
+    hd = handles[g->device];
     cublasSetStream(hd, st);
   }
   const float one = 1.f, zero = 0.f;
