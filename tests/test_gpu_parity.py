@@ -513,13 +513,16 @@ _SWEEP = range(*map(int, os.environ.get("BBF_SWEEP_SEEDS", "0:40").split(":")))
 @pytest.mark.parametrize("seed", _SWEEP)
 def test_random_sweep_tiers_dense_topk(bbf, monkeypatch, seed):
     """Randomized sweep: per-vertex counts of the default tiering, of T3-only (T2 disabled, every
-    start above the warp tier goes through the hub kernel) and of the dense path equal the
-    oracle's vBBFC element by element; global B/N/W_G equal Alg. 2; top-k pairs of both sides
+    start above the warp tier goes through the hub kernel), of the hybrid path with a random
+    forced core and of the dense path equal the oracle's vBBFC element by element; global B/N/W_G equal Alg. 2; top-k pairs of both sides
     equal the oracle's."""
     g = _sweep_graph(seed)
     rg = O.route_g(g, threads=THREADS)
     bal, unb = O.route_s(g, threads=THREADS)
-    runs = [("default", {}, 0), ("t3-only", {"BBF_T2_MAX": "0"}, bbf.BBF_FORCE_SPARSE)]
+    rng = np.random.default_rng(5000 + seed)
+    core = f"{int(rng.integers(2, max(3, g.n_u)))},{int(rng.integers(2, max(3, g.n_v)))}"
+    runs = [("default", {}, 0), ("t3-only", {"BBF_T2_MAX": "0"}, bbf.BBF_FORCE_SPARSE),
+            ("hybrid", {"BBF_HYBRID_CORE": core}, 0)]  # a random forced dense core (DESIGN.md §6b)
     if max(g.n_u, g.n_v) <= 65536:
         runs.append(("dense", {}, bbf.BBF_FORCE_DENSE))
     for name, env, fl in runs:
