@@ -75,8 +75,9 @@ __global__ void k_core_cands(const uint32_t* __restrict__ off, const uint32_t* _
   }
 }
 
-// u8 operands (A = 1, S = +1 / -1 as 0xFF) and bitmaps of one side's core rows over the other
-// side's core columns; one warp per row, buffers zeroed beforehand
+// u8 operands (A = 1, S = +1 / -1 as 0xFF) or bitmaps (the k_pairs fallback's, built on demand)
+// of one side's core rows over the other side's core columns; one warp per row, buffers zeroed
+// beforehand
 __global__ void k_core_fill(const uint32_t* __restrict__ off, const uint32_t* __restrict__ adj,
                             const uint32_t* __restrict__ ccnt, uint32_t row0, uint32_t nrows, uint8_t* __restrict__ A,
                             uint8_t* __restrict__ S, uint64_t k, uint32_t* __restrict__ bmA, uint32_t* __restrict__ bmN,
@@ -86,10 +87,14 @@ __global__ void k_core_fill(const uint32_t* __restrict__ off, const uint32_t* __
     const uint32_t x = row0 + r, b = off[x], c = ccnt[x];
     for (uint32_t i = lane; i < c; i += 32) {
       const uint32_t w = adj[b + i], col = w & kMask, bit = 1u << (col & 31);
-      A[r * k + col] = 1;
-      S[r * k + col] = (w & kNegBit) ? (uint8_t)0xFF : (uint8_t)1;
-      atomicOr(&bmA[(uint64_t)r * nw + (col >> 5)], bit);
-      if (w & kNegBit) atomicOr(&bmN[(uint64_t)r * nw + (col >> 5)], bit);
+      if (A) {
+        A[r * k + col] = 1;
+        S[r * k + col] = (w & kNegBit) ? (uint8_t)0xFF : (uint8_t)1;
+      }
+      if (bmA) {
+        atomicOr(&bmA[(uint64_t)r * nw + (col >> 5)], bit);
+        if (w & kNegBit) atomicOr(&bmN[(uint64_t)r * nw + (col >> 5)], bit);
+      }
     }
   }
 }
@@ -292,7 +297,8 @@ __device__ __forceinline__ uint32_t elig_t(const uint32_t* off, const uint32_t* 
   return p0 < pe ? (adj[p0] & kMask) : nco;
 }
 
-// u8 A / S (rows_pad x k) -> fp16 A, S and the eligibility-masked A', S' (fp16 and u8)
+// u8 A / S (rows_pad x k) -> fp16 A, S and the eligibility-masked A', S' (fp16 and u8); each
+// output pair is optional (nullptr: not written)
 __global__ void k_core_f16(const uint8_t* __restrict__ A, const uint8_t* __restrict__ S, uint64_t rows_pad, uint64_t k,
                            uint32_t nrows, uint32_t nco, const uint32_t* __restrict__ off,
                            const uint32_t* __restrict__ adj, const uint32_t* __restrict__ mid,
@@ -305,12 +311,18 @@ __global__ void k_core_f16(const uint8_t* __restrict__ A, const uint8_t* __restr
       const uint64_t i = r * k + c;
       const float a = A[i] ? 1.f : 0.f;
       const float sv = S[i] == 1 ? 1.f : (S[i] == 0xFF ? -1.f : 0.f);
-      Ah[i] = __float2half(a);
-      Sh[i] = __float2half(sv);
-      Aeh[i] = __float2half(c >= t ? a : 0.f);
-      Seh[i] = __float2half(c >= t ? sv : 0.f);
-      Ae[i] = c >= t ? A[i] : (uint8_t)0;
-      Se[i] = c >= t ? S[i] : (uint8_t)0;
+      if (Ah) {
+        Ah[i] = __float2half(a);
+        Sh[i] = __float2half(sv);
+      }
+      if (Aeh) {
+        Aeh[i] = __float2half(c >= t ? a : 0.f);
+        Seh[i] = __float2half(c >= t ? sv : 0.f);
+      }
+      if (Ae) {
+        Ae[i] = c >= t ? A[i] : (uint8_t)0;
+        Se[i] = c >= t ? S[i] : (uint8_t)0;
+      }
     }
   }
 }
@@ -396,7 +408,7 @@ __global__ void k_pair_epi(uint32_t* __restrict__ R, const float* __restrict__ G
 // core middles: X1_v = sum_x A'_xv M1_xv, X2_v = sum_x S'_xv M2_xv over row chunks (two's
 // complement u64 partial sums), then B_v = (X1 + X2) / 2, N_v = (X1 - X2) / 2 into pv
 constexpr uint32_t kMidRows = 128;
-__global__ void k_mid_epi(const __half* __restrict__ Aeh, const __half* __restrict__ Seh, const float* __restrict__ M1,
+__global__ void k_mid_epi(const uint8_t* __restrict__ Ae, const uint8_t* __restrict__ Se, const float* __restrict__ M1,
                           const float* __restrict__ M2, uint32_t ncs, uint64_t k, uint32_t nco,
                           unsigned long long* __restrict__ X) {
   const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -405,8 +417,8 @@ __global__ void k_mid_epi(const __half* __restrict__ Aeh, const __half* __restri
   long long s1 = 0, s2 = 0;
   for (uint32_t x = x0; x < x1; ++x) {
     const uint64_t i = (uint64_t)x * k + v;
-    s1 += (long long)__half2float(Aeh[i]) * (long long)M1[i];
-    s2 += (long long)__half2float(Seh[i]) * (long long)M2[i];
+    if (Ae[i]) s1 += (long long)M1[i];                          // A'_xv in {0, 1}
+    if (Se[i]) s2 += Se[i] == 1 ? (long long)M2[i] : -(long long)M2[i];  // S'_xv in {0, +1, -1}
   }
   if (s1) atomicAdd(&X[2ull * v], (unsigned long long)s1);
   if (s2) atomicAdd(&X[2ull * v + 1], (unsigned long long)s2);
@@ -463,20 +475,16 @@ bbf_status ensure_hybrid(bbf_graph* g, const uint32_t nc[2]) {
     h.nwords[s] = (nco + 31) / 32;
     h.rows_pad[s] = rup(std::max<uint32_t>(nc[s], 1), 256);
     h.k[s] = rup(std::max<uint32_t>(nco, 1), 128);
-    const uint64_t ob = h.rows_pad[s] * h.k[s], bb = 4ull * nc[s] * h.nwords[s] + 4;
+    const uint64_t ob = h.rows_pad[s] * h.k[s];
     BBF_CUDA(dmalloc(&h.A[s], ob, st));
     BBF_CUDA(dmalloc(&h.S[s], ob, st));
-    BBF_CUDA(dmalloc(&h.bmA[s], bb, st));
-    BBF_CUDA(dmalloc(&h.bmN[s], bb, st));
     BBF_CUDA(dmalloc(&h.R[s], 4ull * nc[s] * nc[s] + 4, st));
     BBF_CUDA(cudaMemsetAsync(h.A[s], 0, ob, st));
     BBF_CUDA(cudaMemsetAsync(h.S[s], 0, ob, st));
-    BBF_CUDA(cudaMemsetAsync(h.bmA[s], 0, bb, st));
-    BBF_CUDA(cudaMemsetAsync(h.bmN[s], 0, bb, st));
     if (nc[s]) {
       const unsigned grid = std::min<unsigned>((nc[s] + 7) / 8, 148u * 8u);
       k_core_fill<<<grid, 256, 0, st>>>(g->off, g->adj, h.ccnt, s ? g->n_u : 0u, nc[s], h.A[s], h.S[s], h.k[s],
-                                        h.bmA[s], h.bmN[s], h.nwords[s]);
+                                        nullptr, nullptr, h.nwords[s]);
       g->launches++;
     }
   }
@@ -600,18 +608,31 @@ bbf_status mixed_side_gemm(bbf_graph* g, int s, bool per_vertex, bool* done) {
   // (a_c, d_c) and the pair / end cross terms fused on the FP4 tensor cores while the packed
   // accumulator is exact (core degrees < 2,048), else cuBLAS fp16 G1, G2 + k_pair_epi
   const bool fused = h.cmaxdeg[s] < 2048u && !getenv("BBF_HYBRID_GEMM");
-  if (!h.Ah[s]) {  // fp16 operands of the core rows (graph-constant)
+  // operands of the core rows (graph-constant, built on first need): u8 A', S' (the fused kernel's I
+  // operand, k_mid_epi), fp16 A, S (the library GEMMs) and fp16 A', S' (the unfused G1, G2)
+  {
     const uint64_t b = 2ull * rp * k;
-    BBF_CUDA(dmalloc(&h.Ah[s], b, st));
-    BBF_CUDA(dmalloc(&h.Sh[s], b, st));
-    BBF_CUDA(dmalloc(&h.Aeh[s], b, st));
-    BBF_CUDA(dmalloc(&h.Seh[s], b, st));
-    BBF_CUDA(dmalloc(&h.Ae[s], rp * k, st));
-    BBF_CUDA(dmalloc(&h.Se[s], rp * k, st));
-    k_core_f16<<<(unsigned)std::min<uint64_t>(rp, 148ull * 16), 256, 0, st>>>(
-        h.A[s], h.S[s], rp, k, ncs, nco, g->off, g->adj, g->mid, h.ccnt, s ? g->n_u : 0u, (__half*)h.Ah[s],
-        (__half*)h.Sh[s], (__half*)h.Aeh[s], (__half*)h.Seh[s], h.Ae[s], h.Se[s]);
-    g->launches++;
+    const bool need_e = !h.Ae[s], need_h = (per_vertex || !fused) && !h.Ah[s], need_eh = !fused && !h.Aeh[s];
+    if (need_e) {
+      BBF_CUDA(dmalloc(&h.Ae[s], rp * k, st));
+      BBF_CUDA(dmalloc(&h.Se[s], rp * k, st));
+    }
+    if (need_h) {
+      BBF_CUDA(dmalloc(&h.Ah[s], b, st));
+      BBF_CUDA(dmalloc(&h.Sh[s], b, st));
+    }
+    if (need_eh) {
+      BBF_CUDA(dmalloc(&h.Aeh[s], b, st));
+      BBF_CUDA(dmalloc(&h.Seh[s], b, st));
+    }
+    if (need_e || need_h || need_eh) {
+      k_core_f16<<<(unsigned)std::min<uint64_t>(rp, 148ull * 16), 256, 0, st>>>(
+          h.A[s], h.S[s], rp, k, ncs, nco, g->off, g->adj, g->mid, h.ccnt, s ? g->n_u : 0u,
+          need_h ? (__half*)h.Ah[s] : nullptr, need_h ? (__half*)h.Sh[s] : nullptr,
+          need_eh ? (__half*)h.Aeh[s] : nullptr, need_eh ? (__half*)h.Seh[s] : nullptr, need_e ? h.Ae[s] : nullptr,
+          need_e ? h.Se[s] : nullptr);
+      g->launches++;
+    }
   }
   __half *Tr = nullptr, *Pr = nullptr;
   if (per_vertex) {  // TrU, PrU before R is overwritten, and the exactness bounds of M1, M2
@@ -698,7 +719,7 @@ bbf_status mixed_side_gemm(bbf_graph* g, int s, bool per_vertex, bool* done) {
     BBF_CUDA(dmalloc(&X, 16ull * nco + 16, st));
     BBF_CUDA(cudaMemsetAsync(X, 0, 16ull * nco + 16, st));
     k_mid_epi<<<dim3((nco + 255) / 256, (ncs + kMidRows - 1) / kMidRows), 256, 0, st>>>(
-        (const __half*)h.Aeh[s], (const __half*)h.Seh[s], M1, M2, ncs, k, nco, X);
+        h.Ae[s], h.Se[s], M1, M2, ncs, k, nco, X);
     k_mid_out<<<(nco + 255) / 256, 256, 0, st>>>(X, nco, s ? 0u : g->n_u, (unsigned long long*)g->pv);
     g->launches += 2;
     dfree(X, st);
@@ -747,6 +768,19 @@ bbf_status run_hybrid(bbf_graph* g, const uint32_t nc[2], bool per_vertex, int r
     bool done = false;
     BBF_TRY(mixed_side_gemm(g, s, per_vertex, &done));
     if (done) continue;
+    if (!h.bmA[s]) {  // the fallback's core-row bitmaps, on first need
+      const uint64_t bb = 4ull * nc[s] * h.nwords[s] + 4;
+      BBF_CUDA(dmalloc(&h.bmA[s], bb, st));
+      BBF_CUDA(dmalloc(&h.bmN[s], bb, st));
+      BBF_CUDA(cudaMemsetAsync(h.bmA[s], 0, bb, st));
+      BBF_CUDA(cudaMemsetAsync(h.bmN[s], 0, bb, st));
+      if (nc[s]) {
+        const unsigned grid = std::min<unsigned>((nc[s] + 7) / 8, 148u * 8u);
+        k_core_fill<<<grid, 256, 0, st>>>(g->off, g->adj, h.ccnt, s ? g->n_u : 0u, nc[s], nullptr, nullptr, h.k[s],
+                                          h.bmA[s], h.bmN[s], h.nwords[s]);
+        g->launches++;
+      }
+    }
     PairArgs pa{h.R[s], h.bmA[s], h.bmN[s], g->off, g->adj, g->mid, h.ccnt, nc[s], nc[1 - s], h.nwords[s],
                 s ? g->n_u : 0u, s ? 0u : g->n_u, per_vertex ? (unsigned long long*)g->pv : nullptr, g->d_acc + 4};
     const int smem = per_vertex ? (int)(16u * nc[1 - s]) : 0;
