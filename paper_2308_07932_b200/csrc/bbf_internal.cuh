@@ -420,8 +420,8 @@ bbf_status run_hybrid(bbf_graph* g, const uint32_t nc[2], bool per_vertex, int r
 void free_hybrid(bbf_graph* g);
 bbf_status dense_core_cross(bbf_graph* g, uint32_t n_rows, uint64_t rows_pad, uint64_t k, uint8_t* Ae, uint8_t* Se,
                             uint8_t** Ae4, uint8_t** Se4, uint8_t* A, uint8_t* S, uint8_t** A4, uint8_t** S4,
-                            uint32_t* R, uint32_t r_ld, uint32_t pv_row0, bool per_vertex, int rank, int nranks,
-                            unsigned long long* acc, double* ops);
+                            uint32_t* R, uint32_t r_ld, uint32_t pv_row0, bool per_vertex, uint32_t xlo,
+                            uint32_t xhi, unsigned long long* acc, double* ops);
 // one side's pair counts of a dense 0/1 / +-1 operand pair (dense_i8.cu): rows_pad x k u8
 // operands, FP4 tensor-core kernels while exact (maxdeg <= 8192), else int8; adds (B, N) into
 // acc[0..1] and, when pv, the per-row counts into pv rows pv_row0 + i

@@ -1764,13 +1764,14 @@ bbf_status dense_core_side(bbf_graph* g, uint32_t n_rows, uint64_t rows_pad, uin
 // middles) and the J operand A, S, whose epilogue turns (T, P) into the core counts (a_c, d_c) of
 // every pair i < j, adds the cross terms against the pair words R (row sums = the start's share,
 // column sums = the end's, total = the global count) and leaves (a_c | d_c << 16) in R.  Exact
-// while every row's core degree is < 2,048 (the packed accumulator); the caller checks.
+// while every row's core degree is < 2,048 (the packed accumulator); the caller checks.  Rows
+// [xlo, xhi) (256-aligned: the caller's rank shard) are the I tiles launched.
 bbf_status dense_core_cross(bbf_graph* g, uint32_t n_rows, uint64_t rows_pad, uint64_t k, uint8_t* Ae, uint8_t* Se,
                             uint8_t** Ae4, uint8_t** Se4, uint8_t* A, uint8_t* S, uint8_t** A4, uint8_t** S4,
-                            uint32_t* R, uint32_t r_ld, uint32_t pv_row0, bool per_vertex, int rank, int nranks,
-                            unsigned long long* acc, double* ops) {
+                            uint32_t* R, uint32_t r_ld, uint32_t pv_row0, bool per_vertex, uint32_t xlo,
+                            uint32_t xhi, unsigned long long* acc, double* ops) {
   cudaStream_t st = g->stream;
-  if (n_rows < 2) return BBF_OK;
+  if (n_rows < 2 || xhi <= xlo) return BBF_OK;
   if (!encode_fn()) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return BBF_ECUDA;
@@ -1792,7 +1793,11 @@ bbf_status dense_core_cross(bbf_graph* g, uint32_t n_rows, uint64_t rows_pad, ui
     set_error("cuTensorMapEncodeTiled failed");
     return BBF_ECUDA;
   }
-  std::vector<uint2> tl = f4_tile_list((uint32_t)rows_pad);
+  // the I tiles (256-row blocks) of rows [xlo, xhi) only: the caller's pair words are zero elsewhere
+  std::vector<uint2> tl;
+  for (const uint2 t : f4_tile_list((uint32_t)rows_pad))
+    if (t.x * kPB >= xlo && t.x * kPB < xhi) tl.push_back(t);
+  if (tl.empty()) return BBF_OK;
   uint2* dt = nullptr;
   BBF_CUDA(dmalloc(&dt, sizeof(uint2) * (tl.size() + 1), st));
   BBF_CUDA(cudaMemcpyAsync(dt, tl.data(), sizeof(uint2) * tl.size(), cudaMemcpyHostToDevice, st));
@@ -1803,8 +1808,8 @@ bbf_status dense_core_cross(bbf_graph* g, uint32_t n_rows, uint64_t rows_pad, ui
   da.n_kb = (uint32_t)(k4 / kBK);
   da.pv_row0 = pv_row0;
   da.n = g->n;
-  da.rank = rank;
-  da.nranks = nranks;
+  da.rank = 0;
+  da.nranks = 1;
   da.pv = per_vertex ? (unsigned long long*)g->pv : nullptr;
   da.acc = acc;
   da.R = R;

@@ -18,7 +18,8 @@
 // (a_r, d_r) of the core pairs are accumulated from the non-core middles (k_mixed, mode 0) into a
 // per-side nc x nc word matrix R; (a_c, d_c) come from core-row bitmaps restricted to x's
 // eligible core middles (k_pairs), for the pairs with R != 0 only.  Every correction term is
-// linear in (a_r, d_r) for fixed (a_c, d_c), so ranks shard the non-core middles and sum.
+// linear in (a_r, d_r) for fixed (a_c, d_c); ranks shard the core pairs by row ranges of their
+// start x (each rank's pair words, GEMM rows and cross-term tiles are its own) and sum.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -105,27 +106,28 @@ struct MixArgs {
   uint32_t* R0;  // U-side core pairs
   uint32_t* R1;  // V-side core pairs
   unsigned long long* pv;
-  int rank, nranks;
+  uint32_t xlo[2], xhi[2];  // this rank's start rows of each core side (row-range shard)
 };
 
 // the mixed wedges x - y - w: y a non-core middle, x and w core vertices of the other side, x an
 // eligible start (r(y) > r(x), i.e. y at or after mid[x] in x's row) and l(w) > l(x).  One warp per
-// y (rank shard y mod N).  mode 0: R[x][w] += agree ? 1 : 1 << 16 (a_r, d_r); mode 1 (after
+// y; a rank takes the wedges whose start x lies in its row range of the core side (so its pair
+// words, GEMM rows and cross-term tiles are its own).  mode 0: R[x][w] += agree ? 1 : 1 << 16 (a_r, d_r); mode 1 (after
 // k_pairs turned R into (a_c, d_c)): y's share (a_c, d_c) if agree else (d_c, a_c)
 template <int MODE>
 __global__ void __launch_bounds__(256) k_mixed(MixArgs a) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;; t += nw) {
-    const uint64_t y64 = (uint64_t)t * a.nranks + a.rank;
-    if (y64 >= a.n) break;
-    const uint32_t y = (uint32_t)y64;
+    if (t >= a.n) break;
+    const uint32_t y = t;
     if (is_core(y, a.n_u, a.nc0, a.nc1)) continue;
     const uint32_t c = a.ccnt[y];
     if (c < 2) continue;
     const uint32_t ob = y < a.n_u ? a.n_u : 0u;  // row base of the core side (x, w side)
     const uint32_t ncs = y < a.n_u ? a.nc1 : a.nc0;
     uint32_t* R = y < a.n_u ? a.R1 : a.R0;
+    const uint32_t xlo = y < a.n_u ? a.xlo[1] : a.xlo[0], xhi = y < a.n_u ? a.xhi[1] : a.xhi[0];
     const uint32_t b = a.off[y];
     // eligible starts: a prefix of the core neighbours (descending priority)
     uint32_t ky = 0;
@@ -141,6 +143,8 @@ __global__ void __launch_bounds__(256) k_mixed(MixArgs a) {
     unsigned long long sB = 0, sN = 0;
     for (uint32_t i = 0; i < ky; ++i) {
       const uint32_t xi = a.adj[b + i];
+      if ((xi & kMask) < xlo) continue;
+      if ((xi & kMask) >= xhi) break;  // the core prefix ascends by rank
       const uint64_t rbase = (uint64_t)(xi & kMask) * ncs;
       for (uint32_t j = i + 1 + lane; j < c; j += 32) {
         const uint32_t wj = a.adj[b + j];
@@ -409,11 +413,11 @@ __global__ void k_pair_epi(uint32_t* __restrict__ R, const float* __restrict__ G
 // complement u64 partial sums), then B_v = (X1 + X2) / 2, N_v = (X1 - X2) / 2 into pv
 constexpr uint32_t kMidRows = 128;
 __global__ void k_mid_epi(const uint8_t* __restrict__ Ae, const uint8_t* __restrict__ Se, const float* __restrict__ M1,
-                          const float* __restrict__ M2, uint32_t ncs, uint64_t k, uint32_t nco,
+                          const float* __restrict__ M2, uint32_t xlo, uint32_t xhi, uint64_t k, uint32_t nco,
                           unsigned long long* __restrict__ X) {
   const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nco) return;
-  const uint32_t x0 = blockIdx.y * kMidRows, x1 = min(ncs, x0 + kMidRows);
+  const uint32_t x0 = xlo + blockIdx.y * kMidRows, x1 = min(xhi, x0 + kMidRows);
   long long s1 = 0, s2 = 0;
   for (uint32_t x = x0; x < x1; ++x) {
     const uint64_t i = (uint64_t)x * k + v;
@@ -597,7 +601,7 @@ namespace {
 // The mixed-pair terms of one core side on the tensor cores (library GEMMs, see k_core_f16):
 // returns BBF_OK with *done = false when a bound for exact fp32 accumulation fails (the caller
 // then runs the bitmap kernel k_pairs, exact for any values).
-bbf_status mixed_side_gemm(bbf_graph* g, int s, bool per_vertex, bool* done) {
+bbf_status mixed_side_gemm(bbf_graph* g, int s, bool per_vertex, uint32_t xlo, uint32_t xhi, bool* done) {
   Hybrid& h = g->hyb;
   cudaStream_t st = g->stream;
   *done = false;
@@ -673,8 +677,8 @@ bbf_status mixed_side_gemm(bbf_graph* g, int s, bool per_vertex, bool* done) {
   double ops = 0;
   if (fused) {
     BBF_TRY(dense_core_cross(g, ncs, rp, k, h.Ae[s], h.Se[s], &h.Ae4[s], &h.Se4[s], h.A[s], h.S[s], &h.A4[s],
-                             &h.S4[s], h.R[s], ncs, s ? g->n_u : 0u, per_vertex, 0, 1, g->d_acc + 4, &ops));
-    // every tile on every rank: the terms are linear in this rank's R, which covers all pairs
+                             &h.S4[s], h.R[s], ncs, s ? g->n_u : 0u, per_vertex, xlo, xhi, g->d_acc + 4, &ops));
+    // the tiles of this rank's rows only (its pair words are zero elsewhere)
   } else {
     float *G1, *G2;
     BBF_CUDA(dmalloc(&G1, 4ull * rp * rp, st));
@@ -700,26 +704,26 @@ bbf_status mixed_side_gemm(bbf_graph* g, int s, bool per_vertex, bool* done) {
     float *M1, *M2;
     BBF_CUDA(dmalloc(&M1, 4ull * rp * k, st));
     BBF_CUDA(dmalloc(&M2, 4ull * rp * k, st));
-    // M1 = TrU A, M2 = PrU S (row-major rp x k; column-major C' = A^T-view . TrU-view).  TrU and
-    // PrU are strictly upper triangular (w > x), so row block I of M needs only the K range from
-    // its own first row: blocks of 1/8 of the rows, each a GEMM over K = rp - I0 (56% of the flops)
-    const uint64_t nb = rp >= 2048 ? 8 : 1, bs = rp / nb;
-    for (uint64_t bi = 0; bi < nb; ++bi) {
-      const uint64_t i0 = bi * bs, kk = rp - i0;
+    // M1 = TrU A, M2 = PrU S (row-major rp x k; column-major C' = A^T-view . TrU-view), for this
+    // rank's rows only.  TrU and PrU are strictly upper triangular (w > x), so a row block needs
+    // only the K range from its own first row: blocks of <= 1,024 rows, each a GEMM over K = rp - i0
+    for (uint64_t i0 = xlo; i0 < xhi; i0 += 1024) {
+      const uint64_t bs = std::min<uint64_t>(1024, xhi - i0), kk = rp - i0;
       ok &= cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_N, (int)k, (int)bs, (int)kk, &one, h.Ah[s] + i0 * k, CUDA_R_16F,
                          (int)k, Tr + i0 * rp + i0, CUDA_R_16F, (int)rp, &zero, M1 + i0 * k, CUDA_R_32F, (int)k,
                          CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
       ok &= cublasGemmEx(hd, CUBLAS_OP_N, CUBLAS_OP_N, (int)k, (int)bs, (int)kk, &one, h.Sh[s] + i0 * k, CUDA_R_16F,
                          (int)k, Pr + i0 * rp + i0, CUDA_R_16F, (int)rp, &zero, M2 + i0 * k, CUDA_R_32F, (int)k,
                          CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
+      g->launches += 2;
     }
-    g->launches += 2 * nb;
     if (!ok) { set_error("cublasGemmEx failed"); return BBF_ECUDA; }
     unsigned long long* X;
     BBF_CUDA(dmalloc(&X, 16ull * nco + 16, st));
     BBF_CUDA(cudaMemsetAsync(X, 0, 16ull * nco + 16, st));
-    k_mid_epi<<<dim3((nco + 255) / 256, (ncs + kMidRows - 1) / kMidRows), 256, 0, st>>>(
-        h.Ae[s], h.Se[s], M1, M2, ncs, k, nco, X);
+    if (xhi > xlo)
+      k_mid_epi<<<dim3((nco + 255) / 256, (xhi - xlo + kMidRows - 1) / kMidRows), 256, 0, st>>>(
+          h.Ae[s], h.Se[s], M1, M2, xlo, xhi, k, nco, X);
     k_mid_out<<<(nco + 255) / 256, 256, 0, st>>>(X, nco, s ? 0u : g->n_u, (unsigned long long*)g->pv);
     g->launches += 2;
     dfree(X, st);
@@ -759,14 +763,33 @@ bbf_status run_hybrid(bbf_graph* g, const uint32_t nc[2], bool per_vertex, int r
   // 3. the mixed core pairs: (a_r, d_r), then (a_c, d_c) and the cross terms, then the non-core
   // middles' shares
   for (int s = 0; s < 2; ++s) BBF_CUDA(cudaMemsetAsync(h.R[s], 0, 4ull * nc[s] * nc[s], st));
+  // row-range shard of the core pairs: 256-row blocks (the cross-term kernel's I tiles) dealt to
+  // ranks in contiguous runs of equal upper-triangle area (pairs x < w)
+  uint32_t xlo[2], xhi[2];
+  for (int s = 0; s < 2; ++s) {
+    const uint32_t ncs = nc[s], nblk = (ncs + 255) / 256;
+    const double tot = 0.5 * (double)ncs * ncs;
+    uint32_t b0 = 0, b1 = 0;
+    double acc = 0;
+    for (uint32_t b = 0; b < nblk; ++b) {  // run of block b: rank floor(N * area before its middle / total)
+      const double x0 = 256.0 * b, x1 = std::min<double>(ncs, x0 + 256.0);
+      const double area = (x1 - x0) * (ncs - 0.5 * (x0 + x1));
+      const int owner = tot > 0 ? std::min(nranks - 1, (int)(nranks * (acc + 0.5 * area) / tot)) : 0;
+      acc += area;
+      if (owner < rank) b0 = b + 1;
+      if (owner <= rank) b1 = b + 1;
+    }
+    xlo[s] = std::min(ncs, 256u * b0);
+    xhi[s] = std::min(ncs, 256u * std::max(b0, b1));
+  }
   MixArgs ma{g->off, g->adj, g->rev, g->mid, h.ccnt, g->n_u, g->n, nc[0], nc[1], h.R[0], h.R[1],
-             (unsigned long long*)g->pv, rank, nranks};
-  const unsigned mgrid = (unsigned)std::min<uint64_t>((g->n / std::max(nranks, 1) + 7) / 8 + 1, 148ull * 16);
+             (unsigned long long*)g->pv, {xlo[0], xlo[1]}, {xhi[0], xhi[1]}};
+  const unsigned mgrid = (unsigned)std::min<uint64_t>((g->n + 7) / 8 + 1, 148ull * 16);
   k_mixed<0><<<mgrid, 256, 0, st>>>(ma);
   g->launches++;
   for (int s = 0; s < 2; ++s) {
     bool done = false;
-    BBF_TRY(mixed_side_gemm(g, s, per_vertex, &done));
+    BBF_TRY(mixed_side_gemm(g, s, per_vertex, xlo[s], xhi[s], &done));
     if (done) continue;
     if (!h.bmA[s]) {  // the fallback's core-row bitmaps, on first need
       const uint64_t bb = 4ull * nc[s] * h.nwords[s] + 4;
