@@ -255,7 +255,9 @@ bbf_status bbf_graph_stats(bbf_graph *g, uint64_t *kernel_launches, uint64_t *al
  * identical either way.  The dispatch is automatic (estimated engine time of the core's wedges
  * vs the core's tensor time); env BBF_NO_HYBRID disables it, BBF_FORCE_SPARSE / BBF_FORCE_DENSE
  * (at load or count) bypass it.  Requires every degree < 65,536 (pair counts packed 16 | 16)
- * and cores of at most 8,192 per side.  Errors: BBF_EINVAL on a null handle. */
+ * and cores of at most 8,192 per side.  Device memory of a hybrid count: ~2.5 GB for 8,192 x 8,192
+ * cores (pair-word matrices nc^2 x 4 B per side, core operands, GEMM temporaries); an allocation
+ * failure returns BBF_ENOMEM from the count call.  Errors: BBF_EINVAL on a null handle. */
 bbf_status bbf_graph_hybrid_core(bbf_graph *g, uint32_t *core_u, uint32_t *core_v);
 
 #ifdef __cplusplus
