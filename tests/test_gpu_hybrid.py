@@ -163,3 +163,16 @@ def test_hybrid_second_workload_auto(bbf):
     assert (c["balanced"], c["unbalanced"], c["wedges_G"]) == (rg["B"], rg["N"], rg["W_G"])
     assert np.array_equal(bu, rg["bal_u"]) and np.array_equal(nu, rg["unb_u"])
     assert np.array_equal(bv, rg["bal_v"]) and np.array_equal(nv, rg["unb_v"])
+
+
+def test_hybrid_dense_core_beyond_packed_accumulator(bbf, monkeypatch):
+    """A core whose inside degrees exceed 2,047 (a 3,072 x 3,072 community at p = 0.8): the dense
+    core runs on the two-accumulator FP4 kernel and the mixed pairs on the library-GEMM form (the
+    fused kernel's packed accumulator would not be exact); counts equal the oracle's."""
+    g = G.core_periphery(60_000, 30_000, 300_000, 2.2, 1500.0, 1500.0, 3072, 3072, 0.8, 0.6, 64, core_random=True)
+    rg = O.route_g_pv(g, threads=THREADS)
+    check(bbf, g, rg, (3072, 3072), monkeypatch)
+    with bbf.Graph.from_synth(g) as h:  # the automatic dispatch on the same graph
+        tot, bu, nu, bv, nv = h.count_per_vertex()
+    assert (tot["balanced"], tot["unbalanced"]) == (rg["B"], rg["N"])
+    assert np.array_equal(bu, rg["bal_u"]) and np.array_equal(nv, rg["unb_v"])
