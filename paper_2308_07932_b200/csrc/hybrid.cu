@@ -16,8 +16,10 @@
 //     global count; to a non-core middle y of the pair (a_c, d_c) if its wedge is symmetric
 //     (agree) else (d_c, a_c); to a core middle v (a_r, d_r) if agree else (d_r, a_r).
 // (a_r, d_r) of the core pairs are accumulated from the non-core middles (k_mixed, mode 0) into a
-// per-side nc x nc word matrix R; (a_c, d_c) come from core-row bitmaps restricted to x's
-// eligible core middles (k_pairs), for the pairs with R != 0 only.  Every correction term is
+// per-side nc x nc word matrix R; (a_c, d_c) of every core pair come from the FP4 tensor cores
+// (k_dense_f4q<true>: A' A^T and S' S^T with A', S' masked to each start's eligible core middles),
+// whose epilogue adds the cross terms against R; the core middles' shares are two fp16 library
+// GEMMs (TrU A, PrU S); k_pairs (core-row bitmaps) is the exact fallback.  Every correction term is
 // linear in (a_r, d_r) for fixed (a_c, d_c); ranks shard the core pairs by row ranges of their
 // start x (each rank's pair words, GEMM rows and cross-term tiles are its own) and sum.
 #include <algorithm>
@@ -112,8 +114,9 @@ struct MixArgs {
 // the mixed wedges x - y - w: y a non-core middle, x and w core vertices of the other side, x an
 // eligible start (r(y) > r(x), i.e. y at or after mid[x] in x's row) and l(w) > l(x).  One warp per
 // y; a rank takes the wedges whose start x lies in its row range of the core side (so its pair
-// words, GEMM rows and cross-term tiles are its own).  mode 0: R[x][w] += agree ? 1 : 1 << 16 (a_r, d_r); mode 1 (after
-// k_pairs turned R into (a_c, d_c)): y's share (a_c, d_c) if agree else (d_c, a_c)
+// words, GEMM rows and cross-term tiles are its own).  mode 0: R[x][w] += agree ? 1 : 1 << 16
+// (a_r, d_r); mode 1 (after the cross-term pass turned R into (a_c, d_c)): y's share (a_c, d_c)
+// if agree else (d_c, a_c)
 template <int MODE>
 __global__ void __launch_bounds__(256) k_mixed(MixArgs a) {
   const uint32_t lane = threadIdx.x & 31;
