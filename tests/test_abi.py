@@ -59,6 +59,16 @@ def test_abi_version_and_no_gpu_refusal(libpath):
     assert e.value.name == "BBF_ECUDA"
 
 
+def test_null_handle_errors(libpath):
+    """Handle-level calls refuse a null graph with BBF_EINVAL (no device needed)."""
+    import ctypes as C
+    from paper_2308_07932_b200 import bbf
+    L = bbf.lib()
+    a, b = C.c_uint32(7), C.c_uint32(7)
+    assert L.bbf_graph_hybrid_core(None, C.byref(a), C.byref(b)) == 1  # BBF_EINVAL
+    assert L.bbf_graph_stats(None, None, None, None, None) == 1
+
+
 def test_binding_never_imports_oracle():
     src = open(os.path.join(ROOT, "paper_2308_07932_b200", "bbf.py")).read()
     src += open(os.path.join(ROOT, "paper_2308_07932_b200", "__init__.py")).read()
