@@ -55,11 +55,19 @@ __global__ void k_rsafe(const unsigned long long* __restrict__ win, const uint32
 // ub, the pruned segment length (ends of degree >= 2) and the full count (all ends; W_G)
 // (win != nullptr, route G) also the per-end bound of incoming wedges (see make_plan): the same entry's
 // middle and reverse position give the eligible starts before it (one pass over erow/adj/rev)
+// the middle row's (off, off + 1, end1, mid) in one 16-byte record: one random sector per entry
+// instead of four
+__global__ void k_rowinfo(const uint32_t* __restrict__ off, const uint32_t* __restrict__ end1,
+                          const uint32_t* __restrict__ mid, uint32_t n, uint4* __restrict__ ri) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) ri[r] = make_uint4(off[r], off[r + 1], end1[r], mid[r]);
+}
+
 __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
                                const uint32_t* __restrict__ adj, const uint32_t* __restrict__ rev,
                                const uint32_t* __restrict__ erow,
                                const uint32_t* __restrict__ mid,
-                               const uint32_t* __restrict__ end1, uint64_t m,
+                               const uint32_t* __restrict__ end1, const uint4* __restrict__ rowinfo, uint64_t m,
                                uint32_t* __restrict__ ub, unsigned long long* __restrict__ work,
                                unsigned long long* __restrict__ w_full, unsigned long long* __restrict__ win) {
   unsigned long long full = 0;
@@ -76,26 +84,29 @@ __global__ void k_plan_entries(RouteRows rr, const uint32_t* __restrict__ off,
       const uint32_t rv = ob + (adj[e] & kMask);
       const uint32_t r = rev[e];
       const uint32_t lo = rr.route == 0 ? mid[x] : off[x];
-      if (rr.in_route(x) && e >= lo && e < end1[x]) {
+      const bool mid_entry = rr.in_route(x) && e >= lo && e < end1[x];
+      uint4 rvi = make_uint4(0, 0, 0, 0);  // off[rv], off[rv + 1], end1[rv], mid[rv]
+      if (mid_entry || win) rvi = rowinfo[rv];
+      if (mid_entry) {
         if (rr.route == 3) {  // ends before x in N(v): [off(v), r), of degree >= 2
-          const uint32_t u = off[rv], en = min(end1[rv], r);
+          const uint32_t u = rvi.x, en = min(rvi.z, r);
           ub[e] = u;
           full += r - u;
           l_seg = en > u ? en - u : 0;
         } else {
-          const uint32_t f = off[rv + 1];
+          const uint32_t f = rvi.y;
           const uint32_t u = r + 1;  // x's entry in its middle's row is the reverse entry
-          const uint32_t en = end1[rv];
+          const uint32_t en = rvi.z;
           // hybrid: a core start's wedges through a core middle skip the core ends (counted by
           // the dense core, hybrid.cu); W_G (full) stays the paper's count
-          const uint32_t u2 = (rr.ccnt && rr.core(x) && rr.core(rv)) ? max(u, off[rv] + rr.ccnt[rv]) : u;
+          const uint32_t u2 = (rr.ccnt && rr.core(x) && rr.core(rv)) ? max(u, rvi.x + rr.ccnt[rv]) : u;
           ub[e] = u2;
           full += f - u;
           l_seg = en > u2 ? en - u2 : 0;
         }
       }
       if (win) {
-        const uint32_t o = off[rv], pos = r - o, hi = mid[rv] - o;
+        const uint32_t o = rvi.x, pos = r - o, hi = rvi.w - o;
         c = pos < hi ? pos : hi;
       }
     }
@@ -317,9 +328,13 @@ bbf_status make_plan(bbf_graph* g, int route, Plan* p, bool all_t3, const uint32
     BBF_CUDA(cudaMemsetAsync(win, 0, 8ull * (n + 1), st));
   }
   if (m) {
-    k_plan_entries<<<grid_for(m, 256), 256, 0, st>>>(rr, g->off, g->adj, g->rev, g->erow, g->mid, g->end1, m, p->ub,
-                                                   (unsigned long long*)p->work, &acc[0], win);
-    g->launches += 1;
+    uint4* rowinfo;
+    BBF_CUDA(dmalloc(&rowinfo, 16ull * n, st));
+    k_rowinfo<<<(n + 255) / 256, 256, 0, st>>>(g->off, g->end1, g->mid, n, rowinfo);
+    k_plan_entries<<<grid_for(m, 256), 256, 0, st>>>(rr, g->off, g->adj, g->rev, g->erow, g->mid, g->end1, rowinfo,
+                                                   m, p->ub, (unsigned long long*)p->work, &acc[0], win);
+    g->launches += 2;
+    dfree(rowinfo, st);
   }
   if (n) {
     k_seg_bounds<<<grid_for(n, 256, 1u << 30), 256, 0, st>>>(rr, g->off, g->mid, g->end1, sb, se);
