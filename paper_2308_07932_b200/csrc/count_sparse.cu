@@ -1367,10 +1367,10 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
 // a CTA scan gives each middle's first wedge, and warp w takes wedge steps w, w + warps, ... ;
 // a lane finds its middle by binary search in the shared prefix.  Pass 2 sums the middle shares
 // per run of equal middles in a step and adds them to per-middle shared totals.
-template <bool PV, bool PAIRS, int kT2Threads, int kSlots>
+template <bool PV, bool PAIRS, int kT2Threads, int kSlots, int kMPT>
 __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
   constexpr int kT2Warps = kT2Threads / 32;
-  constexpr uint32_t kM = 2 * kT2Threads;  // middles per round
+  constexpr uint32_t kM = kMPT * kT2Threads;  // middles per round (kMPT per thread)
   extern __shared__ uint32_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   volatile uint32_t* keys = smem;
@@ -1414,10 +1414,12 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
           // round set-up: two consecutive middles per thread; one CTA-wide exclusive scan of
           // (segment length << 12 | non-empty) compacts the non-empty middles (so their first
           // wedges strictly increase) and gives each one's first flattened wedge
-          uint32_t len2[2], wv2[2] = {0, 0}, s2[2] = {0, 0};
+          uint32_t len2[kMPT], wv2[kMPT], s2[kMPT];
   #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const uint32_t i = 2 * tid + q;
+          for (int q = 0; q < kMPT; ++q) {
+            const uint32_t i = kMPT * tid + q;
+            wv2[q] = 0;
+            s2[q] = 0;
             len2[q] = 0;
             if (i < mc) {
               wv2[q] = a.adj[m_lo + r0 + i];
@@ -1427,7 +1429,9 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
               len2[q] = en > s2[q] ? en - s2[q] : 0;
             }
           }
-          const uint32_t tsum = ((len2[0] + len2[1]) << 12) | ((len2[0] > 0) + (len2[1] > 0));
+          uint32_t tsum = 0;
+  #pragma unroll
+          for (int q = 0; q < kMPT; ++q) tsum += (len2[q] << 12) | (len2[q] > 0 ? 1u : 0u);
           const uint32_t wincl = warp_incl_scan(tsum, lane);
           if (lane == 31) sh_wsum[warp] = wincl;
           __syncthreads();
@@ -1437,10 +1441,10 @@ __global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
           {
             uint32_t k = ex & 0xfffu, pos = ex >> 12;
   #pragma unroll
-            for (int q = 0; q < 2; ++q) {
+            for (int q = 0; q < kMPT; ++q) {
               if (len2[q]) {
                 mP[k] = pos; mS[k] = s2[q]; mW[k] = wv2[q];
-                if (a.edge) mE[k] = m_lo + r0 + 2 * tid + q;
+                if (a.edge) mE[k] = m_lo + r0 + kMPT * tid + q;
                 if (pass == 1) { mB[k] = 0; mN[k] = 0; }
                 ++k;
                 pos += len2[q];
@@ -1598,28 +1602,30 @@ cudaError_t launch_engine(bbf_graph* g, const EngineArgs& ea, cudaStream_t st, P
   if (p->n_t2) {
     EngineArgs eb = ea;
     eb.t2 = p->t2; eb.n_t2 = p->n_t2; eb.t2ctr = 16;
-    const size_t smem2 = sizeof(uint32_t) * (2 * kT2Slots + 5 * 1024 + 1 + (ea.edge ? 1024 : 0));
-    err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 512, kT2Slots>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+    // one middle per thread per round: 74 KB of shared memory, so three CTAs fit an SM (75% of
+    // the warp slots; with two middles per thread it was 86 KB, two CTAs)
+    const size_t smem2 = sizeof(uint32_t) * (2 * kT2Slots + 5 * 512 + 1 + (ea.edge ? 512 : 0));
+    err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 512, kT2Slots, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     if (err != cudaSuccess) return err;
-    k_t2<PV, PAIRS, 512, kT2Slots><<<g->num_sms * 2, 512, smem2, st>>>(eb);
+    k_t2<PV, PAIRS, 512, kT2Slots, 1><<<g->num_sms * 3, 512, smem2, st>>>(eb);
     g->launches++;
   }
   if (p->n_t2h) {
     EngineArgs eh = ea;
     eh.t2 = p->t2h; eh.n_t2 = p->n_t2h; eh.t2ctr = 19;
     const size_t smem2 = sizeof(uint32_t) * (2 * kT2HugeSlots + 5 * 2048 + 1 + (ea.edge ? 2048 : 0));
-    err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 1024, kT2HugeSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+    err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 1024, kT2HugeSlots, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     if (err != cudaSuccess) return err;
-    k_t2<PV, PAIRS, 1024, kT2HugeSlots><<<g->num_sms, 1024, smem2, st>>>(eh);
+    k_t2<PV, PAIRS, 1024, kT2HugeSlots, 2><<<g->num_sms, 1024, smem2, st>>>(eh);
     g->launches++;
   }
   if (p->n_t2s) {
     EngineArgs es = ea;
     es.t2 = p->t2s; es.n_t2 = p->n_t2s; es.t2ctr = 17;
     const size_t smem2 = sizeof(uint32_t) * (kT2Slots + 5 * 512 + 1 + (ea.edge ? 512 : 0));
-    err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 256, kT2Slots / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+    err = cudaFuncSetAttribute(k_t2<PV, PAIRS, 256, kT2Slots / 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
     if (err != cudaSuccess) return err;
-    k_t2<PV, PAIRS, 256, kT2Slots / 2><<<g->num_sms * 5, 256, smem2, st>>>(es);
+    k_t2<PV, PAIRS, 256, kT2Slots / 2, 2><<<g->num_sms * 5, 256, smem2, st>>>(es);
     g->launches++;
   }
   cudaEventRecord(e2, st);
