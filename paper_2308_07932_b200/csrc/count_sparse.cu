@@ -1368,7 +1368,7 @@ __global__ void __launch_bounds__(kT1Warps * 32) k_t1(const EngineArgs a) {
 // a lane finds its middle by binary search in the shared prefix.  Pass 2 sums the middle shares
 // per run of equal middles in a step and adds them to per-middle shared totals.
 template <bool PV, bool PAIRS, int kT2Threads, int kSlots, int kMPT>
-__global__ void __launch_bounds__(kT2Threads) k_t2(const EngineArgs a) {
+__global__ void __launch_bounds__(kT2Threads, kMPT == 1 ? 3 : 1) k_t2(const EngineArgs a) {
   constexpr int kT2Warps = kT2Threads / 32;
   constexpr uint32_t kM = kMPT * kT2Threads;  // middles per round (kMPT per thread)
   extern __shared__ uint32_t smem[];
