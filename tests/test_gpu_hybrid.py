@@ -176,3 +176,22 @@ def test_hybrid_dense_core_beyond_packed_accumulator(bbf, monkeypatch):
         tot, bu, nu, bv, nv = h.count_per_vertex()
     assert (tot["balanced"], tot["unbalanced"]) == (rg["B"], rg["N"])
     assert np.array_equal(bu, rg["bal_u"]) and np.array_equal(nv, rg["unb_v"])
+
+
+def test_hybrid_single_rank_nccl_communicator(bbf, monkeypatch):
+    """The hybrid path under a real one-rank NCCL communicator (the per-vertex all-reduce over the
+    degree >= 2 row prefixes, the status max-reduce): counts equal the oracle's."""
+    g = G.core_periphery(30_000, 10_000, 200_000, 2.2, 2000.0, 2000.0, 1024, 1024, 0.2, 0.6, 62)
+    rg = O.route_g_pv(g, threads=THREADS)
+    monkeypatch.setenv("BBF_HYBRID_CORE", "1024,1024")
+    comm = bbf.Comm(bbf.nccl_unique_id(), 1, 0, 0)
+    try:
+        with bbf.Graph.from_synth(g, comm=comm) as h:
+            tot, bu, nu, bv, nv = h.count_per_vertex()
+            assert h.hybrid_core() == (1024, 1024)
+    finally:
+        comm.free()
+        monkeypatch.delenv("BBF_HYBRID_CORE")
+    assert (tot["balanced"], tot["unbalanced"]) == (rg["B"], rg["N"])
+    assert np.array_equal(bu, rg["bal_u"]) and np.array_equal(nu, rg["unb_u"])
+    assert np.array_equal(bv, rg["bal_v"]) and np.array_equal(nv, rg["unb_v"])
