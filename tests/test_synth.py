@@ -46,7 +46,7 @@ def test_config_shapes_and_simplicity():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg", [3])
+@pytest.mark.parametrize("cfg", [3, 6])
 def test_large_configs_match_recorded_hash(cfg):
     g = G.make_config(cfg)
     sha, n_u, n_v, nnz = golden()[cfg]
@@ -59,6 +59,6 @@ def test_gpu_accelerated_generator_reproduces_numpy():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
-    for cfg in (3, 5):
+    for cfg in (3, 5, 6):
         g = G.make_config(cfg)
         assert g.sha256() == golden()[cfg][0], cfg
